@@ -1,0 +1,184 @@
+/*
+ * nrm_b200.h -- C ABI of the B200-native dense per-pixel stage of the
+ * real-time non-rigid mosaicking pipeline (arXiv 2103.07414).
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API
+ * (namespace nrmosaic, /root/reference/proj/include/nrmosaic). Each entry
+ * point names the reference function it replaces (file:line). The C++ shim
+ * include/nrmosaic_b200/mosaic.hpp maps these back onto the reference's
+ * signatures, exceptions and std::optional so existing callers recompile
+ * unchanged.
+ *
+ * Conventions
+ *   - Every function returns NRM_OK (0) or an NRM_E* code; never throws.
+ *     nrm_last_error() gives a thread-local message for the last failure.
+ *   - Host-pointer entry points copy inputs in (pinned host memory is copied
+ *     directly, pageable memory through the context's pinned staging) and
+ *     block until results are on the host.
+ *   - *_device entry points take device pointers, enqueue on the context's
+ *     stream and return without synchronising.
+ *   - Array layouts:
+ *       points / anchors : double[n][2]  (x, y)          -- Vec2 (geometry.hpp:12)
+ *       warps / locals   : double[n][5]  (scale, w, z, dx, dy)
+ *                                         -- WarpFunction{scale, DualQuat2{w,z,dx,dy}}
+ *                                            (dualquat.hpp:97-107, 22-26)
+ *       frame            : uint8[h][w][ch], ch in {1, 3, 4} -- ImageU8 (image.hpp:21-43)
+ *       canvas colour    : double[h][w][3] in [0,1], weight uint8[h][w]
+ *                                         -- Canvas (mosaic.hpp:100-182)
+ *   - One context = one CUDA device + one stream; a context is used by one
+ *     host thread at a time (the reference's single coordinator thread,
+ *     SPEC.md:438). Several contexts may coexist.
+ *   - Multi-GPU: one process per GPU, each with its own context. A canvas
+ *     can be restricted to block-cyclic 64-row stripes (nrm_canvas_set_band);
+ *     control points and frames are replicated by the caller (NCCL).
+ */
+#ifndef NRM_B200_H
+#define NRM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NRM_ABI_VERSION 1
+
+enum {
+    NRM_OK = 0,
+    NRM_EINVAL = 1,      /* bad argument (reference: std::invalid_argument)        */
+    NRM_ENOSUPPORT = 2,  /* no node carries weight (reference: std::nullopt)       */
+    NRM_EDEGENERATE = 3, /* DualQuat2 real part < 1e-300 (dualquat.hpp:49-50)      */
+    NRM_ECUDA = 4,       /* CUDA runtime / launch failure                          */
+    NRM_ENOMEM = 5,      /* device or pinned allocation failed                     */
+    NRM_ESTATE = 6       /* object used from the wrong context / after destroy     */
+};
+
+typedef struct nrm_ctx nrm_ctx;
+typedef struct nrm_canvas nrm_canvas;
+
+/* BlendStats (mosaic.hpp:184-189). */
+typedef struct nrm_blend_stats {
+    int64_t footprint_pixels;
+    int64_t blended_pixels;
+    int64_t skipped_no_support;
+    int64_t skipped_out_of_frame;
+} nrm_blend_stats;
+
+/* Query grid for the dense fields: pixel (i, j) is the reference-frame
+ * coordinate (x0 + i, y0 + j), 0 <= i < width, 0 <= j < height. */
+typedef struct nrm_grid {
+    double x0, y0;
+    int width, height;
+} nrm_grid;
+
+/* ---- library / context ------------------------------------------------ */
+int nrm_abi_version(void);
+const char *nrm_last_error(void);
+
+/* Creates a context on CUDA device `device` with its own non-blocking stream. */
+int nrm_ctx_create(int device, nrm_ctx **out);
+int nrm_ctx_destroy(nrm_ctx *ctx);
+/* Enqueue subsequent work on an external cudaStream_t (NULL = own stream). */
+int nrm_ctx_set_stream(nrm_ctx *ctx, void *cuda_stream);
+void *nrm_ctx_stream(nrm_ctx *ctx);
+int nrm_ctx_synchronize(nrm_ctx *ctx);
+/* Number of kernels this context has launched so far. */
+int nrm_ctx_launch_count(nrm_ctx *ctx, int64_t *out);
+
+/* ---- Canvas (mosaic.hpp:100-182) ------------------------------------- */
+/* Empty canvas (Canvas::Canvas(), mosaic.hpp:100). Storage lives in HBM:
+ * float32 R/G/B planes + uint8 weight plane. */
+int nrm_canvas_create(nrm_ctx *ctx, nrm_canvas **out);
+int nrm_canvas_destroy(nrm_canvas *cv);
+/* Pre-allocates device storage so growth inside rect never reallocates.
+ * Does not change the logical canvas (origin/width/height). */
+int nrm_canvas_reserve(nrm_canvas *cv, double x0, double y0, double x1, double y1);
+/* Canvas::ensure_contains (mosaic.hpp:131-174): identical origin/size
+ * bookkeeping (256-px tile alignment); existing pixels preserved exactly. */
+int nrm_canvas_ensure_contains(nrm_canvas *cv, double x0, double y0, double x1, double y1);
+/* origin_offset() (mosaic.hpp:109), width(), height(). */
+int nrm_canvas_info(const nrm_canvas *cv, int64_t *origin_x, int64_t *origin_y, int *width,
+                    int *height);
+/* Restrict this canvas (this rank) to block-cyclic stripes of 64 reference
+ * rows: rows with floor(y / 64) mod count == rank. count = 1: whole canvas. */
+int nrm_canvas_set_band(nrm_canvas *cv, int rank, int count);
+/* Reads canvas-pixel rectangle [x, x+w) x [y, y+h) (canvas coordinates, as
+ * Canvas::color(x, y) / weight(x, y), mosaic.hpp:111-120) into host arrays.
+ * Either output may be NULL. */
+int nrm_canvas_download(nrm_canvas *cv, int x, int y, int w, int h, double *rgb,
+                        uint8_t *weight);
+/* Writes a rectangle (Canvas::color(x,y)[k] = ..., weight_ref(x,y) = ...). */
+int nrm_canvas_upload(nrm_canvas *cv, int x, int y, int w, int h, const double *rgb,
+                      const uint8_t *weight);
+/* Canvas::occupied_count (mosaic.hpp:123-127). */
+int nrm_canvas_occupied_count(nrm_canvas *cv, int64_t *out);
+
+/* ---- blend_frame (mosaic.hpp:196-296) -------------------------------- */
+/* Blends one frame into the canvas. anchors[n][2] are the node anchors in
+ * reference coordinates, warps[n][5] their WarpFunctions, alpha the Gaussian
+ * coefficient, poly[npoly][2] the footprint polygon (reference coords).
+ * Returns the reference's BlendStats; an empty frame or npoly < 3 gives
+ * all-zero stats (mosaic.hpp:201). Blocks until done. */
+int nrm_blend_frame(nrm_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                    const double *anchors, const double *warps, int n, double alpha,
+                    const double *poly, int npoly, nrm_blend_stats *out);
+/* Device-resident variant: d_frame, d_anchors, d_warps are device pointers,
+ * poly stays on the host (it only sets the bounding box). Stats are written
+ * to d_stats (int64[4], device) in enqueue order. Asynchronous. */
+int nrm_blend_frame_device(nrm_canvas *cv, const uint8_t *d_frame, int fw, int fh, int ch,
+                           const double *d_anchors, const double *d_warps, int n, double alpha,
+                           const double *poly, int npoly, int64_t *d_stats);
+
+/* ---- render (mosaic.hpp:301-331) -------------------------------------- */
+/* RGBA8 raster of the canvas; alpha 255 where weight > 0. With crop, the
+ * bounding box of occupied pixels. Call with out == NULL to get the size
+ * (0 x 0 when empty) and crop origin, then with an out_w*out_h*4 buffer. */
+int nrm_render(nrm_canvas *cv, int crop, uint8_t *out, int *out_w, int *out_h,
+               double *crop_origin2);
+/* Renders canvas rectangle [x, x+w) x [y, y+h) into device memory d_out
+ * (w*h*4 bytes); rows this rank does not own are written as zeros, so a
+ * SUM-reduce over ranks assembles the banded canvas. Asynchronous. */
+int nrm_render_device(nrm_canvas *cv, int x, int y, int w, int h, uint8_t *d_out);
+/* Occupied bounding box (canvas coords) of the pixels this rank owns;
+ * returns x1 < x0 when nothing is occupied. */
+int nrm_canvas_occupied_bbox(nrm_canvas *cv, int *x0, int *y0, int *x1, int *y1);
+
+/* ---- node field: pixel_warp (mosaic.hpp:22-51) ------------------------ */
+/* pixel_warp at npts arbitrary points (exact FP64 path). out_warps[npts][5];
+ * valid[i] = 0 where the reference returns nullopt. */
+int nrm_pixel_warp(nrm_ctx *ctx, const double *points, int npts, const double *anchors,
+                   const double *warps, int n, double alpha, double *out_warps, uint8_t *valid);
+/* Dense node field on a grid: disp[j][i] = pixel_warp(p)(p) - p (float2),
+ * support[j][i] = 1, or (0, 0) / 0 where nullopt. Either output may be NULL. */
+int nrm_node_field(nrm_ctx *ctx, const nrm_grid *grid, const double *anchors,
+                   const double *warps, int n, double alpha, float *disp, uint8_t *support);
+int nrm_node_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_anchors,
+                          const double *d_warps, int n, double alpha, float *d_disp,
+                          uint8_t *d_support);
+
+/* ---- footprint: invert_frame_boundary (mosaic.hpp:58-96) -------------- */
+/* Writes up to cap points to poly[cap][2]; *npoly = the full polygon size. */
+int nrm_invert_frame_boundary(nrm_ctx *ctx, int fw, int fh, const double *anchors,
+                              const double *warps, int n, double alpha, double step,
+                              double *poly, int cap, int *npoly);
+
+/* ---- EMDQ field: detail::blend_local (fieldest.hpp:75-97) + node_uncertainty
+ *      (fieldest.hpp:44-52) at every grid pixel ---------------------------- */
+/* apts[m_total][2], locals[m_total][5], probs[m_total]: the estimator's
+ * per-match arrays; active[nactive]: the candidate indices (the inliers).
+ * disp[j][i] = blend_local(p)(p) - p (float2), unc[j][i] =
+ * node_uncertainty(p, apts[active], beta). support = FieldParams::blend_support
+ * (fieldest.hpp:26, 1..32). Either output may be NULL. */
+int nrm_emdq_field(nrm_ctx *ctx, const nrm_grid *grid, const double *apts, const double *locals,
+                   const double *probs, int m_total, const int32_t *active, int nactive,
+                   double alpha, int support, double beta, float *disp, float *unc);
+int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_apts,
+                          const double *d_locals, const double *d_probs, int m_total,
+                          const int32_t *d_active, int nactive, double alpha, int support,
+                          double beta, float *d_disp, float *d_unc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NRM_B200_H */

@@ -1,0 +1,177 @@
+"""TEST INFRASTRUCTURE: generates tests/golden/*.npz from the REAL reference
+(oracle/_ref/libnrm_ref.so, the /root/reference headers compiled in place).
+
+    make -C oracle ref && python oracle/make_golden.py
+
+Each fixture holds the inputs and the reference's outputs for one case. The
+reference's own unit tests (proj/tests/test_mosaic.cpp, test_fieldest.cpp)
+supply the case shapes; the larger cases use BASELINE config C1. Canvas
+colour planes are stored as SHA-256 of their float64 bytes (the restatement
+must reproduce them bit-for-bit) plus a seeded sample of values.
+"""
+from __future__ import annotations
+
+import hashlib
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path[0] = str(ROOT)
+
+from oracle.oracle import Reference  # noqa: E402
+from paper_2103_07414_b200 import workload as W  # noqa: E402
+
+OUT = ROOT / "tests" / "golden"
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rigid_warp(scale, angle, tx, ty):
+    return W.similarity_warp(scale, angle, (tx * scale, ty * scale))
+
+
+def mild_deformation(n):
+    """test_mosaic.cpp:190-193."""
+    out = np.zeros((n, 5))
+    for i in range(n):
+        s = 1.0 + 0.0005 * (i % 5)
+        ang = 0.01 * (i % 3)
+        tx, ty = 0.5 * (i % 7), -0.3 * (i % 4)
+        w, z = np.cos(0.5 * ang), np.sin(0.5 * ang)
+        out[i] = [s, w, z, 0.5 * (tx * w + ty * z), 0.5 * (-tx * z + ty * w)]
+    return out
+
+
+def blend_case(R, name, frame, anchors, warps_seq, alpha, polys, sample=4096, seed=0):
+    """Runs a sequence of blends (one per warps/poly) on one reference canvas."""
+    cv = R.canvas()
+    stats = []
+    for warps, poly in zip(warps_seq, polys):
+        stats.append(R.blend_frame(cv, frame, anchors, warps, alpha, poly, workers=4))
+    col, wt = cv.arrays()
+    img, org = R.render(cv, crop=True)
+    full, _ = R.render(cv, crop=False)
+    ox, oy, w, h = cv.info()
+    rng = np.random.default_rng(seed)
+    occ = np.argwhere(wt > 0)
+    pick = occ[rng.choice(len(occ), size=min(sample, len(occ)), replace=False)] if len(occ) else np.zeros((0, 2), int)
+    d = dict(
+        frame=frame, anchors=anchors, warps=np.stack(warps_seq), polys=np.array(polys, dtype=object),
+        npoly=np.array([len(p) for p in polys]), alpha=alpha, stats=np.array(stats, np.int64),
+        canvas_info=np.array([ox, oy, w, h], np.int64), color_sha=sha(col), weight_sha=sha(wt),
+        render_crop_sha=sha(img), render_crop_shape=np.array(img.shape), crop_origin=np.array(org),
+        render_full_sha=sha(full), sample_yx=pick, sample_color=col[pick[:, 0], pick[:, 1]] if len(pick) else np.zeros((0, 3)),
+        sample_weight=wt[pick[:, 0], pick[:, 1]] if len(pick) else np.zeros(0, np.uint8),
+        sample_render=full[pick[:, 0], pick[:, 1]] if len(pick) else np.zeros((0, 4), np.uint8))
+    if w * h <= 600_000:
+        d["weight"] = wt
+        d["render_crop"] = img
+    # object arrays are not loadable without pickle: flatten polygons
+    d["polys"] = np.concatenate(polys) if polys else np.zeros((0, 2))
+    np.savez_compressed(OUT / f"blend_{name}.npz", **d)
+    print(f"blend_{name}: stats={stats[-1]} canvas={ox, oy, w, h}")
+
+
+def main():
+    OUT.mkdir(parents=True, exist_ok=True)
+    R = Reference()
+    alpha0 = 2e-4
+
+    # ---- pixel_warp known answers (test_mosaic.cpp:39-82) + random --------
+    pw = {}
+    pw["single_anchors"] = np.array([[100.0, 100.0]])
+    pw["single_warps"] = rigid_warp(1.5, 0.2, 3, 4)[None]
+    pw["single_out"] = R.pixel_warp(100, 100, pw["single_anchors"], pw["single_warps"], alpha0)
+    anchors = W.hex_lattice((0, 0, 320, 200), 60.0)
+    warps = mild_deformation(len(anchors))
+    rng = np.random.default_rng(11)
+    pts = np.stack([rng.uniform(-600, 900, 4000), rng.uniform(-600, 800, 4000)], axis=1)
+    pts[:64] = np.round(pts[:64])
+    outs, valid = [], []
+    for x, y in pts:
+        r = R.pixel_warp(x, y, anchors, warps, alpha0)
+        valid.append(r is not None)
+        outs.append(r if r is not None else np.zeros(5))
+    np.savez_compressed(OUT / "pixel_warp.npz", anchors=anchors, warps=warps, points=pts, out=np.array(outs),
+                        valid=np.array(valid), alpha=alpha0, **pw)
+    print("pixel_warp:", int(np.sum(valid)), "of", len(pts), "supported")
+
+    # ---- invert_frame_boundary (mosaic.hpp:58-96) --------------------------
+    poly = R.invert_frame_boundary(320, 200, anchors, warps, alpha0)
+    np.savez_compressed(OUT / "invert_boundary.npz", anchors=anchors, warps=warps, poly=poly, alpha=alpha0,
+                        fw=320, fh=200)
+
+    # ---- blend_frame cases --------------------------------------------------
+    ramp = W.ramp_frame(320, 200)
+    ident = lambda a: np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(a), 1))  # noqa: E731
+    rect = lambda w, h: np.array([[0, 0], [w - 1, 0], [w - 1, h - 1], [0, h - 1]], float)  # noqa: E731
+    a = W.hex_lattice((0, 0, 320, 200), 60.0)
+    blend_case(R, "first_frame", ramp, a, [ident(a)], alpha0, [rect(320, 200)])
+
+    const = np.zeros((48, 64, 3), np.uint8)
+    const[..., 0], const[..., 1], const[..., 2] = 100, 150, 200
+    a = W.hex_lattice((0, 0, 64, 48), 20.0)
+    blend_case(R, "repeated_constant", const, a, [ident(a)] * 40, alpha0, [rect(64, 48)] * 40)
+
+    r2 = W.ramp_frame(256, 64)
+    a = W.hex_lattice((0, 0, 256, 64), 30.0)
+    shifted = np.tile(np.array([1.0, 1.0, 0.0, 50.0, 0.0]), (len(a), 1))  # from_translation({100, 0})
+    blend_case(R, "translated", r2, a, [ident(a), shifted], alpha0, [rect(256, 64), rect(256, 64) - [100, 0]])
+
+    a = W.hex_lattice((0, 0, 320, 200), 60.0)
+    wd = mild_deformation(len(a))
+    blend_case(R, "deformed", ramp, a, [wd], alpha0, [R.invert_frame_boundary(320, 200, a, wd, alpha0)])
+
+    r3 = W.ramp_frame(48, 32)
+    a = W.hex_lattice((0, 0, 48, 32), 16.0)
+    blend_case(R, "weight_cap", r3, a, [ident(a)] * 50, alpha0, [rect(48, 32)] * 50)
+
+    gray = W.textured_frame(160, 120, seed=5, channels=1)
+    a = W.hex_lattice((0, 0, 160, 120), 40.0)
+    blend_case(R, "gray_rotated", gray, a, [np.tile(rigid_warp(1.02, 0.05, 3.5, -2.25), (len(a), 1))], alpha0,
+               [R.invert_frame_boundary(160, 120, a, np.tile(rigid_warp(1.02, 0.05, 3.5, -2.25), (len(a), 1)), alpha0)])
+
+    # C1 (BASELINE configs[0]): 640x480, 500 matches (20 % outliers), reference EM
+    sp = W.scaled_params(640, 480)
+    pa, pb = R.synth_matches(640, 480, sp.s, 400, 100, 7000)
+    na = W.hex_lattice((0, 0, 640, 480), sp.hex_spacing)
+    cnt, loc, pr, inl, inc, unc = R.estimate_locals(pa, pb, na, sp.alpha, sp.beta, sp.inlier_threshold)
+    node_warps = np.stack([R.warp_update(np.array([1.0, 1, 0, 0, 0]), inc[i]) for i in range(len(na))])
+    frame_c1 = W.textured_frame(640, 480, seed=7)
+    poly_c1 = R.invert_frame_boundary(640, 480, na, node_warps, sp.alpha)
+    blend_case(R, "c1", frame_c1, na, [node_warps], sp.alpha, [poly_c1])
+    # second frame of a sequence: new warps composed on top (exercises canvas growth + averaging)
+    node_warps2 = np.stack([R.warp_update(node_warps[i], inc[i]) for i in range(len(na))])
+    poly_c1b = R.invert_frame_boundary(640, 480, na, node_warps2, sp.alpha)
+    blend_case(R, "c1_seq", frame_c1, na, [node_warps, node_warps2], sp.alpha, [poly_c1, poly_c1b])
+
+    # ---- EMDQ field (fieldest.hpp:75-97, 44-52) ------------------------------
+    act = np.nonzero(inl)[0].astype(np.int32)
+    grid = (0.0, 0.0, 640, 480)
+    disp, unc_g = R.emdq_field_grid(grid, pa, loc, pr, act, sp.alpha, sp.beta, 16, workers=8)
+    rng = np.random.default_rng(3)
+    qpts = np.stack([rng.uniform(-50, 700, 512), rng.uniform(-50, 530, 512)], axis=1)
+    qout = np.array([R.blend_local(loc, pa, pr, act, x, y, sp.alpha, 16) for x, y in qpts])
+    qunc = np.array([R.node_uncertainty(x, y, pa[act], sp.beta) for x, y in qpts])
+    np.savez_compressed(OUT / "emdq_c1.npz", apts=pa, bpts=pb, locals=loc, probs=pr, active=act, alpha=sp.alpha,
+                        beta=sp.beta, grid=np.array(grid), disp_sub=disp[::4, ::4], unc_sub=unc_g[::4, ::4],
+                        disp_sha=sha(disp), unc_sha=sha(unc_g), qpts=qpts, qout=qout, qunc=qunc,
+                        node_anchors=na, node_inc=inc, node_unc=unc, inlier_count=cnt)
+    print("emdq_c1: inliers", cnt, "disp range", float(np.abs(disp).max()))
+
+    # small-support and tiny-candidate edge cases
+    small_act = act[:10]
+    disp_s, unc_s = R.emdq_field_grid((100.0, 50.0, 96, 64), pa, loc, pr, small_act, sp.alpha, sp.beta, 16, workers=8)
+    disp_4, unc_4 = R.emdq_field_grid((100.0, 50.0, 96, 64), pa, loc, pr, act, sp.alpha, sp.beta, 4, workers=8)
+    np.savez_compressed(OUT / "emdq_edge.npz", apts=pa, locals=loc, probs=pr, active=act, small_active=small_act,
+                        alpha=sp.alpha, beta=sp.beta, grid=np.array([100.0, 50.0, 96, 64]), disp_small=disp_s,
+                        unc_small=unc_s, disp_s4=disp_4, unc_s4=unc_4)
+    print("done")
+
+
+if __name__ == "__main__":
+    main()

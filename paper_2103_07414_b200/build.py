@@ -1,0 +1,105 @@
+"""In-tree build of the CUDA library (sm_100a) and the test-only oracle.
+
+    python -m paper_2103_07414_b200.build          # libnrm_b200.so (+ oracle)
+
+The shared library is written next to this file so it travels with the repo
+snapshot to the GPU box; nothing goes to site-packages or a JIT cache.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libnrm_b200.so"
+OBJ = PKG / "_build"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O2",
+    "-Xptxas", "-v",
+    f"-I{ROOT / 'include'}",
+]
+SOURCES = ["nrm_abi.cu", "k_nodefield.cu", "k_emdq.cu", "k_canvas.cu"]
+
+
+def _nvcc() -> str:
+    cand = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(cand).exists():
+        raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libnrm_b200.so")
+    return cand
+
+
+def _run(cmd: list[str], log: Path | None = None) -> None:
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        log.write_text(res.stdout + res.stderr)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"command failed: {' '.join(cmd)}")
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False) -> Path:
+    nvcc = _nvcc()
+    OBJ.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "nrm_b200.h"]
+    objs = []
+    jobs = []
+    for src in SOURCES:
+        s = CSRC / src
+        o = OBJ / (s.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + headers):
+            jobs.append([nvcc, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
+    if jobs:
+        with ThreadPoolExecutor(max_workers=min(4, len(jobs))) as ex:
+            list(ex.map(lambda c: _run(c, OBJ / (Path(c[-1]).stem + ".ptxas.log")), jobs))
+    if force or jobs or _stale(LIB, objs):
+        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
+              *map(str, objs), "-cudart", "static", "-Xcompiler", "-fPIC"])
+    return LIB
+
+
+def build_oracle() -> None:
+    """Test infrastructure: the C restatement, and the reference itself when
+    /root/reference is present (this container only)."""
+    _run(["make", "-s", "-C", str(ROOT / "oracle"), "liboracle.so"])
+    if Path("/root/reference/proj/include/nrmosaic/mosaic.hpp").exists():
+        _run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"])
+
+
+def build_cpp_tests() -> None:
+    """C++ drop-in test (tests/cpp/test_shim.cpp) against the shim header."""
+    src = ROOT / "tests" / "cpp" / "test_shim.cpp"
+    if not src.exists():
+        return
+    out = ROOT / "tests" / "cpp" / "test_shim"
+    if _stale(out, [src, LIB, ROOT / "include" / "nrmosaic_b200" / "mosaic.hpp"]):
+        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-DNRM_B200_STANDALONE_TYPES",
+              str(src), "-o", str(out), f"-L{PKG}", "-lnrm_b200", f"-Wl,-rpath,{PKG}"])
+
+
+def main() -> None:
+    force = "--force" in sys.argv
+    build_lib(force)
+    build_oracle()
+    build_cpp_tests()
+    print(LIB)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,538 @@
+// k_nodefield.cu -- K1 (fused node field + mosaic update, blend_frame
+// mosaic.hpp:196-296) and K2 (dense node field, pixel_warp mosaic.hpp:22-51
+// at every grid pixel), plus the exact-tier exception pass, the batched
+// pixel_warp and invert_frame_boundary (mosaic.hpp:58-96).
+//
+// K1/K2 design:
+//   CTA = one 64 x 32 pixel tile (256 threads, 8 rows per thread).
+//   Prologue (FP64): cull nodes against the tile rectangle into an ordered
+//   list, classifying each as "inner" (weight > 1e-6 at every tile pixel),
+//   "ring" (the 1e-6 cutoff crosses the tile) or out; pick a per-tile output
+//   origin; conjugate every listed warp into tile-local coordinates
+//   (T(-P) q T(o)); build separable Gaussian tables ex[k][col], ey[k][row]
+//   (exp(-a(dx^2+dy^2)) = exp(-a dx^2) exp(-a dy^2), MUFU.EX2).
+//   Main loop (FP32): per (pixel, node) one FMUL for the weight and six FFMA
+//   accumulations; ring nodes add the cutoff test.
+//   Epilogue: normalise, apply, FP64 recombination with the tile origin,
+//   frame-bounds test, FP32 bilinear sample, capped running average.
+//   Pixels whose discrete decisions are within rounding of a threshold (ring
+//   weight ~1e-6, frame edge within 4e-3 px) or tiles whose warps are not in
+//   one hemisphere go to an exception queue that the exact FP64 pass
+//   (xpixel_warp, mirroring the reference's operation order) resolves.
+#include <cmath>
+
+#include "nrm_common.cuh"
+#include "nrm_internal.h"
+
+namespace nrm {
+namespace {
+
+constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
+constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
+constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
+constexpr double kBoundMargin = 4e-3;
+constexpr unsigned kRingBit = 0x80000000u;
+
+struct Smem {
+    float ex[CHUNK][TW];
+    float ey[CHUNK][TH];
+    float4 q[CHUNK];
+    float d[CHUNK];
+    int ring[CHUNK];
+    unsigned list[LIST_CAP];
+    int warp_cnt[NT / 32];
+    double red_d[NT / 32];
+    int red_i[NT / 32];
+    double red_lo[NT / 32], red_hi[NT / 32];
+    int count, overflow, uniform;
+    double P[2], Y0[2], e0[2], s0;
+};
+
+__device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1, int band_count) {
+    if (band_count <= 1) return tile_j0 + by;
+    const int s = s1 + (by >> 1) * band_count;
+    return 2 * s + (by & 1);
+}
+
+// Pushes every valid pixel of the tile to the exception queue.
+__device__ void tile_to_exceptions(const NodeFieldLaunch& L, int ci0, int ci1, int cj0, int cj1) {
+    const int w = ci1 - ci0 + 1, h = cj1 - cj0 + 1;
+    const int total = w * h;
+    for (int base = 0; base < total; base += NT) {
+        const int e = base + threadIdx.x;
+        const bool v = e < total;
+        queue_push(v, ci0 + (v ? e % w : 0), cj0 + (v ? e / w : 0), L.exc, L.exc_count, L.exc_cap,
+                   L.exc_overflow);
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 2)
+k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s1) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    const int t = threadIdx.x;
+    const int lane = t & 31, wid = t >> 5;
+
+    const int tix = tile_i0 + blockIdx.x;
+    const int tjy = tile_row_of(blockIdx.y, tile_j0, s1, L.band_count);
+    if (tjy < tile_j0 || tjy > tile_j_last) return;
+    const int ti0 = tix * TW, tj0 = tjy * TH;
+    const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
+    const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
+    if (ci0 > ci1 || cj0 > cj1) return;
+
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
+    const double xlo = L.grid.gx + ci0, xhi = L.grid.gx + ci1;
+    const double ylo = L.grid.gy + cj0, yhi = L.grid.gy + cj1;
+    const double alpha = L.alpha;
+
+    // ---- A. ordered cull + classify (FP64) ----------------------------
+    if (t == 0) {
+        s.count = 0;
+        s.overflow = 0;
+    }
+    __syncthreads();
+    for (int base = 0; base < L.n; base += NT) {
+        const int i = base + t;
+        int status = 0;  // 0 out, 1 inner, 2 ring
+        if (i < L.n) {
+            const double ax = __ldg(&L.anchors[2 * i]), ay = __ldg(&L.anchors[2 * i + 1]);
+            const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi);
+            const double dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
+            const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
+            const double amin = alpha * (dxn * dxn + dyn * dyn);
+            const double amax = alpha * (dxf * dxf + dyf * dyf);
+            if (amin <= kLnCutoff + 1e-6) status = amax < kLnCutoff - 1e-5 ? 1 : 2;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, status != 0);
+        if (lane == 0) s.warp_cnt[wid] = __popc(m);
+        __syncthreads();
+        int off = s.count;
+        for (int w = 0; w < wid; ++w) off += s.warp_cnt[w];
+        if (status) {
+            const int pos = off + __popc(m & ((1u << lane) - 1u));
+            if (pos < LIST_CAP)
+                s.list[pos] = (unsigned)i | (status == 2 ? kRingBit : 0u);
+            else
+                s.overflow = 1;
+        }
+        __syncthreads();
+        if (t == 0) {
+            int tot = 0;
+            for (int w = 0; w < NT / 32; ++w) tot += s.warp_cnt[w];
+            s.count += tot;
+        }
+        __syncthreads();
+    }
+    const int count = s.count;
+    if (s.overflow) {
+        tile_to_exceptions(L, ci0, ci1, cj0, cj1);
+        return;
+    }
+
+    // ---- B. no node reaches the tile: every pixel lacks support ----------
+    if (count == 0) {
+        int ns = 0;
+        for (int e = t; e < (ci1 - ci0 + 1) * (cj1 - cj0 + 1); e += NT) {
+            const int w = ci1 - ci0 + 1;
+            const int i = ci0 + e % w, j = cj0 + e / w;
+            if (MODE == 1) {
+                const size_t o = (size_t)(j - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+                if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+                if (L.support) L.support[o] = 0;
+            }
+            ++ns;
+        }
+        if (MODE == 0) block_add3<NT>(L.stats, 0, ns, 0);
+        return;
+    }
+
+    // ---- C. hemisphere check + per-tile reference (FP64) ---------------
+    {
+        const unsigned i0 = s.list[0] & ~kRingBit;
+        const double phi0 = atan2(__ldg(&L.warps[5 * i0 + 2]), __ldg(&L.warps[5 * i0 + 1]));
+        double lo = 0.0, hi = 0.0, best = 1e300;
+        int besti = 0x7fffffff;
+        const double cxm = ox + 0.5 * TW, cym = oy + 0.5 * TH;
+        for (int k = t; k < count; k += NT) {
+            const unsigned i = s.list[k] & ~kRingBit;
+            const double phi = atan2(__ldg(&L.warps[5 * i + 2]), __ldg(&L.warps[5 * i + 1]));
+            double rel = remainder(phi - phi0, 2.0 * M_PI);
+            lo = fmin(lo, rel);
+            hi = fmax(hi, rel);
+            const double ddx = __ldg(&L.anchors[2 * i]) - cxm, ddy = __ldg(&L.anchors[2 * i + 1]) - cym;
+            const double d2 = ddx * ddx + ddy * ddy;
+            if (d2 < best || (d2 == best && (int)i < besti)) {
+                best = d2;
+                besti = (int)i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+            const double bd = __shfl_xor_sync(0xffffffffu, best, o);
+            const int bi = __shfl_xor_sync(0xffffffffu, besti, o);
+            if (bd < best || (bd == best && bi < besti)) {
+                best = bd;
+                besti = bi;
+            }
+        }
+        if (lane == 0) {
+            s.red_lo[wid] = lo;
+            s.red_hi[wid] = hi;
+            s.red_d[wid] = best;
+            s.red_i[wid] = besti;
+        }
+        __syncthreads();
+        if (t == 0) {
+            for (int w = 1; w < NT / 32; ++w) {
+                lo = fmin(lo, s.red_lo[w]);
+                hi = fmax(hi, s.red_hi[w]);
+                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_i[w] < besti)) {
+                    best = s.red_d[w];
+                    besti = s.red_i[w];
+                }
+            }
+            s.uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
+            const W5 qr = load_w5(&L.warps[5 * besti]);
+            double yx, yy;
+            xapply(qr, ox, oy, &yx, &yy);
+            const double s0 = qr.s;
+            s.s0 = s0;
+            s.Y0[0] = rint(yx);
+            s.Y0[1] = rint(yy);
+            s.P[0] = s.Y0[0] / s0;
+            s.P[1] = s.Y0[1] / s0;
+            s.e0[0] = fma(s0, s.P[0], -s.Y0[0]);
+            s.e0[1] = fma(s0, s.P[1], -s.Y0[1]);
+        }
+        __syncthreads();
+    }
+    if (!s.uniform || !(s.s0 > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) {
+        tile_to_exceptions(L, ci0, ci1, cj0, cj1);
+        return;
+    }
+    const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
+
+    // ---- D. main loop over node chunks -----------------------------------
+    const int col = t & (TW - 1);
+    const int rg = t >> 6;  // 0..3, rows rg*8 .. rg*8+7
+    float a0[RPT], a1[RPT], a2[RPT], a3[RPT], a4[RPT], a5[RPT];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) a0[j] = a1[j] = a2[j] = a3[j] = a4[j] = a5[j] = 0.f;
+    unsigned amb = 0;
+
+    for (int c0 = 0; c0 < count; c0 += CHUNK) {
+        const int cn = min(CHUNK, count - c0);
+        __syncthreads();
+        for (int k = t; k < cn; k += NT) {
+            const unsigned e = s.list[c0 + k];
+            const unsigned i = e & ~kRingBit;
+            const W5 q = load_w5(&L.warps[5 * i]);
+            // qa = q * T(o): applies the tile-origin translation first
+            const double hx = 0.5 * ox, hy = 0.5 * oy;
+            const double qa_dx = (q.w * hx - q.z * hy) + q.dx;
+            const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
+            // q' = T(-P) * qa
+            const double px = 0.5 * P0, py = 0.5 * P1;
+            const double qdx = qa_dx + (-px * q.w - py * q.z);
+            const double qdy = qa_dy + (px * q.z - py * q.w);
+            s.q[k] = make_float4((float)q.w, (float)q.z, (float)qdx, (float)qdy);
+            s.d[k] = (float)(q.s - s0);
+            s.ring[k] = (e & kRingBit) ? 1 : 0;
+        }
+        const double nal = -alpha * kLog2e;
+        for (int e = t; e < cn * TW; e += NT) {
+            const int k = e / TW, c = e % TW;
+            const unsigned i = s.list[c0 + k] & ~kRingBit;
+            const double dx = __ldg(&L.anchors[2 * i]) - (ox + c);
+            s.ex[k][c] = ex2_approx((float)(nal * dx * dx));
+        }
+        for (int e = t; e < cn * TH; e += NT) {
+            const int k = e / TH, r = e % TH;
+            const unsigned i = s.list[c0 + k] & ~kRingBit;
+            const double dy = __ldg(&L.anchors[2 * i + 1]) - (oy + r);
+            s.ey[k][r] = ex2_approx((float)(nal * dy * dy));
+        }
+        __syncthreads();
+
+#pragma unroll 2
+        for (int k = 0; k < cn; ++k) {
+            const float4 q = s.q[k];
+            const float dd = s.d[k];
+            const float exv = s.ex[k][col];
+            const float4 e0 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT]);
+            const float4 e1 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT + 4]);
+            const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+            if (!s.ring[k]) {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    const float w = exv * ey[j];
+                    a0[j] = fmaf(w, q.x, a0[j]);
+                    a1[j] = fmaf(w, q.y, a1[j]);
+                    a2[j] = fmaf(w, q.z, a2[j]);
+                    a3[j] = fmaf(w, q.w, a3[j]);
+                    a4[j] = fmaf(w, dd, a4[j]);
+                    a5[j] += w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < RPT; ++j) {
+                    float w = exv * ey[j];
+                    const bool in = w > kCutHi;
+                    amb |= (unsigned)((w >= kCutLo) && !in) << j;
+                    w = in ? w : 0.f;
+                    a0[j] = fmaf(w, q.x, a0[j]);
+                    a1[j] = fmaf(w, q.y, a1[j]);
+                    a2[j] = fmaf(w, q.z, a2[j]);
+                    a3[j] = fmaf(w, q.w, a3[j]);
+                    a4[j] = fmaf(w, dd, a4[j]);
+                    a5[j] += w;
+                }
+            }
+        }
+    }
+
+    // ---- E. epilogue --------------------------------------------------------
+    const double Y00 = s.Y0[0], Y01 = s.Y0[1], e00 = s.e0[0], e01 = s.e0[1];
+    const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
+    int nb = 0, nns = 0, noof = 0;
+    const int i = ti0 + col;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+        const int jj = tj0 + rg * RPT + j;
+        const bool valid = i >= ci0 && i <= ci1 && jj >= cj0 && jj <= cj1;
+        bool exc = false;
+        if (valid) {
+            if ((amb >> j) & 1u) {
+                exc = true;
+            } else if (a5[j] == 0.f) {
+                ++nns;
+                if (MODE == 1) {
+                    const size_t o = (size_t)(jj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+                    if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+                    if (L.support) L.support[o] = 0;
+                }
+            } else {
+                const float rn = rsqrtf(fmaf(a0[j], a0[j], a1[j] * a1[j]));
+                const float qw = a0[j] * rn, qz = a1[j] * rn, qdx = a2[j] * rn, qdy = a3[j] * rn;
+                const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
+                const float ux = (float)col, uy = (float)(rg * RPT + j);
+                const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
+                const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
+                const float dl = a4[j] / a5[j];
+                const double sb = s0 + (double)dl;
+                const double yx = Y00 + (e00 + (double)dl * P0 + sb * (double)Qx);
+                const double yy = Y01 + (e01 + (double)dl * P1 + sb * (double)Qy);
+                if (MODE == 1) {
+                    const size_t o = (size_t)(jj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+                    if (L.disp)
+                        L.disp[o] = make_float2((float)(yx - (L.grid.gx + i)), (float)(yy - (L.grid.gy + jj)));
+                    if (L.support) L.support[o] = 1;
+                } else {
+                    const double margin = fmin(fmin(yx, fxm - yx), fmin(yy, fym - yy));
+                    if (margin < -kBoundMargin) {
+                        ++noof;
+                    } else if (margin < kBoundMargin) {
+                        exc = true;
+                    } else {
+                        int x0 = (int)yx, y0 = (int)yy;
+                        const int xc = L.fw - 2 >= 0 ? L.fw - 2 : 0, yc = L.fh - 2 >= 0 ? L.fh - 2 : 0;
+                        x0 = min(x0, xc);
+                        y0 = min(y0, yc);
+                        const float fx = (float)(yx - x0), fy = (float)(yy - y0);
+                        const int x1 = min(x0 + 1, L.fw - 1), y1 = min(y0 + 1, L.fh - 1);
+                        const uchar4 va = __ldg(&L.frame[(size_t)y0 * L.fw + x0]);
+                        const uchar4 vb = __ldg(&L.frame[(size_t)y0 * L.fw + x1]);
+                        const uchar4 vc = __ldg(&L.frame[(size_t)y1 * L.fw + x0]);
+                        const uchar4 vd = __ldg(&L.frame[(size_t)y1 * L.fw + x1]);
+                        const float gx = 1.f - fx, gy = 1.f - fy;
+                        const float r = (gx * va.x + fx * vb.x) * gy + (gx * vc.x + fx * vd.x) * fy;
+                        const float g = (gx * va.y + fx * vb.y) * gy + (gx * vc.y + fx * vd.y) * fy;
+                        const float b = (gx * va.z + fx * vb.z) * gy + (gx * vc.z + fx * vd.z) * fy;
+                        const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
+                        const uint8_t wg = L.W[idx];
+                        const float wd = (float)wg, inv = 1.f / (wd + 1.f);
+                        L.R[idx] = (wd * L.R[idx] + r / 255.f) * inv;
+                        L.G[idx] = (wd * L.G[idx] + g / 255.f) * inv;
+                        L.B[idx] = (wd * L.B[idx] + b / 255.f) * inv;
+                        L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
+                        ++nb;
+                    }
+                }
+            }
+        }
+        queue_push(exc, i, jj, L.exc, L.exc_count, L.exc_cap, L.exc_overflow);
+    }
+    if (MODE == 0) block_add3<NT>(L.stats, nb, nns, noof);
+}
+
+// Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics).
+template <int MODE>
+__global__ void __launch_bounds__(128) k_node_exceptions(NodeFieldLaunch L) {
+    const unsigned cnt = min(*L.exc_count, L.exc_cap);
+    if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0 && L.stats_footprint) *L.stats_footprint = L.footprint;
+    int nb = 0, nns = 0, noof = 0;
+    const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
+    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+        const int2 p = L.exc[q];
+        const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
+        W5 wp;
+        const int rc = xpixel_warp(x, y, L.anchors, L.warps, L.n, L.alpha, &wp);
+        if (MODE == 1) {
+            const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
+            if (rc == 0) {
+                double yx, yy;
+                xapply(wp, x, y, &yx, &yy);
+                if (L.disp) L.disp[o] = make_float2((float)(yx - x), (float)(yy - y));
+                if (L.support) L.support[o] = 1;
+            } else {
+                if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+                if (L.support) L.support[o] = 0;
+            }
+            continue;
+        }
+        if (rc != 0) {
+            ++nns;
+            continue;
+        }
+        double yx, yy;
+        xapply(wp, x, y, &yx, &yy);
+        if (!(yx >= 0.0 && yx <= fxm && yy >= 0.0 && yy <= fym)) {
+            ++noof;
+            continue;
+        }
+        double rgb[3];
+        xsample_bilinear(L.frame, L.fw, L.fh, yx, yy, rgb);
+        const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
+        const uint8_t wg = L.W[idx];
+        const double wd = wg;
+        L.R[idx] = (float)((wd * (double)L.R[idx] + rgb[0] / 255.0) / (wd + 1.0));
+        L.G[idx] = (float)((wd * (double)L.G[idx] + rgb[1] / 255.0) / (wd + 1.0));
+        L.B[idx] = (float)((wd * (double)L.B[idx] + rgb[2] / 255.0) / (wd + 1.0));
+        L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
+        ++nb;
+    }
+    if (MODE == 0) block_add3<128>(L.stats, nb, nns, noof);
+}
+
+__global__ void k_pixel_warp_points(const double* __restrict__ pts, int npts,
+                                    const double* __restrict__ anchors,
+                                    const double* __restrict__ warps, int n, double alpha,
+                                    double* __restrict__ out, uint8_t* __restrict__ valid) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    W5 wp;
+    const int rc = xpixel_warp(pts[2 * k], pts[2 * k + 1], anchors, warps, n, alpha, &wp);
+    valid[k] = rc == 0 ? 1 : (rc == 2 ? 2 : 0);
+    double* o = &out[5 * k];
+    if (rc == 0) {
+        o[0] = wp.s; o[1] = wp.w; o[2] = wp.z; o[3] = wp.dx; o[4] = wp.dy;
+    } else {
+        o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
+    }
+}
+
+// invert_frame_boundary (mosaic.hpp:58-96): poly holds the frame-boundary
+// samples on entry (generated on the host by the reference's own loops) and
+// their preimages on exit.
+__global__ void k_invert_boundary(const double* __restrict__ anchors,
+                                  const double* __restrict__ warps, int n, double alpha,
+                                  double* __restrict__ poly, int ns) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= ns) return;
+    const double yx = poly[2 * k], yy = poly[2 * k + 1];
+    int nearest = 0;
+    double best = 1.7976931348623157e308, px_n = 0.0, py_n = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const W5 q = load_w5(&warps[5 * i]);
+        double px, py;
+        xapply(q, anchors[2 * i], anchors[2 * i + 1], &px, &py);
+        const double d2 = xdist2(px, py, yx, yy);
+        if (d2 < best) {
+            best = d2;
+            nearest = i;
+            px_n = px;
+            py_n = py;
+        }
+    }
+    double x0 = yx, y0 = yy;
+    if (n > 0) {
+        x0 = xadd(anchors[2 * nearest], xsub(yx, px_n));
+        y0 = xadd(anchors[2 * nearest + 1], xsub(yy, py_n));
+    }
+    for (int it = 0; it < 15; ++it) {
+        W5 wp;
+        if (xpixel_warp(x0, y0, anchors, warps, n, alpha, &wp) != 0) break;
+        double nx, ny;
+        if (!xunapply(wp, yx, yy, &nx, &ny)) break;
+        const double move = sqrt(xdist2(nx, ny, x0, y0));
+        x0 = nx;
+        y0 = ny;
+        if (move < 1e-7) break;
+    }
+    poly[2 * k] = x0;
+    poly[2 * k + 1] = y0;
+}
+
+}  // namespace
+
+cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches) {
+    const int ti0 = floordiv(L.grid.i0, TW), ti1 = floordiv(L.grid.i1, TW);
+    const int tj0 = floordiv(L.grid.j0, TH), tj1 = floordiv(L.grid.j1, TH);
+    const int ntx = ti1 - ti0 + 1;
+    int nty = tj1 - tj0 + 1, s1 = 0;
+    if (L.band_count > 1) {
+        const int stripe_lo = floordiv(tj0 * TH, kStripeRows);
+        s1 = stripe_lo + posmod(L.band_rank - stripe_lo, L.band_count);
+        int cnt = 0;
+        for (int by = 0;; ++by) {
+            const int s = s1 + (by >> 1) * L.band_count;
+            const int row = 2 * s + (by & 1);
+            if (row > tj1) break;
+            cnt = by + 1;
+        }
+        nty = cnt;
+    }
+    const size_t smem = sizeof(Smem);
+    if (ntx > 0 && nty > 0) {
+        if (mode == 0) {
+            cudaFuncSetAttribute(k_node_field<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_node_field<0><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
+        } else {
+            cudaFuncSetAttribute(k_node_field<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            k_node_field<1><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
+        }
+        ++*launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (mode == 0)
+        k_node_exceptions<0><<<296, 128, 0, st>>>(L);
+    else
+        k_node_exceptions<1><<<296, 128, 0, st>>>(L);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pixel_warp_points(const double* pts, int npts, const double* anchors,
+                                     const double* warps, int n, double alpha, double* out,
+                                     uint8_t* valid, cudaStream_t st, int64_t* launches) {
+    if (npts <= 0) return cudaSuccess;
+    k_pixel_warp_points<<<(npts + 127) / 128, 128, 0, st>>>(pts, npts, anchors, warps, n, alpha, out, valid);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_invert_boundary(int, int, const double* anchors, const double* warps, int n,
+                                   double alpha, double, double* poly, int nsamples,
+                                   cudaStream_t st, int64_t* launches) {
+    if (nsamples <= 0) return cudaSuccess;
+    k_invert_boundary<<<(nsamples + 63) / 64, 64, 0, st>>>(anchors, warps, n, alpha, poly, nsamples);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace nrm

@@ -1,0 +1,825 @@
+// nrm_abi.cu -- host side of the C ABI (include/nrm_b200.h): contexts,
+// HBM-resident canvases with the reference's growth bookkeeping, transfers
+// and kernel orchestration. No compute happens on the host: every per-pixel
+// result comes from the kernels in k_*.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "nrm_common.cuh"
+#include "nrm_internal.h"
+
+namespace nrm {
+
+namespace {
+thread_local std::string g_last_error;
+
+constexpr int64_t kTile64 = kTile;
+
+int64_t align_down(int64_t v) { return v >= 0 ? (v / kTile64) * kTile64 : ((v - kTile64 + 1) / kTile64) * kTile64; }
+int64_t align_up(int64_t v) { return -align_down(-v); }
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+#define NRM_CUDA(call)                                  \
+    do {                                                \
+        const cudaError_t e__ = (call);                 \
+        if (e__ != cudaSuccess) return cuda_fail(e__, #call); \
+    } while (0)
+
+#define NRM_CHECK(rc_expr)             \
+    do {                               \
+        const int rc__ = (rc_expr);    \
+        if (rc__ != NRM_OK) return rc__; \
+    } while (0)
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? NRM_ENOMEM : NRM_ECUDA;
+}
+
+cudaError_t DevBuf::ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    const cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+}
+
+cudaError_t PinnedBuf::ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 4096);
+    const cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = want;
+    return e;
+}
+void PinnedBuf::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+}
+
+namespace {
+
+int upload(nrm_ctx* c, DevBuf& dst, const void* src, size_t bytes) {
+    NRM_CUDA(dst.ensure(bytes));
+    if (bytes) NRM_CUDA(cudaMemcpyAsync(dst.p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+    return NRM_OK;
+}
+
+bool finite_all(const double* p, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(p[i])) return false;
+    return true;
+}
+
+// ---- canvas storage ------------------------------------------------------
+void free_planes(nrm_canvas* cv) {
+    cudaFree(cv->r);
+    cudaFree(cv->g);
+    cudaFree(cv->b);
+    cudaFree(cv->w);
+    cv->r = cv->g = cv->b = nullptr;
+    cv->w = nullptr;
+}
+
+// Reallocates physical storage to cover absolute [x0,x1) x [y0,y1) and
+// copies the current logical window across; new pixels are zero.
+int grow_physical(nrm_canvas* cv, int64_t x0, int64_t y0, int64_t x1, int64_t y1) {
+    nrm_ctx* c = cv->ctx;
+    const int64_t w64 = x1 - x0, h64 = y1 - y0;
+    if (w64 <= 0 || h64 <= 0 || w64 > (1 << 30) || h64 > (1 << 30) || w64 * h64 > (int64_t)1 << 36)
+        return fail(NRM_EINVAL, "canvas: requested extent too large");
+    const size_t npx = (size_t)w64 * (size_t)h64;
+    float *r = nullptr, *g = nullptr, *b = nullptr;
+    uint8_t* w = nullptr;
+    cudaError_t e = cudaMalloc(&r, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&g, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&b, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&w, npx);
+    if (e != cudaSuccess) {
+        cudaFree(r);
+        cudaFree(g);
+        cudaFree(b);
+        cudaFree(w);
+        return cuda_fail(e, "canvas allocation");
+    }
+    NRM_CUDA(cudaMemsetAsync(r, 0, npx * sizeof(float), c->stream));
+    NRM_CUDA(cudaMemsetAsync(g, 0, npx * sizeof(float), c->stream));
+    NRM_CUDA(cudaMemsetAsync(b, 0, npx * sizeof(float), c->stream));
+    NRM_CUDA(cudaMemsetAsync(w, 0, npx, c->stream));
+    if (cv->width > 0 && cv->r) {
+        const size_t spitch = (size_t)cv->cap_w, dpitch = (size_t)w64;
+        const size_t soff = (size_t)(cv->origin_y - cv->phys_y0) * spitch + (size_t)(cv->origin_x - cv->phys_x0);
+        const size_t doff = (size_t)(cv->origin_y - y0) * dpitch + (size_t)(cv->origin_x - x0);
+        float* planes_old[3] = {cv->r, cv->g, cv->b};
+        float* planes_new[3] = {r, g, b};
+        for (int k = 0; k < 3; ++k)
+            NRM_CUDA(cudaMemcpy2DAsync(planes_new[k] + doff, dpitch * sizeof(float), planes_old[k] + soff,
+                                       spitch * sizeof(float), (size_t)cv->width * sizeof(float),
+                                       (size_t)cv->height, cudaMemcpyDeviceToDevice, c->stream));
+        NRM_CUDA(cudaMemcpy2DAsync(w + doff, dpitch, cv->w + soff, spitch, (size_t)cv->width,
+                                   (size_t)cv->height, cudaMemcpyDeviceToDevice, c->stream));
+        NRM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    free_planes(cv);
+    cv->r = r;
+    cv->g = g;
+    cv->b = b;
+    cv->w = w;
+    cv->phys_x0 = x0;
+    cv->phys_y0 = y0;
+    cv->cap_w = (int)w64;
+    cv->cap_h = (int)h64;
+    return NRM_OK;
+}
+
+bool covers(const nrm_canvas* cv, int64_t x0, int64_t y0, int64_t x1, int64_t y1) {
+    return cv->r && x0 >= cv->phys_x0 && y0 >= cv->phys_y0 && x1 <= cv->phys_x0 + cv->cap_w &&
+           y1 <= cv->phys_y0 + cv->cap_h;
+}
+
+// Canvas::ensure_contains (mosaic.hpp:131-174), same integer bookkeeping.
+int ensure_contains(nrm_canvas* cv, double rx0, double ry0, double rx1, double ry1) {
+    if (!(std::isfinite(rx0) && std::isfinite(ry0) && std::isfinite(rx1) && std::isfinite(ry1)))
+        return fail(NRM_EINVAL, "ensure_contains: non-finite rectangle");
+    if (std::fabs(rx0) > 1e9 || std::fabs(ry0) > 1e9 || std::fabs(rx1) > 1e9 || std::fabs(ry1) > 1e9)
+        return fail(NRM_EINVAL, "ensure_contains: rectangle out of range");
+    const int64_t nx0n = (int64_t)std::floor(rx0), ny0n = (int64_t)std::floor(ry0);
+    const int64_t nx1n = (int64_t)std::ceil(rx1) + 1, ny1n = (int64_t)std::ceil(ry1) + 1;
+    const bool empty = cv->width == 0;
+    if (!empty && nx0n >= cv->origin_x && ny0n >= cv->origin_y && nx1n <= cv->origin_x + cv->width &&
+        ny1n <= cv->origin_y + cv->height)
+        return NRM_OK;
+    int64_t nx0 = align_down(nx0n), ny0 = align_down(ny0n);
+    int64_t nx1 = nx1n, ny1 = ny1n;
+    if (!empty) {
+        nx0 = std::min(nx0, cv->origin_x);
+        ny0 = std::min(ny0, cv->origin_y);
+        nx1 = std::max(nx1, cv->origin_x + cv->width);
+        ny1 = std::max(ny1, cv->origin_y + cv->height);
+    }
+    const int64_t nw = ((nx1 - nx0 + kTile64 - 1) / kTile64) * kTile64;
+    const int64_t nh = ((ny1 - ny0 + kTile64 - 1) / kTile64) * kTile64;
+    if (!covers(cv, nx0, ny0, nx0 + nw, ny0 + nh)) {
+        int64_t px0 = nx0, py0 = ny0, px1 = nx0 + nw, py1 = ny0 + nh;
+        if (cv->res_x1 > cv->res_x0) {
+            px0 = std::min(px0, cv->res_x0);
+            py0 = std::min(py0, cv->res_y0);
+            px1 = std::max(px1, cv->res_x1);
+            py1 = std::max(py1, cv->res_y1);
+        }
+        NRM_CHECK(grow_physical(cv, px0, py0, px1, py1));
+    }
+    cv->origin_x = nx0;
+    cv->origin_y = ny0;
+    cv->width = (int)nw;
+    cv->height = (int)nh;
+    return NRM_OK;
+}
+
+struct Bbox {
+    double x0, y0, x1, y1;
+};
+
+// polygon_bbox (geometry.hpp:180-190) + Rect::expanded(4.0) (mosaic.hpp:203)
+Bbox footprint_bbox(const double* poly, int npoly) {
+    Bbox r{std::numeric_limits<double>::max(), std::numeric_limits<double>::max(),
+           std::numeric_limits<double>::lowest(), std::numeric_limits<double>::lowest()};
+    for (int i = 0; i < npoly; ++i) {
+        r.x0 = std::min(r.x0, poly[2 * i]);
+        r.y0 = std::min(r.y0, poly[2 * i + 1]);
+        r.x1 = std::max(r.x1, poly[2 * i]);
+        r.y1 = std::max(r.y1, poly[2 * i + 1]);
+    }
+    return {r.x0 - 4.0, r.y0 - 4.0, r.x1 + 4.0, r.y1 + 4.0};
+}
+
+// Shared core of blend_frame: everything after the inputs are in HBM.
+// d_stats: int64[4] on the device (zeroed here, filled by the kernels).
+int blend_core(nrm_canvas* cv, const uchar4* d_rgba, int fw, int fh, const double* d_anchors,
+               const double* d_warps, int n, double alpha, const double* poly, int npoly,
+               unsigned long long* d_stats) {
+    nrm_ctx* c = cv->ctx;
+    NRM_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
+    if (fw <= 0 || fh <= 0 || npoly < 3) return NRM_OK;  // mosaic.hpp:201
+    if (!finite_all(poly, (size_t)npoly * 2)) return fail(NRM_EINVAL, "blend_frame: non-finite polygon");
+    const Bbox bb = footprint_bbox(poly, npoly);
+    NRM_CHECK(ensure_contains(cv, bb.x0, bb.y0, bb.x1, bb.y1));
+    const double orgx = (double)cv->origin_x, orgy = (double)cv->origin_y;
+    const int px0 = (int)std::floor(bb.x0 - orgx), py0 = (int)std::floor(bb.y0 - orgy);
+    const int px1 = (int)std::ceil(bb.x1 - orgx), py1 = (int)std::ceil(bb.y1 - orgy);
+    const int bw = px1 - px0 + 1, bh = py1 - py0 + 1;
+    if (bw <= 0 || bh <= 0) return NRM_OK;  // mosaic.hpp:212
+    const unsigned long long footprint = (unsigned long long)bw * (unsigned long long)bh;
+
+    const size_t exc_cap = std::min<size_t>(footprint, (size_t)1 << 26);
+    NRM_CUDA(c->exc.ensure(exc_cap * sizeof(int2) + 64));
+    NRM_CUDA(c->misc.ensure(256));
+    unsigned* exc_count = c->misc.as<unsigned>();
+    NRM_CUDA(cudaMemsetAsync(exc_count, 0, 2 * sizeof(unsigned), c->stream));
+
+    NodeFieldLaunch L;
+    L.frame = d_rgba;
+    L.fw = fw;
+    L.fh = fh;
+    L.anchors = d_anchors;
+    L.warps = d_warps;
+    L.n = n;
+    L.alpha = alpha;
+    // index space = absolute reference pixel coordinates
+    L.grid.gx = 0.0;
+    L.grid.gy = 0.0;
+    L.grid.i0 = (int)(cv->origin_x + px0);
+    L.grid.i1 = (int)(cv->origin_x + px1);
+    L.grid.j0 = (int)(cv->origin_y + py0);
+    L.grid.j1 = (int)(cv->origin_y + py1);
+    L.R = cv->r;
+    L.G = cv->g;
+    L.B = cv->b;
+    L.W = cv->w;
+    L.pitch = cv->cap_w;
+    L.phys_x0 = (int)cv->phys_x0;
+    L.phys_y0 = (int)cv->phys_y0;
+    L.band_rank = cv->band_rank;
+    L.band_count = cv->band_count;
+    L.stats = d_stats + 1;
+    L.stats_footprint = d_stats;
+    L.footprint = footprint;
+    L.exc = c->exc.as<int2>();
+    L.exc_count = exc_count;
+    L.exc_cap = (unsigned)exc_cap;
+    L.exc_overflow = exc_count + 1;
+    NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
+    return NRM_OK;
+}
+
+int check_overflow(nrm_ctx* c) {
+    unsigned flags[2] = {0, 0};
+    NRM_CUDA(cudaMemcpy(flags, c->misc.p, sizeof(flags), cudaMemcpyDeviceToHost));
+    if (flags[1]) return fail(NRM_ECUDA, "exception queue overflow");
+    return NRM_OK;
+}
+
+int check_canvas(const nrm_canvas* cv) {
+    if (!cv || !cv->ctx) return fail(NRM_ESTATE, "null canvas");
+    return NRM_OK;
+}
+
+int check_region(const nrm_canvas* cv, int x, int y, int w, int h) {
+    if (w < 0 || h < 0 || x < 0 || y < 0 || (int64_t)x + w > cv->width || (int64_t)y + h > cv->height)
+        return fail(NRM_EINVAL, "canvas region out of bounds");
+    return NRM_OK;
+}
+
+int validate_nodes(const double* anchors, const double* warps, int n, double alpha, bool host) {
+    if (n < 0) return fail(NRM_EINVAL, "negative node count");
+    if (n > 0 && (!anchors || !warps)) return fail(NRM_EINVAL, "null node arrays");
+    if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
+    if (host && n > 0 && (!finite_all(anchors, (size_t)n * 2) || !finite_all(warps, (size_t)n * 5)))
+        return fail(NRM_EINVAL, "non-finite node arrays");
+    return NRM_OK;
+}
+
+int grid_indices(const nrm_grid* g, FieldGrid* out) {
+    if (!g || g->width < 0 || g->height < 0) return fail(NRM_EINVAL, "bad grid");
+    if (!std::isfinite(g->x0) || !std::isfinite(g->y0)) return fail(NRM_EINVAL, "non-finite grid origin");
+    out->gx = g->x0;
+    out->gy = g->y0;
+    out->i0 = 0;
+    out->j0 = 0;
+    out->i1 = g->width - 1;
+    out->j1 = g->height - 1;
+    return NRM_OK;
+}
+
+int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, const double* d_warps,
+                    int n, double alpha, float* d_disp, uint8_t* d_support) {
+    FieldGrid fg;
+    NRM_CHECK(grid_indices(grid, &fg));
+    const size_t npx = (size_t)grid->width * (size_t)grid->height;
+    if (npx == 0) return NRM_OK;
+    NRM_CUDA(c->exc.ensure(npx * sizeof(int2) + 64));
+    NRM_CUDA(c->misc.ensure(256));
+    unsigned* exc_count = c->misc.as<unsigned>();
+    NRM_CUDA(cudaMemsetAsync(exc_count, 0, 2 * sizeof(unsigned), c->stream));
+    NodeFieldLaunch L;
+    L.anchors = d_anchors;
+    L.warps = d_warps;
+    L.n = n;
+    L.alpha = alpha;
+    L.grid = fg;
+    L.disp = reinterpret_cast<float2*>(d_disp);
+    L.support = d_support;
+    L.exc = c->exc.as<int2>();
+    L.exc_count = exc_count;
+    L.exc_cap = (unsigned)std::min<size_t>(npx, 0xffffffffu);
+    L.exc_overflow = exc_count + 1;
+    NRM_CUDA(launch_node_field(L, 1, c->stream, &c->launches));
+    return NRM_OK;
+}
+
+int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const double* d_locals,
+              const double* d_probs, int m_total, const int32_t* d_active, int nactive, double alpha,
+              int support, double beta, float* d_disp, float* d_unc) {
+    FieldGrid fg;
+    NRM_CHECK(grid_indices(grid, &fg));
+    if (nactive <= 0 || m_total <= 0) return fail(NRM_EINVAL, "emdq_field: no candidates");
+    if (support < 1 || support > 32) return fail(NRM_EINVAL, "emdq_field: support must be in [1, 32]");
+    if (!(beta > 0.0) || !std::isfinite(beta)) return fail(NRM_EINVAL, "node_uncertainty: beta must be positive");
+    if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
+    if ((size_t)grid->width * (size_t)grid->height == 0) return NRM_OK;
+    const size_t na = (size_t)nactive;
+    NRM_CUDA(c->pts.ensure(na * 9 * sizeof(double) + na * sizeof(int) + 64));
+    double* base = c->pts.as<double>();
+    EmdqLaunch L;
+    L.grid = fg;
+    L.apts = d_apts;
+    L.locals = d_locals;
+    L.probs = d_probs;
+    L.active = d_active;
+    L.m_total = m_total;
+    L.nactive = nactive;
+    L.alpha = alpha;
+    L.beta = beta;
+    L.support = support;
+    L.disp = reinterpret_cast<float2*>(d_disp);
+    L.unc = d_unc;
+    L.cx = base;
+    L.cy = base + na;
+    L.cl = base + 2 * na;
+    L.cp = base + 7 * na;  // cj (int) follows cp: see launch_emdq_field
+    NRM_CUDA(launch_emdq_field(L, c->stream, &c->launches));
+    return NRM_OK;
+}
+
+}  // namespace
+}  // namespace nrm
+
+using namespace nrm;
+
+extern "C" {
+
+int nrm_abi_version(void) { return NRM_ABI_VERSION; }
+const char* nrm_last_error(void) { return g_last_error.c_str(); }
+
+int nrm_ctx_create(int device, nrm_ctx** out) {
+    if (!out) return fail(NRM_EINVAL, "null out");
+    *out = nullptr;
+    int ndev = 0;
+    NRM_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(NRM_EINVAL, "no such CUDA device");
+    nrm_ctx* c = new (std::nothrow) nrm_ctx();
+    if (!c) return fail(NRM_ENOMEM, "context allocation");
+    c->device = device;
+    DeviceGuard g(device);
+    cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaStreamCreate");
+    }
+    c->stream = c->own_stream;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    *out = c;
+    return NRM_OK;
+}
+
+int nrm_ctx_destroy(nrm_ctx* c) {
+    if (!c) return NRM_OK;
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    DevBuf* bufs[] = {&c->frame_raw, &c->frame_rgba, &c->anchors, &c->warps, &c->exc, &c->misc, &c->stats,
+                      &c->pts,       &c->locals,     &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles};
+    for (DevBuf* b : bufs) b->release();
+    c->staging.release();
+    c->staging_out.release();
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return NRM_OK;
+}
+
+int nrm_ctx_set_stream(nrm_ctx* c, void* s) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    return NRM_OK;
+}
+void* nrm_ctx_stream(nrm_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int nrm_ctx_synchronize(nrm_ctx* c) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    DeviceGuard g(c->device);
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    NRM_CUDA(cudaGetLastError());
+    return NRM_OK;
+}
+int nrm_ctx_launch_count(nrm_ctx* c, int64_t* out) {
+    if (!c || !out) return fail(NRM_EINVAL, "null argument");
+    *out = c->launches;
+    return NRM_OK;
+}
+
+// ---- canvas ---------------------------------------------------------------
+int nrm_canvas_create(nrm_ctx* c, nrm_canvas** out) {
+    if (!c || !out) return fail(NRM_EINVAL, "null argument");
+    nrm_canvas* cv = new (std::nothrow) nrm_canvas();
+    if (!cv) return fail(NRM_ENOMEM, "canvas allocation");
+    cv->ctx = c;
+    *out = cv;
+    return NRM_OK;
+}
+
+int nrm_canvas_destroy(nrm_canvas* cv) {
+    if (!cv) return NRM_OK;
+    if (cv->ctx) {
+        DeviceGuard g(cv->ctx->device);
+        cudaStreamSynchronize(cv->ctx->stream);
+        free_planes(cv);
+    }
+    delete cv;
+    return NRM_OK;
+}
+
+int nrm_canvas_reserve(nrm_canvas* cv, double x0, double y0, double x1, double y1) {
+    NRM_CHECK(check_canvas(cv));
+    if (!(std::isfinite(x0) && std::isfinite(y0) && std::isfinite(x1) && std::isfinite(y1)) || x1 < x0 || y1 < y0)
+        return fail(NRM_EINVAL, "reserve: bad rectangle");
+    DeviceGuard g(cv->ctx->device);
+    cv->res_x0 = align_down((int64_t)std::floor(x0));
+    cv->res_y0 = align_down((int64_t)std::floor(y0));
+    cv->res_x1 = align_up((int64_t)std::ceil(x1) + 1);
+    cv->res_y1 = align_up((int64_t)std::ceil(y1) + 1);
+    int64_t px0 = cv->res_x0, py0 = cv->res_y0, px1 = cv->res_x1, py1 = cv->res_y1;
+    if (cv->width > 0) {
+        px0 = std::min(px0, cv->origin_x);
+        py0 = std::min(py0, cv->origin_y);
+        px1 = std::max(px1, cv->origin_x + cv->width);
+        py1 = std::max(py1, cv->origin_y + cv->height);
+    }
+    if (!covers(cv, px0, py0, px1, py1)) NRM_CHECK(grow_physical(cv, px0, py0, px1, py1));
+    NRM_CUDA(cudaStreamSynchronize(cv->ctx->stream));
+    return NRM_OK;
+}
+
+int nrm_canvas_ensure_contains(nrm_canvas* cv, double x0, double y0, double x1, double y1) {
+    NRM_CHECK(check_canvas(cv));
+    DeviceGuard g(cv->ctx->device);
+    NRM_CHECK(ensure_contains(cv, x0, y0, x1, y1));
+    NRM_CUDA(cudaStreamSynchronize(cv->ctx->stream));
+    return NRM_OK;
+}
+
+int nrm_canvas_info(const nrm_canvas* cv, int64_t* ox, int64_t* oy, int* w, int* h) {
+    NRM_CHECK(check_canvas(cv));
+    if (ox) *ox = cv->origin_x;
+    if (oy) *oy = cv->origin_y;
+    if (w) *w = cv->width;
+    if (h) *h = cv->height;
+    return NRM_OK;
+}
+
+int nrm_canvas_set_band(nrm_canvas* cv, int rank, int count) {
+    NRM_CHECK(check_canvas(cv));
+    if (count < 1 || rank < 0 || rank >= count) return fail(NRM_EINVAL, "set_band: need 0 <= rank < count");
+    cv->band_rank = rank;
+    cv->band_count = count;
+    return NRM_OK;
+}
+
+int nrm_canvas_download(nrm_canvas* cv, int x, int y, int w, int h, double* rgb, uint8_t* weight) {
+    NRM_CHECK(check_canvas(cv));
+    NRM_CHECK(check_region(cv, x, y, w, h));
+    if ((size_t)w * h == 0) return NRM_OK;
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    const size_t npx = (size_t)w * h;
+    NRM_CUDA(c->out_a.ensure(npx * 3 * sizeof(double)));
+    NRM_CUDA(c->out_b.ensure(npx));
+    NRM_CUDA(launch_canvas_read(cv, x, y, w, h, rgb ? c->out_a.as<double>() : nullptr,
+                                weight ? c->out_b.as<uint8_t>() : nullptr, c->stream, &c->launches));
+    if (rgb) NRM_CUDA(cudaMemcpyAsync(rgb, c->out_a.p, npx * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (weight) NRM_CUDA(cudaMemcpyAsync(weight, c->out_b.p, npx, cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+int nrm_canvas_upload(nrm_canvas* cv, int x, int y, int w, int h, const double* rgb, const uint8_t* weight) {
+    NRM_CHECK(check_canvas(cv));
+    NRM_CHECK(check_region(cv, x, y, w, h));
+    if ((size_t)w * h == 0) return NRM_OK;
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    const size_t npx = (size_t)w * h;
+    if (rgb) NRM_CHECK(upload(c, c->out_a, rgb, npx * 3 * sizeof(double)));
+    if (weight) NRM_CHECK(upload(c, c->out_b, weight, npx));
+    NRM_CUDA(launch_canvas_write(cv, x, y, w, h, rgb ? c->out_a.as<double>() : nullptr,
+                                 weight ? c->out_b.as<uint8_t>() : nullptr, c->stream, &c->launches));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+static int occupied_scan(nrm_canvas* cv, unsigned long long* count, int bbox[4]) {
+    nrm_ctx* c = cv->ctx;
+    NRM_CUDA(c->stats.ensure(64));
+    const int init[6] = {0, 0, 0x7fffffff, 0x7fffffff, -1, -1};
+    NRM_CUDA(cudaMemcpyAsync(c->stats.p, init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    unsigned long long* d_count = c->stats.as<unsigned long long>();
+    int* d_bbox = reinterpret_cast<int*>(d_count + 1);
+    NRM_CUDA(launch_occupied(cv, d_count, d_bbox, c->stream, &c->launches));
+    int out[6];
+    NRM_CUDA(cudaMemcpyAsync(out, c->stats.p, sizeof(out), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    std::memcpy(count, out, sizeof(unsigned long long));
+    std::memcpy(bbox, out + 2, 4 * sizeof(int));
+    return NRM_OK;
+}
+
+int nrm_canvas_occupied_count(nrm_canvas* cv, int64_t* out) {
+    NRM_CHECK(check_canvas(cv));
+    if (!out) return fail(NRM_EINVAL, "null out");
+    *out = 0;
+    if (cv->width == 0) return NRM_OK;
+    DeviceGuard g(cv->ctx->device);
+    unsigned long long cnt = 0;
+    int bb[4];
+    NRM_CHECK(occupied_scan(cv, &cnt, bb));
+    *out = (int64_t)cnt;
+    return NRM_OK;
+}
+
+int nrm_canvas_occupied_bbox(nrm_canvas* cv, int* x0, int* y0, int* x1, int* y1) {
+    NRM_CHECK(check_canvas(cv));
+    int bb[4] = {0, 0, -1, -1};
+    if (cv->width > 0) {
+        DeviceGuard g(cv->ctx->device);
+        unsigned long long cnt = 0;
+        NRM_CHECK(occupied_scan(cv, &cnt, bb));
+        if (cnt == 0) bb[0] = 0, bb[1] = 0, bb[2] = -1, bb[3] = -1;
+    }
+    if (x0) *x0 = bb[0];
+    if (y0) *y0 = bb[1];
+    if (x1) *x1 = bb[2];
+    if (y1) *y1 = bb[3];
+    return NRM_OK;
+}
+
+// ---- blend_frame ---------------------------------------------------------
+int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, const double* anchors,
+                    const double* warps, int n, double alpha, const double* poly, int npoly,
+                    nrm_blend_stats* out) {
+    NRM_CHECK(check_canvas(cv));
+    if (!out) return fail(NRM_EINVAL, "null stats");
+    *out = nrm_blend_stats{0, 0, 0, 0};
+    if (fw < 0 || fh < 0) return fail(NRM_EINVAL, "negative frame size");
+    if (fw == 0 || fh == 0 || npoly < 3) return NRM_OK;  // mosaic.hpp:201
+    if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "frame channels must be 1, 3 or 4");
+    if (!frame || !poly) return fail(NRM_EINVAL, "null frame or polygon");
+    NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    const size_t fbytes = (size_t)fw * fh * ch;
+    NRM_CHECK(upload(c, c->frame_raw, frame, fbytes));
+    NRM_CUDA(c->frame_rgba.ensure((size_t)fw * fh * 4));
+    NRM_CUDA(launch_frame_to_rgba(c->frame_raw.as<uint8_t>(), fw, fh, ch, c->frame_rgba.as<uchar4>(), c->stream,
+                                  &c->launches));
+    NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
+    NRM_CUDA(c->stats.ensure(64));
+    NRM_CHECK(blend_core(cv, c->frame_rgba.as<uchar4>(), fw, fh, c->anchors.as<double>(), c->warps.as<double>(), n,
+                         alpha, poly, npoly, c->stats.as<unsigned long long>()));
+    NRM_CUDA(c->staging_out.ensure(64));
+    NRM_CUDA(cudaMemcpyAsync(c->staging_out.p, c->stats.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    NRM_CHECK(check_overflow(c));
+    std::memcpy(out, c->staging_out.p, sizeof(nrm_blend_stats));
+    return NRM_OK;
+}
+
+int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
+                           const double* d_warps, int n, double alpha, const double* poly, int npoly,
+                           int64_t* d_stats) {
+    NRM_CHECK(check_canvas(cv));
+    if (!d_stats) return fail(NRM_EINVAL, "null stats");
+    if (fw < 0 || fh < 0) return fail(NRM_EINVAL, "negative frame size");
+    NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    const uchar4* rgba = reinterpret_cast<const uchar4*>(d_frame);
+    if (fw > 0 && fh > 0 && npoly >= 3) {
+        if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "frame channels must be 1, 3 or 4");
+        if (!d_frame || !poly) return fail(NRM_EINVAL, "null frame or polygon");
+        if (ch != 4) {
+            NRM_CUDA(c->frame_rgba.ensure((size_t)fw * fh * 4));
+            NRM_CUDA(launch_frame_to_rgba(d_frame, fw, fh, ch, c->frame_rgba.as<uchar4>(), c->stream, &c->launches));
+            rgba = c->frame_rgba.as<uchar4>();
+        }
+    }
+    return blend_core(cv, rgba, fw, fh, d_anchors, d_warps, n, alpha, poly, npoly,
+                      reinterpret_cast<unsigned long long*>(d_stats));
+}
+
+// ---- render ----------------------------------------------------------------
+int nrm_render(nrm_canvas* cv, int crop, uint8_t* out, int* out_w, int* out_h, double* crop_origin2) {
+    NRM_CHECK(check_canvas(cv));
+    if (!out_w || !out_h) return fail(NRM_EINVAL, "null size outputs");
+    if (crop_origin2) {
+        crop_origin2[0] = (double)cv->origin_x;
+        crop_origin2[1] = (double)cv->origin_y;
+    }
+    *out_w = 0;
+    *out_h = 0;
+    if (cv->width == 0) return NRM_OK;
+    DeviceGuard g(cv->ctx->device);
+    int x0 = 0, y0 = 0, x1 = cv->width - 1, y1 = cv->height - 1;
+    if (crop) {
+        unsigned long long cnt = 0;
+        int bb[4];
+        NRM_CHECK(occupied_scan(cv, &cnt, bb));
+        if (cnt == 0) return NRM_OK;
+        x0 = bb[0];
+        y0 = bb[1];
+        x1 = bb[2];
+        y1 = bb[3];
+        if (crop_origin2) {
+            crop_origin2[0] = (double)cv->origin_x + (double)x0;
+            crop_origin2[1] = (double)cv->origin_y + (double)y0;
+        }
+    }
+    const int w = x1 - x0 + 1, h = y1 - y0 + 1;
+    *out_w = w;
+    *out_h = h;
+    if (!out) return NRM_OK;
+    nrm_ctx* c = cv->ctx;
+    const size_t bytes = (size_t)w * h * 4;
+    NRM_CUDA(c->out_b.ensure(bytes));
+    NRM_CUDA(launch_render(cv, x0, y0, w, h, c->out_b.as<uint8_t>(), c->stream, &c->launches));
+    NRM_CUDA(cudaMemcpyAsync(out, c->out_b.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+int nrm_render_device(nrm_canvas* cv, int x, int y, int w, int h, uint8_t* d_out) {
+    NRM_CHECK(check_canvas(cv));
+    NRM_CHECK(check_region(cv, x, y, w, h));
+    if (!d_out && (size_t)w * h) return fail(NRM_EINVAL, "null output");
+    DeviceGuard g(cv->ctx->device);
+    NRM_CUDA(launch_render(cv, x, y, w, h, d_out, cv->ctx->stream, &cv->ctx->launches));
+    return NRM_OK;
+}
+
+// ---- node field ------------------------------------------------------------
+int nrm_pixel_warp(nrm_ctx* c, const double* points, int npts, const double* anchors, const double* warps, int n,
+                   double alpha, double* out_warps, uint8_t* valid) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (npts < 0 || (npts > 0 && (!points || !out_warps || !valid))) return fail(NRM_EINVAL, "bad point arrays");
+    NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
+    if (npts == 0) return NRM_OK;
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->pts, points, (size_t)npts * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
+    NRM_CUDA(c->out_a.ensure((size_t)npts * 5 * sizeof(double)));
+    NRM_CUDA(c->out_b.ensure((size_t)npts));
+    NRM_CUDA(launch_pixel_warp_points(c->pts.as<double>(), npts, c->anchors.as<double>(), c->warps.as<double>(), n,
+                                      alpha, c->out_a.as<double>(), c->out_b.as<uint8_t>(), c->stream, &c->launches));
+    NRM_CUDA(cudaMemcpyAsync(out_warps, c->out_a.p, (size_t)npts * 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaMemcpyAsync(valid, c->out_b.p, (size_t)npts, cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    for (int i = 0; i < npts; ++i)
+        if (valid[i] == 2) return fail(NRM_EDEGENERATE, "DualQuat2: degenerate real part");
+    return NRM_OK;
+}
+
+int nrm_node_field(nrm_ctx* c, const nrm_grid* grid, const double* anchors, const double* warps, int n, double alpha,
+                   float* disp, uint8_t* support) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
+    if (!grid || grid->width < 0 || grid->height < 0) return fail(NRM_EINVAL, "bad grid");
+    const size_t npx = (size_t)grid->width * grid->height;
+    if (npx == 0) return NRM_OK;
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
+    NRM_CUDA(c->out_a.ensure(npx * sizeof(float2)));
+    NRM_CUDA(c->out_b.ensure(npx));
+    NRM_CHECK(node_field_core(c, grid, c->anchors.as<double>(), c->warps.as<double>(), n, alpha,
+                              disp ? c->out_a.as<float>() : nullptr, support ? c->out_b.as<uint8_t>() : nullptr));
+    if (disp) NRM_CUDA(cudaMemcpyAsync(disp, c->out_a.p, npx * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+    if (support) NRM_CUDA(cudaMemcpyAsync(support, c->out_b.p, npx, cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    NRM_CHECK(check_overflow(c));
+    return NRM_OK;
+}
+
+int nrm_node_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, const double* d_warps, int n,
+                          double alpha, float* d_disp, uint8_t* d_support) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
+    DeviceGuard g(c->device);
+    return node_field_core(c, grid, d_anchors, d_warps, n, alpha, d_disp, d_support);
+}
+
+// ---- footprint -------------------------------------------------------------
+int nrm_invert_frame_boundary(nrm_ctx* c, int fw, int fh, const double* anchors, const double* warps, int n,
+                              double alpha, double step, double* poly, int cap, int* npoly) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!npoly || (cap > 0 && !poly)) return fail(NRM_EINVAL, "null output");
+    if (!(step > 0.0) || !std::isfinite(step)) return fail(NRM_EINVAL, "step must be positive");
+    NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
+    // Boundary samples exactly as mosaic.hpp:62-67 generates them.
+    std::vector<double> s;
+    const double w1 = fw - 1.0, h1 = fh - 1.0;
+    for (double x = 0; x < w1; x += step) s.insert(s.end(), {x, 0.0});
+    for (double y = 0; y < h1; y += step) s.insert(s.end(), {w1, y});
+    for (double x = w1; x > 0; x -= step) s.insert(s.end(), {x, h1});
+    for (double y = h1; y > 0; y -= step) s.insert(s.end(), {0.0, y});
+    const int ns = (int)(s.size() / 2);
+    *npoly = ns;
+    if (ns == 0) return NRM_OK;
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->pts, s.data(), s.size() * sizeof(double)));
+    NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
+    NRM_CUDA(launch_invert_boundary(fw, fh, c->anchors.as<double>(), c->warps.as<double>(), n, alpha, step,
+                                    c->pts.as<double>(), ns, c->stream, &c->launches));
+    const int m = std::min(ns, cap);
+    if (m > 0)
+        NRM_CUDA(cudaMemcpyAsync(poly, c->pts.p, (size_t)m * 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+// ---- EMDQ field --------------------------------------------------------------
+int nrm_emdq_field(nrm_ctx* c, const nrm_grid* grid, const double* apts, const double* locals, const double* probs,
+                   int m_total, const int32_t* active, int nactive, double alpha, int support, double beta,
+                   float* disp, float* unc) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!grid || grid->width < 0 || grid->height < 0) return fail(NRM_EINVAL, "bad grid");
+    if (m_total <= 0 || nactive <= 0 || !apts || !locals || !probs || !active)
+        return fail(NRM_EINVAL, "emdq_field: empty or null candidate arrays");
+    for (int a = 0; a < nactive; ++a)
+        if (active[a] < 0 || active[a] >= m_total) return fail(NRM_EINVAL, "emdq_field: active index out of range");
+    if (!finite_all(apts, (size_t)m_total * 2) || !finite_all(locals, (size_t)m_total * 5))
+        return fail(NRM_EINVAL, "emdq_field: non-finite candidates");
+    const size_t npx = (size_t)grid->width * grid->height;
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->anchors, apts, (size_t)m_total * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->locals, locals, (size_t)m_total * 5 * sizeof(double)));
+    NRM_CHECK(upload(c, c->probs, probs, (size_t)m_total * sizeof(double)));
+    NRM_CHECK(upload(c, c->active, active, (size_t)nactive * sizeof(int32_t)));
+    NRM_CUDA(c->out_a.ensure(npx * sizeof(float2) + 16));
+    NRM_CUDA(c->out_b.ensure(npx * sizeof(float) + 16));
+    NRM_CHECK(emdq_core(c, grid, c->anchors.as<double>(), c->locals.as<double>(), c->probs.as<double>(), m_total,
+                        c->active.as<int32_t>(), nactive, alpha, support, beta, disp ? c->out_a.as<float>() : nullptr,
+                        unc ? c->out_b.as<float>() : nullptr));
+    if (npx) {
+        if (disp) NRM_CUDA(cudaMemcpyAsync(disp, c->out_a.p, npx * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
+        if (unc) NRM_CUDA(cudaMemcpyAsync(unc, c->out_b.p, npx * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    }
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+int nrm_emdq_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const double* d_locals,
+                          const double* d_probs, int m_total, const int32_t* d_active, int nactive, double alpha,
+                          int support, double beta, float* d_disp, float* d_unc) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    DeviceGuard g(c->device);
+    return emdq_core(c, grid, d_apts, d_locals, d_probs, m_total, d_active, nactive, alpha, support, beta, d_disp,
+                     d_unc);
+}
+
+}  // extern "C"

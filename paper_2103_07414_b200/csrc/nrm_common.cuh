@@ -1,0 +1,188 @@
+// nrm_common.cuh -- device helpers shared by the dense-stage kernels.
+//
+// Two arithmetic tiers:
+//   * exact tier (FP64, explicit __dmul_rn/__dadd_rn so nvcc never contracts
+//     into FMA): mirrors the reference's operation order, used for decisions
+//     that must match the reference (support, frame bounds, kNN membership)
+//     and for the exception path;
+//   * fast tier (FP32 FMA + MUFU.EX2) for the Gaussian accumulation, in
+//     tile-local coordinates.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nrm {
+
+constexpr double kPixelWeightCutoff = 1e-6;   // mosaic.hpp:16
+constexpr int kWeightCap = 30;                // mosaic.hpp:102
+constexpr int kTile = 256;                    // mosaic.hpp:103
+constexpr int kStripeRows = 64;               // block-cyclic band stripe
+constexpr double kLnCutoff = 13.815510557964274;  // -ln(1e-6)
+constexpr double kLog2e = 1.4426950408889634;
+
+// ---- exact FP64 (no contraction) ------------------------------------------
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+
+// (a - b).norm2() as geometry.hpp:20,34: x*x + y*y, two rounded products.
+__device__ __forceinline__ double xdist2(double ax, double ay, double bx, double by) {
+    const double dx = xsub(ax, bx), dy = xsub(ay, by);
+    return xadd(xmul(dx, dx), xmul(dy, dy));
+}
+
+struct W5 {
+    double s, w, z, dx, dy;
+};
+
+__device__ __forceinline__ W5 load_w5(const double* p) { return {p[0], p[1], p[2], p[3], p[4]}; }
+
+// DualQuat2::apply (dualquat.hpp:75-80) + WarpFunction scale (dualquat.hpp:107).
+__device__ __forceinline__ void xapply(const W5& q, double px, double py, double* ox, double* oy) {
+    const double c = xsub(xmul(q.w, q.w), xmul(q.z, q.z));
+    const double s = xmul(xmul(2.0, q.w), q.z);
+    const double tx = xmul(2.0, xsub(xmul(q.dx, q.w), xmul(q.dy, q.z)));
+    const double ty = xmul(2.0, xadd(xmul(q.dx, q.z), xmul(q.dy, q.w)));
+    *ox = xmul(xadd(xsub(xmul(c, px), xmul(s, py)), tx), q.s);
+    *oy = xmul(xadd(xadd(xmul(s, px), xmul(c, py)), ty), q.s);
+}
+
+// WarpFunction::unapply (dualquat.hpp:109-114). Returns false on scale <= 0.
+__device__ __forceinline__ bool xunapply(const W5& q, double yx, double yy, double* ox, double* oy) {
+    if (!(q.s > 0.0)) return false;
+    const double c = xsub(xmul(q.w, q.w), xmul(q.z, q.z));
+    const double s = xmul(xmul(2.0, q.w), q.z);
+    const double tx = xmul(2.0, xsub(xmul(q.dx, q.w), xmul(q.dy, q.z)));
+    const double ty = xmul(2.0, xadd(xmul(q.dx, q.z), xmul(q.dy, q.w)));
+    const double vx = xsub(yx / q.s, tx), vy = xsub(yy / q.s, ty);
+    *ox = xadd(xmul(c, vx), xmul(s, vy));
+    *oy = xadd(xmul(-s, vx), xmul(c, vy));
+    return true;
+}
+
+// pixel_warp (mosaic.hpp:22-51), exact tier, over all n nodes in index order.
+// Returns 0 = ok, 1 = no support (nullopt), 2 = degenerate real part.
+__device__ inline int xpixel_warp(double x, double y, const double* __restrict__ anchors,
+                                  const double* __restrict__ warps, int n, double alpha, W5* out) {
+    double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
+    double ref_w = 0.0, ref_z = 0.0;
+    bool have_ref = false;
+    const double na = -alpha;
+    for (int i = 0; i < n; ++i) {
+        const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
+        const double w = exp(xmul(na, d2));
+        if (w <= kPixelWeightCutoff) continue;
+        const double* q = &warps[5 * i];
+        double qw = __ldg(&q[1]), qz = __ldg(&q[2]), qdx = __ldg(&q[3]), qdy = __ldg(&q[4]);
+        if (!have_ref) {
+            ref_w = qw;
+            ref_z = qz;
+            have_ref = true;
+        } else if (xadd(xmul(qw, ref_w), xmul(qz, ref_z)) < 0.0) {
+            qw = -qw; qz = -qz; qdx = -qdx; qdy = -qdy;
+        }
+        aw = xadd(aw, xmul(w, qw));
+        az = xadd(az, xmul(w, qz));
+        adx = xadd(adx, xmul(w, qdx));
+        ady = xadd(ady, xmul(w, qdy));
+        as = xadd(as, xmul(w, __ldg(&q[0])));
+        wsum = xadd(wsum, w);
+    }
+    if (!have_ref) return 1;
+    const double mw = aw / wsum, mz = az / wsum, mdx = adx / wsum, mdy = ady / wsum;
+    const double nrm = hypot(mw, mz);
+    if (nrm < 1e-300) return 2;
+    out->s = as / wsum;
+    out->w = mw / nrm;
+    out->z = mz / nrm;
+    out->dx = mdx / nrm;
+    out->dy = mdy / nrm;
+    return 0;
+}
+
+// sample_bilinear_rgb (image.hpp:78-92) in the exact tier, on an RGBA8
+// device copy of the frame (grey already replicated to RGB).
+__device__ __forceinline__ void xsample_bilinear(const uchar4* __restrict__ im, int iw, int ih,
+                                                 double x, double y, double* out3) {
+    int x0 = (int)x, y0 = (int)y;
+    const int xc = iw - 2 >= 0 ? iw - 2 : 0, yc = ih - 2 >= 0 ? ih - 2 : 0;
+    if (x0 > xc) x0 = xc;
+    if (y0 > yc) y0 = yc;
+    const double fx = xsub(x, (double)x0), fy = xsub(y, (double)y0);
+    const int x1 = x0 + 1 < iw - 1 ? x0 + 1 : iw - 1;
+    const int y1 = y0 + 1 < ih - 1 ? y0 + 1 : ih - 1;
+    const uchar4 a = __ldg(&im[(size_t)y0 * iw + x0]), b = __ldg(&im[(size_t)y0 * iw + x1]);
+    const uchar4 c = __ldg(&im[(size_t)y1 * iw + x0]), d = __ldg(&im[(size_t)y1 * iw + x1]);
+    const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
+    const double va[3] = {(double)a.x, (double)a.y, (double)a.z};
+    const double vb[3] = {(double)b.x, (double)b.y, (double)b.z};
+    const double vc[3] = {(double)c.x, (double)c.y, (double)c.z};
+    const double vd[3] = {(double)d.x, (double)d.y, (double)d.z};
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        out3[k] = xadd(xmul(xadd(xmul(gx, va[k]), xmul(fx, vb[k])), gy),
+                       xmul(xadd(xmul(gx, vc[k]), xmul(fx, vd[k])), fy));
+}
+
+// ---- fast tier ----------------------------------------------------------
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// floor division for possibly negative ints
+__host__ __device__ __forceinline__ int floordiv(int a, int b) {
+    const int q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+__host__ __device__ __forceinline__ int posmod(int a, int b) {
+    const int r = a % b;
+    return r < 0 ? r + b : r;
+}
+
+// Warp-aggregated append to a global queue of (i, j) pixel indices.
+__device__ __forceinline__ void queue_push(bool pred, int i, int j, int2* q, unsigned* count,
+                                           unsigned cap, unsigned* overflow) {
+    const unsigned mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (pred) {
+        const unsigned slot = base + __popc(mask & ((1u << lane) - 1u));
+        if (slot < cap)
+            q[slot] = make_int2(i, j);
+        else
+            atomicExch(overflow, 1u);
+    }
+}
+
+// Block-wide sum of up to three counters, added atomically to dst[0..2].
+template <int NTHREADS>
+__device__ __forceinline__ void block_add3(unsigned long long* dst, int a, int b, int c) {
+    __shared__ int red[3][NTHREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = a;
+        red[1][w] = b;
+        red[2][w] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        long long s = 0;
+        for (int k = 0; k < NTHREADS / 32; ++k) s += red[threadIdx.x][k];
+        if (s) atomicAdd(&dst[threadIdx.x], (unsigned long long)s);
+    }
+}
+
+}  // namespace nrm

@@ -1,0 +1,149 @@
+// nrm_internal.h -- host-side objects behind the C ABI and the kernel
+// launch interfaces shared between translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "nrm_b200.h"
+
+namespace nrm {
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes);
+    void release();
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes);
+    void release();
+};
+
+}  // namespace nrm
+
+struct nrm_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int num_sms = 148;
+    // scratch (grow-only)
+    nrm::DevBuf frame_raw, frame_rgba, anchors, warps, exc, misc, stats, pts, locals, probs,
+        active, out_a, out_b, tiles;
+    nrm::PinnedBuf staging, staging_out;
+};
+
+struct nrm_canvas {
+    nrm_ctx* ctx = nullptr;
+    // logical canvas: reference bookkeeping (mosaic.hpp:176-181)
+    int64_t origin_x = 0, origin_y = 0;
+    int width = 0, height = 0;
+    // physical device storage: cap_w x cap_h pixels whose (0,0) is the
+    // absolute reference coordinate (phys_x0, phys_y0); SoA planes.
+    int64_t phys_x0 = 0, phys_y0 = 0;
+    int cap_w = 0, cap_h = 0;
+    float* r = nullptr;
+    float* g = nullptr;
+    float* b = nullptr;
+    uint8_t* w = nullptr;
+    // reservation (absolute, tile-aligned), 0-size when none
+    int64_t res_x0 = 0, res_y0 = 0, res_x1 = 0, res_y1 = 0;
+    int band_rank = 0, band_count = 1;
+};
+
+namespace nrm {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+
+// ---- launches (k_nodefield.cu) ----------------------------------------
+struct FieldGrid {
+    double gx, gy;      // coordinate of index (0, 0)
+    int i0, j0, i1, j1; // valid index range, inclusive
+};
+
+struct NodeFieldLaunch {
+    // inputs
+    const uchar4* frame = nullptr;
+    int fw = 0, fh = 0;
+    const double* anchors = nullptr;
+    const double* warps = nullptr;
+    int n = 0;
+    double alpha = 0.0;
+    FieldGrid grid{};
+    // BLEND mode: canvas planes (index (i, j) == absolute reference pixel)
+    float* R = nullptr;
+    float* G = nullptr;
+    float* B = nullptr;
+    uint8_t* W = nullptr;
+    long long pitch = 0;
+    int phys_x0 = 0, phys_y0 = 0;
+    int band_rank = 0, band_count = 1;
+    // FIELD mode outputs (row-major over the valid range)
+    float2* disp = nullptr;
+    uint8_t* support = nullptr;
+    // stats[0..2] = blended, no_support, out_of_frame (device, accumulated)
+    unsigned long long* stats = nullptr;
+    // stats_footprint[0] = footprint, written by the exception pass (BLEND mode)
+    unsigned long long* stats_footprint = nullptr;
+    unsigned long long footprint = 0;
+    // exception queue
+    int2* exc = nullptr;
+    unsigned* exc_count = nullptr;
+    unsigned exc_cap = 0;
+    unsigned* exc_overflow = nullptr;
+};
+
+// mode 0 = blend into canvas, 1 = node field (disp/support)
+cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches);
+cudaError_t launch_pixel_warp_points(const double* pts, int npts, const double* anchors,
+                                     const double* warps, int n, double alpha, double* out,
+                                     uint8_t* valid, cudaStream_t st, int64_t* launches);
+cudaError_t launch_invert_boundary(int fw, int fh, const double* anchors, const double* warps,
+                                   int n, double alpha, double step, double* poly, int nsamples,
+                                   cudaStream_t st, int64_t* launches);
+
+// ---- k_emdq.cu ------------------------------------------------------------
+struct EmdqLaunch {
+    FieldGrid grid{};
+    const double* apts = nullptr;     // m_total x 2
+    const double* locals = nullptr;   // m_total x 5
+    const double* probs = nullptr;    // m_total
+    const int32_t* active = nullptr;  // nactive
+    int m_total = 0, nactive = 0;
+    double alpha = 0.0, beta = 0.0;
+    int support = 16;
+    float2* disp = nullptr;
+    float* unc = nullptr;
+    // scratch: gathered candidates (SoA, nactive each)
+    double* cx = nullptr;
+    double* cy = nullptr;
+    double* cl = nullptr;   // nactive x 5 (scale, w, z, dx, dy)
+    double* cp = nullptr;   // max(prob, 1e-6)
+};
+cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches);
+
+// ---- k_canvas.cu ----------------------------------------------------------
+cudaError_t launch_frame_to_rgba(const uint8_t* raw, int w, int h, int ch, uchar4* out,
+                                 cudaStream_t st, int64_t* launches);
+cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
+                          cudaStream_t st, int64_t* launches);
+cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int* bbox4,
+                            cudaStream_t st, int64_t* launches);
+cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h, double* rgb,
+                               uint8_t* weight, cudaStream_t st, int64_t* launches);
+cudaError_t launch_canvas_write(nrm_canvas* cv, int x, int y, int w, int h, const double* rgb,
+                                const uint8_t* weight, cudaStream_t st, int64_t* launches);
+
+}  // namespace nrm

@@ -1,0 +1,347 @@
+"""Python mirror of the reference's dense-stage API (namespace nrmosaic,
+/root/reference/proj/include/nrmosaic/mosaic.hpp and fieldest.hpp), backed
+by libnrm_b200.so. Names, argument meaning and error behaviour follow the
+reference so the parity tests read like its own tests:
+
+    reference (C++)                          here
+    pixel_warp(x, anchors, warps, a)         pixel_warp(x, anchors, warps, a) -> warp5 | None
+    Canvas / ensure_contains / color ...     Canvas (HBM-resident; host reads are explicit)
+    blend_frame(canvas, frame, ..., workers) blend_frame(canvas, frame, ...) -> BlendStats
+    render(canvas, crop, &origin)            render(canvas, crop) -> (rgba, origin)
+    invert_frame_boundary(w, h, ...)         invert_frame_boundary(w, h, ...)
+    detail::blend_local + node_uncertainty   emdq_field(grid, ...) (dense, every pixel)
+
+Host arrays are numpy; the *_device variants take torch CUDA tensors and run
+asynchronously on the context's stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from ._lib import BlendStats, Grid, NoSupport, NrmError, check
+
+__all__ = [
+    "BlendStats", "Canvas", "Context", "Grid", "NoSupport", "NrmError", "blend_frame",
+    "blend_frame_device", "default_context", "emdq_field", "emdq_field_device",
+    "invert_frame_boundary", "node_field", "node_field_device", "pixel_warp", "render",
+    "render_device",
+]
+
+K_WEIGHT_CAP = 30   # mosaic.hpp:102
+K_TILE = 256        # mosaic.hpp:103
+
+
+def _ptr(a: Optional[np.ndarray]) -> Optional[int]:
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a, shape_tail: int, name: str) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.size == 0:
+        return arr.reshape(0, shape_tail)
+    arr = arr.reshape(-1, shape_tail) if arr.ndim != 2 else arr
+    if arr.shape[1] != shape_tail:
+        raise ValueError(f"{name}: expected (n, {shape_tail}) array, got {arr.shape}")
+    return arr
+
+
+def _tptr(t) -> int:
+    """Device pointer of a CUDA torch tensor (must be contiguous)."""
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("device variants need contiguous CUDA tensors")
+    return t.data_ptr()
+
+
+class Context:
+    """One CUDA device + one stream (nrm_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _lib.load()
+        h = C.c_void_p()
+        check(self._lib.nrm_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = int(device)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_handle: Optional[int]) -> None:
+        """Run subsequent work on an external cudaStream_t (e.g.
+        torch.cuda.current_stream().cuda_stream); None = own stream."""
+        check(self._lib.nrm_ctx_set_stream(self._h, stream_handle))
+
+    def stream(self) -> int:
+        return self._lib.nrm_ctx_stream(self._h) or 0
+
+    def synchronize(self) -> None:
+        check(self._lib.nrm_ctx_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        v = C.c_int64()
+        check(self._lib.nrm_ctx_launch_count(self._h, C.byref(v)))
+        return v.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.nrm_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+class Canvas:
+    """Canvas (mosaic.hpp:100-182), stored in HBM as float32 R/G/B planes
+    plus a uint8 weight plane. Logical origin/width/height follow the
+    reference's ensure_contains bookkeeping exactly."""
+
+    kWeightCap = K_WEIGHT_CAP
+    kTile = K_TILE
+
+    def __init__(self, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self._lib = self.ctx._lib
+        h = C.c_void_p()
+        check(self._lib.nrm_canvas_create(self.ctx.handle, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        ox, oy, w, h = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+        check(self._lib.nrm_canvas_info(self._h, C.byref(ox), C.byref(oy), C.byref(w), C.byref(h)))
+        return ox.value, oy.value, w.value, h.value
+
+    def empty(self) -> bool:
+        return self._info()[2] == 0
+
+    def width(self) -> int:
+        return self._info()[2]
+
+    def height(self) -> int:
+        return self._info()[3]
+
+    def origin_offset(self) -> Tuple[float, float]:
+        ox, oy, _, _ = self._info()
+        return float(ox), float(oy)
+
+    def ensure_contains(self, rect: Sequence[float]) -> None:
+        x0, y0, x1, y1 = map(float, rect)
+        check(self._lib.nrm_canvas_ensure_contains(self._h, x0, y0, x1, y1))
+
+    def reserve(self, rect: Sequence[float]) -> None:
+        x0, y0, x1, y1 = map(float, rect)
+        check(self._lib.nrm_canvas_reserve(self._h, x0, y0, x1, y1))
+
+    def set_band(self, rank: int, count: int) -> None:
+        check(self._lib.nrm_canvas_set_band(self._h, int(rank), int(count)))
+
+    def read(self, x: int = 0, y: int = 0, w: Optional[int] = None, h: Optional[int] = None):
+        """(color (h,w,3) float64, weight (h,w) uint8) of a canvas-pixel rectangle."""
+        if w is None:
+            w = self.width() - x
+        if h is None:
+            h = self.height() - y
+        rgb = np.zeros((h, w, 3), np.float64)
+        wt = np.zeros((h, w), np.uint8)
+        check(self._lib.nrm_canvas_download(self._h, x, y, w, h, _ptr(rgb), _ptr(wt)))
+        return rgb, wt
+
+    def write(self, x: int, y: int, rgb: Optional[np.ndarray], weight: Optional[np.ndarray]) -> None:
+        arr = rgb if rgb is not None else weight
+        h, w = arr.shape[:2]
+        rgb_c = None if rgb is None else np.ascontiguousarray(rgb, np.float64)
+        w_c = None if weight is None else np.ascontiguousarray(weight, np.uint8)
+        check(self._lib.nrm_canvas_upload(self._h, x, y, w, h, _ptr(rgb_c), _ptr(w_c)))
+
+    def color(self, x: int, y: int) -> np.ndarray:
+        return self.read(x, y, 1, 1)[0][0, 0]
+
+    def weight(self, x: int, y: int) -> int:
+        return int(self.read(x, y, 1, 1)[1][0, 0])
+
+    def occupied(self, x: int, y: int) -> bool:
+        return self.weight(x, y) > 0
+
+    def occupied_count(self) -> int:
+        v = C.c_int64()
+        check(self._lib.nrm_canvas_occupied_count(self._h, C.byref(v)))
+        return v.value
+
+    def occupied_bbox(self):
+        v = [C.c_int() for _ in range(4)]
+        check(self._lib.nrm_canvas_occupied_bbox(self._h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.nrm_canvas_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _frame(frame: np.ndarray) -> Tuple[np.ndarray, int, int, int]:
+    f = np.ascontiguousarray(frame, dtype=np.uint8)
+    if f.ndim == 2:
+        f = f[:, :, None]
+    if f.ndim != 3:
+        raise ValueError("frame must be (h, w) or (h, w, c)")
+    h, w, c = f.shape
+    return f, w, h, c
+
+
+def blend_frame(canvas: Canvas, frame: np.ndarray, anchors, warps, alpha: float,
+                footprint_polygon, workers: Optional[int] = None) -> BlendStats:
+    """blend_frame (mosaic.hpp:196-296). `workers` is accepted for signature
+    parity and ignored (the GPU grid replaces the thread pool)."""
+    f, w, h, c = _frame(frame)
+    a = _f64(anchors, 2, "anchors")
+    q = _f64(warps, 5, "warps")
+    if len(a) != len(q):
+        raise ValueError("anchors / warps size mismatch")
+    p = _f64(footprint_polygon, 2, "footprint_polygon")
+    st = BlendStats()
+    check(canvas._lib.nrm_blend_frame(canvas.handle, _ptr(f), w, h, c, _ptr(a), _ptr(q), len(a),
+                                      float(alpha), _ptr(p), len(p), C.byref(st)))
+    return st
+
+
+def blend_frame_device(canvas: Canvas, frame_t, fw: int, fh: int, ch: int, anchors_t, warps_t,
+                       alpha: float, footprint_polygon, stats_t) -> None:
+    """Device-resident blend_frame: torch CUDA tensors in, int64[4] stats tensor out (async)."""
+    p = _f64(footprint_polygon, 2, "footprint_polygon")
+    n = anchors_t.shape[0] if anchors_t is not None else 0
+    check(canvas._lib.nrm_blend_frame_device(canvas.handle, _tptr(frame_t), fw, fh, ch,
+                                             _tptr(anchors_t), _tptr(warps_t), n, float(alpha),
+                                             _ptr(p), len(p), _tptr(stats_t)))
+
+
+def render(canvas: Canvas, crop: bool = False):
+    """render (mosaic.hpp:301-331) -> (RGBA uint8 (h, w, 4), crop origin (x, y))."""
+    w, h = C.c_int(), C.c_int()
+    org = (C.c_double * 2)()
+    check(canvas._lib.nrm_render(canvas.handle, int(bool(crop)), None, C.byref(w), C.byref(h), org))
+    out = np.zeros((h.value, w.value, 4), np.uint8)
+    if w.value and h.value:
+        check(canvas._lib.nrm_render(canvas.handle, int(bool(crop)), _ptr(out), C.byref(w),
+                                     C.byref(h), org))
+    return out, (org[0], org[1])
+
+
+def render_device(canvas: Canvas, x: int, y: int, w: int, h: int, out_t) -> None:
+    check(canvas._lib.nrm_render_device(canvas.handle, x, y, w, h, _tptr(out_t)))
+
+
+def pixel_warp(x_ref, anchors, warps, alpha: float, ctx: Optional[Context] = None):
+    """pixel_warp (mosaic.hpp:22-51). x_ref: (2,) -> warp5 array or None;
+    (k, 2) -> (warps (k, 5), valid (k,) bool)."""
+    ctx = ctx or default_context()
+    pts = np.asarray(x_ref, np.float64)
+    single = pts.ndim == 1
+    pts = _f64(pts, 2, "x_ref")
+    a = _f64(anchors, 2, "anchors")
+    q = _f64(warps, 5, "warps")
+    out = np.zeros((len(pts), 5), np.float64)
+    valid = np.zeros(len(pts), np.uint8)
+    check(ctx._lib.nrm_pixel_warp(ctx.handle, _ptr(pts), len(pts), _ptr(a), _ptr(q), len(a),
+                                  float(alpha), _ptr(out), _ptr(valid)))
+    if single:
+        return out[0] if valid[0] else None
+    return out, valid.astype(bool)
+
+
+def node_field(grid: Tuple[float, float, int, int], anchors, warps, alpha: float,
+               ctx: Optional[Context] = None):
+    """Dense pixel_warp: grid = (x0, y0, width, height). Returns
+    (disp (h, w, 2) float32 = warp(p)(p) - p, support (h, w) uint8)."""
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    a = _f64(anchors, 2, "anchors")
+    q = _f64(warps, 5, "warps")
+    disp = np.zeros((g.height, g.width, 2), np.float32)
+    sup = np.zeros((g.height, g.width), np.uint8)
+    check(ctx._lib.nrm_node_field(ctx.handle, C.byref(g), _ptr(a), _ptr(q), len(a), float(alpha),
+                                  _ptr(disp), _ptr(sup)))
+    return disp, sup
+
+
+def node_field_device(grid, anchors_t, warps_t, alpha: float, disp_t, support_t=None,
+                      ctx: Optional[Context] = None) -> None:
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    check(ctx._lib.nrm_node_field_device(ctx.handle, C.byref(g), _tptr(anchors_t), _tptr(warps_t),
+                                         anchors_t.shape[0], float(alpha), _tptr(disp_t),
+                                         _tptr(support_t)))
+
+
+def invert_frame_boundary(frame_w: int, frame_h: int, anchors, warps, alpha: float,
+                          step: float = 8.0, ctx: Optional[Context] = None) -> np.ndarray:
+    """invert_frame_boundary (mosaic.hpp:58-96) -> polygon (k, 2)."""
+    ctx = ctx or default_context()
+    a = _f64(anchors, 2, "anchors")
+    q = _f64(warps, 5, "warps")
+    n = C.c_int()
+    check(ctx._lib.nrm_invert_frame_boundary(ctx.handle, int(frame_w), int(frame_h), _ptr(a), _ptr(q),
+                                             len(a), float(alpha), float(step), None, 0, C.byref(n)))
+    poly = np.zeros((n.value, 2), np.float64)
+    check(ctx._lib.nrm_invert_frame_boundary(ctx.handle, int(frame_w), int(frame_h), _ptr(a), _ptr(q),
+                                             len(a), float(alpha), float(step), _ptr(poly), n.value,
+                                             C.byref(n)))
+    return poly
+
+
+def emdq_field(grid, apts, locals_, probs, active, alpha: float, beta: float, support: int = 16,
+               ctx: Optional[Context] = None):
+    """Dense EMDQ field: detail::blend_local (fieldest.hpp:75-97) applied at
+    every grid pixel plus node_uncertainty (fieldest.hpp:44-52).
+    Returns (disp (h, w, 2) float32, unc (h, w) float32)."""
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    ap = _f64(apts, 2, "apts")
+    lo = _f64(locals_, 5, "locals")
+    pr = np.ascontiguousarray(probs, np.float64).reshape(-1)
+    ac = np.ascontiguousarray(active, np.int32).reshape(-1)
+    if not (len(ap) == len(lo) == len(pr)):
+        raise ValueError("apts / locals / probs size mismatch")
+    disp = np.zeros((g.height, g.width, 2), np.float32)
+    unc = np.zeros((g.height, g.width), np.float32)
+    check(ctx._lib.nrm_emdq_field(ctx.handle, C.byref(g), _ptr(ap), _ptr(lo), _ptr(pr), len(ap),
+                                  _ptr(ac), len(ac), float(alpha), int(support), float(beta),
+                                  _ptr(disp), _ptr(unc)))
+    return disp, unc
+
+
+def emdq_field_device(grid, apts_t, locals_t, probs_t, active_t, alpha: float, beta: float,
+                      disp_t, unc_t, support: int = 16, ctx: Optional[Context] = None) -> None:
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    check(ctx._lib.nrm_emdq_field_device(ctx.handle, C.byref(g), _tptr(apts_t), _tptr(locals_t),
+                                         _tptr(probs_t), apts_t.shape[0], _tptr(active_t),
+                                         active_t.shape[0], float(alpha), int(support), float(beta),
+                                         _tptr(disp_t), _tptr(unc_t)))
