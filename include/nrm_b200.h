@@ -178,6 +178,12 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
                           const int32_t *d_active, int nactive, double alpha, int support,
                           double beta, float *d_disp, float *d_unc);
 
+/* ---- diagnostics ---------------------------------------------------------
+ * Evaluates the exact tier's exp / hypot emulation (nrm_libm.cuh) on the
+ * device so tests can check it bit-for-bit against the host libm. */
+int nrm_selftest_libm(nrm_ctx *ctx, const double *x, const double *y, int n, double *exp_out,
+                      double *hypot_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -172,7 +172,7 @@ __device__ void emdq_pixel(double qx, double qy, int n_in, int n_amb, int m,
     }
     const double inv = 1.0 / wsum;
     const double mw = sw * inv, mz = sz * inv, mdx = sdx * inv, mdy = sdy * inv;
-    const double nr = hypot(mw, mz);
+    const double nr = xhypot(mw, mz);
     float2 dout = make_float2(0.f, 0.f);
     if (nr >= 1e-300) {
         W5 f{ss * inv, mw / nr, mz / nr, mdx / nr, mdy / nr};
@@ -186,7 +186,7 @@ __device__ void emdq_pixel(double qx, double qy, int n_in, int n_amb, int m,
     if (out_u) {
         double arg = beta * d2min;
         if (55.0 < arg) arg = 55.0;
-        *out_u = (float)exp(arg);
+        *out_u = (float)xexp(arg);
     }
 }
 

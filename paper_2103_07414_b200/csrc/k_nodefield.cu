@@ -477,7 +477,23 @@ __global__ void k_invert_boundary(const double* __restrict__ anchors,
     poly[2 * k + 1] = y0;
 }
 
+__global__ void k_selftest_libm(const double* __restrict__ x, const double* __restrict__ y, int n,
+                                double* __restrict__ ex, double* __restrict__ hy) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    ex[k] = xexp(x[k]);
+    hy[k] = xhypot(x[k], y[k]);
+}
+
 }  // namespace
+
+cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double* ex, double* hy,
+                                 cudaStream_t st, int64_t* launches) {
+    if (n <= 0) return cudaSuccess;
+    k_selftest_libm<<<(n + 255) / 256, 256, 0, st>>>(x, y, n, ex, hy);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches) {
     const int ti0 = floordiv(L.grid.i0, TW), ti1 = floordiv(L.grid.i1, TW);

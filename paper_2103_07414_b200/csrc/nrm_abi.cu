@@ -822,4 +822,21 @@ int nrm_emdq_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_apts
                      d_unc);
 }
 
+// ---- diagnostics -------------------------------------------------------------
+int nrm_selftest_libm(nrm_ctx* c, const double* x, const double* y, int n, double* exp_out, double* hypot_out) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (n < 0 || (n > 0 && (!x || !y || !exp_out || !hypot_out))) return fail(NRM_EINVAL, "bad arrays");
+    if (n == 0) return NRM_OK;
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->pts, x, (size_t)n * sizeof(double)));
+    NRM_CHECK(upload(c, c->probs, y, (size_t)n * sizeof(double)));
+    NRM_CUDA(c->out_a.ensure((size_t)n * 2 * sizeof(double)));
+    double* o = c->out_a.as<double>();
+    NRM_CUDA(launch_selftest_libm(c->pts.as<double>(), c->probs.as<double>(), n, o, o + n, c->stream, &c->launches));
+    NRM_CUDA(cudaMemcpyAsync(exp_out, o, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaMemcpyAsync(hypot_out, o + n, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
 }  // extern "C"

@@ -12,6 +12,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "nrm_libm.cuh"
+
 namespace nrm {
 
 constexpr double kPixelWeightCutoff = 1e-6;   // mosaic.hpp:16
@@ -71,7 +73,7 @@ __device__ inline int xpixel_warp(double x, double y, const double* __restrict__
     const double na = -alpha;
     for (int i = 0; i < n; ++i) {
         const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
-        const double w = exp(xmul(na, d2));
+        const double w = xexp(xmul(na, d2));
         if (w <= kPixelWeightCutoff) continue;
         const double* q = &warps[5 * i];
         double qw = __ldg(&q[1]), qz = __ldg(&q[2]), qdx = __ldg(&q[3]), qdy = __ldg(&q[4]);
@@ -91,7 +93,7 @@ __device__ inline int xpixel_warp(double x, double y, const double* __restrict__
     }
     if (!have_ref) return 1;
     const double mw = aw / wsum, mz = az / wsum, mdx = adx / wsum, mdy = ady / wsum;
-    const double nrm = hypot(mw, mz);
+    const double nrm = xhypot(mw, mz);
     if (nrm < 1e-300) return 2;
     out->s = as / wsum;
     out->w = mw / nrm;

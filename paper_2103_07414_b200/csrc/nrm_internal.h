@@ -114,6 +114,9 @@ cudaError_t launch_invert_boundary(int fw, int fh, const double* anchors, const 
                                    int n, double alpha, double step, double* poly, int nsamples,
                                    cudaStream_t st, int64_t* launches);
 
+cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double* ex, double* hy,
+                                 cudaStream_t st, int64_t* launches);
+
 // ---- k_emdq.cu ------------------------------------------------------------
 struct EmdqLaunch {
     FieldGrid grid{};
