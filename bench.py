@@ -1,0 +1,453 @@
+"""Benchmark: dense EMDQ field + mosaic update of a 1080p frame (BASELINE.json
+configs[1]: 1920x1080 frame, 2,000 matches (20 % outliers) into an 8192x8192
+canvas) on B200, plus the reference CPU path timed on this box's host cores.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one frame through the hot path:
+  K3  nrm_emdq_field   dense EMDQ field + per-pixel uncertainty on the frame grid
+                       (detail::blend_local + node_uncertainty, fieldest.hpp:44-97)
+  K1  nrm_blend_frame  node field + bilinear warp + capped running average into
+                       the canvas (blend_frame, mosaic.hpp:196-296)
+value: Mpix/s = frame pixels per second (inputs resident in HBM, CUDA events on
+the launching stream, L2 flushed between steps with a 256 MiB write).
+e2e:   the same step through the host-pointer C ABI (pinned host buffers): frame,
+       control points and matches H2D, the field + uncertainty and BlendStats D2H.
+N > 1: one process per GPU (torchrun); each step is a batch of N frames; rank r
+computes the EMDQ field of frame r and blends all N frames into the block-cyclic
+64-row canvas stripes it owns (weak scaling); BlendStats are all-reduced (NCCL).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Mpix/s of dense EMDQ field + mosaic update; frames/s at 1080p (1/2/4/8 B200)"
+CFG_NAME = {"c1": "configs[0]: 640x480 frame, 500 matches (20% outliers) into 2048x2048 canvas",
+            "c2": "configs[1]: 1920x1080 frame, 2,000 matches (20% outliers) into 8192x8192 canvas",
+            "c4": "configs[3]: 3840x2160 frame, 10,000 matches (20% outliers) into 16384x16384 canvas"}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def host_cpu():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
+                          if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle/_ref: the reference headers compiled in place;
+# else the C restatement). Bounded sample of the same workload.
+# ---------------------------------------------------------------------------
+def cpu_reference_step(wl, poly, rows: int, workers: int):
+    """Times one sampled step on the host: blend_frame (full footprint) plus
+    the dense EMDQ field over `rows` frame rows; returns (sec per frame-equivalent, info)."""
+    from oracle import oracle as orc
+
+    e = wl.emdq
+    H = wl.frame_h
+    r0 = (H - rows) // 2
+    grid = (0.0, 0.0, wl.frame_w, H)
+    pre = np.array(wl.canvas_rect)
+    if orc.reference_available():
+        R = orc.Reference()
+        t_blend, st = R.time_blend_frame(wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly, pre, workers)
+        t0 = time.perf_counter()
+        R.emdq_field_grid(grid, e.apts, e.locals_, e.probs, e.active, wl.params.alpha, wl.params.beta, 16,
+                          workers=workers, rows=(r0, r0 + rows))
+        t_field = time.perf_counter() - t0
+        kind = "reference"
+    else:
+        O = orc.Oracle()
+        cv = O.canvas()
+        cv.ensure_contains(pre)
+        t0 = time.perf_counter()
+        O.blend_frame(cv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly)
+        t_blend = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        O.emdq_field_grid(grid, e.apts, e.locals_, e.probs, e.active, wl.params.alpha, wl.params.beta, 16,
+                          rows=(r0, r0 + rows))
+        t_field = time.perf_counter() - t0
+        kind, workers = "port", 1
+    t_frame = t_blend + t_field * (H / rows)
+    return t_frame, {"kind": kind, "cores": workers, "t_blend_s": t_blend, "t_field_sample_s": t_field,
+                     "field_rows": rows}
+
+
+def run_reference_arm(args, wl_name):
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    from paper_2103_07414_b200 import workload as W
+
+    wl = W.frame_workload(wl_name)
+    poly = footprint_polygon_cpu(wl)
+    model, ncpu = host_cpu()
+    rows = max(8, min(wl.frame_h, args.ref_rows))
+    for _ in range(args.warmup):
+        cpu_reference_step(wl, poly, rows, ncpu)
+    times, info = [], None
+    for _ in range(args.steps):
+        t, info = cpu_reference_step(wl, poly, rows, ncpu)
+        times.append(t)
+    tot = sum(times)
+    mpix = wl.frame_w * wl.frame_h / 1e6
+    value = mpix * args.steps / tot
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "frames_per_s": args.steps / tot,
+        "config": {"workload": CFG_NAME[wl_name], "frame": [wl.frame_w, wl.frame_h], "matches": len(wl.emdq.apts),
+                   "inliers": int(len(wl.emdq.active)), "nodes": int(len(wl.anchors)), "canvas": wl.canvas},
+        "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": info["cores"], "kind": info["kind"],
+                         "sample": f"per step: full blend_frame + dense EMDQ field over {rows} of {wl.frame_h} "
+                                   f"frame rows, extrapolated to the frame; host {model}"},
+        "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def footprint_polygon_cpu(wl):
+    """Footprint polygon for the CPU arm: the reference's own invert_frame_boundary
+    when available (it is the reference's producer of this input), else the oracle."""
+    from oracle import oracle as orc
+
+    if orc.reference_available():
+        return orc.Reference().invert_frame_boundary(wl.frame_w, wl.frame_h, wl.anchors, wl.warps, wl.params.alpha)
+    return orc.Oracle().invert_frame_boundary(wl.frame_w, wl.frame_h, wl.anchors, wl.warps, wl.params.alpha)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--ref-rows", type=int, default=48, help="frame rows of the EMDQ field in the CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: --steps)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args, args.config)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2103_07414_b200 import mosaic as M
+    from paper_2103_07414_b200 import workload as W
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    ctx = M.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    # ---- workload: one frame per rank (frames of a batch sit side by side) --
+    wl = W.frame_workload(args.config)
+    fw, fh = wl.frame_w, wl.frame_h
+    alpha, beta = wl.params.alpha, wl.params.beta
+    e = wl.emdq
+    nfr = world
+    shift = [float(k * fw) for k in range(nfr)]           # frame k: anchors shifted by k*fw in x
+    anchors_k = [wl.anchors + np.array([s, 0.0]) for s in shift]
+    # node warps of frame k: W_k(x) = W(x - shift) -> conjugate by a translation
+    warps_k = []
+    for s in shift:
+        q = wl.warps.copy()
+        # x -> W(x - s e_x): dual += -0.5 * s * (w, -z) rotated: T(-s) on the input side
+        w_, z_ = q[:, 1], q[:, 2]
+        q[:, 3] = q[:, 3] + 0.5 * (-s) * w_
+        q[:, 4] = q[:, 4] + 0.5 * (-s) * z_
+        warps_k.append(q)
+    polys = [M.invert_frame_boundary(fw, fh, anchors_k[k], warps_k[k], alpha, ctx=ctx) for k in range(nfr)]
+    x_lo = wl.canvas_rect[0]
+    rect = (x_lo, wl.canvas_rect[1], wl.canvas_rect[2] + shift[-1], wl.canvas_rect[3])
+
+    cv = M.Canvas(ctx)
+    cv.reserve(rect)
+    cv.ensure_contains(rect)
+    if world > 1:
+        cv.set_band(rank, world)
+
+    frame_t = torch.from_numpy(np.ascontiguousarray(wl.frame)).to(dev)
+    anc_t = [torch.from_numpy(a).to(dev) for a in anchors_k]
+    war_t = [torch.from_numpy(q).to(dev) for q in warps_k]
+    apts_t = torch.from_numpy(e.apts).to(dev)
+    loc_t = torch.from_numpy(e.locals_).to(dev)
+    prob_t = torch.from_numpy(e.probs).to(dev)
+    act_t = torch.from_numpy(e.active).to(dev)
+    disp_t = torch.empty((fh, fw, 2), dtype=torch.float32, device=dev)
+    unc_t = torch.empty((fh, fw), dtype=torch.float32, device=dev)
+    stats_t = torch.zeros((nfr, 4), dtype=torch.int64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    grid = (0.0, 0.0, fw, fh)
+
+    ev = {k: [] for k in ("step", "emdq", "blend")}
+
+    def step(timed: bool):
+        if timed:
+            flush.fill_(1)  # L2 flush (untimed): 256 MiB > 126 MB L2
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+        M.emdq_field_device(grid, apts_t, loc_t, prob_t, act_t, alpha, beta, disp_t, unc_t, 16, ctx=ctx)
+        if timed:
+            e1.record(stream)
+        for k in range(nfr):
+            M.blend_frame_device(cv, frame_t, fw, fh, 3, anc_t[k], war_t[k], alpha, polys[k], stats_t[k])
+        if world > 1:
+            dist.all_reduce(stats_t)
+        if timed:
+            e2.record(stream)
+            ev["step"].append((e0, e2))
+            ev["emdq"].append((e0, e1))
+            ev["blend"].append((e1, e2))
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    l0 = ctx.launch_count()
+    for _ in range(args.steps):
+        step(True)
+    torch.cuda.synchronize()
+    launches = (ctx.launch_count() - l0)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+    tmax = ms["step"]
+    if world > 1:
+        t = torch.tensor([tmax], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tmax = float(t.item())
+    st = stats_t.cpu().numpy()
+    mpix_step = nfr * fw * fh / 1e6
+    value = mpix_step * args.steps / (tmax * 1e-3)
+
+    # ---- e2e: host-pointer C ABI, pinned buffers -----------------------------
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    h_frame = pin(wl.frame)
+    h_anc = [pin(a) for a in anchors_k]
+    h_war = [pin(q) for q in warps_k]
+    h_apts, h_loc, h_prob, h_act = pin(e.apts), pin(e.locals_), pin(e.probs), pin(e.active)
+    h_disp = torch.empty((fh, fw, 2), dtype=torch.float32).pin_memory().numpy()
+    h_unc = torch.empty((fh, fw), dtype=torch.float32).pin_memory().numpy()
+    g = M.Grid(0.0, 0.0, fw, fh)
+    lib = ctx._lib
+    import ctypes as C
+
+    def e2e_step():
+        M.check(lib.nrm_emdq_field(ctx.handle, C.byref(g), h_apts.ctypes.data, h_loc.ctypes.data,
+                                   h_prob.ctypes.data, len(h_apts), h_act.ctypes.data, len(h_act), alpha, 16, beta,
+                                   h_disp.ctypes.data, h_unc.ctypes.data))
+        out = []
+        for k in range(nfr):
+            s = M.BlendStats()
+            p = np.ascontiguousarray(polys[k])
+            M.check(lib.nrm_blend_frame(cv.handle, h_frame.ctypes.data, fw, fh, 3, h_anc[k].ctypes.data,
+                                        h_war[k].ctypes.data, len(h_anc[k]), alpha, p.ctypes.data, len(p),
+                                        C.byref(s)))
+            out.append(s)
+        return out
+
+    e2e_steps = args.e2e_steps or args.steps
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    t_e2e = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    h2d = h_frame.nbytes * nfr + sum(a.nbytes for a in h_anc) + sum(q.nbytes for q in h_war) + h_apts.nbytes + \
+        h_loc.nbytes + h_prob.nbytes + h_act.nbytes
+    d2h = h_disp.nbytes + h_unc.nbytes + 32 * nfr
+    e2e = {"value": mpix_step * e2e_steps / t_e2e, "unit": "Mpix/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "frames_per_s": nfr * e2e_steps / t_e2e,
+           "path": "nrm_emdq_field + nrm_blend_frame with pinned host buffers (blocking C ABI calls)"}
+
+    # ---- roofline for the dominant kernel -----------------------------------
+    roof = None
+    if rank == 0:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        fp32_peak = ctx.peak("fp32")   # measured FFMA lane-ops/s on this device
+        contrib = wl_contributors(wl, polys[0])
+        k_blend = ms["blend"] / args.steps / nfr   # per launch (one frame)
+        k_emdq = ms["emdq"] / args.steps
+        # K1: 10 FP32 pipe instructions per contributing (pixel, node) pair
+        # (SURVEY §8d), 2 flops per instruction-equivalent FMA
+        blend_flops = contrib["pairs"] * 10 * 2
+        emdq_flops = fw * fh * 16 * 8 * 2   # 16 blend pairs x (exp + 6 FMA + weight) per pixel, FMA-equivalents
+        dominant = "blend" if k_blend * nfr >= k_emdq else "emdq"
+        traffic = load_traffic()
+        if dominant == "blend":
+            ach = blend_flops / (k_blend * 1e-3) / 1e12
+            roof = {"kernel": "k_node_field<0> (K1 fused node field + mosaic update)", "bound": "fp32",
+                    "achieved": ach, "peak": 2 * fp32_peak / 1e12, "unit": "TFLOP/s",
+                    "frac": ach / (2 * fp32_peak / 1e12), "traffic": traffic.get("k_node_field"),
+                    "algorithmic": f"{contrib['pairs']:.4g} contributing pixel-node pairs x 10 FP32 ops",
+                    "peak_source": "measured FFMA probe (nrm_selftest_peak) on this device"}
+        else:
+            ach = emdq_flops / (k_emdq * 1e-3) / 1e12
+            roof = {"kernel": "k_emdq (K3 dense EMDQ field)", "bound": "fp32", "achieved": ach,
+                    "peak": 2 * fp32_peak / 1e12, "unit": "TFLOP/s", "frac": ach / (2 * fp32_peak / 1e12),
+                    "traffic": traffic.get("k_emdq"), "peak_source": "measured FFMA probe (nrm_selftest_peak)"}
+        # HBM view of the fused update: 29 B per footprint pixel (canvas r+w 26 B + frame 3 B)
+        fp_px = int(st[0][0])
+        roof["hbm_view"] = {"kernel": "K1", "achieved_gbs": fp_px * 29 / (k_blend * 1e-3) / 1e9,
+                            "peak_gbs": peaks.get("hbm_gbs"), "bytes_per_footprint_px": 29}
+        roof["kernel_ms"] = {"emdq_field": k_emdq, "blend_frame_per_frame": k_blend}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            model, ncpu = host_cpu()
+            t_frame, info = cpu_reference_step(wl, footprint_polygon_cpu(wl), max(8, args.ref_rows), ncpu)
+            cpu = {"value": fw * fh / 1e6 / t_frame, "unit": "Mpix/s", "cores": info["cores"], "kind": info["kind"],
+                   "sample": f"full blend_frame ({info['t_blend_s']*1e3:.0f} ms) + dense EMDQ field over "
+                             f"{info['field_rows']} of {fh} rows ({info['t_field_sample_s']*1e3:.0f} ms), "
+                             f"extrapolated to one frame; host {model}"}
+        except Exception as ex:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "Mpix/s", "cores": 0, "kind": "unavailable", "sample": repr(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tmax / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "frames_per_s": nfr * args.steps / (tmax * 1e-3),
+            "config": {"workload": CFG_NAME[args.config], "frame": [fw, fh], "matches": len(e.apts),
+                       "inliers": int(len(e.active)), "nodes": int(len(wl.anchors)), "canvas": wl.canvas,
+                       "frames_per_step": nfr, "parallelism": f"band{world}" if world > 1 else "single",
+                       "l2": "flushed between steps (256 MiB write, untimed)",
+                       "blend_stats_frame0": [int(v) for v in st[0]]},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def wl_contributors(wl, poly, sample: int = 20000):
+    """Contributing (pixel, node) pairs of one blend: the footprint pixel count
+    times the mean number of nodes with w > 1e-6 (the reference's cutoff,
+    mosaic.hpp:250), estimated on a seeded sample of footprint pixels."""
+    bx0, by0 = poly[:, 0].min() - 4, poly[:, 1].min() - 4
+    bx1, by1 = poly[:, 0].max() + 4, poly[:, 1].max() + 4
+    rng = np.random.default_rng(0)
+    xs = np.floor(rng.uniform(bx0, bx1, sample))
+    ys = np.floor(rng.uniform(by0, by1, sample))
+    d2 = (xs[:, None] - wl.anchors[None, :, 0]) ** 2 + (ys[:, None] - wl.anchors[None, :, 1]) ** 2
+    cnt = (np.exp(-wl.params.alpha * d2) > 1e-6).sum(1).mean()
+    npx = (np.ceil(bx1) - np.floor(bx0) + 1) * (np.ceil(by1) - np.floor(by0) + 1)
+    return {"pairs": float(npx * cnt), "per_px": float(cnt)}
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return {}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

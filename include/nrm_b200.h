@@ -183,6 +183,9 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
  * device so tests can check it bit-for-bit against the host libm. */
 int nrm_selftest_libm(nrm_ctx *ctx, const double *x, const double *y, int n, double *exp_out,
                       double *hypot_out);
+/* Measured pipe throughput on this device, lane-operations per second:
+ * which = 0: FP32 FFMA, which = 1: MUFU.EX2 (roofline denominators). */
+int nrm_selftest_peak(nrm_ctx *ctx, int which, double *ops_per_s);
 
 #ifdef __cplusplus
 }

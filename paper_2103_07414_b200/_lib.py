@@ -95,6 +95,7 @@ SIGNATURES = [
     ("nrm_emdq_field_device", C.c_int, [_P, C.POINTER(Grid), _P, _P, _P, C.c_int, _P, C.c_int,
                                         C.c_double, C.c_int, C.c_double, _P, _P]),
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
+    ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
 ]
 
 _lib: C.CDLL | None = None

@@ -839,4 +839,18 @@ int nrm_selftest_libm(nrm_ctx* c, const double* x, const double* y, int n, doubl
     return NRM_OK;
 }
 
+int nrm_selftest_peak(nrm_ctx* c, int which, double* ops_per_s) {
+    if (!c || !ops_per_s) return fail(NRM_EINVAL, "null argument");
+    if (which != 0 && which != 1) return fail(NRM_EINVAL, "which: 0 = FP32 FFMA, 1 = MUFU.EX2");
+    DeviceGuard g(c->device);
+    NRM_CUDA(c->misc.ensure(256));
+    const int iters = which == 0 ? 4096 : 1024;
+    float ms = 0.f;
+    NRM_CUDA(run_peak_probe(which, c->num_sms, iters, reinterpret_cast<float*>(c->misc.as<char>() + 64), c->stream,
+                            &ms, &c->launches));
+    const double ops = (double)c->num_sms * 8 * 256 * (double)iters * 16 * 8;  // lane-ops
+    *ops_per_s = ops / (ms * 1e-3);
+    return NRM_OK;
+}
+
 }  // extern "C"

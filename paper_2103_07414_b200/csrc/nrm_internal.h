@@ -117,6 +117,9 @@ cudaError_t launch_invert_boundary(int fw, int fh, const double* anchors, const 
 cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double* ex, double* hy,
                                  cudaStream_t st, int64_t* launches);
 
+cudaError_t run_peak_probe(int which, int num_sms, int iters, float* scratch, cudaStream_t st,
+                           float* ms, int64_t* launches);
+
 // ---- k_emdq.cu ------------------------------------------------------------
 struct EmdqLaunch {
     FieldGrid grid{};

@@ -88,6 +88,12 @@ class Context:
         check(self._lib.nrm_ctx_launch_count(self._h, C.byref(v)))
         return v.value
 
+    def peak(self, which: str = "fp32") -> float:
+        """Measured lane-ops/s of the FP32 FFMA ("fp32") or MUFU.EX2 ("mufu") pipe."""
+        v = C.c_double()
+        check(self._lib.nrm_selftest_peak(self._h, 0 if which == "fp32" else 1, C.byref(v)))
+        return v.value
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             self._lib.nrm_ctx_destroy(self._h)
