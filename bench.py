@@ -197,8 +197,8 @@ def footprint_polygon_cpu(wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
     ap.add_argument("--ref-rows", type=int, default=48, help="frame rows of the EMDQ field in the CPU sample")
@@ -224,7 +224,8 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     ctx = M.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)           # explicit stream: kernels and events share it
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
     # ---- workload: one frame per rank (frames of a batch sit side by side) --

@@ -8,20 +8,26 @@
 //   unc(p)   = node_uncertainty(p, apts[active], beta) = bounded_exp(beta d2min)
 //              (fieldest.hpp:44-52; the nearest inlier is the kNN's first).
 //
-// kNN membership decides which warps are blended, so it must match the
-// reference exactly: d^2 is computed in the exact tier (same FP64 operation
-// order as dist2) and ranked by the reference's (d^2, j) key.
-//
-// CTA = 16 x 16 pixel tile, one pixel per thread.
-//   1. radius bound: 256-bin histogram of squared centre distances gives
-//      R >= r_S(centre); every pixel's S nearest lie within R + 2*hd of the
-//      centre (hd = tile half-diagonal).
-//   2. candidates inside that disc are classified against the tile
-//      rectangle: "sure-in" (fewer than S other candidates can ever be
-//      closer), "sure-out" (at least S are always closer) or ambiguous.
-//   3. per pixel: exact d^2 for sure-in + ambiguous, sorted insertion of the
-//      ambiguous into the m = S - |sure-in| free slots, then the blend:
-//      weights on MUFU.EX2 (FP32), accumulation and normalisation in FP64.
+// The kNN membership decides which warps are blended, so it must equal the
+// reference's exactly. Design:
+//   CTA = 16 x 16 pixel tile; warp w owns an 8 x 4 sub-tile.
+//   1. radius bound: a 256-bin histogram of squared centre distances gives
+//      R >= r_S(centre); every pixel's S nearest lie within R + 2 hd.
+//   2. the candidates in that disc are classified in FP64 against the CTA
+//      rectangle -- "in" (fewer than S others can ever be closer), "out" (at
+//      least S are always closer), or ambiguous -- and the non-out ones are
+//      staged in shared memory in tile-local coordinates with their warps
+//      conjugated to the tile origin (T(-P) q T(o)).
+//   3. each warp re-classifies the ambiguous ones against its own sub-tile,
+//      leaving ~S/2 sure members and a handful of ambiguous ones per pixel.
+//   4. per pixel (FP32): distances, sorted insertion of the ambiguous keys
+//      into the m free slots, then the blend -- weights on MUFU.EX2, six FFMA
+//      accumulations. If the selected/rejected boundary keys are closer than
+//      the FP32 error bound, the pixel re-runs in the exact tier (FP64, the
+//      reference's operation order and libm, bit-identical kNN and blend).
+//   Tiles whose candidates span more than a quarter turn of rotation
+//   (hemisphere flips possible) or overflow the staging capacity run every
+//   pixel in the exact tier.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -34,36 +40,60 @@ namespace {
 
 constexpr int ET = 16;            // tile edge
 constexpr int ENT = ET * ET;      // threads
-constexpr int CAND_CAP = 512;     // candidates per tile
+constexpr int NW = ENT / 32;      // warps
+constexpr int WCAP = 128;         // per-warp gather capacity
+constexpr int CAND_CAP = NW * WCAP;
+constexpr int SCAP = 192;         // staged (non-out) candidates per tile
 constexpr int MAX_SUPPORT = 32;
+
+// Gathered candidate arrays (one entry per active index, in active order).
+struct Cand {
+    const double* x;
+    const double* y;
+    const float2* c32;   // coarse absolute coordinates for culling
+    const double* l;     // 5 per entry
+    const double* p;     // max(prob, 1e-6)
+    const double* phi;   // atan2(z, w)
+    const int* j;        // original index (reference tie-break)
+};
 
 struct ESmem {
     int hist[256];
-    int cand[CAND_CAP];
+    int wcand[NW][WCAP];
+    int wcnt[NW];
+    int list[CAND_CAP];
     double dmin2[CAND_CAP], dmax2[CAND_CAP];
-    unsigned char cls[CAND_CAP];  // 0 out, 1 in, 2 ambiguous
-    // staged blend-eligible points: [0, n_in) sure-in, [n_in, n_in + n_amb) ambiguous
-    double px[CAND_CAP], py[CAND_CAP], pp[CAND_CAP];
-    double pl[CAND_CAP][5];
-    int pj[CAND_CAP];
-    int stage[CAND_CAP];
-    int warp_cnt[ENT / 32];
-    int ncand, n_in, n_amb, slow;
+    unsigned char cls[CAND_CAP];
+    // staged: [0, n_in) CTA-in, [n_in, n_in + n_amb) CTA-ambiguous
+    int sidx[SCAP];
+    float ux[SCAP], uy[SCAP], dl[SCAP], pr[SCAP];
+    float4 q[SCAP];
+    float wdmin[NW][SCAP], wdmax[NW][SCAP];
+    unsigned char wcls[NW][SCAP];
+    unsigned char wl[NW][SCAP];  // per-warp list: [0, win) sure-in, then ambiguous
+    double red_lo[NW], red_hi[NW], red_d[NW];
+    int red_k[NW];
+    int nc, n_in, n_amb, slow, uniform;
     float R;
+    double P[2], Y0[2], e0[2], s0;
 };
 
 __global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
                          const double* __restrict__ probs, const int32_t* __restrict__ active,
-                         int nactive, double* cx, double* cy, double* cl, double* cp, int* cj) {
+                         int nactive, double* cx, double* cy, float2* c32, double* cl, double* cp,
+                         double* cphi, int* cj) {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= nactive) return;
     const int j = active[a];
-    cx[a] = apts[2 * j];
-    cy[a] = apts[2 * j + 1];
+    const double x = apts[2 * j], y = apts[2 * j + 1];
+    cx[a] = x;
+    cy[a] = y;
+    c32[a] = make_float2((float)x, (float)y);
 #pragma unroll
     for (int k = 0; k < 5; ++k) cl[5 * a + k] = locals[5 * j + k];
     const double p = probs[j];
     cp[a] = p < 1e-6 ? 1e-6 : p;  // std::max(probs[j], 1e-6)
+    cphi[a] = atan2(locals[5 * j + 2], locals[5 * j + 1]);
     cj[a] = j;
 }
 
@@ -78,104 +108,86 @@ __device__ __forceinline__ int hist_bin(float d2) {
 }
 __device__ __forceinline__ float bin_upper(int b) { return __uint_as_float((unsigned)(b + 1 + (127 << 3)) << 20); }
 
-// One pixel: S-nearest selection + blend. E* point into smem (fast tiles) or
-// the gathered global arrays (slow tiles: n_in = 0, every point ambiguous).
+// ---------------------------------------------------------------------------
+// Exact tier: detail::blend_local at (qx, qy) over candidate entries
+// idx[0..n) (or 0..n when idx is null) in the reference's operation order.
+// ---------------------------------------------------------------------------
 template <int MS>
-__device__ void emdq_pixel(double qx, double qy, int n_in, int n_amb, int m,
-                           const double* __restrict__ Ex, const double* __restrict__ Ey,
-                           const double* __restrict__ Ep, const double* __restrict__ El,
-                           const int* __restrict__ Ej, double alpha, double beta, float2* out_d,
-                           float* out_u) {
-    // sure-in: nearest key among them
-    double best_d = DBL_MAX;
-    int best_j = INT_MAX, best_k = -1;
-    for (int k = 0; k < n_in; ++k) {
-        const double d2 = xdist2(qx, qy, Ex[k], Ey[k]);
-        if (key_less(d2, Ej[k], best_d, best_j)) {
-            best_d = d2;
-            best_j = Ej[k];
-            best_k = k;
-        }
+__device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, int n, int S, const Cand& C,
+                           double alpha, double beta, float2* out_d, float* out_u) {
+    double sd[MS];
+    int sj[MS], sa[MS];
+#pragma unroll
+    for (int s = 0; s < MS; ++s) {
+        sd[s] = DBL_MAX;
+        sj[s] = INT_MAX;
+        sa[s] = -1;
     }
-    // ambiguous: keep the m smallest (d2, j) keys, sorted ascending
-    double sd[MS > 0 ? MS : 1];
-    int sj[MS > 0 ? MS : 1], sk[MS > 0 ? MS : 1];
-    if (MS > 0) {
+    for (int e = 0; e < n; ++e) {
+        const int a = idx ? idx[e] : e;
+        const double d2 = xdist2(qx, qy, C.x[a], C.y[a]);
+        const int j = C.j[a];
+        bool lt[MS];
 #pragma unroll
-        for (int s = 0; s < MS; ++s) {
-            sd[s] = DBL_MAX;
-            sj[s] = INT_MAX;
-            sk[s] = -1;
-        }
-        double wd = DBL_MAX;
-        int wj = INT_MAX;
-        for (int a = 0; a < n_amb; ++a) {
-            const int k = n_in + a;
-            const double d2 = xdist2(qx, qy, Ex[k], Ey[k]);
-            const int j = Ej[k];
-            if (!key_less(d2, j, wd, wj)) continue;
-            bool lt[MS > 0 ? MS : 1];
+        for (int s = 0; s < MS; ++s) lt[s] = key_less(d2, j, sd[s], sj[s]);
 #pragma unroll
-            for (int s = 0; s < MS; ++s) lt[s] = key_less(d2, j, sd[s], sj[s]);
-#pragma unroll
-            for (int s = MS - 1; s >= 0; --s) {
-                if (s < m) {
-                    if (s > 0 && lt[s - 1]) {
-                        sd[s] = sd[s - 1];
-                        sj[s] = sj[s - 1];
-                        sk[s] = sk[s - 1];
-                    } else if (lt[s]) {
-                        sd[s] = d2;
-                        sj[s] = j;
-                        sk[s] = k;
-                    }
+        for (int s = MS - 1; s >= 0; --s) {
+            if (s < S) {
+                if (s > 0 && lt[s - 1]) {
+                    sd[s] = sd[s - 1];
+                    sj[s] = sj[s - 1];
+                    sa[s] = sa[s - 1];
+                } else if (lt[s]) {
+                    sd[s] = d2;
+                    sj[s] = j;
+                    sa[s] = a;
                 }
             }
-#pragma unroll
-            for (int s = 0; s < MS; ++s)
-                if (s == m - 1) {
-                    wd = sd[s];
-                    wj = sj[s];
-                }
-        }
-        if (m > 0 && key_less(sd[0], sj[0], best_d, best_j)) {
-            best_d = sd[0];
-            best_j = sj[0];
-            best_k = sk[0];
         }
     }
-    const double d2min = best_d;
-    const double rw = El[5 * best_k + 1], rz = El[5 * best_k + 2];
-    const float nal = (float)(-alpha * kLog2e);
-    double wsum = 0.0, sw = 0.0, sz = 0.0, sdx = 0.0, sdy = 0.0, ss = 0.0;
-    auto accum = [&](int k, double d2) {
-        const float arg = (float)(d2 - d2min) * nal;
-        const double w = (double)ex2_approx(arg) * Ep[k];
-        wsum += w;
-        if (w <= 0.0) return;
-        const double* q = &El[5 * k];
-        double qw = q[1], qz = q[2], qdx = q[3], qdy = q[4];
-        if (xadd(xmul(qw, rw), xmul(qz, rz)) < 0.0) {
-            qw = -qw; qz = -qz; qdx = -qdx; qdy = -qdy;
-        }
-        sw = fma(w, qw, sw);
-        sz = fma(w, qz, sz);
-        sdx = fma(w, qdx, sdx);
-        sdy = fma(w, qdy, sdy);
-        ss = fma(w, q[0], ss);
-    };
-    for (int k = 0; k < n_in; ++k) accum(k, xdist2(qx, qy, Ex[k], Ey[k]));
-    if (MS > 0) {
+    // dq_blend (dualquat.hpp:133-162) over the sorted S nearest
+    const double d2min = sd[0];
+    const double na = -alpha;
+    double w[MS];
+    double wsum = 0.0;
+    int ref = -1;
 #pragma unroll
-        for (int s = 0; s < MS; ++s)
-            if (s < m) accum(sk[s], sd[s]);
+    for (int s = 0; s < MS; ++s) {
+        w[s] = 0.0;
+        if (s < S) {
+            w[s] = xmul(xexp(xmul(na, xsub(sd[s], d2min))), C.p[sa[s]]);
+            if (w[s] > 0.0 && ref < 0) ref = s;
+            wsum = xadd(wsum, w[s]);
+        }
     }
-    const double inv = 1.0 / wsum;
-    const double mw = sw * inv, mz = sz * inv, mdx = sdx * inv, mdy = sdy * inv;
+    double sw = 0.0, sz = 0.0, sdx = 0.0, sdy = 0.0, ss = 0.0;
+    double rw = 0.0, rz = 0.0;
+#pragma unroll
+    for (int s = 0; s < MS; ++s)
+        if (s == ref) {
+            rw = C.l[5 * sa[s] + 1];
+            rz = C.l[5 * sa[s] + 2];
+        }
+#pragma unroll
+    for (int s = 0; s < MS; ++s) {
+        if (s < S && w[s] > 0.0) {
+            const double* q = &C.l[5 * sa[s]];
+            double qw = q[1], qz = q[2], qdx = q[3], qdy = q[4];
+            if (xadd(xmul(qw, rw), xmul(qz, rz)) < 0.0) {
+                qw = -qw; qz = -qz; qdx = -qdx; qdy = -qdy;
+            }
+            sw = xadd(sw, xmul(w[s], qw));
+            sz = xadd(sz, xmul(w[s], qz));
+            sdx = xadd(sdx, xmul(w[s], qdx));
+            sdy = xadd(sdy, xmul(w[s], qdy));
+            ss = xadd(ss, xmul(w[s], q[0]));
+        }
+    }
+    const double mw = sw / wsum, mz = sz / wsum, mdx = sdx / wsum, mdy = sdy / wsum;
     const double nr = xhypot(mw, mz);
-    float2 dout = make_float2(0.f, 0.f);
-    if (nr >= 1e-300) {
-        W5 f{ss * inv, mw / nr, mz / nr, mdx / nr, mdy / nr};
+    float2 dout;
+    if (ref >= 0 && nr >= 1e-300) {
+        const W5 f{ss / wsum, mw / nr, mz / nr, mdx / nr, mdy / nr};
         double yx, yy;
         xapply(f, qx, qy, &yx, &yy);
         dout = make_float2((float)(yx - qx), (float)(yy - qy));
@@ -184,111 +196,250 @@ __device__ void emdq_pixel(double qx, double qy, int n_in, int n_amb, int m,
     }
     if (out_d) *out_d = dout;
     if (out_u) {
-        double arg = beta * d2min;
+        double arg = xmul(beta, d2min);
         if (55.0 < arg) arg = 55.0;
         *out_u = (float)xexp(arg);
     }
 }
 
-template <int MS>
-__device__ __forceinline__ void emdq_dispatch_leaf(double qx, double qy, int n_in, int n_amb, int m,
-                                                   const double* Ex, const double* Ey,
-                                                   const double* Ep, const double* El,
-                                                   const int* Ej, double alpha, double beta,
-                                                   float2* od, float* ou) {
-    emdq_pixel<MS>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
-}
-
-template <int MAXMS>
-__device__ void emdq_dispatch(double qx, double qy, int n_in, int n_amb, int m, const double* Ex,
-                              const double* Ey, const double* Ep, const double* El, const int* Ej,
-                              double alpha, double beta, float2* od, float* ou) {
-    if (m <= 0)
-        emdq_dispatch_leaf<0>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
-    else if (m <= 2)
-        emdq_dispatch_leaf<2>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
-    else if (m <= 4)
-        emdq_dispatch_leaf<4>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
-    else if (m <= 8)
-        emdq_dispatch_leaf<8>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
-    else if (m <= 16 || MAXMS <= 16)
-        emdq_dispatch_leaf<16>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
+template <int MAXS>
+__device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx, int n, int S, const Cand& C,
+                                            double alpha, double beta, float2* od, float* ou) {
+    if (S <= 16 || MAXS <= 16)
+        emdq_exact<16>(qx, qy, idx, n, S, C, alpha, beta, od, ou);
     else
-        emdq_dispatch_leaf<MAXMS>(qx, qy, n_in, n_amb, m, Ex, Ey, Ep, El, Ej, alpha, beta, od, ou);
+        emdq_exact<MAXS>(qx, qy, idx, n, S, C, alpha, beta, od, ou);
 }
 
-template <int MAXMS>
-__global__ void __launch_bounds__(ENT)
-k_emdq(EmdqLaunch L, const int* __restrict__ cj, int S) {
+// ---------------------------------------------------------------------------
+// Fast tier for one pixel (ux, uy = tile-local pixel position).
+// ---------------------------------------------------------------------------
+struct FastOut {
+    float s0, s1, s2, s3, s4, s5;  // sums: w*qw, w*qz, w*qdx, w*qdy, w*(s-s0), w
+    int k0, k1;                    // nearest and runner-up staged entries
+    float d0, d1;                  // their FP32 squared distances
+    bool exact;                    // boundary near-tie: rerun in the exact tier
+};
+
+// Bound on |FP32 d^2 - exact d^2| for tile-local coordinates.
+__device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
+
+template <int MS>
+__device__ __forceinline__ void fast_pixel(float ux, float uy, const unsigned char* __restrict__ lst, int nin,
+                                           int namb, int m, const ESmem& s, float nal, FastOut& o) {
+    float b0 = FLT_MAX, b1 = FLT_MAX;
+    int k0 = -1, k1 = -1;
+    auto track = [&](float d2, int k) {
+        if (d2 < b0) {
+            b1 = b0;
+            k1 = k0;
+            b0 = d2;
+            k0 = k;
+        } else if (d2 < b1) {
+            b1 = d2;
+            k1 = k;
+        }
+    };
+    for (int e = 0; e < nin; ++e) {
+        const int k = lst[e];
+        const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
+        track(fmaf(dx, dx, dy * dy), k);
+    }
+    float sd[MS > 0 ? MS : 1];
+    int sk[MS > 0 ? MS : 1];
+    bool exact = false;
+    if (MS > 0) {
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            sd[q] = FLT_MAX;
+            sk[q] = -1;
+        }
+        float rej = FLT_MAX, worst = FLT_MAX;
+        for (int e = 0; e < namb; ++e) {
+            const int k = lst[nin + e];
+            const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
+            const float d2 = fmaf(dx, dx, dy * dy);
+            if (!(d2 < worst)) {
+                rej = fminf(rej, d2);
+                continue;
+            }
+            rej = fminf(rej, worst);  // the current last member is evicted (or a sentinel)
+            bool lt[MS > 0 ? MS : 1];
+#pragma unroll
+            for (int q = 0; q < MS; ++q) lt[q] = d2 < sd[q];
+#pragma unroll
+            for (int q = MS - 1; q >= 0; --q) {
+                if (q < m) {
+                    if (q > 0 && lt[q - 1]) {
+                        sd[q] = sd[q - 1];
+                        sk[q] = sk[q - 1];
+                    } else if (lt[q]) {
+                        sd[q] = d2;
+                        sk[q] = k;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < MS; ++q)
+                if (q == m - 1) worst = sd[q];
+        }
+        // near-tie between the last member and the first rejected key
+        if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
+#pragma unroll
+        for (int q = 0; q < MS; ++q)
+            if (q < m) track(sd[q], sk[q]);
+    }
+    const float d2min = b0;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+    auto acc = [&](int k, float d2) {
+        const float w = ex2_approx((d2 - d2min) * nal) * s.pr[k];
+        const float4 q = s.q[k];
+        a0 = fmaf(w, q.x, a0);
+        a1 = fmaf(w, q.y, a1);
+        a2 = fmaf(w, q.z, a2);
+        a3 = fmaf(w, q.w, a3);
+        a4 = fmaf(w, s.dl[k], a4);
+        a5 += w;
+    };
+    for (int e = 0; e < nin; ++e) {
+        const int k = lst[e];
+        const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
+        acc(k, fmaf(dx, dx, dy * dy));
+    }
+    if (MS > 0) {
+#pragma unroll
+        for (int q = 0; q < MS; ++q)
+            if (q < m) acc(sk[q], sd[q]);
+    }
+    o = FastOut{a0, a1, a2, a3, a4, a5, k0, k1, b0, b1, exact};
+}
+
+__device__ __forceinline__ void fast_dispatch(float ux, float uy, const unsigned char* lst, int nin, int namb,
+                                              int m, const ESmem& s, float nal, FastOut& o) {
+    if (m <= 0)
+        fast_pixel<0>(ux, uy, lst, nin, namb, m, s, nal, o);
+    else if (m <= 2)
+        fast_pixel<2>(ux, uy, lst, nin, namb, m, s, nal, o);
+    else if (m <= 4)
+        fast_pixel<4>(ux, uy, lst, nin, namb, m, s, nal, o);
+    else if (m <= 8)
+        fast_pixel<8>(ux, uy, lst, nin, namb, m, s, nal, o);
+    else
+        fast_pixel<16>(ux, uy, lst, nin, namb, m, s, nal, o);
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(ENT, 2)
+k_emdq(EmdqLaunch L, Cand C, int S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ESmem& s = *reinterpret_cast<ESmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int ti0 = L.grid.i0 + blockIdx.x * ET, tj0 = L.grid.j0 + blockIdx.y * ET;
     const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
-    const double xlo = L.grid.gx + ti0, xhi = L.grid.gx + ti1;
-    const double ylo = L.grid.gy + tj0, yhi = L.grid.gy + tj1;
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // tile origin (pixel (ti0, tj0))
+    const double xlo = ox, xhi = L.grid.gx + ti1, ylo = oy, yhi = L.grid.gy + tj1;
     const double cxm = 0.5 * (xlo + xhi), cym = 0.5 * (ylo + yhi);
     const double hd = 0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo));
     const int N = L.nactive;
+    const float cxf = (float)cxm, cyf = (float)cym;
 
-    // ---- 1. radius bound from a histogram of centre distances -----------
+    // this thread's pixel: warp w -> 8x4 sub-tile
+    const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
+    const int pi = ti0 + lx, pj = tj0 + ly;
+    const bool valid = pi <= ti1 && pj <= tj1;
+    const size_t o = (size_t)(pj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (pi - L.grid.i0);
+    const double qx = L.grid.gx + pi, qy = L.grid.gy + pj;
+    float2* od = (valid && L.disp) ? &L.disp[o] : nullptr;
+    float* ou = (valid && L.unc) ? &L.unc[o] : nullptr;
+
+    // ---- 1. radius bound ------------------------------------------------
     s.hist[t] = 0;
     if (t == 0) {
-        s.ncand = 0;
         s.slow = 0;
+        s.uniform = 1;
     }
     __syncthreads();
     for (int a = t; a < N; a += ENT) {
-        const float dx = (float)(L.cx[a] - cxm), dy = (float)(L.cy[a] - cym);
-        atomicAdd(&s.hist[hist_bin(dx * dx + dy * dy)], 1);
+        const float2 c = C.c32[a];
+        const float dx = c.x - cxf, dy = c.y - cyf;
+        atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
     }
     __syncthreads();
-    if (t == 0) {
-        int acc = 0, b = 0;
-        for (; b < 256; ++b) {
-            acc += s.hist[b];
-            if (acc >= S) break;
+    if (wid == 0) {
+        int v[8], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            v[k] = s.hist[lane * 8 + k];
+            sum += v[k];
         }
-        // bin upper edges are exact floats; relative slack covers FP32 error
-        s.R = (b >= 255) ? INFINITY : sqrtf(bin_upper(b)) * 1.0001f + 0.01f;
+        int incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int n = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += n;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= S);
+        const int hl = __ffs(hit) - 1;
+        if (lane == hl) {
+            int acc = incl - sum, b = lane * 8 + 7;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                acc += v[k];
+                if (acc >= S) {
+                    b = lane * 8 + k;
+                    break;
+                }
+            }
+            // slack for the FP32 coarse coordinates
+            s.R = (b >= 255) ? INFINITY : sqrtf(bin_upper(b)) * 1.0001f + 0.05f;
+        }
+        if (hit == 0 && lane == 0) s.R = INFINITY;
     }
     __syncthreads();
     const float lim = s.R + (float)(2.0 * hd) + 1.0f;
     const float lim2 = lim * lim;
 
-    // ---- 2. ordered candidate gather --------------------------------------
-    for (int base = 0; base < N; base += ENT) {
-        const int a = base + t;
-        bool keep = false;
-        if (a < N) {
-            const float dx = (float)(L.cx[a] - cxm), dy = (float)(L.cy[a] - cym);
-            keep = !(dx * dx + dy * dy > lim2);
+    // ---- 2. per-warp gather (deterministic order: warp-major) -----------
+    {
+        const int per = (N + NW - 1) / NW;
+        const int a0 = wid * per, a1 = min(N, a0 + per);
+        int cnt = 0;
+        for (int base = a0; base < a1; base += 32) {
+            const int a = base + lane;
+            bool keep = false;
+            if (a < a1) {
+                const float2 c = C.c32[a];
+                const float dx = c.x - cxf, dy = c.y - cyf;
+                keep = !(fmaf(dx, dx, dy * dy) > lim2);
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = cnt + __popc(msk & ((1u << lane) - 1u));
+                if (pos < WCAP) s.wcand[wid][pos] = a;
+            }
+            cnt += __popc(msk);
         }
-        const unsigned msk = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) s.warp_cnt[wid] = __popc(msk);
-        __syncthreads();
-        int off = s.ncand;
-        for (int w = 0; w < wid; ++w) off += s.warp_cnt[w];
-        if (keep) {
-            const int pos = off + __popc(msk & ((1u << lane) - 1u));
-            if (pos < CAND_CAP) s.cand[pos] = a;
-            else s.slow = 1;
+        if (lane == 0) {
+            s.wcnt[wid] = cnt;
+            if (cnt > WCAP) s.slow = 1;
         }
-        __syncthreads();
-        if (t == 0) {
-            int tot = 0;
-            for (int w = 0; w < ENT / 32; ++w) tot += s.warp_cnt[w];
-            s.ncand += tot;
-        }
-        __syncthreads();
     }
-    const int nc = min(s.ncand, CAND_CAP);
+    __syncthreads();
+    {
+        int off = 0;
+        for (int w = 0; w < wid; ++w) off += min(s.wcnt[w], WCAP);
+        const int cnt = min(s.wcnt[wid], WCAP);
+        for (int k = lane; k < cnt; k += 32) s.list[off + k] = s.wcand[wid][k];
+        if (t == ENT - 1) s.nc = off + cnt;
+    }
+    __syncthreads();
+    const int nc = s.nc;
 
-    // ---- 3. classify against the tile rectangle (FP64) ----------------------
+    // ---- 3. CTA classification (FP64) -----------------------------------
     if (!s.slow) {
         for (int k = t; k < nc; k += ENT) {
-            const int a = s.cand[k];
-            const double ax = L.cx[a], ay = L.cy[a];
+            const int a = s.list[k];
+            const double ax = C.x[a], ay = C.y[a];
             const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
             const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
             s.dmin2[k] = dxn * dxn + dyn * dyn;
@@ -307,65 +458,230 @@ k_emdq(EmdqLaunch L, const int* __restrict__ cj, int S) {
             s.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
         }
         __syncthreads();
-        if (t == 0) {
+        // ordered staging: in first, then ambiguous (one warp, ballot compaction)
+        if (wid == 0) {
             int ni = 0, na = 0;
-            for (int k = 0; k < nc; ++k) {
-                ni += s.cls[k] == 1;
-                na += s.cls[k] == 2;
+            for (int base = 0; base < nc; base += 32) {
+                const int k = base + lane;
+                const int c = k < nc ? s.cls[k] : 0;
+                ni += __popc(__ballot_sync(0xffffffffu, c == 1));
+                na += __popc(__ballot_sync(0xffffffffu, c == 2));
             }
-            s.n_in = ni;
-            s.n_amb = na;
-            if (ni > S || ni + na < S || ni + na > CAND_CAP) s.slow = 1;
+            const bool bad = ni > S || ni + na < S || ni + na > SCAP;
+            if (lane == 0) {
+                s.n_in = ni;
+                s.n_amb = na;
+                if (bad) s.slow = 1;
+            }
+            if (!bad) {
+                int pi_ = 0, pa_ = ni;
+                for (int base = 0; base < nc; base += 32) {
+                    const int k = base + lane;
+                    const int c = k < nc ? s.cls[k] : 0;
+                    const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+                    const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+                    const unsigned lt = (1u << lane) - 1u;
+                    if (c == 1) s.sidx[pi_ + __popc(mi & lt)] = s.list[k];
+                    if (c == 2) s.sidx[pa_ + __popc(ma & lt)] = s.list[k];
+                    pi_ += __popc(mi);
+                    pa_ += __popc(ma);
+                }
+            }
         }
         __syncthreads();
     }
 
-    const int i = ti0 + (t % ET), j = tj0 + (t / ET);
-    const bool valid = i <= ti1 && j <= tj1;
-    const size_t o = (size_t)(j - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
-    const double qx = L.grid.gx + i, qy = L.grid.gy + j;
-    float2* od = (valid && L.disp) ? &L.disp[o] : nullptr;
-    float* ou = (valid && L.unc) ? &L.unc[o] : nullptr;
-
-    if (s.slow) {  // exact brute force over every candidate (pathological tiles)
-        if (valid) emdq_dispatch<MAXMS>(qx, qy, 0, N, S, L.cx, L.cy, L.cp, L.cl, cj, L.alpha, L.beta, od, ou);
+    if (s.slow) {  // overflow / inconsistent classification: exact brute force over all candidates
+        if (valid) exact_dispatch<MAXS>(qx, qy, nullptr, N, S, C, L.alpha, L.beta, od, ou);
         return;
     }
 
-    // ---- 4. stage sure-in then ambiguous (ordered) -----------------------
-    if (t == 0) {
-        int pi = 0, pa = s.n_in;
-        for (int k = 0; k < nc; ++k) {
-            const int c = s.cls[k];
-            if (c == 0) continue;
-            const int pos = c == 1 ? pi++ : pa++;
-            s.stage[pos] = s.cand[k];
+    // ---- 4. hemisphere arc + per-tile reference (FP64) -------------------
+    const int ne = s.n_in + s.n_amb;
+    {
+        const double phi0 = C.phi[s.sidx[0]];
+        double lo = 0.0, hi = 0.0, best = 1e300;
+        int bestk = 0x7fffffff;
+        for (int k = t; k < ne; k += ENT) {
+            const int a = s.sidx[k];
+            const double rel = remainder(C.phi[a] - phi0, 2.0 * M_PI);
+            lo = fmin(lo, rel);
+            hi = fmax(hi, rel);
+            const double dx = C.x[a] - cxm, dy = C.y[a] - cym;
+            const double d2 = dx * dx + dy * dy;
+            if (d2 < best || (d2 == best && k < bestk)) {
+                best = d2;
+                bestk = k;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+            const double bd = __shfl_xor_sync(0xffffffffu, best, d);
+            const int bk = __shfl_xor_sync(0xffffffffu, bestk, d);
+            if (bd < best || (bd == best && bk < bestk)) {
+                best = bd;
+                bestk = bk;
+            }
+        }
+        if (lane == 0) {
+            s.red_lo[wid] = lo;
+            s.red_hi[wid] = hi;
+            s.red_d[wid] = best;
+            s.red_k[wid] = bestk;
+        }
+        __syncthreads();
+        if (t == 0) {
+            for (int w = 1; w < NW; ++w) {
+                lo = fmin(lo, s.red_lo[w]);
+                hi = fmax(hi, s.red_hi[w]);
+                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_k[w] < bestk)) {
+                    best = s.red_d[w];
+                    bestk = s.red_k[w];
+                }
+            }
+            s.uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
+            const W5 qr = load_w5(&C.l[5 * s.sidx[bestk]]);
+            double yx, yy;
+            xapply(qr, ox, oy, &yx, &yy);
+            s.s0 = qr.s;
+            s.Y0[0] = rint(yx);
+            s.Y0[1] = rint(yy);
+            s.P[0] = s.Y0[0] / qr.s;
+            s.P[1] = s.Y0[1] / qr.s;
+            s.e0[0] = fma(qr.s, s.P[0], -s.Y0[0]);
+            s.e0[1] = fma(qr.s, s.P[1], -s.Y0[1]);
+            if (!(qr.s > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) s.uniform = 0;
+        }
+        __syncthreads();
+    }
+    if (!s.uniform) {  // hemisphere flips possible: exact tier over the staged candidates
+        if (valid) exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        return;
+    }
+
+    // ---- 5. stage local coordinates + conjugated warps -------------------
+    {
+        const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
+        for (int k = t; k < ne; k += ENT) {
+            const int a = s.sidx[k];
+            const W5 q = load_w5(&C.l[5 * a]);
+            const double hx = 0.5 * ox, hy = 0.5 * oy;
+            const double qa_dx = (q.w * hx - q.z * hy) + q.dx;  // q * T(o)
+            const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
+            const double px = 0.5 * P0, py = 0.5 * P1;         // T(-P) * (q * T(o))
+            s.q[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
+                                 (float)(qa_dy + (px * q.z - py * q.w)));
+            s.dl[k] = (float)(q.s - s0);
+            s.pr[k] = (float)C.p[a];
+            s.ux[k] = (float)(C.x[a] - ox);
+            s.uy[k] = (float)(C.y[a] - oy);
         }
     }
     __syncthreads();
-    const int ne = s.n_in + s.n_amb;
-    for (int pos = t; pos < ne; pos += ENT) {
-        const int a = s.stage[pos];
-        s.px[pos] = L.cx[a];
-        s.py[pos] = L.cy[a];
-        s.pp[pos] = L.cp[a];
-        s.pj[pos] = cj[a];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) s.pl[pos][q] = L.cl[5 * a + q];
+
+    // ---- 6. per-warp re-classification of the CTA-ambiguous --------------
+    const int nin = s.n_in;
+    const float wx0 = (float)((wid & 1) * 8), wy0 = (float)((wid >> 1) * 4);
+    const float cx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), cy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
+    const bool wempty = wx0 > cx1 || wy0 > cy1;
+    for (int k = lane; k < ne; k += 32) {
+        const float ax = s.ux[k], ay = s.uy[k];
+        const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - cx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - cy1);
+        const float dxf = fmaxf(ax - wx0, cx1 - ax), dyf = fmaxf(ay - wy0, cy1 - ay);
+        s.wdmin[wid][k] = fmaf(dxn, dxn, dyn * dyn);
+        s.wdmax[wid][k] = fmaf(dxf, dxf, dyf * dyf);
     }
-    __syncthreads();
-    if (valid)
-        emdq_dispatch<MAXMS>(qx, qy, s.n_in, s.n_amb, S - s.n_in, s.px, s.py, s.pp, &s.pl[0][0], s.pj,
-                      L.alpha, L.beta, od, ou);
+    __syncwarp();
+    int wi = nin, wa = 0;
+    if (!wempty) {
+        for (int k = nin + lane; k < ne; k += 32) {
+            const float hi = s.wdmax[wid][k] * (1.f + 1e-5f) + 1e-2f;
+            const float lo = s.wdmin[wid][k] * (1.f - 1e-5f) - 1e-2f;
+            int cle = 0, clt = 0;
+            for (int l = 0; l < ne; ++l) {
+                if (l == k) continue;
+                cle += s.wdmin[wid][l] <= hi;
+                clt += s.wdmax[wid][l] < lo;
+            }
+            s.wcls[wid][k] = (unsigned char)(cle < S ? 1 : (clt >= S ? 0 : 2));
+        }
+        __syncwarp();
+        for (int base = nin; base < ne; base += 32) {
+            const int k = base + lane;
+            const int c = k < ne ? s.wcls[wid][k] : 0;
+            const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+            if (c == 1) s.wl[wid][wi + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
+            wi += __popc(mi);
+        }
+        for (int base = nin; base < ne; base += 32) {
+            const int k = base + lane;
+            const int c = k < ne ? s.wcls[wid][k] : 0;
+            const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+            if (c == 2) s.wl[wid][wi + wa + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
+            wa += __popc(ma);
+        }
+    }
+    for (int k = lane; k < nin; k += 32) s.wl[wid][k] = (unsigned char)k;
+    __syncwarp();
+    const int m = S - wi;
+    const bool wslow = wempty || m < 0 || wi + wa < S || m > 16;
+
+    // ---- 7. per pixel --------------------------------------------------------
+    if (!valid) return;
+    FastOut fo;
+    bool ex = wslow;
+    if (!wslow) {
+        const float nal = (float)(-L.alpha * kLog2e);
+        fast_dispatch((float)lx, (float)ly, s.wl[wid], wi, wa, m, s, nal, fo);
+        ex = fo.exact || !(fo.s5 > 0.f);
+    }
+    if (ex) {
+        exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        return;
+    }
+    const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
+    const float qw = fo.s0 * rn, qz = fo.s1 * rn, qdx = fo.s2 * rn, qdy = fo.s3 * rn;
+    const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
+    const float ux = (float)lx, uy = (float)ly;
+    const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
+    const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
+    const float dlb = fo.s4 / fo.s5;
+    const double sb = s.s0 + (double)dlb;
+    const double yx = s.Y0[0] + (s.e0[0] + (double)dlb * s.P[0] + sb * (double)Qx);
+    const double yy = s.Y0[1] + (s.e0[1] + (double)dlb * s.P[1] + sb * (double)Qy);
+    if (od) *od = make_float2((float)(yx - qx), (float)(yy - qy));
+    if (ou) {
+        // d2min in the exact tier (the nearest, or the closer of two near-tied)
+        double d2m = xdist2(qx, qy, C.x[s.sidx[fo.k0]], C.y[s.sidx[fo.k0]]);
+        if (fo.k1 >= 0 && fo.d1 - fo.d0 <= d2_tol(fo.d1))
+            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[fo.k1]], C.y[s.sidx[fo.k1]]));
+        double arg = xmul(L.beta, d2m);
+        if (55.0 < arg) arg = 55.0;
+        *ou = (float)xexp(arg);
+    }
 }
 
 }  // namespace
 
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches) {
     if (L.nactive <= 0) return cudaErrorInvalidValue;
-    int* cj = reinterpret_cast<int*>(L.cp + L.nactive);  // scratch follows cp (see nrm_abi.cu)
-    k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active,
-                                                       L.nactive, L.cx, L.cy, L.cl, L.cp, cj);
+    const size_t na = (size_t)L.nactive;
+    // scratch layout (see emdq_core): x, y, l[5], p, phi (double) | c32 (float2) | j (int)
+    Cand C;
+    C.x = L.cx;
+    C.y = L.cy;
+    C.l = L.cl;
+    C.p = L.cp;
+    double* phi = L.cp + na;
+    C.phi = phi;
+    float2* c32 = reinterpret_cast<float2*>(phi + na);
+    C.c32 = c32;
+    int* cj = reinterpret_cast<int*>(c32 + na);
+    C.j = cj;
+    k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
+                                                       c32, L.cl, L.cp, phi, cj);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -375,10 +691,10 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     const size_t smem = sizeof(ESmem);
     if (S <= 16) {
         cudaFuncSetAttribute(k_emdq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<16><<<dim3(nx, ny), ENT, smem, st>>>(L, cj, S);
+        k_emdq<16><<<dim3(nx, ny), ENT, smem, st>>>(L, C, S);
     } else {
         cudaFuncSetAttribute(k_emdq<MAX_SUPPORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<MAX_SUPPORT><<<dim3(nx, ny), ENT, smem, st>>>(L, cj, S);
+        k_emdq<MAX_SUPPORT><<<dim3(nx, ny), ENT, smem, st>>>(L, C, S);
     }
     ++*launches;
     return cudaGetLastError();

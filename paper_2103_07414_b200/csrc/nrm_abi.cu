@@ -365,7 +365,7 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
     if ((size_t)grid->width * (size_t)grid->height == 0) return NRM_OK;
     const size_t na = (size_t)nactive;
-    NRM_CUDA(c->pts.ensure(na * 9 * sizeof(double) + na * sizeof(int) + 64));
+    NRM_CUDA(c->pts.ensure(na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + 64));
     double* base = c->pts.as<double>();
     EmdqLaunch L;
     L.grid = fg;
