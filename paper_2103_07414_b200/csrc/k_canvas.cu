@@ -1,5 +1,4 @@
-// k_canvas.cu -- canvas-wide passes: frame ingest (ImageU8 -> RGBA8),
-// render (mosaic.hpp:301-331), occupancy (mosaic.hpp:121-127) and the
+// k_canvas.cu -- canvas-wide passes: render (mosaic.hpp:301-331), occupancy (mosaic.hpp:121-127) and the
 // host-mirror transfers behind Canvas::color()/weight() (mosaic.hpp:111-120).
 // All are HBM-bound streaming kernels: one pixel per thread, coalesced rows.
 #include <cmath>
@@ -44,21 +43,6 @@ CanvasView view_of(const nrm_canvas* cv) {
     v.band_rank = cv->band_rank;
     v.band_count = cv->band_count;
     return v;
-}
-
-__global__ void k_frame_to_rgba(const uint8_t* __restrict__ raw, int npx, int ch, uchar4* __restrict__ out) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= npx) return;
-    uchar4 v;
-    if (ch == 1) {
-        const uint8_t g = raw[k];
-        v = make_uchar4(g, g, g, 255);
-    } else if (ch == 3) {
-        v = make_uchar4(raw[3 * k], raw[3 * k + 1], raw[3 * k + 2], 255);
-    } else {
-        v = reinterpret_cast<const uchar4*>(raw)[k];
-    }
-    out[k] = v;
 }
 
 __global__ void k_render(CanvasView v, int x0, int y0, int w, int h, uchar4* __restrict__ out) {
@@ -162,15 +146,6 @@ __global__ void k_canvas_write(float* r, float* g, float* b, uint8_t* wp, long l
 }
 
 }  // namespace
-
-cudaError_t launch_frame_to_rgba(const uint8_t* raw, int w, int h, int ch, uchar4* out,
-                                 cudaStream_t st, int64_t* launches) {
-    const int npx = w * h;
-    if (npx <= 0) return cudaSuccess;
-    k_frame_to_rgba<<<(npx + 255) / 256, 256, 0, st>>>(raw, npx, ch, out);
-    ++*launches;
-    return cudaGetLastError();
-}
 
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches) {

@@ -10,24 +10,26 @@
 //
 // The kNN membership decides which warps are blended, so it must equal the
 // reference's exactly. Design:
-//   CTA = 16 x 16 pixel tile; warp w owns an 8 x 4 sub-tile.
-//   1. radius bound: a 256-bin histogram of squared centre distances gives
-//      R >= r_S(centre); every pixel's S nearest lie within R + 2 hd.
-//   2. the candidates in that disc are classified in FP64 against the CTA
-//      rectangle -- "in" (fewer than S others can ever be closer), "out" (at
-//      least S are always closer), or ambiguous -- and the non-out ones are
-//      staged in shared memory in tile-local coordinates with their warps
-//      conjugated to the tile origin (T(-P) q T(o)).
-//   3. each warp re-classifies the ambiguous ones against its own sub-tile,
-//      leaving ~S/2 sure members and a handful of ambiguous ones per pixel.
-//   4. per pixel (FP32): distances, sorted insertion of the ambiguous keys
-//      into the m free slots, then the blend -- weights on MUFU.EX2, six FFMA
-//      accumulations. If the selected/rejected boundary keys are closer than
-//      the FP32 error bound, the pixel re-runs in the exact tier (FP64, the
-//      reference's operation order and libm, bit-identical kNN and blend).
+//   k_super (64 x 64 supertiles): a 256-bin histogram of squared centre
+//     distances bounds the S-th neighbour distance R; every point that can be
+//     among the S nearest of a supertile pixel lies within R + 2 hd of its
+//     centre. Those points form the supertile list (plus a rotation-arc flag).
+//   k_emdq (16 x 16 tiles, one pixel per thread): the same bound over the
+//     supertile list, then an FP64 classification of the tile's candidates
+//     against the tile rectangle: "in" (fewer than S others can ever be
+//     closer), "out" (at least S are always closer) or ambiguous. In and
+//     ambiguous ones are staged as packed records in tile-local coordinates
+//     with their warps conjugated to the tile origin (T(-P) q T(o)).
+//   Per pixel (FP32): one pass over the sure members accumulating weighted
+//     warps (weights on MUFU.EX2 relative to a tile-wide d^2 floor: a common
+//     factor cancels in dq_blend's normalisation), an early-reject sorted
+//     insertion of the ambiguous (closest first) into the m = S - |in| free
+//     slots, their accumulation, and the epilogue. When the selected and
+//     rejected boundary keys are within the FP32 error bound, the pixel re-runs
+//     in the exact tier (FP64, reference operation order and libm: the kNN
+//     set and blend are bit-identical to the reference's).
 //   Tiles whose candidates span more than a quarter turn of rotation
-//   (hemisphere flips possible) or overflow the staging capacity run every
-//   pixel in the exact tier.
+//   (hemisphere flips possible) or overflow a capacity run in the exact tier.
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -41,10 +43,13 @@ namespace {
 constexpr int ET = 16;            // tile edge
 constexpr int ENT = ET * ET;      // threads
 constexpr int NW = ENT / 32;      // warps
-constexpr int WCAP = 128;         // per-warp gather capacity
-constexpr int CAND_CAP = NW * WCAP;
-constexpr int SCAP = 192;         // staged (non-out) candidates per tile
+constexpr int CAND_CAP = 512;     // tile candidates
+constexpr int SCAP = 192;         // staged (in + ambiguous) per tile
 constexpr int MAX_SUPPORT = 32;
+constexpr int ST = 64;            // supertile edge (4 x 4 tiles)
+constexpr int WCAP_S = 256;       // per-warp gather capacity in the supertile pass
+constexpr int SLIST_CAP = 1024;   // supertile list capacity
+constexpr int SFLAG_OVERFLOW = 1, SFLAG_NONUNIFORM = 2;
 
 // Gathered candidate arrays (one entry per active index, in active order).
 struct Cand {
@@ -57,25 +62,36 @@ struct Cand {
     const int* j;        // original index (reference tie-break)
 };
 
+struct SuperLists {
+    int* list;   // [nsuper][SLIST_CAP]
+    int* count;  // [nsuper]
+    int* flag;   // [nsuper]
+    int nsx;     // supertiles per row
+};
+
 struct ESmem {
     int hist[256];
-    int wcand[NW][WCAP];
     int wcnt[NW];
     int list[CAND_CAP];
-    double dmin2[CAND_CAP], dmax2[CAND_CAP];
+    double dmin2[CAND_CAP], dmax2[CAND_CAP], dc2[CAND_CAP];
     unsigned char cls[CAND_CAP];
-    // staged: [0, n_in) CTA-in, [n_in, n_in + n_amb) CTA-ambiguous
+    // staged: [0, n_in) CTA-in (index order), [n_in, ne) ambiguous (closest first)
     int sidx[SCAP];
-    float ux[SCAP], uy[SCAP], dl[SCAP], pr[SCAP];
-    float4 q[SCAP];
-    float wdmin[NW][SCAP], wdmax[NW][SCAP];
-    unsigned char wcls[NW][SCAP];
-    unsigned char wl[NW][SCAP];  // per-warp list: [0, win) sure-in, then ambiguous
-    double red_lo[NW], red_hi[NW], red_d[NW];
+    float4 rec0[SCAP];  // ux, uy (tile-local), prob, s - s0
+    float4 rec1[SCAP];  // conjugated dual quaternion (w, z, dx, dy)
+    double red_d[NW];
     int red_k[NW];
-    int nc, n_in, n_amb, slow, uniform;
-    float R;
+    int nc, n_in, n_amb, slow;
+    float R, d2ref;
     double P[2], Y0[2], e0[2], s0;
+};
+
+struct SSmem {
+    int hist[256];
+    int wcnt[NW];
+    int wcand[NW][WCAP_S];
+    double red_lo[NW], red_hi[NW];
+    float R;
 };
 
 __global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
@@ -107,6 +123,139 @@ __device__ __forceinline__ int hist_bin(float d2) {
     return b < 0 ? 0 : (b > 254 ? 255 : b);
 }
 __device__ __forceinline__ float bin_upper(int b) { return __uint_as_float((unsigned)(b + 1 + (127 << 3)) << 20); }
+
+// Warp 0: from a 256-bin histogram, an upper bound on the S-th smallest
+// squared distance -> R (with slack for the FP32 coarse coordinates).
+__device__ __forceinline__ void radius_from_hist(const int* hist, int S, int lane, float* R) {
+    int v[8], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[k] = hist[lane * 8 + k];
+        sum += v[k];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += n;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, incl >= S);
+    if (hit == 0) {
+        if (lane == 0) *R = INFINITY;
+        return;
+    }
+    if (lane == __ffs(hit) - 1) {
+        int acc = incl - sum, b = lane * 8 + 7;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            acc += v[k];
+            if (acc >= S) {
+                b = lane * 8 + k;
+                break;
+            }
+        }
+        *R = (b >= 255) ? INFINITY : sqrtf(bin_upper(b)) * 1.0001f + 0.05f;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Supertile pass: candidate superset + rotation arc for each 64 x 64 block.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists SL, int S) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int sid = blockIdx.y * SL.nsx + blockIdx.x;
+    const int i0 = L.grid.i0 + blockIdx.x * ST, j0 = L.grid.j0 + blockIdx.y * ST;
+    const int i1 = min(i0 + ST - 1, L.grid.i1), j1 = min(j0 + ST - 1, L.grid.j1);
+    const double xlo = L.grid.gx + i0, xhi = L.grid.gx + i1, ylo = L.grid.gy + j0, yhi = L.grid.gy + j1;
+    const float cx = (float)(0.5 * (xlo + xhi)), cy = (float)(0.5 * (ylo + yhi));
+    const float hd = (float)(0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo)));
+    const int N = L.nactive;
+
+    s.hist[t] = 0;
+    __syncthreads();
+    for (int a = t; a < N; a += ENT) {
+        const float2 c = C.c32[a];
+        const float dx = c.x - cx, dy = c.y - cy;
+        atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
+    }
+    __syncthreads();
+    if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
+    __syncthreads();
+    const float lim = s.R + 2.f * hd + 1.f, lim2 = lim * lim;
+    // per-warp contiguous chunks keep the list order deterministic
+    const int per = (N + NW - 1) / NW;
+    const int a0 = wid * per, a1 = min(N, a0 + per);
+    int cnt = 0;
+    double lo = 0.0, hi = 0.0, phi0 = 0.0;
+    bool have0 = false;
+    for (int base = a0; base < a1; base += 32) {
+        const int a = base + lane;
+        bool keep = false;
+        if (a < a1) {
+            const float2 c = C.c32[a];
+            const float dx = c.x - cx, dy = c.y - cy;
+            keep = !(fmaf(dx, dx, dy * dy) > lim2);
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int pos = cnt + __popc(msk & ((1u << lane) - 1u));
+            if (pos < WCAP_S) s.wcand[wid][pos] = a;
+        }
+        cnt += __popc(msk);
+    }
+    if (lane == 0) s.wcnt[wid] = cnt;
+    __syncthreads();
+    int off = 0, total = 0;
+    for (int w = 0; w < NW; ++w) {
+        const int c = s.wcnt[w];
+        if (w < wid) off += c;
+        total += c;
+    }
+    bool overflow = total > SLIST_CAP;
+    for (int w = 0; w < NW; ++w) overflow |= s.wcnt[w] > WCAP_S;
+    if (!overflow) {
+        for (int k = lane; k < cnt; k += 32) SL.list[(size_t)sid * SLIST_CAP + off + k] = s.wcand[wid][k];
+    }
+    // rotation arc over the list (relative to the first listed point)
+    if (total > 0 && !overflow) {
+        int first = -1;
+        for (int w = 0; w < NW && first < 0; ++w)
+            if (s.wcnt[w] > 0) first = s.wcand[w][0];
+        phi0 = C.phi[first];
+        have0 = true;
+        for (int k = lane; k < cnt; k += 32) {
+            double rel = C.phi[s.wcand[wid][k]] - phi0;
+            if (rel > M_PI) rel -= 2.0 * M_PI;
+            if (rel < -M_PI) rel += 2.0 * M_PI;
+            lo = fmin(lo, rel);
+            hi = fmax(hi, rel);
+        }
+    }
+    (void)have0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+    }
+    if (lane == 0) {
+        s.red_lo[wid] = lo;
+        s.red_hi[wid] = hi;
+    }
+    __syncthreads();
+    if (t == 0) {
+        for (int w = 0; w < NW; ++w) {
+            lo = fmin(lo, s.red_lo[w]);
+            hi = fmax(hi, s.red_hi[w]);
+        }
+        int f = 0;
+        if (overflow) f |= SFLAG_OVERFLOW;
+        if (!((hi - lo) < (0.5 * M_PI - 1e-6))) f |= SFLAG_NONUNIFORM;
+        SL.flag[sid] = f;
+        SL.count[sid] = overflow ? N : total;
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Exact tier: detail::blend_local at (qx, qy) over candidate entries
@@ -203,7 +352,7 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
 }
 
 template <int MAXS>
-__device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx, int n, int S, const Cand& C,
+__device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx, int n, int S, const Cand C,
                                             double alpha, double beta, float2* od, float* ou) {
     if (S <= 16 || MAXS <= 16)
         emdq_exact<16>(qx, qy, idx, n, S, C, alpha, beta, od, ou);
@@ -225,11 +374,12 @@ struct FastOut {
 __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
 template <int MS>
-__device__ __forceinline__ void fast_pixel(float ux, float uy, const unsigned char* __restrict__ lst, int nin,
-                                           int namb, int m, const ESmem& s, float nal, FastOut& o) {
+__device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, int namb, int m, const ESmem& s, float nal,
+                                           float c0, FastOut& o) {
     float b0 = FLT_MAX, b1 = FLT_MAX;
     int k0 = -1, k1 = -1;
-    auto track = [&](float d2, int k) {
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
+    auto take = [&](int k, float d2, const float4& r0) {
         if (d2 < b0) {
             b1 = b0;
             k1 = k0;
@@ -239,25 +389,36 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, const unsigned ch
             b1 = d2;
             k1 = k;
         }
+        // exp(-alpha (d2 - d2ref)): the factor exp(alpha (d2min - d2ref)) common
+        // to every weight cancels in dq_blend's normalisation
+        const float w = ex2_approx(fmaf(d2, nal, c0)) * r0.z;
+        const float4 q = s.rec1[k];
+        a0 = fmaf(w, q.x, a0);
+        a1 = fmaf(w, q.y, a1);
+        a2 = fmaf(w, q.z, a2);
+        a3 = fmaf(w, q.w, a3);
+        a4 = fmaf(w, r0.w, a4);
+        a5 += w;
     };
-    for (int e = 0; e < nin; ++e) {
-        const int k = lst[e];
-        const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
-        track(fmaf(dx, dx, dy * dy), k);
+    for (int k = 0; k < nin; ++k) {
+        const float4 r0 = s.rec0[k];
+        const float dx = r0.x - ux, dy = r0.y - uy;
+        take(k, fmaf(dx, dx, dy * dy), r0);
     }
-    float sd[MS > 0 ? MS : 1];
-    int sk[MS > 0 ? MS : 1];
     bool exact = false;
     if (MS > 0) {
+        float sd[MS > 0 ? MS : 1];
+        int sk[MS > 0 ? MS : 1];
 #pragma unroll
         for (int q = 0; q < MS; ++q) {
             sd[q] = FLT_MAX;
-            sk[q] = -1;
+            sk[q] = 0;
         }
         float rej = FLT_MAX, worst = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
-            const int k = lst[nin + e];
-            const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
+            const int k = nin + e;
+            const float2 u = *reinterpret_cast<const float2*>(&s.rec0[k]);
+            const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
             if (!(d2 < worst)) {
                 rej = fminf(rej, d2);
@@ -287,50 +448,28 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, const unsigned ch
         if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
 #pragma unroll
         for (int q = 0; q < MS; ++q)
-            if (q < m) track(sd[q], sk[q]);
-    }
-    const float d2min = b0;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-    auto acc = [&](int k, float d2) {
-        const float w = ex2_approx((d2 - d2min) * nal) * s.pr[k];
-        const float4 q = s.q[k];
-        a0 = fmaf(w, q.x, a0);
-        a1 = fmaf(w, q.y, a1);
-        a2 = fmaf(w, q.z, a2);
-        a3 = fmaf(w, q.w, a3);
-        a4 = fmaf(w, s.dl[k], a4);
-        a5 += w;
-    };
-    for (int e = 0; e < nin; ++e) {
-        const int k = lst[e];
-        const float dx = s.ux[k] - ux, dy = s.uy[k] - uy;
-        acc(k, fmaf(dx, dx, dy * dy));
-    }
-    if (MS > 0) {
-#pragma unroll
-        for (int q = 0; q < MS; ++q)
-            if (q < m) acc(sk[q], sd[q]);
+            if (q < m) take(sk[q], sd[q], s.rec0[sk[q]]);
     }
     o = FastOut{a0, a1, a2, a3, a4, a5, k0, k1, b0, b1, exact};
 }
 
-__device__ __forceinline__ void fast_dispatch(float ux, float uy, const unsigned char* lst, int nin, int namb,
-                                              int m, const ESmem& s, float nal, FastOut& o) {
+__device__ __forceinline__ void fast_dispatch(float ux, float uy, int nin, int namb, int m, const ESmem& s,
+                                              float nal, float c0, FastOut& o) {
     if (m <= 0)
-        fast_pixel<0>(ux, uy, lst, nin, namb, m, s, nal, o);
+        fast_pixel<0>(ux, uy, nin, namb, m, s, nal, c0, o);
     else if (m <= 2)
-        fast_pixel<2>(ux, uy, lst, nin, namb, m, s, nal, o);
+        fast_pixel<2>(ux, uy, nin, namb, m, s, nal, c0, o);
     else if (m <= 4)
-        fast_pixel<4>(ux, uy, lst, nin, namb, m, s, nal, o);
+        fast_pixel<4>(ux, uy, nin, namb, m, s, nal, c0, o);
     else if (m <= 8)
-        fast_pixel<8>(ux, uy, lst, nin, namb, m, s, nal, o);
+        fast_pixel<8>(ux, uy, nin, namb, m, s, nal, c0, o);
     else
-        fast_pixel<16>(ux, uy, lst, nin, namb, m, s, nal, o);
+        fast_pixel<16>(ux, uy, nin, namb, m, s, nal, c0, o);
 }
 
 template <int MAXS>
 __global__ void __launch_bounds__(ENT, 2)
-k_emdq(EmdqLaunch L, Cand C, int S) {
+k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ESmem& s = *reinterpret_cast<ESmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -340,11 +479,16 @@ k_emdq(EmdqLaunch L, Cand C, int S) {
     const double xlo = ox, xhi = L.grid.gx + ti1, ylo = oy, yhi = L.grid.gy + tj1;
     const double cxm = 0.5 * (xlo + xhi), cym = 0.5 * (ylo + yhi);
     const double hd = 0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo));
-    const int N = L.nactive;
     const float cxf = (float)cxm, cyf = (float)cym;
 
-    // this thread's pixel: warp w -> 8x4 sub-tile
-    const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
+    // supertile list of this tile
+    const int sid = (blockIdx.y / (ST / ET)) * SL.nsx + blockIdx.x / (ST / ET);
+    const int sflag = SL.flag[sid];
+    const int nsrc = SL.count[sid];
+    const int* src = (sflag & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
+
+    // this thread's pixel (row-major 16 x 16)
+    const int lx = t & (ET - 1), ly = t >> 4;
     const int pi = ti0 + lx, pj = tj0 + ly;
     const bool valid = pi <= ti1 && pj <= tj1;
     const size_t o = (size_t)(pj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (pi - L.grid.i0);
@@ -352,172 +496,112 @@ k_emdq(EmdqLaunch L, Cand C, int S) {
     float2* od = (valid && L.disp) ? &L.disp[o] : nullptr;
     float* ou = (valid && L.unc) ? &L.unc[o] : nullptr;
 
-    // ---- 1. radius bound ------------------------------------------------
+    // ---- 1. radius bound over the supertile list --------------------------
     s.hist[t] = 0;
     if (t == 0) {
         s.slow = 0;
-        s.uniform = 1;
+        s.nc = 0;
     }
     __syncthreads();
-    for (int a = t; a < N; a += ENT) {
-        const float2 c = C.c32[a];
+    for (int e = t; e < nsrc; e += ENT) {
+        const float2 c = C.c32[src ? src[e] : e];
         const float dx = c.x - cxf, dy = c.y - cyf;
         atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
     }
     __syncthreads();
+    if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
+    __syncthreads();
+    const float lim = s.R + (float)(2.0 * hd) + 1.0f, lim2 = lim * lim;
+
+    // ---- 2. ordered gather ------------------------------------------------
+    for (int base = 0; base < nsrc; base += ENT) {
+        const int e = base + t;
+        int a = -1;
+        if (e < nsrc) {
+            a = src ? src[e] : e;
+            const float2 c = C.c32[a];
+            const float dx = c.x - cxf, dy = c.y - cyf;
+            if (fmaf(dx, dx, dy * dy) > lim2) a = -1;
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, a >= 0);
+        if (lane == 0) s.wcnt[wid] = __popc(msk);
+        __syncthreads();
+        int off = s.nc;
+        for (int w = 0; w < wid; ++w) off += s.wcnt[w];
+        if (a >= 0) {
+            const int pos = off + __popc(msk & ((1u << lane) - 1u));
+            if (pos < CAND_CAP) s.list[pos] = a;
+            else s.slow = 1;
+        }
+        __syncthreads();
+        if (t == 0)
+            for (int w = 0; w < NW; ++w) s.nc += s.wcnt[w];
+        __syncthreads();
+    }
+    const int nc = min(s.nc, CAND_CAP);
+
+    // ---- 3. classification against the tile rectangle (FP64) ------------
+    for (int k = t; k < nc; k += ENT) {
+        const int a = s.list[k];
+        const double ax = C.x[a], ay = C.y[a];
+        const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
+        const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
+        s.dmin2[k] = dxn * dxn + dyn * dyn;
+        s.dmax2[k] = dxf * dxf + dyf * dyf;
+        s.dc2[k] = (ax - cxm) * (ax - cxm) + (ay - cym) * (ay - cym);
+    }
+    __syncthreads();
+    for (int k = t; k < nc; k += ENT) {
+        const double hi = s.dmax2[k] * (1.0 + 1e-12) + 1e-9;
+        const double lo = s.dmin2[k] * (1.0 - 1e-12) - 1e-9;
+        int cle = 0, clt = 0;
+        for (int l = 0; l < nc; ++l) {
+            if (l == k) continue;
+            cle += s.dmin2[l] <= hi;
+            clt += s.dmax2[l] < lo;
+        }
+        s.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
+    }
+    __syncthreads();
+
+    // ---- 4. staging (warp 0): in-list in index order, ambiguous by centre
+    //         distance; tile reference = staged point nearest the centre ----
     if (wid == 0) {
-        int v[8], sum = 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            v[k] = s.hist[lane * 8 + k];
-            sum += v[k];
+        int ni = 0, na = 0;
+        for (int base = 0; base < nc; base += 32) {
+            const int k = base + lane;
+            const int c = k < nc ? s.cls[k] : 0;
+            ni += __popc(__ballot_sync(0xffffffffu, c == 1));
+            na += __popc(__ballot_sync(0xffffffffu, c == 2));
         }
-        int incl = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int n = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += n;
-        }
-        const unsigned hit = __ballot_sync(0xffffffffu, incl >= S);
-        const int hl = __ffs(hit) - 1;
-        if (lane == hl) {
-            int acc = incl - sum, b = lane * 8 + 7;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                acc += v[k];
-                if (acc >= S) {
-                    b = lane * 8 + k;
-                    break;
-                }
-            }
-            // slack for the FP32 coarse coordinates
-            s.R = (b >= 255) ? INFINITY : sqrtf(bin_upper(b)) * 1.0001f + 0.05f;
-        }
-        if (hit == 0 && lane == 0) s.R = INFINITY;
-    }
-    __syncthreads();
-    const float lim = s.R + (float)(2.0 * hd) + 1.0f;
-    const float lim2 = lim * lim;
-
-    // ---- 2. per-warp gather (deterministic order: warp-major) -----------
-    {
-        const int per = (N + NW - 1) / NW;
-        const int a0 = wid * per, a1 = min(N, a0 + per);
-        int cnt = 0;
-        for (int base = a0; base < a1; base += 32) {
-            const int a = base + lane;
-            bool keep = false;
-            if (a < a1) {
-                const float2 c = C.c32[a];
-                const float dx = c.x - cxf, dy = c.y - cyf;
-                keep = !(fmaf(dx, dx, dy * dy) > lim2);
-            }
-            const unsigned msk = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int pos = cnt + __popc(msk & ((1u << lane) - 1u));
-                if (pos < WCAP) s.wcand[wid][pos] = a;
-            }
-            cnt += __popc(msk);
-        }
-        if (lane == 0) {
-            s.wcnt[wid] = cnt;
-            if (cnt > WCAP) s.slow = 1;
-        }
-    }
-    __syncthreads();
-    {
-        int off = 0;
-        for (int w = 0; w < wid; ++w) off += min(s.wcnt[w], WCAP);
-        const int cnt = min(s.wcnt[wid], WCAP);
-        for (int k = lane; k < cnt; k += 32) s.list[off + k] = s.wcand[wid][k];
-        if (t == ENT - 1) s.nc = off + cnt;
-    }
-    __syncthreads();
-    const int nc = s.nc;
-
-    // ---- 3. CTA classification (FP64) -----------------------------------
-    if (!s.slow) {
-        for (int k = t; k < nc; k += ENT) {
-            const int a = s.list[k];
-            const double ax = C.x[a], ay = C.y[a];
-            const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
-            const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
-            s.dmin2[k] = dxn * dxn + dyn * dyn;
-            s.dmax2[k] = dxf * dxf + dyf * dyf;
-        }
-        __syncthreads();
-        for (int k = t; k < nc; k += ENT) {
-            const double hi = s.dmax2[k] * (1.0 + 1e-12) + 1e-9;
-            const double lo = s.dmin2[k] * (1.0 - 1e-12) - 1e-9;
-            int cle = 0, clt = 0;
-            for (int l = 0; l < nc; ++l) {
-                if (l == k) continue;
-                cle += s.dmin2[l] <= hi;
-                clt += s.dmax2[l] < lo;
-            }
-            s.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
-        }
-        __syncthreads();
-        // ordered staging: in first, then ambiguous (one warp, ballot compaction)
-        if (wid == 0) {
-            int ni = 0, na = 0;
+        const bool bad = s.slow || ni > S || ni + na < S || ni + na > SCAP;
+        double best = 1e300;
+        int bestk = 0x7fffffff;
+        if (!bad) {
+            int pi_ = 0;
             for (int base = 0; base < nc; base += 32) {
                 const int k = base + lane;
                 const int c = k < nc ? s.cls[k] : 0;
-                ni += __popc(__ballot_sync(0xffffffffu, c == 1));
-                na += __popc(__ballot_sync(0xffffffffu, c == 2));
+                const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+                if (c == 1) s.sidx[pi_ + __popc(mi & ((1u << lane) - 1u))] = k;
+                pi_ += __popc(mi);
             }
-            const bool bad = ni > S || ni + na < S || ni + na > SCAP;
-            if (lane == 0) {
-                s.n_in = ni;
-                s.n_amb = na;
-                if (bad) s.slow = 1;
-            }
-            if (!bad) {
-                int pi_ = 0, pa_ = ni;
-                for (int base = 0; base < nc; base += 32) {
-                    const int k = base + lane;
-                    const int c = k < nc ? s.cls[k] : 0;
-                    const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-                    const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
-                    const unsigned lt = (1u << lane) - 1u;
-                    if (c == 1) s.sidx[pi_ + __popc(mi & lt)] = s.list[k];
-                    if (c == 2) s.sidx[pa_ + __popc(ma & lt)] = s.list[k];
-                    pi_ += __popc(mi);
-                    pa_ += __popc(ma);
+            for (int k = lane; k < nc; k += 32) {
+                if (s.cls[k] == 2) {
+                    int r = 0;
+                    const double dk = s.dc2[k];
+                    for (int l = 0; l < nc; ++l)
+                        if (s.cls[l] == 2 && (s.dc2[l] < dk || (s.dc2[l] == dk && l < k))) ++r;
+                    s.sidx[ni + r] = k;
                 }
-            }
-        }
-        __syncthreads();
-    }
-
-    if (s.slow) {  // overflow / inconsistent classification: exact brute force over all candidates
-        if (valid) exact_dispatch<MAXS>(qx, qy, nullptr, N, S, C, L.alpha, L.beta, od, ou);
-        return;
-    }
-
-    // ---- 4. hemisphere arc + per-tile reference (FP64) -------------------
-    const int ne = s.n_in + s.n_amb;
-    {
-        const double phi0 = C.phi[s.sidx[0]];
-        double lo = 0.0, hi = 0.0, best = 1e300;
-        int bestk = 0x7fffffff;
-        for (int k = t; k < ne; k += ENT) {
-            const int a = s.sidx[k];
-            const double rel = remainder(C.phi[a] - phi0, 2.0 * M_PI);
-            lo = fmin(lo, rel);
-            hi = fmax(hi, rel);
-            const double dx = C.x[a] - cxm, dy = C.y[a] - cym;
-            const double d2 = dx * dx + dy * dy;
-            if (d2 < best || (d2 == best && k < bestk)) {
-                best = d2;
-                bestk = k;
+                if (s.cls[k] != 0 && (s.dc2[k] < best || (s.dc2[k] == best && k < bestk))) {
+                    best = s.dc2[k];
+                    bestk = k;
+                }
             }
         }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, d));
-            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, d));
             const double bd = __shfl_xor_sync(0xffffffffu, best, d);
             const int bk = __shfl_xor_sync(0xffffffffu, bestk, d);
             if (bd < best || (bd == best && bk < bestk)) {
@@ -526,44 +610,43 @@ k_emdq(EmdqLaunch L, Cand C, int S) {
             }
         }
         if (lane == 0) {
-            s.red_lo[wid] = lo;
-            s.red_hi[wid] = hi;
-            s.red_d[wid] = best;
-            s.red_k[wid] = bestk;
-        }
-        __syncthreads();
-        if (t == 0) {
-            for (int w = 1; w < NW; ++w) {
-                lo = fmin(lo, s.red_lo[w]);
-                hi = fmax(hi, s.red_hi[w]);
-                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_k[w] < bestk)) {
-                    best = s.red_d[w];
-                    bestk = s.red_k[w];
-                }
+            s.n_in = ni;
+            s.n_amb = na;
+            int slow = bad;
+            if (!bad) {
+                const W5 qr = load_w5(&C.l[5 * s.list[bestk]]);
+                double yx, yy;
+                xapply(qr, ox, oy, &yx, &yy);
+                s.s0 = qr.s;
+                s.Y0[0] = rint(yx);
+                s.Y0[1] = rint(yy);
+                s.P[0] = s.Y0[0] / qr.s;
+                s.P[1] = s.Y0[1] / qr.s;
+                s.e0[0] = fma(qr.s, s.P[0], -s.Y0[0]);
+                s.e0[1] = fma(qr.s, s.P[1], -s.Y0[1]);
+                if (!(qr.s > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) slow = 1;
             }
-            s.uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
-            const W5 qr = load_w5(&C.l[5 * s.sidx[bestk]]);
-            double yx, yy;
-            xapply(qr, ox, oy, &yx, &yy);
-            s.s0 = qr.s;
-            s.Y0[0] = rint(yx);
-            s.Y0[1] = rint(yy);
-            s.P[0] = s.Y0[0] / qr.s;
-            s.P[1] = s.Y0[1] / qr.s;
-            s.e0[0] = fma(qr.s, s.P[0], -s.Y0[0]);
-            s.e0[1] = fma(qr.s, s.P[1], -s.Y0[1]);
-            if (!(qr.s > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) s.uniform = 0;
+            s.slow = slow;
         }
-        __syncthreads();
     }
-    if (!s.uniform) {  // hemisphere flips possible: exact tier over the staged candidates
+    __syncthreads();
+    const int nin = s.n_in, namb = s.n_amb, ne = nin + namb;
+    if (s.slow) {  // overflow / inconsistent classification: exact brute force over the supertile list
+        if (valid) exact_dispatch<MAXS>(qx, qy, src, nsrc, S, C, L.alpha, L.beta, od, ou);
+        return;
+    }
+    // staged entries -> candidate indices (sidx held tile-list positions)
+    for (int k = t; k < ne; k += ENT) s.sidx[k] = s.list[s.sidx[k]];
+    __syncthreads();
+    if (sflag & SFLAG_NONUNIFORM) {  // hemisphere flips possible: exact tier
         if (valid) exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
 
-    // ---- 5. stage local coordinates + conjugated warps -------------------
+    // ---- 5. packed records: local coordinates + conjugated warps ----------
     {
         const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
+        float d2lo = FLT_MAX, d2hi = 0.f;
         for (int k = t; k < ne; k += ENT) {
             const int a = s.sidx[k];
             const W5 q = load_w5(&C.l[5 * a]);
@@ -571,70 +654,44 @@ k_emdq(EmdqLaunch L, Cand C, int S) {
             const double qa_dx = (q.w * hx - q.z * hy) + q.dx;  // q * T(o)
             const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
             const double px = 0.5 * P0, py = 0.5 * P1;         // T(-P) * (q * T(o))
-            s.q[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
-                                 (float)(qa_dy + (px * q.z - py * q.w)));
-            s.dl[k] = (float)(q.s - s0);
-            s.pr[k] = (float)C.p[a];
-            s.ux[k] = (float)(C.x[a] - ox);
-            s.uy[k] = (float)(C.y[a] - oy);
+            s.rec1[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
+                                    (float)(qa_dy + (px * q.z - py * q.w)));
+            const double ux = C.x[a] - ox, uy = C.y[a] - oy;
+            s.rec0[k] = make_float4((float)ux, (float)uy, (float)C.p[a], (float)(q.s - s0));
+            // d^2 range over the tile (for the weight reference)
+            const double dxn = fmax(fmax(-ux, 0.0), ux - (xhi - xlo)), dyn = fmax(fmax(-uy, 0.0), uy - (yhi - ylo));
+            const double dxf = fmax(ux, (xhi - xlo) - ux), dyf = fmax(uy, (yhi - ylo) - uy);
+            d2lo = fminf(d2lo, (float)(dxn * dxn + dyn * dyn));
+            d2hi = fmaxf(d2hi, (float)(dxf * dxf + dyf * dyf));
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            d2lo = fminf(d2lo, __shfl_xor_sync(0xffffffffu, d2lo, d));
+            d2hi = fmaxf(d2hi, __shfl_xor_sync(0xffffffffu, d2hi, d));
+        }
+        if (lane == 0) {
+            s.red_d[wid] = d2lo;
+            s.red_k[wid] = __float_as_int(d2hi);
         }
     }
     __syncthreads();
-
-    // ---- 6. per-warp re-classification of the CTA-ambiguous --------------
-    const int nin = s.n_in;
-    const float wx0 = (float)((wid & 1) * 8), wy0 = (float)((wid >> 1) * 4);
-    const float cx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), cy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
-    const bool wempty = wx0 > cx1 || wy0 > cy1;
-    for (int k = lane; k < ne; k += 32) {
-        const float ax = s.ux[k], ay = s.uy[k];
-        const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - cx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - cy1);
-        const float dxf = fmaxf(ax - wx0, cx1 - ax), dyf = fmaxf(ay - wy0, cy1 - ay);
-        s.wdmin[wid][k] = fmaf(dxn, dxn, dyn * dyn);
-        s.wdmax[wid][k] = fmaf(dxf, dxf, dyf * dyf);
+    float d2ref = FLT_MAX, d2top = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        d2ref = fminf(d2ref, (float)s.red_d[w]);
+        d2top = fmaxf(d2top, __int_as_float(s.red_k[w]));
     }
-    __syncwarp();
-    int wi = nin, wa = 0;
-    if (!wempty) {
-        for (int k = nin + lane; k < ne; k += 32) {
-            const float hi = s.wdmax[wid][k] * (1.f + 1e-5f) + 1e-2f;
-            const float lo = s.wdmin[wid][k] * (1.f - 1e-5f) - 1e-2f;
-            int cle = 0, clt = 0;
-            for (int l = 0; l < ne; ++l) {
-                if (l == k) continue;
-                cle += s.wdmin[wid][l] <= hi;
-                clt += s.wdmax[wid][l] < lo;
-            }
-            s.wcls[wid][k] = (unsigned char)(cle < S ? 1 : (clt >= S ? 0 : 2));
-        }
-        __syncwarp();
-        for (int base = nin; base < ne; base += 32) {
-            const int k = base + lane;
-            const int c = k < ne ? s.wcls[wid][k] : 0;
-            const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-            if (c == 1) s.wl[wid][wi + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
-            wi += __popc(mi);
-        }
-        for (int base = nin; base < ne; base += 32) {
-            const int k = base + lane;
-            const int c = k < ne ? s.wcls[wid][k] : 0;
-            const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
-            if (c == 2) s.wl[wid][wi + wa + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
-            wa += __popc(ma);
-        }
-    }
-    for (int k = lane; k < nin; k += 32) s.wl[wid][k] = (unsigned char)k;
-    __syncwarp();
-    const int m = S - wi;
-    const bool wslow = wempty || m < 0 || wi + wa < S || m > 16;
-
-    // ---- 7. per pixel --------------------------------------------------------
     if (!valid) return;
+    // exponent range guard: weights relative to the tile floor stay far from FP32 underflow
+    const bool range_ok = (float)L.alpha * (d2top - d2ref) < 60.f;
+
+    // ---- 6. per pixel ------------------------------------------------------
     FastOut fo;
-    bool ex = wslow;
-    if (!wslow) {
+    bool ex = !range_ok;
+    const int m = S - nin;
+    if (!ex) {
         const float nal = (float)(-L.alpha * kLog2e);
-        fast_dispatch((float)lx, (float)ly, s.wl[wid], wi, wa, m, s, nal, fo);
+        fast_dispatch((float)lx, (float)ly, nin, namb, m, s, nal, -nal * d2ref, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
@@ -665,10 +722,18 @@ k_emdq(EmdqLaunch L, Cand C, int S) {
 
 }  // namespace
 
+size_t emdq_scratch_bytes(int nactive, const FieldGrid& g) {
+    const size_t na = (size_t)nactive;
+    const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
+    const size_t nsuper = (size_t)nsx * nsy;
+    return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
+           256;
+}
+
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches) {
     if (L.nactive <= 0) return cudaErrorInvalidValue;
     const size_t na = (size_t)L.nactive;
-    // scratch layout (see emdq_core): x, y, l[5], p, phi (double) | c32 (float2) | j (int)
+    // scratch layout (emdq_scratch_bytes): x, y, l[5], p, phi (double) | c32 (float2) | j (int) | supertile lists
     Cand C;
     C.x = L.cx;
     C.y = L.cy;
@@ -680,21 +745,34 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     C.c32 = c32;
     int* cj = reinterpret_cast<int*>(c32 + na);
     C.j = cj;
+    SuperLists SL;
+    SL.nsx = (L.grid.i1 - L.grid.i0 + ST) / ST;
+    const int nsy = (L.grid.j1 - L.grid.j0 + ST) / ST;
+    const size_t nsuper = (size_t)SL.nsx * nsy;
+    SL.list = cj + na;
+    SL.count = SL.list + nsuper * SLIST_CAP;
+    SL.flag = SL.count + nsuper;
     k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
                                                        c32, L.cl, L.cp, phi, cj);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int S = L.support < L.nactive ? L.support : L.nactive;
-    const int nx = (L.grid.i1 - L.grid.i0 + 1 + ET - 1) / ET;
-    const int ny = (L.grid.j1 - L.grid.j0 + 1 + ET - 1) / ET;
+    const size_t ssm = sizeof(SSmem);
+    cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, S);
+    ++*launches;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int nx = (L.grid.i1 - L.grid.i0 + ET) / ET;
+    const int ny = (L.grid.j1 - L.grid.j0 + ET) / ET;
     const size_t smem = sizeof(ESmem);
     if (S <= 16) {
         cudaFuncSetAttribute(k_emdq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<16><<<dim3(nx, ny), ENT, smem, st>>>(L, C, S);
+        k_emdq<16><<<dim3(nx, ny), ENT, smem, st>>>(L, C, SL, S);
     } else {
         cudaFuncSetAttribute(k_emdq<MAX_SUPPORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<MAX_SUPPORT><<<dim3(nx, ny), ENT, smem, st>>>(L, C, S);
+        k_emdq<MAX_SUPPORT><<<dim3(nx, ny), ENT, smem, st>>>(L, C, SL, S);
     }
     ++*launches;
     return cudaGetLastError();

@@ -5,20 +5,24 @@
 //
 // K1/K2 design:
 //   CTA = one 64 x 32 pixel tile (256 threads, 8 rows per thread).
-//   Prologue (FP64): cull nodes against the tile rectangle into an ordered
-//   list, classifying each as "inner" (weight > 1e-6 at every tile pixel),
-//   "ring" (the 1e-6 cutoff crosses the tile) or out; pick a per-tile output
-//   origin; conjugate every listed warp into tile-local coordinates
-//   (T(-P) q T(o)); build separable Gaussian tables ex[k][col], ey[k][row]
-//   (exp(-a(dx^2+dy^2)) = exp(-a dx^2) exp(-a dy^2), MUFU.EX2).
+//   Prologue: (K1) cp.async the tile's canvas R/G/B/W rows into shared memory
+//   so the read-modify-write latency overlaps the compute; (FP64) cull nodes
+//   against the tile into an ordered list, classifying each as "inner"
+//   (weight > 1e-6 at every tile pixel), "ring" (the 1e-6 cutoff crosses the
+//   tile) or out; pick a per-tile output origin; conjugate every listed warp
+//   into tile-local coordinates (T(-P) q T(o)); build separable Gaussian
+//   tables ex[k][col], ey[k][row] (exp(-a(dx^2+dy^2)) = exp(-a dx^2)
+//   exp(-a dy^2), MUFU.EX2).
 //   Main loop (FP32): per (pixel, node) one FMUL for the weight and six FFMA
 //   accumulations; ring nodes add the cutoff test.
 //   Epilogue: normalise, apply, FP64 recombination with the tile origin,
-//   frame-bounds test, FP32 bilinear sample, capped running average.
+//   frame-bounds test, FP32 bilinear sample of the raw frame, capped running
+//   average from the staged canvas values.
 //   Pixels whose discrete decisions are within rounding of a threshold (ring
 //   weight ~1e-6, frame edge within 4e-3 px) or tiles whose warps are not in
 //   one hemisphere go to an exception queue that the exact FP64 pass
-//   (xpixel_warp, mirroring the reference's operation order) resolves.
+//   (xpixel_warp, the reference's operation order and libm) resolves. That
+//   pass also finalises BlendStats and resets the per-context counters.
 #include <cmath>
 
 #include "nrm_common.cuh"
@@ -28,6 +32,7 @@ namespace nrm {
 namespace {
 
 constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
+constexpr int EXC_THREADS = 1024;
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
 constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 constexpr double kBoundMargin = 4e-3;
@@ -45,8 +50,21 @@ struct Smem {
     int red_i[NT / 32];
     double red_lo[NT / 32], red_hi[NT / 32];
     int count, overflow, uniform;
-    double P[2], Y0[2], e0[2], s0;
+    double P[2], Y0[2], e0[2], s0, phi0;
 };
+
+// K1 only: the tile's canvas values, staged with cp.async at kernel entry.
+struct CanvasTile {
+    float r[TH][TW], g[TH][TW], b[TH][TW];
+    uint8_t w[TH][TW];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1, int band_count) {
     if (band_count <= 1) return tile_j0 + by;
@@ -71,6 +89,7 @@ __global__ void __launch_bounds__(NT, 2)
 k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s1) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+    CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
     const int lane = t & 31, wid = t >> 5;
 
@@ -81,6 +100,27 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
     const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
     const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
     if (ci0 > ci1 || cj0 > cj1) return;
+
+    // ---- 0. stage the canvas tile (whole 64 x 32 tile lies in the canvas:
+    //         tiles and canvas bounds are both 32/64-aligned, mosaic.hpp:141-151)
+    if (MODE == 0) {
+        const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (ti0 - L.phys_x0);
+        constexpr int kF = TW / 4;       // 16-byte chunks per float row
+        constexpr int kB = TW / 16;      // 16-byte chunks per byte row
+        constexpr int nF = 3 * TH * kF;  // 1536
+        for (int c = t; c < nF + TH * kB; c += NT) {
+            if (c < nF) {
+                const int plane = c / (TH * kF), rem = c % (TH * kF), r = rem / kF, k = rem % kF;
+                const float* src = (plane == 0 ? L.R : plane == 1 ? L.G : L.B) + base + (long long)r * L.pitch + 4 * k;
+                float* dst = (plane == 0 ? &ct.r[r][4 * k] : plane == 1 ? &ct.g[r][4 * k] : &ct.b[r][4 * k]);
+                cp_async16(dst, src);
+            } else {
+                const int rem = c - nF, r = rem / kB, k = rem % kB;
+                cp_async16(&ct.w[r][16 * k], L.W + base + (long long)r * L.pitch + 16 * k);
+            }
+        }
+        cp_async_commit();
+    }
 
     const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
     const double xlo = L.grid.gx + ci0, xhi = L.grid.gx + ci1;
@@ -122,12 +162,17 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
             int tot = 0;
             for (int w = 0; w < NT / 32; ++w) tot += s.warp_cnt[w];
             s.count += tot;
+            if (s.count > 0 && base == 0) {
+                const unsigned i0 = s.list[0] & ~kRingBit;
+                s.phi0 = atan2(__ldg(&L.warps[5 * i0 + 2]), __ldg(&L.warps[5 * i0 + 1]));
+            }
         }
         __syncthreads();
     }
     const int count = s.count;
     if (s.overflow) {
         tile_to_exceptions(L, ci0, ci1, cj0, cj1);
+        if (MODE == 0) cp_async_wait_all();
         return;
     }
 
@@ -144,21 +189,24 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
             }
             ++ns;
         }
-        if (MODE == 0) block_add3<NT>(L.stats, 0, ns, 0);
+        if (MODE == 0) {
+            cp_async_wait_all();
+            block_add3<NT>(L.acc, 0, ns, 0);
+        }
         return;
     }
 
-    // ---- C. hemisphere check + per-tile reference (FP64) ---------------
+    // ---- C. hemisphere arc + per-tile reference (FP64) -----------------
     {
-        const unsigned i0 = s.list[0] & ~kRingBit;
-        const double phi0 = atan2(__ldg(&L.warps[5 * i0 + 2]), __ldg(&L.warps[5 * i0 + 1]));
+        const double phi0 = s.phi0;
         double lo = 0.0, hi = 0.0, best = 1e300;
         int besti = 0x7fffffff;
         const double cxm = ox + 0.5 * TW, cym = oy + 0.5 * TH;
         for (int k = t; k < count; k += NT) {
             const unsigned i = s.list[k] & ~kRingBit;
-            const double phi = atan2(__ldg(&L.warps[5 * i + 2]), __ldg(&L.warps[5 * i + 1]));
-            double rel = remainder(phi - phi0, 2.0 * M_PI);
+            double rel = atan2(__ldg(&L.warps[5 * i + 2]), __ldg(&L.warps[5 * i + 1])) - phi0;
+            if (rel > M_PI) rel -= 2.0 * M_PI;
+            if (rel < -M_PI) rel += 2.0 * M_PI;
             lo = fmin(lo, rel);
             hi = fmax(hi, rel);
             const double ddx = __ldg(&L.anchors[2 * i]) - cxm, ddy = __ldg(&L.anchors[2 * i + 1]) - cym;
@@ -195,7 +243,7 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
                     besti = s.red_i[w];
                 }
             }
-            s.uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
+            int uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
             const W5 qr = load_w5(&L.warps[5 * besti]);
             double yx, yy;
             xapply(qr, ox, oy, &yx, &yy);
@@ -207,11 +255,14 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
             s.P[1] = s.Y0[1] / s0;
             s.e0[0] = fma(s0, s.P[0], -s.Y0[0]);
             s.e0[1] = fma(s0, s.P[1], -s.Y0[1]);
+            if (!(s0 > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) uniform = 0;
+            s.uniform = uniform;
         }
         __syncthreads();
     }
-    if (!s.uniform || !(s.s0 > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) {
+    if (!s.uniform) {
         tile_to_exceptions(L, ci0, ci1, cj0, cj1);
+        if (MODE == 0) cp_async_wait_all();
         return;
     }
     const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
@@ -296,13 +347,18 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
     }
 
     // ---- E. epilogue --------------------------------------------------------
+    if (MODE == 0) {
+        cp_async_wait_all();
+        __syncthreads();
+    }
     const double Y00 = s.Y0[0], Y01 = s.Y0[1], e00 = s.e0[0], e01 = s.e0[1];
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
     int nb = 0, nns = 0, noof = 0;
     const int i = ti0 + col;
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
-        const int jj = tj0 + rg * RPT + j;
+        const int r = rg * RPT + j;
+        const int jj = tj0 + r;
         const bool valid = i >= ci0 && i <= ci1 && jj >= cj0 && jj <= cj1;
         bool exc = false;
         if (valid) {
@@ -319,7 +375,7 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
                 const float rn = rsqrtf(fmaf(a0[j], a0[j], a1[j] * a1[j]));
                 const float qw = a0[j] * rn, qz = a1[j] * rn, qdx = a2[j] * rn, qdy = a3[j] * rn;
                 const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
-                const float ux = (float)col, uy = (float)(rg * RPT + j);
+                const float ux = (float)col, uy = (float)r;
                 const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
                 const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
                 const float dl = a4[j] / a5[j];
@@ -344,20 +400,21 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
                         y0 = min(y0, yc);
                         const float fx = (float)(yx - x0), fy = (float)(yy - y0);
                         const int x1 = min(x0 + 1, L.fw - 1), y1 = min(y0 + 1, L.fh - 1);
-                        const uchar4 va = __ldg(&L.frame[(size_t)y0 * L.fw + x0]);
-                        const uchar4 vb = __ldg(&L.frame[(size_t)y0 * L.fw + x1]);
-                        const uchar4 vc = __ldg(&L.frame[(size_t)y1 * L.fw + x0]);
-                        const uchar4 vd = __ldg(&L.frame[(size_t)y1 * L.fw + x1]);
+                        float va[3], vb[3], vc[3], vd[3];
+                        texel(L.frame, (size_t)y0 * L.fw + x0, L.fch, va);
+                        texel(L.frame, (size_t)y0 * L.fw + x1, L.fch, vb);
+                        texel(L.frame, (size_t)y1 * L.fw + x0, L.fch, vc);
+                        texel(L.frame, (size_t)y1 * L.fw + x1, L.fch, vd);
                         const float gx = 1.f - fx, gy = 1.f - fy;
-                        const float r = (gx * va.x + fx * vb.x) * gy + (gx * vc.x + fx * vd.x) * fy;
-                        const float g = (gx * va.y + fx * vb.y) * gy + (gx * vc.y + fx * vd.y) * fy;
-                        const float b = (gx * va.z + fx * vb.z) * gy + (gx * vc.z + fx * vd.z) * fy;
-                        const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
-                        const uint8_t wg = L.W[idx];
+                        const float vr = (gx * va[0] + fx * vb[0]) * gy + (gx * vc[0] + fx * vd[0]) * fy;
+                        const float vg = (gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy;
+                        const float vbl = (gx * va[2] + fx * vb[2]) * gy + (gx * vc[2] + fx * vd[2]) * fy;
+                        const uint8_t wg = ct.w[r][col];
                         const float wd = (float)wg, inv = 1.f / (wd + 1.f);
-                        L.R[idx] = (wd * L.R[idx] + r / 255.f) * inv;
-                        L.G[idx] = (wd * L.G[idx] + g / 255.f) * inv;
-                        L.B[idx] = (wd * L.B[idx] + b / 255.f) * inv;
+                        const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
+                        L.R[idx] = (wd * ct.r[r][col] + vr / 255.f) * inv;
+                        L.G[idx] = (wd * ct.g[r][col] + vg / 255.f) * inv;
+                        L.B[idx] = (wd * ct.b[r][col] + vbl / 255.f) * inv;
                         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
                         ++nb;
                     }
@@ -366,17 +423,19 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
         }
         queue_push(exc, i, jj, L.exc, L.exc_count, L.exc_cap, L.exc_overflow);
     }
-    if (MODE == 0) block_add3<NT>(L.stats, nb, nns, noof);
+    if (MODE == 0) block_add3<NT>(L.acc, nb, nns, noof);
 }
 
-// Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics).
+// Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics), one
+// CTA. It then writes BlendStats (footprint + partial sums) and restores the
+// per-context state (acc = 0, exc_count = 0) for the next call.
 template <int MODE>
-__global__ void __launch_bounds__(128) k_node_exceptions(NodeFieldLaunch L) {
+__global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
+    __shared__ int red[3][EXC_THREADS / 32];
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
-    if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0 && L.stats_footprint) *L.stats_footprint = L.footprint;
     int nb = 0, nns = 0, noof = 0;
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
-    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cnt; q += gridDim.x * blockDim.x) {
+    for (unsigned q = threadIdx.x; q < cnt; q += EXC_THREADS) {
         const int2 p = L.exc[q];
         const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
         W5 wp;
@@ -405,7 +464,7 @@ __global__ void __launch_bounds__(128) k_node_exceptions(NodeFieldLaunch L) {
             continue;
         }
         double rgb[3];
-        xsample_bilinear(L.frame, L.fw, L.fh, yx, yy, rgb);
+        xsample_bilinear(L.frame, L.fw, L.fh, L.fch, yx, yy, rgb);
         const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
         const uint8_t wg = L.W[idx];
         const double wd = wg;
@@ -415,7 +474,33 @@ __global__ void __launch_bounds__(128) k_node_exceptions(NodeFieldLaunch L) {
         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
         ++nb;
     }
-    if (MODE == 0) block_add3<128>(L.stats, nb, nns, noof);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nb += __shfl_xor_sync(0xffffffffu, nb, o);
+        nns += __shfl_xor_sync(0xffffffffu, nns, o);
+        noof += __shfl_xor_sync(0xffffffffu, noof, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = nb;
+        red[1][threadIdx.x >> 5] = nns;
+        red[2][threadIdx.x >> 5] = noof;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (MODE == 0) {
+            unsigned long long tot[3] = {0, 0, 0};
+            for (int k = 0; k < 3; ++k)
+                for (int w = 0; w < EXC_THREADS / 32; ++w) tot[k] += (unsigned long long)red[k][w];
+            if (L.stats_out) {
+                L.stats_out[0] = L.footprint;
+                L.stats_out[1] = L.acc[0] + tot[0];
+                L.stats_out[2] = L.acc[1] + tot[1];
+                L.stats_out[3] = L.acc[2] + tot[2];
+            }
+            L.acc[0] = L.acc[1] = L.acc[2] = 0;
+        }
+        *L.exc_count = 0;
+    }
 }
 
 __global__ void k_pixel_warp_points(const double* __restrict__ pts, int npts,
@@ -512,7 +597,8 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
         }
         nty = cnt;
     }
-    const size_t smem = sizeof(Smem);
+    const size_t base = (sizeof(Smem) + 15) & ~size_t(15);
+    const size_t smem = mode == 0 ? base + sizeof(CanvasTile) : sizeof(Smem);
     if (ntx > 0 && nty > 0) {
         if (mode == 0) {
             cudaFuncSetAttribute(k_node_field<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -526,9 +612,9 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
         if (e != cudaSuccess) return e;
     }
     if (mode == 0)
-        k_node_exceptions<0><<<296, 128, 0, st>>>(L);
+        k_node_exceptions<0><<<1, EXC_THREADS, 0, st>>>(L);
     else
-        k_node_exceptions<1><<<296, 128, 0, st>>>(L);
+        k_node_exceptions<1><<<1, EXC_THREADS, 0, st>>>(L);
     ++*launches;
     return cudaGetLastError();
 }

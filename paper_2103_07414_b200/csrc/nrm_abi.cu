@@ -230,14 +230,29 @@ Bbox footprint_bbox(const double* poly, int npoly) {
     return {r.x0 - 4.0, r.y0 - 4.0, r.x1 + 4.0, r.y1 + 4.0};
 }
 
+// Per-context device state (c->misc, zeroed at context creation and restored
+// by every exception pass): acc[3] (u64) | exc_count (u32) | overflow (u32).
+struct State {
+    unsigned long long* acc;
+    unsigned* exc_count;
+    unsigned* overflow;
+};
+State state_of(nrm_ctx* c) {
+    char* b = c->misc.as<char>();
+    return {reinterpret_cast<unsigned long long*>(b), reinterpret_cast<unsigned*>(b + 24),
+            reinterpret_cast<unsigned*>(b + 28)};
+}
+
 // Shared core of blend_frame: everything after the inputs are in HBM.
-// d_stats: int64[4] on the device (zeroed here, filled by the kernels).
-int blend_core(nrm_canvas* cv, const uchar4* d_rgba, int fw, int fh, const double* d_anchors,
+// d_stats: int64[4] on the device, written by the exception pass.
+int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
                const double* d_warps, int n, double alpha, const double* poly, int npoly,
                unsigned long long* d_stats) {
     nrm_ctx* c = cv->ctx;
-    NRM_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
-    if (fw <= 0 || fh <= 0 || npoly < 3) return NRM_OK;  // mosaic.hpp:201
+    if (fw <= 0 || fh <= 0 || npoly < 3) {  // mosaic.hpp:201: empty stats, canvas untouched
+        NRM_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
+        return NRM_OK;
+    }
     if (!finite_all(poly, (size_t)npoly * 2)) return fail(NRM_EINVAL, "blend_frame: non-finite polygon");
     const Bbox bb = footprint_bbox(poly, npoly);
     NRM_CHECK(ensure_contains(cv, bb.x0, bb.y0, bb.x1, bb.y1));
@@ -245,19 +260,20 @@ int blend_core(nrm_canvas* cv, const uchar4* d_rgba, int fw, int fh, const doubl
     const int px0 = (int)std::floor(bb.x0 - orgx), py0 = (int)std::floor(bb.y0 - orgy);
     const int px1 = (int)std::ceil(bb.x1 - orgx), py1 = (int)std::ceil(bb.y1 - orgy);
     const int bw = px1 - px0 + 1, bh = py1 - py0 + 1;
-    if (bw <= 0 || bh <= 0) return NRM_OK;  // mosaic.hpp:212
+    if (bw <= 0 || bh <= 0) {  // mosaic.hpp:212
+        NRM_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
+        return NRM_OK;
+    }
     const unsigned long long footprint = (unsigned long long)bw * (unsigned long long)bh;
-
     const size_t exc_cap = std::min<size_t>(footprint, (size_t)1 << 26);
     NRM_CUDA(c->exc.ensure(exc_cap * sizeof(int2) + 64));
-    NRM_CUDA(c->misc.ensure(256));
-    unsigned* exc_count = c->misc.as<unsigned>();
-    NRM_CUDA(cudaMemsetAsync(exc_count, 0, 2 * sizeof(unsigned), c->stream));
+    const State st = state_of(c);
 
     NodeFieldLaunch L;
-    L.frame = d_rgba;
+    L.frame = d_frame;
     L.fw = fw;
     L.fh = fh;
+    L.fch = ch;
     L.anchors = d_anchors;
     L.warps = d_warps;
     L.n = n;
@@ -278,21 +294,24 @@ int blend_core(nrm_canvas* cv, const uchar4* d_rgba, int fw, int fh, const doubl
     L.phys_y0 = (int)cv->phys_y0;
     L.band_rank = cv->band_rank;
     L.band_count = cv->band_count;
-    L.stats = d_stats + 1;
-    L.stats_footprint = d_stats;
+    L.acc = st.acc;
+    L.stats_out = d_stats;
     L.footprint = footprint;
     L.exc = c->exc.as<int2>();
-    L.exc_count = exc_count;
+    L.exc_count = st.exc_count;
     L.exc_cap = (unsigned)exc_cap;
-    L.exc_overflow = exc_count + 1;
+    L.exc_overflow = st.overflow;
     NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
     return NRM_OK;
 }
 
 int check_overflow(nrm_ctx* c) {
-    unsigned flags[2] = {0, 0};
-    NRM_CUDA(cudaMemcpy(flags, c->misc.p, sizeof(flags), cudaMemcpyDeviceToHost));
-    if (flags[1]) return fail(NRM_ECUDA, "exception queue overflow");
+    unsigned flag = 0;
+    NRM_CUDA(cudaMemcpy(&flag, state_of(c).overflow, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (flag) {
+        cudaMemset(state_of(c).overflow, 0, sizeof(unsigned));
+        return fail(NRM_ECUDA, "exception queue overflow");
+    }
     return NRM_OK;
 }
 
@@ -335,9 +354,7 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     const size_t npx = (size_t)grid->width * (size_t)grid->height;
     if (npx == 0) return NRM_OK;
     NRM_CUDA(c->exc.ensure(npx * sizeof(int2) + 64));
-    NRM_CUDA(c->misc.ensure(256));
-    unsigned* exc_count = c->misc.as<unsigned>();
-    NRM_CUDA(cudaMemsetAsync(exc_count, 0, 2 * sizeof(unsigned), c->stream));
+    const State st = state_of(c);
     NodeFieldLaunch L;
     L.anchors = d_anchors;
     L.warps = d_warps;
@@ -347,9 +364,9 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.disp = reinterpret_cast<float2*>(d_disp);
     L.support = d_support;
     L.exc = c->exc.as<int2>();
-    L.exc_count = exc_count;
+    L.exc_count = st.exc_count;
     L.exc_cap = (unsigned)std::min<size_t>(npx, 0xffffffffu);
-    L.exc_overflow = exc_count + 1;
+    L.exc_overflow = st.overflow;
     NRM_CUDA(launch_node_field(L, 1, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -365,7 +382,7 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
     if ((size_t)grid->width * (size_t)grid->height == 0) return NRM_OK;
     const size_t na = (size_t)nactive;
-    NRM_CUDA(c->pts.ensure(na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + 64));
+    NRM_CUDA(c->pts.ensure(emdq_scratch_bytes(nactive, fg)));
     double* base = c->pts.as<double>();
     EmdqLaunch L;
     L.grid = fg;
@@ -415,6 +432,14 @@ int nrm_ctx_create(int device, nrm_ctx** out) {
     }
     c->stream = c->own_stream;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    // per-context device state (see State): zero once, restored by every exception pass
+    e = c->misc.ensure(256);
+    if (e == cudaSuccess) e = cudaMemset(c->misc.p, 0, 256);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(c->own_stream);
+        delete c;
+        return cuda_fail(e, "context state allocation");
+    }
     *out = c;
     return NRM_OK;
 }
@@ -423,7 +448,7 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     if (!c) return NRM_OK;
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf* bufs[] = {&c->frame_raw, &c->frame_rgba, &c->anchors, &c->warps, &c->exc, &c->misc, &c->stats,
+    DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc, &c->misc, &c->stats,
                       &c->pts,       &c->locals,     &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
@@ -612,13 +637,10 @@ int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch
     DeviceGuard g(c->device);
     const size_t fbytes = (size_t)fw * fh * ch;
     NRM_CHECK(upload(c, c->frame_raw, frame, fbytes));
-    NRM_CUDA(c->frame_rgba.ensure((size_t)fw * fh * 4));
-    NRM_CUDA(launch_frame_to_rgba(c->frame_raw.as<uint8_t>(), fw, fh, ch, c->frame_rgba.as<uchar4>(), c->stream,
-                                  &c->launches));
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
     NRM_CUDA(c->stats.ensure(64));
-    NRM_CHECK(blend_core(cv, c->frame_rgba.as<uchar4>(), fw, fh, c->anchors.as<double>(), c->warps.as<double>(), n,
+    NRM_CHECK(blend_core(cv, c->frame_raw.as<uint8_t>(), fw, fh, ch, c->anchors.as<double>(), c->warps.as<double>(), n,
                          alpha, poly, npoly, c->stats.as<unsigned long long>()));
     NRM_CUDA(c->staging_out.ensure(64));
     NRM_CUDA(cudaMemcpyAsync(c->staging_out.p, c->stats.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -637,17 +659,11 @@ int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int f
     NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
     nrm_ctx* c = cv->ctx;
     DeviceGuard g(c->device);
-    const uchar4* rgba = reinterpret_cast<const uchar4*>(d_frame);
     if (fw > 0 && fh > 0 && npoly >= 3) {
         if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "frame channels must be 1, 3 or 4");
         if (!d_frame || !poly) return fail(NRM_EINVAL, "null frame or polygon");
-        if (ch != 4) {
-            NRM_CUDA(c->frame_rgba.ensure((size_t)fw * fh * 4));
-            NRM_CUDA(launch_frame_to_rgba(d_frame, fw, fh, ch, c->frame_rgba.as<uchar4>(), c->stream, &c->launches));
-            rgba = c->frame_rgba.as<uchar4>();
-        }
     }
-    return blend_core(cv, rgba, fw, fh, d_anchors, d_warps, n, alpha, poly, npoly,
+    return blend_core(cv, d_frame, fw, fh, ch, d_anchors, d_warps, n, alpha, poly, npoly,
                       reinterpret_cast<unsigned long long*>(d_stats));
 }
 

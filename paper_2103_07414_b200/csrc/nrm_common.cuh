@@ -103,9 +103,26 @@ __device__ inline int xpixel_warp(double x, double y, const double* __restrict__
     return 0;
 }
 
-// sample_bilinear_rgb (image.hpp:78-92) in the exact tier, on an RGBA8
-// device copy of the frame (grey already replicated to RGB).
-__device__ __forceinline__ void xsample_bilinear(const uchar4* __restrict__ im, int iw, int ih,
+// One texel of an ImageU8 (image.hpp:21-43) as RGB; grey is replicated
+// (sample_bilinear_rgb reads channel 0 for every output channel).
+__device__ __forceinline__ void texel(const uint8_t* __restrict__ f, size_t idx, int ch, float* v) {
+    if (ch == 3) {
+        const uint8_t* p = f + 3 * idx;
+        v[0] = __ldg(p);
+        v[1] = __ldg(p + 1);
+        v[2] = __ldg(p + 2);
+    } else if (ch == 4) {
+        const uchar4 q = __ldg(reinterpret_cast<const uchar4*>(f) + idx);
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+    } else {
+        v[0] = v[1] = v[2] = __ldg(f + idx);
+    }
+}
+
+// sample_bilinear_rgb (image.hpp:78-92) in the exact tier.
+__device__ __forceinline__ void xsample_bilinear(const uint8_t* __restrict__ im, int iw, int ih, int ch,
                                                  double x, double y, double* out3) {
     int x0 = (int)x, y0 = (int)y;
     const int xc = iw - 2 >= 0 ? iw - 2 : 0, yc = ih - 2 >= 0 ? ih - 2 : 0;
@@ -114,17 +131,16 @@ __device__ __forceinline__ void xsample_bilinear(const uchar4* __restrict__ im, 
     const double fx = xsub(x, (double)x0), fy = xsub(y, (double)y0);
     const int x1 = x0 + 1 < iw - 1 ? x0 + 1 : iw - 1;
     const int y1 = y0 + 1 < ih - 1 ? y0 + 1 : ih - 1;
-    const uchar4 a = __ldg(&im[(size_t)y0 * iw + x0]), b = __ldg(&im[(size_t)y0 * iw + x1]);
-    const uchar4 c = __ldg(&im[(size_t)y1 * iw + x0]), d = __ldg(&im[(size_t)y1 * iw + x1]);
+    float a[3], b[3], c[3], d[3];
+    texel(im, (size_t)y0 * iw + x0, ch, a);
+    texel(im, (size_t)y0 * iw + x1, ch, b);
+    texel(im, (size_t)y1 * iw + x0, ch, c);
+    texel(im, (size_t)y1 * iw + x1, ch, d);
     const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
-    const double va[3] = {(double)a.x, (double)a.y, (double)a.z};
-    const double vb[3] = {(double)b.x, (double)b.y, (double)b.z};
-    const double vc[3] = {(double)c.x, (double)c.y, (double)c.z};
-    const double vd[3] = {(double)d.x, (double)d.y, (double)d.z};
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-        out3[k] = xadd(xmul(xadd(xmul(gx, va[k]), xmul(fx, vb[k])), gy),
-                       xmul(xadd(xmul(gx, vc[k]), xmul(fx, vd[k])), fy));
+        out3[k] = xadd(xmul(xadd(xmul(gx, (double)a[k]), xmul(fx, (double)b[k])), gy),
+                       xmul(xadd(xmul(gx, (double)c[k]), xmul(fx, (double)d[k])), fy));
 }
 
 // ---- fast tier ----------------------------------------------------------

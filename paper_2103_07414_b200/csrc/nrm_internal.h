@@ -38,7 +38,7 @@ struct nrm_ctx {
     int64_t launches = 0;
     int num_sms = 148;
     // scratch (grow-only)
-    nrm::DevBuf frame_raw, frame_rgba, anchors, warps, exc, misc, stats, pts, locals, probs,
+    nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
         active, out_a, out_b, tiles;
     nrm::PinnedBuf staging, staging_out;
 };
@@ -75,8 +75,8 @@ struct FieldGrid {
 
 struct NodeFieldLaunch {
     // inputs
-    const uchar4* frame = nullptr;
-    int fw = 0, fh = 0;
+    const uint8_t* frame = nullptr;  // ImageU8 layout: h x w x fch, fch in {1, 3, 4}
+    int fw = 0, fh = 0, fch = 3;
     const double* anchors = nullptr;
     const double* warps = nullptr;
     int n = 0;
@@ -93,16 +93,17 @@ struct NodeFieldLaunch {
     // FIELD mode outputs (row-major over the valid range)
     float2* disp = nullptr;
     uint8_t* support = nullptr;
-    // stats[0..2] = blended, no_support, out_of_frame (device, accumulated)
-    unsigned long long* stats = nullptr;
-    // stats_footprint[0] = footprint, written by the exception pass (BLEND mode)
-    unsigned long long* stats_footprint = nullptr;
+    // Persistent per-context state, zero between calls (the exception pass
+    // restores it): acc[0..2] = blended, no_support, out_of_frame partial sums.
+    unsigned long long* acc = nullptr;
+    // BLEND mode: final BlendStats (int64[4]) written by the exception pass
+    unsigned long long* stats_out = nullptr;
     unsigned long long footprint = 0;
-    // exception queue
+    // exception queue (count persistent-zero, reset by the exception pass)
     int2* exc = nullptr;
     unsigned* exc_count = nullptr;
     unsigned exc_cap = 0;
-    unsigned* exc_overflow = nullptr;
+    unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
 };
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
@@ -139,10 +140,9 @@ struct EmdqLaunch {
     double* cp = nullptr;   // max(prob, 1e-6)
 };
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches);
+size_t emdq_scratch_bytes(int nactive, const FieldGrid& g);
 
 // ---- k_canvas.cu ----------------------------------------------------------
-cudaError_t launch_frame_to_rgba(const uint8_t* raw, int w, int h, int ch, uchar4* out,
-                                 cudaStream_t st, int64_t* launches);
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches);
 cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int* bbox4,
