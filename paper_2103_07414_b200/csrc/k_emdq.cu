@@ -20,6 +20,8 @@
 //     closer), "out" (at least S are always closer) or ambiguous. In and
 //     ambiguous ones are staged as packed records in tile-local coordinates
 //     with their warps conjugated to the tile origin (T(-P) q T(o)).
+//   Each warp re-classifies the ambiguous ones against its own 8 x 4 sub-tile
+//   (FP32 with conservative margins), leaving ~2 free slots per pixel.
 //   Per pixel (FP32): one pass over the sure members accumulating weighted
 //     warps (weights on MUFU.EX2 relative to a tile-wide d^2 floor: a common
 //     factor cancels in dq_blend's normalisation), an early-reject sorted
@@ -79,6 +81,9 @@ struct ESmem {
     int sidx[SCAP];
     float4 rec0[SCAP];  // ux, uy (tile-local), prob, s - s0
     float4 rec1[SCAP];  // conjugated dual quaternion (w, z, dx, dy)
+    float2 wd[NW][SCAP];          // per-warp (min, max) squared distance to the sub-tile
+    unsigned char wl[NW][SCAP];   // per-warp lists: extra sure members, then ambiguous
+    unsigned char wc[NW][SCAP];   // per-warp class of the CTA-ambiguous
     double red_d[NW];
     int red_k[NW];
     int nc, n_in, n_amb, slow;
@@ -362,6 +367,8 @@ __device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx
 
 // ---------------------------------------------------------------------------
 // Fast tier for one pixel (ux, uy = tile-local pixel position).
+//   sure members: staged [0, nin) plus the warp's extra sure ones wl[0, nxin)
+//   ambiguous:    wl[nxin, nxin + namb), closest-to-centre first
 // ---------------------------------------------------------------------------
 struct FastOut {
     float s0, s1, s2, s3, s4, s5;  // sums: w*qw, w*qz, w*qdx, w*qdy, w*(s-s0), w
@@ -374,8 +381,9 @@ struct FastOut {
 __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
 template <int MS>
-__device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, int namb, int m, const ESmem& s, float nal,
-                                           float c0, FastOut& o) {
+__device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, const unsigned char* __restrict__ wl,
+                                           int nxin, int namb, int m, const ESmem& s, float nal, float c0,
+                                           FastOut& o) {
     float b0 = FLT_MAX, b1 = FLT_MAX;
     int k0 = -1, k1 = -1;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
@@ -405,6 +413,12 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, int namb
         const float dx = r0.x - ux, dy = r0.y - uy;
         take(k, fmaf(dx, dx, dy * dy), r0);
     }
+    for (int e = 0; e < nxin; ++e) {
+        const int k = wl[e];
+        const float4 r0 = s.rec0[k];
+        const float dx = r0.x - ux, dy = r0.y - uy;
+        take(k, fmaf(dx, dx, dy * dy), r0);
+    }
     bool exact = false;
     if (MS > 0) {
         float sd[MS > 0 ? MS : 1];
@@ -416,7 +430,7 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, int namb
         }
         float rej = FLT_MAX, worst = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
-            const int k = nin + e;
+            const int k = wl[nxin + e];
             const float2 u = *reinterpret_cast<const float2*>(&s.rec0[k]);
             const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
@@ -453,18 +467,18 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, int namb
     o = FastOut{a0, a1, a2, a3, a4, a5, k0, k1, b0, b1, exact};
 }
 
-__device__ __forceinline__ void fast_dispatch(float ux, float uy, int nin, int namb, int m, const ESmem& s,
-                                              float nal, float c0, FastOut& o) {
+__device__ __forceinline__ void fast_dispatch(float ux, float uy, int nin, const unsigned char* wl, int nxin,
+                                              int namb, int m, const ESmem& s, float nal, float c0, FastOut& o) {
     if (m <= 0)
-        fast_pixel<0>(ux, uy, nin, namb, m, s, nal, c0, o);
+        fast_pixel<0>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else if (m <= 2)
-        fast_pixel<2>(ux, uy, nin, namb, m, s, nal, c0, o);
+        fast_pixel<2>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else if (m <= 4)
-        fast_pixel<4>(ux, uy, nin, namb, m, s, nal, c0, o);
+        fast_pixel<4>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else if (m <= 8)
-        fast_pixel<8>(ux, uy, nin, namb, m, s, nal, c0, o);
+        fast_pixel<8>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else
-        fast_pixel<16>(ux, uy, nin, namb, m, s, nal, c0, o);
+        fast_pixel<16>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
 }
 
 template <int MAXS>
@@ -487,8 +501,8 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
     const int nsrc = SL.count[sid];
     const int* src = (sflag & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
 
-    // this thread's pixel (row-major 16 x 16)
-    const int lx = t & (ET - 1), ly = t >> 4;
+    // this thread's pixel: warp w owns the 8 x 4 sub-tile ((w & 1) * 8, (w >> 1) * 4)
+    const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
     const int pi = ti0 + lx, pj = tj0 + ly;
     const bool valid = pi <= ti1 && pj <= tj1;
     const size_t o = (size_t)(pj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (pi - L.grid.i0);
@@ -564,40 +578,29 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
     }
     __syncthreads();
 
-    // ---- 4. staging (warp 0): in-list in index order, ambiguous by centre
-    //         distance; tile reference = staged point nearest the centre ----
-    if (wid == 0) {
-        int ni = 0, na = 0;
-        for (int base = 0; base < nc; base += 32) {
-            const int k = base + lane;
-            const int c = k < nc ? s.cls[k] : 0;
-            ni += __popc(__ballot_sync(0xffffffffu, c == 1));
-            na += __popc(__ballot_sync(0xffffffffu, c == 2));
-        }
-        const bool bad = s.slow || ni > S || ni + na < S || ni + na > SCAP;
+    // ---- 4. staging (all threads): in-list in index order, ambiguous by
+    //         centre distance; tile reference = staged point nearest the centre
+    {
         double best = 1e300;
-        int bestk = 0x7fffffff;
-        if (!bad) {
-            int pi_ = 0;
-            for (int base = 0; base < nc; base += 32) {
-                const int k = base + lane;
-                const int c = k < nc ? s.cls[k] : 0;
-                const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-                if (c == 1) s.sidx[pi_ + __popc(mi & ((1u << lane) - 1u))] = k;
-                pi_ += __popc(mi);
+        int bestk = 0x7fffffff, nin_t = 0, namb_t = 0;
+        for (int k = t; k < nc; k += ENT) {
+            const int c = s.cls[k];
+            const double dk = s.dc2[k];
+            int before_in = 0, rank = 0, ni = 0, na = 0;
+            for (int l = 0; l < nc; ++l) {
+                const int cl = s.cls[l];
+                ni += cl == 1;
+                na += cl == 2;
+                before_in += (cl == 1) & (l < k);
+                rank += (cl == 2) & ((s.dc2[l] < dk) | ((s.dc2[l] == dk) & (l < k)));
             }
-            for (int k = lane; k < nc; k += 32) {
-                if (s.cls[k] == 2) {
-                    int r = 0;
-                    const double dk = s.dc2[k];
-                    for (int l = 0; l < nc; ++l)
-                        if (s.cls[l] == 2 && (s.dc2[l] < dk || (s.dc2[l] == dk && l < k))) ++r;
-                    s.sidx[ni + r] = k;
-                }
-                if (s.cls[k] != 0 && (s.dc2[k] < best || (s.dc2[k] == best && k < bestk))) {
-                    best = s.dc2[k];
-                    bestk = k;
-                }
+            nin_t = ni;
+            namb_t = na;
+            if (c == 1 && before_in < SCAP) s.sidx[before_in] = k;
+            if (c == 2 && ni + rank < SCAP) s.sidx[ni + rank] = k;
+            if (c != 0 && (dk < best || (dk == best && k < bestk))) {
+                best = dk;
+                bestk = k;
             }
         }
 #pragma unroll
@@ -610,10 +613,23 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
             }
         }
         if (lane == 0) {
-            s.n_in = ni;
-            s.n_amb = na;
-            int slow = bad;
-            if (!bad) {
+            s.red_d[wid] = best;
+            s.red_k[wid] = bestk;
+        }
+        if (t == 0) {
+            s.n_in = nin_t;
+            s.n_amb = namb_t;
+        }
+        __syncthreads();
+        if (t == 0) {
+            for (int w = 1; w < NW; ++w)
+                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_k[w] < bestk)) {
+                    best = s.red_d[w];
+                    bestk = s.red_k[w];
+                }
+            const int ni = s.n_in, na = s.n_amb;
+            int slow = s.slow || ni > S || ni + na < S || ni + na > SCAP || bestk >= nc;
+            if (!slow) {
                 const W5 qr = load_w5(&C.l[5 * s.list[bestk]]);
                 double yx, yy;
                 xapply(qr, ox, oy, &yx, &yy);
@@ -628,8 +644,8 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
             }
             s.slow = slow;
         }
+        __syncthreads();
     }
-    __syncthreads();
     const int nin = s.n_in, namb = s.n_amb, ne = nin + namb;
     if (s.slow) {  // overflow / inconsistent classification: exact brute force over the supertile list
         if (valid) exact_dispatch<MAXS>(qx, qy, src, nsrc, S, C, L.alpha, L.beta, od, ou);
@@ -681,17 +697,62 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
         d2ref = fminf(d2ref, (float)s.red_d[w]);
         d2top = fmaxf(d2top, __int_as_float(s.red_k[w]));
     }
-    if (!valid) return;
-    // exponent range guard: weights relative to the tile floor stay far from FP32 underflow
-    const bool range_ok = (float)L.alpha * (d2top - d2ref) < 60.f;
 
-    // ---- 6. per pixel ------------------------------------------------------
+    // ---- 6. per-warp refinement of the CTA-ambiguous (FP32, margins) ------
+    const float wx0 = (float)((wid & 1) * 8), wy0 = (float)((wid >> 1) * 4);
+    const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
+    const bool wempty = wx0 > wx1 || wy0 > wy1;
+    int nxin = 0, nwamb = 0;
+    if (!wempty) {
+        for (int k = lane; k < ne; k += 32) {
+            const float4 r0 = s.rec0[k];
+            const float dxn = fmaxf(fmaxf(wx0 - r0.x, 0.f), r0.x - wx1), dyn = fmaxf(fmaxf(wy0 - r0.y, 0.f), r0.y - wy1);
+            const float dxf = fmaxf(r0.x - wx0, wx1 - r0.x), dyf = fmaxf(r0.y - wy0, wy1 - r0.y);
+            s.wd[wid][k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
+        }
+        __syncwarp();
+        for (int base = nin; base < ne; base += 32) {
+            const int k = base + lane;
+            int c = 0;
+            if (k < ne) {
+                const float2 dk = s.wd[wid][k];
+                const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
+                int cle = 0, clt = 0;
+                for (int l = 0; l < ne; ++l) {
+                    const float2 dl = s.wd[wid][l];
+                    cle += dl.x <= hi;
+                    clt += dl.y < lo;
+                }
+                --cle;  // l == k is always counted (dk.x <= dk.y <= hi)
+                c = cle < S ? 1 : (clt >= S ? 0 : 2);
+            }
+            const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+            if (c == 1) s.wl[wid][nxin + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
+            nxin += __popc(mi);
+            if (k < ne) s.wc[wid][k] = (unsigned char)c;
+        }
+        __syncwarp();
+        for (int base = nin; base < ne; base += 32) {
+            const int k = base + lane;
+            const int c = k < ne ? s.wc[wid][k] : 0;
+            const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+            if (c == 2) s.wl[wid][nxin + nwamb + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
+            nwamb += __popc(ma);
+        }
+        __syncwarp();
+    }
+    if (!valid) return;
+    const int wi = nin + nxin, m = S - wi;
+    // exponent range guard: weights relative to the tile floor stay far from FP32 underflow
+    const bool fast_ok = !wempty && m >= 0 && m <= 16 && wi + nwamb >= S &&
+                         (float)L.alpha * (d2top - d2ref) < 60.f;
+
+    // ---- 7. per pixel ------------------------------------------------------
     FastOut fo;
-    bool ex = !range_ok;
-    const int m = S - nin;
+    bool ex = !fast_ok;
     if (!ex) {
         const float nal = (float)(-L.alpha * kLog2e);
-        fast_dispatch((float)lx, (float)ly, nin, namb, m, s, nal, -nal * d2ref, fo);
+        fast_dispatch((float)lx, (float)ly, nin, s.wl[wid], nxin, nwamb, m, s, nal, -nal * d2ref, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
