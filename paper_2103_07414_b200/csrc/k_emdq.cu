@@ -14,22 +14,23 @@
 //     distances bounds the S-th neighbour distance R; every point that can be
 //     among the S nearest of a supertile pixel lies within R + 2 hd of its
 //     centre. Those points form the supertile list (plus a rotation-arc flag).
-//   k_emdq (16 x 16 tiles, one pixel per thread): the same bound over the
-//     supertile list, then an FP64 classification of the tile's candidates
-//     against the tile rectangle: "in" (fewer than S others can ever be
-//     closer), "out" (at least S are always closer) or ambiguous. In and
-//     ambiguous ones are staged as packed records in tile-local coordinates
-//     with their warps conjugated to the tile origin (T(-P) q T(o)).
-//   Each warp re-classifies the ambiguous ones against its own 8 x 4 sub-tile
-//   (FP32 with conservative margins), leaving ~2 free slots per pixel.
-//   Per pixel (FP32): one pass over the sure members accumulating weighted
-//     warps (weights on MUFU.EX2 relative to a tile-wide d^2 floor: a common
-//     factor cancels in dq_blend's normalisation), an early-reject sorted
-//     insertion of the ambiguous (closest first) into the m = S - |in| free
-//     slots, their accumulation, and the epilogue. When the selected and
-//     rejected boundary keys are within the FP32 error bound, the pixel re-runs
-//     in the exact tier (FP64, reference operation order and libm: the kNN
-//     set and blend are bit-identical to the reference's).
+//   k_plan (one warp per 16 x 16 tile, no block barriers): the same bound
+//     over the supertile list, then an FP64 classification of the tile's
+//     candidates against the tile rectangle: "in" (fewer than S others can
+//     ever be closer), "out" (at least S are always closer) or ambiguous. In
+//     and ambiguous ones become packed records in tile-local coordinates with
+//     their warps conjugated to the tile origin (T(-P) q T(o)); the ambiguous
+//     are then re-classified per 8 x 4 sub-tile (FP32, conservative margins),
+//     leaving ~2 free slots per pixel. Plans go to HBM (L2-resident).
+//   k_pixels (one CTA per tile, warp = sub-tile, one pixel per thread): one
+//     pass over the sure members accumulating weighted warps (weights on
+//     MUFU.EX2 relative to a tile-wide d^2 floor: the common factor cancels in
+//     dq_blend's normalisation), an early-reject sorted insertion of the
+//     ambiguous (closest first) into the m = S - |in| free slots, their
+//     accumulation and the epilogue. When the selected and rejected boundary
+//     keys are within the FP32 error bound, the pixel re-runs in the exact
+//     tier (FP64, reference operation order and libm: the kNN set and blend
+//     are bit-identical to the reference's).
 //   Tiles whose candidates span more than a quarter turn of rotation
 //   (hemisphere flips possible) or overflow a capacity run in the exact tier.
 #include <cfloat>
@@ -52,6 +53,7 @@ constexpr int ST = 64;            // supertile edge (4 x 4 tiles)
 constexpr int WCAP_S = 256;       // per-warp gather capacity in the supertile pass
 constexpr int SLIST_CAP = 1024;   // supertile list capacity
 constexpr int SFLAG_OVERFLOW = 1, SFLAG_NONUNIFORM = 2;
+constexpr int EMDQ_CHUNK_TILES = 16384;  // tile plans resident per launch chunk
 
 // Gathered candidate arrays (one entry per active index, in active order).
 struct Cand {
@@ -71,26 +73,48 @@ struct SuperLists {
     int nsx;     // supertiles per row
 };
 
-struct ESmem {
-    int hist[256];
-    int wcnt[NW];
-    int list[CAND_CAP];
-    double dmin2[CAND_CAP], dmax2[CAND_CAP], dc2[CAND_CAP];
-    unsigned char cls[CAND_CAP];
-    // staged: [0, n_in) CTA-in (index order), [n_in, ne) ambiguous (closest first)
-    int sidx[SCAP];
-    float4 rec0[SCAP];  // ux, uy (tile-local), prob, s - s0
-    float4 rec1[SCAP];  // conjugated dual quaternion (w, z, dx, dy)
-    float2 wd[NW][SCAP];          // per-warp (min, max) squared distance to the sub-tile
-    unsigned char wl[NW][SCAP];   // per-warp lists: extra sure members, then ambiguous
-    unsigned char wc[NW][SCAP];   // per-warp class of the CTA-ambiguous
-    double red_d[NW];
-    int red_k[NW];
-    int nc, n_in, n_amb, slow;
-    float R, d2ref;
-    double P[2], Y0[2], e0[2], s0;
+constexpr int TREC = 64;          // staged records per tile (in + ambiguous)
+constexpr int TCAND = 128;        // tile candidates before classification
+constexpr int PLAN_WARPS = 8;     // planning warps (tiles) per CTA
+constexpr int TFLAG_EXACT_SUPER = 1, TFLAG_EXACT_STAGED = 2;
+
+// Per-tile plan written by k_plan, read by k_pixels (one 16 x 16 tile).
+struct __align__(16) TileHdr {
+    double P[2], Y0[2], e0[2], s0;  // output origin / reference scale (FP64)
+    float d2ref, d2top;             // tile-wide d^2 floor / ceiling of the staged points
+    int nin, ne, flags, pad;
+    unsigned char nx[NW], na[NW];   // per sub-tile: extra sure members, ambiguous
 };
 
+struct TilePlans {
+    TileHdr* hdr;          // [ntiles]
+    float4* rec0;          // [ntiles][TREC]  ux, uy (tile-local), prob, s - s0
+    float4* rec1;          // [ntiles][TREC]  conjugated dual quaternion
+    int* sidx;             // [ntiles][TREC]  candidate indices (exact-tier fallback)
+    unsigned char* sub;    // [ntiles][NW][TREC]  per sub-tile: extra sure, then ambiguous
+    int tx0, ty0, ntx;     // chunk: first tile column/row, tiles per row
+};
+
+// Per-warp planning scratch.
+struct PlanWarp {
+    int hist[256];
+    int cand[TCAND];
+    double dmin2[TCAND], dmax2[TCAND], dc2[TCAND];
+    unsigned char cls[TCAND];
+    int sidx[TREC];
+    float2 wd[TREC];
+    float ux[TREC], uy[TREC];
+    unsigned char wcls[TREC];
+    float R;
+    double ref[7];
+};
+
+// Pixel-kernel shared memory (one tile).
+struct PixSmem {
+    float4 rec0[TREC], rec1[TREC];
+    int sidx[TREC];
+    unsigned char sub[NW][TREC];
+};
 struct SSmem {
     int hist[256];
     int wcnt[NW];
@@ -366,14 +390,273 @@ __device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx
 }
 
 // ---------------------------------------------------------------------------
+// k_plan: one warp per 16 x 16 tile (no block barriers).
+//   radius bound over the supertile list -> candidates -> FP64 in/out/
+//   ambiguous classification against the tile -> staged records (in: index
+//   order, ambiguous: by centre distance) in tile-local coordinates with
+//   conjugated warps -> per 8 x 4 sub-tile refinement of the ambiguous.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PLAN_WARPS * 32)
+k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    PlanWarp& w = reinterpret_cast<PlanWarp*>(smem_raw)[wid];
+    const int g = blockIdx.x * PLAN_WARPS + wid;  // tile index within the chunk
+    if (g >= ntiles) return;
+    const int tx = TP.tx0 + g % TP.ntx, ty = TP.ty0 + g / TP.ntx;
+    const int ti0 = L.grid.i0 + tx * ET, tj0 = L.grid.j0 + ty * ET;
+    const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;
+    const double xlo = ox, xhi = L.grid.gx + ti1, ylo = oy, yhi = L.grid.gy + tj1;
+    const double cxm = 0.5 * (xlo + xhi), cym = 0.5 * (ylo + yhi);
+    const double hd = 0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo));
+    const float cxf = (float)cxm, cyf = (float)cym;
+    const int sid = (ty / (ST / ET)) * SL.nsx + tx / (ST / ET);
+    const int sflag = SL.flag[sid];
+    const int nsrc = SL.count[sid];
+    const int* src = (sflag & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
+    TileHdr* hdr = TP.hdr + g;
+    int flags = 0;
+
+    // 1. radius bound
+#pragma unroll
+    for (int k = 0; k < 8; ++k) w.hist[lane + 32 * k] = 0;
+    __syncwarp();
+    for (int e = lane; e < nsrc; e += 32) {
+        const float2 c = C.c32[src ? src[e] : e];
+        const float dx = c.x - cxf, dy = c.y - cyf;
+        atomicAdd(&w.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
+    }
+    __syncwarp();
+    radius_from_hist(w.hist, S, lane, &w.R);
+    __syncwarp();
+    const float lim = w.R + (float)(2.0 * hd) + 1.0f, lim2 = lim * lim;
+
+    // 2. ordered gather
+    int nc = 0;
+    for (int base = 0; base < nsrc; base += 32) {
+        const int e = base + lane;
+        int a = -1;
+        if (e < nsrc) {
+            a = src ? src[e] : e;
+            const float2 c = C.c32[a];
+            const float dx = c.x - cxf, dy = c.y - cyf;
+            if (fmaf(dx, dx, dy * dy) > lim2) a = -1;
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, a >= 0);
+        if (a >= 0) {
+            const int pos = nc + __popc(msk & ((1u << lane) - 1u));
+            if (pos < TCAND) w.cand[pos] = a;
+        }
+        nc += __popc(msk);
+    }
+    if (nc > TCAND) flags |= TFLAG_EXACT_SUPER;
+    nc = min(nc, TCAND);
+    __syncwarp();
+
+    // 3. FP64 classification against the tile rectangle
+    for (int k = lane; k < nc; k += 32) {
+        const int a = w.cand[k];
+        const double ax = C.x[a], ay = C.y[a];
+        const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
+        const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
+        w.dmin2[k] = dxn * dxn + dyn * dyn;
+        w.dmax2[k] = dxf * dxf + dyf * dyf;
+        w.dc2[k] = (ax - cxm) * (ax - cxm) + (ay - cym) * (ay - cym);
+    }
+    __syncwarp();
+    for (int k = lane; k < nc; k += 32) {
+        const double hi = w.dmax2[k] * (1.0 + 1e-12) + 1e-9;
+        const double lo = w.dmin2[k] * (1.0 - 1e-12) - 1e-9;
+        int cle = 0, clt = 0;
+        for (int l = 0; l < nc; ++l) {
+            if (l == k) continue;
+            cle += w.dmin2[l] <= hi;
+            clt += w.dmax2[l] < lo;
+        }
+        w.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
+    }
+    __syncwarp();
+
+    // 4. staging order + tile reference
+    int ni = 0, na = 0;
+    for (int base = 0; base < nc; base += 32) {
+        const int k = base + lane;
+        const int c = k < nc ? w.cls[k] : 0;
+        const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+        if (c == 1 && ni + __popc(mi & ((1u << lane) - 1u)) < TREC)
+            w.sidx[ni + __popc(mi & ((1u << lane) - 1u))] = w.cand[k];
+        ni += __popc(mi);
+        na += __popc(__ballot_sync(0xffffffffu, c == 2));
+    }
+    const int ne = ni + na;
+    if (ni > S || ne < S || ne > TREC) flags |= TFLAG_EXACT_SUPER;
+    double best = 1e300;
+    int bestk = 0x7fffffff;
+    if (!(flags & TFLAG_EXACT_SUPER)) {
+        for (int k = lane; k < nc; k += 32) {
+            const int c = w.cls[k];
+            const double dk = w.dc2[k];
+            if (c == 2) {
+                int r = 0;
+                for (int l = 0; l < nc; ++l)
+                    r += (w.cls[l] == 2) & ((w.dc2[l] < dk) | ((w.dc2[l] == dk) & (l < k)));
+                w.sidx[ni + r] = w.cand[k];
+            }
+            if (c != 0 && (dk < best || (dk == best && k < bestk))) {
+                best = dk;
+                bestk = k;
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const double bd = __shfl_xor_sync(0xffffffffu, best, d);
+        const int bk = __shfl_xor_sync(0xffffffffu, bestk, d);
+        if (bd < best || (bd == best && bk < bestk)) {
+            best = bd;
+            bestk = bk;
+        }
+    }
+    if (flags & TFLAG_EXACT_SUPER) {
+        if (lane == 0) {
+            hdr->flags = flags;
+            hdr->ne = 0;
+            hdr->nin = 0;
+        }
+        return;
+    }
+    if (lane == 0) {
+        const W5 qr = load_w5(&C.l[5 * w.cand[bestk]]);
+        double yx, yy;
+        xapply(qr, ox, oy, &yx, &yy);
+        const double Y0 = rint(yx), Y1 = rint(yy);
+        const double P0 = Y0 / qr.s, P1 = Y1 / qr.s;
+        w.ref[0] = P0;
+        w.ref[1] = P1;
+        w.ref[2] = Y0;
+        w.ref[3] = Y1;
+        w.ref[4] = fma(qr.s, P0, -Y0);
+        w.ref[5] = fma(qr.s, P1, -Y1);
+        w.ref[6] = qr.s;
+    }
+    __syncwarp();
+    const double P0 = w.ref[0], P1 = w.ref[1], s0 = w.ref[6];
+    if (!(s0 > 0.0) || !isfinite(P0) || !isfinite(P1)) flags |= TFLAG_EXACT_STAGED;
+    if (sflag & SFLAG_NONUNIFORM) flags |= TFLAG_EXACT_STAGED;
+
+    // 5. records (tile-local coordinates, conjugated warps)
+    float4* r0g = TP.rec0 + (size_t)g * TREC;
+    float4* r1g = TP.rec1 + (size_t)g * TREC;
+    int* sg = TP.sidx + (size_t)g * TREC;
+    float d2lo = FLT_MAX, d2hi = 0.f;
+    for (int k = lane; k < ne; k += 32) {
+        const int a = w.sidx[k];
+        const W5 q = load_w5(&C.l[5 * a]);
+        const double hx = 0.5 * ox, hy = 0.5 * oy;
+        const double qa_dx = (q.w * hx - q.z * hy) + q.dx;  // q * T(o)
+        const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
+        const double px = 0.5 * P0, py = 0.5 * P1;         // T(-P) * (q * T(o))
+        r1g[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
+                             (float)(qa_dy + (px * q.z - py * q.w)));
+        const double ux = C.x[a] - ox, uy = C.y[a] - oy;
+        r0g[k] = make_float4((float)ux, (float)uy, (float)C.p[a], (float)(q.s - s0));
+        sg[k] = a;
+        w.ux[k] = (float)ux;
+        w.uy[k] = (float)uy;
+        const double dxn = fmax(fmax(-ux, 0.0), ux - (xhi - xlo)), dyn = fmax(fmax(-uy, 0.0), uy - (yhi - ylo));
+        const double dxf = fmax(ux, (xhi - xlo) - ux), dyf = fmax(uy, (yhi - ylo) - uy);
+        d2lo = fminf(d2lo, (float)(dxn * dxn + dyn * dyn));
+        d2hi = fmaxf(d2hi, (float)(dxf * dxf + dyf * dyf));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        d2lo = fminf(d2lo, __shfl_xor_sync(0xffffffffu, d2lo, d));
+        d2hi = fmaxf(d2hi, __shfl_xor_sync(0xffffffffu, d2hi, d));
+    }
+    if ((float)L.alpha * (d2hi - d2lo) >= 60.f) flags |= TFLAG_EXACT_STAGED;
+    __syncwarp();
+
+    // 6. per sub-tile refinement of the tile-ambiguous (FP32, conservative margins)
+    unsigned char* subg = TP.sub + (size_t)g * NW * TREC;
+    int my_nx = 0, my_na = 0;  // lane st < NW keeps sub-tile st's counts
+    for (int st = 0; st < NW; ++st) {
+        const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
+        const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
+        int nx = 0, nw = 0;
+        if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
+            for (int k = lane; k < ne; k += 32) {
+                const float ax = w.ux[k], ay = w.uy[k];
+                const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
+                const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
+                w.wd[k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
+            }
+            __syncwarp();
+            for (int base = ni; base < ne; base += 32) {
+                const int k = base + lane;
+                int c = 0;
+                if (k < ne) {
+                    const float2 dk = w.wd[k];
+                    const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
+                    int cle = -1, clt = 0;  // l == k always counts in cle
+                    for (int l = 0; l < ne; ++l) {
+                        const float2 dl = w.wd[l];
+                        cle += dl.x <= hi;
+                        clt += dl.y < lo;
+                    }
+                    c = cle < S ? 1 : (clt >= S ? 0 : 2);
+                    w.wcls[k] = (unsigned char)c;
+                }
+                const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+                if (c == 1) subg[st * TREC + nx + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
+                nx += __popc(mi);
+            }
+            __syncwarp();
+            for (int base = ni; base < ne; base += 32) {
+                const int k = base + lane;
+                const int c = k < ne ? w.wcls[k] : 0;
+                const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+                if (c == 2) subg[st * TREC + nx + nw + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
+                nw += __popc(ma);
+            }
+            __syncwarp();
+        } else {
+            nx = 255;  // sub-tile without valid pixels, or exact tile
+        }
+        if (lane == st) {
+            my_nx = nx;
+            my_na = nw;
+        }
+    }
+    if (lane < NW) {
+        hdr->nx[lane] = (unsigned char)my_nx;
+        hdr->na[lane] = (unsigned char)my_na;
+    }
+    if (lane == 0) {
+        hdr->P[0] = P0;
+        hdr->P[1] = P1;
+        hdr->Y0[0] = w.ref[2];
+        hdr->Y0[1] = w.ref[3];
+        hdr->e0[0] = w.ref[4];
+        hdr->e0[1] = w.ref[5];
+        hdr->s0 = s0;
+        hdr->d2ref = d2lo;
+        hdr->d2top = d2hi;
+        hdr->nin = ni;
+        hdr->ne = ne;
+        hdr->flags = flags;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Fast tier for one pixel (ux, uy = tile-local pixel position).
-//   sure members: staged [0, nin) plus the warp's extra sure ones wl[0, nxin)
-//   ambiguous:    wl[nxin, nxin + namb), closest-to-centre first
+//   sure members: records [0, nin) plus sub-list [0, nxin)
+//   ambiguous:    sub-list [nxin, nxin + namb), closest-to-centre first
 // ---------------------------------------------------------------------------
 struct FastOut {
     float s0, s1, s2, s3, s4, s5;  // sums: w*qw, w*qz, w*qdx, w*qdy, w*(s-s0), w
-    int k0, k1;                    // nearest and runner-up staged entries
-    float d0, d1;                  // their FP32 squared distances
+    int k0;                        // nearest staged entry
+    float d0, d1;                  // smallest and second-smallest FP32 squared distance
     bool exact;                    // boundary near-tie: rerun in the exact tier
 };
 
@@ -382,21 +665,16 @@ __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
 template <int MS>
 __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, const unsigned char* __restrict__ wl,
-                                           int nxin, int namb, int m, const ESmem& s, float nal, float c0,
+                                           int nxin, int namb, int m, const PixSmem& s, float nal, float c0,
                                            FastOut& o) {
     float b0 = FLT_MAX, b1 = FLT_MAX;
-    int k0 = -1, k1 = -1;
+    int k0 = 0;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
     auto take = [&](int k, float d2, const float4& r0) {
-        if (d2 < b0) {
-            b1 = b0;
-            k1 = k0;
-            b0 = d2;
-            k0 = k;
-        } else if (d2 < b1) {
-            b1 = d2;
-            k1 = k;
-        }
+        const bool nb = d2 < b0;
+        b1 = nb ? b0 : fminf(b1, d2);
+        k0 = nb ? k : k0;
+        b0 = nb ? d2 : b0;
         // exp(-alpha (d2 - d2ref)): the factor exp(alpha (d2min - d2ref)) common
         // to every weight cancels in dq_blend's normalisation
         const float w = ex2_approx(fmaf(d2, nal, c0)) * r0.z;
@@ -464,44 +742,36 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, const un
         for (int q = 0; q < MS; ++q)
             if (q < m) take(sk[q], sd[q], s.rec0[sk[q]]);
     }
-    o = FastOut{a0, a1, a2, a3, a4, a5, k0, k1, b0, b1, exact};
+    o = FastOut{a0, a1, a2, a3, a4, a5, k0, b0, b1, exact};
 }
 
 __device__ __forceinline__ void fast_dispatch(float ux, float uy, int nin, const unsigned char* wl, int nxin,
-                                              int namb, int m, const ESmem& s, float nal, float c0, FastOut& o) {
+                                              int namb, int m, const PixSmem& s, float nal, float c0, FastOut& o) {
     if (m <= 0)
         fast_pixel<0>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else if (m <= 2)
         fast_pixel<2>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else if (m <= 4)
         fast_pixel<4>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
-    else if (m <= 8)
-        fast_pixel<8>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
     else
-        fast_pixel<16>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
+        fast_pixel<8>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
 }
 
+// ---------------------------------------------------------------------------
+// k_pixels: one CTA per 16 x 16 tile, warp w = 8 x 4 sub-tile w.
+// ---------------------------------------------------------------------------
 template <int MAXS>
-__global__ void __launch_bounds__(ENT, 2)
-k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ESmem& s = *reinterpret_cast<ESmem*>(smem_raw);
+__global__ void __launch_bounds__(ENT, 3)
+k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
+    __shared__ __align__(16) PixSmem s;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int ti0 = L.grid.i0 + blockIdx.x * ET, tj0 = L.grid.j0 + blockIdx.y * ET;
+    const int g = blockIdx.y * TP.ntx + blockIdx.x;
+    const int tx = TP.tx0 + blockIdx.x, ty = TP.ty0 + blockIdx.y;
+    const int ti0 = L.grid.i0 + tx * ET, tj0 = L.grid.j0 + ty * ET;
     const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
-    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // tile origin (pixel (ti0, tj0))
-    const double xlo = ox, xhi = L.grid.gx + ti1, ylo = oy, yhi = L.grid.gy + tj1;
-    const double cxm = 0.5 * (xlo + xhi), cym = 0.5 * (ylo + yhi);
-    const double hd = 0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo));
-    const float cxf = (float)cxm, cyf = (float)cym;
+    const TileHdr& h = TP.hdr[g];
+    const int flags = h.flags, ne = h.ne, nin = h.nin;
 
-    // supertile list of this tile
-    const int sid = (blockIdx.y / (ST / ET)) * SL.nsx + blockIdx.x / (ST / ET);
-    const int sflag = SL.flag[sid];
-    const int nsrc = SL.count[sid];
-    const int* src = (sflag & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
-
-    // this thread's pixel: warp w owns the 8 x 4 sub-tile ((w & 1) * 8, (w >> 1) * 4)
     const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
     const int pi = ti0 + lx, pj = tj0 + ly;
     const bool valid = pi <= ti1 && pj <= tj1;
@@ -510,249 +780,37 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
     float2* od = (valid && L.disp) ? &L.disp[o] : nullptr;
     float* ou = (valid && L.unc) ? &L.unc[o] : nullptr;
 
-    // ---- 1. radius bound over the supertile list --------------------------
-    s.hist[t] = 0;
-    if (t == 0) {
-        s.slow = 0;
-        s.nc = 0;
-    }
-    __syncthreads();
-    for (int e = t; e < nsrc; e += ENT) {
-        const float2 c = C.c32[src ? src[e] : e];
-        const float dx = c.x - cxf, dy = c.y - cyf;
-        atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
-    }
-    __syncthreads();
-    if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
-    __syncthreads();
-    const float lim = s.R + (float)(2.0 * hd) + 1.0f, lim2 = lim * lim;
-
-    // ---- 2. ordered gather ------------------------------------------------
-    for (int base = 0; base < nsrc; base += ENT) {
-        const int e = base + t;
-        int a = -1;
-        if (e < nsrc) {
-            a = src ? src[e] : e;
-            const float2 c = C.c32[a];
-            const float dx = c.x - cxf, dy = c.y - cyf;
-            if (fmaf(dx, dx, dy * dy) > lim2) a = -1;
-        }
-        const unsigned msk = __ballot_sync(0xffffffffu, a >= 0);
-        if (lane == 0) s.wcnt[wid] = __popc(msk);
-        __syncthreads();
-        int off = s.nc;
-        for (int w = 0; w < wid; ++w) off += s.wcnt[w];
-        if (a >= 0) {
-            const int pos = off + __popc(msk & ((1u << lane) - 1u));
-            if (pos < CAND_CAP) s.list[pos] = a;
-            else s.slow = 1;
-        }
-        __syncthreads();
-        if (t == 0)
-            for (int w = 0; w < NW; ++w) s.nc += s.wcnt[w];
-        __syncthreads();
-    }
-    const int nc = min(s.nc, CAND_CAP);
-
-    // ---- 3. classification against the tile rectangle (FP64) ------------
-    for (int k = t; k < nc; k += ENT) {
-        const int a = s.list[k];
-        const double ax = C.x[a], ay = C.y[a];
-        const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
-        const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
-        s.dmin2[k] = dxn * dxn + dyn * dyn;
-        s.dmax2[k] = dxf * dxf + dyf * dyf;
-        s.dc2[k] = (ax - cxm) * (ax - cxm) + (ay - cym) * (ay - cym);
-    }
-    __syncthreads();
-    for (int k = t; k < nc; k += ENT) {
-        const double hi = s.dmax2[k] * (1.0 + 1e-12) + 1e-9;
-        const double lo = s.dmin2[k] * (1.0 - 1e-12) - 1e-9;
-        int cle = 0, clt = 0;
-        for (int l = 0; l < nc; ++l) {
-            if (l == k) continue;
-            cle += s.dmin2[l] <= hi;
-            clt += s.dmax2[l] < lo;
-        }
-        s.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
-    }
-    __syncthreads();
-
-    // ---- 4. staging (all threads): in-list in index order, ambiguous by
-    //         centre distance; tile reference = staged point nearest the centre
-    {
-        double best = 1e300;
-        int bestk = 0x7fffffff, nin_t = 0, namb_t = 0;
-        for (int k = t; k < nc; k += ENT) {
-            const int c = s.cls[k];
-            const double dk = s.dc2[k];
-            int before_in = 0, rank = 0, ni = 0, na = 0;
-            for (int l = 0; l < nc; ++l) {
-                const int cl = s.cls[l];
-                ni += cl == 1;
-                na += cl == 2;
-                before_in += (cl == 1) & (l < k);
-                rank += (cl == 2) & ((s.dc2[l] < dk) | ((s.dc2[l] == dk) & (l < k)));
-            }
-            nin_t = ni;
-            namb_t = na;
-            if (c == 1 && before_in < SCAP) s.sidx[before_in] = k;
-            if (c == 2 && ni + rank < SCAP) s.sidx[ni + rank] = k;
-            if (c != 0 && (dk < best || (dk == best && k < bestk))) {
-                best = dk;
-                bestk = k;
-            }
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            const double bd = __shfl_xor_sync(0xffffffffu, best, d);
-            const int bk = __shfl_xor_sync(0xffffffffu, bestk, d);
-            if (bd < best || (bd == best && bk < bestk)) {
-                best = bd;
-                bestk = bk;
-            }
-        }
-        if (lane == 0) {
-            s.red_d[wid] = best;
-            s.red_k[wid] = bestk;
-        }
-        if (t == 0) {
-            s.n_in = nin_t;
-            s.n_amb = namb_t;
-        }
-        __syncthreads();
-        if (t == 0) {
-            for (int w = 1; w < NW; ++w)
-                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_k[w] < bestk)) {
-                    best = s.red_d[w];
-                    bestk = s.red_k[w];
-                }
-            const int ni = s.n_in, na = s.n_amb;
-            int slow = s.slow || ni > S || ni + na < S || ni + na > SCAP || bestk >= nc;
-            if (!slow) {
-                const W5 qr = load_w5(&C.l[5 * s.list[bestk]]);
-                double yx, yy;
-                xapply(qr, ox, oy, &yx, &yy);
-                s.s0 = qr.s;
-                s.Y0[0] = rint(yx);
-                s.Y0[1] = rint(yy);
-                s.P[0] = s.Y0[0] / qr.s;
-                s.P[1] = s.Y0[1] / qr.s;
-                s.e0[0] = fma(qr.s, s.P[0], -s.Y0[0]);
-                s.e0[1] = fma(qr.s, s.P[1], -s.Y0[1]);
-                if (!(qr.s > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) slow = 1;
-            }
-            s.slow = slow;
-        }
-        __syncthreads();
-    }
-    const int nin = s.n_in, namb = s.n_amb, ne = nin + namb;
-    if (s.slow) {  // overflow / inconsistent classification: exact brute force over the supertile list
-        if (valid) exact_dispatch<MAXS>(qx, qy, src, nsrc, S, C, L.alpha, L.beta, od, ou);
+    if (flags & TFLAG_EXACT_SUPER) {  // exact brute force over the supertile list
+        const int sid = (ty / (ST / ET)) * SL.nsx + tx / (ST / ET);
+        const int* src = (SL.flag[sid] & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
+        if (valid) exact_dispatch<MAXS>(qx, qy, src, SL.count[sid], S, C, L.alpha, L.beta, od, ou);
         return;
     }
-    // staged entries -> candidate indices (sidx held tile-list positions)
-    for (int k = t; k < ne; k += ENT) s.sidx[k] = s.list[s.sidx[k]];
+    // stage the plan (records, candidate indices, sub-tile lists)
+    const float4* r0g = TP.rec0 + (size_t)g * TREC;
+    const float4* r1g = TP.rec1 + (size_t)g * TREC;
+    for (int k = t; k < ne; k += ENT) {
+        s.rec0[k] = r0g[k];
+        s.rec1[k] = r1g[k];
+        s.sidx[k] = TP.sidx[(size_t)g * TREC + k];
+    }
+    const int nxin = h.nx[wid], namb = h.na[wid];
+    const unsigned char* subg = TP.sub + ((size_t)g * NW + wid) * TREC;
+    if (nxin != 255)
+        for (int k = lane; k < nxin + namb; k += 32) s.sub[wid][k] = subg[k];
     __syncthreads();
-    if (sflag & SFLAG_NONUNIFORM) {  // hemisphere flips possible: exact tier
-        if (valid) exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
-        return;
-    }
-
-    // ---- 5. packed records: local coordinates + conjugated warps ----------
-    {
-        const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
-        float d2lo = FLT_MAX, d2hi = 0.f;
-        for (int k = t; k < ne; k += ENT) {
-            const int a = s.sidx[k];
-            const W5 q = load_w5(&C.l[5 * a]);
-            const double hx = 0.5 * ox, hy = 0.5 * oy;
-            const double qa_dx = (q.w * hx - q.z * hy) + q.dx;  // q * T(o)
-            const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
-            const double px = 0.5 * P0, py = 0.5 * P1;         // T(-P) * (q * T(o))
-            s.rec1[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
-                                    (float)(qa_dy + (px * q.z - py * q.w)));
-            const double ux = C.x[a] - ox, uy = C.y[a] - oy;
-            s.rec0[k] = make_float4((float)ux, (float)uy, (float)C.p[a], (float)(q.s - s0));
-            // d^2 range over the tile (for the weight reference)
-            const double dxn = fmax(fmax(-ux, 0.0), ux - (xhi - xlo)), dyn = fmax(fmax(-uy, 0.0), uy - (yhi - ylo));
-            const double dxf = fmax(ux, (xhi - xlo) - ux), dyf = fmax(uy, (yhi - ylo) - uy);
-            d2lo = fminf(d2lo, (float)(dxn * dxn + dyn * dyn));
-            d2hi = fmaxf(d2hi, (float)(dxf * dxf + dyf * dyf));
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-            d2lo = fminf(d2lo, __shfl_xor_sync(0xffffffffu, d2lo, d));
-            d2hi = fmaxf(d2hi, __shfl_xor_sync(0xffffffffu, d2hi, d));
-        }
-        if (lane == 0) {
-            s.red_d[wid] = d2lo;
-            s.red_k[wid] = __float_as_int(d2hi);
-        }
-    }
-    __syncthreads();
-    float d2ref = FLT_MAX, d2top = 0.f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-        d2ref = fminf(d2ref, (float)s.red_d[w]);
-        d2top = fmaxf(d2top, __int_as_float(s.red_k[w]));
-    }
-
-    // ---- 6. per-warp refinement of the CTA-ambiguous (FP32, margins) ------
-    const float wx0 = (float)((wid & 1) * 8), wy0 = (float)((wid >> 1) * 4);
-    const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
-    const bool wempty = wx0 > wx1 || wy0 > wy1;
-    int nxin = 0, nwamb = 0;
-    if (!wempty) {
-        for (int k = lane; k < ne; k += 32) {
-            const float4 r0 = s.rec0[k];
-            const float dxn = fmaxf(fmaxf(wx0 - r0.x, 0.f), r0.x - wx1), dyn = fmaxf(fmaxf(wy0 - r0.y, 0.f), r0.y - wy1);
-            const float dxf = fmaxf(r0.x - wx0, wx1 - r0.x), dyf = fmaxf(r0.y - wy0, wy1 - r0.y);
-            s.wd[wid][k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
-        }
-        __syncwarp();
-        for (int base = nin; base < ne; base += 32) {
-            const int k = base + lane;
-            int c = 0;
-            if (k < ne) {
-                const float2 dk = s.wd[wid][k];
-                const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
-                int cle = 0, clt = 0;
-                for (int l = 0; l < ne; ++l) {
-                    const float2 dl = s.wd[wid][l];
-                    cle += dl.x <= hi;
-                    clt += dl.y < lo;
-                }
-                --cle;  // l == k is always counted (dk.x <= dk.y <= hi)
-                c = cle < S ? 1 : (clt >= S ? 0 : 2);
-            }
-            const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-            if (c == 1) s.wl[wid][nxin + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
-            nxin += __popc(mi);
-            if (k < ne) s.wc[wid][k] = (unsigned char)c;
-        }
-        __syncwarp();
-        for (int base = nin; base < ne; base += 32) {
-            const int k = base + lane;
-            const int c = k < ne ? s.wc[wid][k] : 0;
-            const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
-            if (c == 2) s.wl[wid][nxin + nwamb + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
-            nwamb += __popc(ma);
-        }
-        __syncwarp();
-    }
     if (!valid) return;
+    if (flags & TFLAG_EXACT_STAGED) {
+        exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        return;
+    }
     const int wi = nin + nxin, m = S - wi;
-    // exponent range guard: weights relative to the tile floor stay far from FP32 underflow
-    const bool fast_ok = !wempty && m >= 0 && m <= 16 && wi + nwamb >= S &&
-                         (float)L.alpha * (d2top - d2ref) < 60.f;
-
-    // ---- 7. per pixel ------------------------------------------------------
     FastOut fo;
-    bool ex = !fast_ok;
+    bool ex = nxin == 255 || m < 0 || m > 8 || wi + namb < S;
+    const float d2ref = h.d2ref;
     if (!ex) {
         const float nal = (float)(-L.alpha * kLog2e);
-        fast_dispatch((float)lx, (float)ly, nin, s.wl[wid], nxin, nwamb, m, s, nal, -nal * d2ref, fo);
+        fast_dispatch((float)lx, (float)ly, nin, s.sub[wid], nxin, namb, m, s, nal, -nal * d2ref, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
@@ -766,15 +824,21 @@ k_emdq(EmdqLaunch L, Cand C, SuperLists SL, int S) {
     const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
     const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
     const float dlb = fo.s4 / fo.s5;
-    const double sb = s.s0 + (double)dlb;
-    const double yx = s.Y0[0] + (s.e0[0] + (double)dlb * s.P[0] + sb * (double)Qx);
-    const double yy = s.Y0[1] + (s.e0[1] + (double)dlb * s.P[1] + sb * (double)Qy);
+    const double sb = h.s0 + (double)dlb;
+    const double yx = h.Y0[0] + (h.e0[0] + (double)dlb * h.P[0] + sb * (double)Qx);
+    const double yy = h.Y0[1] + (h.e0[1] + (double)dlb * h.P[1] + sb * (double)Qy);
     if (od) *od = make_float2((float)(yx - qx), (float)(yy - qy));
     if (ou) {
-        // d2min in the exact tier (the nearest, or the closer of two near-tied)
+        // d2min in the exact tier: the nearest, or the exact minimum over every
+        // staged point within the FP32 error of it (near-tie, rare)
         double d2m = xdist2(qx, qy, C.x[s.sidx[fo.k0]], C.y[s.sidx[fo.k0]]);
-        if (fo.k1 >= 0 && fo.d1 - fo.d0 <= d2_tol(fo.d1))
-            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[fo.k1]], C.y[s.sidx[fo.k1]]));
+        if (fo.d1 - fo.d0 <= d2_tol(fo.d1)) {
+            for (int k = 0; k < ne; ++k) {
+                const float dx = s.rec0[k].x - ux, dy = s.rec0[k].y - uy;
+                if (fmaf(dx, dx, dy * dy) - fo.d0 <= d2_tol(fo.d1))
+                    d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[k]], C.y[s.sidx[k]]));
+            }
+        }
         double arg = xmul(L.beta, d2m);
         if (55.0 < arg) arg = 55.0;
         *ou = (float)xexp(arg);
@@ -787,14 +851,16 @@ size_t emdq_scratch_bytes(int nactive, const FieldGrid& g) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nsuper = (size_t)nsx * nsy;
+    const size_t plans = (size_t)EMDQ_CHUNK_TILES * (sizeof(TileHdr) + TREC * (2 * sizeof(float4) + sizeof(int) + NW));
     return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
-           256;
+           plans + 1024;
 }
 
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches) {
     if (L.nactive <= 0) return cudaErrorInvalidValue;
     const size_t na = (size_t)L.nactive;
-    // scratch layout (emdq_scratch_bytes): x, y, l[5], p, phi (double) | c32 (float2) | j (int) | supertile lists
+    // scratch layout (emdq_scratch_bytes): x, y, l[5], p, phi (double) | c32 (float2) | j (int) |
+    // supertile lists | tile plans (one chunk)
     Cand C;
     C.x = L.cx;
     C.y = L.cy;
@@ -813,6 +879,15 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     SL.list = cj + na;
     SL.count = SL.list + nsuper * SLIST_CAP;
     SL.flag = SL.count + nsuper;
+    char* pbase = reinterpret_cast<char*>(SL.flag + nsuper);
+    pbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(pbase) + 255) & ~uintptr_t(255));
+    TilePlans TP;
+    TP.hdr = reinterpret_cast<TileHdr*>(pbase);
+    TP.rec0 = reinterpret_cast<float4*>(TP.hdr + EMDQ_CHUNK_TILES);
+    TP.rec1 = TP.rec0 + (size_t)EMDQ_CHUNK_TILES * TREC;
+    TP.sidx = reinterpret_cast<int*>(TP.rec1 + (size_t)EMDQ_CHUNK_TILES * TREC);
+    TP.sub = reinterpret_cast<unsigned char*>(TP.sidx + (size_t)EMDQ_CHUNK_TILES * TREC);
+
     k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
                                                        c32, L.cl, L.cp, phi, cj);
     ++*launches;
@@ -825,18 +900,29 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     ++*launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const int nx = (L.grid.i1 - L.grid.i0 + ET) / ET;
-    const int ny = (L.grid.j1 - L.grid.j0 + ET) / ET;
-    const size_t smem = sizeof(ESmem);
-    if (S <= 16) {
-        cudaFuncSetAttribute(k_emdq<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<16><<<dim3(nx, ny), ENT, smem, st>>>(L, C, SL, S);
-    } else {
-        cudaFuncSetAttribute(k_emdq<MAX_SUPPORT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k_emdq<MAX_SUPPORT><<<dim3(nx, ny), ENT, smem, st>>>(L, C, SL, S);
+    const int ntx = (L.grid.i1 - L.grid.i0 + ET) / ET;
+    const int nty = (L.grid.j1 - L.grid.j0 + ET) / ET;
+    const int rows_per_chunk = EMDQ_CHUNK_TILES / ntx > 0 ? EMDQ_CHUNK_TILES / ntx : 1;
+    const size_t psm = sizeof(PlanWarp) * PLAN_WARPS;
+    cudaFuncSetAttribute(k_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+    for (int ty0 = 0; ty0 < nty; ty0 += rows_per_chunk) {
+        const int rows = min(rows_per_chunk, nty - ty0);
+        if ((size_t)rows * ntx > (size_t)EMDQ_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
+        TP.tx0 = 0;
+        TP.ty0 = ty0;
+        TP.ntx = ntx;
+        const int ntiles = rows * ntx;
+        k_plan<<<(ntiles + PLAN_WARPS - 1) / PLAN_WARPS, PLAN_WARPS * 32, psm, st>>>(L, C, SL, TP, ntiles, S);
+        ++*launches;
+        if (S <= 16)
+            k_pixels<16><<<dim3(ntx, rows), ENT, 0, st>>>(L, C, SL, TP, S);
+        else
+            k_pixels<MAX_SUPPORT><<<dim3(ntx, rows), ENT, 0, st>>>(L, C, SL, TP, S);
+        ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
-    ++*launches;
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 }  // namespace nrm
