@@ -313,6 +313,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tmax = float(t.item())
     st = stats_t.cpu().numpy()
+    exc_blend, exc_emdq = ctx.exceptions()
     mpix_step = nfr * fw * fh / 1e6
     value = mpix_step * args.steps / (tmax * 1e-3)
 
@@ -417,7 +418,8 @@ def main():
                        "inliers": int(len(e.active)), "nodes": int(len(wl.anchors)), "canvas": wl.canvas,
                        "frames_per_step": nfr, "parallelism": f"band{world}" if world > 1 else "single",
                        "l2": "flushed between steps (256 MiB write, untimed)",
-                       "blend_stats_frame0": [int(v) for v in st[0]]},
+                       "blend_stats_frame0": [int(v) for v in st[0]],
+                       "exact_tier_pixels": {"blend_last_frame": int(exc_blend), "emdq_last_frame": int(exc_emdq)}},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

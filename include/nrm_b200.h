@@ -183,6 +183,11 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
  * device so tests can check it bit-for-bit against the host libm. */
 int nrm_selftest_libm(nrm_ctx *ctx, const double *x, const double *y, int n, double *exp_out,
                       double *hypot_out);
+/* Margin-classified exceptions of the last calls on this context (parity
+ * reporting): pixels the last blend_frame / node_field exception pass resolved
+ * in the exact tier, and pixels of the last emdq_field that took the exact
+ * tier. Synchronises the context stream. */
+int nrm_ctx_exceptions(nrm_ctx *ctx, int64_t *blend_exceptions, int64_t *emdq_exact);
 /* Measured pipe throughput on this device, lane-operations per second:
  * which = 0: FP32 FFMA, which = 1: MUFU.EX2 (roofline denominators). */
 int nrm_selftest_peak(nrm_ctx *ctx, int which, double *ops_per_s);

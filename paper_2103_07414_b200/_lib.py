@@ -96,6 +96,7 @@ SIGNATURES = [
                                         C.c_double, C.c_int, C.c_double, _P, _P]),
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
+    ("nrm_ctx_exceptions", C.c_int, [_P, _I64, _I64]),
 ]
 
 _lib: C.CDLL | None = None

@@ -783,7 +783,10 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     if (flags & TFLAG_EXACT_SUPER) {  // exact brute force over the supertile list
         const int sid = (ty / (ST / ET)) * SL.nsx + tx / (ST / ET);
         const int* src = (SL.flag[sid] & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
-        if (valid) exact_dispatch<MAXS>(qx, qy, src, SL.count[sid], S, C, L.alpha, L.beta, od, ou);
+        if (valid) {
+            if (L.exact_count) atomicAdd(L.exact_count, 1u);
+            exact_dispatch<MAXS>(qx, qy, src, SL.count[sid], S, C, L.alpha, L.beta, od, ou);
+        }
         return;
     }
     // stage the plan (records, candidate indices, sub-tile lists)
@@ -801,6 +804,7 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     __syncthreads();
     if (!valid) return;
     if (flags & TFLAG_EXACT_STAGED) {
+        if (L.exact_count) atomicAdd(L.exact_count, 1u);
         exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
@@ -814,6 +818,7 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
+        if (L.exact_count) atomicAdd(L.exact_count, 1u);
         exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }

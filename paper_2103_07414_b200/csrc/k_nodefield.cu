@@ -33,6 +33,7 @@ namespace {
 
 constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
 constexpr int EXC_THREADS = 1024;
+constexpr int EXC_CHUNK = 384;  // nodes staged per chunk in the exception pass (21 KB)
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
 constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 constexpr double kBoundMargin = 4e-3;
@@ -432,14 +433,31 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
 template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
+    __shared__ double sa[2 * EXC_CHUNK], sq[5 * EXC_CHUNK];
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
     int nb = 0, nns = 0, noof = 0;
-    const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
-    for (unsigned q = threadIdx.x; q < cnt; q += EXC_THREADS) {
-        const int2 p = L.exc[q];
+    const double fxm = L.fw - 1.0, fym = L.fh - 1.0, na = -L.alpha;
+    // batches of EXC_THREADS pixels; nodes streamed through shared memory in
+    // index order (the reference's summation order), one chunk at a time
+    for (unsigned q0 = 0; q0 < cnt; q0 += EXC_THREADS) {
+        const unsigned q = q0 + threadIdx.x;
+        const bool act = q < cnt;
+        const int2 p = act ? L.exc[q] : make_int2(0, 0);
         const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
+        XPW st;
+        xpw_init(st);
+        for (int c0 = 0; c0 < L.n; c0 += EXC_CHUNK) {
+            const int cn = min(EXC_CHUNK, L.n - c0);
+            __syncthreads();
+            for (int k = threadIdx.x; k < 2 * cn; k += EXC_THREADS) sa[k] = L.anchors[2 * c0 + k];
+            for (int k = threadIdx.x; k < 5 * cn; k += EXC_THREADS) sq[k] = L.warps[5 * c0 + k];
+            __syncthreads();
+            if (act)
+                for (int i = 0; i < cn; ++i) xpw_add(st, x, y, sa[2 * i], sa[2 * i + 1], &sq[5 * i], na);
+        }
+        if (!act) continue;
         W5 wp;
-        const int rc = xpixel_warp(x, y, L.anchors, L.warps, L.n, L.alpha, &wp);
+        const int rc = xpw_finish(st, &wp);
         if (MODE == 1) {
             const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
             if (rc == 0) {
@@ -499,6 +517,7 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
             }
             L.acc[0] = L.acc[1] = L.acc[2] = 0;
         }
+        if (L.exc_last) *L.exc_last = cnt;
         *L.exc_count = 0;
     }
 }

@@ -232,15 +232,20 @@ Bbox footprint_bbox(const double* poly, int npoly) {
 
 // Per-context device state (c->misc, zeroed at context creation and restored
 // by every exception pass): acc[3] (u64) | exc_count (u32) | overflow (u32).
+// Diagnostics follow: last_exc (u32, pixels the last exception pass resolved),
+// emdq_exact (u32, K3 pixels that took the exact tier, reset per call).
 struct State {
     unsigned long long* acc;
     unsigned* exc_count;
     unsigned* overflow;
+    unsigned* last_exc;
+    unsigned* emdq_exact;
 };
 State state_of(nrm_ctx* c) {
     char* b = c->misc.as<char>();
     return {reinterpret_cast<unsigned long long*>(b), reinterpret_cast<unsigned*>(b + 24),
-            reinterpret_cast<unsigned*>(b + 28)};
+            reinterpret_cast<unsigned*>(b + 28), reinterpret_cast<unsigned*>(b + 32),
+            reinterpret_cast<unsigned*>(b + 36)};
 }
 
 // Shared core of blend_frame: everything after the inputs are in HBM.
@@ -301,6 +306,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.exc_count = st.exc_count;
     L.exc_cap = (unsigned)exc_cap;
     L.exc_overflow = st.overflow;
+    L.exc_last = st.last_exc;
     NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -367,6 +373,7 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.exc_count = st.exc_count;
     L.exc_cap = (unsigned)std::min<size_t>(npx, 0xffffffffu);
     L.exc_overflow = st.overflow;
+    L.exc_last = st.last_exc;
     NRM_CUDA(launch_node_field(L, 1, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -400,7 +407,9 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     L.cx = base;
     L.cy = base + na;
     L.cl = base + 2 * na;
-    L.cp = base + 7 * na;  // cj (int) follows cp: see launch_emdq_field
+    L.cp = base + 7 * na;  // phi, c32, j, supertile lists and plans follow: see launch_emdq_field
+    L.exact_count = state_of(c).emdq_exact;
+    NRM_CUDA(cudaMemsetAsync(L.exact_count, 0, sizeof(unsigned), c->stream));
     NRM_CUDA(launch_emdq_field(L, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -866,6 +875,17 @@ int nrm_selftest_peak(nrm_ctx* c, int which, double* ops_per_s) {
                             &ms, &c->launches));
     const double ops = (double)c->num_sms * 8 * 256 * (double)iters * 16 * 8;  // lane-ops
     *ops_per_s = ops / (ms * 1e-3);
+    return NRM_OK;
+}
+
+int nrm_ctx_exceptions(nrm_ctx* c, int64_t* blend_exceptions, int64_t* emdq_exact) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    DeviceGuard g(c->device);
+    unsigned v[2] = {0, 0};
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    NRM_CUDA(cudaMemcpy(v, state_of(c).last_exc, sizeof(v), cudaMemcpyDeviceToHost));
+    if (blend_exceptions) *blend_exceptions = v[0];
+    if (emdq_exact) *emdq_exact = v[1];
     return NRM_OK;
 }
 

@@ -63,44 +63,64 @@ __device__ __forceinline__ bool xunapply(const W5& q, double yx, double yy, doub
     return true;
 }
 
-// pixel_warp (mosaic.hpp:22-51), exact tier, over all n nodes in index order.
-// Returns 0 = ok, 1 = no support (nullopt), 2 = degenerate real part.
-__device__ inline int xpixel_warp(double x, double y, const double* __restrict__ anchors,
-                                  const double* __restrict__ warps, int n, double alpha, W5* out) {
-    double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
-    double ref_w = 0.0, ref_z = 0.0;
-    bool have_ref = false;
-    const double na = -alpha;
-    for (int i = 0; i < n; ++i) {
-        const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
-        const double w = xexp(xmul(na, d2));
-        if (w <= kPixelWeightCutoff) continue;
-        const double* q = &warps[5 * i];
-        double qw = __ldg(&q[1]), qz = __ldg(&q[2]), qdx = __ldg(&q[3]), qdy = __ldg(&q[4]);
-        if (!have_ref) {
-            ref_w = qw;
-            ref_z = qz;
-            have_ref = true;
-        } else if (xadd(xmul(qw, ref_w), xmul(qz, ref_z)) < 0.0) {
-            qw = -qw; qz = -qz; qdx = -qdx; qdy = -qdy;
-        }
-        aw = xadd(aw, xmul(w, qw));
-        az = xadd(az, xmul(w, qz));
-        adx = xadd(adx, xmul(w, qdx));
-        ady = xadd(ady, xmul(w, qdy));
-        as = xadd(as, xmul(w, __ldg(&q[0])));
-        wsum = xadd(wsum, w);
+// pixel_warp (mosaic.hpp:22-51), exact tier, as a running state so callers
+// can feed the nodes in index-ordered chunks (e.g. staged in shared memory).
+struct XPW {
+    double wsum, aw, az, adx, ady, as, ref_w, ref_z;
+    bool have_ref;
+};
+__device__ __forceinline__ void xpw_init(XPW& s) {
+    s.wsum = s.aw = s.az = s.adx = s.ady = s.as = s.ref_w = s.ref_z = 0.0;
+    s.have_ref = false;
+}
+// One node (anchor a, warp q = {scale, w, z, dx, dy}); na = -alpha.
+__device__ __forceinline__ void xpw_add(XPW& s, double x, double y, double ax, double ay, const double* q,
+                                        double na) {
+    const double d2 = xdist2(ax, ay, x, y);
+    const double w = xexp(xmul(na, d2));
+    if (w <= kPixelWeightCutoff) return;
+    double qw = q[1], qz = q[2], qdx = q[3], qdy = q[4];
+    if (!s.have_ref) {
+        s.ref_w = qw;
+        s.ref_z = qz;
+        s.have_ref = true;
+    } else if (xadd(xmul(qw, s.ref_w), xmul(qz, s.ref_z)) < 0.0) {
+        qw = -qw; qz = -qz; qdx = -qdx; qdy = -qdy;
     }
-    if (!have_ref) return 1;
-    const double mw = aw / wsum, mz = az / wsum, mdx = adx / wsum, mdy = ady / wsum;
+    s.aw = xadd(s.aw, xmul(w, qw));
+    s.az = xadd(s.az, xmul(w, qz));
+    s.adx = xadd(s.adx, xmul(w, qdx));
+    s.ady = xadd(s.ady, xmul(w, qdy));
+    s.as = xadd(s.as, xmul(w, q[0]));
+    s.wsum = xadd(s.wsum, w);
+}
+// Returns 0 = ok, 1 = no support (nullopt), 2 = degenerate real part.
+__device__ __forceinline__ int xpw_finish(const XPW& s, W5* out) {
+    if (!s.have_ref) return 1;
+    const double mw = s.aw / s.wsum, mz = s.az / s.wsum, mdx = s.adx / s.wsum, mdy = s.ady / s.wsum;
     const double nrm = xhypot(mw, mz);
     if (nrm < 1e-300) return 2;
-    out->s = as / wsum;
+    out->s = s.as / s.wsum;
     out->w = mw / nrm;
     out->z = mz / nrm;
     out->dx = mdx / nrm;
     out->dy = mdy / nrm;
     return 0;
+}
+
+// pixel_warp over all n nodes in index order, straight from global memory.
+__device__ inline int xpixel_warp(double x, double y, const double* __restrict__ anchors,
+                                  const double* __restrict__ warps, int n, double alpha, W5* out) {
+    XPW s;
+    xpw_init(s);
+    const double na = -alpha;
+    for (int i = 0; i < n; ++i) {
+        double q[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) q[k] = __ldg(&warps[5 * i + k]);
+        xpw_add(s, x, y, __ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), q, na);
+    }
+    return xpw_finish(s, out);
 }
 
 // One texel of an ImageU8 (image.hpp:21-43) as RGB; grey is replicated

@@ -104,6 +104,7 @@ struct NodeFieldLaunch {
     unsigned* exc_count = nullptr;
     unsigned exc_cap = 0;
     unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
+    unsigned* exc_last = nullptr;      // pixels the last exception pass resolved (diagnostics)
 };
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
@@ -133,6 +134,7 @@ struct EmdqLaunch {
     int support = 16;
     float2* disp = nullptr;
     float* unc = nullptr;
+    unsigned* exact_count = nullptr;  // pixels that took the exact tier (diagnostics, accumulated)
     // scratch: gathered candidates (SoA, nactive each)
     double* cx = nullptr;
     double* cy = nullptr;

@@ -88,6 +88,13 @@ class Context:
         check(self._lib.nrm_ctx_launch_count(self._h, C.byref(v)))
         return v.value
 
+    def exceptions(self):
+        """(blend/node-field pixels resolved by the last exception pass, EMDQ
+        pixels of the last emdq_field that took the exact tier)."""
+        a, b = C.c_int64(), C.c_int64()
+        check(self._lib.nrm_ctx_exceptions(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def peak(self, which: str = "fp32") -> float:
         """Measured lane-ops/s of the FP32 FFMA ("fp32") or MUFU.EX2 ("mufu") pipe."""
         v = C.c_double()
