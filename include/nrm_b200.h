@@ -178,6 +178,23 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
                           const int32_t *d_active, int nactive, double alpha, int support,
                           double beta, float *d_disp, float *d_unc);
 
+/* ---- pure host planning (no CUDA device needed) --------------------------
+ * The host-side bookkeeping the entry points above perform, exposed for
+ * testing and for multi-GPU orchestration. */
+/* Canvas::ensure_contains (mosaic.hpp:131-174): logical canvas after growth. */
+int nrm_plan_ensure_contains(int64_t origin_x, int64_t origin_y, int width, int height, double x0,
+                             double y0, double x1, double y1, int64_t *new_origin_x,
+                             int64_t *new_origin_y, int *new_width, int *new_height);
+/* blend_frame's pixel window (mosaic.hpp:203-213) on a canvas whose origin
+ * (after ensure_contains) is (origin_x, origin_y): inclusive canvas-pixel
+ * bbox {px0, py0, px1, py1} of polygon_bbox(poly).expanded(4) and its pixel
+ * count (BlendStats::footprint_pixels). */
+int nrm_plan_footprint(const double *poly, int npoly, int64_t origin_x, int64_t origin_y,
+                       int64_t *bbox4, int64_t *footprint);
+/* 1 if absolute reference row `abs_row` belongs to band `rank` of `count`
+ * (block-cyclic 64-row stripes, nrm_canvas_set_band). */
+int nrm_band_owns_row(int64_t abs_row, int rank, int count);
+
 /* ---- diagnostics ---------------------------------------------------------
  * Evaluates the exact tier's exp / hypot emulation (nrm_libm.cuh) on the
  * device so tests can check it bit-for-bit against the host libm. */

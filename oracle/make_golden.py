@@ -100,6 +100,17 @@ def main():
                         valid=np.array(valid), alpha=alpha0, **pw)
     print("pixel_warp:", int(np.sum(valid)), "of", len(pts), "supported")
 
+    # ---- node lattices (insert_nodes, slam.hpp:270-360) ---------------------
+    rects = [((0, 0, 320, 200), 60.0), ((0, 0, 64, 48), 20.0), ((0, 0, 48, 32), 16.0), ((0, 0, 256, 64), 30.0),
+             ((0, 0, 640, 480), 60.0 * 1.5555555555555556), ((0, 0, 1920, 1080), 240.0),
+             ((0, 0, 3840, 2160), 480.0), ((-500, -300, 900, 700), 75.0)]
+    lat = {}
+    for k, (r, sp) in enumerate(rects):
+        lat[f"rect{k}"] = np.array(r, float)
+        lat[f"spacing{k}"] = sp
+        lat[f"anchors{k}"] = R.rect_lattice(r, sp)
+    np.savez_compressed(OUT / "lattice.npz", n=len(rects), **lat)
+
     # ---- invert_frame_boundary (mosaic.hpp:58-96) --------------------------
     poly = R.invert_frame_boundary(320, 200, anchors, warps, alpha0)
     np.savez_compressed(OUT / "invert_boundary.npz", anchors=anchors, warps=warps, poly=poly, alpha=alpha0,

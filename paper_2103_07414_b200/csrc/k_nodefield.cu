@@ -33,7 +33,6 @@ namespace {
 
 constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
 constexpr int EXC_THREADS = 1024;
-constexpr int EXC_CHUNK = 384;  // nodes staged per chunk in the exception pass (21 KB)
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
 constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 constexpr double kBoundMargin = 4e-3;
@@ -430,34 +429,71 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
 // Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics), one
 // CTA. It then writes BlendStats (footprint + partial sums) and restores the
 // per-context state (acc = 0, exc_count = 0) for the next call.
+// Warp-cooperative pixel_warp (mosaic.hpp:22-51) for one pixel: lanes
+// evaluate the node weights in parallel (exact tier), then every lane sums the
+// contributors' products in ascending node order -- the reference's order, so
+// the result is bit-identical -- with shuffles. All lanes end with the result.
+__device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ anchors,
+                                const double* __restrict__ warps, int n, double alpha, W5* out) {
+    const int lane = threadIdx.x & 31;
+    const double na = -alpha;
+    double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
+    double ref_w = 0.0, ref_z = 0.0;
+    bool have_ref = false;
+    for (int c0 = 0; c0 < n; c0 += 32) {
+        const int i = c0 + lane;
+        double w = 0.0, q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        bool contrib = false;
+        if (i < n) {
+            const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
+            w = xexp(xmul(na, d2));
+            contrib = !(w <= kPixelWeightCutoff);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) q[k] = __ldg(&warps[5 * i + k]);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, contrib);
+        if (!m) continue;
+        if (!have_ref) {  // first contributing node in index order
+            const int src = __ffs(m) - 1;
+            ref_w = __shfl_sync(0xffffffffu, q[1], src);
+            ref_z = __shfl_sync(0xffffffffu, q[2], src);
+            have_ref = true;
+            if (lane != src && xadd(xmul(q[1], ref_w), xmul(q[2], ref_z)) < 0.0) {
+                q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; q[4] = -q[4];
+            }
+        } else if (xadd(xmul(q[1], ref_w), xmul(q[2], ref_z)) < 0.0) {
+            q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; q[4] = -q[4];
+        }
+        const double p0 = xmul(w, q[1]), p1 = xmul(w, q[2]), p2 = xmul(w, q[3]), p3 = xmul(w, q[4]);
+        const double p4 = xmul(w, q[0]);
+        for (unsigned mm = m; mm; mm &= mm - 1) {
+            const int j = __ffs(mm) - 1;
+            aw = xadd(aw, __shfl_sync(0xffffffffu, p0, j));
+            az = xadd(az, __shfl_sync(0xffffffffu, p1, j));
+            adx = xadd(adx, __shfl_sync(0xffffffffu, p2, j));
+            ady = xadd(ady, __shfl_sync(0xffffffffu, p3, j));
+            as = xadd(as, __shfl_sync(0xffffffffu, p4, j));
+            wsum = xadd(wsum, __shfl_sync(0xffffffffu, w, j));
+        }
+    }
+    XPW s{wsum, aw, az, adx, ady, as, ref_w, ref_z, have_ref};
+    return xpw_finish(s, out);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
-    __shared__ double sa[2 * EXC_CHUNK], sq[5 * EXC_CHUNK];
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int nb = 0, nns = 0, noof = 0;
-    const double fxm = L.fw - 1.0, fym = L.fh - 1.0, na = -L.alpha;
-    // batches of EXC_THREADS pixels; nodes streamed through shared memory in
-    // index order (the reference's summation order), one chunk at a time
-    for (unsigned q0 = 0; q0 < cnt; q0 += EXC_THREADS) {
-        const unsigned q = q0 + threadIdx.x;
-        const bool act = q < cnt;
-        const int2 p = act ? L.exc[q] : make_int2(0, 0);
+    const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
+    // one warp per queued pixel
+    for (unsigned q = wid; q < cnt; q += EXC_THREADS / 32) {
+        const int2 p = L.exc[q];
         const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
-        XPW st;
-        xpw_init(st);
-        for (int c0 = 0; c0 < L.n; c0 += EXC_CHUNK) {
-            const int cn = min(EXC_CHUNK, L.n - c0);
-            __syncthreads();
-            for (int k = threadIdx.x; k < 2 * cn; k += EXC_THREADS) sa[k] = L.anchors[2 * c0 + k];
-            for (int k = threadIdx.x; k < 5 * cn; k += EXC_THREADS) sq[k] = L.warps[5 * c0 + k];
-            __syncthreads();
-            if (act)
-                for (int i = 0; i < cn; ++i) xpw_add(st, x, y, sa[2 * i], sa[2 * i + 1], &sq[5 * i], na);
-        }
-        if (!act) continue;
         W5 wp;
-        const int rc = xpw_finish(st, &wp);
+        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, L.n, L.alpha, &wp);
+        if (lane != 0) continue;
         if (MODE == 1) {
             const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
             if (rc == 0) {

@@ -174,28 +174,47 @@ bool covers(const nrm_canvas* cv, int64_t x0, int64_t y0, int64_t x1, int64_t y1
            y1 <= cv->phys_y0 + cv->cap_h;
 }
 
-// Canvas::ensure_contains (mosaic.hpp:131-174), same integer bookkeeping.
-int ensure_contains(nrm_canvas* cv, double rx0, double ry0, double rx1, double ry1) {
+// Canvas::ensure_contains (mosaic.hpp:131-174) bookkeeping as a pure host
+// function: the logical canvas (ox, oy, w, h) after growing to contain the
+// rectangle. Returns NRM_OK; *grew = 0 when the canvas already contains it.
+int plan_ensure_contains(int64_t ox, int64_t oy, int w, int h, double rx0, double ry0, double rx1, double ry1,
+                         int64_t* nox, int64_t* noy, int64_t* nw, int64_t* nh, int* grew) {
     if (!(std::isfinite(rx0) && std::isfinite(ry0) && std::isfinite(rx1) && std::isfinite(ry1)))
         return fail(NRM_EINVAL, "ensure_contains: non-finite rectangle");
     if (std::fabs(rx0) > 1e9 || std::fabs(ry0) > 1e9 || std::fabs(rx1) > 1e9 || std::fabs(ry1) > 1e9)
         return fail(NRM_EINVAL, "ensure_contains: rectangle out of range");
     const int64_t nx0n = (int64_t)std::floor(rx0), ny0n = (int64_t)std::floor(ry0);
     const int64_t nx1n = (int64_t)std::ceil(rx1) + 1, ny1n = (int64_t)std::ceil(ry1) + 1;
-    const bool empty = cv->width == 0;
-    if (!empty && nx0n >= cv->origin_x && ny0n >= cv->origin_y && nx1n <= cv->origin_x + cv->width &&
-        ny1n <= cv->origin_y + cv->height)
-        return NRM_OK;
+    const bool empty = w == 0;
+    *nox = ox;
+    *noy = oy;
+    *nw = w;
+    *nh = h;
+    *grew = 0;
+    if (!empty && nx0n >= ox && ny0n >= oy && nx1n <= ox + w && ny1n <= oy + h) return NRM_OK;
     int64_t nx0 = align_down(nx0n), ny0 = align_down(ny0n);
     int64_t nx1 = nx1n, ny1 = ny1n;
     if (!empty) {
-        nx0 = std::min(nx0, cv->origin_x);
-        ny0 = std::min(ny0, cv->origin_y);
-        nx1 = std::max(nx1, cv->origin_x + cv->width);
-        ny1 = std::max(ny1, cv->origin_y + cv->height);
+        nx0 = std::min(nx0, ox);
+        ny0 = std::min(ny0, oy);
+        nx1 = std::max(nx1, ox + (int64_t)w);
+        ny1 = std::max(ny1, oy + (int64_t)h);
     }
-    const int64_t nw = ((nx1 - nx0 + kTile64 - 1) / kTile64) * kTile64;
-    const int64_t nh = ((ny1 - ny0 + kTile64 - 1) / kTile64) * kTile64;
+    *nox = nx0;
+    *noy = ny0;
+    *nw = ((nx1 - nx0 + kTile64 - 1) / kTile64) * kTile64;
+    *nh = ((ny1 - ny0 + kTile64 - 1) / kTile64) * kTile64;
+    if (*nw > (1 << 30) || *nh > (1 << 30)) return fail(NRM_EINVAL, "ensure_contains: canvas too large");
+    *grew = 1;
+    return NRM_OK;
+}
+
+int ensure_contains(nrm_canvas* cv, double rx0, double ry0, double rx1, double ry1) {
+    int64_t nx0, ny0, nw, nh;
+    int grew = 0;
+    NRM_CHECK(plan_ensure_contains(cv->origin_x, cv->origin_y, cv->width, cv->height, rx0, ry0, rx1, ry1, &nx0, &ny0,
+                                   &nw, &nh, &grew));
+    if (!grew) return NRM_OK;
     if (!covers(cv, nx0, ny0, nx0 + nw, ny0 + nh)) {
         int64_t px0 = nx0, py0 = ny0, px1 = nx0 + nw, py1 = ny0 + nh;
         if (cv->res_x1 > cv->res_x0) {
@@ -876,6 +895,49 @@ int nrm_selftest_peak(nrm_ctx* c, int which, double* ops_per_s) {
     const double ops = (double)c->num_sms * 8 * 256 * (double)iters * 16 * 8;  // lane-ops
     *ops_per_s = ops / (ms * 1e-3);
     return NRM_OK;
+}
+
+// ---- pure host planning (no device needed) --------------------------------
+int nrm_plan_ensure_contains(int64_t ox, int64_t oy, int w, int h, double x0, double y0, double x1, double y1,
+                             int64_t* new_ox, int64_t* new_oy, int* new_w, int* new_h) {
+    if (!new_ox || !new_oy || !new_w || !new_h) return fail(NRM_EINVAL, "null output");
+    if (w < 0 || h < 0) return fail(NRM_EINVAL, "negative canvas size");
+    int64_t a, b, c2, d;
+    int grew;
+    NRM_CHECK(plan_ensure_contains(ox, oy, w, h, x0, y0, x1, y1, &a, &b, &c2, &d, &grew));
+    *new_ox = a;
+    *new_oy = b;
+    *new_w = (int)c2;
+    *new_h = (int)d;
+    return NRM_OK;
+}
+
+int nrm_plan_footprint(const double* poly, int npoly, int64_t origin_x, int64_t origin_y, int64_t* bbox4,
+                       int64_t* footprint) {
+    if (!bbox4 || !footprint) return fail(NRM_EINVAL, "null output");
+    bbox4[0] = bbox4[1] = 0;
+    bbox4[2] = bbox4[3] = -1;
+    *footprint = 0;
+    if (npoly < 3) return NRM_OK;
+    if (!poly || !finite_all(poly, (size_t)npoly * 2)) return fail(NRM_EINVAL, "bad polygon");
+    const Bbox bb = footprint_bbox(poly, npoly);
+    const double orgx = (double)origin_x, orgy = (double)origin_y;  // mosaic.hpp:206-213
+    bbox4[0] = (int64_t)std::floor(bb.x0 - orgx);
+    bbox4[1] = (int64_t)std::floor(bb.y0 - orgy);
+    bbox4[2] = (int64_t)std::ceil(bb.x1 - orgx);
+    bbox4[3] = (int64_t)std::ceil(bb.y1 - orgy);
+    const int64_t bw = bbox4[2] - bbox4[0] + 1, bh = bbox4[3] - bbox4[1] + 1;
+    *footprint = bw > 0 && bh > 0 ? bw * bh : 0;
+    return NRM_OK;
+}
+
+int nrm_band_owns_row(int64_t abs_row, int rank, int count) {
+    if (count <= 1) return 1;
+    int64_t s = abs_row / kStripeRows;
+    if (abs_row % kStripeRows != 0 && abs_row < 0) --s;
+    int64_t m = s % count;
+    if (m < 0) m += count;
+    return m == rank;
 }
 
 int nrm_ctx_exceptions(nrm_ctx* c, int64_t* blend_exceptions, int64_t* emdq_exact) {

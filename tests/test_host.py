@@ -1,0 +1,101 @@
+"""CPU: the C ABI library loads and exports every declared symbol; its
+pure-host planning (canvas growth, footprint window, band ownership) matches
+the reference's bookkeeping (via the oracle); the product fails loudly
+without a GPU; the synthetic workload reproduces the reference's lattices."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2103_07414_b200 import _lib
+    return _lib.load()
+
+
+def header_symbols():
+    text = (ROOT / "include" / "nrm_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return set(re.findall(r"\b(nrm_[a-z0-9_]+)\s*\(", text))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2103_07414_b200 import _lib
+    syms = header_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert syms == {name for name, _, _ in _lib.SIGNATURES}
+    assert lib.nrm_abi_version() == 1
+
+
+def test_no_gpu_fails_loudly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = C.c_void_p()
+    rc = lib.nrm_ctx_create(0, C.byref(h))
+    assert rc != 0 and not h.value
+    assert lib.nrm_last_error()
+
+
+def plan(lib, ox, oy, w, h, rect):
+    a, b, c, d = C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+    assert lib.nrm_plan_ensure_contains(ox, oy, w, h, *map(float, rect), C.byref(a), C.byref(b), C.byref(c),
+                                        C.byref(d)) == 0
+    return a.value, b.value, c.value, d.value
+
+
+def test_ensure_contains_bookkeeping_matches_reference(lib, oracle):
+    rng = np.random.default_rng(1)
+    for _ in range(150):
+        cv = oracle.canvas()
+        state = (0, 0, 0, 0)
+        for _ in range(4):
+            x0, y0 = rng.uniform(-700, 700, 2)
+            rect = (x0, y0, x0 + rng.uniform(0, 400), y0 + rng.uniform(0, 400))
+            cv.ensure_contains(rect)
+            state = plan(lib, *state, rect)
+            assert state == tuple(cv.info())
+
+
+def test_footprint_window_matches_reference(lib, oracle, golden):
+    for case in ["first_frame", "deformed", "c1", "gray_rotated"]:
+        g = golden(f"blend_{case}")
+        poly = np.ascontiguousarray(g["polys"][: g["npoly"][0]])
+        ox, oy = int(g["canvas_info"][0]), int(g["canvas_info"][1])
+        bb = (C.c_int64 * 4)()
+        fp = C.c_int64()
+        assert lib.nrm_plan_footprint(poly.ctypes.data, len(poly), ox, oy, bb, C.byref(fp)) == 0
+        assert fp.value == g["stats"][0][0]
+
+
+def test_band_ownership_partitions_rows(lib):
+    for count in (1, 2, 3, 4, 8):
+        rows = np.arange(-700, 1500)
+        owners = np.array([[lib.nrm_band_owns_row(int(r), k, count) for k in range(count)] for r in rows])
+        assert (owners.sum(1) == 1).all()          # every row has exactly one owner
+        stripe = np.floor_divide(rows, 64)
+        assert (owners.argmax(1) == np.mod(stripe, count)).all()
+
+
+def test_hex_lattice_matches_reference(golden):
+    from paper_2103_07414_b200 import workload as W
+    g = golden("lattice")
+    for k in range(int(g["n"])):
+        got = W.hex_lattice(tuple(g[f"rect{k}"]), float(g[f"spacing{k}"]))
+        assert np.array_equal(got, g[f"anchors{k}"]), k
+
+
+def test_scaled_params_match_config():
+    """resolve_scaled_params (config.hpp:144-157) for the BASELINE configs."""
+    from paper_2103_07414_b200 import workload as W
+    p = W.scaled_params(1920, 1080)
+    assert p.s == 4.0 and abs(p.alpha - 1.25e-5) < 1e-18 and p.hex_spacing == 240.0
+    p = W.scaled_params(640, 480)
+    assert abs(p.s - 1.5555555555555556) < 1e-15

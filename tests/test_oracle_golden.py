@@ -1,0 +1,145 @@
+"""CPU: the C restatement (oracle/) must reproduce the reference's golden
+vectors (tests/golden, produced by the real reference via oracle/_ref and
+oracle/make_golden.py) bit for bit. This pins the oracle the GPU parity
+tests compare against."""
+import hashlib
+
+import numpy as np
+import pytest
+
+BLEND_CASES = ["first_frame", "repeated_constant", "translated", "deformed", "weight_cap", "gray_rotated",
+               "c1", "c1_seq"]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def split_polys(g):
+    out, o = [], 0
+    for n in g["npoly"]:
+        out.append(g["polys"][o:o + n])
+        o += n
+    return out
+
+
+def test_pixel_warp_known_answers(oracle, golden):
+    g = golden("pixel_warp")
+    # test_mosaic.cpp:39-49 SingleNodeDominates
+    w = oracle.pixel_warp(100, 100, g["single_anchors"], g["single_warps"], 2e-4)
+    assert w[0] == 1.5
+    assert np.array_equal(w, g["single_out"])
+    got = oracle.warp_apply(w, 7, 9)
+    want = oracle.warp_apply(g["single_warps"][0], 7, 9)
+    assert np.abs(got - want).max() < 1e-12
+    # test_mosaic.cpp:67-76 MidpointOfTwoTranslationsAverages
+    a = np.array([[100.0, 100.0], [140.0, 100.0]])
+    q = np.array([[1.0, 1.0, 0.0, 0.0, 0.0], [1.0, 1.0, 0.0, 1.0, 0.0]])
+    w = oracle.pixel_warp(120, 100, a, q, 2e-4)
+    assert np.abs(oracle.warp_apply(w, 120, 100) - [121.0, 100.0]).max() < 1e-12
+    # test_mosaic.cpp:78-82 NoSupportFarFromNodes
+    assert oracle.pixel_warp(1e4, 1e4, np.array([[0.0, 0.0]]), np.array([[1.0, 1, 0, 0, 0]]), 2e-4) is None
+
+
+def test_pixel_warp_matches_reference_bitwise(oracle, golden):
+    g = golden("pixel_warp")
+    for (x, y), want, ok in zip(g["points"], g["out"], g["valid"]):
+        got = oracle.pixel_warp(x, y, g["anchors"], g["warps"], float(g["alpha"]))
+        assert (got is not None) == bool(ok)
+        if ok:
+            assert np.array_equal(got, want)
+
+
+def test_invert_frame_boundary_matches_reference_bitwise(oracle, golden):
+    g = golden("invert_boundary")
+    poly = oracle.invert_frame_boundary(int(g["fw"]), int(g["fh"]), g["anchors"], g["warps"], float(g["alpha"]))
+    assert np.array_equal(poly, g["poly"])
+
+
+@pytest.mark.parametrize("case", BLEND_CASES)
+def test_blend_frame_matches_reference_bitwise(oracle, golden, case):
+    g = golden(f"blend_{case}")
+    cv = oracle.canvas()
+    for k, poly in enumerate(split_polys(g)):
+        st = oracle.blend_frame(cv, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly)
+        assert st == tuple(g["stats"][k])
+    assert tuple(cv.info()) == tuple(g["canvas_info"])
+    col, wt = cv.arrays()
+    assert sha(col) == str(g["color_sha"])
+    assert sha(wt) == str(g["weight_sha"])
+    img, org = oracle.render(cv, crop=True)
+    assert sha(img) == str(g["render_crop_sha"])
+    assert org == tuple(g["crop_origin"])
+    full, _ = oracle.render(cv, crop=False)
+    assert sha(full) == str(g["render_full_sha"])
+
+
+def test_blend_frame_reference_test_semantics(oracle, golden):
+    """The reference's own BlendFrame assertions (test_mosaic.cpp:84-224)."""
+    g = golden("blend_first_frame")
+    assert tuple(g["stats"][0])[1] == 320 * 200                      # FirstFrameInsertsExactly
+    img = g["render_crop"]
+    assert img.shape == (200, 320, 4) and np.array_equal(img[..., :3], g["frame"])
+    g = golden("blend_repeated_constant")                             # capped weight 30
+    assert int(g["weight"].max()) == 30
+    g = golden("blend_weight_cap")
+    assert int(g["weight"].max()) <= 30
+    g = golden("blend_translated")                                    # overlap weight 2
+    assert int(g["weight"].max()) == 2 and g["render_crop"].shape[1] == 256 + 100
+
+
+def test_empty_inputs_give_empty_stats(oracle):
+    cv = oracle.canvas()
+    a = np.array([[0.0, 0.0]])
+    q = np.array([[1.0, 1, 0, 0, 0]])
+    assert oracle.blend_frame(cv, np.zeros((0, 0, 3), np.uint8), a, q, 2e-4, [[0, 0], [1, 0], [1, 1]]) == (0, 0, 0, 0)
+    assert oracle.blend_frame(cv, np.zeros((8, 8, 3), np.uint8), a, q, 2e-4, [[0, 0], [1, 0]]) == (0, 0, 0, 0)
+    assert cv.info()[2] == 0  # canvas untouched (mosaic.hpp:201)
+    img, _ = oracle.render(cv, crop=True)
+    assert img.shape[:2] == (0, 0)
+
+
+def test_node_uncertainty_known_answers(oracle):
+    """test_fieldest.cpp:184-214."""
+    assert oracle.node_uncertainty(100, 100, [[100, 100]], 3e-3) == 1.0
+    assert abs(oracle.node_uncertainty(100, 100, [[110, 100]], 3e-3) - 1.3498588075760032) < 1e-12
+    assert oracle.node_uncertainty(100, 100, [[105, 100], [150, 100]], 3e-3) == np.exp(3e-3 * 25.0)
+    assert np.isnan(oracle.node_uncertainty(0, 0, np.zeros((0, 2)), 3e-3))
+    prev = 0.0
+    for d in range(0, 401, 20):
+        u = oracle.node_uncertainty(d, 0, [[0, 0]], 3e-3)
+        assert u >= prev and u >= 1.0
+        prev = u
+
+
+def test_emdq_points_match_reference_bitwise(oracle, golden):
+    g = golden("emdq_c1")
+    for (x, y), want, wu in zip(g["qpts"], g["qout"], g["qunc"]):
+        got = oracle.blend_local(g["locals"], g["apts"], g["probs"], g["active"], x, y, float(g["alpha"]))
+        assert np.array_equal(got, want)
+        assert oracle.node_uncertainty(x, y, g["apts"][g["active"]], float(g["beta"])) == wu
+    # node increments of the reference's estimate_field = blend_local at the anchors
+    for a, inc in zip(g["node_anchors"], g["node_inc"]):
+        got = oracle.blend_local(g["locals"], g["apts"], g["probs"], g["active"], a[0], a[1], float(g["alpha"]))
+        assert np.array_equal(got, inc)
+
+
+def test_emdq_grid_matches_reference(oracle, golden):
+    g = golden("emdq_c1")
+    x0, y0, w, h = g["grid"]
+    disp, unc = oracle.emdq_field_grid((x0, y0, int(w), int(h)), g["apts"], g["locals"], g["probs"], g["active"],
+                                       float(g["alpha"]), float(g["beta"]))
+    assert sha(disp) == str(g["disp_sha"])
+    assert sha(unc) == str(g["unc_sha"])
+
+
+def test_emdq_edge_cases_match_reference(oracle, golden):
+    g = golden("emdq_edge")
+    x0, y0, w, h = g["grid"]
+    grid = (x0, y0, int(w), int(h))
+    d, u = oracle.emdq_field_grid(grid, g["apts"], g["locals"], g["probs"], g["small_active"], float(g["alpha"]),
+                                  float(g["beta"]))
+    assert np.array_equal(d, g["disp_small"]) and np.array_equal(u, g["unc_small"])
+    d, u = oracle.emdq_field_grid(grid, g["apts"], g["locals"], g["probs"], g["active"], float(g["alpha"]),
+                                  float(g["beta"]), support=4)
+    assert np.array_equal(d, g["disp_s4"]) and np.array_equal(u, g["unc_s4"])
