@@ -32,7 +32,8 @@ namespace nrm {
 namespace {
 
 constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
-constexpr int EXC_THREADS = 1024;
+constexpr int EXC_THREADS = 128;
+constexpr int EXC_BLOCKS = 148;
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
 constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 constexpr double kBoundMargin = 4e-3;
@@ -483,12 +484,14 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
 template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
+    __shared__ bool last;
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + wid, nwarps = gridDim.x * (EXC_THREADS / 32);
     int nb = 0, nns = 0, noof = 0;
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
-    // one warp per queued pixel
-    for (unsigned q = wid; q < cnt; q += EXC_THREADS / 32) {
+    // one warp per queued pixel, spread over the whole GPU
+    for (unsigned q = gw; q < cnt; q += nwarps) {
         const int2 p = L.exc[q];
         const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
         W5 wp;
@@ -534,27 +537,39 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         nns += __shfl_xor_sync(0xffffffffu, nns, o);
         noof += __shfl_xor_sync(0xffffffffu, noof, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = nb;
-        red[1][threadIdx.x >> 5] = nns;
-        red[2][threadIdx.x >> 5] = noof;
+    if (lane == 0) {
+        red[0][wid] = nb;
+        red[1][wid] = nns;
+        red[2][wid] = noof;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        if (MODE == 0) {
-            unsigned long long tot[3] = {0, 0, 0};
+        unsigned long long tot[3] = {0, 0, 0};
+        for (int k = 0; k < 3; ++k)
+            for (int w = 0; w < EXC_THREADS / 32; ++w) tot[k] += (unsigned long long)red[k][w];
+        if (MODE == 0)
             for (int k = 0; k < 3; ++k)
-                for (int w = 0; w < EXC_THREADS / 32; ++w) tot[k] += (unsigned long long)red[k][w];
+                if (tot[k]) atomicAdd(&L.acc[k], tot[k]);
+        __threadfence();
+        last = atomicAdd(L.exc_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    // the last CTA finalises BlendStats and restores the per-context state
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        if (MODE == 0) {
+            volatile unsigned long long* acc = L.acc;
             if (L.stats_out) {
                 L.stats_out[0] = L.footprint;
-                L.stats_out[1] = L.acc[0] + tot[0];
-                L.stats_out[2] = L.acc[1] + tot[1];
-                L.stats_out[3] = L.acc[2] + tot[2];
+                L.stats_out[1] = acc[0];
+                L.stats_out[2] = acc[1];
+                L.stats_out[3] = acc[2];
             }
-            L.acc[0] = L.acc[1] = L.acc[2] = 0;
+            acc[0] = acc[1] = acc[2] = 0;
         }
         if (L.exc_last) *L.exc_last = cnt;
         *L.exc_count = 0;
+        *L.exc_done = 0;
     }
 }
 
@@ -667,9 +682,9 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
         if (e != cudaSuccess) return e;
     }
     if (mode == 0)
-        k_node_exceptions<0><<<1, EXC_THREADS, 0, st>>>(L);
+        k_node_exceptions<0><<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
     else
-        k_node_exceptions<1><<<1, EXC_THREADS, 0, st>>>(L);
+        k_node_exceptions<1><<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
     ++*launches;
     return cudaGetLastError();
 }

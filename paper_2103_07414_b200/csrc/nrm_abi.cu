@@ -259,12 +259,13 @@ struct State {
     unsigned* overflow;
     unsigned* last_exc;
     unsigned* emdq_exact;
+    unsigned* exc_done;
 };
 State state_of(nrm_ctx* c) {
     char* b = c->misc.as<char>();
     return {reinterpret_cast<unsigned long long*>(b), reinterpret_cast<unsigned*>(b + 24),
             reinterpret_cast<unsigned*>(b + 28), reinterpret_cast<unsigned*>(b + 32),
-            reinterpret_cast<unsigned*>(b + 36)};
+            reinterpret_cast<unsigned*>(b + 36), reinterpret_cast<unsigned*>(b + 40)};
 }
 
 // Shared core of blend_frame: everything after the inputs are in HBM.
@@ -326,6 +327,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.exc_cap = (unsigned)exc_cap;
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
+    L.exc_done = st.exc_done;
     NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -393,6 +395,7 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.exc_cap = (unsigned)std::min<size_t>(npx, 0xffffffffu);
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
+    L.exc_done = st.exc_done;
     NRM_CUDA(launch_node_field(L, 1, c->stream, &c->launches));
     return NRM_OK;
 }

@@ -105,6 +105,7 @@ struct NodeFieldLaunch {
     unsigned exc_cap = 0;
     unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
     unsigned* exc_last = nullptr;      // pixels the last exception pass resolved (diagnostics)
+    unsigned* exc_done = nullptr;      // finished exception CTAs (persistent-zero)
 };
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
