@@ -77,6 +77,7 @@ constexpr int TREC = 64;          // staged records per tile (in + ambiguous)
 constexpr int TCAND = 128;        // tile candidates before classification
 constexpr int PLAN_WARPS = 8;     // planning warps (tiles) per CTA
 constexpr int TFLAG_EXACT_SUPER = 1, TFLAG_EXACT_STAGED = 2;
+constexpr int NEAR_CAP = 8;       // per sub-tile: candidates that can be the nearest
 
 // Per-tile plan written by k_plan, read by k_pixels (one 16 x 16 tile).
 struct __align__(16) TileHdr {
@@ -84,6 +85,7 @@ struct __align__(16) TileHdr {
     float d2ref, d2top;             // tile-wide d^2 floor / ceiling of the staged points
     int nin, ne, flags, pad;
     unsigned char nx[NW], na[NW];   // per sub-tile: extra sure members, ambiguous
+    unsigned char nn[NW];           // per sub-tile: possible-nearest list size (255: scan all)
 };
 
 struct TilePlans {
@@ -92,6 +94,7 @@ struct TilePlans {
     float4* rec1;          // [ntiles][TREC]  conjugated dual quaternion
     int* sidx;             // [ntiles][TREC]  candidate indices (exact-tier fallback)
     unsigned char* sub;    // [ntiles][NW][TREC]  per sub-tile: extra sure, then ambiguous
+    unsigned char* near;   // [ntiles][NW][NEAR_CAP]  per sub-tile: possible nearest points
     int tx0, ty0, ntx;     // chunk: first tile column/row, tiles per row
 };
 
@@ -112,8 +115,10 @@ struct PlanWarp {
 // Pixel-kernel shared memory (one tile).
 struct PixSmem {
     float4 rec0[TREC], rec1[TREC];
+    float ex[TREC][ET], ey[TREC][ET];  // separable weights: w = ex[k][col] * ey[k][row]
     int sidx[TREC];
     unsigned char sub[NW][TREC];
+    unsigned char near[NW][NEAR_CAP];
 };
 struct SSmem {
     int hist[256];
@@ -579,11 +584,12 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
 
     // 6. per sub-tile refinement of the tile-ambiguous (FP32, conservative margins)
     unsigned char* subg = TP.sub + (size_t)g * NW * TREC;
-    int my_nx = 0, my_na = 0;  // lane st < NW keeps sub-tile st's counts
+    unsigned char* nearg = TP.near + (size_t)g * NW * NEAR_CAP;
+    int my_nx = 0, my_na = 0, my_nn = 0;  // lane st < NW keeps sub-tile st's counts
     for (int st = 0; st < NW; ++st) {
         const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
         const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
-        int nx = 0, nw = 0;
+        int nx = 0, nw = 0, nn = 0;
         if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
             for (int k = lane; k < ne; k += 32) {
                 const float ax = w.ux[k], ay = w.uy[k];
@@ -592,6 +598,21 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
                 w.wd[k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
             }
             __syncwarp();
+            // points that can be the nearest somewhere in the sub-tile
+            float thr = FLT_MAX;
+            for (int k = lane; k < ne; k += 32) thr = fminf(thr, w.wd[k].y);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) thr = fminf(thr, __shfl_xor_sync(0xffffffffu, thr, d));
+            thr = thr * (1.f + 1e-5f) + 1e-2f;
+            for (int base = 0; base < ne; base += 32) {
+                const int k = base + lane;
+                const bool cand = k < ne && w.wd[k].x <= thr;
+                const unsigned mn = __ballot_sync(0xffffffffu, cand);
+                const int pos = nn + __popc(mn & ((1u << lane) - 1u));
+                if (cand && pos < NEAR_CAP) nearg[st * NEAR_CAP + pos] = (unsigned char)k;
+                nn += __popc(mn);
+            }
+            if (nn > NEAR_CAP) nn = 255;
             for (int base = ni; base < ne; base += 32) {
                 const int k = base + lane;
                 int c = 0;
@@ -626,11 +647,13 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
         if (lane == st) {
             my_nx = nx;
             my_na = nw;
+            my_nn = nn;
         }
     }
     if (lane < NW) {
         hdr->nx[lane] = (unsigned char)my_nx;
         hdr->na[lane] = (unsigned char)my_na;
+        hdr->nn[lane] = (unsigned char)my_nn;
     }
     if (lane == 0) {
         hdr->P[0] = P0;
@@ -649,14 +672,15 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
 }
 
 // ---------------------------------------------------------------------------
-// Fast tier for one pixel (ux, uy = tile-local pixel position).
+// Fast tier for one pixel (col, row = tile-local pixel position).
 //   sure members: records [0, nin) plus sub-list [0, nxin)
 //   ambiguous:    sub-list [nxin, nxin + namb), closest-to-centre first
+// Weights come from the tile's separable tables (w = ex[k][col] ey[k][row],
+// prob and the tile-wide d^2 floor folded into ey); the ambiguous are ranked
+// by their FP32 squared distance.
 // ---------------------------------------------------------------------------
 struct FastOut {
     float s0, s1, s2, s3, s4, s5;  // sums: w*qw, w*qz, w*qdx, w*qdy, w*(s-s0), w
-    int k0;                        // nearest staged entry
-    float d0, d1;                  // smallest and second-smallest FP32 squared distance
     bool exact;                    // boundary near-tie: rerun in the exact tier
 };
 
@@ -664,41 +688,25 @@ struct FastOut {
 __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
 template <int MS>
-__device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, const unsigned char* __restrict__ wl,
-                                           int nxin, int namb, int m, const PixSmem& s, float nal, float c0,
-                                           FastOut& o) {
-    float b0 = FLT_MAX, b1 = FLT_MAX;
-    int k0 = 0;
+__device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsigned char* __restrict__ wl,
+                                           int nxin, int namb, int m, const PixSmem& s, FastOut& o) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-    auto take = [&](int k, float d2, const float4& r0) {
-        const bool nb = d2 < b0;
-        b1 = nb ? b0 : fminf(b1, d2);
-        k0 = nb ? k : k0;
-        b0 = nb ? d2 : b0;
-        // exp(-alpha (d2 - d2ref)): the factor exp(alpha (d2min - d2ref)) common
-        // to every weight cancels in dq_blend's normalisation
-        const float w = ex2_approx(fmaf(d2, nal, c0)) * r0.z;
+    auto take = [&](int k) {
+        const float w = s.ex[k][col] * s.ey[k][row];
         const float4 q = s.rec1[k];
         a0 = fmaf(w, q.x, a0);
         a1 = fmaf(w, q.y, a1);
         a2 = fmaf(w, q.z, a2);
         a3 = fmaf(w, q.w, a3);
-        a4 = fmaf(w, r0.w, a4);
+        a4 = fmaf(w, s.rec0[k].w, a4);
         a5 += w;
     };
-    for (int k = 0; k < nin; ++k) {
-        const float4 r0 = s.rec0[k];
-        const float dx = r0.x - ux, dy = r0.y - uy;
-        take(k, fmaf(dx, dx, dy * dy), r0);
-    }
-    for (int e = 0; e < nxin; ++e) {
-        const int k = wl[e];
-        const float4 r0 = s.rec0[k];
-        const float dx = r0.x - ux, dy = r0.y - uy;
-        take(k, fmaf(dx, dx, dy * dy), r0);
-    }
+#pragma unroll 4
+    for (int k = 0; k < nin; ++k) take(k);
+    for (int e = 0; e < nxin; ++e) take(wl[e]);
     bool exact = false;
     if (MS > 0) {
+        const float ux = (float)col, uy = (float)row;
         float sd[MS > 0 ? MS : 1];
         int sk[MS > 0 ? MS : 1];
 #pragma unroll
@@ -740,21 +748,21 @@ __device__ __forceinline__ void fast_pixel(float ux, float uy, int nin, const un
         if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
 #pragma unroll
         for (int q = 0; q < MS; ++q)
-            if (q < m) take(sk[q], sd[q], s.rec0[sk[q]]);
+            if (q < m) take(sk[q]);
     }
-    o = FastOut{a0, a1, a2, a3, a4, a5, k0, b0, b1, exact};
+    o = FastOut{a0, a1, a2, a3, a4, a5, exact};
 }
 
-__device__ __forceinline__ void fast_dispatch(float ux, float uy, int nin, const unsigned char* wl, int nxin,
-                                              int namb, int m, const PixSmem& s, float nal, float c0, FastOut& o) {
+__device__ __forceinline__ void fast_dispatch(int col, int row, int nin, const unsigned char* wl, int nxin,
+                                              int namb, int m, const PixSmem& s, FastOut& o) {
     if (m <= 0)
-        fast_pixel<0>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
+        fast_pixel<0>(col, row, nin, wl, nxin, namb, m, s, o);
     else if (m <= 2)
-        fast_pixel<2>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
+        fast_pixel<2>(col, row, nin, wl, nxin, namb, m, s, o);
     else if (m <= 4)
-        fast_pixel<4>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
+        fast_pixel<4>(col, row, nin, wl, nxin, namb, m, s, o);
     else
-        fast_pixel<8>(ux, uy, nin, wl, nxin, namb, m, s, nal, c0, o);
+        fast_pixel<8>(col, row, nin, wl, nxin, namb, m, s, o);
 }
 
 // ---------------------------------------------------------------------------
@@ -797,10 +805,30 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         s.rec1[k] = r1g[k];
         s.sidx[k] = TP.sidx[(size_t)g * TREC + k];
     }
-    const int nxin = h.nx[wid], namb = h.na[wid];
+    const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
     const unsigned char* subg = TP.sub + ((size_t)g * NW + wid) * TREC;
-    if (nxin != 255)
+    if (nxin != 255) {
         for (int k = lane; k < nxin + namb; k += 32) s.sub[wid][k] = subg[k];
+        if (lane < NEAR_CAP && lane < nnear) s.near[wid][lane] = TP.near[((size_t)g * NW + wid) * NEAR_CAP + lane];
+    }
+    __syncthreads();
+    // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
+    if (!(flags & TFLAG_EXACT_STAGED)) {
+        const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
+        for (int e = t; e < ne * 2 * ET; e += ENT) {
+            const int k = e / (2 * ET), c = e % (2 * ET);
+            const float4 r0 = s.rec0[k];
+            const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
+            const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
+            if (c < ET) {
+                const float dx = r0.x - (float)c;
+                s.ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
+            } else {
+                const float dy = r0.y - (float)(c - ET);
+                s.ey[k][c - ET] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
+            }
+        }
+    }
     __syncthreads();
     if (!valid) return;
     if (flags & TFLAG_EXACT_STAGED) {
@@ -811,10 +839,8 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     const int wi = nin + nxin, m = S - wi;
     FastOut fo;
     bool ex = nxin == 255 || m < 0 || m > 8 || wi + namb < S;
-    const float d2ref = h.d2ref;
     if (!ex) {
-        const float nal = (float)(-L.alpha * kLog2e);
-        fast_dispatch((float)lx, (float)ly, nin, s.sub[wid], nxin, namb, m, s, nal, -nal * d2ref, fo);
+        fast_dispatch(lx, ly, nin, s.sub[wid], nxin, namb, m, s, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
@@ -834,15 +860,13 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     const double yy = h.Y0[1] + (h.e0[1] + (double)dlb * h.P[1] + sb * (double)Qy);
     if (od) *od = make_float2((float)(yx - qx), (float)(yy - qy));
     if (ou) {
-        // d2min in the exact tier: the nearest, or the exact minimum over every
-        // staged point within the FP32 error of it (near-tie, rare)
-        double d2m = xdist2(qx, qy, C.x[s.sidx[fo.k0]], C.y[s.sidx[fo.k0]]);
-        if (fo.d1 - fo.d0 <= d2_tol(fo.d1)) {
-            for (int k = 0; k < ne; ++k) {
-                const float dx = s.rec0[k].x - ux, dy = s.rec0[k].y - uy;
-                if (fmaf(dx, dx, dy * dy) - fo.d0 <= d2_tol(fo.d1))
-                    d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[k]], C.y[s.sidx[k]]));
-            }
+        // d2min in the exact tier (FP64, reference dist2) over the points that
+        // can be the nearest in this sub-tile
+        double d2m = DBL_MAX;
+        const int nl = nnear == 255 ? ne : nnear;
+        for (int e = 0; e < nl; ++e) {
+            const int k = nnear == 255 ? e : s.near[wid][e];
+            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[k]], C.y[s.sidx[k]]));
         }
         double arg = xmul(L.beta, d2m);
         if (55.0 < arg) arg = 55.0;
@@ -856,7 +880,8 @@ size_t emdq_scratch_bytes(int nactive, const FieldGrid& g) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nsuper = (size_t)nsx * nsy;
-    const size_t plans = (size_t)EMDQ_CHUNK_TILES * (sizeof(TileHdr) + TREC * (2 * sizeof(float4) + sizeof(int) + NW));
+    const size_t plans =
+        (size_t)EMDQ_CHUNK_TILES * (sizeof(TileHdr) + TREC * (2 * sizeof(float4) + sizeof(int) + NW) + NW * NEAR_CAP);
     return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
            plans + 1024;
 }
@@ -892,6 +917,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     TP.rec1 = TP.rec0 + (size_t)EMDQ_CHUNK_TILES * TREC;
     TP.sidx = reinterpret_cast<int*>(TP.rec1 + (size_t)EMDQ_CHUNK_TILES * TREC);
     TP.sub = reinterpret_cast<unsigned char*>(TP.sidx + (size_t)EMDQ_CHUNK_TILES * TREC);
+    TP.near = TP.sub + (size_t)EMDQ_CHUNK_TILES * NW * TREC;
 
     k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
                                                        c32, L.cl, L.cp, phi, cj);
