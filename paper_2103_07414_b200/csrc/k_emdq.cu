@@ -88,13 +88,18 @@ struct __align__(16) TileHdr {
     unsigned char nn[NW];           // per sub-tile: possible-nearest list size (255: scan all)
 };
 
+// One tile's plan, contiguous so k_pixels stages it with 16-byte loads.
+struct __align__(16) TilePlan {
+    TileHdr hdr;
+    float4 rec0[TREC];                  // ux, uy (tile-local), prob, s - s0
+    float4 rec1[TREC];                  // conjugated dual quaternion
+    int sidx[TREC];                     // candidate indices (exact-tier fallback)
+    unsigned char sub[NW][TREC];        // per sub-tile: extra sure, then ambiguous
+    unsigned char near[NW][NEAR_CAP];   // per sub-tile: points that can be the nearest
+};
+
 struct TilePlans {
-    TileHdr* hdr;          // [ntiles]
-    float4* rec0;          // [ntiles][TREC]  ux, uy (tile-local), prob, s - s0
-    float4* rec1;          // [ntiles][TREC]  conjugated dual quaternion
-    int* sidx;             // [ntiles][TREC]  candidate indices (exact-tier fallback)
-    unsigned char* sub;    // [ntiles][NW][TREC]  per sub-tile: extra sure, then ambiguous
-    unsigned char* near;   // [ntiles][NW][NEAR_CAP]  per sub-tile: possible nearest points
+    TilePlan* plan;        // [chunk tiles]
     int tx0, ty0, ntx;     // chunk: first tile column/row, tiles per row
 };
 
@@ -114,11 +119,8 @@ struct PlanWarp {
 
 // Pixel-kernel shared memory (one tile).
 struct PixSmem {
-    float4 rec0[TREC], rec1[TREC];
+    TilePlan p;
     float ex[TREC][ET], ey[TREC][ET];  // separable weights: w = ex[k][col] * ey[k][row]
-    int sidx[TREC];
-    unsigned char sub[NW][TREC];
-    unsigned char near[NW][NEAR_CAP];
 };
 struct SSmem {
     int hist[256];
@@ -420,7 +422,8 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     const int sflag = SL.flag[sid];
     const int nsrc = SL.count[sid];
     const int* src = (sflag & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
-    TileHdr* hdr = TP.hdr + g;
+    TilePlan& tp = TP.plan[g];
+    TileHdr* hdr = &tp.hdr;
     int flags = 0;
 
     // 1. radius bound
@@ -551,9 +554,9 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     if (sflag & SFLAG_NONUNIFORM) flags |= TFLAG_EXACT_STAGED;
 
     // 5. records (tile-local coordinates, conjugated warps)
-    float4* r0g = TP.rec0 + (size_t)g * TREC;
-    float4* r1g = TP.rec1 + (size_t)g * TREC;
-    int* sg = TP.sidx + (size_t)g * TREC;
+    float4* r0g = tp.rec0;
+    float4* r1g = tp.rec1;
+    int* sg = tp.sidx;
     float d2lo = FLT_MAX, d2hi = 0.f;
     for (int k = lane; k < ne; k += 32) {
         const int a = w.sidx[k];
@@ -583,8 +586,8 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     __syncwarp();
 
     // 6. per sub-tile refinement of the tile-ambiguous (FP32, conservative margins)
-    unsigned char* subg = TP.sub + (size_t)g * NW * TREC;
-    unsigned char* nearg = TP.near + (size_t)g * NW * NEAR_CAP;
+    unsigned char* subg = &tp.sub[0][0];
+    unsigned char* nearg = &tp.near[0][0];
     int my_nx = 0, my_na = 0, my_nn = 0;  // lane st < NW keeps sub-tile st's counts
     for (int st = 0; st < NW; ++st) {
         const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
@@ -693,12 +696,12 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
     auto take = [&](int k) {
         const float w = s.ex[k][col] * s.ey[k][row];
-        const float4 q = s.rec1[k];
+        const float4 q = s.p.rec1[k];
         a0 = fmaf(w, q.x, a0);
         a1 = fmaf(w, q.y, a1);
         a2 = fmaf(w, q.z, a2);
         a3 = fmaf(w, q.w, a3);
-        a4 = fmaf(w, s.rec0[k].w, a4);
+        a4 = fmaf(w, s.p.rec0[k].w, a4);
         a5 += w;
     };
 #pragma unroll 4
@@ -717,7 +720,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         float rej = FLT_MAX, worst = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
             const int k = wl[nxin + e];
-            const float2 u = *reinterpret_cast<const float2*>(&s.rec0[k]);
+            const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[k]);
             const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
             if (!(d2 < worst)) {
@@ -755,11 +758,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
 
 __device__ __forceinline__ void fast_dispatch(int col, int row, int nin, const unsigned char* wl, int nxin,
                                               int namb, int m, const PixSmem& s, FastOut& o) {
-    if (m <= 0)
-        fast_pixel<0>(col, row, nin, wl, nxin, namb, m, s, o);
-    else if (m <= 2)
-        fast_pixel<2>(col, row, nin, wl, nxin, namb, m, s, o);
-    else if (m <= 4)
+    if (m <= 4)
         fast_pixel<4>(col, row, nin, wl, nxin, namb, m, s, o);
     else
         fast_pixel<8>(col, row, nin, wl, nxin, namb, m, s, o);
@@ -777,8 +776,8 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     const int tx = TP.tx0 + blockIdx.x, ty = TP.ty0 + blockIdx.y;
     const int ti0 = L.grid.i0 + tx * ET, tj0 = L.grid.j0 + ty * ET;
     const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
-    const TileHdr& h = TP.hdr[g];
-    const int flags = h.flags, ne = h.ne, nin = h.nin;
+    const TileHdr& hg = TP.plan[g].hdr;
+    const int flags = hg.flags;
 
     const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
     const int pi = ti0 + lx, pj = tj0 + ly;
@@ -797,27 +796,22 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         }
         return;
     }
-    // stage the plan (records, candidate indices, sub-tile lists)
-    const float4* r0g = TP.rec0 + (size_t)g * TREC;
-    const float4* r1g = TP.rec1 + (size_t)g * TREC;
-    for (int k = t; k < ne; k += ENT) {
-        s.rec0[k] = r0g[k];
-        s.rec1[k] = r1g[k];
-        s.sidx[k] = TP.sidx[(size_t)g * TREC + k];
-    }
-    const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
-    const unsigned char* subg = TP.sub + ((size_t)g * NW + wid) * TREC;
-    if (nxin != 255) {
-        for (int k = lane; k < nxin + namb; k += 32) s.sub[wid][k] = subg[k];
-        if (lane < NEAR_CAP && lane < nnear) s.near[wid][lane] = TP.near[((size_t)g * NW + wid) * NEAR_CAP + lane];
+    // stage the whole plan with 16-byte loads
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&TP.plan[g]);
+        uint4* dst = reinterpret_cast<uint4*>(&s.p);
+        for (int k = t; k < (int)(sizeof(TilePlan) / 16); k += ENT) dst[k] = src[k];
     }
     __syncthreads();
+    const TileHdr& h = s.p.hdr;
+    const int ne = h.ne, nin = h.nin;
+    const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
     // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
     if (!(flags & TFLAG_EXACT_STAGED)) {
         const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
         for (int e = t; e < ne * 2 * ET; e += ENT) {
             const int k = e / (2 * ET), c = e % (2 * ET);
-            const float4 r0 = s.rec0[k];
+            const float4 r0 = s.p.rec0[k];
             const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
             const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
             if (c < ET) {
@@ -833,19 +827,19 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     if (!valid) return;
     if (flags & TFLAG_EXACT_STAGED) {
         if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        exact_dispatch<MAXS>(qx, qy, s.p.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
     const int wi = nin + nxin, m = S - wi;
     FastOut fo;
     bool ex = nxin == 255 || m < 0 || m > 8 || wi + namb < S;
     if (!ex) {
-        fast_dispatch(lx, ly, nin, s.sub[wid], nxin, namb, m, s, fo);
+        fast_dispatch(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
         if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, s.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        exact_dispatch<MAXS>(qx, qy, s.p.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
     const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
@@ -865,8 +859,8 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         double d2m = DBL_MAX;
         const int nl = nnear == 255 ? ne : nnear;
         for (int e = 0; e < nl; ++e) {
-            const int k = nnear == 255 ? e : s.near[wid][e];
-            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.sidx[k]], C.y[s.sidx[k]]));
+            const int k = nnear == 255 ? e : s.p.near[wid][e];
+            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.p.sidx[k]], C.y[s.p.sidx[k]]));
         }
         double arg = xmul(L.beta, d2m);
         if (55.0 < arg) arg = 55.0;
@@ -880,8 +874,7 @@ size_t emdq_scratch_bytes(int nactive, const FieldGrid& g) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nsuper = (size_t)nsx * nsy;
-    const size_t plans =
-        (size_t)EMDQ_CHUNK_TILES * (sizeof(TileHdr) + TREC * (2 * sizeof(float4) + sizeof(int) + NW) + NW * NEAR_CAP);
+    const size_t plans = (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan);
     return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
            plans + 1024;
 }
@@ -912,12 +905,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     char* pbase = reinterpret_cast<char*>(SL.flag + nsuper);
     pbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(pbase) + 255) & ~uintptr_t(255));
     TilePlans TP;
-    TP.hdr = reinterpret_cast<TileHdr*>(pbase);
-    TP.rec0 = reinterpret_cast<float4*>(TP.hdr + EMDQ_CHUNK_TILES);
-    TP.rec1 = TP.rec0 + (size_t)EMDQ_CHUNK_TILES * TREC;
-    TP.sidx = reinterpret_cast<int*>(TP.rec1 + (size_t)EMDQ_CHUNK_TILES * TREC);
-    TP.sub = reinterpret_cast<unsigned char*>(TP.sidx + (size_t)EMDQ_CHUNK_TILES * TREC);
-    TP.near = TP.sub + (size_t)EMDQ_CHUNK_TILES * NW * TREC;
+    TP.plan = reinterpret_cast<TilePlan*>(pbase);
 
     k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
                                                        c32, L.cl, L.cp, phi, cj);
