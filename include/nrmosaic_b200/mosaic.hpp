@@ -1,0 +1,360 @@
+// nrmosaic_b200/mosaic.hpp -- drop-in replacement for the reference's
+// nrmosaic/mosaic.hpp (proj/include/nrmosaic/mosaic.hpp) backed by the
+// B200 C ABI (include/nrm_b200.h, libnrm_b200.so).
+//
+// Existing callers (tools/main.cpp:174-176, 229-230, 268; the acceptance
+// harness acceptance.cpp:371-387) switch by replacing
+//     #include "nrmosaic/mosaic.hpp"
+// with
+//     #include "nrmosaic_b200/mosaic.hpp"
+// and linking -lnrm_b200. Same names, signatures, exceptions and
+// std::optional returns:
+//   pixel_warp            (mosaic.hpp:22)   -> std::optional<WarpFunction>
+//   invert_frame_boundary (mosaic.hpp:58)   -> std::vector<Vec2>
+//   Canvas                (mosaic.hpp:100)  kWeightCap, kTile, empty, width, height,
+//                                           origin_offset, color, weight, weight_ref,
+//                                           occupied, occupied_count, ensure_contains
+//   BlendStats            (mosaic.hpp:184)
+//   blend_frame           (mosaic.hpp:196)
+//   render                (mosaic.hpp:301)
+// plus the dense EMDQ field (detail::blend_local + node_uncertainty at every
+// pixel of a grid, fieldest.hpp:44-97) as dense_emdq_field().
+//
+// Canvas pixels live in HBM. Canvas::color()/weight() read through a host
+// mirror that is downloaded lazily after GPU updates; writes through
+// color()/weight_ref() mark the mirror dirty and are uploaded before the next
+// GPU operation on that canvas (the explicit sync SURVEY §7 calls for).
+//
+// Types: by default Vec2, Rect, DualQuat2, WarpFunction and ImageU8 come
+// from the reference headers (nrmosaic/geometry.hpp, dualquat.hpp,
+// image.hpp) so the rest of a caller's code is untouched. Define
+// NRM_B200_STANDALONE_TYPES to use minimal layout-compatible stand-ins
+// instead (for builds without the reference tree).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "nrm_b200.h"
+
+#ifndef NRM_B200_STANDALONE_TYPES
+#include "nrmosaic/dualquat.hpp"
+#include "nrmosaic/geometry.hpp"
+#include "nrmosaic/image.hpp"
+#else
+namespace nrmosaic {
+struct Vec2 {
+    double x = 0.0, y = 0.0;
+    Vec2() = default;
+    constexpr Vec2(double x_, double y_) : x(x_), y(y_) {}
+    Vec2 operator+(const Vec2& o) const { return {x + o.x, y + o.y}; }
+    Vec2 operator-(const Vec2& o) const { return {x - o.x, y - o.y}; }
+};
+struct Rect {
+    double x0 = 0.0, y0 = 0.0, x1 = 0.0, y1 = 0.0;
+    static Rect of_size(double w, double h) { return {0.0, 0.0, w, h}; }
+};
+struct DualQuat2 {
+    double w = 1.0, z = 0.0, dx = 0.0, dy = 0.0;
+    static DualQuat2 from_translation(const Vec2& t) { return {1.0, 0.0, 0.5 * t.x, 0.5 * t.y}; }
+    static DualQuat2 from_rigid(double angle, const Vec2& t) {
+        DualQuat2 q;
+        q.w = std::cos(0.5 * angle);
+        q.z = std::sin(0.5 * angle);
+        q.dx = 0.5 * (t.x * q.w + t.y * q.z);
+        q.dy = 0.5 * (-t.x * q.z + t.y * q.w);
+        return q;
+    }
+    Vec2 apply(const Vec2& p) const {
+        const double c = w * w - z * z, s = 2.0 * w * z;
+        return {c * p.x - s * p.y + 2.0 * (dx * w - dy * z), s * p.x + c * p.y + 2.0 * (dx * z + dy * w)};
+    }
+};
+struct WarpFunction {
+    double scale = 1.0;
+    DualQuat2 dq;
+    static WarpFunction identity() { return {}; }
+    Vec2 apply(const Vec2& p) const {
+        const Vec2 q = dq.apply(p);
+        return {q.x * scale, q.y * scale};
+    }
+};
+struct ImageU8 {
+    int width = 0, height = 0, channels = 0;
+    std::vector<std::uint8_t> data;
+    static ImageU8 make(int w, int h, int c, std::uint8_t fill = 0) {
+        ImageU8 im;
+        im.width = w;
+        im.height = h;
+        im.channels = c;
+        im.data.assign(static_cast<std::size_t>(w) * h * c, fill);
+        return im;
+    }
+    bool empty() const { return width == 0 || height == 0; }
+    std::uint8_t& at(int x, int y, int c) { return data[(static_cast<std::size_t>(y) * width + x) * channels + c]; }
+    std::uint8_t at(int x, int y, int c) const {
+        return data[(static_cast<std::size_t>(y) * width + x) * channels + c];
+    }
+};
+}  // namespace nrmosaic
+#endif
+
+namespace nrmosaic {
+
+constexpr double kPixelWeightCutoff = 1e-6;  // mosaic.hpp:16
+
+namespace b200 {
+
+// Maps C ABI status codes onto the reference's exception types.
+inline void check(int rc) {
+    if (rc == NRM_OK) return;
+    const std::string msg = nrm_last_error();
+    if (rc == NRM_EINVAL || rc == NRM_EDEGENERATE) throw std::invalid_argument(msg);
+    throw std::runtime_error("nrm_b200: " + msg);
+}
+
+// One context per process (device from NRM_B200_DEVICE, default 0).
+inline nrm_ctx* context() {
+    struct Holder {
+        nrm_ctx* c = nullptr;
+        Holder() {
+            const char* d = std::getenv("NRM_B200_DEVICE");
+            check(nrm_ctx_create(d ? std::atoi(d) : 0, &c));
+        }
+        ~Holder() { nrm_ctx_destroy(c); }
+    };
+    static Holder h;
+    return h.c;
+}
+
+inline std::vector<double> pack_points(std::span<const Vec2> pts) {
+    std::vector<double> v(pts.size() * 2);
+    for (std::size_t i = 0; i < pts.size(); ++i) {
+        v[2 * i] = pts[i].x;
+        v[2 * i + 1] = pts[i].y;
+    }
+    return v;
+}
+
+inline std::vector<double> pack_warps(std::span<const WarpFunction> w) {
+    std::vector<double> v(w.size() * 5);
+    for (std::size_t i = 0; i < w.size(); ++i) {
+        v[5 * i] = w[i].scale;
+        v[5 * i + 1] = w[i].dq.w;
+        v[5 * i + 2] = w[i].dq.z;
+        v[5 * i + 3] = w[i].dq.dx;
+        v[5 * i + 4] = w[i].dq.dy;
+    }
+    return v;
+}
+
+inline WarpFunction unpack_warp(const double* p) {
+    WarpFunction w;
+    w.scale = p[0];
+    w.dq.w = p[1];
+    w.dq.z = p[2];
+    w.dq.dx = p[3];
+    w.dq.dy = p[4];
+    return w;
+}
+
+}  // namespace b200
+
+/// pixel_warp (mosaic.hpp:22-51), evaluated on the GPU in the exact tier.
+inline std::optional<WarpFunction> pixel_warp(const Vec2& x_ref, std::span<const Vec2> anchors,
+                                              std::span<const WarpFunction> warps, double alpha) {
+    if (anchors.size() != warps.size()) throw std::invalid_argument("pixel_warp: size mismatch");
+    const double p[2] = {x_ref.x, x_ref.y};
+    const auto a = b200::pack_points(anchors);
+    const auto w = b200::pack_warps(warps);
+    double out[5];
+    std::uint8_t valid = 0;
+    b200::check(nrm_pixel_warp(b200::context(), p, 1, a.data(), w.data(), static_cast<int>(anchors.size()), alpha,
+                               out, &valid));
+    if (!valid) return std::nullopt;
+    return b200::unpack_warp(out);
+}
+
+/// invert_frame_boundary (mosaic.hpp:58-96), one GPU thread per boundary sample.
+inline std::vector<Vec2> invert_frame_boundary(int frame_w, int frame_h, std::span<const Vec2> anchors,
+                                               std::span<const WarpFunction> warps, double alpha,
+                                               double step = 8.0) {
+    const auto a = b200::pack_points(anchors);
+    const auto w = b200::pack_warps(warps);
+    int n = 0;
+    b200::check(nrm_invert_frame_boundary(b200::context(), frame_w, frame_h, a.data(), w.data(),
+                                          static_cast<int>(anchors.size()), alpha, step, nullptr, 0, &n));
+    std::vector<double> poly(static_cast<std::size_t>(n) * 2);
+    b200::check(nrm_invert_frame_boundary(b200::context(), frame_w, frame_h, a.data(), w.data(),
+                                          static_cast<int>(anchors.size()), alpha, step, poly.data(), n, &n));
+    std::vector<Vec2> out(n);
+    for (int i = 0; i < n; ++i) out[i] = Vec2{poly[2 * i], poly[2 * i + 1]};
+    return out;
+}
+
+/// Canvas (mosaic.hpp:100-182), HBM-resident.
+class Canvas {
+public:
+    static constexpr int kWeightCap = 30;
+    static constexpr int kTile = 256;
+
+    Canvas() { b200::check(nrm_canvas_create(b200::context(), &h_)); }
+    ~Canvas() {
+        if (h_) nrm_canvas_destroy(h_);
+    }
+    Canvas(const Canvas&) = delete;
+    Canvas& operator=(const Canvas&) = delete;
+    Canvas(Canvas&& o) noexcept { *this = std::move(o); }
+    Canvas& operator=(Canvas&& o) noexcept {
+        std::swap(h_, o.h_);
+        std::swap(color_, o.color_);
+        std::swap(weight_, o.weight_);
+        std::swap(mirror_, o.mirror_);
+        return *this;
+    }
+
+    bool empty() const { return width() == 0; }
+    int width() const { return info().w; }
+    int height() const { return info().h; }
+    /// Reference-frame coordinate of canvas pixel (0, 0).
+    Vec2 origin_offset() const {
+        const Info i = info();
+        return {static_cast<double>(i.ox), static_cast<double>(i.oy)};
+    }
+
+    double* color(int x, int y) {
+        pull();
+        mirror_ = Mirror::Dirty;
+        return &color_[(static_cast<std::size_t>(y) * width() + x) * 3];
+    }
+    const double* color(int x, int y) const {
+        pull();
+        return &color_[(static_cast<std::size_t>(y) * width() + x) * 3];
+    }
+    std::uint8_t weight(int x, int y) const {
+        pull();
+        return weight_[static_cast<std::size_t>(y) * width() + x];
+    }
+    std::uint8_t& weight_ref(int x, int y) {
+        pull();
+        mirror_ = Mirror::Dirty;
+        return weight_[static_cast<std::size_t>(y) * width() + x];
+    }
+    bool occupied(int x, int y) const { return weight(x, y) > 0; }
+    std::int64_t occupied_count() const {
+        push();
+        std::int64_t n = 0;
+        b200::check(nrm_canvas_occupied_count(h_, &n));
+        return n;
+    }
+    /// Grows the canvas (tile-aligned) so the reference-frame rectangle fits.
+    void ensure_contains(const Rect& r) {
+        push();
+        b200::check(nrm_canvas_ensure_contains(h_, r.x0, r.y0, r.x1, r.y1));
+        mirror_ = Mirror::Stale;
+    }
+
+    /// B200 extensions: pre-allocate HBM for a region; band for multi-GPU.
+    void reserve(const Rect& r) { b200::check(nrm_canvas_reserve(h_, r.x0, r.y0, r.x1, r.y1)); }
+    void set_band(int rank, int count) { b200::check(nrm_canvas_set_band(h_, rank, count)); }
+    nrm_canvas* handle() const {
+        push();
+        return h_;
+    }
+    void invalidate_mirror() { mirror_ = Mirror::Stale; }
+
+private:
+    enum class Mirror { Stale, Clean, Dirty };
+    struct Info {
+        std::int64_t ox, oy;
+        int w, h;
+    };
+    Info info() const {
+        Info i{};
+        b200::check(nrm_canvas_info(h_, &i.ox, &i.oy, &i.w, &i.h));
+        return i;
+    }
+    void pull() const {
+        if (mirror_ != Mirror::Stale) return;
+        const Info i = info();
+        color_.assign(static_cast<std::size_t>(i.w) * i.h * 3, 0.0);
+        weight_.assign(static_cast<std::size_t>(i.w) * i.h, 0);
+        if (i.w && i.h) b200::check(nrm_canvas_download(h_, 0, 0, i.w, i.h, color_.data(), weight_.data()));
+        mirror_ = Mirror::Clean;
+    }
+    void push() const {
+        if (mirror_ != Mirror::Dirty) return;
+        const Info i = info();
+        b200::check(nrm_canvas_upload(h_, 0, 0, i.w, i.h, color_.data(), weight_.data()));
+        mirror_ = Mirror::Clean;
+    }
+
+    nrm_canvas* h_ = nullptr;
+    mutable std::vector<double> color_;
+    mutable std::vector<std::uint8_t> weight_;
+    mutable Mirror mirror_ = Mirror::Stale;
+};
+
+struct BlendStats {
+    std::int64_t footprint_pixels = 0;
+    std::int64_t blended_pixels = 0;
+    std::int64_t skipped_no_support = 0;
+    std::int64_t skipped_out_of_frame = 0;
+};
+
+/// blend_frame (mosaic.hpp:196-296). `workers` is accepted for signature
+/// compatibility; the GPU grid replaces the host thread pool.
+inline BlendStats blend_frame(Canvas& canvas, const ImageU8& frame, std::span<const Vec2> anchors,
+                              std::span<const WarpFunction> warps, double alpha,
+                              std::span<const Vec2> footprint_polygon, int workers) {
+    (void)workers;
+    if (anchors.size() != warps.size()) throw std::invalid_argument("blend_frame: size mismatch");
+    const auto a = b200::pack_points(anchors);
+    const auto w = b200::pack_warps(warps);
+    const auto p = b200::pack_points(footprint_polygon);
+    nrm_blend_stats s{};
+    b200::check(nrm_blend_frame(canvas.handle(), frame.data.data(), frame.width, frame.height,
+                                frame.channels ? frame.channels : 3, a.data(), w.data(),
+                                static_cast<int>(anchors.size()), alpha, p.data(),
+                                static_cast<int>(footprint_polygon.size()), &s));
+    canvas.invalidate_mirror();
+    return {s.footprint_pixels, s.blended_pixels, s.skipped_no_support, s.skipped_out_of_frame};
+}
+
+/// render (mosaic.hpp:301-331).
+inline ImageU8 render(const Canvas& canvas, bool crop = false, Vec2* crop_origin = nullptr) {
+    int w = 0, h = 0;
+    double org[2] = {0.0, 0.0};
+    b200::check(nrm_render(canvas.handle(), crop ? 1 : 0, nullptr, &w, &h, org));
+    if (crop_origin) *crop_origin = Vec2{org[0], org[1]};
+    if (w == 0 || h == 0) return ImageU8{};
+    ImageU8 out = ImageU8::make(w, h, 4);
+    b200::check(nrm_render(canvas.handle(), crop ? 1 : 0, out.data.data(), &w, &h, org));
+    return out;
+}
+
+/// Dense EMDQ field: detail::blend_local (fieldest.hpp:75-97) applied at every
+/// pixel (x0 + i, y0 + j) of a w x h grid plus node_uncertainty
+/// (fieldest.hpp:44-52). disp receives w*h*2 floats (warp(p) - p), unc w*h.
+inline void dense_emdq_field(double x0, double y0, int w, int h, std::span<const Vec2> apts,
+                             std::span<const WarpFunction> locals, std::span<const double> probs,
+                             std::span<const int> active, double alpha, int support, double beta, float* disp,
+                             float* unc) {
+    if (apts.size() != locals.size() || apts.size() != probs.size())
+        throw std::invalid_argument("dense_emdq_field: size mismatch");
+    const auto a = b200::pack_points(apts);
+    const auto l = b200::pack_warps(locals);
+    std::vector<std::int32_t> act(active.begin(), active.end());
+    const nrm_grid g{x0, y0, w, h};
+    b200::check(nrm_emdq_field(b200::context(), &g, a.data(), l.data(), probs.data(), static_cast<int>(apts.size()),
+                               act.data(), static_cast<int>(act.size()), alpha, support, beta, disp, unc));
+}
+
+}  // namespace nrmosaic
