@@ -298,10 +298,13 @@ def main():
     clk.start()
     time.sleep(0.3)
     l0 = ctx.launch_count()
+    ctx.profile(True)
     for _ in range(args.steps):
         step(True)
     torch.cuda.synchronize()
     launches = (ctx.launch_count() - l0)
+    kt = ctx.kernel_times()
+    ctx.profile(False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -368,33 +371,42 @@ def main():
     roof = None
     if rank == 0:
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-        fp32_peak = ctx.peak("fp32")   # measured FFMA lane-ops/s on this device
+        fp32_peak = 2.0 * ctx.peak("fp32") / 1e12   # measured FFMA lane-ops/s -> TFLOP/s (FMA = 2 flops)
         contrib = wl_contributors(wl, polys[0])
-        k_blend = ms["blend"] / args.steps / nfr   # per launch (one frame)
-        k_emdq = ms["emdq"] / args.steps
-        # K1: 10 FP32 pipe instructions per contributing (pixel, node) pair
-        # (SURVEY §8d), 2 flops per instruction-equivalent FMA
-        blend_flops = contrib["pairs"] * 10 * 2
-        emdq_flops = fw * fh * 16 * 8 * 2   # 16 blend pairs x (exp + 6 FMA + weight) per pixel, FMA-equivalents
-        dominant = "blend" if k_blend * nfr >= k_emdq else "emdq"
+        # algorithmic FP32 flops per unit:
+        #   K1 per contributing (pixel, node) pair (w > 1e-6, mosaic.hpp:249-262):
+        #      d2 5 + exponent 1 + exp 1 + 5 weighted sums x 2 + wsum 1 = 18
+        #   K3 per pixel: 16 blend members x (distance 5 + exp 1 + prob 1 + 5 sums x 2 + wsum 1) = 288
+        algo = {"k_node_field": contrib["pairs"] * 18.0, "k_pixels": fw * fh * 16 * 18.0}
         traffic = load_traffic()
-        if dominant == "blend":
-            ach = blend_flops / (k_blend * 1e-3) / 1e12
-            roof = {"kernel": "k_node_field<0> (K1 fused node field + mosaic update)", "bound": "fp32",
-                    "achieved": ach, "peak": 2 * fp32_peak / 1e12, "unit": "TFLOP/s",
-                    "frac": ach / (2 * fp32_peak / 1e12), "traffic": traffic.get("k_node_field"),
-                    "algorithmic": f"{contrib['pairs']:.4g} contributing pixel-node pairs x 10 FP32 ops",
-                    "peak_source": "measured FFMA probe (nrm_selftest_peak) on this device"}
+        kernels = []
+        for name, (tot_ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0]):
+            per = tot_ms / max(n, 1)
+            ent = {"kernel": name, "ms_per_launch": per, "launches": n,
+                   "share_of_step": tot_ms / max(sum(v[0] for v in kt.values()), 1e-9)}
+            if name in algo:
+                per_launch_flops = algo[name] / (1 if name == "k_node_field" else 1)
+                ach = per_launch_flops / (per * 1e-3) / 1e12
+                ent.update({"achieved_tflops": ach, "frac_fp32": ach / fp32_peak})
+            kernels.append(ent)
+        dom = kernels[0]
+        name = dom["kernel"]
+        if name in algo:
+            roof = {"kernel": name, "bound": "fp32", "achieved": dom["achieved_tflops"], "peak": fp32_peak,
+                    "unit": "TFLOP/s", "frac": dom["frac_fp32"], "traffic": traffic.get(name),
+                    "peak_source": "measured FFMA throughput on this B200 (nrm_selftest_peak), FMA = 2 flops"}
         else:
-            ach = emdq_flops / (k_emdq * 1e-3) / 1e12
-            roof = {"kernel": "k_emdq (K3 dense EMDQ field)", "bound": "fp32", "achieved": ach,
-                    "peak": 2 * fp32_peak / 1e12, "unit": "TFLOP/s", "frac": ach / (2 * fp32_peak / 1e12),
-                    "traffic": traffic.get("k_emdq"), "peak_source": "measured FFMA probe (nrm_selftest_peak)"}
+            roof = {"kernel": name, "bound": "fp32", "achieved": None, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": None, "traffic": traffic.get(name)}
+        roof["algorithmic"] = {"k_node_field": f"{contrib['pairs']:.4g} contributing pixel-node pairs "
+                                               f"({contrib['per_px']:.1f}/px) x 18 flops",
+                               "k_pixels": f"{fw * fh} px x 16 members x 18 flops"}
         # HBM view of the fused update: 29 B per footprint pixel (canvas r+w 26 B + frame 3 B)
+        kb = kt.get("k_node_field", (0.0, 1))
         fp_px = int(st[0][0])
-        roof["hbm_view"] = {"kernel": "K1", "achieved_gbs": fp_px * 29 / (k_blend * 1e-3) / 1e9,
-                            "peak_gbs": peaks.get("hbm_gbs"), "bytes_per_footprint_px": 29}
-        roof["kernel_ms"] = {"emdq_field": k_emdq, "blend_frame_per_frame": k_blend}
+        roof["hbm_view_k_node_field"] = {"achieved_gbs": fp_px * 29 / (kb[0] / max(kb[1], 1) * 1e-3) / 1e9,
+                                         "peak_gbs": peaks.get("hbm_gbs"), "bytes_per_footprint_px": 29}
+        roof["kernels"] = kernels
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

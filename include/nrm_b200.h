@@ -178,6 +178,16 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
                           const int32_t *d_active, int nactive, double alpha, int support,
                           double beta, float *d_disp, float *d_unc);
 
+/* ---- kernel timing -------------------------------------------------------
+ * With profiling on, a CUDA event is recorded on the context stream before
+ * every kernel and at the end of every compute call; a kernel's time is the
+ * interval to the next event. nrm_ctx_profile(ctx, 1) clears and enables,
+ * 0 disables. nrm_ctx_profile_read returns per-kernel totals: names joined
+ * by '\n' into `names`, total ms and launch counts (up to cap entries). */
+int nrm_ctx_profile(nrm_ctx *ctx, int enable);
+int nrm_ctx_profile_read(nrm_ctx *ctx, char *names, int names_len, double *ms, int64_t *counts,
+                         int cap, int *n);
+
 /* ---- pure host planning (no CUDA device needed) --------------------------
  * The host-side bookkeeping the entry points above perform, exposed for
  * testing and for multi-GPU orchestration. */

@@ -97,6 +97,8 @@ SIGNATURES = [
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
     ("nrm_ctx_exceptions", C.c_int, [_P, _I64, _I64]),
+    ("nrm_ctx_profile", C.c_int, [_P, C.c_int]),
+    ("nrm_ctx_profile_read", C.c_int, [_P, C.c_char_p, C.c_int, _P, _P, C.c_int, _I]),
     ("nrm_plan_ensure_contains", C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
                                            C.c_double, C.c_double, _I64, _I64, _I, _I]),
     ("nrm_plan_footprint", C.c_int, [_P, C.c_int, C.c_int64, C.c_int64, _I64, _I64]),

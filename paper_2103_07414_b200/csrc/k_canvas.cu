@@ -150,6 +150,7 @@ __global__ void k_canvas_write(float* r, float* g, float* b, uint8_t* wp, long l
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
+    prof_mark("k_render", st);
     k_render<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), x, y, w, h, reinterpret_cast<uchar4*>(out));
     ++*launches;
     return cudaGetLastError();
@@ -159,6 +160,7 @@ cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int
                             cudaStream_t st, int64_t* launches) {
     if (cv->width <= 0 || cv->height <= 0) return cudaSuccess;
     const int blocks = cv->height < 148 * 8 ? cv->height : 148 * 8;
+    prof_mark("k_occupied", st);
     k_occupied<<<blocks, 256, 0, st>>>(view_of(cv), cv->width, cv->height, count, bbox4);
     ++*launches;
     return cudaGetLastError();
@@ -167,6 +169,7 @@ cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int
 cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h, double* rgb,
                                uint8_t* weight, cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
+    prof_mark("k_canvas_read", st);
     k_canvas_read<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), x, y, w, h, rgb, weight);
     ++*launches;
     return cudaGetLastError();
@@ -175,6 +178,7 @@ cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h,
 cudaError_t launch_canvas_write(nrm_canvas* cv, int x, int y, int w, int h, const double* rgb,
                                 const uint8_t* weight, cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
+    prof_mark("k_canvas_write", st);
     k_canvas_write<<<dim3((w + 255) / 256, h), 256, 0, st>>>(cv->r, cv->g, cv->b, cv->w, cv->cap_w,
                                                             cv->origin_x - cv->phys_x0,
                                                             cv->origin_y - cv->phys_y0, x, y, w, h, rgb,

@@ -907,6 +907,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     TilePlans TP;
     TP.plan = reinterpret_cast<TilePlan*>(pbase);
 
+    prof_mark("k_gather", st);
     k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
                                                        c32, L.cl, L.cp, phi, cj);
     ++*launches;
@@ -915,6 +916,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     const int S = L.support < L.nactive ? L.support : L.nactive;
     const size_t ssm = sizeof(SSmem);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    prof_mark("k_super", st);
     k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, S);
     ++*launches;
     e = cudaGetLastError();
@@ -931,8 +933,10 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
         TP.ty0 = ty0;
         TP.ntx = ntx;
         const int ntiles = rows * ntx;
+        prof_mark("k_plan", st);
         k_plan<<<(ntiles + PLAN_WARPS - 1) / PLAN_WARPS, PLAN_WARPS * 32, psm, st>>>(L, C, SL, TP, ntiles, S);
         ++*launches;
+        prof_mark("k_pixels", st);
         if (S <= 16)
             k_pixels<16><<<dim3(ntx, rows), ENT, 0, st>>>(L, C, SL, TP, S);
         else

@@ -645,6 +645,7 @@ __global__ void k_selftest_libm(const double* __restrict__ x, const double* __re
 cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double* ex, double* hy,
                                  cudaStream_t st, int64_t* launches) {
     if (n <= 0) return cudaSuccess;
+    prof_mark("k_selftest_libm", st);
     k_selftest_libm<<<(n + 255) / 256, 256, 0, st>>>(x, y, n, ex, hy);
     ++*launches;
     return cudaGetLastError();
@@ -672,15 +673,18 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
     if (ntx > 0 && nty > 0) {
         if (mode == 0) {
             cudaFuncSetAttribute(k_node_field<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            prof_mark("k_node_field", st);
             k_node_field<0><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
         } else {
             cudaFuncSetAttribute(k_node_field<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            prof_mark("k_node_field", st);
             k_node_field<1><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
         }
         ++*launches;
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
+    prof_mark("k_node_exceptions", st);
     if (mode == 0)
         k_node_exceptions<0><<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
     else
@@ -693,6 +697,7 @@ cudaError_t launch_pixel_warp_points(const double* pts, int npts, const double* 
                                      const double* warps, int n, double alpha, double* out,
                                      uint8_t* valid, cudaStream_t st, int64_t* launches) {
     if (npts <= 0) return cudaSuccess;
+    prof_mark("k_pixel_warp_points", st);
     k_pixel_warp_points<<<(npts + 127) / 128, 128, 0, st>>>(pts, npts, anchors, warps, n, alpha, out, valid);
     ++*launches;
     return cudaGetLastError();
@@ -702,6 +707,7 @@ cudaError_t launch_invert_boundary(int, int, const double* anchors, const double
                                    double alpha, double, double* poly, int nsamples,
                                    cudaStream_t st, int64_t* launches) {
     if (nsamples <= 0) return cudaSuccess;
+    prof_mark("k_invert_boundary", st);
     k_invert_boundary<<<(nsamples + 63) / 64, 64, 0, st>>>(anchors, warps, n, alpha, poly, nsamples);
     ++*launches;
     return cudaGetLastError();

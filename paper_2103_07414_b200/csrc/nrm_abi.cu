@@ -52,6 +52,31 @@ struct DeviceGuard {
 
 }  // namespace
 
+namespace {
+thread_local nrm_ctx* g_prof_ctx = nullptr;
+}
+
+void prof_mark(const char* name, cudaStream_t st) {
+    nrm_ctx* c = g_prof_ctx;
+    if (!c || !c->prof.on) return;
+    Prof& p = c->prof;
+    if (p.used == p.ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        p.ev.push_back(e);
+        p.name.push_back(nullptr);
+    }
+    p.name[p.used] = name;
+    cudaEventRecord(p.ev[p.used], st);
+    ++p.used;
+}
+
+ProfScope::ProfScope(nrm_ctx* c) : prev(g_prof_ctx) { g_prof_ctx = c; }
+ProfScope::~ProfScope() {
+    if (g_prof_ctx) prof_mark(nullptr, g_prof_ctx->stream);  // end of the call
+    g_prof_ctx = prev;
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -484,6 +509,7 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();
+    for (cudaEvent_t e : c->prof.ev) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return NRM_OK;
@@ -666,6 +692,7 @@ int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch
     NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
     nrm_ctx* c = cv->ctx;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     const size_t fbytes = (size_t)fw * fh * ch;
     NRM_CHECK(upload(c, c->frame_raw, frame, fbytes));
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
@@ -690,6 +717,7 @@ int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int f
     NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
     nrm_ctx* c = cv->ctx;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     if (fw > 0 && fh > 0 && npoly >= 3) {
         if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "frame channels must be 1, 3 or 4");
         if (!d_frame || !poly) return fail(NRM_EINVAL, "null frame or polygon");
@@ -710,6 +738,7 @@ int nrm_render(nrm_canvas* cv, int crop, uint8_t* out, int* out_w, int* out_h, d
     *out_h = 0;
     if (cv->width == 0) return NRM_OK;
     DeviceGuard g(cv->ctx->device);
+    ProfScope prof_scope(cv->ctx);
     int x0 = 0, y0 = 0, x1 = cv->width - 1, y1 = cv->height - 1;
     if (crop) {
         unsigned long long cnt = 0;
@@ -743,6 +772,7 @@ int nrm_render_device(nrm_canvas* cv, int x, int y, int w, int h, uint8_t* d_out
     NRM_CHECK(check_region(cv, x, y, w, h));
     if (!d_out && (size_t)w * h) return fail(NRM_EINVAL, "null output");
     DeviceGuard g(cv->ctx->device);
+    ProfScope prof_scope(cv->ctx);
     NRM_CUDA(launch_render(cv, x, y, w, h, d_out, cv->ctx->stream, &cv->ctx->launches));
     return NRM_OK;
 }
@@ -755,6 +785,7 @@ int nrm_pixel_warp(nrm_ctx* c, const double* points, int npts, const double* anc
     NRM_CHECK(validate_nodes(anchors, warps, n, alpha, true));
     if (npts == 0) return NRM_OK;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     NRM_CHECK(upload(c, c->pts, points, (size_t)npts * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
@@ -778,6 +809,7 @@ int nrm_node_field(nrm_ctx* c, const nrm_grid* grid, const double* anchors, cons
     const size_t npx = (size_t)grid->width * grid->height;
     if (npx == 0) return NRM_OK;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
     NRM_CUDA(c->out_a.ensure(npx * sizeof(float2)));
@@ -796,6 +828,7 @@ int nrm_node_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anch
     if (!c) return fail(NRM_ESTATE, "null context");
     NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     return node_field_core(c, grid, d_anchors, d_warps, n, alpha, d_disp, d_support);
 }
 
@@ -817,6 +850,7 @@ int nrm_invert_frame_boundary(nrm_ctx* c, int fw, int fh, const double* anchors,
     *npoly = ns;
     if (ns == 0) return NRM_OK;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     NRM_CHECK(upload(c, c->pts, s.data(), s.size() * sizeof(double)));
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
@@ -843,6 +877,7 @@ int nrm_emdq_field(nrm_ctx* c, const nrm_grid* grid, const double* apts, const d
         return fail(NRM_EINVAL, "emdq_field: non-finite candidates");
     const size_t npx = (size_t)grid->width * grid->height;
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     NRM_CHECK(upload(c, c->anchors, apts, (size_t)m_total * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->locals, locals, (size_t)m_total * 5 * sizeof(double)));
     NRM_CHECK(upload(c, c->probs, probs, (size_t)m_total * sizeof(double)));
@@ -865,6 +900,7 @@ int nrm_emdq_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_apts
                           int support, double beta, float* d_disp, float* d_unc) {
     if (!c) return fail(NRM_ESTATE, "null context");
     DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
     return emdq_core(c, grid, d_apts, d_locals, d_probs, m_total, d_active, nactive, alpha, support, beta, d_disp,
                      d_unc);
 }
@@ -897,6 +933,55 @@ int nrm_selftest_peak(nrm_ctx* c, int which, double* ops_per_s) {
                             &ms, &c->launches));
     const double ops = (double)c->num_sms * 8 * 256 * (double)iters * 16 * 8;  // lane-ops
     *ops_per_s = ops / (ms * 1e-3);
+    return NRM_OK;
+}
+
+// ---- kernel timing -------------------------------------------------------------
+int nrm_ctx_profile(nrm_ctx* c, int enable) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    DeviceGuard g(c->device);
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    c->prof.on = enable != 0;
+    c->prof.used = 0;
+    return NRM_OK;
+}
+
+int nrm_ctx_profile_read(nrm_ctx* c, char* names, int names_len, double* ms, int64_t* counts, int cap, int* n) {
+    if (!c || !n) return fail(NRM_EINVAL, "null argument");
+    DeviceGuard g(c->device);
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<std::string> keys;
+    std::vector<double> tot;
+    std::vector<int64_t> cnt;
+    Prof& p = c->prof;
+    for (size_t i = 0; i + 1 < p.used; ++i) {
+        if (!p.name[i]) continue;
+        float dt = 0.f;
+        NRM_CUDA(cudaEventElapsedTime(&dt, p.ev[i], p.ev[i + 1]));
+        size_t k = 0;
+        while (k < keys.size() && keys[k] != p.name[i]) ++k;
+        if (k == keys.size()) {
+            keys.emplace_back(p.name[i]);
+            tot.push_back(0.0);
+            cnt.push_back(0);
+        }
+        tot[k] += dt;
+        cnt[k] += 1;
+    }
+    *n = (int)keys.size();
+    std::string joined;
+    for (size_t k = 0; k < keys.size(); ++k) {
+        if (k < (size_t)cap) {
+            if (ms) ms[k] = tot[k];
+            if (counts) counts[k] = cnt[k];
+        }
+        joined += keys[k];
+        joined += '\n';
+    }
+    if (names && names_len > 0) {
+        std::strncpy(names, joined.c_str(), (size_t)names_len - 1);
+        names[names_len - 1] = 0;
+    }
     return NRM_OK;
 }
 

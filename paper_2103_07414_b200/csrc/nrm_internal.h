@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "nrm_b200.h"
 
@@ -29,6 +30,20 @@ struct PinnedBuf {
     void release();
 };
 
+// Per-context kernel timing (nrm_ctx_profile): a CUDA event is recorded on the
+// launching stream before every kernel and after every profiled API call; a
+// kernel's time is the interval to the next event.
+struct Prof {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<const char*> name;
+    size_t used = 0;
+};
+
+// Records a timing mark for the context of the current API call (no-op
+// unless that context has profiling enabled).
+void prof_mark(const char* name, cudaStream_t st);
+
 }  // namespace nrm
 
 struct nrm_ctx {
@@ -41,6 +56,7 @@ struct nrm_ctx {
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
         active, out_a, out_b, tiles;
     nrm::PinnedBuf staging, staging_out;
+    nrm::Prof prof;
 };
 
 struct nrm_canvas {
@@ -62,6 +78,14 @@ struct nrm_canvas {
 };
 
 namespace nrm {
+
+// Makes `c` the profiled context of this thread for the scope of an API call
+// and closes the call with an end mark.
+struct ProfScope {
+    nrm_ctx* prev;
+    explicit ProfScope(nrm_ctx* c);
+    ~ProfScope();
+};
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);

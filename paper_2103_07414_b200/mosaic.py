@@ -95,6 +95,20 @@ class Context:
         check(self._lib.nrm_ctx_exceptions(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel CUDA-event timing on the context stream (clears on enable)."""
+        check(self._lib.nrm_ctx_profile(self._h, int(bool(enable))))
+
+    def kernel_times(self) -> dict:
+        """{kernel name: (total ms, launches)} since profile(True)."""
+        buf = C.create_string_buffer(4096)
+        ms = (C.c_double * 64)()
+        cnt = (C.c_int64 * 64)()
+        n = C.c_int()
+        check(self._lib.nrm_ctx_profile_read(self._h, buf, 4096, ms, cnt, 64, C.byref(n)))
+        names = buf.value.decode().split("\n")[: n.value]
+        return {nm: (ms[i], cnt[i]) for i, nm in enumerate(names)}
+
     def peak(self, which: str = "fp32") -> float:
         """Measured lane-ops/s of the FP32 FFMA ("fp32") or MUFU.EX2 ("mufu") pipe."""
         v = C.c_double()
