@@ -63,7 +63,7 @@ def host_cpu():
 # clocks (nvidia-smi sampled during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -76,7 +76,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -88,6 +88,10 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
+    def mark(self, which: str):
+        """Host wall time of the timed region's start / end (samples outside are dropped)."""
+        setattr(self, which, time.time())
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -98,13 +102,23 @@ class ClockSampler:
             self.proc.kill()
         if self._t:
             self._t.join(timeout=2)
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        import datetime
+        t0, t1 = getattr(self, "start", None), getattr(self, "end", None)
+
+        def inside(r):
+            try:
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                return True
+            return t0 is None or t1 is None or (t0 - 0.05) <= ts <= (t1 + 0.05)
+
+        rows = [r for r in self.rows if len(r) >= 9 and inside(r)]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
-                          if r[5 + k].lower().startswith("active")})
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 # ---------------------------------------------------------------------------
@@ -197,13 +211,13 @@ def footprint_polygon_cpu(wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
     ap.add_argument("--ref-rows", type=int, default=48, help="frame rows of the EMDQ field in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: --steps)")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -299,9 +313,11 @@ def main():
     time.sleep(0.3)
     l0 = ctx.launch_count()
     ctx.profile(True)
+    clk.mark("start")
     for _ in range(args.steps):
         step(True)
     torch.cuda.synchronize()
+    clk.mark("end")
     launches = (ctx.launch_count() - l0)
     kt = ctx.kernel_times()
     ctx.profile(False)
@@ -346,7 +362,7 @@ def main():
             out.append(s)
         return out
 
-    e2e_steps = args.e2e_steps or args.steps
+    e2e_steps = args.e2e_steps or min(args.steps, 300)
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
