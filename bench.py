@@ -217,6 +217,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
     ap.add_argument("--ref-rows", type=int, default=48, help="frame rows of the EMDQ field in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false",
+                    help="run K1 after K3 on one stream (default: K1 || K3 on two streams)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -263,7 +265,11 @@ def main():
     x_lo = wl.canvas_rect[0]
     rect = (x_lo, wl.canvas_rect[1], wl.canvas_rect[2] + shift[-1], wl.canvas_rect[3])
 
-    cv = M.Canvas(ctx)
+    # K1 (canvas) runs on its own context/stream so it overlaps K3 (independent work)
+    stream_b = torch.cuda.Stream(dev)
+    ctx_b = M.Context(local)
+    ctx_b.set_stream(stream_b.cuda_stream)
+    cv = M.Canvas(ctx_b if args.overlap else ctx)
     cv.reserve(rect)
     cv.ensure_contains(rect)
     if world > 1:
@@ -284,26 +290,31 @@ def main():
 
     ev = {k: [] for k in ("step", "emdq", "blend")}
 
-    def step(timed: bool):
+    def step(timed: bool, overlap: bool = True):
         if timed:
             flush.fill_(1)  # L2 flush (untimed): 256 MiB > 126 MB L2
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record(stream)
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        if overlap:
+            stream_b.wait_event(e0)  # K1 on stream B starts with K3 on stream A
         M.emdq_field_device(grid, apts_t, loc_t, prob_t, act_t, alpha, beta, disp_t, unc_t, 16, ctx=ctx)
-        if timed:
-            e1.record(stream)
+        e1.record(stream)
         for k in range(nfr):
             M.blend_frame_device(cv, frame_t, fw, fh, 3, anc_t[k], war_t[k], alpha, polys[k], stats_t[k])
+        if overlap:
+            eb = torch.cuda.Event()
+            eb.record(stream_b)
+            stream.wait_event(eb)
         if world > 1:
             dist.all_reduce(stats_t)
+        e2.record(stream)
         if timed:
-            e2.record(stream)
             ev["step"].append((e0, e2))
             ev["emdq"].append((e0, e1))
             ev["blend"].append((e1, e2))
 
     for _ in range(args.warmup):
-        step(False)
+        step(False, args.overlap)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -311,28 +322,52 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    l0 = ctx.launch_count()
-    ctx.profile(True)
+    l0 = ctx.launch_count() + ctx_b.launch_count()
     clk.mark("start")
     for _ in range(args.steps):
-        step(True)
+        step(True, args.overlap)
     torch.cuda.synchronize()
     clk.mark("end")
-    launches = (ctx.launch_count() - l0)
-    kt = ctx.kernel_times()
-    ctx.profile(False)
+    launches = ctx.launch_count() + ctx_b.launch_count() - l0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in ev.items()}
+    # per-kernel CUDA-event timing in a separate serialised pass (kernels alone
+    # on the GPU, L2 flushed per step) for the roofline
+    prof_steps = max(20, min(200, args.steps))
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ctx_b.profile(True)
+    for _ in range(prof_steps):
+        flush.fill_(1)
+        step(False, overlap=False) if not args.overlap else None
+        if args.overlap:
+            e = torch.cuda.Event()
+            M.emdq_field_device(grid, apts_t, loc_t, prob_t, act_t, alpha, beta, disp_t, unc_t, 16, ctx=ctx)
+            e.record(stream)
+            stream_b.wait_event(e)
+            for k in range(nfr):
+                M.blend_frame_device(cv, frame_t, fw, fh, 3, anc_t[k], war_t[k], alpha, polys[k], stats_t[k])
+            eb = torch.cuda.Event()
+            eb.record(stream_b)
+            stream.wait_event(eb)
+    torch.cuda.synchronize()
+    kt = dict(ctx.kernel_times())
+    for k2, v in ctx_b.kernel_times().items():
+        a = kt.get(k2, (0.0, 0))
+        kt[k2] = (a[0] + v[0], a[1] + v[1])
+    ctx.profile(False)
+    ctx_b.profile(False)
     tmax = ms["step"]
     if world > 1:
         t = torch.tensor([tmax], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tmax = float(t.item())
     st = stats_t.cpu().numpy()
-    exc_blend, exc_emdq = ctx.exceptions()
+    exc_emdq = ctx.exceptions()[1]
+    exc_blend = (ctx_b if args.overlap else ctx).exceptions()[0]
     mpix_step = nfr * fw * fh / 1e6
     value = mpix_step * args.steps / (tmax * 1e-3)
 
@@ -446,6 +481,7 @@ def main():
                        "inliers": int(len(e.active)), "nodes": int(len(wl.anchors)), "canvas": wl.canvas,
                        "frames_per_step": nfr, "parallelism": f"band{world}" if world > 1 else "single",
                        "l2": "flushed between steps (256 MiB write, untimed)",
+                       "streams": "K3 || K1 on two CUDA streams" if args.overlap else "K3 then K1, one stream",
                        "blend_stats_frame0": [int(v) for v in st[0]],
                        "exact_tier_pixels": {"blend_last_frame": int(exc_blend), "emdq_last_frame": int(exc_emdq)}},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
