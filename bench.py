@@ -344,10 +344,10 @@ def main():
         flush.fill_(1)
         step(False, overlap=False) if not args.overlap else None
         if args.overlap:
-            e = torch.cuda.Event()
+            ea = torch.cuda.Event()
             M.emdq_field_device(grid, apts_t, loc_t, prob_t, act_t, alpha, beta, disp_t, unc_t, 16, ctx=ctx)
-            e.record(stream)
-            stream_b.wait_event(e)
+            ea.record(stream)
+            stream_b.wait_event(ea)
             for k in range(nfr):
                 M.blend_frame_device(cv, frame_t, fw, fh, 3, anc_t[k], war_t[k], alpha, polys[k], stats_t[k])
             eb = torch.cuda.Event()
