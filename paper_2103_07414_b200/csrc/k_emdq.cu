@@ -690,6 +690,7 @@ struct FastOut {
 // Bound on |FP32 d^2 - exact d^2| for tile-local coordinates.
 __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
+template <int MS>
 __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsigned char* __restrict__ wl,
                                            int nxin, int namb, int m, const PixSmem& s, FastOut& o) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
@@ -706,13 +707,57 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
 #pragma unroll 4
     for (int k = 0; k < nin; ++k) take(k);
     for (int e = 0; e < nxin; ++e) take(wl[e]);
-    // m smallest ambiguous keys by repeated minimum selection (m is ~2,
-    // namb ~5 per pixel); pass m + 1 finds the first rejected key for the
-    // near-tie test.
     bool exact = false;
-    if (m > 0) {
-        const float ux = (float)col, uy = (float)row;
-        const unsigned char* amb = wl + nxin;
+    const float ux = (float)col, uy = (float)row;
+    const unsigned char* amb = wl + nxin;
+    if (MS > 0) {
+        // sorted insertion of the ambiguous keys (closest-to-centre first, so
+        // most later keys are rejected by one compare) into m <= MS slots
+        float sd[MS > 0 ? MS : 1];
+        int sk[MS > 0 ? MS : 1];
+#pragma unroll
+        for (int q = 0; q < MS; ++q) {
+            sd[q] = FLT_MAX;
+            sk[q] = 0;
+        }
+        float rej = FLT_MAX, worst = FLT_MAX;
+        for (int e = 0; e < namb; ++e) {
+            const int k = amb[e];
+            const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[k]);
+            const float dx = u.x - ux, dy = u.y - uy;
+            const float d2 = fmaf(dx, dx, dy * dy);
+            if (!(d2 < worst)) {
+                rej = fminf(rej, d2);
+                continue;
+            }
+            rej = fminf(rej, worst);  // the current last member is evicted (or a sentinel)
+            bool lt[MS > 0 ? MS : 1];
+#pragma unroll
+            for (int q = 0; q < MS; ++q) lt[q] = d2 < sd[q];
+#pragma unroll
+            for (int q = MS - 1; q >= 0; --q) {
+                if (q < m) {
+                    if (q > 0 && lt[q - 1]) {
+                        sd[q] = sd[q - 1];
+                        sk[q] = sk[q - 1];
+                    } else if (lt[q]) {
+                        sd[q] = d2;
+                        sk[q] = k;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < MS; ++q)
+                if (q == m - 1) worst = sd[q];
+        }
+        // near-tie between the last member and the first rejected key
+        if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
+#pragma unroll
+        for (int q = 0; q < MS; ++q)
+            if (q < m) take(sk[q]);
+    } else if (m > 0) {
+        // many free slots (rare): repeated minimum selection; pass m + 1
+        // finds the first rejected key for the near-tie test
         unsigned taken = 0u;
         float last = 0.f;
         for (int r = 0; r <= m; ++r) {
@@ -728,7 +773,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
                     bi = e;
                 }
             }
-            if (r == m) {  // first rejected vs last selected
+            if (r == m) {
                 if (bi >= 0 && !(best - last > d2_tol(best))) exact = true;
                 break;
             }
@@ -738,6 +783,16 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         }
     }
     o = FastOut{a0, a1, a2, a3, a4, a5, exact};
+}
+
+__device__ __forceinline__ void fast_dispatch(int col, int row, int nin, const unsigned char* wl, int nxin,
+                                              int namb, int m, const PixSmem& s, FastOut& o) {
+    if (m <= 4)
+        fast_pixel<4>(col, row, nin, wl, nxin, namb, m, s, o);
+    else if (m <= 8)
+        fast_pixel<8>(col, row, nin, wl, nxin, namb, m, s, o);
+    else
+        fast_pixel<0>(col, row, nin, wl, nxin, namb, m, s, o);
 }
 
 // ---------------------------------------------------------------------------
@@ -810,7 +865,7 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     FastOut fo;
     bool ex = nxin == 255 || m < 0 || wi + namb < S || namb > 32;
     if (!ex) {
-        fast_pixel(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s, fo);
+        fast_dispatch(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s, fo);
         ex = fo.exact || !(fo.s5 > 0.f);
     }
     if (ex) {
