@@ -118,14 +118,9 @@ struct PlanWarp {
 };
 
 // Pixel-kernel shared memory (one tile).
-// Per staged point, one 160-byte record so the per-pixel loops address
-// everything from a single advancing pointer with immediate offsets:
-//   [0,16) ex[col], [16,32) ey[row] (separable weights, prob folded into ey),
-//   [32,36) conjugated dual quaternion, 36 s - s0, [38,40) ux, uy.
-constexpr int RSTRIDE = 40;
 struct PixSmem {
     TilePlan p;
-    float rec[TREC][RSTRIDE];
+    float ex[TREC][ET], ey[TREC][ET];  // separable weights: w = ex[k][col] * ey[k][row]
 };
 struct SSmem {
     int hist[256];
@@ -699,23 +694,18 @@ template <int MS>
 __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsigned char* __restrict__ wl,
                                            int nxin, int namb, int m, const PixSmem& s, FastOut& o) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
-    const float* R = &s.rec[0][0];
-    auto take_r = [&](const float* r) {
-        const float w = r[col] * r[ET + row];
-        const float4 q = *reinterpret_cast<const float4*>(r + 32);
+    auto take = [&](int k) {
+        const float w = s.ex[k][col] * s.ey[k][row];
+        const float4 q = s.p.rec1[k];
         a0 = fmaf(w, q.x, a0);
         a1 = fmaf(w, q.y, a1);
         a2 = fmaf(w, q.z, a2);
         a3 = fmaf(w, q.w, a3);
-        a4 = fmaf(w, r[36], a4);
+        a4 = fmaf(w, s.p.rec0[k].w, a4);
         a5 += w;
     };
-    auto take = [&](int k) { take_r(R + k * RSTRIDE); };
-    {
-        const float* r = R;
 #pragma unroll 4
-        for (int k = 0; k < nin; ++k, r += RSTRIDE) take_r(r);
-    }
+    for (int k = 0; k < nin; ++k) take(k);
     for (int e = 0; e < nxin; ++e) take(wl[e]);
     bool exact = false;
     const float ux = (float)col, uy = (float)row;
@@ -733,7 +723,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         float rej = FLT_MAX, worst = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
             const int k = amb[e];
-            const float2 u = *reinterpret_cast<const float2*>(R + k * RSTRIDE + 38);
+            const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[k]);
             const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
             if (!(d2 < worst)) {
@@ -775,7 +765,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
             int bi = -1;
             for (int e = 0; e < namb; ++e) {
                 if ((taken >> e) & 1u) continue;
-                const float2 u = *reinterpret_cast<const float2*>(R + amb[e] * RSTRIDE + 38);
+                const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[amb[e]]);
                 const float dx = u.x - ux, dy = u.y - uy;
                 const float d2 = fmaf(dx, dx, dy * dy);
                 if (d2 < best) {
@@ -847,31 +837,21 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     const TileHdr& h = s.p.hdr;
     const int ne = h.ne, nin = h.nin;
     const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
-    // per-point records: separable weight tables (prob and the tile-wide d^2
-    // floor folded into ey), conjugated warp, s - s0 and local coordinates
+    // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
     if (!(flags & TFLAG_EXACT_STAGED)) {
         const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
-        for (int e = t; e < ne * RSTRIDE; e += ENT) {
-            const int k = e / RSTRIDE, c = e % RSTRIDE;
+        for (int e = t; e < ne * 2 * ET; e += ENT) {
+            const int k = e / (2 * ET), c = e % (2 * ET);
             const float4 r0 = s.p.rec0[k];
-            float v;
-            if (c < 2 * ET) {
-                const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
-                const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
-                if (c < ET) {
-                    const float dx = r0.x - (float)c;
-                    v = ex2_approx(nal * (dx * dx - dxr));
-                } else {
-                    const float dy = r0.y - (float)(c - ET);
-                    v = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
-                }
-            } else if (c < 36) {
-                const float4 q = s.p.rec1[k];
-                v = c == 32 ? q.x : c == 33 ? q.y : c == 34 ? q.z : q.w;
+            const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
+            const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
+            if (c < ET) {
+                const float dx = r0.x - (float)c;
+                s.ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
             } else {
-                v = c == 36 ? r0.w : c == 38 ? r0.x : c == 39 ? r0.y : 0.f;
+                const float dy = r0.y - (float)(c - ET);
+                s.ey[k][c - ET] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
             }
-            s.rec[k][c] = v;
         }
     }
     __syncthreads();
