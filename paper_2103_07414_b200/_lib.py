@@ -6,9 +6,12 @@ machine without the built library raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libnrm_b200.so"
+if os.environ.get("NRM_B200_VARIANT"):  # development: tools/variants.py builds
+    LIB_PATH = Path(__file__).resolve().parents[1] / "_variants" / os.environ["NRM_B200_VARIANT"] / "libnrm_b200.so"
 
 NRM_OK, NRM_EINVAL, NRM_ENOSUPPORT, NRM_EDEGENERATE, NRM_ECUDA, NRM_ENOMEM, NRM_ESTATE = range(7)
 

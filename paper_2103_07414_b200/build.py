@@ -53,25 +53,26 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build_lib(force: bool = False) -> Path:
+def build_lib(force: bool = False, extra_flags: tuple = (), lib: Path = LIB, objdir: Path = OBJ) -> Path:
+    """extra_flags/lib/objdir: development variants (tools/variants.py)."""
     nvcc = _nvcc()
-    OBJ.mkdir(exist_ok=True)
+    objdir.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "nrm_b200.h"]
     objs = []
     jobs = []
     for src in SOURCES:
         s = CSRC / src
-        o = OBJ / (s.stem + ".o")
+        o = objdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([nvcc, *NVCC_FLAGS, "-c", str(s), "-o", str(o)])
+            jobs.append([nvcc, *NVCC_FLAGS, *extra_flags, "-c", str(s), "-o", str(o)])
     if jobs:
         with ThreadPoolExecutor(max_workers=min(4, len(jobs))) as ex:
-            list(ex.map(lambda c: _run(c, OBJ / (Path(c[-1]).stem + ".ptxas.log")), jobs))
-    if force or jobs or _stale(LIB, objs):
-        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB),
+            list(ex.map(lambda c: _run(c, objdir / (Path(c[-1]).stem + ".ptxas.log")), jobs))
+    if force or jobs or _stale(lib, objs):
+        _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib),
               *map(str, objs), "-cudart", "static", "-Xcompiler", "-fPIC"])
-    return LIB
+    return lib
 
 
 def build_oracle() -> None:

@@ -53,7 +53,10 @@ constexpr int ST = 64;            // supertile edge (4 x 4 tiles)
 constexpr int WCAP_S = 256;       // per-warp gather capacity in the supertile pass
 constexpr int SLIST_CAP = 1024;   // supertile list capacity
 constexpr int SFLAG_OVERFLOW = 1, SFLAG_NONUNIFORM = 2;
-constexpr int EMDQ_CHUNK_TILES = 16384;  // tile plans resident per launch chunk
+constexpr int EMDQ_CHUNK_TILES = 16384;
+#ifndef NRM_PIX_MINB
+#define NRM_PIX_MINB 4  // k_pixels resident CTAs per SM (register budget: 64)
+#endif  // tile plans resident per launch chunk
 
 // Gathered candidate arrays (one entry per active index, in active order).
 struct Cand {
@@ -93,6 +96,7 @@ struct __align__(16) TilePlan {
     TileHdr hdr;
     float4 rec0[TREC];                  // ux, uy (tile-local), prob, s - s0
     float4 rec1[TREC];                  // conjugated dual quaternion
+    double2 axy[TREC];                  // absolute coordinates (exact d^2 for the uncertainty)
     int sidx[TREC];                     // candidate indices (exact-tier fallback)
     unsigned char sub[NW][TREC];        // per sub-tile: extra sure, then ambiguous
     unsigned char near[NW][NEAR_CAP];   // per sub-tile: points that can be the nearest
@@ -570,6 +574,7 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
         const double ux = C.x[a] - ox, uy = C.y[a] - oy;
         r0g[k] = make_float4((float)ux, (float)uy, (float)C.p[a], (float)(q.s - s0));
         sg[k] = a;
+        tp.axy[k] = make_double2(C.x[a], C.y[a]);
         w.ux[k] = (float)ux;
         w.uy[k] = (float)uy;
         const double dxn = fmax(fmax(-ux, 0.0), ux - (xhi - xlo)), dyn = fmax(fmax(-uy, 0.0), uy - (yhi - ylo));
@@ -692,16 +697,17 @@ __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
 template <int MS>
 __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsigned char* __restrict__ wl,
-                                           int nxin, int namb, int m, const PixSmem& s, FastOut& o) {
+                                           int nxin, int namb, int m, const TilePlan& p, const float (*ex)[ET],
+                                           const float (*ey)[ET], FastOut& o) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f, a5 = 0.f;
     auto take = [&](int k) {
-        const float w = s.ex[k][col] * s.ey[k][row];
-        const float4 q = s.p.rec1[k];
+        const float w = ex[k][col] * ey[k][row];
+        const float4 q = p.rec1[k];
         a0 = fmaf(w, q.x, a0);
         a1 = fmaf(w, q.y, a1);
         a2 = fmaf(w, q.z, a2);
         a3 = fmaf(w, q.w, a3);
-        a4 = fmaf(w, s.p.rec0[k].w, a4);
+        a4 = fmaf(w, p.rec0[k].w, a4);
         a5 += w;
     };
 #pragma unroll 4
@@ -723,7 +729,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         float rej = FLT_MAX, worst = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
             const int k = amb[e];
-            const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[k]);
+            const float2 u = *reinterpret_cast<const float2*>(&p.rec0[k]);
             const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
             if (!(d2 < worst)) {
@@ -765,7 +771,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
             int bi = -1;
             for (int e = 0; e < namb; ++e) {
                 if ((taken >> e) & 1u) continue;
-                const float2 u = *reinterpret_cast<const float2*>(&s.p.rec0[amb[e]]);
+                const float2 u = *reinterpret_cast<const float2*>(&p.rec0[amb[e]]);
                 const float dx = u.x - ux, dy = u.y - uy;
                 const float d2 = fmaf(dx, dx, dy * dy);
                 if (d2 < best) {
@@ -786,29 +792,29 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
 }
 
 __device__ __forceinline__ void fast_dispatch(int col, int row, int nin, const unsigned char* wl, int nxin,
-                                              int namb, int m, const PixSmem& s, FastOut& o) {
+                                              int namb, int m, const TilePlan& p, const float (*ex)[ET],
+                                              const float (*ey)[ET], FastOut& o) {
     if (m <= 4)
-        fast_pixel<4>(col, row, nin, wl, nxin, namb, m, s, o);
+        fast_pixel<4>(col, row, nin, wl, nxin, namb, m, p, ex, ey, o);
     else if (m <= 8)
-        fast_pixel<8>(col, row, nin, wl, nxin, namb, m, s, o);
+        fast_pixel<8>(col, row, nin, wl, nxin, namb, m, p, ex, ey, o);
     else
-        fast_pixel<0>(col, row, nin, wl, nxin, namb, m, s, o);
+        fast_pixel<0>(col, row, nin, wl, nxin, namb, m, p, ex, ey, o);
 }
 
 // ---------------------------------------------------------------------------
-// k_pixels: one CTA per 16 x 16 tile, warp w = 8 x 4 sub-tile w.
+// One 16 x 16 tile whose plan is staged in shared memory (warp w = 8 x 4
+// sub-tile w). Contains one block barrier, taken by all threads or none
+// (the tile flags are uniform).
 // ---------------------------------------------------------------------------
 template <int MAXS>
-__global__ void __launch_bounds__(ENT, 3)
-k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
-    __shared__ __align__(16) PixSmem s;
+__device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, const SuperLists& SL, const PixSmem& s,
+                                            float (*ex)[ET], float (*ey)[ET], int tx, int ty, int S) {
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int g = blockIdx.y * TP.ntx + blockIdx.x;
-    const int tx = TP.tx0 + blockIdx.x, ty = TP.ty0 + blockIdx.y;
     const int ti0 = L.grid.i0 + tx * ET, tj0 = L.grid.j0 + ty * ET;
     const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
-    const TileHdr& hg = TP.plan[g].hdr;
-    const int flags = hg.flags;
+    const TileHdr& h = s.p.hdr;
+    const int flags = h.flags;
 
     const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
     const int pi = ti0 + lx, pj = tj0 + ly;
@@ -827,14 +833,6 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         }
         return;
     }
-    // stage the whole plan with 16-byte loads
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(&TP.plan[g]);
-        uint4* dst = reinterpret_cast<uint4*>(&s.p);
-        for (int k = t; k < (int)(sizeof(TilePlan) / 16); k += ENT) dst[k] = src[k];
-    }
-    __syncthreads();
-    const TileHdr& h = s.p.hdr;
     const int ne = h.ne, nin = h.nin;
     const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
     // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
@@ -847,10 +845,10 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
             const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
             if (c < ET) {
                 const float dx = r0.x - (float)c;
-                s.ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
+                ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
             } else {
                 const float dy = r0.y - (float)(c - ET);
-                s.ey[k][c - ET] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
+                ey[k][c - ET] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
             }
         }
     }
@@ -863,12 +861,12 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     }
     const int wi = nin + nxin, m = S - wi;
     FastOut fo;
-    bool ex = nxin == 255 || m < 0 || wi + namb < S || namb > 32;
-    if (!ex) {
-        fast_dispatch(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s, fo);
-        ex = fo.exact || !(fo.s5 > 0.f);
+    bool exr = nxin == 255 || m < 0 || wi + namb < S || namb > 32;
+    if (!exr) {
+        fast_dispatch(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s.p, ex, ey, fo);
+        exr = fo.exact || !(fo.s5 > 0.f);
     }
-    if (ex) {
+    if (exr) {
         if (L.exact_count) atomicAdd(L.exact_count, 1u);
         exact_dispatch<MAXS>(qx, qy, s.p.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
@@ -891,12 +889,28 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         const int nl = nnear == 255 ? ne : nnear;
         for (int e = 0; e < nl; ++e) {
             const int k = nnear == 255 ? e : s.p.near[wid][e];
-            d2m = fmin(d2m, xdist2(qx, qy, C.x[s.p.sidx[k]], C.y[s.p.sidx[k]]));
+            const double2 a = s.p.axy[k];
+            d2m = fmin(d2m, xdist2(qx, qy, a.x, a.y));
         }
         double arg = xmul(L.beta, d2m);
         if (55.0 < arg) arg = 55.0;
         *ou = (float)xexp(arg);
     }
+}
+
+// k_pixels: one CTA per tile.
+template <int MAXS>
+__global__ void __launch_bounds__(ENT, NRM_PIX_MINB)
+k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
+    __shared__ __align__(16) PixSmem s;
+    const int g = blockIdx.y * TP.ntx + blockIdx.x;
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(&TP.plan[g]);
+        uint4* dst = reinterpret_cast<uint4*>(&s.p);
+        for (int k = threadIdx.x; k < (int)(sizeof(TilePlan) / 16); k += ENT) dst[k] = src[k];
+    }
+    __syncthreads();
+    pixels_tile<MAXS>(L, C, SL, s, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
 }
 
 }  // namespace

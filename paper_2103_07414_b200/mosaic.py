@@ -344,10 +344,12 @@ def invert_frame_boundary(frame_w: int, frame_h: int, anchors, warps, alpha: flo
 
 
 def emdq_field(grid, apts, locals_, probs, active, alpha: float, beta: float, support: int = 16,
-               ctx: Optional[Context] = None):
+               ctx: Optional[Context] = None, out=None):
     """Dense EMDQ field: detail::blend_local (fieldest.hpp:75-97) applied at
     every grid pixel plus node_uncertainty (fieldest.hpp:44-52).
-    Returns (disp (h, w, 2) float32, unc (h, w) float32)."""
+    Returns (disp (h, w, 2) float32, unc (h, w) float32).
+    out: optional (disp, unc) host arrays to fill (either may be None to skip
+    that output); page-locked arrays get a readback pipelined with the kernels."""
     ctx = ctx or default_context()
     g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
     ap = _f64(apts, 2, "apts")
@@ -356,8 +358,14 @@ def emdq_field(grid, apts, locals_, probs, active, alpha: float, beta: float, su
     ac = np.ascontiguousarray(active, np.int32).reshape(-1)
     if not (len(ap) == len(lo) == len(pr)):
         raise ValueError("apts / locals / probs size mismatch")
-    disp = np.zeros((g.height, g.width, 2), np.float32)
-    unc = np.zeros((g.height, g.width), np.float32)
+    if out is None:
+        disp = np.zeros((g.height, g.width, 2), np.float32)
+        unc = np.zeros((g.height, g.width), np.float32)
+    else:
+        disp, unc = out
+        for a, shp in ((disp, (g.height, g.width, 2)), (unc, (g.height, g.width))):
+            if a is not None and (a.dtype != np.float32 or a.shape != shp or not a.flags.c_contiguous):
+                raise ValueError(f"out arrays must be C-contiguous float32 of shape {shp}")
     check(ctx._lib.nrm_emdq_field(ctx.handle, C.byref(g), _ptr(ap), _ptr(lo), _ptr(pr), len(ap),
                                   _ptr(ac), len(ac), float(alpha), int(support), float(beta),
                                   _ptr(disp), _ptr(unc)))
