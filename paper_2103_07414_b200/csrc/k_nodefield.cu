@@ -31,7 +31,16 @@
 namespace nrm {
 namespace {
 
-constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = 128, LIST_CAP = 2048;
+#ifndef NRM_K1_CHUNK
+#define NRM_K1_CHUNK 64   // nodes per table chunk
+#endif
+#ifndef NRM_K1_MINB
+#define NRM_K1_MINB 3     // resident CTAs per SM (80 registers)
+#endif
+constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = NRM_K1_CHUNK;
+constexpr int NF_CAP = 512;           // listed nodes per tile plan (more: the tile goes to the exact pass)
+constexpr int NF_CHUNK_TILES = 2048;  // tile plans resident per launch chunk
+constexpr int NF_PLAN_WARPS = 8;      // planning warps (tiles) per CTA
 constexpr int EXC_THREADS = 128;
 constexpr int EXC_BLOCKS = 148;
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
@@ -39,19 +48,28 @@ constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 constexpr double kBoundMargin = 4e-3;
 constexpr unsigned kRingBit = 0x80000000u;
 
+// Per-tile plan written by k_nf_plan (one warp per tile), read by k_node_field.
+enum NfStatus : int { NF_OK = 0, NF_EXACT = 1, NF_EMPTY = 2, NF_OUTSIDE = 3 };
+struct __align__(16) NfHdr {
+    double P[2], Y0[2], e0[2], s0;  // output origin / reference scale (FP64)
+    int count, status, pad0, pad1;
+};
+struct __align__(16) NfEntry {
+    float4 q;      // warp conjugated to the tile origin (T(-P) q T(o))
+    double2 a;     // anchor (absolute, FP64) for the separable tables
+    float d;       // scale - s0
+    unsigned idx;  // node index | kRingBit
+    unsigned pad[2];
+};
+struct __align__(16) NfPlan {
+    NfHdr h;
+    NfEntry e[NF_CAP];
+};
+
 struct Smem {
     float ex[CHUNK][TW];
     float ey[CHUNK][TH];
-    float4 q[CHUNK];
-    float d[CHUNK];
-    int ring[CHUNK];
-    unsigned list[LIST_CAP];
-    int warp_cnt[NT / 32];
-    double red_d[NT / 32];
-    int red_i[NT / 32];
-    double red_lo[NT / 32], red_hi[NT / 32];
-    int count, overflow, uniform;
-    double P[2], Y0[2], e0[2], s0, phi0;
+    NfEntry e[CHUNK];
 };
 
 // K1 only: the tile's canvas values, staged with cp.async at kernel entry.
@@ -79,25 +97,188 @@ __device__ void tile_to_exceptions(const NodeFieldLaunch& L, int ci0, int ci1, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_nf_plan: one warp per tile. Ordered FP64 cull of the nodes against the
+// tile (inner: weight > 1e-6 at every tile pixel; ring: the cutoff crosses
+// the tile), hemisphere arc of the listed warps and the reference node
+// nearest the tile centre, the tile's output origin, and the listed warps
+// conjugated into tile-local coordinates.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
+k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
+          int rows, int ntx) {
+    __shared__ unsigned list_s[NF_PLAN_WARPS][NF_CAP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.x * NF_PLAN_WARPS + wid;
+    if (g >= rows * ntx) return;
+    unsigned* list = list_s[wid];
+    NfPlan& pl = plans[g];
+    const int tix = tile_i0 + g % ntx;
+    const int tjy = tile_row_of(by0 + g / ntx, tile_j0, s1, L.band_count);
+    const int ti0 = tix * TW, tj0 = tjy * TH;
+    const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
+    const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
+    if (tjy < tile_j0 || tjy > tile_j_last || ci0 > ci1 || cj0 > cj1) {
+        if (lane == 0) pl.h.status = NF_OUTSIDE;
+        return;
+    }
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
+    const double xlo = L.grid.gx + ci0, xhi = L.grid.gx + ci1;
+    const double ylo = L.grid.gy + cj0, yhi = L.grid.gy + cj1;
+    const double alpha = L.alpha;
+
+    // ordered cull + classify (index order is kept: the first listed node
+    // seeds the hemisphere arc)
+    int count = 0;
+    for (int base = 0; base < L.n; base += 32) {
+        const int i = base + lane;
+        int status = 0;  // 0 out, 1 inner, 2 ring
+        if (i < L.n) {
+            const double2 a = make_double2(__ldg(&L.anchors[2 * i]), __ldg(&L.anchors[2 * i + 1]));
+            const double dxn = fmax(fmax(xlo - a.x, 0.0), a.x - xhi);
+            const double dyn = fmax(fmax(ylo - a.y, 0.0), a.y - yhi);
+            const double dxf = fmax(a.x - xlo, xhi - a.x), dyf = fmax(a.y - ylo, yhi - a.y);
+            const double amin = alpha * (dxn * dxn + dyn * dyn);
+            const double amax = alpha * (dxf * dxf + dyf * dyf);
+            if (amin <= kLnCutoff + 1e-6) status = amax < kLnCutoff - 1e-5 ? 1 : 2;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, status != 0);
+        const int pos = count + __popc(m & ((1u << lane) - 1u));
+        if (status && pos < NF_CAP) list[pos] = (unsigned)i | (status == 2 ? kRingBit : 0u);
+        count += __popc(m);
+    }
+    if (count > NF_CAP || count == 0) {
+        if (lane == 0) {
+            pl.h.count = count;
+            pl.h.status = count == 0 ? NF_EMPTY : NF_EXACT;
+        }
+        return;
+    }
+    __syncwarp();
+    // hemisphere arc + reference node (nearest the tile centre, lowest index
+    // on ties); the listed warps are loaded once and kept in registers
+    constexpr int KPL = 4;  // entries per lane held in registers (count <= 128)
+    W5 qk[KPL];
+    double2 ak[KPL];
+    const unsigned i0 = list[0] & ~kRingBit;
+    const double phi0 = atan2(__ldg(&L.warps[5 * i0 + 2]), __ldg(&L.warps[5 * i0 + 1]));
+    double lo = 0.0, hi = 0.0, best = 1e300;
+    int besti = 0x7fffffff;
+    const double cxm = ox + 0.5 * TW, cym = oy + 0.5 * TH;
+    auto arc = [&](unsigned i, const W5& q, const double2& a) {
+        double rel = atan2(q.z, q.w) - phi0;
+        if (rel > M_PI) rel -= 2.0 * M_PI;
+        if (rel < -M_PI) rel += 2.0 * M_PI;
+        lo = fmin(lo, rel);
+        hi = fmax(hi, rel);
+        const double ddx = a.x - cxm, ddy = a.y - cym;
+        const double d2 = ddx * ddx + ddy * ddy;
+        if (d2 < best || (d2 == best && (int)i < besti)) {
+            best = d2;
+            besti = (int)i;
+        }
+    };
+#pragma unroll
+    for (int r = 0; r < KPL; ++r) {
+        const int k = lane + 32 * r;
+        if (k < count) {
+            const unsigned i = list[k] & ~kRingBit;
+            qk[r] = load_w5(&L.warps[5 * i]);
+            ak[r] = make_double2(__ldg(&L.anchors[2 * i]), __ldg(&L.anchors[2 * i + 1]));
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < KPL; ++r)
+        if (lane + 32 * r < count) arc(list[lane + 32 * r] & ~kRingBit, qk[r], ak[r]);
+    for (int k = lane + 32 * KPL; k < count; k += 32) {
+        const unsigned i = list[k] & ~kRingBit;
+        arc(i, load_w5(&L.warps[5 * i]), make_double2(__ldg(&L.anchors[2 * i]), __ldg(&L.anchors[2 * i + 1])));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        const double bd = __shfl_xor_sync(0xffffffffu, best, o);
+        const int bi = __shfl_xor_sync(0xffffffffu, besti, o);
+        if (bd < best || (bd == best && bi < besti)) {
+            best = bd;
+            besti = bi;
+        }
+    }
+    const W5 qr = load_w5(&L.warps[5 * besti]);
+    double yx, yy;
+    xapply(qr, ox, oy, &yx, &yy);
+    const double s0 = qr.s;
+    const double Y00 = rint(yx), Y01 = rint(yy);
+    const double P0 = Y00 / s0, P1 = Y01 / s0;
+    const bool uniform = (hi - lo) < (0.5 * M_PI - 1e-6) && s0 > 0.0 && isfinite(P0) && isfinite(P1);
+    if (lane == 0) {
+        pl.h.P[0] = P0;
+        pl.h.P[1] = P1;
+        pl.h.Y0[0] = Y00;
+        pl.h.Y0[1] = Y01;
+        pl.h.e0[0] = fma(s0, P0, -Y00);
+        pl.h.e0[1] = fma(s0, P1, -Y01);
+        pl.h.s0 = s0;
+        pl.h.count = count;
+        pl.h.status = uniform ? NF_OK : NF_EXACT;
+    }
+    if (!uniform) return;
+    // listed warps in tile-local coordinates
+    auto conj = [&](int k, const W5& q, const double2& a) {
+        // qa = q * T(o): applies the tile-origin translation first
+        const double hx = 0.5 * ox, hy = 0.5 * oy;
+        const double qa_dx = (q.w * hx - q.z * hy) + q.dx;
+        const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
+        // q' = T(-P) * qa
+        const double px = 0.5 * P0, py = 0.5 * P1;
+        const double qdx = qa_dx + (-px * q.w - py * q.z);
+        const double qdy = qa_dy + (px * q.z - py * q.w);
+        NfEntry en;
+        en.q = make_float4((float)q.w, (float)q.z, (float)qdx, (float)qdy);
+        en.a = a;
+        en.d = (float)(q.s - s0);
+        en.idx = list[k];
+        en.pad[0] = en.pad[1] = 0u;
+        pl.e[k] = en;
+    };
+#pragma unroll
+    for (int r = 0; r < KPL; ++r)
+        if (lane + 32 * r < count) conj(lane + 32 * r, qk[r], ak[r]);
+    for (int k = lane + 32 * KPL; k < count; k += 32) {
+        const unsigned i = list[k] & ~kRingBit;
+        conj(k, load_w5(&L.warps[5 * i]), make_double2(__ldg(&L.anchors[2 * i]), __ldg(&L.anchors[2 * i + 1])));
+    }
+}
+
+__device__ __forceinline__ void stage_entries(NfEntry* dst, const NfEntry* src, int n) {
+    constexpr int kC = (int)(sizeof(NfEntry) / 16);
+    for (int c = threadIdx.x; c < n * kC; c += NT)
+        cp_async16(reinterpret_cast<char*>(dst) + 16 * c, reinterpret_cast<const char*>(src) + 16 * c);
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(NT, 2)
-k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s1) {
+__global__ void __launch_bounds__(NT, NRM_K1_MINB)
+k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
+             int ntx) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
-    const int lane = t & 31, wid = t >> 5;
+    const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x];
+    const int status = pl.h.status;
+    if (status == NF_OUTSIDE) return;
 
     const int tix = tile_i0 + blockIdx.x;
-    const int tjy = tile_row_of(blockIdx.y, tile_j0, s1, L.band_count);
-    if (tjy < tile_j0 || tjy > tile_j_last) return;
+    const int tjy = tile_row_of(by0 + blockIdx.y, tile_j0, s1, L.band_count);
     const int ti0 = tix * TW, tj0 = tjy * TH;
     const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
     const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
-    if (ci0 > ci1 || cj0 > cj1) return;
+    const int count = pl.h.count;
 
     // ---- 0. stage the canvas tile (whole 64 x 32 tile lies in the canvas:
     //         tiles and canvas bounds are both 32/64-aligned, mosaic.hpp:141-151)
+    //         and the first chunk of the tile's plan
     if (MODE == 0) {
         const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (ti0 - L.phys_x0);
         constexpr int kF = TW / 4;       // 16-byte chunks per float row
@@ -114,65 +295,18 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
                 cp_async16(&ct.w[r][16 * k], L.W + base + (long long)r * L.pitch + 16 * k);
             }
         }
-        cp_async_commit();
     }
+    if (status == NF_OK) stage_entries(s.e, pl.e, min(CHUNK, count));
+    cp_async_commit();
 
-    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
-    const double xlo = L.grid.gx + ci0, xhi = L.grid.gx + ci1;
-    const double ylo = L.grid.gy + cj0, yhi = L.grid.gy + cj1;
-    const double alpha = L.alpha;
-
-    // ---- A. ordered cull + classify (FP64) ----------------------------
-    if (t == 0) {
-        s.count = 0;
-        s.overflow = 0;
-    }
-    __syncthreads();
-    for (int base = 0; base < L.n; base += NT) {
-        const int i = base + t;
-        int status = 0;  // 0 out, 1 inner, 2 ring
-        if (i < L.n) {
-            const double ax = __ldg(&L.anchors[2 * i]), ay = __ldg(&L.anchors[2 * i + 1]);
-            const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi);
-            const double dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
-            const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
-            const double amin = alpha * (dxn * dxn + dyn * dyn);
-            const double amax = alpha * (dxf * dxf + dyf * dyf);
-            if (amin <= kLnCutoff + 1e-6) status = amax < kLnCutoff - 1e-5 ? 1 : 2;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, status != 0);
-        if (lane == 0) s.warp_cnt[wid] = __popc(m);
-        __syncthreads();
-        int off = s.count;
-        for (int w = 0; w < wid; ++w) off += s.warp_cnt[w];
-        if (status) {
-            const int pos = off + __popc(m & ((1u << lane) - 1u));
-            if (pos < LIST_CAP)
-                s.list[pos] = (unsigned)i | (status == 2 ? kRingBit : 0u);
-            else
-                s.overflow = 1;
-        }
-        __syncthreads();
-        if (t == 0) {
-            int tot = 0;
-            for (int w = 0; w < NT / 32; ++w) tot += s.warp_cnt[w];
-            s.count += tot;
-            if (s.count > 0 && base == 0) {
-                const unsigned i0 = s.list[0] & ~kRingBit;
-                s.phi0 = atan2(__ldg(&L.warps[5 * i0 + 2]), __ldg(&L.warps[5 * i0 + 1]));
-            }
-        }
-        __syncthreads();
-    }
-    const int count = s.count;
-    if (s.overflow) {
+    if (status == NF_EXACT) {
         tile_to_exceptions(L, ci0, ci1, cj0, cj1);
-        if (MODE == 0) cp_async_wait_all();
+        cp_async_wait_all();
         return;
     }
 
     // ---- B. no node reaches the tile: every pixel lacks support ----------
-    if (count == 0) {
+    if (status == NF_EMPTY) {
         int ns = 0;
         for (int e = t; e < (ci1 - ci0 + 1) * (cj1 - cj0 + 1); e += NT) {
             const int w = ci1 - ci0 + 1;
@@ -184,83 +318,13 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
             }
             ++ns;
         }
-        if (MODE == 0) {
-            cp_async_wait_all();
-            block_add3<NT>(L.acc, 0, ns, 0);
-        }
+        cp_async_wait_all();
+        if (MODE == 0) block_add3<NT>(L.acc, 0, ns, 0);
         return;
     }
-
-    // ---- C. hemisphere arc + per-tile reference (FP64) -----------------
-    {
-        const double phi0 = s.phi0;
-        double lo = 0.0, hi = 0.0, best = 1e300;
-        int besti = 0x7fffffff;
-        const double cxm = ox + 0.5 * TW, cym = oy + 0.5 * TH;
-        for (int k = t; k < count; k += NT) {
-            const unsigned i = s.list[k] & ~kRingBit;
-            double rel = atan2(__ldg(&L.warps[5 * i + 2]), __ldg(&L.warps[5 * i + 1])) - phi0;
-            if (rel > M_PI) rel -= 2.0 * M_PI;
-            if (rel < -M_PI) rel += 2.0 * M_PI;
-            lo = fmin(lo, rel);
-            hi = fmax(hi, rel);
-            const double ddx = __ldg(&L.anchors[2 * i]) - cxm, ddy = __ldg(&L.anchors[2 * i + 1]) - cym;
-            const double d2 = ddx * ddx + ddy * ddy;
-            if (d2 < best || (d2 == best && (int)i < besti)) {
-                best = d2;
-                besti = (int)i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-            const double bd = __shfl_xor_sync(0xffffffffu, best, o);
-            const int bi = __shfl_xor_sync(0xffffffffu, besti, o);
-            if (bd < best || (bd == best && bi < besti)) {
-                best = bd;
-                besti = bi;
-            }
-        }
-        if (lane == 0) {
-            s.red_lo[wid] = lo;
-            s.red_hi[wid] = hi;
-            s.red_d[wid] = best;
-            s.red_i[wid] = besti;
-        }
-        __syncthreads();
-        if (t == 0) {
-            for (int w = 1; w < NT / 32; ++w) {
-                lo = fmin(lo, s.red_lo[w]);
-                hi = fmax(hi, s.red_hi[w]);
-                if (s.red_d[w] < best || (s.red_d[w] == best && s.red_i[w] < besti)) {
-                    best = s.red_d[w];
-                    besti = s.red_i[w];
-                }
-            }
-            int uniform = (hi - lo) < (0.5 * M_PI - 1e-6);
-            const W5 qr = load_w5(&L.warps[5 * besti]);
-            double yx, yy;
-            xapply(qr, ox, oy, &yx, &yy);
-            const double s0 = qr.s;
-            s.s0 = s0;
-            s.Y0[0] = rint(yx);
-            s.Y0[1] = rint(yy);
-            s.P[0] = s.Y0[0] / s0;
-            s.P[1] = s.Y0[1] / s0;
-            s.e0[0] = fma(s0, s.P[0], -s.Y0[0]);
-            s.e0[1] = fma(s0, s.P[1], -s.Y0[1]);
-            if (!(s0 > 0.0) || !isfinite(s.P[0]) || !isfinite(s.P[1])) uniform = 0;
-            s.uniform = uniform;
-        }
-        __syncthreads();
-    }
-    if (!s.uniform) {
-        tile_to_exceptions(L, ci0, ci1, cj0, cj1);
-        if (MODE == 0) cp_async_wait_all();
-        return;
-    }
-    const double P0 = s.P[0], P1 = s.P[1], s0 = s.s0;
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
+    const double alpha = L.alpha;
+    const double P0 = pl.h.P[0], P1 = pl.h.P[1], s0 = pl.h.s0;
 
     // ---- D. main loop over node chunks -----------------------------------
     const int col = t & (TW - 1);
@@ -270,49 +334,37 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
     for (int j = 0; j < RPT; ++j) a0[j] = a1[j] = a2[j] = a3[j] = a4[j] = a5[j] = 0.f;
     unsigned amb = 0;
 
+    const double nal = -alpha * kLog2e;
     for (int c0 = 0; c0 < count; c0 += CHUNK) {
         const int cn = min(CHUNK, count - c0);
-        __syncthreads();
-        for (int k = t; k < cn; k += NT) {
-            const unsigned e = s.list[c0 + k];
-            const unsigned i = e & ~kRingBit;
-            const W5 q = load_w5(&L.warps[5 * i]);
-            // qa = q * T(o): applies the tile-origin translation first
-            const double hx = 0.5 * ox, hy = 0.5 * oy;
-            const double qa_dx = (q.w * hx - q.z * hy) + q.dx;
-            const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
-            // q' = T(-P) * qa
-            const double px = 0.5 * P0, py = 0.5 * P1;
-            const double qdx = qa_dx + (-px * q.w - py * q.z);
-            const double qdy = qa_dy + (px * q.z - py * q.w);
-            s.q[k] = make_float4((float)q.w, (float)q.z, (float)qdx, (float)qdy);
-            s.d[k] = (float)(q.s - s0);
-            s.ring[k] = (e & kRingBit) ? 1 : 0;
+        if (c0 > 0) {  // later chunks (tiles with more than CHUNK listed nodes)
+            __syncthreads();
+            stage_entries(s.e, pl.e + c0, cn);
+            cp_async_commit();
         }
-        const double nal = -alpha * kLog2e;
+        cp_async_wait_all();
+        __syncthreads();
         for (int e = t; e < cn * TW; e += NT) {
             const int k = e / TW, c = e % TW;
-            const unsigned i = s.list[c0 + k] & ~kRingBit;
-            const double dx = __ldg(&L.anchors[2 * i]) - (ox + c);
+            const double dx = s.e[k].a.x - (ox + c);
             s.ex[k][c] = ex2_approx((float)(nal * dx * dx));
         }
         for (int e = t; e < cn * TH; e += NT) {
             const int k = e / TH, r = e % TH;
-            const unsigned i = s.list[c0 + k] & ~kRingBit;
-            const double dy = __ldg(&L.anchors[2 * i + 1]) - (oy + r);
+            const double dy = s.e[k].a.y - (oy + r);
             s.ey[k][r] = ex2_approx((float)(nal * dy * dy));
         }
         __syncthreads();
 
 #pragma unroll 2
         for (int k = 0; k < cn; ++k) {
-            const float4 q = s.q[k];
-            const float dd = s.d[k];
+            const float4 q = s.e[k].q;
+            const float dd = s.e[k].d;
             const float exv = s.ex[k][col];
             const float4 e0 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT]);
             const float4 e1 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT + 4]);
             const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-            if (!s.ring[k]) {
+            if (!(s.e[k].idx & kRingBit)) {
 #pragma unroll
                 for (int j = 0; j < RPT; ++j) {
                     const float w = exv * ey[j];
@@ -342,11 +394,7 @@ k_node_field(NodeFieldLaunch L, int tile_i0, int tile_j0, int tile_j_last, int s
     }
 
     // ---- E. epilogue --------------------------------------------------------
-    if (MODE == 0) {
-        cp_async_wait_all();
-        __syncthreads();
-    }
-    const double Y00 = s.Y0[0], Y01 = s.Y0[1], e00 = s.e0[0], e01 = s.e0[1];
+    const double Y00 = pl.h.Y0[0], Y01 = pl.h.Y0[1], e00 = pl.h.e0[0], e01 = pl.h.e0[1];
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
     int nb = 0, nns = 0, noof = 0;
     const int i = ti0 + col;
@@ -645,6 +693,8 @@ cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double
     return cudaGetLastError();
 }
 
+size_t node_field_plan_bytes() { return (size_t)NF_CHUNK_TILES * sizeof(NfPlan); }
+
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches) {
     const int ti0 = floordiv(L.grid.i0, TW), ti1 = floordiv(L.grid.i1, TW);
     const int tj0 = floordiv(L.grid.j0, TH), tj1 = floordiv(L.grid.j1, TH);
@@ -665,18 +715,28 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
     const size_t base = (sizeof(Smem) + 15) & ~size_t(15);
     const size_t smem = mode == 0 ? base + sizeof(CanvasTile) : sizeof(Smem);
     if (ntx > 0 && nty > 0) {
-        if (mode == 0) {
+        NfPlan* plans = static_cast<NfPlan*>(L.plans);
+        if (mode == 0)
             cudaFuncSetAttribute(k_node_field<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            prof_mark("k_node_field", st);
-            k_node_field<0><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
-        } else {
+        else
             cudaFuncSetAttribute(k_node_field<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int rows_per_chunk = max(1, NF_CHUNK_TILES / ntx);
+        for (int by0 = 0; by0 < nty; by0 += rows_per_chunk) {
+            const int rows = min(rows_per_chunk, nty - by0);
+            if ((size_t)rows * ntx > (size_t)NF_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
+            prof_mark("k_nf_plan", st);
+            k_nf_plan<<<(rows * ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS, NF_PLAN_WARPS * 32, 0, st>>>(
+                L, plans, ti0, tj0, tj1, s1, by0, rows, ntx);
+            ++*launches;
             prof_mark("k_node_field", st);
-            k_node_field<1><<<dim3(ntx, nty), NT, smem, st>>>(L, ti0, tj0, tj1, s1);
+            if (mode == 0)
+                k_node_field<0><<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
+            else
+                k_node_field<1><<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
+            ++*launches;
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
         }
-        ++*launches;
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
     }
     prof_mark("k_node_exceptions", st);
     if (mode == 0)

@@ -130,7 +130,9 @@ struct NodeFieldLaunch {
     unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
     unsigned* exc_last = nullptr;      // pixels the last exception pass resolved (diagnostics)
     unsigned* exc_done = nullptr;      // finished exception CTAs (persistent-zero)
+    void* plans = nullptr;             // tile-plan scratch (node_field_plan_bytes())
 };
+size_t node_field_plan_bytes();
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches);
