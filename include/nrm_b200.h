@@ -178,6 +178,31 @@ int nrm_emdq_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_ap
                           const int32_t *d_active, int nactive, double alpha, int support,
                           double beta, float *d_disp, float *d_unc);
 
+/* ---- EMDQ at scattered points: the EM E-step and the final field --------
+ * detail::blend_local (fieldest.hpp:75-97) at nq query points q[nq][2], in
+ * the exact tier (FP64, the reference's operation order and libm: results
+ * are bit-identical to the reference's). exclude[k] (or NULL: none) is an
+ * original match index left out of query k's candidates: the E-step's
+ * leave-one-out residual passes q = apts, exclude[j] = j over the matches
+ * (fieldest.hpp:195-209); the final field passes the node anchors and no
+ * exclusion (fieldest.hpp:263-270). Outputs (each may be NULL):
+ *   warps[nq][5] = blend_local(q) as {scale, w, z, dx, dy},
+ *   pred[nq][2]  = blend_local(q).apply(q),
+ *   unc[nq]      = bounded_exp(beta * d2min) over the same candidates
+ *                  (node_uncertainty, fieldest.hpp:44-52; beta > 0),
+ *   status[nq]   = 0 ok, 1 no candidate left (the E-step's `others.empty()`),
+ *                  2 dq_blend would throw (no positive weight / degenerate).
+ * Non-zero status leaves warps/pred zero and unc as computed. */
+int nrm_emdq_points(nrm_ctx *ctx, const double *q, const int32_t *exclude, int nq,
+                    const double *apts, const double *locals, const double *probs, int m_total,
+                    const int32_t *active, int nactive, double alpha, int support, double beta,
+                    double *warps, double *pred, double *unc, int32_t *status);
+int nrm_emdq_points_device(nrm_ctx *ctx, const double *d_q, const int32_t *d_exclude, int nq,
+                           const double *d_apts, const double *d_locals, const double *d_probs,
+                           int m_total, const int32_t *d_active, int nactive, double alpha,
+                           int support, double beta, double *d_warps, double *d_pred,
+                           double *d_unc, int32_t *d_status);
+
 /* ---- kernel timing -------------------------------------------------------
  * With profiling on, a CUDA event is recorded on the context stream before
  * every kernel and at the end of every compute call; a kernel's time is the

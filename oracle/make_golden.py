@@ -184,5 +184,28 @@ def main():
     print("done")
 
 
+def estep_cases():
+    """EM E-step leave-one-out (fieldest.hpp:195-209) through the reference's
+    own blend_local / apply: C1 (the reference's EM outputs from emdq_c1), a
+    tiny active set (the `others.empty()` branch) and a C2-sized match set."""
+    R = Reference()
+    g = dict(np.load(OUT / "emdq_c1.npz"))
+    out = {}
+    for name, act in (("c1", g["active"]), ("tiny", g["active"][:1]), ("few", g["active"][:3])):
+        w, pred, emp = R.estep_loo(g["apts"], g["bpts"], g["locals"], g["probs"], act, float(g["alpha"]), 16)
+        out.update({f"{name}_active": act, f"{name}_warps": w, f"{name}_pred": pred, f"{name}_empty": emp})
+    e = W.emdq_inputs(1920, 1080, 2000, 0.2, 7002)
+    sp = W.scaled_params(1920, 1080)
+    w, pred, emp = R.estep_loo(e.apts, e.bpts, e.locals_, e.probs, e.active, sp.alpha, 16)
+    out.update(c2_apts=e.apts, c2_bpts=e.bpts, c2_locals=e.locals_, c2_probs=e.probs, c2_active=e.active,
+               c2_alpha=sp.alpha, c2_warps=w, c2_pred=pred, c2_empty=emp)
+    np.savez_compressed(OUT / "emdq_estep.npz", **out)
+    print("emdq_estep: c2 empty", int(emp.sum()))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["estep"]:
+        estep_cases()
+    else:
+        main()
+        estep_cases()

@@ -288,6 +288,37 @@ int ref_estimate_locals(const double* pa, const double* pb, int n, const double*
     return est->inlier_count;
 }
 
+// The EM E-step's leave-one-out prediction (fieldest.hpp:195-209) for every
+// match j over the candidate set `active`, using the reference's own
+// detail::blend_local and WarpFunction::apply: warps[n*5] (zeros when no
+// other candidate remains), pred[n*2] (bpts[j] in that case, as the
+// reference does), empty[n] = 1 for that case.
+void ref_estep_loo(const double* apts, const double* bpts, const double* locals, const double* probs,
+                   int n, const std::int32_t* active, int nactive, double alpha, int support, double* warps,
+                   double* pred, std::uint8_t* empty) {
+    const auto l = to_warps(locals, n);
+    const auto a = to_vec2(apts, n);
+    const std::vector<double> p(probs, probs + n);
+    std::vector<int> others;
+    for (int j = 0; j < n; ++j) {
+        others.clear();
+        for (int k = 0; k < nactive; ++k)
+            if (active[k] != j) others.push_back(active[k]);
+        empty[j] = others.empty() ? 1 : 0;
+        if (others.empty()) {
+            for (int c = 0; c < 5; ++c) warps[5 * j + c] = 0.0;
+            pred[2 * j] = bpts[2 * j];
+            pred[2 * j + 1] = bpts[2 * j + 1];
+            continue;
+        }
+        const WarpFunction f = detail::blend_local(l, a, p, others, a[j], alpha, support);
+        put_warp(f, &warps[5 * j]);
+        const Vec2 y = f.apply(a[j]);
+        pred[2 * j] = y.x;
+        pred[2 * j + 1] = y.y;
+    }
+}
+
 // warp_update (dualquat.hpp:181-190)
 void ref_warp_update(const double* old5, const double* delta5, double* out5) {
     const auto o = to_warps(old5, 1);

@@ -97,6 +97,10 @@ SIGNATURES = [
                                  C.c_int, C.c_double, _P, _P]),
     ("nrm_emdq_field_device", C.c_int, [_P, C.POINTER(Grid), _P, _P, _P, C.c_int, _P, C.c_int,
                                         C.c_double, C.c_int, C.c_double, _P, _P]),
+    ("nrm_emdq_points", C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, C.c_int, C.c_double, C.c_int,
+                                  C.c_double, _P, _P, _P, _P]),
+    ("nrm_emdq_points_device", C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, C.c_int, C.c_double,
+                                         C.c_int, C.c_double, _P, _P, _P, _P]),
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
     ("nrm_ctx_exceptions", C.c_int, [_P, _I64, _I64]),

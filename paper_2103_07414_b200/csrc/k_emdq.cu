@@ -201,7 +201,7 @@ __device__ __forceinline__ void radius_from_hist(const int* hist, int S, int lan
 // ---------------------------------------------------------------------------
 // Supertile pass: candidate superset + rotation arc for each 64 x 64 block.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists SL, int S) {
+__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists SL, int S, float pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists 
     __syncthreads();
     if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
     __syncthreads();
-    const float lim = s.R + 2.f * hd + 1.f, lim2 = lim * lim;
+    const float lim = s.R + 2.f * hd + 1.f + pad, lim2 = lim * lim;
     // per-warp contiguous chunks keep the list order deterministic
     const int per = (N + NW - 1) / NW;
     const int a0 = wid * per, a1 = min(N, a0 + per);
@@ -299,11 +299,15 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists 
 
 // ---------------------------------------------------------------------------
 // Exact tier: detail::blend_local at (qx, qy) over candidate entries
-// idx[0..n) (or 0..n when idx is null) in the reference's operation order.
+// idx[0..n) (or 0..n when idx is null) in the reference's operation order,
+// skipping the candidate whose original index is `excl` (leave-one-out, the
+// EM E-step fieldest.hpp:195-209; -1: none). Returns 0 with the blended warp
+// and the nearest squared distance, 1 when no candidate remains, 2 when
+// dq_blend would throw (no positive weight or a degenerate real part).
 // ---------------------------------------------------------------------------
 template <int MS>
-__device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, int n, int S, const Cand& C,
-                           double alpha, double beta, float2* out_d, float* out_u) {
+__device__ int emdq_blend_exact(double qx, double qy, const int* __restrict__ idx, int n, int S, const Cand& C,
+                                double alpha, int excl, W5* out, double* d2min_out) {
     double sd[MS];
     int sj[MS], sa[MS];
 #pragma unroll
@@ -312,10 +316,13 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
         sj[s] = INT_MAX;
         sa[s] = -1;
     }
+    int navail = 0;
     for (int e = 0; e < n; ++e) {
         const int a = idx ? idx[e] : e;
-        const double d2 = xdist2(qx, qy, C.x[a], C.y[a]);
         const int j = C.j[a];
+        if (j == excl) continue;
+        ++navail;
+        const double d2 = xdist2(qx, qy, C.x[a], C.y[a]);
         bool lt[MS];
 #pragma unroll
         for (int s = 0; s < MS; ++s) lt[s] = key_less(d2, j, sd[s], sj[s]);
@@ -334,7 +341,10 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
             }
         }
     }
-    // dq_blend (dualquat.hpp:133-162) over the sorted S nearest
+    const int kk = min(S, navail);  // std::min(support, cand.size())
+    *d2min_out = sd[0];
+    if (kk == 0) return 1;
+    // dq_blend (dualquat.hpp:133-162) over the sorted kk nearest
     const double d2min = sd[0];
     const double na = -alpha;
     double w[MS];
@@ -343,7 +353,7 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
 #pragma unroll
     for (int s = 0; s < MS; ++s) {
         w[s] = 0.0;
-        if (s < S) {
+        if (s < kk) {
             w[s] = xmul(xexp(xmul(na, xsub(sd[s], d2min))), C.p[sa[s]]);
             if (w[s] > 0.0 && ref < 0) ref = s;
             wsum = xadd(wsum, w[s]);
@@ -359,7 +369,7 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
         }
 #pragma unroll
     for (int s = 0; s < MS; ++s) {
-        if (s < S && w[s] > 0.0) {
+        if (s < kk && w[s] > 0.0) {
             const double* q = &C.l[5 * sa[s]];
             double qw = q[1], qz = q[2], qdx = q[3], qdy = q[4];
             if (xadd(xmul(qw, rw), xmul(qz, rz)) < 0.0) {
@@ -372,11 +382,24 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
             ss = xadd(ss, xmul(w[s], q[0]));
         }
     }
+    if (ref < 0) return 2;
     const double mw = sw / wsum, mz = sz / wsum, mdx = sdx / wsum, mdy = sdy / wsum;
     const double nr = xhypot(mw, mz);
+    if (!(nr >= 1e-300)) return 2;
+    *out = W5{ss / wsum, mw / nr, mz / nr, mdx / nr, mdy / nr};
+    return 0;
+}
+
+// Dense-grid exact pixel: displacement (NaN where dq_blend would throw) and
+// the uncertainty bounded_exp(beta d2min) (node_uncertainty, fieldest.hpp:44-52).
+template <int MS>
+__device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, int n, int S, const Cand& C,
+                           double alpha, double beta, float2* out_d, float* out_u) {
+    W5 f;
+    double d2min;
+    const int rc = emdq_blend_exact<MS>(qx, qy, idx, n, S, C, alpha, -1, &f, &d2min);
     float2 dout;
-    if (ref >= 0 && nr >= 1e-300) {
-        const W5 f{ss / wsum, mw / nr, mz / nr, mdx / nr, mdy / nr};
+    if (rc == 0) {
         double yx, yy;
         xapply(f, qx, qy, &yx, &yy);
         dout = make_float2((float)(yx - qx), (float)(yy - qy));
@@ -913,13 +936,100 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     pixels_tile<MAXS>(L, C, SL, s, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
 }
 
+// ---------------------------------------------------------------------------
+// k_points: one thread per scattered query, exact tier over the candidate
+// list of the supertile holding the query (k_super with one extra neighbour
+// when a candidate is left out, and a margin for queries between pixels).
+// ---------------------------------------------------------------------------
+template <int MAXS>
+__global__ void __launch_bounds__(128) k_points(EmdqLaunch L, Cand C, SuperLists SL, PointsLaunch P, int S,
+                                                int nsy) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P.nq) return;
+    const double qx = P.q[2 * k], qy = P.q[2 * k + 1];
+    const int excl = P.excl ? P.excl[k] : -1;
+    const int* src = nullptr;
+    int n = L.nactive;
+    if (!P.full_scan) {
+        int sx = (int)floor((qx - L.grid.gx - L.grid.i0) / ST), sy = (int)floor((qy - L.grid.gy - L.grid.j0) / ST);
+        sx = min(max(sx, 0), SL.nsx - 1);
+        sy = min(max(sy, 0), nsy - 1);
+        const int sid = sy * SL.nsx + sx;
+        src = (SL.flag[sid] & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
+        n = SL.count[sid];
+    }
+    W5 f;
+    double d2min;
+    const int rc = (S <= 16 || MAXS <= 16) ? emdq_blend_exact<16>(qx, qy, src, n, S, C, L.alpha, excl, &f, &d2min)
+                                           : emdq_blend_exact<MAXS>(qx, qy, src, n, S, C, L.alpha, excl, &f, &d2min);
+    if (P.status) P.status[k] = rc;
+    if (P.warps) {
+        double* o = &P.warps[5 * k];
+        if (rc == 0) {
+            o[0] = f.s; o[1] = f.w; o[2] = f.z; o[3] = f.dx; o[4] = f.dy;
+        } else {
+            o[0] = o[1] = o[2] = o[3] = o[4] = 0.0;
+        }
+    }
+    if (P.pred) {
+        double yx = 0.0, yy = 0.0;
+        if (rc == 0) xapply(f, qx, qy, &yx, &yy);
+        P.pred[2 * k] = yx;
+        P.pred[2 * k + 1] = yy;
+    }
+    if (P.unc) {
+        double arg = xmul(L.beta, d2min);
+        if (55.0 < arg) arg = 55.0;  // bounded_exp (geometry.hpp:85-88)
+        P.unc[k] = xexp(arg);
+    }
+}
+
+__global__ void k_points_bbox(const double* __restrict__ q, int nq, double* out4) {
+    __shared__ double red[4][32];
+    double mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    for (int k = threadIdx.x; k < nq; k += blockDim.x) {
+        const double x = q[2 * k], y = q[2 * k + 1];
+        mnx = fmin(mnx, x);
+        mny = fmin(mny, y);
+        mxx = fmax(mxx, x);
+        mxy = fmax(mxy, y);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        mnx = fmin(mnx, __shfl_xor_sync(0xffffffffu, mnx, d));
+        mny = fmin(mny, __shfl_xor_sync(0xffffffffu, mny, d));
+        mxx = fmax(mxx, __shfl_xor_sync(0xffffffffu, mxx, d));
+        mxy = fmax(mxy, __shfl_xor_sync(0xffffffffu, mxy, d));
+    }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        red[0][w] = mnx;
+        red[1][w] = mny;
+        red[2][w] = mxx;
+        red[3][w] = mxy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int v = 1; v < (int)(blockDim.x >> 5); ++v) {
+            mnx = fmin(mnx, red[0][v]);
+            mny = fmin(mny, red[1][v]);
+            mxx = fmax(mxx, red[2][v]);
+            mxy = fmax(mxy, red[3][v]);
+        }
+        out4[0] = mnx;
+        out4[1] = mny;
+        out4[2] = mxx;
+        out4[3] = mxy;
+    }
+}
+
 }  // namespace
 
-size_t emdq_scratch_bytes(int nactive, const FieldGrid& g) {
+size_t emdq_scratch_bytes(int nactive, const FieldGrid& g, bool tile_plans) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nsuper = (size_t)nsx * nsy;
-    const size_t plans = (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan);
+    const size_t plans = tile_plans ? (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan) : 0;
     return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
            plans + 1024;
 }
@@ -962,7 +1072,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     const size_t ssm = sizeof(SSmem);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
-    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, S);
+    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, S, 0.f);
     ++*launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -991,6 +1101,67 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
+}
+
+}  // namespace nrm
+
+namespace nrm {
+
+cudaError_t launch_points_bbox(const double* q, int nq, double* out4, cudaStream_t st, int64_t* launches) {
+    prof_mark("k_points_bbox", st);
+    k_points_bbox<<<1, 1024, 0, st>>>(q, nq, out4);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaStream_t st, int64_t* launches) {
+    if (L.nactive <= 0 || P.nq <= 0) return cudaErrorInvalidValue;
+    const size_t na = (size_t)L.nactive;
+    Cand C;
+    C.x = L.cx;
+    C.y = L.cy;
+    C.l = L.cl;
+    C.p = L.cp;
+    double* phi = L.cp + na;
+    C.phi = phi;
+    float2* c32 = reinterpret_cast<float2*>(phi + na);
+    C.c32 = c32;
+    int* cj = reinterpret_cast<int*>(c32 + na);
+    C.j = cj;
+    SuperLists SL;
+    SL.nsx = (L.grid.i1 - L.grid.i0 + ST) / ST;
+    const int nsy = (L.grid.j1 - L.grid.j0 + ST) / ST;
+    const size_t nsuper = (size_t)SL.nsx * nsy;
+    SL.list = cj + na;
+    SL.count = SL.list + nsuper * SLIST_CAP;
+    SL.flag = SL.count + nsuper;
+
+    prof_mark("k_gather", st);
+    k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
+                                                       c32, L.cl, L.cp, phi, cj);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int S = L.support < L.nactive ? L.support : L.nactive;
+    // one more neighbour when a candidate may be left out; queries lie within
+    // one pixel of their supertile's pixel rectangle
+    const int Ssup = min(L.nactive, S + (P.excl ? 1 : 0));
+    if (!P.full_scan) {
+        const size_t ssm = sizeof(SSmem);
+        cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        prof_mark("k_super", st);
+        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, Ssup, 3.f);
+        ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    prof_mark("k_points", st);
+    if (S <= 16)
+        k_points<16><<<(P.nq + 127) / 128, 128, 0, st>>>(L, C, SL, P, S, nsy);
+    else
+        k_points<MAX_SUPPORT><<<(P.nq + 127) / 128, 128, 0, st>>>(L, C, SL, P, S, nsy);
+    ++*launches;
+    return cudaGetLastError();
 }
 
 }  // namespace nrm

@@ -465,6 +465,61 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     return NRM_OK;
 }
 
+// Scattered-query EMDQ (E-step / final field) on device arrays; bbox4 =
+// {minx, miny, maxx, maxy} of the queries.
+constexpr double kPointsSpanMax = 32768.0;  // wider query spreads scan every candidate
+int points_core(nrm_ctx* c, const double* bbox4, const double* d_q, const int32_t* d_excl, int nq,
+                const double* d_apts, const double* d_locals, const double* d_probs, int m_total,
+                const int32_t* d_active, int nactive, double alpha, int support, double beta, double* d_warps,
+                double* d_pred, double* d_unc, int32_t* d_status) {
+    if (nq == 0) return NRM_OK;
+    if (nactive <= 0 || m_total <= 0) return fail(NRM_EINVAL, "emdq_points: no candidates");
+    if (support < 1 || support > 32) return fail(NRM_EINVAL, "emdq_points: support must be in [1, 32]");
+    if (d_unc && (!(beta > 0.0) || !std::isfinite(beta)))
+        return fail(NRM_EINVAL, "node_uncertainty: beta must be positive");
+    if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
+    for (int k = 0; k < 4; ++k)
+        if (!std::isfinite(bbox4[k]) || std::fabs(bbox4[k]) > 1e9)
+            return fail(NRM_EINVAL, "emdq_points: non-finite or out-of-range query");
+    FieldGrid fg;
+    fg.gx = 0.0;
+    fg.gy = 0.0;
+    fg.i0 = (int)std::floor(bbox4[0]);
+    fg.j0 = (int)std::floor(bbox4[1]);
+    fg.i1 = (int)std::floor(bbox4[2]);
+    fg.j1 = (int)std::floor(bbox4[3]);
+    PointsLaunch P;
+    P.full_scan = (bbox4[2] - bbox4[0]) * (bbox4[3] - bbox4[1]) > kPointsSpanMax * kPointsSpanMax;
+    if (P.full_scan) fg.i1 = fg.i0, fg.j1 = fg.j0;
+    const size_t na = (size_t)nactive;
+    NRM_CUDA(c->pts.ensure(emdq_scratch_bytes(nactive, fg, false)));
+    double* base = c->pts.as<double>();
+    EmdqLaunch L;
+    L.grid = fg;
+    L.apts = d_apts;
+    L.locals = d_locals;
+    L.probs = d_probs;
+    L.active = d_active;
+    L.m_total = m_total;
+    L.nactive = nactive;
+    L.alpha = alpha;
+    L.beta = beta;
+    L.support = support;
+    L.cx = base;
+    L.cy = base + na;
+    L.cl = base + 2 * na;
+    L.cp = base + 7 * na;
+    P.q = d_q;
+    P.excl = d_excl;
+    P.nq = nq;
+    P.warps = d_warps;
+    P.pred = d_pred;
+    P.unc = d_unc;
+    P.status = d_status;
+    NRM_CUDA(launch_emdq_points(L, P, c->stream, &c->launches));
+    return NRM_OK;
+}
+
 }  // namespace
 }  // namespace nrm
 
@@ -907,6 +962,78 @@ int nrm_emdq_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_apts
     ProfScope prof_scope(c);
     return emdq_core(c, grid, d_apts, d_locals, d_probs, m_total, d_active, nactive, alpha, support, beta, d_disp,
                      d_unc);
+}
+
+// ---- EMDQ at scattered points (EM E-step, final field) -------------------------
+int nrm_emdq_points(nrm_ctx* c, const double* q, const int32_t* exclude, int nq, const double* apts,
+                    const double* locals, const double* probs, int m_total, const int32_t* active, int nactive,
+                    double alpha, int support, double beta, double* warps, double* pred, double* unc,
+                    int32_t* status) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (nq < 0 || (nq > 0 && !q)) return fail(NRM_EINVAL, "emdq_points: bad query array");
+    if (m_total <= 0 || nactive <= 0 || !apts || !locals || !probs || !active)
+        return fail(NRM_EINVAL, "emdq_points: empty or null candidate arrays");
+    for (int a = 0; a < nactive; ++a)
+        if (active[a] < 0 || active[a] >= m_total) return fail(NRM_EINVAL, "emdq_points: active index out of range");
+    if (!finite_all(apts, (size_t)m_total * 2) || !finite_all(locals, (size_t)m_total * 5))
+        return fail(NRM_EINVAL, "emdq_points: non-finite candidates");
+    if (nq == 0) return NRM_OK;
+    double bb[4] = {q[0], q[1], q[0], q[1]};
+    for (int k = 0; k < nq; ++k) {
+        const double x = q[2 * k], y = q[2 * k + 1];
+        if (!std::isfinite(x) || !std::isfinite(y)) return fail(NRM_EINVAL, "emdq_points: non-finite query");
+        bb[0] = std::min(bb[0], x);
+        bb[1] = std::min(bb[1], y);
+        bb[2] = std::max(bb[2], x);
+        bb[3] = std::max(bb[3], y);
+    }
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    const size_t nqs = (size_t)nq;
+    // queries + exclusions share frame_raw; outputs share out_a
+    NRM_CUDA(c->frame_raw.ensure(nqs * 2 * sizeof(double) + nqs * sizeof(int32_t) + 16));
+    double* d_q = c->frame_raw.as<double>();
+    int32_t* d_ex = exclude ? reinterpret_cast<int32_t*>(d_q + 2 * nqs) : nullptr;
+    NRM_CUDA(cudaMemcpyAsync(d_q, q, nqs * 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (exclude) NRM_CUDA(cudaMemcpyAsync(d_ex, exclude, nqs * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    NRM_CHECK(upload(c, c->anchors, apts, (size_t)m_total * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->locals, locals, (size_t)m_total * 5 * sizeof(double)));
+    NRM_CHECK(upload(c, c->probs, probs, (size_t)m_total * sizeof(double)));
+    NRM_CHECK(upload(c, c->active, active, (size_t)nactive * sizeof(int32_t)));
+    NRM_CUDA(c->out_a.ensure(nqs * 8 * sizeof(double) + nqs * sizeof(int32_t) + 16));
+    double* o = c->out_a.as<double>();
+    double* d_w = warps ? o : nullptr;
+    double* d_p = pred ? o + 5 * nqs : nullptr;
+    double* d_u = unc ? o + 7 * nqs : nullptr;
+    int32_t* d_s = status ? reinterpret_cast<int32_t*>(o + 8 * nqs) : nullptr;
+    NRM_CHECK(points_core(c, bb, d_q, d_ex, nq, c->anchors.as<double>(), c->locals.as<double>(),
+                          c->probs.as<double>(), m_total, c->active.as<int32_t>(), nactive, alpha, support, beta, d_w,
+                          d_p, d_u, d_s));
+    if (warps) NRM_CUDA(cudaMemcpyAsync(warps, d_w, nqs * 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (pred) NRM_CUDA(cudaMemcpyAsync(pred, d_p, nqs * 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (unc) NRM_CUDA(cudaMemcpyAsync(unc, d_u, nqs * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (status) NRM_CUDA(cudaMemcpyAsync(status, d_s, nqs * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+int nrm_emdq_points_device(nrm_ctx* c, const double* d_q, const int32_t* d_exclude, int nq, const double* d_apts,
+                           const double* d_locals, const double* d_probs, int m_total, const int32_t* d_active,
+                           int nactive, double alpha, int support, double beta, double* d_warps, double* d_pred,
+                           double* d_unc, int32_t* d_status) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (nq < 0 || (nq > 0 && !d_q)) return fail(NRM_EINVAL, "emdq_points: bad query array");
+    if (nq == 0) return NRM_OK;
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    NRM_CUDA(c->misc.ensure(256));
+    double* d_bb = reinterpret_cast<double*>(c->misc.as<char>() + 192);  // misc[192..224): scratch
+    NRM_CUDA(launch_points_bbox(d_q, nq, d_bb, c->stream, &c->launches));
+    double bb[4];
+    NRM_CUDA(cudaMemcpyAsync(bb, d_bb, sizeof(bb), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return points_core(c, bb, d_q, d_exclude, nq, d_apts, d_locals, d_probs, m_total, d_active, nactive, alpha,
+                       support, beta, d_warps, d_pred, d_unc, d_status);
 }
 
 // ---- diagnostics -------------------------------------------------------------

@@ -169,7 +169,22 @@ struct EmdqLaunch {
     double* cp = nullptr;   // max(prob, 1e-6)
 };
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches);
-size_t emdq_scratch_bytes(int nactive, const FieldGrid& g);
+size_t emdq_scratch_bytes(int nactive, const FieldGrid& g, bool tile_plans = true);
+// Scattered queries (EM E-step / final field): L.grid is a grid covering the
+// queries (only its supertile geometry is used); exact tier throughout.
+struct PointsLaunch {
+    const double* q = nullptr;
+    const int32_t* excl = nullptr;
+    int nq = 0;
+    double* warps = nullptr;
+    double* pred = nullptr;
+    double* unc = nullptr;
+    int32_t* status = nullptr;
+    bool full_scan = false;  // every query scans all candidates (very spread-out queries)
+};
+cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaStream_t st, int64_t* launches);
+// Device-side bounding box of nq points -> out4 = {minx, miny, maxx, maxy}.
+cudaError_t launch_points_bbox(const double* q, int nq, double* out4, cudaStream_t st, int64_t* launches);
 
 // ---- k_canvas.cu ----------------------------------------------------------
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,

@@ -380,3 +380,47 @@ def emdq_field_device(grid, apts_t, locals_t, probs_t, active_t, alpha: float, b
                                          _tptr(probs_t), apts_t.shape[0], _tptr(active_t),
                                          active_t.shape[0], float(alpha), int(support), float(beta),
                                          _tptr(disp_t), _tptr(unc_t)))
+
+
+def emdq_points(q, apts, locals_, probs, active, alpha: float, beta: float = 1.0, support: int = 16,
+                exclude=None, want_unc: bool = True, ctx: Optional[Context] = None):
+    """detail::blend_local (fieldest.hpp:75-97) at scattered points q (n, 2),
+    bit-identical to the reference (exact FP64 tier). exclude[k] leaves one
+    original match index out of query k's candidates (the EM E-step's
+    leave-one-out, fieldest.hpp:195-209); without it this is the final field
+    at the node anchors (fieldest.hpp:263-270).
+    Returns (warps (n, 5) {scale, w, z, dx, dy}, pred (n, 2) = warp.apply(q),
+    unc (n,) = bounded_exp(beta d2min) or None, status (n,) int32:
+    0 ok, 1 no candidate left, 2 dq_blend would throw)."""
+    ctx = ctx or default_context()
+    qq = _f64(q, 2, "q")
+    ap = _f64(apts, 2, "apts")
+    lo = _f64(locals_, 5, "locals")
+    pr = np.ascontiguousarray(probs, np.float64).reshape(-1)
+    ac = np.ascontiguousarray(active, np.int32).reshape(-1)
+    if not (len(ap) == len(lo) == len(pr)):
+        raise ValueError("apts / locals / probs size mismatch")
+    ex = None
+    if exclude is not None:
+        ex = np.ascontiguousarray(exclude, np.int32).reshape(-1)
+        if len(ex) != len(qq):
+            raise ValueError("exclude must have one entry per query")
+    n = len(qq)
+    warps = np.zeros((n, 5), np.float64)
+    pred = np.zeros((n, 2), np.float64)
+    unc = np.zeros(n, np.float64) if want_unc else None
+    status = np.zeros(n, np.int32)
+    check(ctx._lib.nrm_emdq_points(ctx.handle, _ptr(qq), _ptr(ex), n, _ptr(ap), _ptr(lo), _ptr(pr), len(ap),
+                                   _ptr(ac), len(ac), float(alpha), int(support), float(beta), _ptr(warps),
+                                   _ptr(pred), _ptr(unc), _ptr(status)))
+    return warps, pred, unc, status
+
+
+def emdq_points_device(q_t, apts_t, locals_t, probs_t, active_t, alpha: float, beta: float, warps_t, pred_t,
+                       unc_t, status_t, support: int = 16, exclude_t=None, ctx: Optional[Context] = None) -> None:
+    """Zero-copy variant of emdq_points on device tensors (any output may be None)."""
+    ctx = ctx or default_context()
+    check(ctx._lib.nrm_emdq_points_device(ctx.handle, _tptr(q_t), _tptr(exclude_t), q_t.shape[0], _tptr(apts_t),
+                                          _tptr(locals_t), _tptr(probs_t), apts_t.shape[0], _tptr(active_t),
+                                          active_t.shape[0], float(alpha), int(support), float(beta),
+                                          _tptr(warps_t), _tptr(pred_t), _tptr(unc_t), _tptr(status_t)))

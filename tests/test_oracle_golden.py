@@ -143,3 +143,18 @@ def test_emdq_edge_cases_match_reference(oracle, golden):
     d, u = oracle.emdq_field_grid(grid, g["apts"], g["locals"], g["probs"], g["active"], float(g["alpha"]),
                                   float(g["beta"]), support=4)
     assert np.array_equal(d, g["disp_s4"]) and np.array_equal(u, g["unc_s4"])
+
+
+def test_oracle_estep_matches_reference(oracle, golden):
+    """The C restatement's blend_local over active minus j reproduces the
+    reference's E-step (fieldest.hpp:195-209) bit for bit."""
+    g = golden("emdq_estep")
+    c1 = golden("emdq_c1")
+    for name in ("c1", "few"):
+        act = g[f"{name}_active"]
+        for j in range(0, len(c1["apts"]), 7):
+            others = act[act != j]
+            w = oracle.blend_local(c1["locals"], c1["apts"], c1["probs"], others, *c1["apts"][j],
+                                   float(c1["alpha"]), 16)
+            assert np.array_equal(w, g[f"{name}_warps"][j]), (name, j)
+            assert np.array_equal(oracle.warp_apply(w, *c1["apts"][j]), g[f"{name}_pred"][j]), (name, j)
