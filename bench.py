@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--no-overlap", dest="overlap", action="store_false",
                     help="run K1 after K3 on one stream (default: K1 || K3 on two streams)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
+    ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -488,6 +489,10 @@ def main():
         except Exception as ex:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "Mpix/s", "cores": 0, "kind": "unavailable", "sample": repr(ex)}
 
+    estep = None
+    if rank == 0 and not args.no_estep:
+        estep = em_estep_numbers(ctx, with_cpu=world == 1 and not args.no_cpu_baseline)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
@@ -502,12 +507,53 @@ def main():
                        "blend_stats_frame0": [int(v) for v in st[0]],
                        "exact_tier_pixels": {"blend_last_frame": int(exc_blend), "emdq_last_frame": int(exc_emdq)}},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
+            "em_estep": estep,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def em_estep_numbers(ctx, with_cpu: bool):
+    """SURVEY §8f NEXT #1, reported beside the headline: the EM E-step's
+    leave-one-out blend_local at every match (fieldest.hpp:195-209) through
+    nrm_emdq_points (host API, best of 5), and the reference's own loop on the
+    host cores over a bounded sample of the same matches (oracle/_ref)."""
+    from paper_2103_07414_b200 import mosaic as M
+    from paper_2103_07414_b200 import workload as W
+    out = []
+    for n, frac in ((10000, 0.2), (50000, 0.5)):
+        e = W.emdq_inputs(3840, 2160, n, frac, 7100 + n)
+        sp = W.scaled_params(3840, 2160)
+        ex = np.arange(n, dtype=np.int32)
+        args = (e.apts, e.apts, e.locals_, e.probs, e.active, sp.alpha, 1.0, 16)
+        M.emdq_points(*args, exclude=ex, want_unc=False, ctx=ctx)
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            w, pred, _, _ = M.emdq_points(*args, exclude=ex, want_unc=False, ctx=ctx)
+            ts.append(time.perf_counter() - t0)
+        r = {"matches": n, "active": int(len(e.active)), "gpu_ms": min(ts) * 1e3,
+             "gpu_matches_per_s": n / min(ts), "path": "nrm_emdq_points, host buffers, exact FP64 tier"}
+        if with_cpu:
+            try:
+                from oracle.oracle import Reference
+                R = Reference()
+                k = min(n, max(64, int(2e8 / max(len(e.active), 1) / 16)))
+                ncpu = os.cpu_count() or 1
+                t0 = time.perf_counter()
+                rw, rp, _ = R.estep_loo(e.apts, e.bpts, e.locals_, e.probs, e.active, sp.alpha, 16, workers=ncpu,
+                                        rows=(0, k))
+                tc = time.perf_counter() - t0
+                r["cpu_reference"] = {"matches_per_s": k / tc, "cores": ncpu, "sample": f"matches [0, {k})",
+                                      "bit_exact_on_sample": bool(np.array_equal(rw[:k], w[:k]) and
+                                                                  np.array_equal(rp[:k], pred[:k]))}
+            except Exception as ex:  # noqa: BLE001  (reported, never required)
+                r["cpu_reference"] = {"unavailable": repr(ex)}
+        out.append(r)
+    return out
 
 
 def wl_contributors(wl, poly, sample: int = 20000):

@@ -203,7 +203,7 @@ class Reference:
         L.ref_synth_matches.argtypes = [_I, _I, _D, _I, _I, C.c_uint64, _P, _P]
         L.ref_estimate_locals.argtypes = [_P, _P, _I, _P, _I, _D, _D, _D, _I, _I, C.c_uint64, _I, _P, _P, _P, _P, _P]
         L.ref_warp_update.argtypes = [_P, _P, _P]
-        L.ref_estep_loo.argtypes = [_P, _P, _P, _P, _I, _P, _I, _D, _I, _P, _P, _P]
+        L.ref_estep_loo.argtypes = [_P, _P, _P, _P, _I, _P, _I, _D, _I, _I, _I, _I, _P, _P, _P]
         L.ref_scene_render.argtypes = [_I, _I, _I, C.c_uint64, _I, _D, _D, _D, _I, _I, _P]
         L.ref_time_blend_frame.argtypes = [_P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _I, _P]
         L.ref_time_blend_frame.restype = _D
@@ -324,8 +324,9 @@ class Reference:
                                          _p(unc))
         return cnt, locals_, probs, inl, inc, unc
 
-    def estep_loo(self, apts, bpts, locals_, probs, active, alpha, support=16):
-        """fieldest.hpp:195-209 for every match: (warps (n, 5), pred (n, 2), empty (n,))."""
+    def estep_loo(self, apts, bpts, locals_, probs, active, alpha, support=16, workers=1, rows=None):
+        """fieldest.hpp:195-209 for every match (or matches [rows[0], rows[1])):
+        (warps (n, 5), pred (n, 2), empty (n,))."""
         ap, bp, lo = _f64(apts, 2), _f64(bpts, 2), _f64(locals_, 5)
         pr = np.ascontiguousarray(probs, np.float64)
         ac = np.ascontiguousarray(active, np.int32)
@@ -333,8 +334,9 @@ class Reference:
         w = np.zeros((n, 5))
         pred = np.zeros((n, 2))
         emp = np.zeros(n, np.uint8)
-        self.L.ref_estep_loo(_p(ap), _p(bp), _p(lo), _p(pr), n, _p(ac), len(ac), float(alpha), int(support), _p(w),
-                             _p(pred), _p(emp))
+        j0, j1 = rows if rows else (0, n)
+        self.L.ref_estep_loo(_p(ap), _p(bp), _p(lo), _p(pr), n, _p(ac), len(ac), float(alpha), int(support),
+                             int(workers), int(j0), int(j1), _p(w), _p(pred), _p(emp))
         return w, pred, emp
 
     def warp_update(self, old5, delta5):

@@ -294,29 +294,35 @@ int ref_estimate_locals(const double* pa, const double* pb, int n, const double*
 // other candidate remains), pred[n*2] (bpts[j] in that case, as the
 // reference does), empty[n] = 1 for that case.
 void ref_estep_loo(const double* apts, const double* bpts, const double* locals, const double* probs,
-                   int n, const std::int32_t* active, int nactive, double alpha, int support, double* warps,
-                   double* pred, std::uint8_t* empty) {
+                   int n, const std::int32_t* active, int nactive, double alpha, int support, int workers,
+                   int j_begin, int j_end, double* warps, double* pred, std::uint8_t* empty) {
     const auto l = to_warps(locals, n);
     const auto a = to_vec2(apts, n);
     const std::vector<double> p(probs, probs + n);
-    std::vector<int> others;
-    for (int j = 0; j < n; ++j) {
-        others.clear();
-        for (int k = 0; k < nactive; ++k)
-            if (active[k] != j) others.push_back(active[k]);
-        empty[j] = others.empty() ? 1 : 0;
-        if (others.empty()) {
-            for (int c = 0; c < 5; ++c) warps[5 * j + c] = 0.0;
-            pred[2 * j] = bpts[2 * j];
-            pred[2 * j + 1] = bpts[2 * j + 1];
-            continue;
+    if (j_begin < 0) j_begin = 0;
+    if (j_end < 0 || j_end > n) j_end = n;
+    // the reference's own runner and grain for this loop (fieldest.hpp:197)
+    parallel_for(static_cast<std::size_t>(j_end - j_begin), workers, [&](std::size_t i0, std::size_t i1) {
+        std::vector<int> others;
+        for (std::size_t ii = i0; ii < i1; ++ii) {
+            const int j = j_begin + static_cast<int>(ii);
+            others.clear();
+            for (int k = 0; k < nactive; ++k)
+                if (active[k] != j) others.push_back(active[k]);
+            empty[j] = others.empty() ? 1 : 0;
+            if (others.empty()) {
+                for (int c = 0; c < 5; ++c) warps[5 * j + c] = 0.0;
+                pred[2 * j] = bpts[2 * j];
+                pred[2 * j + 1] = bpts[2 * j + 1];
+                continue;
+            }
+            const WarpFunction f = detail::blend_local(l, a, p, others, a[j], alpha, support);
+            put_warp(f, &warps[5 * j]);
+            const Vec2 y = f.apply(a[j]);
+            pred[2 * j] = y.x;
+            pred[2 * j + 1] = y.y;
         }
-        const WarpFunction f = detail::blend_local(l, a, p, others, a[j], alpha, support);
-        put_warp(f, &warps[5 * j]);
-        const Vec2 y = f.apply(a[j]);
-        pred[2 * j] = y.x;
-        pred[2 * j + 1] = y.y;
-    }
+    }, 16);
 }
 
 // warp_update (dualquat.hpp:181-190)
