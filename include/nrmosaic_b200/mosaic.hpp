@@ -18,7 +18,10 @@
 //   blend_frame           (mosaic.hpp:196)
 //   render                (mosaic.hpp:301)
 // plus the dense EMDQ field (detail::blend_local + node_uncertainty at every
-// pixel of a grid, fieldest.hpp:44-97) as dense_emdq_field().
+// pixel of a grid, fieldest.hpp:44-97) as dense_emdq_field(), and
+// blend_local at scattered points for the EM loop of estimate_field (the
+// E-step's leave-one-out, fieldest.hpp:195-209, and the final field,
+// fieldest.hpp:263-270) as blend_local_points().
 //
 // Canvas pixels live in HBM. Canvas::color()/weight() read through a host
 // mirror that is downloaded lazily after GPU updates; writes through
@@ -355,6 +358,46 @@ inline void dense_emdq_field(double x0, double y0, int w, int h, std::span<const
     const nrm_grid g{x0, y0, w, h};
     b200::check(nrm_emdq_field(b200::context(), &g, a.data(), l.data(), probs.data(), static_cast<int>(apts.size()),
                                act.data(), static_cast<int>(act.size()), alpha, support, beta, disp, unc));
+}
+
+/// detail::blend_local (fieldest.hpp:75-97) at every query point, bit-identical
+/// to the reference (GPU exact tier). exclude[k] (empty span: none) is a match
+/// index left out of query k's candidates: the E-step passes the match points
+/// and exclude[j] = j, i.e. `others` = active minus j (fieldest.hpp:197-206).
+/// Returns nullopt where no candidate remains (the E-step then uses bpts[j]);
+/// throws std::invalid_argument where dq_blend would (dualquat.hpp:137-146).
+/// Optional outputs: pred[k] = warp.apply(q[k]); unc[k] = node_uncertainty
+/// over the same candidates (fieldest.hpp:44-52, needs beta > 0).
+inline std::vector<std::optional<WarpFunction>> blend_local_points(
+    std::span<const Vec2> queries, std::span<const int> exclude, std::span<const WarpFunction> locals,
+    std::span<const Vec2> apts, std::span<const double> probs, std::span<const int> active, double alpha,
+    int support, std::vector<Vec2>* pred = nullptr, std::vector<double>* unc = nullptr, double beta = 1.0) {
+    if (apts.size() != locals.size() || apts.size() != probs.size())
+        throw std::invalid_argument("blend_local_points: size mismatch");
+    if (!exclude.empty() && exclude.size() != queries.size())
+        throw std::invalid_argument("blend_local_points: exclude must be empty or one per query");
+    const std::size_t n = queries.size();
+    std::vector<std::optional<WarpFunction>> out(n);
+    if (n == 0) return out;
+    const auto q = b200::pack_points(queries);
+    const auto a = b200::pack_points(apts);
+    const auto l = b200::pack_warps(locals);
+    std::vector<std::int32_t> act(active.begin(), active.end());
+    std::vector<std::int32_t> ex(exclude.begin(), exclude.end());
+    std::vector<double> w(5 * n), pr(pred ? 2 * n : 0), un(unc ? n : 0);
+    std::vector<std::int32_t> st(n);
+    b200::check(nrm_emdq_points(b200::context(), q.data(), ex.empty() ? nullptr : ex.data(), static_cast<int>(n),
+                                a.data(), l.data(), probs.data(), static_cast<int>(apts.size()), act.data(),
+                                static_cast<int>(act.size()), alpha, support, beta, w.data(),
+                                pred ? pr.data() : nullptr, unc ? un.data() : nullptr, st.data()));
+    if (pred) pred->assign(n, Vec2{});
+    for (std::size_t k = 0; k < n; ++k) {
+        if (st[k] == 2) throw std::invalid_argument("dq_blend: all weights are zero or degenerate blend");
+        if (st[k] == 0) out[k] = b200::unpack_warp(&w[5 * k]);
+        if (pred) (*pred)[k] = Vec2{pr[2 * k], pr[2 * k + 1]};
+    }
+    if (unc) *unc = std::move(un);
+    return out;
 }
 
 }  // namespace nrmosaic
