@@ -38,7 +38,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "Mpix/s of dense EMDQ field + mosaic update; frames/s at 1080p (1/2/4/8 B200)"
 CFG_NAME = {"c1": "configs[0]: 640x480 frame, 500 matches (20% outliers) into 2048x2048 canvas",
             "c2": "configs[1]: 1920x1080 frame, 2,000 matches (20% outliers) into 8192x8192 canvas",
-            "c4": "configs[3]: 3840x2160 frame, 10,000 matches (20% outliers) into 16384x16384 canvas"}
+            "c4": "configs[3]: 3840x2160 frame, 10,000 matches (20% outliers) into 16384x16384 canvas",
+            "c5": "configs[4]: 3840x2160 frame, 50,000 matches (50% outliers) into 32768x32768 canvas"}
 
 
 def env_int(k, d):
@@ -215,7 +216,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c5"])
     ap.add_argument("--ref-rows", type=int, default=48, help="frame rows of the EMDQ field in the CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false",
@@ -446,7 +447,8 @@ def main():
         #   K1 per contributing (pixel, node) pair (w > 1e-6, mosaic.hpp:249-262):
         #      d2 5 + exponent 1 + exp 1 + 5 weighted sums x 2 + wsum 1 = 18
         #   K3 per pixel: 16 blend members x (distance 5 + exp 1 + prob 1 + 5 sums x 2 + wsum 1) = 288
-        algo = {"k_node_field": contrib["pairs"] * 18.0, "k_pixels": fw * fh * 16 * 18.0}
+        # per profiled step: K1 blends nfr frames, K3 computes one field
+        algo = {"k_node_field": contrib["pairs"] * 18.0 * nfr, "k_pixels": fw * fh * 16 * 18.0}
         traffic = load_traffic()
         kernels = []
         for name, (tot_ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0]):
@@ -454,8 +456,9 @@ def main():
             ent = {"kernel": name, "ms_per_launch": per, "launches": n,
                    "share_of_step": tot_ms / max(sum(v[0] for v in kt.values()), 1e-9)}
             if name in algo:
-                per_launch_flops = algo[name] / (1 if name == "k_node_field" else 1)
-                ach = per_launch_flops / (per * 1e-3) / 1e12
+                # total algorithmic flops over total kernel time (= per launch when a
+                # step's work is split into equal launch chunks)
+                ach = algo[name] * prof_steps / (tot_ms * 1e-3) / 1e12
                 ent.update({"achieved_tflops": ach, "frac_fp32": ach / fp32_peak})
             kernels.append(ent)
         dom = kernels[0]
@@ -473,7 +476,7 @@ def main():
         # HBM view of the fused update: 29 B per footprint pixel (canvas r+w 26 B + frame 3 B)
         kb = kt.get("k_node_field", (0.0, 1))
         fp_px = int(st[0][0])
-        roof["hbm_view_k_node_field"] = {"achieved_gbs": fp_px * 29 / (kb[0] / max(kb[1], 1) * 1e-3) / 1e9,
+        roof["hbm_view_k_node_field"] = {"achieved_gbs": fp_px * 29 * nfr * prof_steps / (max(kb[0], 1e-9) * 1e-3) / 1e9,
                                          "peak_gbs": peaks.get("hbm_gbs"), "bytes_per_footprint_px": 29}
         roof["kernels"] = kernels
 
