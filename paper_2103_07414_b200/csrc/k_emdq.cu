@@ -781,9 +781,14 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         }
         // near-tie between the last member and the first rejected key
         if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
+        // m is warp-uniform: a real loop, not MS predicated takes
+        for (int q = 0; q < m; ++q) {
+            int k = sk[0];
 #pragma unroll
-        for (int q = 0; q < MS; ++q)
-            if (q < m) take(sk[q]);
+            for (int u = 1; u < (MS > 0 ? MS : 1); ++u)
+                if (q == u) k = sk[u];
+            take(k);
+        }
     } else if (m > 0) {
         // many free slots (rare): repeated minimum selection; pass m + 1
         // finds the first rejected key for the near-tie test
@@ -861,18 +866,14 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
     if (!(flags & TFLAG_EXACT_STAGED)) {
         const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
-        for (int e = t; e < ne * 2 * ET; e += ENT) {
-            const int k = e / (2 * ET), c = e % (2 * ET);
+        for (int e = t; e < ne * ET; e += ENT) {  // one column and one row entry per iteration
+            const int k = e / ET, c = e % ET;
             const float4 r0 = s.p.rec0[k];
             const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
             const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
-            if (c < ET) {
-                const float dx = r0.x - (float)c;
-                ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
-            } else {
-                const float dy = r0.y - (float)(c - ET);
-                ey[k][c - ET] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
-            }
+            const float dx = r0.x - (float)c, dy = r0.y - (float)c;
+            ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
+            ey[k][c] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
         }
     }
     __syncthreads();
