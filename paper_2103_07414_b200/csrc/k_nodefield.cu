@@ -52,7 +52,7 @@ constexpr unsigned kRingBit = 0x80000000u;
 enum NfStatus : int { NF_OK = 0, NF_EXACT = 1, NF_EMPTY = 2, NF_OUTSIDE = 3 };
 struct __align__(16) NfHdr {
     double P[2], Y0[2], e0[2], s0;  // output origin / reference scale (FP64)
-    int count, status, pad0, pad1;
+    int count, status, ninner, pad1;  // listed nodes; inner ones come first
 };
 struct __align__(16) NfEntry {
     float4 q;      // warp conjugated to the tile origin (T(-P) q T(o))
@@ -127,11 +127,8 @@ k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j
     const double ylo = L.grid.gy + cj0, yhi = L.grid.gy + cj1;
     const double alpha = L.alpha;
 
-    // ordered cull + classify (index order is kept: the first listed node
-    // seeds the hemisphere arc)
-    int count = 0;
-    for (int base = 0; base < L.n; base += 32) {
-        const int i = base + lane;
+    // cull + classify: inner nodes (index order), then ring nodes (index order)
+    auto classify = [&](int i) {
         int status = 0;  // 0 out, 1 inner, 2 ring
         if (i < L.n) {
             const double2 a = make_double2(__ldg(&L.anchors[2 * i]), __ldg(&L.anchors[2 * i + 1]));
@@ -142,10 +139,19 @@ k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j
             const double amax = alpha * (dxf * dxf + dyf * dyf);
             if (amin <= kLnCutoff + 1e-6) status = amax < kLnCutoff - 1e-5 ? 1 : 2;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, status != 0);
-        const int pos = count + __popc(m & ((1u << lane) - 1u));
-        if (status && pos < NF_CAP) list[pos] = (unsigned)i | (status == 2 ? kRingBit : 0u);
-        count += __popc(m);
+        return status;
+    };
+    int count = 0, ninner = 0;
+    for (int pass = 1; pass <= 2; ++pass) {
+        for (int base = 0; base < L.n; base += 32) {
+            const int i = base + lane;
+            const bool take = classify(i) == pass;
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            const int pos = count + __popc(m & ((1u << lane) - 1u));
+            if (take && pos < NF_CAP) list[pos] = (unsigned)i | (pass == 2 ? kRingBit : 0u);
+            count += __popc(m);
+        }
+        if (pass == 1) ninner = count;
     }
     if (count > NF_CAP || count == 0) {
         if (lane == 0) {
@@ -221,6 +227,7 @@ k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j
         pl.h.e0[1] = fma(s0, P1, -Y01);
         pl.h.s0 = s0;
         pl.h.count = count;
+        pl.h.ninner = ninner;
         pl.h.status = uniform ? NF_OK : NF_EXACT;
     }
     if (!uniform) return;
@@ -325,6 +332,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
     const double alpha = L.alpha;
     const double P0 = pl.h.P[0], P1 = pl.h.P[1], s0 = pl.h.s0;
+    const int ninner = pl.h.ninner;
 
     // ---- D. main loop over node chunks -----------------------------------
     const int col = t & (TW - 1);
@@ -356,39 +364,52 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
         }
         __syncthreads();
 
+        // inner nodes first (the planner lists them before the ring nodes):
+        // no per-node branch, pointer-stepped shared-memory reads
+        const int kin = min(max(ninner - c0, 0), cn);
+        const float* pex = &s.ex[0][col];
+        const float4* pey = reinterpret_cast<const float4*>(&s.ey[0][rg * RPT]);
+        const NfEntry* pe = s.e;
 #pragma unroll 2
-        for (int k = 0; k < cn; ++k) {
+        for (int k = 0; k < kin; ++k) {
+            const float4 q = pe->q;
+            const float dd = pe->d;
+            const float exv = *pex;
+            const float4 e0 = pey[0], e1 = pey[1];
+            pex += TW;
+            pey += TH / 4;
+            ++pe;
+            const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const float w = exv * ey[j];
+                a0[j] = fmaf(w, q.x, a0[j]);
+                a1[j] = fmaf(w, q.y, a1[j]);
+                a2[j] = fmaf(w, q.z, a2[j]);
+                a3[j] = fmaf(w, q.w, a3[j]);
+                a4[j] = fmaf(w, dd, a4[j]);
+                a5[j] += w;
+            }
+        }
+        for (int k = kin; k < cn; ++k) {  // ring nodes: the 1e-6 cutoff per pixel
             const float4 q = s.e[k].q;
             const float dd = s.e[k].d;
             const float exv = s.ex[k][col];
             const float4 e0 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT]);
             const float4 e1 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT + 4]);
             const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-            if (!(s.e[k].idx & kRingBit)) {
 #pragma unroll
-                for (int j = 0; j < RPT; ++j) {
-                    const float w = exv * ey[j];
-                    a0[j] = fmaf(w, q.x, a0[j]);
-                    a1[j] = fmaf(w, q.y, a1[j]);
-                    a2[j] = fmaf(w, q.z, a2[j]);
-                    a3[j] = fmaf(w, q.w, a3[j]);
-                    a4[j] = fmaf(w, dd, a4[j]);
-                    a5[j] += w;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < RPT; ++j) {
-                    float w = exv * ey[j];
-                    const bool in = w > kCutHi;
-                    amb |= (unsigned)((w >= kCutLo) && !in) << j;
-                    w = in ? w : 0.f;
-                    a0[j] = fmaf(w, q.x, a0[j]);
-                    a1[j] = fmaf(w, q.y, a1[j]);
-                    a2[j] = fmaf(w, q.z, a2[j]);
-                    a3[j] = fmaf(w, q.w, a3[j]);
-                    a4[j] = fmaf(w, dd, a4[j]);
-                    a5[j] += w;
-                }
+            for (int j = 0; j < RPT; ++j) {
+                float w = exv * ey[j];
+                const bool in = w > kCutHi;
+                amb |= (unsigned)((w >= kCutLo) && !in) << j;
+                w = in ? w : 0.f;
+                a0[j] = fmaf(w, q.x, a0[j]);
+                a1[j] = fmaf(w, q.y, a1[j]);
+                a2[j] = fmaf(w, q.z, a2[j]);
+                a3[j] = fmaf(w, q.w, a3[j]);
+                a4[j] = fmaf(w, dd, a4[j]);
+                a5[j] += w;
             }
         }
     }
