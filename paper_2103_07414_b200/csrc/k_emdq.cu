@@ -901,7 +901,7 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     const float ux = (float)lx, uy = (float)ly;
     const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
     const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
-    const float dlb = fo.s4 / fo.s5;
+    const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
     const double sb = h.s0 + (double)dlb;
     const double yx = h.Y0[0] + (h.e0[0] + (double)dlb * h.P[0] + sb * (double)Qx);
     const double yy = h.Y0[1] + (h.e0[1] + (double)dlb * h.P[1] + sb * (double)Qy);

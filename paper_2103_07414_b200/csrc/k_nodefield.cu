@@ -442,7 +442,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                 const float ux = (float)col, uy = (float)r;
                 const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
                 const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
-                const float dl = a4[j] / a5[j];
+                const float dl = __fdividef(a4[j], a5[j]);  // a5 > 0, far from 2^126
                 const double sb = s0 + (double)dl;
                 const double yx = Y00 + (e00 + (double)dl * P0 + sb * (double)Qx);
                 const double yy = Y01 + (e01 + (double)dl * P1 + sb * (double)Qy);
@@ -474,11 +474,12 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                         const float vg = (gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy;
                         const float vbl = (gx * va[2] + fx * vb[2]) * gy + (gx * vc[2] + fx * vd[2]) * fy;
                         const uint8_t wg = ct.w[r][col];
-                        const float wd = (float)wg, inv = 1.f / (wd + 1.f);
+                        const float wd = (float)wg, inv = __fdividef(1.f, wd + 1.f);
+                        constexpr float k255 = 1.f / 255.f;
                         const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
-                        L.R[idx] = (wd * ct.r[r][col] + vr / 255.f) * inv;
-                        L.G[idx] = (wd * ct.g[r][col] + vg / 255.f) * inv;
-                        L.B[idx] = (wd * ct.b[r][col] + vbl / 255.f) * inv;
+                        L.R[idx] = (wd * ct.r[r][col] + vr * k255) * inv;
+                        L.G[idx] = (wd * ct.g[r][col] + vg * k255) * inv;
+                        L.B[idx] = (wd * ct.b[r][col] + vbl * k255) * inv;
                         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
                         ++nb;
                     }
