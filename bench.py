@@ -20,6 +20,7 @@ computes the EMDQ field of frame r and blends all N frames into the block-cyclic
 from __future__ import annotations
 
 import argparse
+import collections
 import json
 from concurrent.futures import ThreadPoolExecutor
 import os
@@ -223,6 +224,8 @@ def main():
                     help="run K1 after K3 on one stream (default: K1 || K3 on two streams)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
     ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
+    ap.add_argument("--e2e-inflight", type=int, default=2,
+                    help="EMDQ field calls in flight in the e2e loop (own context + pinned outputs each)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -243,7 +246,9 @@ def main():
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     ctx = M.Context(local)
-    stream = torch.cuda.Stream(dev)           # explicit stream: kernels and events share it
+    # explicit stream: kernels and events share it. K3 (the longer dependency
+    # chain) gets the higher priority so K1 fills the SMs it leaves idle.
+    stream = torch.cuda.Stream(dev, priority=-1 if env_int("NRM_BENCH_PRIO", 1) else 0)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
@@ -386,10 +391,22 @@ def main():
     lib = ctx._lib
     import ctypes as C
 
-    def e2e_field():
-        M.check(lib.nrm_emdq_field(ctx.handle, C.byref(g), h_apts.ctypes.data, h_loc.ctypes.data,
+    # EMDQ field calls in flight (each on its own context, stream and pinned
+    # outputs): frame k+1's field computes while frame k's field is read back
+    # over PCIe. The blends stay sequential on one canvas context (ctx_b).
+    inflight = max(1, args.e2e_inflight) if args.overlap else 1
+    slots = [(ctx, h_disp, h_unc)]
+    for _ in range(inflight - 1):
+        c2 = M.Context(local)
+        c2.set_stream(torch.cuda.Stream(dev, priority=-1).cuda_stream)
+        slots.append((c2, torch.empty((fh, fw, 2), dtype=torch.float32).pin_memory().numpy(),
+                      torch.empty((fh, fw), dtype=torch.float32).pin_memory().numpy()))
+
+    def e2e_field(slot):
+        c_, d_, u_ = slot
+        M.check(lib.nrm_emdq_field(c_.handle, C.byref(g), h_apts.ctypes.data, h_loc.ctypes.data,
                                    h_prob.ctypes.data, len(h_apts), h_act.ctypes.data, len(h_act), alpha, 16, beta,
-                                   h_disp.ctypes.data, h_unc.ctypes.data))
+                                   d_.ctypes.data, u_.ctypes.data))
 
     def e2e_blends():
         out = []
@@ -402,28 +419,37 @@ def main():
             out.append(s)
         return out
 
-    # with overlap, the two blocking calls run on their own contexts from two
-    # host threads (ctypes releases the GIL), as K3 || K1 on the device
-    pool = ThreadPoolExecutor(max_workers=1) if args.overlap else None
+    # with overlap, the blocking calls run from host threads (ctypes releases
+    # the GIL), as K3 || K1 on the device
+    pool = ThreadPoolExecutor(max_workers=inflight) if args.overlap else None
+    pending = collections.deque()
+    e2e_count = [0]
 
     def e2e_step():
         if pool is None:
-            e2e_field()
+            e2e_field(slots[0])
             return e2e_blends()
-        fut = pool.submit(e2e_field)
-        out = e2e_blends()
-        fut.result()
-        return out
+        if len(pending) == inflight:
+            pending.popleft().result()
+        pending.append(pool.submit(e2e_field, slots[e2e_count[0] % inflight]))
+        e2e_count[0] += 1
+        return e2e_blends()
+
+    def e2e_drain():
+        while pending:
+            pending.popleft().result()
 
     e2e_steps = args.e2e_steps or min(args.steps, 300)
-    for _ in range(2):
+    for _ in range(2 * inflight):
         e2e_step()
+    e2e_drain()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
+    e2e_drain()
     t_e2e = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
@@ -435,7 +461,8 @@ def main():
     e2e = {"value": mpix_step * e2e_steps / t_e2e, "unit": "Mpix/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h), "frames_per_s": nfr * e2e_steps / t_e2e,
            "path": "nrm_emdq_field + nrm_blend_frame with pinned host buffers (blocking C ABI calls" +
-           (", one host thread per context)" if args.overlap else ")")}
+           (f", one host thread per context, {inflight} field calls in flight)" if args.overlap else ")"),
+           "fields_in_flight": inflight}
 
     # ---- roofline for the dominant kernel -----------------------------------
     roof = None
