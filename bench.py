@@ -86,6 +86,9 @@ class ClockSampler:
             return
         self._t = threading.Thread(target=self._read, daemon=True)
         self._t.start()
+        t_end = time.time() + 5.0  # nvidia-smi start-up: wait for its first sample
+        while not self.rows and time.time() < t_end and self.proc.poll() is None:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -240,9 +243,18 @@ def main():
 
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
+    # NRM_BENCH_FUNCTIONAL_GLOO=1: functional check of the N>1 code path with
+    # fewer GPUs than ranks (gloo collectives, ranks share devices; no kernel
+    # waits on another rank). Never a measurement.
+    functional = world > 1 and env_int("NRM_BENCH_FUNCTIONAL_GLOO", 0) == 1
+    if functional:
+        local = local % torch.cuda.device_count()
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     ctx = M.Context(local)
@@ -293,6 +305,7 @@ def main():
     disp_t = torch.empty((fh, fw, 2), dtype=torch.float32, device=dev)
     unc_t = torch.empty((fh, fw), dtype=torch.float32, device=dev)
     stats_t = torch.zeros((nfr, 4), dtype=torch.int64, device=dev)
+    stats_red = torch.zeros_like(stats_t)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     grid = (0.0, 0.0, fw, fh)
 
@@ -314,7 +327,13 @@ def main():
             eb.record(stream_b)
             stream.wait_event(eb)
         if world > 1:
-            dist.all_reduce(stats_t)
+            # BlendStats across the bands (dist.reduce_stats semantics): the
+            # counts add up; footprint (column 0) is the same on every rank and
+            # is divided back when reported
+            stats_red.copy_(stats_t)
+            if functional:  # gloo stages CUDA tensors on the host
+                stream.synchronize()
+            dist.all_reduce(stats_red)
         e2.record(stream)
         if timed:
             ev["step"].append((e0, e2))
@@ -329,7 +348,7 @@ def main():
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
     l0 = ctx.launch_count() + ctx_b.launch_count()
     clk.mark("start")
     for _ in range(args.steps):
@@ -373,7 +392,9 @@ def main():
         t = torch.tensor([tmax], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tmax = float(t.item())
-    st = stats_t.cpu().numpy()
+    st = (stats_red if world > 1 else stats_t).cpu().numpy()
+    if world > 1:
+        st[:, 0] //= world
     exc_emdq = ctx.exceptions()[1]
     exc_blend = (ctx_b if args.overlap else ctx).exceptions()[0]
     mpix_step = nfr * fw * fh / 1e6
