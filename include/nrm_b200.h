@@ -130,6 +130,22 @@ int nrm_blend_frame_device(nrm_canvas *cv, const uint8_t *d_frame, int fw, int f
                            const double *d_anchors, const double *d_warps, int n, double alpha,
                            const double *poly, int npoly, int64_t *d_stats);
 
+/* Extension (north_star "uncertainty-weighted blending"; no reference
+ * counterpart): blend_frame with a frame-aligned
+ * per-pixel uncertainty map unc[fh][fw] (node_uncertainty values, >= 1, e.g.
+ * the `unc` output of nrm_emdq_field on the frame grid). At a blended pixel
+ * the confidence cf = 1 / max(u, 1), u sampled bilinearly at the frame
+ * position, scales the update:
+ *   colour <- ((w + 1 - cf) colour + cf rgb / 255) / (w + 1),  w <- min(w + 1, 30).
+ * With u == 1 everywhere this is the reference rule (mosaic.hpp:278-282) bit
+ * for bit. BlendStats and the weight plane are unchanged by the map. */
+int nrm_blend_frame_weighted(nrm_canvas *canvas, const uint8_t *frame, int fw, int fh, int ch,
+                             const double *anchors, const double *warps, int n, double alpha,
+                             const double *poly, int npoly, const float *unc, nrm_blend_stats *out);
+int nrm_blend_frame_weighted_device(nrm_canvas *canvas, const uint8_t *d_frame, int fw, int fh, int ch,
+                                    const double *d_anchors, const double *d_warps, int n, double alpha,
+                                    const double *poly, int npoly, const float *d_unc, int64_t *d_stats);
+
 /* ---- render (mosaic.hpp:301-331) -------------------------------------- */
 /* RGBA8 raster of the canvas; alpha 255 where weight > 0. With crop, the
  * bounding box of occupied pixels. Call with out == NULL to get the size

@@ -331,6 +331,28 @@ inline BlendStats blend_frame(Canvas& canvas, const ImageU8& frame, std::span<co
     return {s.footprint_pixels, s.blended_pixels, s.skipped_no_support, s.skipped_out_of_frame};
 }
 
+/// Extension (north_star "uncertainty-weighted blending", no reference
+/// counterpart): blend_frame whose update step is scaled by the confidence
+/// 1 / max(u, 1) of a frame-aligned uncertainty map (e.g. dense_emdq_field's
+/// `unc`); u == 1 everywhere is blend_frame bit for bit. See nrm_b200.h.
+inline BlendStats blend_frame_weighted(Canvas& canvas, const ImageU8& frame, std::span<const Vec2> anchors,
+                                       std::span<const WarpFunction> warps, double alpha,
+                                       std::span<const Vec2> footprint_polygon, std::span<const float> unc) {
+    if (anchors.size() != warps.size()) throw std::invalid_argument("blend_frame: size mismatch");
+    if (unc.size() != static_cast<std::size_t>(frame.width) * static_cast<std::size_t>(frame.height))
+        throw std::invalid_argument("blend_frame_weighted: uncertainty map must match the frame");
+    const auto a = b200::pack_points(anchors);
+    const auto w = b200::pack_warps(warps);
+    const auto p = b200::pack_points(footprint_polygon);
+    nrm_blend_stats s{};
+    b200::check(nrm_blend_frame_weighted(canvas.handle(), frame.data.data(), frame.width, frame.height,
+                                         frame.channels ? frame.channels : 3, a.data(), w.data(),
+                                         static_cast<int>(anchors.size()), alpha, p.data(),
+                                         static_cast<int>(footprint_polygon.size()), unc.data(), &s));
+    canvas.invalidate_mirror();
+    return {s.footprint_pixels, s.blended_pixels, s.skipped_no_support, s.skipped_out_of_frame};
+}
+
 /// render (mosaic.hpp:301-331).
 inline ImageU8 render(const Canvas& canvas, bool crop = false, Vec2* crop_origin = nullptr) {
     int w = 0, h = 0;

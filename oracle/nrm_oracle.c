@@ -191,9 +191,41 @@ static double rect_distance(double rx0, double ry0, double rx1, double ry1, doub
 /* ------------------------------------------------------------------------ */
 /* blend_frame (mosaic.hpp:196-296)                                          */
 /* ------------------------------------------------------------------------ */
+/* Bilinear sample of a float map with sample_bilinear_rgb's taps. */
+static double sample_bilinear_f32(const float *m, int w, int h, double x, double y) {
+    int x0 = (int)x, y0 = (int)y;
+    const int xc = w - 2 >= 0 ? w - 2 : 0, yc = h - 2 >= 0 ? h - 2 : 0;
+    if (x0 > xc) x0 = xc;
+    if (y0 > yc) y0 = yc;
+    const double fx = x - x0, fy = y - y0;
+    const int x1 = x0 + 1 < w - 1 ? x0 + 1 : w - 1;
+    const int y1 = y0 + 1 < h - 1 ? y0 + 1 : h - 1;
+    const double a = m[(size_t)y0 * w + x0], b = m[(size_t)y0 * w + x1];
+    const double c = m[(size_t)y1 * w + x0], d = m[(size_t)y1 * w + x1];
+    return ((1.0 - fx) * a + fx * b) * (1.0 - fy) + ((1.0 - fx) * c + fx * d) * fy;
+}
+
+static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                            const double *anchors, const double *warps, int n, double alpha,
+                            const double *poly, int npoly, const float *unc, int64_t *stats);
+
 int orc_blend_frame(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
                     const double *anchors, const double *warps, int n, double alpha,
                     const double *poly, int npoly, int64_t *stats) {
+    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, NULL, stats);
+}
+
+/* Extension (not in the reference): the uncertainty-weighted update of
+ * nrm_blend_frame_weighted; unc == 1 everywhere gives orc_blend_frame. */
+int orc_blend_frame_weighted(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                             const double *anchors, const double *warps, int n, double alpha,
+                             const double *poly, int npoly, const float *unc, int64_t *stats) {
+    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, unc, stats);
+}
+
+static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                            const double *anchors, const double *warps, int n, double alpha,
+                            const double *poly, int npoly, const float *unc, int64_t *stats) {
     stats[0] = stats[1] = stats[2] = stats[3] = 0;
     if (fw == 0 || fh == 0 || npoly < 3) return 0;
 
@@ -278,9 +310,16 @@ int orc_blend_frame(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch
                 double *c = &cv->color[((size_t)cy * cv->width + cx) * 3];
                 uint8_t *wgt = &cv->weight[(size_t)cy * cv->width + cx];
                 const double wd = *wgt;
-                c[0] = (wd * c[0] + rgb[0] / 255.0) / (wd + 1.0);
-                c[1] = (wd * c[1] + rgb[1] / 255.0) / (wd + 1.0);
-                c[2] = (wd * c[2] + rgb[2] / 255.0) / (wd + 1.0);
+                if (unc) {
+                    double u = sample_bilinear_f32(unc, fw, fh, yv[0], yv[1]);
+                    const double cf = 1.0 / (u > 1.0 ? u : 1.0);
+                    const double a = wd + 1.0 - cf;
+                    for (int k = 0; k < 3; ++k) c[k] = (a * c[k] + cf * (rgb[k] / 255.0)) / (wd + 1.0);
+                } else {
+                    c[0] = (wd * c[0] + rgb[0] / 255.0) / (wd + 1.0);
+                    c[1] = (wd * c[1] + rgb[1] / 255.0) / (wd + 1.0);
+                    c[2] = (wd * c[2] + rgb[2] / 255.0) / (wd + 1.0);
+                }
                 if (*wgt < K_WEIGHT_CAP) ++*wgt;
                 ++blended;
             }

@@ -57,6 +57,11 @@ int orc_blend_frame(orc_canvas *c, const uint8_t *frame, int fw, int fh, int ch,
 
 /* render (mosaic.hpp:301-331). Two-phase: call with out == NULL to get the size
  * (out_w, out_h; 0x0 when empty) and crop origin; then with a w*h*4 buffer. */
+/* Extension (no reference counterpart): uncertainty-weighted blend_frame,
+ * unc[fh][fw] frame-aligned; see nrm_blend_frame_weighted. */
+int orc_blend_frame_weighted(orc_canvas *c, const uint8_t *frame, int fw, int fh, int ch,
+                             const double *anchors, const double *warps, int n, double alpha,
+                             const double *poly, int npoly, const float *unc, int64_t *stats);
 void orc_render(const orc_canvas *c, int crop, uint8_t *out, int *out_w, int *out_h,
                 double *crop_origin2);
 

@@ -56,6 +56,7 @@ class Oracle:
         L.orc_pixel_warp.argtypes = [_D, _D, _P, _P, _I, _D, _P]
         L.orc_warp_apply.argtypes = [_P, _D, _D, _P]
         L.orc_blend_frame.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P]
+        L.orc_blend_frame_weighted.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _P]
         L.orc_render.argtypes = [_P, _I, _P, _P, _P, _P]
         L.orc_invert_frame_boundary.argtypes = [_I, _I, _P, _P, _I, _D, _D, _P, _I]
         L.orc_blend_local.argtypes = [_P, _P, _P, _P, _I, _D, _D, _D, _I, _P]
@@ -123,6 +124,21 @@ class Oracle:
                                     len(p), _p(st))
         if rc:
             raise MemoryError("oracle blend_frame")
+        return tuple(int(v) for v in st)
+
+    def blend_frame_weighted(self, canvas, frame, anchors, warps, alpha, poly, unc):
+        f = np.ascontiguousarray(frame, np.uint8)
+        if f.ndim == 2:
+            f = f[:, :, None]
+        h, w, c = f.shape
+        a, q, p = _f64(anchors, 2), _f64(warps, 5), _f64(poly, 2)
+        u = np.ascontiguousarray(unc, np.float32)
+        assert u.shape == (h, w)
+        st = np.zeros(4, np.int64)
+        rc = self.L.orc_blend_frame_weighted(canvas.h, _p(f), w, h, c, _p(a), _p(q), len(a), float(alpha), _p(p),
+                                             len(p), _p(u), _p(st))
+        if rc:
+            raise MemoryError("oracle blend_frame_weighted")
         return tuple(int(v) for v in st)
 
     def render(self, canvas, crop=False):

@@ -85,6 +85,10 @@ SIGNATURES = [
                                   _P, C.c_int, C.POINTER(BlendStats)]),
     ("nrm_blend_frame_device", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int,
                                          C.c_double, _P, C.c_int, _P]),
+    ("nrm_blend_frame_weighted", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double, _P,
+                                           C.c_int, _P, _P]),
+    ("nrm_blend_frame_weighted_device", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double,
+                                                  _P, C.c_int, _P, _P]),
     ("nrm_render", C.c_int, [_P, C.c_int, _P, _I, _I, _D]),
     ("nrm_render_device", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("nrm_canvas_occupied_bbox", C.c_int, [_P, _I, _I, _I, _I]),

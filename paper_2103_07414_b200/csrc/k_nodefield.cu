@@ -286,7 +286,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     // ---- 0. stage the canvas tile (whole 64 x 32 tile lies in the canvas:
     //         tiles and canvas bounds are both 32/64-aligned, mosaic.hpp:141-151)
     //         and the first chunk of the tile's plan
-    if (MODE == 0) {
+    if (MODE != 1) {
         const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (ti0 - L.phys_x0);
         constexpr int kF = TW / 4;       // 16-byte chunks per float row
         constexpr int kB = TW / 16;      // 16-byte chunks per byte row
@@ -326,7 +326,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
             ++ns;
         }
         cp_async_wait_all();
-        if (MODE == 0) block_add3<NT>(L.acc, 0, ns, 0);
+        if (MODE != 1) block_add3<NT>(L.acc, 0, ns, 0);
         return;
     }
     const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
@@ -477,9 +477,21 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                         const float wd = (float)wg, inv = __fdividef(1.f, wd + 1.f);
                         constexpr float k255 = 1.f / 255.f;
                         const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
-                        L.R[idx] = (wd * ct.r[r][col] + vr * k255) * inv;
-                        L.G[idx] = (wd * ct.g[r][col] + vg * k255) * inv;
-                        L.B[idx] = (wd * ct.b[r][col] + vbl * k255) * inv;
+                        // reference rule: (w c + v) / (w + 1); weighted mode:
+                        // ((w + 1 - cf) c + cf v) / (w + 1), identical for cf == 1
+                        float a = wd, cf = 1.f;
+                        if (MODE == 2) {
+                            const float* U = L.unc;
+                            const float u = (gx * U[(size_t)y0 * L.fw + x0] + fx * U[(size_t)y0 * L.fw + x1]) * gy +
+                                            (gx * U[(size_t)y1 * L.fw + x0] + fx * U[(size_t)y1 * L.fw + x1]) * fy;
+                            cf = __frcp_rn(fmaxf(u, 1.f));
+                            a = wd + 1.f - cf;
+                        }
+                        // explicit FMAs: the same instructions in both modes, so
+                        // cf == 1 reproduces the reference rule bit for bit
+                        L.R[idx] = fmaf(a, ct.r[r][col], cf * (vr * k255)) * inv;
+                        L.G[idx] = fmaf(a, ct.g[r][col], cf * (vg * k255)) * inv;
+                        L.B[idx] = fmaf(a, ct.b[r][col], cf * (vbl * k255)) * inv;
                         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
                         ++nb;
                     }
@@ -488,7 +500,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
         }
         queue_push(exc, i, jj, L.exc, L.exc_count, L.exc_cap, L.exc_overflow);
     }
-    if (MODE == 0) block_add3<NT>(L.acc, nb, nns, noof);
+    if (MODE != 1) block_add3<NT>(L.acc, nb, nns, noof);
 }
 
 // Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics), one
@@ -589,9 +601,16 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
         const uint8_t wg = L.W[idx];
         const double wd = wg;
-        L.R[idx] = (float)((wd * (double)L.R[idx] + rgb[0] / 255.0) / (wd + 1.0));
-        L.G[idx] = (float)((wd * (double)L.G[idx] + rgb[1] / 255.0) / (wd + 1.0));
-        L.B[idx] = (float)((wd * (double)L.B[idx] + rgb[2] / 255.0) / (wd + 1.0));
+        // reference operation order, no contraction (mosaic.hpp:278-282); the
+        // weighted mode runs the same operations with a = w + 1 - cf, cf <= 1
+        double a = wd, cf = 1.0;
+        if (MODE == 2) {  // weighted mode (see NodeFieldLaunch::unc)
+            cf = 1.0 / fmax(xsample_bilinear_f32(L.unc, L.fw, L.fh, yx, yy), 1.0);
+            a = xsub(xadd(wd, 1.0), cf);
+        }
+        L.R[idx] = (float)(xadd(xmul(a, (double)L.R[idx]), xmul(cf, rgb[0] / 255.0)) / xadd(wd, 1.0));
+        L.G[idx] = (float)(xadd(xmul(a, (double)L.G[idx]), xmul(cf, rgb[1] / 255.0)) / xadd(wd, 1.0));
+        L.B[idx] = (float)(xadd(xmul(a, (double)L.B[idx]), xmul(cf, rgb[2] / 255.0)) / xadd(wd, 1.0));
         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
         ++nb;
     }
@@ -611,7 +630,7 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         unsigned long long tot[3] = {0, 0, 0};
         for (int k = 0; k < 3; ++k)
             for (int w = 0; w < EXC_THREADS / 32; ++w) tot[k] += (unsigned long long)red[k][w];
-        if (MODE == 0)
+        if (MODE != 1)
             for (int k = 0; k < 3; ++k)
                 if (tot[k]) atomicAdd(&L.acc[k], tot[k]);
         __threadfence();
@@ -621,7 +640,7 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
     // the last CTA finalises BlendStats and restores the per-context state
     if (last && threadIdx.x == 0) {
         __threadfence();
-        if (MODE == 0) {
+        if (MODE != 1) {
             volatile unsigned long long* acc = L.acc;
             if (L.stats_out) {
                 L.stats_out[0] = L.footprint;
@@ -735,13 +754,13 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
         nty = cnt;
     }
     const size_t base = (sizeof(Smem) + 15) & ~size_t(15);
-    const size_t smem = mode == 0 ? base + sizeof(CanvasTile) : sizeof(Smem);
+    const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : sizeof(Smem);
+    const int kmode = mode == 1 ? 1 : (L.unc ? 2 : 0);  // 2: uncertainty-weighted blend
+    auto k_field = kmode == 0 ? k_node_field<0> : (kmode == 1 ? k_node_field<1> : k_node_field<2>);
+    auto k_exc = kmode == 0 ? k_node_exceptions<0> : (kmode == 1 ? k_node_exceptions<1> : k_node_exceptions<2>);
     if (ntx > 0 && nty > 0) {
         NfPlan* plans = static_cast<NfPlan*>(L.plans);
-        if (mode == 0)
-            cudaFuncSetAttribute(k_node_field<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        else
-            cudaFuncSetAttribute(k_node_field<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_field, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int rows_per_chunk = max(1, NF_CHUNK_TILES / ntx);
         for (int by0 = 0; by0 < nty; by0 += rows_per_chunk) {
             const int rows = min(rows_per_chunk, nty - by0);
@@ -751,20 +770,14 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t s
                 L, plans, ti0, tj0, tj1, s1, by0, rows, ntx);
             ++*launches;
             prof_mark("k_node_field", st);
-            if (mode == 0)
-                k_node_field<0><<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
-            else
-                k_node_field<1><<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
+            k_field<<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
             ++*launches;
             const cudaError_t e = cudaGetLastError();
             if (e != cudaSuccess) return e;
         }
     }
     prof_mark("k_node_exceptions", st);
-    if (mode == 0)
-        k_node_exceptions<0><<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
-    else
-        k_node_exceptions<1><<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
+    k_exc<<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
     ++*launches;
     return cudaGetLastError();
 }

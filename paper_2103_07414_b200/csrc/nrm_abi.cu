@@ -297,7 +297,7 @@ State state_of(nrm_ctx* c) {
 // d_stats: int64[4] on the device, written by the exception pass.
 int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
                const double* d_warps, int n, double alpha, const double* poly, int npoly,
-               unsigned long long* d_stats) {
+               unsigned long long* d_stats, const float* d_unc = nullptr) {
     nrm_ctx* c = cv->ctx;
     if (fw <= 0 || fh <= 0 || npoly < 3) {  // mosaic.hpp:201: empty stats, canvas untouched
         NRM_CUDA(cudaMemsetAsync(d_stats, 0, 4 * sizeof(unsigned long long), c->stream));
@@ -324,6 +324,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.fw = fw;
     L.fh = fh;
     L.fch = ch;
+    L.unc = d_unc;
     L.anchors = d_anchors;
     L.warps = d_warps;
     L.n = n;
@@ -738,9 +739,10 @@ int nrm_canvas_occupied_bbox(nrm_canvas* cv, int* x0, int* y0, int* x1, int* y1)
 }
 
 // ---- blend_frame ---------------------------------------------------------
-int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, const double* anchors,
-                    const double* warps, int n, double alpha, const double* poly, int npoly,
-                    nrm_blend_stats* out) {
+namespace {
+int blend_host(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, const double* anchors,
+               const double* warps, int n, double alpha, const double* poly, int npoly, const float* unc,
+               nrm_blend_stats* out) {
     NRM_CHECK(check_canvas(cv));
     if (!out) return fail(NRM_EINVAL, "null stats");
     *out = nrm_blend_stats{0, 0, 0, 0};
@@ -753,12 +755,20 @@ int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch
     DeviceGuard g(c->device);
     ProfScope prof_scope(c);
     const size_t fbytes = (size_t)fw * fh * ch;
-    NRM_CHECK(upload(c, c->frame_raw, frame, fbytes));
+    const size_t ubytes = unc ? (size_t)fw * fh * sizeof(float) : 0;
+    const size_t uoff = (fbytes + 255) & ~size_t(255);
+    NRM_CUDA(c->frame_raw.ensure(uoff + ubytes));
+    NRM_CUDA(cudaMemcpyAsync(c->frame_raw.p, frame, fbytes, cudaMemcpyHostToDevice, c->stream));
+    const float* d_unc = nullptr;
+    if (unc) {
+        NRM_CUDA(cudaMemcpyAsync(c->frame_raw.as<char>() + uoff, unc, ubytes, cudaMemcpyHostToDevice, c->stream));
+        d_unc = reinterpret_cast<const float*>(c->frame_raw.as<char>() + uoff);
+    }
     NRM_CHECK(upload(c, c->anchors, anchors, (size_t)n * 2 * sizeof(double)));
     NRM_CHECK(upload(c, c->warps, warps, (size_t)n * 5 * sizeof(double)));
     NRM_CUDA(c->stats.ensure(64));
     NRM_CHECK(blend_core(cv, c->frame_raw.as<uint8_t>(), fw, fh, ch, c->anchors.as<double>(), c->warps.as<double>(), n,
-                         alpha, poly, npoly, c->stats.as<unsigned long long>()));
+                         alpha, poly, npoly, c->stats.as<unsigned long long>(), d_unc));
     NRM_CUDA(c->staging_out.ensure(64));
     NRM_CUDA(cudaMemcpyAsync(c->staging_out.p, c->stats.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     NRM_CUDA(cudaStreamSynchronize(c->stream));
@@ -767,9 +777,9 @@ int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch
     return NRM_OK;
 }
 
-int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
-                           const double* d_warps, int n, double alpha, const double* poly, int npoly,
-                           int64_t* d_stats) {
+int blend_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
+                 const double* d_warps, int n, double alpha, const double* poly, int npoly, const float* d_unc,
+                 int64_t* d_stats) {
     NRM_CHECK(check_canvas(cv));
     if (!d_stats) return fail(NRM_EINVAL, "null stats");
     if (fw < 0 || fh < 0) return fail(NRM_EINVAL, "negative frame size");
@@ -782,7 +792,34 @@ int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int f
         if (!d_frame || !poly) return fail(NRM_EINVAL, "null frame or polygon");
     }
     return blend_core(cv, d_frame, fw, fh, ch, d_anchors, d_warps, n, alpha, poly, npoly,
-                      reinterpret_cast<unsigned long long*>(d_stats));
+                      reinterpret_cast<unsigned long long*>(d_stats), d_unc);
+}
+}  // namespace
+
+int nrm_blend_frame(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, const double* anchors,
+                    const double* warps, int n, double alpha, const double* poly, int npoly,
+                    nrm_blend_stats* out) {
+    return blend_host(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, nullptr, out);
+}
+
+int nrm_blend_frame_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
+                           const double* d_warps, int n, double alpha, const double* poly, int npoly,
+                           int64_t* d_stats) {
+    return blend_device(cv, d_frame, fw, fh, ch, d_anchors, d_warps, n, alpha, poly, npoly, nullptr, d_stats);
+}
+
+int nrm_blend_frame_weighted(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, const double* anchors,
+                             const double* warps, int n, double alpha, const double* poly, int npoly,
+                             const float* unc, nrm_blend_stats* out) {
+    if (!unc && fw > 0 && fh > 0) return fail(NRM_EINVAL, "blend_frame_weighted: null uncertainty map");
+    return blend_host(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, unc, out);
+}
+
+int nrm_blend_frame_weighted_device(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch,
+                                    const double* d_anchors, const double* d_warps, int n, double alpha,
+                                    const double* poly, int npoly, const float* d_unc, int64_t* d_stats) {
+    if (!d_unc && fw > 0 && fh > 0) return fail(NRM_EINVAL, "blend_frame_weighted: null uncertainty map");
+    return blend_device(cv, d_frame, fw, fh, ch, d_anchors, d_warps, n, alpha, poly, npoly, d_unc, d_stats);
 }
 
 // ---- render ----------------------------------------------------------------

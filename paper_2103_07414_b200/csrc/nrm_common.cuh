@@ -163,6 +163,23 @@ __device__ __forceinline__ void xsample_bilinear(const uint8_t* __restrict__ im,
                        xmul(xadd(xmul(gx, (double)c[k]), xmul(fx, (double)d[k])), fy));
 }
 
+// Bilinear sample of a single-channel float map with the same tap rule as
+// sample_bilinear_rgb (image.hpp:78-92), FP64 arithmetic.
+__device__ __forceinline__ double xsample_bilinear_f32(const float* __restrict__ m, int iw, int ih, double x,
+                                                       double y) {
+    int x0 = (int)x, y0 = (int)y;
+    const int xc = iw - 2 >= 0 ? iw - 2 : 0, yc = ih - 2 >= 0 ? ih - 2 : 0;
+    if (x0 > xc) x0 = xc;
+    if (y0 > yc) y0 = yc;
+    const double fx = xsub(x, (double)x0), fy = xsub(y, (double)y0);
+    const int x1 = x0 + 1 < iw - 1 ? x0 + 1 : iw - 1;
+    const int y1 = y0 + 1 < ih - 1 ? y0 + 1 : ih - 1;
+    const double a = m[(size_t)y0 * iw + x0], b = m[(size_t)y0 * iw + x1];
+    const double c = m[(size_t)y1 * iw + x0], d = m[(size_t)y1 * iw + x1];
+    const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
+    return xadd(xmul(xadd(xmul(gx, a), xmul(fx, b)), gy), xmul(xadd(xmul(gx, c), xmul(fx, d)), fy));
+}
+
 // ---- fast tier ----------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;

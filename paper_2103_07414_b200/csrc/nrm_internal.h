@@ -101,6 +101,11 @@ struct NodeFieldLaunch {
     // inputs
     const uint8_t* frame = nullptr;  // ImageU8 layout: h x w x fch, fch in {1, 3, 4}
     int fw = 0, fh = 0, fch = 3;
+    // optional (extension): frame-aligned per-pixel
+    // uncertainty (fw x fh, node_uncertainty >= 1); the blend's update step is
+    // scaled by the confidence 1 / max(u, 1) sampled bilinearly at the frame
+    // position. Null (or u == 1 everywhere) is the reference rule bit for bit.
+    const float* unc = nullptr;
     const double* anchors = nullptr;
     const double* warps = nullptr;
     int n = 0;

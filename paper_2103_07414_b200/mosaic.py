@@ -244,9 +244,11 @@ def _frame(frame: np.ndarray) -> Tuple[np.ndarray, int, int, int]:
 
 
 def blend_frame(canvas: Canvas, frame: np.ndarray, anchors, warps, alpha: float,
-                footprint_polygon, workers: Optional[int] = None) -> BlendStats:
+                footprint_polygon, workers: Optional[int] = None, unc=None) -> BlendStats:
     """blend_frame (mosaic.hpp:196-296). `workers` is accepted for signature
-    parity and ignored (the GPU grid replaces the thread pool)."""
+    parity and ignored (the GPU grid replaces the thread pool).
+    unc: optional frame-aligned (h, w) uncertainty map -> the uncertainty-
+    weighted extension (nrm_blend_frame_weighted; unc == 1 is the reference)."""
     f, w, h, c = _frame(frame)
     a = _f64(anchors, 2, "anchors")
     q = _f64(warps, 5, "warps")
@@ -254,19 +256,32 @@ def blend_frame(canvas: Canvas, frame: np.ndarray, anchors, warps, alpha: float,
         raise ValueError("anchors / warps size mismatch")
     p = _f64(footprint_polygon, 2, "footprint_polygon")
     st = BlendStats()
-    check(canvas._lib.nrm_blend_frame(canvas.handle, _ptr(f), w, h, c, _ptr(a), _ptr(q), len(a),
-                                      float(alpha), _ptr(p), len(p), C.byref(st)))
+    if unc is None:
+        check(canvas._lib.nrm_blend_frame(canvas.handle, _ptr(f), w, h, c, _ptr(a), _ptr(q), len(a),
+                                          float(alpha), _ptr(p), len(p), C.byref(st)))
+    else:
+        u = np.ascontiguousarray(unc, np.float32)
+        if u.shape != (h, w):
+            raise ValueError(f"unc must be the frame's (h, w) = {(h, w)}")
+        check(canvas._lib.nrm_blend_frame_weighted(canvas.handle, _ptr(f), w, h, c, _ptr(a), _ptr(q), len(a),
+                                                   float(alpha), _ptr(p), len(p), _ptr(u), C.byref(st)))
     return st
 
 
 def blend_frame_device(canvas: Canvas, frame_t, fw: int, fh: int, ch: int, anchors_t, warps_t,
-                       alpha: float, footprint_polygon, stats_t) -> None:
-    """Device-resident blend_frame: torch CUDA tensors in, int64[4] stats tensor out (async)."""
+                       alpha: float, footprint_polygon, stats_t, unc_t=None) -> None:
+    """Device-resident blend_frame: torch CUDA tensors in, int64[4] stats tensor out (async).
+    unc_t: optional (fh, fw) float32 uncertainty map (weighted extension)."""
     p = _f64(footprint_polygon, 2, "footprint_polygon")
     n = anchors_t.shape[0] if anchors_t is not None else 0
-    check(canvas._lib.nrm_blend_frame_device(canvas.handle, _tptr(frame_t), fw, fh, ch,
-                                             _tptr(anchors_t), _tptr(warps_t), n, float(alpha),
-                                             _ptr(p), len(p), _tptr(stats_t)))
+    if unc_t is None:
+        check(canvas._lib.nrm_blend_frame_device(canvas.handle, _tptr(frame_t), fw, fh, ch,
+                                                 _tptr(anchors_t), _tptr(warps_t), n, float(alpha),
+                                                 _ptr(p), len(p), _tptr(stats_t)))
+    else:
+        check(canvas._lib.nrm_blend_frame_weighted_device(canvas.handle, _tptr(frame_t), fw, fh, ch,
+                                                          _tptr(anchors_t), _tptr(warps_t), n, float(alpha),
+                                                          _ptr(p), len(p), _tptr(unc_t), _tptr(stats_t)))
 
 
 def render(canvas: Canvas, crop: bool = False):

@@ -1,0 +1,91 @@
+"""Extension (north_star "uncertainty-weighted blending"; SURVEY Appendix A.2,
+no reference counterpart): nrm_blend_frame_weighted.
+
+* u == 1 everywhere must be the reference rule bit for bit (same canvas as
+  nrm_blend_frame, same BlendStats);
+* with a real uncertainty map (the EMDQ field's own per-pixel uncertainty on
+  the frame grid) the GPU matches the C restatement of the same rule
+  (oracle/nrm_oracle.c: orc_blend_frame_weighted): BlendStats and weights
+  exact, colour within 1e-3, as for the reference rule."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+COLOR_TOL = 1e-3
+
+
+def split_polys(g):
+    out, o = [], 0
+    for n in g["npoly"]:
+        out.append(g["polys"][o:o + n])
+        o += n
+    return out
+
+
+def test_uniform_uncertainty_is_the_reference_rule(nrm, ctx, golden):
+    g = golden("blend_c1_seq")
+    polys = split_polys(g)
+    h, w = g["frame"].shape[:2]
+    ones = np.ones((h, w), np.float32)
+    a, b = nrm.Canvas(ctx), nrm.Canvas(ctx)
+    for k, poly in enumerate(polys):
+        sa = nrm.blend_frame(a, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly).as_tuple()
+        sb = nrm.blend_frame(b, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly,
+                             unc=ones).as_tuple()
+        assert sa == sb
+    ca, wa = a.read()
+    cb, wb = b.read()
+    assert np.array_equal(wa, wb)
+    assert np.array_equal(ca, cb)
+
+
+def test_weighted_blend_matches_oracle(nrm, ctx, oracle, golden):
+    from paper_2103_07414_b200 import workload as W
+    g = golden("blend_c1_seq")
+    e = golden("emdq_c1")
+    polys = split_polys(g)
+    h, w = g["frame"].shape[:2]
+    # the EMDQ field's own per-pixel uncertainty on the frame grid (>= 1)
+    _, unc = nrm.emdq_field((0.0, 0.0, w, h), e["apts"], e["locals"], e["probs"], e["active"], float(e["alpha"]),
+                            float(e["beta"]) * 40.0, 16, ctx=ctx)
+    assert unc.min() >= 1.0 and unc.max() > 2.0
+    cv, ocv = nrm.Canvas(ctx), oracle.canvas()
+    for k, poly in enumerate(polys):
+        st = nrm.blend_frame(cv, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly,
+                             unc=unc).as_tuple()
+        ost = oracle.blend_frame_weighted(ocv, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly,
+                                          unc)
+        assert st == ost
+    col, wt = cv.read()
+    ocol, owt = ocv.arrays()
+    assert np.array_equal(wt, owt)
+    assert np.abs(col.astype(np.float64) - ocol).max() <= COLOR_TOL
+    # and the weighting did something: differs from the reference rule
+    ref = oracle.canvas()
+    for k, poly in enumerate(polys):
+        oracle.blend_frame(ref, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), poly)
+    rcol, _ = ref.arrays()
+    assert np.abs(rcol - ocol).max() > 1e-2
+    del W
+
+
+def test_weighted_device_variant(nrm, ctx, golden):
+    import torch
+    g = golden("blend_c1")
+    polys = split_polys(g)
+    h, w = g["frame"].shape[:2]
+    rng = np.random.default_rng(1)
+    unc = (1.0 + 3.0 * rng.random((h, w))).astype(np.float32)
+    dev = torch.device("cuda", 0)
+    a, b = nrm.Canvas(ctx), nrm.Canvas(ctx)
+    sa = nrm.blend_frame(a, g["frame"], g["anchors"], g["warps"][0], float(g["alpha"]), polys[0], unc=unc)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    st = torch.zeros(4, dtype=torch.int64, device=dev)
+    nrm.blend_frame_device(b, T(g["frame"]), w, h, 3, T(g["anchors"]), T(g["warps"][0]), float(g["alpha"]),
+                           polys[0], st, unc_t=T(unc))
+    ctx.synchronize()
+    assert tuple(st.cpu().tolist()) == sa.as_tuple()
+    ca, wa = a.read()
+    cb, wb = b.read()
+    assert np.array_equal(wa, wb) and np.array_equal(ca, cb)

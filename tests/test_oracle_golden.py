@@ -158,3 +158,18 @@ def test_oracle_estep_matches_reference(oracle, golden):
                                    float(c1["alpha"]), 16)
             assert np.array_equal(w, g[f"{name}_warps"][j]), (name, j)
             assert np.array_equal(oracle.warp_apply(w, *c1["apts"][j]), g[f"{name}_pred"][j]), (name, j)
+
+
+def test_oracle_weighted_blend_with_unit_uncertainty_is_reference(oracle, golden):
+    """Extension rule: u == 1 everywhere reproduces the reference update bit for bit."""
+    g = golden("blend_c1")
+    poly = g["polys"][: g["npoly"][0]]
+    h, w = g["frame"].shape[:2]
+    a, b = oracle.canvas(), oracle.canvas()
+    sa = oracle.blend_frame(a, g["frame"], g["anchors"], g["warps"][0], float(g["alpha"]), poly)
+    sb = oracle.blend_frame_weighted(b, g["frame"], g["anchors"], g["warps"][0], float(g["alpha"]), poly,
+                                     np.ones((h, w), np.float32))
+    assert sa == sb
+    ca, wa = a.arrays()
+    cb, wb = b.arrays()
+    assert np.array_equal(wa, wb) and np.array_equal(ca, cb)
