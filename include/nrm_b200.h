@@ -111,6 +111,16 @@ int nrm_canvas_download(nrm_canvas *cv, int x, int y, int w, int h, double *rgb,
 /* Writes a rectangle (Canvas::color(x,y)[k] = ..., weight_ref(x,y) = ...). */
 int nrm_canvas_upload(nrm_canvas *cv, int x, int y, int w, int h, const double *rgb,
                       const uint8_t *weight);
+/* Extension (north_star "deforming the existing canvas with bilinear
+ * sampling"; no reference counterpart): over the canvas
+ * rectangle [x, x+w) x [y, y+h), new(p) = old(p + d(p)) with d = disp[h][w][2]
+ * in canvas pixels (e.g. a dense field from nrm_node_field / nrm_emdq_field).
+ * Bilinear in FP64 over the occupied taps (weights renormalised), weight of
+ * the nearest occupied tap; sources outside the canvas or without occupied
+ * taps leave the pixel unoccupied. d == 0 is a bit-exact no-op. Single-band
+ * canvases only (a banded canvas would need a halo exchange). */
+int nrm_canvas_deform(nrm_canvas *cv, int x, int y, int w, int h, const float *disp);
+int nrm_canvas_deform_device(nrm_canvas *cv, int x, int y, int w, int h, const float *d_disp);
 /* Canvas::occupied_count (mosaic.hpp:123-127). */
 int nrm_canvas_occupied_count(nrm_canvas *cv, int64_t *out);
 

@@ -353,6 +353,17 @@ inline BlendStats blend_frame_weighted(Canvas& canvas, const ImageU8& frame, std
     return {s.footprint_pixels, s.blended_pixels, s.skipped_no_support, s.skipped_out_of_frame};
 }
 
+/// Extension (north_star "deforming the existing canvas", no reference
+/// counterpart): new(p) = old(p + d(p)) over the canvas rectangle
+/// [x, x+w) x [y, y+h); disp holds h*w (dx, dy) pairs in canvas pixels.
+/// d == 0 is a bit-exact no-op. See nrm_canvas_deform.
+inline void deform_canvas(Canvas& canvas, int x, int y, int w, int h, std::span<const float> disp) {
+    if (disp.size() != static_cast<std::size_t>(w) * static_cast<std::size_t>(h) * 2)
+        throw std::invalid_argument("deform_canvas: displacement field must hold w * h * 2 floats");
+    b200::check(nrm_canvas_deform(canvas.handle(), x, y, w, h, disp.data()));  // handle() pushes host edits
+    canvas.invalidate_mirror();
+}
+
 /// render (mosaic.hpp:301-331).
 inline ImageU8 render(const Canvas& canvas, bool crop = false, Vec2* crop_origin = nullptr) {
     int w = 0, h = 0;

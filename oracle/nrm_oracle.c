@@ -333,6 +333,59 @@ static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh
     return 0;
 }
 
+/* Extension (no reference counterpart): canvas deformation
+ * new(p) = old(p + d(p)) over a rectangle; see nrm_canvas_deform. */
+int orc_canvas_deform(orc_canvas *cv, int x0, int y0, int w, int h, const float *disp) {
+    const int W = cv->width, H = cv->height;
+    double *nc = (double *)malloc(sizeof(double) * 3 * (size_t)(w > 0 ? w : 1) * (h > 0 ? h : 1));
+    uint8_t *nw = (uint8_t *)malloc((size_t)(w > 0 ? w : 1) * (h > 0 ? h : 1));
+    if (!nc || !nw) { free(nc); free(nw); return -1; }
+    for (int j = 0; j < h; ++j) {
+        for (int i = 0; i < w; ++i) {
+            const size_t o = (size_t)j * w + i;
+            const double sx = (double)(x0 + i) + (double)disp[2 * o];
+            const double sy = (double)(y0 + j) + (double)disp[2 * o + 1];
+            double c3[3] = {0.0, 0.0, 0.0};
+            uint8_t cw = 0;
+            if (sx >= 0.0 && sx <= W - 1.0 && sy >= 0.0 && sy <= H - 1.0) {
+                int tx0 = (int)sx, ty0 = (int)sy;
+                if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
+                if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
+                const double fx = sx - tx0, fy = sy - ty0;
+                const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
+                const double gx = 1.0 - fx, gy = 1.0 - fy;
+                const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
+                const double bw[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
+                double n3[3] = {0.0, 0.0, 0.0}, den = 0.0, best = -1.0;
+                for (int t = 0; t < 4; ++t) {
+                    const size_t idx = (size_t)tys[t] * W + txs[t];
+                    const uint8_t wt = cv->weight[idx];
+                    if (wt == 0) continue;
+                    for (int k = 0; k < 3; ++k) n3[k] = n3[k] + bw[t] * (double)(float)cv->color[3 * idx + k];
+                    den = den + bw[t];
+                    if (bw[t] > best) { best = bw[t]; cw = wt; }
+                }
+                if (den > 0.0) {
+                    for (int k = 0; k < 3; ++k) c3[k] = (double)(float)(n3[k] / den);
+                } else {
+                    cw = 0;
+                }
+            }
+            for (int k = 0; k < 3; ++k) nc[3 * o + k] = c3[k];
+            nw[o] = cw;
+        }
+    }
+    for (int j = 0; j < h; ++j)
+        for (int i = 0; i < w; ++i) {
+            const size_t o = (size_t)j * w + i, idx = (size_t)(y0 + j) * W + (x0 + i);
+            for (int k = 0; k < 3; ++k) cv->color[3 * idx + k] = nc[3 * o + k];
+            cv->weight[idx] = nw[o];
+        }
+    free(nc);
+    free(nw);
+    return 0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* render (mosaic.hpp:301-331)                                               */
 /* ------------------------------------------------------------------------ */

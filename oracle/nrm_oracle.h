@@ -62,6 +62,10 @@ int orc_blend_frame(orc_canvas *c, const uint8_t *frame, int fw, int fh, int ch,
 int orc_blend_frame_weighted(orc_canvas *c, const uint8_t *frame, int fw, int fh, int ch,
                              const double *anchors, const double *warps, int n, double alpha,
                              const double *poly, int npoly, const float *unc, int64_t *stats);
+/* Extension (no reference counterpart): new(p) = old(p + d(p)) over the
+ * canvas rectangle [x, x+w) x [y, y+h), d = disp[h][w][2]; colours are read
+ * as float32 (the GPU canvas precision) and rounded to float32 on output. */
+int orc_canvas_deform(orc_canvas *c, int x, int y, int w, int h, const float *disp);
 void orc_render(const orc_canvas *c, int crop, uint8_t *out, int *out_w, int *out_h,
                 double *crop_origin2);
 

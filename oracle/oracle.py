@@ -57,6 +57,7 @@ class Oracle:
         L.orc_warp_apply.argtypes = [_P, _D, _D, _P]
         L.orc_blend_frame.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P]
         L.orc_blend_frame_weighted.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _P]
+        L.orc_canvas_deform.argtypes = [_P, _I, _I, _I, _I, _P]
         L.orc_render.argtypes = [_P, _I, _P, _P, _P, _P]
         L.orc_invert_frame_boundary.argtypes = [_I, _I, _P, _P, _I, _D, _D, _P, _I]
         L.orc_blend_local.argtypes = [_P, _P, _P, _P, _I, _D, _D, _D, _I, _P]
@@ -96,6 +97,22 @@ class Oracle:
             col = np.ctypeslib.as_array((C.c_double * (w * h * 3)).from_address(cp)).reshape(h, w, 3).copy()
             wt = np.ctypeslib.as_array((C.c_uint8 * (w * h)).from_address(wp)).reshape(h, w).copy()
             return col, wt
+
+        def set_arrays(self, color, weight):
+            """Overwrites the whole logical canvas (test setup)."""
+            _, _, w, h = self.info()
+            cp = self.o.L.orc_canvas_color(self.h)
+            wp = self.o.L.orc_canvas_weight(self.h)
+            np.ctypeslib.as_array((C.c_double * (w * h * 3)).from_address(cp))[:] = \
+                np.ascontiguousarray(color, np.float64).reshape(-1)
+            np.ctypeslib.as_array((C.c_uint8 * (w * h)).from_address(wp))[:] = \
+                np.ascontiguousarray(weight, np.uint8).reshape(-1)
+
+        def deform(self, x, y, w, h, disp):
+            d = np.ascontiguousarray(disp, np.float32)
+            assert d.shape == (h, w, 2)
+            if self.o.L.orc_canvas_deform(self.h, int(x), int(y), int(w), int(h), _p(d)):
+                raise MemoryError("oracle canvas_deform")
 
     def canvas(self) -> "Oracle.Canvas":
         return Oracle.Canvas(self)

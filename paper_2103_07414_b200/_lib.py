@@ -80,6 +80,8 @@ SIGNATURES = [
     ("nrm_canvas_set_band", C.c_int, [_P, C.c_int, C.c_int]),
     ("nrm_canvas_download", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("nrm_canvas_upload", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
+    ("nrm_canvas_deform", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("nrm_canvas_deform_device", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("nrm_canvas_occupied_count", C.c_int, [_P, _I64]),
     ("nrm_blend_frame", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double,
                                   _P, C.c_int, C.POINTER(BlendStats)]),

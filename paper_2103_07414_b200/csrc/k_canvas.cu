@@ -145,7 +145,90 @@ __global__ void k_canvas_write(float* r, float* g, float* b, uint8_t* wp, long l
     if (win) wp[idx] = win[o];
 }
 
+// Canvas deformation (extension, north_star; no
+// reference counterpart): new(p) = old(p + d(p)) over a region, bilinear in
+// FP64 with the taps of sample_bilinear_rgb (image.hpp:78-92) restricted to
+// occupied pixels (weights renormalised), weight from the nearest occupied
+// tap; a source outside the canvas or with no occupied tap leaves the pixel
+// unoccupied. d == 0 reproduces the canvas bit for bit. Output goes to
+// scratch planes (sources may lie anywhere in the canvas).
+__global__ void k_canvas_deform(CanvasView v, int W, int H, int x0, int y0, int w, int h,
+                                const float2* __restrict__ disp, float* __restrict__ outr, float* __restrict__ outg,
+                                float* __restrict__ outb, uint8_t* __restrict__ outw) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (i >= w) return;
+    const size_t o = (size_t)j * w + i;
+    const float2 d = disp[o];
+    const double sx = xadd((double)(x0 + i), (double)d.x), sy = xadd((double)(y0 + j), (double)d.y);
+    float cr = 0.f, cg = 0.f, cb = 0.f;
+    uint8_t cw = 0;
+    if (sx >= 0.0 && sx <= W - 1.0 && sy >= 0.0 && sy <= H - 1.0) {
+        int tx0 = (int)sx, ty0 = (int)sy;
+        if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
+        if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
+        const double fx = xsub(sx, (double)tx0), fy = xsub(sy, (double)ty0);
+        const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
+        const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
+        const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
+        const double bw[4] = {xmul(gx, gy), xmul(fx, gy), xmul(gx, fy), xmul(fx, fy)};
+        double nr = 0.0, ng = 0.0, nb = 0.0, den = 0.0, best = -1.0;
+        for (int t = 0; t < 4; ++t) {
+            const long long idx = (v.oy + tys[t]) * v.pitch + (v.ox + txs[t]);
+            const uint8_t wt = v.w[idx];
+            if (wt == 0) continue;
+            nr = xadd(nr, xmul(bw[t], (double)v.r[idx]));
+            ng = xadd(ng, xmul(bw[t], (double)v.g[idx]));
+            nb = xadd(nb, xmul(bw[t], (double)v.b[idx]));
+            den = xadd(den, bw[t]);
+            if (bw[t] > best) {
+                best = bw[t];
+                cw = wt;
+            }
+        }
+        if (den > 0.0) {
+            cr = (float)(nr / den);
+            cg = (float)(ng / den);
+            cb = (float)(nb / den);
+        } else {
+            cw = 0;
+        }
+    }
+    outr[o] = cr;
+    outg[o] = cg;
+    outb[o] = cb;
+    outw[o] = cw;
+}
+
 }  // namespace
+
+cudaError_t launch_canvas_deform(const nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
+                                 cudaStream_t st, int64_t* launches) {
+    if (w <= 0 || h <= 0) return cudaSuccess;
+    const size_t npx = (size_t)w * h;
+    float* r = scratch;
+    float* g = r + npx;
+    float* b = g + npx;
+    uint8_t* wt = reinterpret_cast<uint8_t*>(b + npx);
+    prof_mark("k_canvas_deform", st);
+    k_canvas_deform<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), cv->width, cv->height, x, y, w, h, disp,
+                                                              r, g, b, wt);
+    ++*launches;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    // scratch -> canvas planes
+    const long long ox = cv->origin_x - cv->phys_x0, oy = cv->origin_y - cv->phys_y0;
+    const size_t off = (size_t)(oy + y) * cv->cap_w + (size_t)(ox + x);
+    float* planes[3] = {cv->r, cv->g, cv->b};
+    const float* src[3] = {r, g, b};
+    for (int k = 0; k < 3; ++k) {
+        e = cudaMemcpy2DAsync(planes[k] + off, (size_t)cv->cap_w * sizeof(float), src[k], (size_t)w * sizeof(float),
+                              (size_t)w * sizeof(float), (size_t)h, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaMemcpy2DAsync(cv->w + off, (size_t)cv->cap_w, wt, (size_t)w, (size_t)w, (size_t)h,
+                             cudaMemcpyDeviceToDevice, st);
+}
 
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches) {

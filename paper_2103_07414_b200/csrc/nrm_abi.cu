@@ -693,6 +693,42 @@ int nrm_canvas_upload(nrm_canvas* cv, int x, int y, int w, int h, const double* 
     return NRM_OK;
 }
 
+// ---- extension: canvas deformation (north_star) ------------
+static int deform_core(nrm_canvas* cv, int x, int y, int w, int h, const float* d_disp) {
+    nrm_ctx* c = cv->ctx;
+    if (cv->band_count > 1)
+        return fail(NRM_EINVAL, "canvas_deform: banded canvases need a halo exchange (not supported)");
+    const size_t npx = (size_t)w * h;
+    NRM_CUDA(c->out_b.ensure(npx * 13 + 64));
+    NRM_CUDA(launch_canvas_deform(cv, x, y, w, h, reinterpret_cast<const float2*>(d_disp), c->out_b.as<float>(),
+                                  c->stream, &c->launches));
+    return NRM_OK;
+}
+
+int nrm_canvas_deform(nrm_canvas* cv, int x, int y, int w, int h, const float* disp) {
+    NRM_CHECK(check_canvas(cv));
+    NRM_CHECK(check_region(cv, x, y, w, h));
+    if ((size_t)w * h == 0) return NRM_OK;
+    if (!disp) return fail(NRM_EINVAL, "canvas_deform: null displacement field");
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    NRM_CHECK(upload(c, c->out_a, disp, (size_t)w * h * 2 * sizeof(float)));
+    NRM_CHECK(deform_core(cv, x, y, w, h, c->out_a.as<float>()));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
+int nrm_canvas_deform_device(nrm_canvas* cv, int x, int y, int w, int h, const float* d_disp) {
+    NRM_CHECK(check_canvas(cv));
+    NRM_CHECK(check_region(cv, x, y, w, h));
+    if ((size_t)w * h == 0) return NRM_OK;
+    if (!d_disp) return fail(NRM_EINVAL, "canvas_deform: null displacement field");
+    DeviceGuard g(cv->ctx->device);
+    ProfScope prof_scope(cv->ctx);
+    return deform_core(cv, x, y, w, h, d_disp);
+}
+
 static int occupied_scan(nrm_canvas* cv, unsigned long long* count, int bbox[4]) {
     nrm_ctx* c = cv->ctx;
     NRM_CUDA(c->stats.ensure(64));

@@ -194,6 +194,10 @@ cudaError_t launch_points_bbox(const double* q, int nq, double* out4, cudaStream
 // ---- k_canvas.cu ----------------------------------------------------------
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches);
+// Extension: canvas deformation new(p) = old(p + d(p)) over a logical
+// region; scratch holds 13 B per region pixel.
+cudaError_t launch_canvas_deform(const nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
+                                 cudaStream_t st, int64_t* launches);
 cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int* bbox4,
                             cudaStream_t st, int64_t* launches);
 cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h, double* rgb,

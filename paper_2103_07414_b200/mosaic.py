@@ -202,6 +202,20 @@ class Canvas:
         w_c = None if weight is None else np.ascontiguousarray(weight, np.uint8)
         check(self._lib.nrm_canvas_upload(self._h, x, y, w, h, _ptr(rgb_c), _ptr(w_c)))
 
+    def deform(self, disp, x: int = 0, y: int = 0) -> None:
+        """Extension (north_star, no reference counterpart): new(p) =
+        old(p + d(p)) over the rectangle at (x, y) of disp's (h, w) shape;
+        disp is a host float32 (h, w, 2) array or a CUDA tensor. d == 0 is a
+        bit-exact no-op (nrm_canvas_deform)."""
+        if hasattr(disp, "is_cuda"):
+            h, w = int(disp.shape[0]), int(disp.shape[1])
+            check(self._lib.nrm_canvas_deform_device(self._h, int(x), int(y), w, h, _tptr(disp)))
+        else:
+            d = np.ascontiguousarray(disp, np.float32)
+            if d.ndim != 3 or d.shape[2] != 2:
+                raise ValueError("disp must be (h, w, 2)")
+            check(self._lib.nrm_canvas_deform(self._h, int(x), int(y), d.shape[1], d.shape[0], _ptr(d)))
+
     def color(self, x: int, y: int) -> np.ndarray:
         return self.read(x, y, 1, 1)[0][0, 0]
 
