@@ -331,3 +331,32 @@ def frame_workload(name: str = "c2", seed: int = 7) -> FrameWorkload:
     cx, cy = fw / 2.0, fh / 2.0
     rect = (cx - cs / 2.0, cy - cs / 2.0, cx + cs / 2.0 - 1.0, cy + cs / 2.0 - 1.0)
     return FrameWorkload(fw, fh, cs, sp, frame, anchors, warps, emdq, rect)
+
+
+# ---------------------------------------------------------------------------
+# Sequences (BASELINE configs[2]: a frame sequence sweeping the canvas)
+# ---------------------------------------------------------------------------
+def shifted_warps(warps: np.ndarray, tx: float, ty: float) -> np.ndarray:
+    """Warps of x -> W(x - t): the same field moved by t in reference
+    coordinates. For a unit DQ (w, z, dx, dy), apply(x - t) = R x + T0 - R t
+    with R = M^2, T = 2 M d, M = [[w, -z], [z, w]], so d' = d - M t / 2."""
+    q = np.array(warps, dtype=np.float64, copy=True)
+    w_, z_ = q[:, 1], q[:, 2]
+    q[:, 3] = q[:, 3] - 0.5 * (w_ * tx - z_ * ty)
+    q[:, 4] = q[:, 4] - 0.5 * (z_ * tx + w_ * ty)
+    return q
+
+
+def scan_offsets(n: int, frame_w: int, frame_h: int, canvas: int, overlap: float = 0.6) -> np.ndarray:
+    """Serpentine scan of n frame positions (reference-coordinate offsets of
+    the frame origin) over a canvas x canvas area centred on the first frame,
+    consecutive frames overlapping by `overlap` of the frame width."""
+    step_x = (1.0 - overlap) * frame_w
+    step_y = (1.0 - overlap) * frame_h
+    cols = max(1, int((canvas - frame_w) // step_x) + 1)
+    out = []
+    for k in range(n):
+        r, c = divmod(k, cols)
+        c = c if r % 2 == 0 else cols - 1 - c
+        out.append((c * step_x - 0.5 * (canvas - frame_w), r * step_y - 0.5 * (canvas - frame_h)))
+    return np.array(out)
