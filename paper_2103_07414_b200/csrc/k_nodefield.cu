@@ -41,6 +41,7 @@ constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = NRM_K1_CHUNK;
 constexpr int NF_CAP = 512;           // listed nodes per tile plan (more: the tile goes to the exact pass)
 constexpr int NF_CHUNK_TILES = 2048;  // tile plans resident per launch chunk
 constexpr int NF_PLAN_WARPS = 8;      // planning warps (tiles) per CTA
+constexpr int NF_GROUP_TILES = 64;    // prefilter node lists per 64 tile columns (4096 px)
 constexpr int EXC_THREADS = 128;
 constexpr int EXC_BLOCKS = 148;
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
@@ -79,7 +80,7 @@ struct CanvasTile {
 };
 
 
-__device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1, int band_count) {
+__host__ __device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1, int band_count) {
     if (band_count <= 1) return tile_j0 + by;
     const int s = s1 + (by >> 1) * band_count;
     return 2 * s + (by & 1);
@@ -104,6 +105,68 @@ __device__ void tile_to_exceptions(const NodeFieldLaunch& L, int ci0, int ci1, i
 // nearest the tile centre, the tile's output origin, and the listed warps
 // conjugated into tile-local coordinates.
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// k_nf_prefilter: one CTA; the index-ordered list of nodes that can reach
+// (weight > 1e-6, same conservative test as k_nf_plan) any pixel of the
+// launch chunk's rectangle [xlo, xhi] x [ylo, yhi]. Planning and the exact
+// pass then scan this list instead of all n nodes (canvas-wide lattices:
+// thousands of nodes, ~100 per tile).
+// ---------------------------------------------------------------------------
+constexpr int PF_THREADS = 512;
+__global__ void __launch_bounds__(PF_THREADS) k_nf_prefilter(NodeFieldLaunch L, int ti0, int ti1, int tj1, int nty) {
+    __shared__ int wsum[PF_THREADS / 32];
+    __shared__ int base;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int ci = blockIdx.y, gi = blockIdx.x;
+    const int by0 = ci * L.chunk_rows, by1 = min(by0 + L.chunk_rows, nty) - 1;
+    const int gx0 = ti0 + gi * NF_GROUP_TILES, gx1 = min(gx0 + NF_GROUP_TILES - 1, ti1);
+    // the chunk's tile rows (block-cyclic with bands: their bounding range)
+    const int r0 = tile_row_of(by0, L.tile_j0, L.band_s1, L.band_count);
+    const int r1 = min(tile_row_of(by1, L.tile_j0, L.band_s1, L.band_count), tj1);
+    const double xlo = L.grid.gx + max(gx0 * TW, L.grid.i0), xhi = L.grid.gx + min((gx1 + 1) * TW - 1, L.grid.i1);
+    const double ylo = L.grid.gy + max(r0 * TH, L.grid.j0), yhi = L.grid.gy + min((r1 + 1) * TH - 1, L.grid.j1);
+    const int li = ci * L.col_groups + gi;
+    int* list = L.lists + (size_t)li * L.lstride;
+    if (t == 0) base = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < L.n; b0 += PF_THREADS) {
+        const int i = b0 + t;
+        bool keep = false;
+        if (i < L.n) {
+            const double ax = __ldg(&L.anchors[2 * i]), ay = __ldg(&L.anchors[2 * i + 1]);
+            const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi);
+            const double dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
+            keep = L.alpha * (dxn * dxn + dyn * dyn) <= kLnCutoff + 1e-6;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[wid] = __popc(m);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < wid; ++w) off += wsum[w];
+        if (keep) list[off + __popc(m & ((1u << lane) - 1u))] = i;
+        __syncthreads();
+        if (t == 0) {
+            int tot = 0;
+            for (int w = 0; w < PF_THREADS / 32; ++w) tot += wsum[w];
+            base += tot;
+        }
+        __syncthreads();
+    }
+    if (t == 0) L.lcounts[li] = base;
+}
+
+// The node list of (launch chunk ci, tile column group gi): (list, count);
+// all n nodes without lists.
+__device__ __forceinline__ const int* chunk_nodes(const NodeFieldLaunch& L, int ci, int gi, int* n) {
+    if (!L.lists) {
+        *n = L.n;
+        return nullptr;
+    }
+    const int li = ci * L.col_groups + gi;
+    *n = L.lcounts[li];
+    return L.lists + (size_t)li * L.lstride;
+}
+
 __global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
 k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
           int rows, int ntx) {
@@ -142,9 +205,12 @@ k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j
         return status;
     };
     int count = 0, ninner = 0;
+    int nsrc;
+    const int* src = chunk_nodes(L, by0 / L.chunk_rows, (g % ntx) / NF_GROUP_TILES, &nsrc);
     for (int pass = 1; pass <= 2; ++pass) {
-        for (int base = 0; base < L.n; base += 32) {
-            const int i = base + lane;
+        for (int base = 0; base < nsrc; base += 32) {
+            const int e = base + lane;
+            const int i = e < nsrc ? (src ? src[e] : e) : L.n;  // L.n: out of range -> not listed
             const bool take = classify(i) == pass;
             const unsigned m = __ballot_sync(0xffffffffu, take);
             const int pos = count + __popc(m & ((1u << lane) - 1u));
@@ -511,17 +577,19 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
 // contributors' products in ascending node order -- the reference's order, so
 // the result is bit-identical -- with shuffles. All lanes end with the result.
 __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ anchors,
-                                const double* __restrict__ warps, int n, double alpha, W5* out) {
+                                const double* __restrict__ warps, const int* __restrict__ src, int n, double alpha,
+                                W5* out) {
     const int lane = threadIdx.x & 31;
     const double na = -alpha;
     double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
     double ref_w = 0.0, ref_z = 0.0;
     bool have_ref = false;
     for (int c0 = 0; c0 < n; c0 += 32) {
-        const int i = c0 + lane;
+        const int e = c0 + lane;
+        const int i = e < n ? (src ? src[e] : e) : 0;  // src: index-ordered subset
         double w = 0.0, q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         bool contrib = false;
-        if (i < n) {
+        if (e < n) {
             const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
             w = xexp(xmul(na, d2));
             contrib = !(w <= kPixelWeightCutoff);
@@ -571,7 +639,14 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         const int2 p = L.exc[q];
         const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
         W5 wp;
-        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, L.n, L.alpha, &wp);
+        // the pixel's launch chunk: tile row -> launch row (inverse of tile_row_of)
+        const int tjy = floordiv(p.y, TH);
+        const int by = L.band_count <= 1 ? tjy - L.tile_j0
+                                         : 2 * (((tjy >> 1) - L.band_s1) / L.band_count) + (tjy & 1);
+        int nsrc;
+        const int tix = floordiv(p.x, TW) - floordiv(L.grid.i0, TW);
+        const int* src = chunk_nodes(L, by / L.chunk_rows, tix / NF_GROUP_TILES, &nsrc);
+        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp);
         if (lane != 0) continue;
         if (MODE == 1) {
             const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
@@ -734,47 +809,82 @@ cudaError_t launch_selftest_libm(const double* x, const double* y, int n, double
     return cudaGetLastError();
 }
 
-size_t node_field_plan_bytes() { return (size_t)NF_CHUNK_TILES * sizeof(NfPlan); }
-
-cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches) {
-    const int ti0 = floordiv(L.grid.i0, TW), ti1 = floordiv(L.grid.i1, TW);
-    const int tj0 = floordiv(L.grid.j0, TH), tj1 = floordiv(L.grid.j1, TH);
-    const int ntx = ti1 - ti0 + 1;
-    int nty = tj1 - tj0 + 1, s1 = 0;
+// Launch geometry shared by the scratch sizing and the launcher.
+struct NfGeom {
+    int ti0, ti1, tj0, tj1, ntx, nty, s1, chunk_rows, nchunks;
+};
+NfGeom nf_geom(const NodeFieldLaunch& L) {
+    NfGeom g;
+    g.ti0 = floordiv(L.grid.i0, TW);
+    g.ti1 = floordiv(L.grid.i1, TW);
+    g.tj0 = floordiv(L.grid.j0, TH);
+    g.tj1 = floordiv(L.grid.j1, TH);
+    g.ntx = g.ti1 - g.ti0 + 1;
+    g.nty = g.tj1 - g.tj0 + 1;
+    g.s1 = 0;
     if (L.band_count > 1) {
-        const int stripe_lo = floordiv(tj0 * TH, kStripeRows);
-        s1 = stripe_lo + posmod(L.band_rank - stripe_lo, L.band_count);
+        const int stripe_lo = floordiv(g.tj0 * TH, kStripeRows);
+        g.s1 = stripe_lo + posmod(L.band_rank - stripe_lo, L.band_count);
         int cnt = 0;
         for (int by = 0;; ++by) {
-            const int s = s1 + (by >> 1) * L.band_count;
+            const int s = g.s1 + (by >> 1) * L.band_count;
             const int row = 2 * s + (by & 1);
-            if (row > tj1) break;
+            if (row > g.tj1) break;
             cnt = by + 1;
         }
-        nty = cnt;
+        g.nty = cnt;
+    }
+    g.chunk_rows = g.ntx > 0 ? max(1, NF_CHUNK_TILES / g.ntx) : 1;
+    g.nchunks = (g.ntx > 0 && g.nty > 0) ? (g.nty + g.chunk_rows - 1) / g.chunk_rows : 0;
+    return g;
+}
+constexpr int kPrefilterMinNodes = 257;  // small lattices: every node reaches every tile anyway
+
+size_t node_field_scratch_bytes(const NodeFieldLaunch& L) {
+    const NfGeom g = nf_geom(L);
+    size_t b = (size_t)NF_CHUNK_TILES * sizeof(NfPlan);
+    const size_t nl = (size_t)g.nchunks * (size_t)((g.ntx + NF_GROUP_TILES - 1) / NF_GROUP_TILES);
+    if (L.n >= kPrefilterMinNodes) b += (nl * (size_t)L.n + nl + 64) * sizeof(int);
+    return b;
+}
+
+cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t st, int64_t* launches) {
+    const NfGeom g = nf_geom(L0);
+    NodeFieldLaunch L = L0;
+    L.chunk_rows = g.chunk_rows;
+    L.tile_j0 = g.tj0;
+    L.band_s1 = g.s1;
+    NfPlan* plans = static_cast<NfPlan*>(L.plans);
+    if (L.n >= kPrefilterMinNodes && g.nchunks > 0) {
+        L.lstride = L.n;
+        L.col_groups = (g.ntx + NF_GROUP_TILES - 1) / NF_GROUP_TILES;
+        L.lists = reinterpret_cast<int*>(reinterpret_cast<char*>(L.plans) + (size_t)NF_CHUNK_TILES * sizeof(NfPlan));
+        L.lcounts = L.lists + (size_t)g.nchunks * L.col_groups * L.lstride;
     }
     const size_t base = (sizeof(Smem) + 15) & ~size_t(15);
     const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : sizeof(Smem);
     const int kmode = mode == 1 ? 1 : (L.unc ? 2 : 0);  // 2: uncertainty-weighted blend
     auto k_field = kmode == 0 ? k_node_field<0> : (kmode == 1 ? k_node_field<1> : k_node_field<2>);
     auto k_exc = kmode == 0 ? k_node_exceptions<0> : (kmode == 1 ? k_node_exceptions<1> : k_node_exceptions<2>);
-    if (ntx > 0 && nty > 0) {
-        NfPlan* plans = static_cast<NfPlan*>(L.plans);
-        cudaFuncSetAttribute(k_field, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        const int rows_per_chunk = max(1, NF_CHUNK_TILES / ntx);
-        for (int by0 = 0; by0 < nty; by0 += rows_per_chunk) {
-            const int rows = min(rows_per_chunk, nty - by0);
-            if ((size_t)rows * ntx > (size_t)NF_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
-            prof_mark("k_nf_plan", st);
-            k_nf_plan<<<(rows * ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS, NF_PLAN_WARPS * 32, 0, st>>>(
-                L, plans, ti0, tj0, tj1, s1, by0, rows, ntx);
-            ++*launches;
-            prof_mark("k_node_field", st);
-            k_field<<<dim3(ntx, rows), NT, smem, st>>>(L, plans, ti0, tj0, s1, by0, ntx);
-            ++*launches;
-            const cudaError_t e = cudaGetLastError();
-            if (e != cudaSuccess) return e;
-        }
+    if (L.lists) {  // all chunks' node lists in one launch
+        prof_mark("k_nf_prefilter", st);
+        k_nf_prefilter<<<dim3(L.col_groups, g.nchunks), PF_THREADS, 0, st>>>(L, g.ti0, g.ti1, g.tj1, g.nty);
+        ++*launches;
+    }
+    cudaFuncSetAttribute(k_field, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int ci = 0; ci < g.nchunks; ++ci) {
+        const int by0 = ci * g.chunk_rows;
+        const int rows = min(g.chunk_rows, g.nty - by0);
+        if ((size_t)rows * g.ntx > (size_t)NF_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
+        prof_mark("k_nf_plan", st);
+        k_nf_plan<<<(rows * g.ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS, NF_PLAN_WARPS * 32, 0, st>>>(
+            L, plans, g.ti0, g.tj0, g.tj1, g.s1, by0, rows, g.ntx);
+        ++*launches;
+        prof_mark("k_node_field", st);
+        k_field<<<dim3(g.ntx, rows), NT, smem, st>>>(L, plans, g.ti0, g.tj0, g.s1, by0, g.ntx);
+        ++*launches;
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
     prof_mark("k_node_exceptions", st);
     k_exc<<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);

@@ -354,7 +354,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
     L.exc_done = st.exc_done;
-    NRM_CUDA(c->tiles.ensure(node_field_plan_bytes()));
+    NRM_CUDA(c->tiles.ensure(node_field_scratch_bytes(L)));
     L.plans = c->tiles.p;
     NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
     return NRM_OK;
@@ -424,7 +424,7 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
     L.exc_done = st.exc_done;
-    NRM_CUDA(c->tiles.ensure(node_field_plan_bytes()));
+    NRM_CUDA(c->tiles.ensure(node_field_scratch_bytes(L)));
     L.plans = c->tiles.p;
     NRM_CUDA(launch_node_field(L, 1, c->stream, &c->launches));
     return NRM_OK;

@@ -135,9 +135,17 @@ struct NodeFieldLaunch {
     unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
     unsigned* exc_last = nullptr;      // pixels the last exception pass resolved (diagnostics)
     unsigned* exc_done = nullptr;      // finished exception CTAs (persistent-zero)
-    void* plans = nullptr;             // tile-plan scratch (node_field_plan_bytes())
+    void* plans = nullptr;             // tile-plan scratch (node_field_plan_bytes(n))
+    // Per launch chunk (chunk_rows launch tile rows each): index-ordered
+    // lists of the nodes that can reach the chunk, written by k_nf_prefilter
+    // (lists == null: every chunk scans all n nodes).
+    int* lists = nullptr;              // [nchunks][col_groups][lstride]
+    int* lcounts = nullptr;            // [nchunks][col_groups]
+    int lstride = 0, chunk_rows = 1;
+    int col_groups = 1;                // tile-column groups of NF_GROUP_TILES per chunk
+    int tile_j0 = 0, band_s1 = 0;      // launch-row <-> tile-row mapping (exact pass)
 };
-size_t node_field_plan_bytes();
+size_t node_field_scratch_bytes(const NodeFieldLaunch& L);
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches);
