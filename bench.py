@@ -227,6 +227,7 @@ def main():
                     help="run K1 after K3 on one stream (default: K1 || K3 on two streams)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
     ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
+    ap.add_argument("--no-canvas-field", action="store_true", help="skip the canvas-wide field side measurement")
     ap.add_argument("--e2e-inflight", type=int, default=2,
                     help="EMDQ field calls in flight in the e2e loop (own context + pinned outputs each)")
     args = ap.parse_args()
@@ -543,6 +544,9 @@ def main():
     estep = None
     if rank == 0 and not args.no_estep:
         estep = em_estep_numbers(ctx, with_cpu=world == 1 and not args.no_cpu_baseline)
+    canvas_field = None
+    if rank == 0 and not args.no_canvas_field:
+        canvas_field = canvas_field_numbers(ctx, stream, fp32_peak=2.0 * ctx.peak("fp32") / 1e12)
 
     if rank == 0:
         line = {
@@ -559,12 +563,66 @@ def main():
                        "exact_tier_pixels": {"blend_last_frame": int(exc_blend), "emdq_last_frame": int(exc_emdq)}},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
             "em_estep": estep,
+            "canvas_field": canvas_field,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
+    """Side measurement (BASELINE configs[3]: the canvas-wide field of a
+    16384^2 canvas with its canvas-covering 1,497-node lattice, K2 =
+    k_node_field<1>): one pass, device-timed, with the roofline of the same
+    FP32 main loop the blend uses, here without the canvas epilogue.
+    Algorithmic work: contributing (pixel, node) pairs x 18 flops, counted
+    with the reference's cutoff on a seeded pixel sample."""
+    import torch
+    from paper_2103_07414_b200 import mosaic as M
+    from paper_2103_07414_b200 import workload as W
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sp = W.scaled_params(3840, 2160)
+    anchors = W.hex_lattice((0.0, 0.0, float(n), float(n)), sp.hex_spacing)
+    rng = np.random.default_rng(5)
+    warps = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(anchors), 1))
+    ang = rng.uniform(-0.02, 0.02, len(anchors))
+    warps[:, 0] = rng.uniform(0.99, 1.01, len(anchors))
+    warps[:, 1], warps[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    warps[:, 3:5] = rng.normal(0, 4.0, (len(anchors), 2))
+    a_t, q_t = torch.from_numpy(anchors).to(dev), torch.from_numpy(warps).to(dev)
+    disp = torch.empty((n, n, 2), dtype=torch.float32, device=dev)
+    sup = torch.empty((n, n), dtype=torch.uint8, device=dev)
+    M.node_field_device((0.0, 0.0, n, n), a_t, q_t, sp.alpha, disp, sup, ctx=ctx)
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        M.node_field_device((0.0, 0.0, n, n), a_t, q_t, sp.alpha, disp, sup, ctx=ctx)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = min(ts)
+    xs, ys = rng.uniform(0, n, 20000), rng.uniform(0, n, 20000)
+    cut = -np.log(1e-6) / sp.alpha
+    per_px = float(np.mean([(((anchors[:, 0] - x) ** 2 + (anchors[:, 1] - y) ** 2) < cut).sum()
+                            for x, y in zip(xs, ys)]))
+    ctx.profile(True)
+    M.node_field_device((0.0, 0.0, n, n), a_t, q_t, sp.alpha, disp, sup, ctx=ctx)
+    torch.cuda.synchronize()
+    kt = ctx.kernel_times()
+    ctx.profile(False)
+    k_ms = kt.get("k_node_field", (ms, 1))[0]
+    ach = n * n * per_px * 18.0 / (k_ms * 1e-3) / 1e12
+    del disp, sup
+    torch.cuda.empty_cache()
+    return {"workload": f"configs[3] canvas-wide node field: {n}x{n} grid, {len(anchors)}-node canvas lattice",
+            "ms": ms, "gpx_per_s": n * n / (ms * 1e-3) / 1e9,
+            "kernels_ms": {k: v[0] for k, v in kt.items()},
+            "roofline_k_node_field": {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                                      "frac": ach / fp32_peak,
+                                      "algorithmic": f"{n * n} px x {per_px:.1f} contributing nodes x 18 flops"}}
 
 
 def em_estep_numbers(ctx, with_cpu: bool):
