@@ -481,8 +481,16 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     }
 
     // ---- E. epilogue --------------------------------------------------------
-    const double Y00 = pl.h.Y0[0], Y01 = pl.h.Y0[1], e00 = pl.h.e0[0], e01 = pl.h.e0[1];
-    const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
+    // Output position y = Y0 + r with the integer tile image origin Y0 and a
+    // tile-relative remainder r = e0 + dl P + (s0 + dl) Q(u) that stays small
+    // (|r| ~ 1e2 px): FP32 keeps it to ~1e-5 px at any canvas coordinate.
+    const double Y00 = pl.h.Y0[0], Y01 = pl.h.Y0[1];
+    const int Y0x = (int)Y00, Y0y = (int)Y01;  // rint() results: exact integers
+    const float P0f = (float)P0, P1f = (float)P1, s0f = (float)s0;
+    const float e00f = (float)pl.h.e0[0], e01f = (float)pl.h.e0[1];
+    const float fxm = (float)(L.fw - 1), fym = (float)(L.fh - 1);
+    // K2: displacement base (Y0 - tile origin), exact small integer - grid offset
+    const float bdx = (float)(Y00 - ox), bdy = (float)(Y01 - oy);
     int nb = 0, nns = 0, noof = 0;
     const int i = ti0 + col;
 #pragma unroll
@@ -509,32 +517,31 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                 const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
                 const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
                 const float dl = __fdividef(a4[j], a5[j]);  // a5 > 0, far from 2^126
-                const double sb = s0 + (double)dl;
-                const double yx = Y00 + (e00 + (double)dl * P0 + sb * (double)Qx);
-                const double yy = Y01 + (e01 + (double)dl * P1 + sb * (double)Qy);
+                const float sbf = s0f + dl;
+                const float rx = fmaf(sbf, Qx, fmaf(dl, P0f, e00f));
+                const float ry = fmaf(sbf, Qy, fmaf(dl, P1f, e01f));
                 if (MODE == 1) {
                     const size_t o = (size_t)(jj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
-                    if (L.disp)
-                        L.disp[o] = make_float2((float)(yx - (L.grid.gx + i)), (float)(yy - (L.grid.gy + jj)));
+                    if (L.disp) L.disp[o] = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
                     if (L.support) L.support[o] = 1;
                 } else {
-                    const double margin = fmin(fmin(yx, fxm - yx), fmin(yy, fym - yy));
-                    if (margin < -kBoundMargin) {
+                    const float yx = (float)Y0x + rx, yy = (float)Y0y + ry;  // margin test only
+                    const float margin = fminf(fminf(yx, fxm - yx), fminf(yy, fym - yy));
+                    if (margin < (float)-kBoundMargin) {
                         ++noof;
-                    } else if (margin < kBoundMargin) {
+                    } else if (margin < (float)kBoundMargin) {
                         exc = true;
                     } else {
-                        int x0 = (int)yx, y0 = (int)yy;
                         const int xc = L.fw - 2 >= 0 ? L.fw - 2 : 0, yc = L.fh - 2 >= 0 ? L.fh - 2 : 0;
-                        x0 = min(x0, xc);
-                        y0 = min(y0, yc);
-                        const float fx = (float)(yx - x0), fy = (float)(yy - y0);
+                        const int x0 = min(Y0x + (int)floorf(rx), xc), y0 = min(Y0y + (int)floorf(ry), yc);
+                        const float fx = rx - (float)(x0 - Y0x), fy = ry - (float)(y0 - Y0y);
                         const int x1 = min(x0 + 1, L.fw - 1), y1 = min(y0 + 1, L.fh - 1);
+                        const unsigned row0 = (unsigned)y0 * (unsigned)L.fw, row1 = (unsigned)y1 * (unsigned)L.fw;
                         float va[3], vb[3], vc[3], vd[3];
-                        texel(L.frame, (size_t)y0 * L.fw + x0, L.fch, va);
-                        texel(L.frame, (size_t)y0 * L.fw + x1, L.fch, vb);
-                        texel(L.frame, (size_t)y1 * L.fw + x0, L.fch, vc);
-                        texel(L.frame, (size_t)y1 * L.fw + x1, L.fch, vd);
+                        texel_u32(L.frame, row0 + x0, L.fch, va);
+                        texel_u32(L.frame, row0 + x1, L.fch, vb);
+                        texel_u32(L.frame, row1 + x0, L.fch, vc);
+                        texel_u32(L.frame, row1 + x1, L.fch, vd);
                         const float gx = 1.f - fx, gy = 1.f - fy;
                         const float vr = (gx * va[0] + fx * vb[0]) * gy + (gx * vc[0] + fx * vd[0]) * fy;
                         const float vg = (gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy;
@@ -548,8 +555,8 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                         float a = wd, cf = 1.f;
                         if (MODE == 2) {
                             const float* U = L.unc;
-                            const float u = (gx * U[(size_t)y0 * L.fw + x0] + fx * U[(size_t)y0 * L.fw + x1]) * gy +
-                                            (gx * U[(size_t)y1 * L.fw + x0] + fx * U[(size_t)y1 * L.fw + x1]) * fy;
+                            const float u = (gx * U[row0 + x0] + fx * U[row0 + x1]) * gy +
+                                            (gx * U[row1 + x0] + fx * U[row1 + x1]) * fy;
                             cf = __frcp_rn(fmaxf(u, 1.f));
                             a = wd + 1.f - cf;
                         }

@@ -141,6 +141,23 @@ __device__ __forceinline__ void texel(const uint8_t* __restrict__ f, size_t idx,
     }
 }
 
+// Same, 32-bit pixel index (frames below 2^31 bytes; fewer address ops).
+__device__ __forceinline__ void texel_u32(const uint8_t* __restrict__ f, unsigned idx, int ch, float* v) {
+    if (ch == 3) {
+        const uint8_t* p = f + 3u * idx;
+        v[0] = __ldg(p);
+        v[1] = __ldg(p + 1);
+        v[2] = __ldg(p + 2);
+    } else if (ch == 4) {
+        const uchar4 q = __ldg(reinterpret_cast<const uchar4*>(f) + idx);
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+    } else {
+        v[0] = v[1] = v[2] = __ldg(f + idx);
+    }
+}
+
 // sample_bilinear_rgb (image.hpp:78-92) in the exact tier.
 __device__ __forceinline__ void xsample_bilinear(const uint8_t* __restrict__ im, int iw, int ih, int ch,
                                                  double x, double y, double* out3) {
