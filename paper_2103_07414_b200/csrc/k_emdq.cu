@@ -203,6 +203,7 @@ __device__ __forceinline__ void radius_from_hist(const int* hist, int S, int lan
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists SL, int S, float pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int sid = blockIdx.y * SL.nsx + blockIdx.x;
@@ -433,6 +434,7 @@ __device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx
 __global__ void __launch_bounds__(PLAN_WARPS * 32)
 k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     PlanWarp& w = reinterpret_cast<PlanWarp*>(smem_raw)[wid];
     const int g = blockIdx.x * PLAN_WARPS + wid;  // tile index within the chunk
@@ -927,6 +929,7 @@ template <int MAXS>
 __global__ void __launch_bounds__(ENT, NRM_PIX_MINB)
 k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     __shared__ __align__(16) PixSmem s;
+    pdl_wait();
     const int g = blockIdx.y * TP.ntx + blockIdx.x;
     {
         const uint4* src = reinterpret_cast<const uint4*>(&TP.plan[g]);
@@ -1073,7 +1076,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     const size_t ssm = sizeof(SSmem);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
-    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, S, 0.f);
+    e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, L, C, SL, S, 0.f);
     ++*launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1090,13 +1093,13 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
         TP.ntx = ntx;
         const int ntiles = rows * ntx;
         prof_mark("k_plan", st);
-        k_plan<<<(ntiles + PLAN_WARPS - 1) / PLAN_WARPS, PLAN_WARPS * 32, psm, st>>>(L, C, SL, TP, ntiles, S);
+        e = launch_pdl(k_plan, dim3((ntiles + PLAN_WARPS - 1) / PLAN_WARPS), dim3(PLAN_WARPS * 32), psm, st, L, C, SL,
+                       TP, ntiles, S);
+        if (e != cudaSuccess) return e;
         ++*launches;
         prof_mark("k_pixels", st);
-        if (S <= 16)
-            k_pixels<16><<<dim3(ntx, rows), ENT, 0, st>>>(L, C, SL, TP, S);
-        else
-            k_pixels<MAX_SUPPORT><<<dim3(ntx, rows), ENT, 0, st>>>(L, C, SL, TP, S);
+        e = launch_pdl(S <= 16 ? k_pixels<16> : k_pixels<MAX_SUPPORT>, dim3(ntx, rows), dim3(ENT), 0, st, L, C, SL,
+                       TP, S);
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

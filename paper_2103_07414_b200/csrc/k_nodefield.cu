@@ -338,6 +338,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     Smem& s = *reinterpret_cast<Smem*>(smem_raw);
     CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
+    pdl_wait();
     const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x];
     const int status = pl.h.status;
     if (status == NF_OUTSIDE) return;
@@ -636,6 +637,7 @@ template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
     __shared__ bool last;
+    pdl_wait();
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + wid, nwarps = gridDim.x * (EXC_THREADS / 32);
@@ -888,15 +890,15 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
             L, plans, g.ti0, g.tj0, g.tj1, g.s1, by0, rows, g.ntx);
         ++*launches;
         prof_mark("k_node_field", st);
-        k_field<<<dim3(g.ntx, rows), NT, smem, st>>>(L, plans, g.ti0, g.tj0, g.s1, by0, g.ntx);
+        const cudaError_t e = launch_pdl(k_field, dim3(g.ntx, rows), dim3(NT), smem, st, L,
+                                         static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx);
         ++*launches;
-        const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     prof_mark("k_node_exceptions", st);
-    k_exc<<<EXC_BLOCKS, EXC_THREADS, 0, st>>>(L);
+    const cudaError_t e = launch_pdl(k_exc, dim3(EXC_BLOCKS), dim3(EXC_THREADS), 0, st, L);
     ++*launches;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_pixel_warp_points(const double* pts, int npts, const double* anchors,

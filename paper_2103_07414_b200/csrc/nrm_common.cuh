@@ -197,6 +197,19 @@ __device__ __forceinline__ double xsample_bilinear_f32(const float* __restrict__
     return xadd(xmul(xadd(xmul(gx, a), xmul(fx, b)), gy), xmul(xadd(xmul(gx, c), xmul(fx, d)), fy));
 }
 
+// ---- programmatic dependent launch (sm_90+) -------------------------------
+// A kernel launched with launch_pdl() may be scheduled before its stream
+// predecessor finishes; it must call pdl_wait() before touching anything the
+// predecessor writes (or reads). -DNRM_NO_PDL makes both plain launches.
+#ifndef NRM_NO_PDL
+#define NRM_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#ifdef NRM_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
 // ---- fast tier ----------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -264,5 +277,26 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+#ifdef NRM_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+#else
+    kern<<<grid, block, smem, st>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+#endif
+}
 
 }  // namespace nrm
