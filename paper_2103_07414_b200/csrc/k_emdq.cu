@@ -838,12 +838,12 @@ __device__ __forceinline__ void fast_dispatch(int col, int row, int nin, const u
 // (the tile flags are uniform).
 // ---------------------------------------------------------------------------
 template <int MAXS>
-__device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, const SuperLists& SL, const PixSmem& s,
+__device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, const SuperLists& SL, const TilePlan& sp,
                                             float (*ex)[ET], float (*ey)[ET], int tx, int ty, int S) {
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int ti0 = L.grid.i0 + tx * ET, tj0 = L.grid.j0 + ty * ET;
     const int ti1 = min(ti0 + ET - 1, L.grid.i1), tj1 = min(tj0 + ET - 1, L.grid.j1);
-    const TileHdr& h = s.p.hdr;
+    const TileHdr& h = sp.hdr;
     const int flags = h.flags;
 
     const int lx = (wid & 1) * 8 + (lane & 7), ly = (wid >> 1) * 4 + (lane >> 3);
@@ -870,7 +870,7 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
         const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
         for (int e = t; e < ne * ET; e += ENT) {  // one column and one row entry per iteration
             const int k = e / ET, c = e % ET;
-            const float4 r0 = s.p.rec0[k];
+            const float4 r0 = sp.rec0[k];
             const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
             const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
             const float dx = r0.x - (float)c, dy = r0.y - (float)c;
@@ -882,19 +882,19 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     if (!valid) return;
     if (flags & TFLAG_EXACT_STAGED) {
         if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, s.p.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        exact_dispatch<MAXS>(qx, qy, sp.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
     const int wi = nin + nxin, m = S - wi;
     FastOut fo;
     bool exr = nxin == 255 || m < 0 || wi + namb < S || namb > 32;
     if (!exr) {
-        fast_dispatch(lx, ly, nin, s.p.sub[wid], nxin, namb, m, s.p, ex, ey, fo);
+        fast_dispatch(lx, ly, nin, sp.sub[wid], nxin, namb, m, sp, ex, ey, fo);
         exr = fo.exact || !(fo.s5 > 0.f);
     }
     if (exr) {
         if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, s.p.sidx, ne, S, C, L.alpha, L.beta, od, ou);
+        exact_dispatch<MAXS>(qx, qy, sp.sidx, ne, S, C, L.alpha, L.beta, od, ou);
         return;
     }
     const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
@@ -914,8 +914,8 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
         double d2m = DBL_MAX;
         const int nl = nnear == 255 ? ne : nnear;
         for (int e = 0; e < nl; ++e) {
-            const int k = nnear == 255 ? e : s.p.near[wid][e];
-            const double2 a = s.p.axy[k];
+            const int k = nnear == 255 ? e : sp.near[wid][e];
+            const double2 a = sp.axy[k];
             d2m = fmin(d2m, xdist2(qx, qy, a.x, a.y));
         }
         double arg = xmul(L.beta, d2m);
@@ -937,7 +937,7 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
         for (int k = threadIdx.x; k < (int)(sizeof(TilePlan) / 16); k += ENT) dst[k] = src[k];
     }
     __syncthreads();
-    pixels_tile<MAXS>(L, C, SL, s, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
+    pixels_tile<MAXS>(L, C, SL, s.p, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
 }
 
 // ---------------------------------------------------------------------------
