@@ -167,10 +167,25 @@ __device__ __forceinline__ const int* chunk_nodes(const NodeFieldLaunch& L, int 
     return L.lists + (size_t)li * L.lstride;
 }
 
+__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int tile_i0,
+                                             int tile_j0, int tile_j_last, int s1, int by0, int rows, int ntx,
+                                             unsigned (*list_s)[NF_CAP]);
+
+// The planner reads only the nodes, so it may run while the previous blend's
+// exact pass finishes (programmatic dependent launch); it waits for that
+// predecessor before exiting, which keeps the canvas order for the next
+// kernel (k_node_field waits for the planner).
 __global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
 k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
           int rows, int ntx) {
     __shared__ unsigned list_s[NF_PLAN_WARPS][NF_CAP];
+    nf_plan_tile(L, plans, tile_i0, tile_j0, tile_j_last, s1, by0, rows, ntx, list_s);
+    pdl_wait();
+}
+
+__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int tile_i0,
+                                             int tile_j0, int tile_j_last, int s1, int by0, int rows, int ntx,
+                                             unsigned (*list_s)[NF_CAP]) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.x * NF_PLAN_WARPS + wid;
     if (g >= rows * ntx) return;
@@ -637,6 +652,7 @@ template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
     __shared__ bool last;
+    pdl_trigger();  // the next blend's planner may start (it only reads nodes)
     pdl_wait();
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -886,11 +902,13 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         const int rows = min(g.chunk_rows, g.nty - by0);
         if ((size_t)rows * g.ntx > (size_t)NF_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
         prof_mark("k_nf_plan", st);
-        k_nf_plan<<<(rows * g.ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS, NF_PLAN_WARPS * 32, 0, st>>>(
-            L, plans, g.ti0, g.tj0, g.tj1, g.s1, by0, rows, g.ntx);
+        cudaError_t e = launch_pdl(k_nf_plan, dim3((rows * g.ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS),
+                                   dim3(NF_PLAN_WARPS * 32), 0, st, L, plans, g.ti0, g.tj0, g.tj1, g.s1, by0, rows,
+                                   g.ntx);
         ++*launches;
+        if (e != cudaSuccess) return e;
         prof_mark("k_node_field", st);
-        const cudaError_t e = launch_pdl(k_field, dim3(g.ntx, rows), dim3(NT), smem, st, L,
+        e = launch_pdl(k_field, dim3(g.ntx, rows), dim3(NT), smem, st, L,
                                          static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx);
         ++*launches;
         if (e != cudaSuccess) return e;

@@ -209,6 +209,12 @@ __device__ __forceinline__ void pdl_wait() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
+// Lets the stream successor (launched with launch_pdl) be scheduled now.
+__device__ __forceinline__ void pdl_trigger() {
+#ifdef NRM_PDL
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 // ---- fast tier ----------------------------------------------------------
 __device__ __forceinline__ float ex2_approx(float x) {
