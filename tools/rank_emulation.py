@@ -63,4 +63,14 @@ for G in Gs:
         ts.append((a, b))
     torch.cuda.synchronize()
     ms = sorted(x.elapsed_time(y) for x, y in ts)[len(ts) // 2]
-    print(json.dumps({"G": G, "per_rank_step_ms": ms, "rank_frames_per_s": G / (ms * 1e-3)}), flush=True)
+    # serialised per-kernel times of one rank's step (library CUDA events)
+    ctx.profile(True)
+    ctx_b.profile(True)
+    for _ in range(20):
+        step()
+    torch.cuda.synchronize()
+    kt = {k: round(1e3 * v[0] / 20, 1) for k, v in {**ctx.kernel_times(), **ctx_b.kernel_times()}.items()}
+    ctx.profile(False)
+    ctx_b.profile(False)
+    print(json.dumps({"G": G, "per_rank_step_ms": ms, "rank_frames_per_s": G / (ms * 1e-3),
+                      "kernel_us_per_step": kt}), flush=True)
