@@ -602,46 +602,58 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
 __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ anchors,
                                 const double* __restrict__ warps, const int* __restrict__ src, int n, double alpha,
                                 W5* out) {
+    constexpr int KC = 4;  // node chunks whose weights are evaluated together (latency, not throughput)
     const int lane = threadIdx.x & 31;
     const double na = -alpha;
     double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
     double ref_w = 0.0, ref_z = 0.0;
     bool have_ref = false;
-    for (int c0 = 0; c0 < n; c0 += 32) {
-        const int e = c0 + lane;
-        const int i = e < n ? (src ? src[e] : e) : 0;  // src: index-ordered subset
-        double w = 0.0, q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        bool contrib = false;
-        if (e < n) {
-            const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
-            w = xexp(xmul(na, d2));
-            contrib = !(w <= kPixelWeightCutoff);
+    for (int g0 = 0; g0 < n; g0 += 32 * KC) {
+        double w[KC], q[KC][5];
+        bool contrib[KC];
 #pragma unroll
-            for (int k = 0; k < 5; ++k) q[k] = __ldg(&warps[5 * i + k]);
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, contrib);
-        if (!m) continue;
-        if (!have_ref) {  // first contributing node in index order
-            const int src = __ffs(m) - 1;
-            ref_w = __shfl_sync(0xffffffffu, q[1], src);
-            ref_z = __shfl_sync(0xffffffffu, q[2], src);
-            have_ref = true;
-            if (lane != src && xadd(xmul(q[1], ref_w), xmul(q[2], ref_z)) < 0.0) {
-                q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; q[4] = -q[4];
+        for (int c = 0; c < KC; ++c) {  // independent: loads and exps overlap
+            const int e = g0 + 32 * c + lane;
+            w[c] = 0.0;
+            contrib[c] = false;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) q[c][k] = 0.0;
+            if (e < n) {
+                const int i = src ? src[e] : e;  // src: index-ordered subset
+                const double d2 = xdist2(__ldg(&anchors[2 * i]), __ldg(&anchors[2 * i + 1]), x, y);
+                w[c] = xexp(xmul(na, d2));
+                contrib[c] = !(w[c] <= kPixelWeightCutoff);
+#pragma unroll
+                for (int k = 0; k < 5; ++k) q[c][k] = __ldg(&warps[5 * i + k]);
             }
-        } else if (xadd(xmul(q[1], ref_w), xmul(q[2], ref_z)) < 0.0) {
-            q[1] = -q[1]; q[2] = -q[2]; q[3] = -q[3]; q[4] = -q[4];
         }
-        const double p0 = xmul(w, q[1]), p1 = xmul(w, q[2]), p2 = xmul(w, q[3]), p3 = xmul(w, q[4]);
-        const double p4 = xmul(w, q[0]);
-        for (unsigned mm = m; mm; mm &= mm - 1) {
-            const int j = __ffs(mm) - 1;
-            aw = xadd(aw, __shfl_sync(0xffffffffu, p0, j));
-            az = xadd(az, __shfl_sync(0xffffffffu, p1, j));
-            adx = xadd(adx, __shfl_sync(0xffffffffu, p2, j));
-            ady = xadd(ady, __shfl_sync(0xffffffffu, p3, j));
-            as = xadd(as, __shfl_sync(0xffffffffu, p4, j));
-            wsum = xadd(wsum, __shfl_sync(0xffffffffu, w, j));
+#pragma unroll
+        for (int c = 0; c < KC; ++c) {  // ordered accumulation, chunk by chunk
+            const unsigned m = __ballot_sync(0xffffffffu, contrib[c]);
+            if (!m) continue;
+            double* qc = q[c];
+            if (!have_ref) {  // first contributing node in index order
+                const int sl = __ffs(m) - 1;
+                ref_w = __shfl_sync(0xffffffffu, qc[1], sl);
+                ref_z = __shfl_sync(0xffffffffu, qc[2], sl);
+                have_ref = true;
+                if (lane != sl && xadd(xmul(qc[1], ref_w), xmul(qc[2], ref_z)) < 0.0) {
+                    qc[1] = -qc[1]; qc[2] = -qc[2]; qc[3] = -qc[3]; qc[4] = -qc[4];
+                }
+            } else if (xadd(xmul(qc[1], ref_w), xmul(qc[2], ref_z)) < 0.0) {
+                qc[1] = -qc[1]; qc[2] = -qc[2]; qc[3] = -qc[3]; qc[4] = -qc[4];
+            }
+            const double p0 = xmul(w[c], qc[1]), p1 = xmul(w[c], qc[2]), p2 = xmul(w[c], qc[3]);
+            const double p3 = xmul(w[c], qc[4]), p4 = xmul(w[c], qc[0]);
+            for (unsigned mm = m; mm; mm &= mm - 1) {
+                const int jl = __ffs(mm) - 1;
+                aw = xadd(aw, __shfl_sync(0xffffffffu, p0, jl));
+                az = xadd(az, __shfl_sync(0xffffffffu, p1, jl));
+                adx = xadd(adx, __shfl_sync(0xffffffffu, p2, jl));
+                ady = xadd(ady, __shfl_sync(0xffffffffu, p3, jl));
+                as = xadd(as, __shfl_sync(0xffffffffu, p4, jl));
+                wsum = xadd(wsum, __shfl_sync(0xffffffffu, w[c], jl));
+            }
         }
     }
     XPW s{wsum, aw, az, adx, ady, as, ref_w, ref_z, have_ref};
