@@ -599,9 +599,10 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
 // evaluate the node weights in parallel (exact tier), then every lane sums the
 // contributors' products in ascending node order -- the reference's order, so
 // the result is bit-identical -- with shuffles. All lanes end with the result.
+// stage: optional per-warp shared scratch (32 x 6 doubles) for the ordered sum.
 __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ anchors,
                                 const double* __restrict__ warps, const int* __restrict__ src, int n, double alpha,
-                                W5* out) {
+                                W5* out, double* stage = nullptr) {
     constexpr int KC = 4;  // node chunks whose weights are evaluated together (latency, not throughput)
     const int lane = threadIdx.x & 31;
     const double na = -alpha;
@@ -643,6 +644,35 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
             } else if (xadd(xmul(qc[1], ref_w), xmul(qc[2], ref_z)) < 0.0) {
                 qc[1] = -qc[1]; qc[2] = -qc[2]; qc[3] = -qc[3]; qc[4] = -qc[4];
             }
+            if (stage) {
+                // contributors' terms in index order through shared memory; lane 0
+                // adds them with pipelined loads (same sequence of rounded adds)
+                if (contrib[c]) {
+                    double* d = stage + 6 * __popc(m & ((1u << lane) - 1u));
+                    d[0] = xmul(w[c], qc[1]);
+                    d[1] = xmul(w[c], qc[2]);
+                    d[2] = xmul(w[c], qc[3]);
+                    d[3] = xmul(w[c], qc[4]);
+                    d[4] = xmul(w[c], qc[0]);
+                    d[5] = w[c];
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    const int cnt = __popc(m);
+#pragma unroll 4
+                    for (int e = 0; e < cnt; ++e) {
+                        const double* d = stage + 6 * e;
+                        aw = xadd(aw, d[0]);
+                        az = xadd(az, d[1]);
+                        adx = xadd(adx, d[2]);
+                        ady = xadd(ady, d[3]);
+                        as = xadd(as, d[4]);
+                        wsum = xadd(wsum, d[5]);
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
             const double p0 = xmul(w[c], qc[1]), p1 = xmul(w[c], qc[2]), p2 = xmul(w[c], qc[3]);
             const double p3 = xmul(w[c], qc[4]), p4 = xmul(w[c], qc[0]);
             for (unsigned mm = m; mm; mm &= mm - 1) {
@@ -656,6 +686,14 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
             }
         }
     }
+    if (stage) {  // lane 0 holds the sums
+        aw = __shfl_sync(0xffffffffu, aw, 0);
+        az = __shfl_sync(0xffffffffu, az, 0);
+        adx = __shfl_sync(0xffffffffu, adx, 0);
+        ady = __shfl_sync(0xffffffffu, ady, 0);
+        as = __shfl_sync(0xffffffffu, as, 0);
+        wsum = __shfl_sync(0xffffffffu, wsum, 0);
+    }
     XPW s{wsum, aw, az, adx, ady, as, ref_w, ref_z, have_ref};
     return xpw_finish(s, out);
 }
@@ -664,6 +702,7 @@ template <int MODE>
 __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
     __shared__ int red[3][EXC_THREADS / 32];
     __shared__ bool last;
+    __shared__ double stage[EXC_THREADS / 32][32 * 6];
     pdl_trigger();  // the next blend's planner may start (it only reads nodes)
     pdl_wait();
     const unsigned cnt = min(*L.exc_count, L.exc_cap);
@@ -683,7 +722,7 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         int nsrc;
         const int tix = floordiv(p.x, TW) - floordiv(L.grid.i0, TW);
         const int* src = chunk_nodes(L, by / L.chunk_rows, tix / NF_GROUP_TILES, &nsrc);
-        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp);
+        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp, stage[wid]);
         if (lane != 0) continue;
         if (MODE == 1) {
             const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
