@@ -113,3 +113,25 @@ def test_deform_edges(nrm, ctx, golden):
     banded.set_band(0, 2)
     with pytest.raises(ValueError):
         banded.deform(np.zeros((8, 8, 2), np.float32))
+
+
+def test_rgba_frame_ignores_alpha(nrm, ctx, oracle, golden):
+    """ImageU8 with 4 channels: sample_bilinear_rgb reads RGB and ignores
+    alpha (image.hpp:78-92). An RGBA copy of the golden frame must give the
+    same canvas as the RGB frame, on the GPU and in the oracle."""
+    g = golden("blend_c1")
+    poly = g["polys"][: g["npoly"][0]]
+    rgb = g["frame"]
+    rng = np.random.default_rng(4)
+    rgba = np.concatenate([rgb, rng.integers(0, 256, rgb.shape[:2] + (1,), dtype=np.uint8)], axis=2)
+    a, b = nrm.Canvas(ctx), nrm.Canvas(ctx)
+    sa = nrm.blend_frame(a, rgb, g["anchors"], g["warps"][0], float(g["alpha"]), poly).as_tuple()
+    sb = nrm.blend_frame(b, rgba, g["anchors"], g["warps"][0], float(g["alpha"]), poly).as_tuple()
+    assert sa == sb
+    ca, wa = a.read()
+    cb, wb = b.read()
+    assert np.array_equal(wa, wb) and np.array_equal(ca, cb)
+    oa, ob = oracle.canvas(), oracle.canvas()
+    assert oracle.blend_frame(oa, rgb, g["anchors"], g["warps"][0], float(g["alpha"]), poly) == \
+        oracle.blend_frame(ob, rgba, g["anchors"], g["warps"][0], float(g["alpha"]), poly)
+    assert np.array_equal(oa.arrays()[0], ob.arrays()[0])
