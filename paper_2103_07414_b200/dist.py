@@ -13,8 +13,8 @@ Collectives (torch.distributed; NCCL over NVLink on GPUs, gloo in tests):
                        no-support / out-of-frame counts (footprint is the same
                        on every rank and is taken from rank-local stats)
   assemble_bbox     -- crop box for render(crop=True): min/max over ranks
-  assemble_render   -- rendered RGBA bands, SUM-reduced to the destination
-                       rank (non-owned rows are zero, so the sum is exact)
+  assemble_render   -- rendered RGBA bands: each rank sends only its owned
+                       rows (one gather of equal-size padded stripe packs)
 No collective touches the per-pixel data path of blend_frame itself.
 """
 from __future__ import annotations
@@ -66,10 +66,32 @@ def assemble_bbox(bbox4: Tuple[int, int, int, int], group=None, device=None) -> 
     return int(v[0]), int(v[1]), int(-v[2]), int(-v[3])
 
 
-def assemble_render(local_rgba, dst: int = 0, group=None):
-    """SUM-reduce rank-local RGBA rasters (uint8, zeros outside owned rows)."""
+def assemble_render(local_rgba, origin_y: int, rank: int, world: int, dst: int = 0, group=None):
+    """Assembles rank-local RGBA rasters (h, w, 4) whose row 0 is reference
+    row origin_y: every rank packs the rows it owns (owned_rows_mask) and
+    one gather brings the packs to `dst`, which writes them into its raster.
+    Each rank moves ~1/world of the image. Returns the assembled raster on
+    dst (the local raster elsewhere)."""
+    import torch
     import torch.distributed as dist
-    dist.reduce(local_rgba, dst=dst, group=group)
+    if world <= 1:
+        return local_rgba
+    h = local_rgba.shape[0]
+    masks = [torch.from_numpy(owned_rows_mask(origin_y, h, r, world)) for r in range(world)]
+    rows = [int(m.sum()) for m in masks]
+    cap = max(max(rows), 1)
+    pack = torch.zeros((cap,) + tuple(local_rgba.shape[1:]), dtype=local_rgba.dtype, device=local_rgba.device)
+    mine = masks[rank].to(local_rgba.device)
+    if rows[rank]:
+        pack[: rows[rank]] = local_rgba[mine]
+    if rank == dst:
+        packs = [torch.empty_like(pack) for _ in range(world)]
+        dist.gather(pack, packs, dst=dst, group=group)
+        for r in range(world):
+            if rows[r]:
+                local_rgba[masks[r].to(local_rgba.device)] = packs[r][: rows[r]]
+    else:
+        dist.gather(pack, None, dst=dst, group=group)
     return local_rgba
 
 
@@ -111,5 +133,5 @@ class BandedMosaic:
         out = torch.zeros((y1 - y0 + 1, x1 - x0 + 1, 4), dtype=torch.uint8, device=dev)
         self.M.render_device(self.canvas, x0, y0, x1 - x0 + 1, y1 - y0 + 1, out)
         self.ctx.synchronize()
-        assemble_render(out, dst=dst)
+        assemble_render(out, int(oy) + y0, self.rank, self.world, dst=dst)
         return out.cpu().numpy(), (ox + x0, oy + y0)

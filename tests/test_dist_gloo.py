@@ -59,7 +59,7 @@ def _worker(rank, world, port, q):
             if len(occ) else (0, 0, -1, -1)
         x0, y0, x1, y1 = D.assemble_bbox(bb)
         crop = torch.from_numpy(np.ascontiguousarray(local[y0:y1 + 1, x0:x1 + 1]))
-        D.assemble_render(crop, dst=0)
+        D.assemble_render(crop, oy + y0, rank, world, dst=0)
         if rank == 0:
             ref_crop, ref_org = O.render(cv, crop=True)
             q.put(("ok", np.array_equal(crop.numpy(), ref_crop), (ox + x0, oy + y0) == ref_org,
@@ -72,7 +72,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_banded_assembly_equals_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
