@@ -131,19 +131,31 @@ class ClockSampler:
 # CPU reference arm (oracle/_ref: the reference headers compiled in place;
 # else the C restatement). Bounded sample of the same workload.
 # ---------------------------------------------------------------------------
-def cpu_reference_step(wl, poly, rows: int, workers: int):
-    """Times one sampled step on the host: blend_frame (full footprint) plus
-    the dense EMDQ field over `rows` frame rows; returns (sec per frame-equivalent, info)."""
+def cpu_reference_step(wl, poly, rows: int, workers: int, blend_rows: int = 0):
+    """Times one sampled step on the host: blend_frame over the footprint (or,
+    with blend_rows > 0, over a centred strip of that many canvas rows of the
+    footprint's bounding box: the reference iterates the polygon's bbox,
+    mosaic.hpp:203-229) plus the dense EMDQ field over `rows` frame rows; both
+    are extrapolated to a frame. Returns (sec per frame-equivalent, info)."""
     from oracle import oracle as orc
 
     e = wl.emdq
     H = wl.frame_h
     r0 = (H - rows) // 2
     grid = (0.0, 0.0, wl.frame_w, H)
-    pre = np.array(wl.canvas_rect)
+    bx0, by0 = poly[:, 0].min(), poly[:, 1].min()
+    bx1, by1 = poly[:, 0].max(), poly[:, 1].max()
+    full_rows = int(np.ceil(by1 + 4.0) - np.floor(by0 - 4.0)) + 1
+    scale, bpoly = 1.0, poly
+    if 0 < blend_rows < full_rows - 16:
+        ym = 0.5 * (by0 + by1)
+        h = max(1.0, blend_rows - 9.0)  # the bbox is expanded by 4 px on each side
+        bpoly = np.array([[bx0, ym], [bx1, ym], [bx1, ym + h], [bx0, ym + h]])
+        scale = full_rows / float(int(np.ceil(ym + h + 4.0) - np.floor(ym - 4.0)) + 1)
+    pre = np.array([bpoly[:, 0].min() - 5, bpoly[:, 1].min() - 5, bpoly[:, 0].max() + 5, bpoly[:, 1].max() + 5])
     if orc.reference_available():
         R = orc.Reference()
-        t_blend, st = R.time_blend_frame(wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly, pre, workers)
+        t_blend, st = R.time_blend_frame(wl.frame, wl.anchors, wl.warps, wl.params.alpha, bpoly, pre, workers)
         t0 = time.perf_counter()
         R.emdq_field_grid(grid, e.apts, e.locals_, e.probs, e.active, wl.params.alpha, wl.params.beta, 16,
                           workers=workers, rows=(r0, r0 + rows))
@@ -154,16 +166,17 @@ def cpu_reference_step(wl, poly, rows: int, workers: int):
         cv = O.canvas()
         cv.ensure_contains(pre)
         t0 = time.perf_counter()
-        O.blend_frame(cv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly)
+        O.blend_frame(cv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, bpoly)
         t_blend = time.perf_counter() - t0
         t0 = time.perf_counter()
         O.emdq_field_grid(grid, e.apts, e.locals_, e.probs, e.active, wl.params.alpha, wl.params.beta, 16,
                           rows=(r0, r0 + rows))
         t_field = time.perf_counter() - t0
         kind, workers = "port", 1
-    t_frame = t_blend + t_field * (H / rows)
+    t_frame = t_blend * scale + t_field * (H / rows)
     return t_frame, {"kind": kind, "cores": workers, "t_blend_s": t_blend, "t_field_sample_s": t_field,
-                     "field_rows": rows}
+                     "field_rows": rows, "blend_rows": full_rows if scale == 1.0 else blend_rows,
+                     "blend_rows_full": full_rows}
 
 
 def run_reference_arm(args, wl_name):
@@ -175,12 +188,21 @@ def run_reference_arm(args, wl_name):
     wl = W.frame_workload(wl_name)
     poly = footprint_polygon_cpu(wl)
     model, ncpu = host_cpu()
-    rows = max(8, min(wl.frame_h, args.ref_rows))
+    # size each step's sample so that warmup + steps stay within ~2.5 minutes:
+    # calibrate the per-row costs once, then split the per-step budget
+    budget = min(30.0, 150.0 / max(1, args.steps + args.warmup))
+    _, cal = cpu_reference_step(wl, poly, 8, ncpu, blend_rows=64)
+    per_b = cal["t_blend_s"] / max(cal["blend_rows"], 1)
+    per_f = cal["t_field_sample_s"] / 8
+    # floors keep every worker busy (8-row chunks, parallel.hpp:29-60), so a
+    # small sample is not slower per row than the full frame
+    brows = int(min(cal["blend_rows_full"], max(16 * 8 * ncpu // 8, 0.5 * budget / max(per_b, 1e-9))))
+    rows = int(min(wl.frame_h, max(2 * ncpu, 0.5 * budget / max(per_f, 1e-9))))
     for _ in range(args.warmup):
-        cpu_reference_step(wl, poly, rows, ncpu)
+        cpu_reference_step(wl, poly, rows, ncpu, blend_rows=brows)
     times, info = [], None
     for _ in range(args.steps):
-        t, info = cpu_reference_step(wl, poly, rows, ncpu)
+        t, info = cpu_reference_step(wl, poly, rows, ncpu, blend_rows=brows)
         times.append(t)
     tot = sum(times)
     mpix = wl.frame_w * wl.frame_h / 1e6
@@ -193,8 +215,9 @@ def run_reference_arm(args, wl_name):
         "config": {"workload": CFG_NAME[wl_name], "frame": [wl.frame_w, wl.frame_h], "matches": len(wl.emdq.apts),
                    "inliers": int(len(wl.emdq.active)), "nodes": int(len(wl.anchors)), "canvas": wl.canvas},
         "cpu_baseline": {"value": value, "unit": "Mpix/s", "cores": info["cores"], "kind": info["kind"],
-                         "sample": f"per step: full blend_frame + dense EMDQ field over {rows} of {wl.frame_h} "
-                                   f"frame rows, extrapolated to the frame; host {model}"},
+                         "sample": f"per step: blend_frame over {info['blend_rows']} of {info['blend_rows_full']} "
+                                   f"footprint rows + dense EMDQ field over {rows} of {wl.frame_h} frame rows, "
+                                   f"extrapolated to the frame; host {model}"},
         "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
