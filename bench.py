@@ -522,11 +522,18 @@ def main():
         # per profiled step: K1 blends nfr frames, K3 computes one field
         algo = {"k_node_field": contrib["pairs"] * 18.0 * nfr, "k_pixels": fw * fh * 16 * 18.0}
         traffic = load_traffic()
+        # issue-rate view: ncu warp instructions per launch over the live launch
+        # time against the scheduler peak (SMs x 4 issue slots x SM clock)
+        insts = load_traffic("instructions.json")
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        clk_hz = 1e6 * (clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0)
         kernels = []
         for name, (tot_ms, n) in sorted(kt.items(), key=lambda kv: -kv[1][0]):
             per = tot_ms / max(n, 1)
             ent = {"kernel": name, "ms_per_launch": per, "launches": n,
                    "share_of_step": tot_ms / max(sum(v[0] for v in kt.values()), 1e-9)}
+            if name in insts and per > 0:
+                ent["issue_frac"] = insts[name] / (per * 1e-3 * nsm * 4 * clk_hz)
             if name in algo:
                 # total algorithmic flops over total kernel time (= per launch when a
                 # step's work is split into equal launch chunks)
@@ -551,6 +558,11 @@ def main():
         roof["hbm_view_k_node_field"] = {"achieved_gbs": fp_px * 29 * nfr * prof_steps / (max(kb[0], 1e-9) * 1e-3) / 1e9,
                                          "peak_gbs": peaks.get("hbm_gbs"), "bytes_per_footprint_px": 29}
         roof["kernels"] = kernels
+        if "issue_frac" in dom:
+            roof["issue_view"] = {"issue_frac": dom["issue_frac"],
+                                  "definition": "ncu smsp__inst_executed.sum per launch (profiles/instructions.json) "
+                                                "/ (live launch time x SMs x 4 schedulers x sampled SM clock)",
+                                  "note": "the dense-stage kernels are instruction-issue bound, not HBM bound"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -703,8 +715,8 @@ def wl_contributors(wl, poly, sample: int = 20000):
     return {"pairs": float(npx * cnt), "per_px": float(cnt)}
 
 
-def load_traffic():
-    p = ROOT / "profiles" / "traffic.json"
+def load_traffic(name: str = "traffic.json"):
+    p = ROOT / "profiles" / name
     try:
         return json.loads(p.read_text())
     except Exception:
