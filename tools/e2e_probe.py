@@ -114,3 +114,32 @@ st = [min(durs["field"][i][0], durs["blend"][i][0]) for i in range(30)]
 off = [(durs["blend"][i][0] - durs["field"][i][0]) * 1e3 for i in range(30)]
 print("blend start - field start (ms) median", round(S.median(off[5:]), 3))
 print(f"field || field-dev {tm(lambda: (pool.submit(field_dev), blend())):.3f}")
+
+# ---- fields in flight (own contexts + pinned outputs), with and without the blend
+import collections  # noqa: E402
+for nfl in (1, 2, 3):
+    ctxs = [ctx] + [M.Context(0) for _ in range(nfl - 1)]
+    outs = [(h_disp, h_unc)] + [(torch.empty((fh, fw, 2), dtype=torch.float32).pin_memory().numpy(),
+                                 torch.empty((fh, fw), dtype=torch.float32).pin_memory().numpy())
+                                for _ in range(nfl - 1)]
+
+    def fld(k):
+        c_, (d_, u_) = ctxs[k], outs[k]
+        M.check(lib.nrm_emdq_field(c_.handle, C.byref(g), h_apts.ctypes.data, h_loc.ctypes.data, h_prob.ctypes.data,
+                                   len(h_apts), h_act.ctypes.data, len(h_act), alpha, 16, beta, d_.ctypes.data,
+                                   u_.ctypes.data))
+    pl = ThreadPoolExecutor(nfl)
+    for with_blend in (False, True):
+        pend = collections.deque()
+        t0 = time.perf_counter()
+        N = 200
+        for i in range(N):
+            if len(pend) == nfl:
+                pend.popleft().result()
+            pend.append(pl.submit(fld, i % nfl))
+            if with_blend:
+                blend()
+        while pend:
+            pend.popleft().result()
+        dt = (time.perf_counter() - t0) / N
+        print(f"fields in flight {nfl}, blend {with_blend}: {dt * 1e3:.3f} ms/frame, {1 / dt:.0f} frames/s")
