@@ -111,7 +111,7 @@ struct TilePlans {
 struct PlanWarp {
     int hist[256];
     int cand[TCAND];
-    double dmin2[TCAND], dmax2[TCAND], dc2[TCAND];
+    double dmin2[TCAND], dmax2[TCAND], dc2[TCAND];  // dmin2: float2 bounds; dmax2: ambiguous keys
     unsigned char cls[TCAND];
     int sidx[TREC];
     float2 wd[TREC];
@@ -491,55 +491,70 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     nc = min(nc, TCAND);
     __syncwarp();
 
-    // 3. FP64 classification against the tile rectangle
+    // 3. classification against the tile rectangle. The bounds are FP64 and
+    //    rounded outwards to FP32 (dmin down, dmax up), and the FP32 margins
+    //    (1e-6 relative) dwarf the FP64 rounding of the pixels' exact d^2, so
+    //    "in" and "out" stay conservative.
+    float2* dmm = reinterpret_cast<float2*>(w.dmin2);  // {dmin^2, dmax^2} per candidate
     for (int k = lane; k < nc; k += 32) {
         const int a = w.cand[k];
         const double ax = C.x[a], ay = C.y[a];
         const double dxn = fmax(fmax(xlo - ax, 0.0), ax - xhi), dyn = fmax(fmax(ylo - ay, 0.0), ay - yhi);
         const double dxf = fmax(ax - xlo, xhi - ax), dyf = fmax(ay - ylo, yhi - ay);
-        w.dmin2[k] = dxn * dxn + dyn * dyn;
-        w.dmax2[k] = dxf * dxf + dyf * dyf;
+        dmm[k] = make_float2(__double2float_rd(dxn * dxn + dyn * dyn), __double2float_ru(dxf * dxf + dyf * dyf));
         w.dc2[k] = (ax - cxm) * (ax - cxm) + (ay - cym) * (ay - cym);
     }
     __syncwarp();
     for (int k = lane; k < nc; k += 32) {
-        const double hi = w.dmax2[k] * (1.0 + 1e-12) + 1e-9;
-        const double lo = w.dmin2[k] * (1.0 - 1e-12) - 1e-9;
-        int cle = 0, clt = 0;
+        const float2 dk = dmm[k];
+        const float hi = fmaf(dk.y, 1.000001f, 1e-6f), lo = fmaf(dk.x, 0.999999f, -1e-6f);
+        int cle = -1, clt = 0;  // l == k always counts in cle, never in clt
+#pragma unroll 4
         for (int l = 0; l < nc; ++l) {
-            if (l == k) continue;
-            cle += w.dmin2[l] <= hi;
-            clt += w.dmax2[l] < lo;
+            const float2 dl = dmm[l];
+            cle += dl.x <= hi;
+            clt += dl.y < lo;
         }
         w.cls[k] = cle < S ? 1 : (clt >= S ? 0 : 2);
     }
     __syncwarp();
 
-    // 4. staging order + tile reference
+    // 4. staging order + tile reference. The ambiguous are staged closest to
+    //    the tile centre first (a heuristic order for the pixels' early-reject
+    //    insertion, not a correctness property): unique 32-bit keys = FP32
+    //    centre distance with the candidate slot in the low 7 bits.
+    unsigned* akey = reinterpret_cast<unsigned*>(w.dmax2);
+    int* acand = reinterpret_cast<int*>(akey + TCAND);
     int ni = 0, na = 0;
     for (int base = 0; base < nc; base += 32) {
         const int k = base + lane;
         const int c = k < nc ? w.cls[k] : 0;
+        const unsigned below = (1u << lane) - 1u;
         const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-        if (c == 1 && ni + __popc(mi & ((1u << lane) - 1u)) < TREC)
-            w.sidx[ni + __popc(mi & ((1u << lane) - 1u))] = w.cand[k];
+        if (c == 1 && ni + __popc(mi & below) < TREC) w.sidx[ni + __popc(mi & below)] = w.cand[k];
+        const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+        if (c == 2) {
+            akey[na + __popc(ma & below)] = (__float_as_uint((float)w.dc2[k]) & ~127u) | (unsigned)k;
+            acand[na + __popc(ma & below)] = w.cand[k];
+        }
         ni += __popc(mi);
-        na += __popc(__ballot_sync(0xffffffffu, c == 2));
+        na += __popc(ma);
     }
+    __syncwarp();
     const int ne = ni + na;
     if (ni > S || ne < S || ne > TREC) flags |= TFLAG_EXACT_SUPER;
     double best = 1e300;
     int bestk = 0x7fffffff;
     if (!(flags & TFLAG_EXACT_SUPER)) {
+        for (int e = lane; e < na; e += 32) {
+            const unsigned key = akey[e];
+            int r = 0;
+            for (int l = 0; l < na; ++l) r += akey[l] < key;
+            w.sidx[ni + r] = acand[e];
+        }
         for (int k = lane; k < nc; k += 32) {
             const int c = w.cls[k];
             const double dk = w.dc2[k];
-            if (c == 2) {
-                int r = 0;
-                for (int l = 0; l < nc; ++l)
-                    r += (w.cls[l] == 2) & ((w.dc2[l] < dk) | ((w.dc2[l] == dk) & (l < k)));
-                w.sidx[ni + r] = w.cand[k];
-            }
             if (c != 0 && (dk < best || (dk == best && k < bestk))) {
                 best = dk;
                 bestk = k;
@@ -653,6 +668,7 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
                     const float2 dk = w.wd[k];
                     const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
                     int cle = -1, clt = 0;  // l == k always counts in cle
+#pragma unroll 4
                     for (int l = 0; l < ne; ++l) {
                         const float2 dl = w.wd[l];
                         cle += dl.x <= hi;

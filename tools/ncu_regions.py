@@ -1,8 +1,10 @@
 """Instruction / stall shares of an ncu report per source region.
     python tools/ncu_regions.py <report> <kernel-regex> <file> <npx> marker1 marker2 ...
-Each marker is a substring of a line in <file>; regions run between markers."""
+Each marker is a substring of a line in <file> or a line number "L<n>";
+regions run between markers."""
 import csv
 import io
+import re
 import subprocess
 import sys
 
@@ -30,7 +32,10 @@ src = open(fname).read().splitlines()
 base = fname.split("/")[-1]
 pos = []
 for m in marks:
-    ln = next((i + 1 for i, l in enumerate(src) if m in l), None)
+    if re.fullmatch(r"L\d+", m):  # a line number
+        ln = int(m[1:])
+    else:
+        ln = next((i + 1 for i, l in enumerate(src) if m in l), None)
     pos.append((m[:24], ln))
 pos.append(("<end>", len(src) + 1))
 print(f"total {tot * 32 / npx:.1f} thread-inst/px")
