@@ -32,12 +32,16 @@ namespace nrm {
 namespace {
 
 #ifndef NRM_K1_CHUNK
-#define NRM_K1_CHUNK 64   // nodes per table chunk
+#define NRM_K1_CHUNK 64   // nodes per table chunk (multiple of 8)
 #endif
 #ifndef NRM_K1_MINB
-#define NRM_K1_MINB 3     // resident CTAs per SM (80 registers)
+#define NRM_K1_MINB 4     // resident CTAs per SM (64 registers)
 #endif
-constexpr int TW = 64, TH = 32, NT = 256, RPT = 8, CHUNK = NRM_K1_CHUNK;
+// Planning tiles are 64 x 32 px; a K1/K2 CTA takes one 32 x 32 half.
+constexpr int TW = 64, TH = 32, HW = 32, NT = 256, CHUNK = NRM_K1_CHUNK;
+static_assert(CHUNK % 8 == 0 && CHUNK <= 64, "k-steps of 8 nodes; one table thread per node");
+constexpr int KP = CHUNK + 4;  // [col][node] table pitch: conflict-free ldmatrix rows
+constexpr int EYP = 40;        // [node][row] table pitch: conflict-free B-fragment reads
 constexpr int NF_CAP = 512;           // listed nodes per tile plan (more: the tile goes to the exact pass)
 constexpr int NF_CHUNK_TILES = 2048;  // tile plans resident per launch chunk
 constexpr int NF_PLAN_WARPS = 8;      // planning warps (tiles) per CTA
@@ -67,16 +71,19 @@ struct __align__(16) NfPlan {
     NfEntry e[NF_CAP];
 };
 
+// Per-chunk tables. The Gaussian factorises, w = ex[col] * ey[row]; the
+// column factor is the MMA's A operand, split into TF32 hi + lo.
 struct Smem {
-    float ex[CHUNK][TW];
-    float ey[CHUNK][TH];
+    float exh[HW][KP], exl[HW][KP];  // column factor [col][node], hi / lo
+    float ey[CHUNK][EYP];            // row factor [node][row]
+    float4 qt[CHUNK][2];             // B columns per inner node: qw, qz, qdx, qdy, ds, 1, 0, 0
     NfEntry e[CHUNK];
 };
 
 // K1 only: the tile's canvas values, staged with cp.async at kernel entry.
 struct CanvasTile {
-    float r[TH][TW], g[TH][TW], b[TH][TW];
-    uint8_t w[TH][TW];
+    float r[TH][HW], g[TH][HW], b[TH][HW];
+    uint8_t w[TH][HW];
 };
 
 
@@ -354,35 +361,35 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
     pdl_wait();
-    const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x];
+    const int half = blockIdx.x & 1;  // this CTA's 32-column half of the planning tile
+    const NfPlan& pl = plans[blockIdx.y * ntx + (blockIdx.x >> 1)];
     const int status = pl.h.status;
     if (status == NF_OUTSIDE) return;
 
-    const int tix = tile_i0 + blockIdx.x;
+    const int tix = tile_i0 + (blockIdx.x >> 1);
     const int tjy = tile_row_of(by0 + blockIdx.y, tile_j0, s1, L.band_count);
-    const int ti0 = tix * TW, tj0 = tjy * TH;
-    const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
+    const int ti0 = tix * TW, tj0 = tjy * TH;  // planning tile origin
+    const int hi0 = ti0 + HW * half;           // first column of this half
+    const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + HW - 1, L.grid.i1);
     const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
+    if (ci0 > ci1) return;  // the half lies right of the grid
     const int count = pl.h.count;
 
-    // ---- 0. stage the canvas tile (whole 64 x 32 tile lies in the canvas:
-    //         tiles and canvas bounds are both 32/64-aligned, mosaic.hpp:141-151)
-    //         and the first chunk of the tile's plan
+    // ---- 0. stage the canvas half tile (the whole 64 x 32 tile lies in the
+    //         canvas: tiles and canvas bounds are both 32/64-aligned,
+    //         mosaic.hpp:141-151) and the first chunk of the tile's plan
     if (MODE != 1) {
-        const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (ti0 - L.phys_x0);
-        constexpr int kF = TW / 4;       // 16-byte chunks per float row
-        constexpr int kB = TW / 16;      // 16-byte chunks per byte row
-        constexpr int nF = 3 * TH * kF;  // 1536
-        for (int c = t; c < nF + TH * kB; c += NT) {
-            if (c < nF) {
-                const int plane = c / (TH * kF), rem = c % (TH * kF), r = rem / kF, k = rem % kF;
-                const float* src = (plane == 0 ? L.R : plane == 1 ? L.G : L.B) + base + (long long)r * L.pitch + 4 * k;
-                float* dst = (plane == 0 ? &ct.r[r][4 * k] : plane == 1 ? &ct.g[r][4 * k] : &ct.b[r][4 * k]);
-                cp_async16(dst, src);
-            } else {
-                const int rem = c - nF, r = rem / kB, k = rem % kB;
-                cp_async16(&ct.w[r][16 * k], L.W + base + (long long)r * L.pitch + 16 * k);
-            }
+        const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (hi0 - L.phys_x0);
+        {  // float planes: thread = (row r, 16-byte chunk k) for rows r and r + 16
+            const int k = t & 7, r = t >> 3;  // r < 32
+            const long long o = base + (long long)r * L.pitch + 4 * k;
+            cp_async16(&ct.r[r][4 * k], L.R + o);
+            cp_async16(&ct.g[r][4 * k], L.G + o);
+            cp_async16(&ct.b[r][4 * k], L.B + o);
+        }
+        if (t < 2 * TH) {  // weight plane: 2 chunks per row
+            const int k = t & 1, r = t >> 1;
+            cp_async16(&ct.w[r][16 * k], L.W + base + (long long)r * L.pitch + 16 * k);
         }
     }
     if (status == NF_OK) stage_entries(s.e, pl.e, min(CHUNK, count));
@@ -417,16 +424,30 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     const int ninner = pl.h.ninner;
 
     // ---- D. main loop over node chunks -----------------------------------
-    const int col = t & (TW - 1);
-    const int rg = t >> 6;  // 0..3, rows rg*8 .. rg*8+7
-    float a0[RPT], a1[RPT], a2[RPT], a3[RPT], a4[RPT], a5[RPT];
+    // Inner nodes run on the tensor cores. The sums are a product of two
+    // factored matrices: for component j (qw, qz, qdx, qdy, s - s0, 1),
+    //   D_j[col][row] = sum_k ex[k][col] * (ey[k][row] * q_k[j]),
+    // i.e. A = ex (32 cols x K nodes), B_j = ey * q_j (K x 32 rows). Warp w
+    // owns 16 columns x 8 rows: one m16 tile x 6 n8 tiles (one per
+    // component, the 8 rows on n), so every thread ends with all six sums of
+    // its 4 pixels. 3xTF32 split products keep ~2^-21 relative accuracy. Ring
+    // nodes (the 1e-6 cutoff crosses the tile) follow on the CUDA cores with
+    // the per-pixel cutoff test.
+    const int lane = t & 31, wid = t >> 5, g = lane >> 2, tig = lane & 3;
+    const int cw = 16 * (wid & 1), rw = 8 * (wid >> 1);  // within the half
+    float acc[6][4];  // [component][fragment f]: pixel (cw + 8 (f >> 1) + g, rw + 2 tig + (f & 1))
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) a0[j] = a1[j] = a2[j] = a3[j] = a4[j] = a5[j] = 0.f;
+    for (int j = 0; j < 6; ++j)
+#pragma unroll
+        for (int f = 0; f < 4; ++f) acc[j][f] = 0.f;
     unsigned amb = 0;
 
     const double nal = -alpha * kLog2e;
+    const double hx0 = ox + HW * half;  // x of the half's first column
     for (int c0 = 0; c0 < count; c0 += CHUNK) {
         const int cn = min(CHUNK, count - c0);
+        const int kin = min(max(ninner - c0, 0), cn);  // inner nodes of this chunk come first
+        const int cn8 = (cn + 7) & ~7;
         if (c0 > 0) {  // later chunks (tiles with more than CHUNK listed nodes)
             __syncthreads();
             stage_entries(s.e, pl.e + c0, cn);
@@ -434,64 +455,89 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
         }
         cp_async_wait_all();
         __syncthreads();
-        for (int e = t; e < cn * TW; e += NT) {
-            const int k = e / TW, c = e % TW;
-            const double dx = s.e[k].a.x - (ox + c);
-            s.ex[k][c] = ex2_approx((float)(nal * dx * dx));
+        // Tables; padding up to a multiple of 8 nodes is zero. Column factor:
+        // thread = (node, 8-column block), node fastest (conflict-free
+        // stores); along a row the FP64 exponent -a (ax - x)^2 advances by
+        // its exact second differences.
+        {
+            const int k = t & 63, cb = (t >> 6) * 8;
+            float* ph = &s.exh[cb][k];
+            float* pq = &s.exl[cb][k];
+            if (k < cn) {
+                const double d0 = s.e[k].a.x - (hx0 + cb);
+                double E = nal * d0 * d0, D = nal * (1.0 - 2.0 * d0);
+                const double D2 = 2.0 * nal;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float v = ex2_approx((float)E);
+                    const float hi = tf32_hi(v);
+                    ph[c * KP] = hi;
+                    pq[c * KP] = v - hi;
+                    E += D;
+                    D += D2;
+                }
+            } else if (k < cn8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) ph[c * KP] = pq[c * KP] = 0.f;
+            }
         }
-        for (int e = t; e < cn * TH; e += NT) {
-            const int k = e / TH, r = e % TH;
-            const double dy = s.e[k].a.y - (oy + r);
-            s.ey[k][r] = ex2_approx((float)(nal * dy * dy));
+        {  // row factor: thread = (row, every 8th node)
+            const int r = t & 31;
+            const double y = oy + r;
+            for (int k = t >> 5; k < cn8; k += 8) {
+                float v = 0.f;
+                if (k < cn) {
+                    const double dy = s.e[k].a.y - y;
+                    v = ex2_approx((float)(nal * dy * dy));
+                }
+                s.ey[k][r] = v;
+            }
+        }
+        for (int k = t; k < cn8; k += NT) {
+            const bool in = k < kin;  // ring nodes and padding: zero B columns
+            s.qt[k][0] = in ? s.e[k].q : make_float4(0.f, 0.f, 0.f, 0.f);
+            s.qt[k][1] = make_float4(in ? s.e[k].d : 0.f, in ? 1.f : 0.f, 0.f, 0.f);
         }
         __syncthreads();
 
-        // inner nodes first (the planner lists them before the ring nodes):
-        // no per-node branch, pointer-stepped shared-memory reads
-        const int kin = min(max(ninner - c0, 0), cn);
-        const float* pex = &s.ex[0][col];
-        const float4* pey = reinterpret_cast<const float4*>(&s.ey[0][rg * RPT]);
-        const NfEntry* pe = s.e;
-#pragma unroll 2
-        for (int k = 0; k < kin; ++k) {
-            const float4 q = pe->q;
-            const float dd = pe->d;
-            const float exv = *pex;
-            const float4 e0 = pey[0], e1 = pey[1];
-            pex += TW;
-            pey += TH / 4;
-            ++pe;
-            const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        for (int kb = 0; kb < kin; kb += 8) {
+            unsigned ah[4], al[4];
+            ldsm_x4(&s.exh[cw + (lane & 15)][kb + 4 * (lane >> 4)], ah);
+            ldsm_x4(&s.exl[cw + (lane & 15)][kb + 4 * (lane >> 4)], al);
+            const float ey0 = s.ey[kb + tig][rw + g], ey1 = s.ey[kb + tig + 4][rw + g];
+            const float* qa = &s.qt[kb + tig][0].x;
+            const float* qb = &s.qt[kb + tig + 4][0].x;
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) {
-                const float w = exv * ey[j];
-                a0[j] = fmaf(w, q.x, a0[j]);
-                a1[j] = fmaf(w, q.y, a1[j]);
-                a2[j] = fmaf(w, q.z, a2[j]);
-                a3[j] = fmaf(w, q.w, a3[j]);
-                a4[j] = fmaf(w, dd, a4[j]);
-                a5[j] += w;
+            for (int j = 0; j < 6; ++j) {
+                const float b0 = ey0 * qa[j], b1 = ey1 * qb[j];
+                const float b0h = tf32_hi(b0), b1h = tf32_hi(b1);
+                mma_tf32(acc[j], al, b0h, b1h);
+                mma_tf32(acc[j], ah, b0 - b0h, b1 - b1h);
+                mma_tf32(acc[j], ah, b0h, b1h);
             }
         }
         for (int k = kin; k < cn; ++k) {  // ring nodes: the 1e-6 cutoff per pixel
             const float4 q = s.e[k].q;
             const float dd = s.e[k].d;
-            const float exv = s.ex[k][col];
-            const float4 e0 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT]);
-            const float4 e1 = *reinterpret_cast<const float4*>(&s.ey[k][rg * RPT + 4]);
-            const float ey[RPT] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+            const float2 eyv = *reinterpret_cast<const float2*>(&s.ey[k][rw + 2 * tig]);
 #pragma unroll
-            for (int j = 0; j < RPT; ++j) {
-                float w = exv * ey[j];
-                const bool in = w > kCutHi;
-                amb |= (unsigned)((w >= kCutLo) && !in) << j;
-                w = in ? w : 0.f;
-                a0[j] = fmaf(w, q.x, a0[j]);
-                a1[j] = fmaf(w, q.y, a1[j]);
-                a2[j] = fmaf(w, q.z, a2[j]);
-                a3[j] = fmaf(w, q.w, a3[j]);
-                a4[j] = fmaf(w, dd, a4[j]);
-                a5[j] += w;
+            for (int hc = 0; hc < 2; ++hc) {
+                const int c = cw + 8 * hc + g;
+                const float exv = s.exh[c][k] + s.exl[c][k];
+#pragma unroll
+                for (int hr = 0; hr < 2; ++hr) {
+                    const int f = 2 * hc + hr;
+                    float w = exv * (hr ? eyv.y : eyv.x);
+                    const bool in = w > kCutHi;
+                    amb |= (unsigned)((w >= kCutLo) && !in) << f;
+                    w = in ? w : 0.f;
+                    acc[0][f] = fmaf(w, q.x, acc[0][f]);
+                    acc[1][f] = fmaf(w, q.y, acc[1][f]);
+                    acc[2][f] = fmaf(w, q.z, acc[2][f]);
+                    acc[3][f] = fmaf(w, q.w, acc[3][f]);
+                    acc[4][f] = fmaf(w, dd, acc[4][f]);
+                    acc[5][f] += w;
+                }
             }
         }
     }
@@ -508,17 +554,19 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     // K2: displacement base (Y0 - tile origin), exact small integer - grid offset
     const float bdx = (float)(Y00 - ox), bdy = (float)(Y01 - oy);
     int nb = 0, nns = 0, noof = 0;
-    const int i = ti0 + col;
 #pragma unroll
-    for (int j = 0; j < RPT; ++j) {
-        const int r = rg * RPT + j;
-        const int jj = tj0 + r;
+    for (int p = 0; p < 4; ++p) {
+        const int hcol = cw + 8 * (p >> 1) + g, r = rw + 2 * tig + (p & 1);  // within the half
+        const int col = HW * half + hcol;                                      // within the planning tile
+        const int i = ti0 + col, jj = tj0 + r;
+        const float s0v = acc[0][p], s1v = acc[1][p], s2v = acc[2][p];
+        const float s3v = acc[3][p], s4v = acc[4][p], s5v = acc[5][p];
         const bool valid = i >= ci0 && i <= ci1 && jj >= cj0 && jj <= cj1;
         bool exc = false;
         if (valid) {
-            if ((amb >> j) & 1u) {
+            if ((amb >> p) & 1u) {
                 exc = true;
-            } else if (a5[j] == 0.f) {
+            } else if (s5v == 0.f) {
                 ++nns;
                 if (MODE == 1) {
                     const size_t o = (size_t)(jj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
@@ -526,13 +574,13 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                     if (L.support) L.support[o] = 0;
                 }
             } else {
-                const float rn = rsqrtf(fmaf(a0[j], a0[j], a1[j] * a1[j]));
-                const float qw = a0[j] * rn, qz = a1[j] * rn, qdx = a2[j] * rn, qdy = a3[j] * rn;
+                const float rn = rsqrtf(fmaf(s0v, s0v, s1v * s1v));
+                const float qw = s0v * rn, qz = s1v * rn, qdx = s2v * rn, qdy = s3v * rn;
                 const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
                 const float ux = (float)col, uy = (float)r;
                 const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
                 const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
-                const float dl = __fdividef(a4[j], a5[j]);  // a5 > 0, far from 2^126
+                const float dl = __fdividef(s4v, s5v);  // s5 > 0, far from 2^126
                 const float sbf = s0f + dl;
                 const float rx = fmaf(sbf, Qx, fmaf(dl, P0f, e00f));
                 const float ry = fmaf(sbf, Qy, fmaf(dl, P1f, e01f));
@@ -562,7 +610,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                         const float vr = (gx * va[0] + fx * vb[0]) * gy + (gx * vc[0] + fx * vd[0]) * fy;
                         const float vg = (gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy;
                         const float vbl = (gx * va[2] + fx * vb[2]) * gy + (gx * vc[2] + fx * vd[2]) * fy;
-                        const uint8_t wg = ct.w[r][col];
+                        const uint8_t wg = ct.w[r][hcol];
                         const float wd = (float)wg, inv = __fdividef(1.f, wd + 1.f);
                         constexpr float k255 = 1.f / 255.f;
                         const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
@@ -578,9 +626,9 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                         }
                         // explicit FMAs: the same instructions in both modes, so
                         // cf == 1 reproduces the reference rule bit for bit
-                        L.R[idx] = fmaf(a, ct.r[r][col], cf * (vr * k255)) * inv;
-                        L.G[idx] = fmaf(a, ct.g[r][col], cf * (vg * k255)) * inv;
-                        L.B[idx] = fmaf(a, ct.b[r][col], cf * (vbl * k255)) * inv;
+                        L.R[idx] = fmaf(a, ct.r[r][hcol], cf * (vr * k255)) * inv;
+                        L.G[idx] = fmaf(a, ct.g[r][hcol], cf * (vg * k255)) * inv;
+                        L.B[idx] = fmaf(a, ct.b[r][hcol], cf * (vbl * k255)) * inv;
                         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
                         ++nb;
                     }
@@ -959,7 +1007,7 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         ++*launches;
         if (e != cudaSuccess) return e;
         prof_mark("k_node_field", st);
-        e = launch_pdl(k_field, dim3(g.ntx, rows), dim3(NT), smem, st, L,
+        e = launch_pdl(k_field, dim3(2 * g.ntx, rows), dim3(NT), smem, st, L,
                                          static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx);
         ++*launches;
         if (e != cudaSuccess) return e;

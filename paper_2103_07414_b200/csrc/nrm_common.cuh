@@ -223,6 +223,31 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// ---- tensor cores (3xTF32 split products) ---------------------------------
+// x = hi + lo with hi = x rounded to TF32 (low 13 bits zero) and lo = x - hi
+// exact in FP32; the MMA reads lo's top 19 bits. hi*hi + hi*lo + lo*hi keeps
+// ~2^-21 relative per product with FP32 accumulation.
+__device__ __forceinline__ float tf32_hi(float x) {
+    unsigned r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// Four 8 x 4 TF32 matrices (an m16n8k8 A fragment) from shared memory: lane l
+// supplies the address of row (l & 7) of matrix (l >> 3).
+__device__ __forceinline__ void ldsm_x4(const void* smem, unsigned (&r)[4]) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a)
+                 : "memory");
+}
+// d += a * b, m16n8k8, TF32 inputs, FP32 accumulators.
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], float b0, float b1) {
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b0)), "r"(__float_as_uint(b1)));
+}
+
 // floor division for possibly negative ints
 __host__ __device__ __forceinline__ int floordiv(int a, int b) {
     const int q = a / b;

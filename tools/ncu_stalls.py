@@ -1,7 +1,9 @@
 """Stall reasons per source region from an ncu report (source page, SASS
-correlated): python tools/ncu_stalls.py <rep> <kernel-regex> <file> marker1 ..."""
+correlated): python tools/ncu_stalls.py <rep> <kernel-regex> <file> marker1 ...
+A marker is a substring of a source line or a line number "L<n>"."""
 import csv
 import io
+import re
 import subprocess
 import sys
 
@@ -10,7 +12,7 @@ marks = sys.argv[4:]
 src = open(fname).read().splitlines()
 starts = []
 for m in marks:
-    ln = next(i + 1 for i, l in enumerate(src) if m in l)
+    ln = int(m[1:]) if re.fullmatch(r"L\d+", m) else next(i + 1 for i, l in enumerate(src) if m in l)
     starts.append((ln, m))
 starts.sort()
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source",
