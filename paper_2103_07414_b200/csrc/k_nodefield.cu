@@ -35,10 +35,22 @@ namespace {
 #define NRM_K1_CHUNK 64   // nodes per table chunk (multiple of 8)
 #endif
 #ifndef NRM_K1_MINB
-#define NRM_K1_MINB 4     // resident CTAs per SM (64 registers)
+#define NRM_K1_MINB 4     // K1: resident CTAs per SM (64 registers)
 #endif
-// Planning tiles are 64 x 32 px; a K1/K2 CTA takes one 32 x 32 half.
+#ifndef NRM_K2_MINB
+#define NRM_K2_MINB 2     // K2: resident CTAs per SM (128 registers: 6.08 ms vs 6.38 at 3 CTAs, 16384^2 C4 field)
+#endif
+// Planning tiles are 64 x 32 px. A K1 CTA takes one 32 x 32 half (one m16
+// tile per warp, 64 registers, 4 CTAs/SM); a K2 CTA takes the whole tile (two
+// m16 tiles per warp, 128 registers, 2 CTAs/SM), which pays off there because
+// its canvas-wide lattices list ~80 nodes per tile.
 constexpr int TW = 64, TH = 32, HW = 32, NT = 256, CHUNK = NRM_K1_CHUNK;
+template <int MODE> struct K1Shape {
+    static constexpr int MT = MODE == 1 ? 2 : 1;  // m16 tiles per warp
+    static constexpr int CW = 32 * MT;            // CTA columns
+    static constexpr int NH = TW / CW;            // CTAs per planning tile
+    static constexpr int MINB = MODE == 1 ? NRM_K2_MINB : NRM_K1_MINB;
+};
 static_assert(CHUNK % 8 == 0 && CHUNK <= 64, "k-steps of 8 nodes; one table thread per node");
 constexpr int KP = CHUNK + 4;  // [col][node] table pitch: conflict-free ldmatrix rows
 constexpr int EYP = 40;        // [node][row] table pitch: conflict-free B-fragment reads
@@ -73,8 +85,9 @@ struct __align__(16) NfPlan {
 
 // Per-chunk tables. The Gaussian factorises, w = ex[col] * ey[row]; the
 // column factor is the MMA's A operand, split into TF32 hi + lo.
+template <int CW>
 struct Smem {
-    float exh[HW][KP], exl[HW][KP];  // column factor [col][node], hi / lo
+    float exh[CW][KP], exl[CW][KP];  // column factor [col][node], hi / lo
     float ey[CHUNK][EYP];            // row factor [node][row]
     float4 qt[CHUNK][2];             // B columns per inner node: qw, qz, qdx, qdy, ds, 1, 0, 0
     NfEntry e[CHUNK];
@@ -353,26 +366,27 @@ __device__ __forceinline__ void stage_entries(NfEntry* dst, const NfEntry* src, 
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(NT, NRM_K1_MINB)
+__global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
 k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
              int ntx) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem& s = *reinterpret_cast<Smem*>(smem_raw);
-    CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem) + 15) & ~size_t(15)));
+    constexpr int MT = K1Shape<MODE>::MT, CW = K1Shape<MODE>::CW, NH = K1Shape<MODE>::NH;
+    Smem<CW>& s = *reinterpret_cast<Smem<CW>*>(smem_raw);
+    CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem<CW>) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
     pdl_wait();
-    const int half = blockIdx.x & 1;  // this CTA's 32-column half of the planning tile
-    const NfPlan& pl = plans[blockIdx.y * ntx + (blockIdx.x >> 1)];
+    const int half = blockIdx.x % NH;  // this CTA's column slice of the planning tile
+    const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x / NH];
     const int status = pl.h.status;
     if (status == NF_OUTSIDE) return;
 
-    const int tix = tile_i0 + (blockIdx.x >> 1);
+    const int tix = tile_i0 + blockIdx.x / NH;
     const int tjy = tile_row_of(by0 + blockIdx.y, tile_j0, s1, L.band_count);
     const int ti0 = tix * TW, tj0 = tjy * TH;  // planning tile origin
-    const int hi0 = ti0 + HW * half;           // first column of this half
-    const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + HW - 1, L.grid.i1);
+    const int hi0 = ti0 + CW * half;           // first column of this slice
+    const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + CW - 1, L.grid.i1);
     const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
-    if (ci0 > ci1) return;  // the half lies right of the grid
+    if (ci0 > ci1) return;  // the slice lies right of the grid
     const int count = pl.h.count;
 
     // ---- 0. stage the canvas half tile (the whole 64 x 32 tile lies in the
@@ -434,16 +448,18 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     // nodes (the 1e-6 cutoff crosses the tile) follow on the CUDA cores with
     // the per-pixel cutoff test.
     const int lane = t & 31, wid = t >> 5, g = lane >> 2, tig = lane & 3;
-    const int cw = 16 * (wid & 1), rw = 8 * (wid >> 1);  // within the half
-    float acc[6][4];  // [component][fragment f]: pixel (cw + 8 (f >> 1) + g, rw + 2 tig + (f & 1))
+    const int cw = 16 * MT * (wid & 1), rw = 8 * (wid >> 1);  // within the slice
+    float acc[MT][6][4];  // [m tile][component][fragment f]: pixel (cw + 16 mt + 8 (f >> 1) + g, rw + 2 tig + (f & 1))
 #pragma unroll
-    for (int j = 0; j < 6; ++j)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int f = 0; f < 4; ++f) acc[j][f] = 0.f;
+        for (int j = 0; j < 6; ++j)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) acc[mt][j][f] = 0.f;
     unsigned amb = 0;
 
     const double nal = -alpha * kLog2e;
-    const double hx0 = ox + HW * half;  // x of the half's first column
+    const double hx0 = ox + CW * half;  // x of the slice's first column
     for (int c0 = 0; c0 < count; c0 += CHUNK) {
         const int cn = min(CHUNK, count - c0);
         const int kin = min(max(ninner - c0, 0), cn);  // inner nodes of this chunk come first
@@ -460,15 +476,16 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
         // stores); along a row the FP64 exponent -a (ax - x)^2 advances by
         // its exact second differences.
         {
-            const int k = t & 63, cb = (t >> 6) * 8;
+            constexpr int CB = CW / 4;  // columns per thread
+            const int k = t & 63, cb = (t >> 6) * CB;
             float* ph = &s.exh[cb][k];
             float* pq = &s.exl[cb][k];
             if (k < cn) {
                 const double d0 = s.e[k].a.x - (hx0 + cb);
                 double E = nal * d0 * d0, D = nal * (1.0 - 2.0 * d0);
                 const double D2 = 2.0 * nal;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
+#pragma unroll 8
+                for (int c = 0; c < CB; ++c) {
                     const float v = ex2_approx((float)E);
                     const float hi = tf32_hi(v);
                     ph[c * KP] = hi;
@@ -477,8 +494,8 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
                     D += D2;
                 }
             } else if (k < cn8) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) ph[c * KP] = pq[c * KP] = 0.f;
+#pragma unroll 8
+                for (int c = 0; c < CB; ++c) ph[c * KP] = pq[c * KP] = 0.f;
             }
         }
         {  // row factor: thread = (row, every 8th node)
@@ -501,9 +518,12 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
         __syncthreads();
 
         for (int kb = 0; kb < kin; kb += 8) {
-            unsigned ah[4], al[4];
-            ldsm_x4(&s.exh[cw + (lane & 15)][kb + 4 * (lane >> 4)], ah);
-            ldsm_x4(&s.exl[cw + (lane & 15)][kb + 4 * (lane >> 4)], al);
+            unsigned ah[MT][4], al[MT][4];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                ldsm_x4(&s.exh[cw + 16 * mt + (lane & 15)][kb + 4 * (lane >> 4)], ah[mt]);
+                ldsm_x4(&s.exl[cw + 16 * mt + (lane & 15)][kb + 4 * (lane >> 4)], al[mt]);
+            }
             const float ey0 = s.ey[kb + tig][rw + g], ey1 = s.ey[kb + tig + 4][rw + g];
             const float* qa = &s.qt[kb + tig][0].x;
             const float* qb = &s.qt[kb + tig + 4][0].x;
@@ -511,9 +531,12 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
             for (int j = 0; j < 6; ++j) {
                 const float b0 = ey0 * qa[j], b1 = ey1 * qb[j];
                 const float b0h = tf32_hi(b0), b1h = tf32_hi(b1);
-                mma_tf32(acc[j], al, b0h, b1h);
-                mma_tf32(acc[j], ah, b0 - b0h, b1 - b1h);
-                mma_tf32(acc[j], ah, b0h, b1h);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    mma_tf32(acc[mt][j], al[mt], b0h, b1h);
+                    mma_tf32(acc[mt][j], ah[mt], b0 - b0h, b1 - b1h);
+                    mma_tf32(acc[mt][j], ah[mt], b0h, b1h);
+                }
             }
         }
         for (int k = kin; k < cn; ++k) {  // ring nodes: the 1e-6 cutoff per pixel
@@ -521,22 +544,25 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
             const float dd = s.e[k].d;
             const float2 eyv = *reinterpret_cast<const float2*>(&s.ey[k][rw + 2 * tig]);
 #pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                const int c = cw + 8 * hc + g;
-                const float exv = s.exh[c][k] + s.exl[c][k];
+            for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-                for (int hr = 0; hr < 2; ++hr) {
-                    const int f = 2 * hc + hr;
-                    float w = exv * (hr ? eyv.y : eyv.x);
-                    const bool in = w > kCutHi;
-                    amb |= (unsigned)((w >= kCutLo) && !in) << f;
-                    w = in ? w : 0.f;
-                    acc[0][f] = fmaf(w, q.x, acc[0][f]);
-                    acc[1][f] = fmaf(w, q.y, acc[1][f]);
-                    acc[2][f] = fmaf(w, q.z, acc[2][f]);
-                    acc[3][f] = fmaf(w, q.w, acc[3][f]);
-                    acc[4][f] = fmaf(w, dd, acc[4][f]);
-                    acc[5][f] += w;
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int c = cw + 16 * mt + 8 * hc + g;
+                    const float exv = s.exh[c][k] + s.exl[c][k];
+#pragma unroll
+                    for (int hr = 0; hr < 2; ++hr) {
+                        const int f = 2 * hc + hr;
+                        float w = exv * (hr ? eyv.y : eyv.x);
+                        const bool in = w > kCutHi;
+                        amb |= (unsigned)((w >= kCutLo) && !in) << (4 * mt + f);
+                        w = in ? w : 0.f;
+                        acc[mt][0][f] = fmaf(w, q.x, acc[mt][0][f]);
+                        acc[mt][1][f] = fmaf(w, q.y, acc[mt][1][f]);
+                        acc[mt][2][f] = fmaf(w, q.z, acc[mt][2][f]);
+                        acc[mt][3][f] = fmaf(w, q.w, acc[mt][3][f]);
+                        acc[mt][4][f] = fmaf(w, dd, acc[mt][4][f]);
+                        acc[mt][5][f] += w;
+                    }
                 }
             }
         }
@@ -555,12 +581,13 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     const float bdx = (float)(Y00 - ox), bdy = (float)(Y01 - oy);
     int nb = 0, nns = 0, noof = 0;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const int hcol = cw + 8 * (p >> 1) + g, r = rw + 2 * tig + (p & 1);  // within the half
-        const int col = HW * half + hcol;                                      // within the planning tile
+    for (int p = 0; p < 4 * MT; ++p) {
+        const int mt = p >> 2, f = p & 3;
+        const int hcol = cw + 16 * mt + 8 * (f >> 1) + g, r = rw + 2 * tig + (f & 1);  // within the slice
+        const int col = CW * half + hcol;                                                // within the planning tile
         const int i = ti0 + col, jj = tj0 + r;
-        const float s0v = acc[0][p], s1v = acc[1][p], s2v = acc[2][p];
-        const float s3v = acc[3][p], s4v = acc[4][p], s5v = acc[5][p];
+        const float s0v = acc[mt][0][f], s1v = acc[mt][1][f], s2v = acc[mt][2][f];
+        const float s3v = acc[mt][3][f], s4v = acc[mt][4][f], s5v = acc[mt][5][f];
         const bool valid = i >= ci0 && i <= ci1 && jj >= cj0 && jj <= cj1;
         bool exc = false;
         if (valid) {
@@ -985,8 +1012,9 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         L.lists = reinterpret_cast<int*>(reinterpret_cast<char*>(L.plans) + (size_t)NF_CHUNK_TILES * sizeof(NfPlan));
         L.lcounts = L.lists + (size_t)g.nchunks * L.col_groups * L.lstride;
     }
-    const size_t base = (sizeof(Smem) + 15) & ~size_t(15);
-    const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : sizeof(Smem);
+    const size_t base = (sizeof(Smem<K1Shape<0>::CW>) + 15) & ~size_t(15);
+    const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : sizeof(Smem<K1Shape<1>::CW>);
+    const int nh = mode == 1 ? K1Shape<1>::NH : K1Shape<0>::NH;
     const int kmode = mode == 1 ? 1 : (L.unc ? 2 : 0);  // 2: uncertainty-weighted blend
     auto k_field = kmode == 0 ? k_node_field<0> : (kmode == 1 ? k_node_field<1> : k_node_field<2>);
     auto k_exc = kmode == 0 ? k_node_exceptions<0> : (kmode == 1 ? k_node_exceptions<1> : k_node_exceptions<2>);
@@ -1007,7 +1035,7 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         ++*launches;
         if (e != cudaSuccess) return e;
         prof_mark("k_node_field", st);
-        e = launch_pdl(k_field, dim3(2 * g.ntx, rows), dim3(NT), smem, st, L,
+        e = launch_pdl(k_field, dim3(nh * g.ntx, rows), dim3(NT), smem, st, L,
                                          static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx);
         ++*launches;
         if (e != cudaSuccess) return e;
