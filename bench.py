@@ -657,7 +657,9 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
             "kernels_ms": {k: v[0] for k, v in kt.items()},
             "roofline_k_node_field": {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
                                       "frac": ach / fp32_peak,
-                                      "algorithmic": f"{n * n} px x {per_px:.1f} contributing nodes x 18 flops"}}
+                                      "algorithmic": f"{n * n} px x {per_px:.1f} contributing nodes x 18 flops",
+                                      "note": "the inner-node sums run on the tensor cores (3xTF32 mma.sync); "
+                                              "this is the reference loop's FP32 work against the FP32 peak"}}
 
 
 def em_estep_numbers(ctx, with_cpu: bool):
