@@ -251,6 +251,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
     ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
     ap.add_argument("--no-canvas-field", action="store_true", help="skip the canvas-wide field side measurement")
+    ap.add_argument("--no-features", action="store_true", help="skip the feature detection / matching side measurement")
     ap.add_argument("--e2e-inflight", type=int, default=2,
                     help="EMDQ field calls in flight in the e2e loop (own context + pinned outputs each)")
     args = ap.parse_args()
@@ -582,6 +583,9 @@ def main():
     canvas_field = None
     if rank == 0 and not args.no_canvas_field:
         canvas_field = canvas_field_numbers(ctx, stream, fp32_peak=2.0 * ctx.peak("fp32") / 1e12)
+    feats = None
+    if rank == 0 and not args.no_features:
+        feats = features_numbers(ctx, stream, with_cpu=world == 1 and not args.no_cpu_baseline)
 
     if rank == 0:
         line = {
@@ -599,6 +603,7 @@ def main():
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "roofline": roof, "cpu_baseline": cpu,
             "em_estep": estep,
             "canvas_field": canvas_field,
+            "features": feats,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -611,7 +616,8 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
     """Side measurement (BASELINE configs[3]: the canvas-wide field of a
     16384^2 canvas with its canvas-covering 1,497-node lattice, K2 =
     k_node_field<1>): one pass, device-timed, with the roofline of the same
-    FP32 main loop the blend uses, here without the canvas epilogue.
+    accumulation the blend uses (tensor cores), here without the canvas
+    epilogue.
     Algorithmic work: contributing (pixel, node) pairs x 18 flops, counted
     with the reference's cutoff on a seeded pixel sample."""
     import torch
@@ -700,6 +706,87 @@ def em_estep_numbers(ctx, with_cpu: bool):
                 r["cpu_reference"] = {"unavailable": repr(ex)}
         out.append(r)
     return out
+
+
+def features_numbers(ctx, stream, with_cpu: bool):
+    """SURVEY §8f NEXT #4, reported beside the headline: the sparse front end
+    of one 1080p frame as the reference's callers run it (main.cpp:198-202):
+    to_gray + detect_features on the new frame, then match_features against
+    the previous frame's 800 keypoints. Device-resident (CUDA events on the
+    context stream, inputs in HBM) and through the host API (the frame and
+    features copied in and out), against the reference itself (oracle/_ref)
+    on the host cores; bit-exactness is checked on the same frames."""
+    import torch
+    from paper_2103_07414_b200 import mosaic as M
+    from paper_2103_07414_b200 import workload as W
+    wl = W.frame_workload("c2")
+    a = wl.frame
+    b = np.roll(a, (7, -12), axis=(0, 1))
+    fh, fw, ch = b.shape
+    ka, da = M.detect_features(a, ctx=ctx)
+    kb, db = M.detect_features(b, ctx=ctx)
+    m = M.match_features(ka, da, kb, db, 0.8, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    ib = torch.from_numpy(np.ascontiguousarray(b)).to(dev)
+    kp_a, ds_a = torch.from_numpy(ka).to(dev), torch.from_numpy(da).to(dev)
+    kp_b = torch.zeros((800, 3), dtype=torch.float64, device=dev)
+    ds_b = torch.zeros((800, 64), dtype=torch.float32, device=dev)
+    nb_t = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = torch.zeros((len(ka), 5), dtype=torch.float64, device=dev)
+    nm = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step():
+        M.detect_features_device(ib, fw, fh, ch, kp_b, ds_b, nb_t, ctx=ctx)
+        M.match_features_device(kp_a, ds_a, len(ka), kp_b, ds_b, len(kb), 0.8, out, nm, ctx=ctx)
+
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / reps
+    ctx.profile(True)
+    step()
+    torch.cuda.synchronize()
+    kt = {k: round(v[0], 4) for k, v in ctx.kernel_times().items()}
+    ctx.profile(False)
+    ok_dev = bool(np.array_equal(out[:int(nm.item())].cpu().numpy(), m))
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        k2, d2 = M.detect_features(b, ctx=ctx)
+        M.match_features(ka, da, k2, d2, 0.8, ctx=ctx)
+        ts.append(time.perf_counter() - t0)
+    r = {"workload": "1080p RGB frame (C2 scene): to_gray + detect_features + match_features against the "
+                     "previous frame's keypoints (main.cpp:198-202)",
+         "keypoints": int(len(kb)), "matches": int(len(m)), "device_ms": dev_ms, "device_frames_per_s": 1e3 / dev_ms,
+         "host_api_ms": min(ts) * 1e3, "host_api_frames_per_s": 1.0 / min(ts), "kernels_ms": kt,
+         "device_path_equals_host_path": ok_dev}
+    if with_cpu:
+        try:
+            from oracle.oracle import Reference
+            R = Reference()
+            rk, rd = R.detect_features(R.to_gray(b))
+            ra, rda = R.detect_features(R.to_gray(a))
+            r["bit_exact_vs_reference"] = bool(np.array_equal(rk, kb) and np.array_equal(rd, db) and
+                                               np.array_equal(ra, ka) and
+                                               np.array_equal(R.match_features(ra, rda, rk, rd, 0.8), m))
+            ncpu = os.cpu_count() or 1
+            best = None
+            for wk in (1, ncpu):
+                dt = min(R.time_detect_match(b, ka, da, workers=wk)[0] for _ in range(3))
+                if best is None or dt < best[0]:
+                    best = (dt, wk)
+            r["cpu_reference"] = {"ms": best[0] * 1e3, "frames_per_s": 1.0 / best[0], "cores": best[1],
+                                  "sample": f"whole frame, best of 3, best of workers in (1, {ncpu})"}
+        except Exception as ex:  # noqa: BLE001  (reported, never required)
+            r["cpu_reference"] = {"unavailable": repr(ex)}
+    return r
 
 
 def wl_contributors(wl, poly, sample: int = 20000):

@@ -229,6 +229,47 @@ int nrm_emdq_points_device(nrm_ctx *ctx, const double *d_q, const int32_t *d_exc
                            int support, double beta, double *d_warps, double *d_pred,
                            double *d_unc, int32_t *d_status);
 
+/* ---- sparse front end -------------------------------
+ * Corner detection and ratio-test matching before the EM, bit-identical to
+ * the reference (features.hpp). */
+/* DetectorConfig (features.hpp:30-36); `workers` has no meaning here. */
+typedef struct nrm_detector_config {
+    int max_features;      /* 800 */
+    double quality_level;  /* 0.005: fraction of the maximum corner response */
+    int nms_radius;        /* 4 */
+    double ratio_test;     /* 0.8: used by nrm_match_features callers */
+} nrm_detector_config;
+
+/* detect_features(to_gray(image), cfg) (features.hpp:140-205,
+ * image.hpp:63-75). Keypoints in the reference's order (response desc, y, x),
+ * at most cfg->max_features: kp = double[n][3] (x, y, response), desc =
+ * float[n][64] (FrameFeatures::descriptors). Both arrays must hold
+ * cfg->max_features rows; *n receives the count. An image smaller than
+ * 2 * 10 + 1 px in either direction, or without a positive response, gives 0
+ * keypoints, as in the reference. */
+int nrm_detect_features(nrm_ctx *ctx, const uint8_t *image, int w, int h, int ch,
+                        const nrm_detector_config *cfg, double *kp, float *desc, int *n);
+/* The same on an FP32 gray image (ImageF, detect_features' own input). */
+int nrm_detect_features_gray(nrm_ctx *ctx, const float *gray, int w, int h,
+                             const nrm_detector_config *cfg, double *kp, float *desc, int *n);
+/* Device pointers; d_n is a device int. Enqueued on the context stream;
+ * returns without synchronising. */
+int nrm_detect_features_device(nrm_ctx *ctx, const uint8_t *d_image, int w, int h, int ch,
+                               const nrm_detector_config *cfg, double *d_kp, float *d_desc,
+                               int *d_n);
+
+/* match_features(a, b, ratio) (features.hpp:208-254): for every keypoint of
+ * a (in order) whose nearest descriptor in b passes the ratio test, one row
+ * (ax, ay, bx, by, score) of `out` (double[na][5]); *n receives the count.
+ * nb < 2 or na == 0 gives no matches. kp_* use the nrm_detect_features
+ * layout (x, y, response). */
+int nrm_match_features(nrm_ctx *ctx, const double *kp_a, const float *desc_a, int na,
+                       const double *kp_b, const float *desc_b, int nb, double ratio,
+                       double *out, int *n);
+int nrm_match_features_device(nrm_ctx *ctx, const double *d_kp_a, const float *d_desc_a, int na,
+                              const double *d_kp_b, const float *d_desc_b, int nb,
+                              double ratio, double *d_out, int *d_n);
+
 /* ---- kernel timing -------------------------------------------------------
  * With profiling on, a CUDA event is recorded on the context stream before
  * every kernel and at the end of every compute call; a kernel's time is the

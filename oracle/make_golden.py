@@ -203,9 +203,47 @@ def estep_cases():
     print("emdq_estep: c2 empty", int(emp.sum()))
 
 
+def features_cases():
+    """The sparse front end (features.hpp) through the
+    reference's own to_gray / detect_features / match_features, on the
+    fixtures of its detector tests (test_features.cpp:14-127): the smoothed
+    random texture, its wrap-around translation, pure noise, a tiny image,
+    and an RGB frame of the synthetic scene."""
+    R = Reference()
+    out = {}
+
+    def case(name, a, b, ratios=(0.8,)):
+        ga, gb = R.to_gray(a), R.to_gray(b)
+        ka, da = R.detect_features(ga)
+        kb, db = R.detect_features(gb)
+        out.update({f"{name}_a": a, f"{name}_b": b, f"{name}_ga_sha": sha(ga), f"{name}_gb_sha": sha(gb), f"{name}_kpa": ka,
+                    f"{name}_da": da, f"{name}_kpb": kb, f"{name}_db": db})
+        for r in ratios:
+            out[f"{name}_m{int(round(100 * r))}"] = R.match_features(ka, da, kb, db, r)
+        print(f"features {name}: {len(ka)} / {len(kb)} keypoints, "
+              f"{len(out[f'{name}_m{int(round(100 * ratios[0]))}'])} matches")
+
+    tex = R.textured_image(240, 160, 42)
+    case("self", tex, tex)                                   # SelfMatchHasZeroDisplacement
+    a = R.textured_image(320, 200, 7)
+    case("translate", a, np.roll(a, 10, axis=1), (0.8, 0.6, 0.95))  # RecoversPureTranslation, ratio monotone
+    rng = np.random.default_rng(1)
+    case("noise", rng.integers(0, 256, (150, 200), dtype=np.uint8),
+         rng.integers(0, 256, (150, 200), dtype=np.uint8))   # PureNoiseProducesFewMatches
+    t = R.textured_image(12, 12, 3)
+    case("tiny", t, t)                                       # TinyImageYieldsEmptyList
+    f0 = R.scene_frame(320, 240, 10, 7, 6, 15.0, 80.0, 40.0, 0)
+    f1 = R.scene_frame(320, 240, 10, 7, 6, 15.0, 80.0, 40.0, 1)
+    case("scene_rgb", f0, f1)
+    np.savez_compressed(OUT / "features.npz", **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["estep"]:
         estep_cases()
+    elif sys.argv[1:] == ["features"]:
+        features_cases()
     else:
         main()
         estep_cases()
+        features_cases()

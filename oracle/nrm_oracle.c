@@ -617,3 +617,187 @@ int orc_emdq_field_grid(double x0, double y0, int w, int h, const double *apts,
     free(pts);
     return rc;
 }
+
+/* ==========================================================================
+ * Sparse front end (features.hpp). FP32 arithmetic in the
+ * reference's order; this file is built with -ffp-contract=off, so every
+ * float operation rounds separately, like the reference's SSE code.
+ * ========================================================================== */
+
+/* to_gray (image.hpp:63-75) */
+void orc_to_gray(const uint8_t *im, int w, int h, int ch, float *out) {
+    const size_t n = (size_t)w * (size_t)h;
+    for (size_t i = 0; i < n; ++i) {
+        if (ch == 1) {
+            out[i] = im[i] * (1.f / 255.f);
+        } else {
+            const uint8_t *p = im + i * (size_t)ch;
+            out[i] = (0.299f * p[0] + 0.587f * p[1] + 0.114f * p[2]) * (1.f / 255.f);
+        }
+    }
+}
+
+typedef struct orc_kp {
+    double x, y, resp;
+    int idx; /* raster order of detection (stable-sort tie-break) */
+} orc_kp;
+
+static int orc_kp_cmp(const void *pa, const void *pb) {
+    const orc_kp *a = (const orc_kp *)pa, *b = (const orc_kp *)pb;
+    /* features.hpp:186-191: response desc, y asc, x asc; stable */
+    if (a->resp != b->resp) return a->resp > b->resp ? -1 : 1;
+    if (a->y != b->y) return a->y < b->y ? -1 : 1;
+    if (a->x != b->x) return a->x < b->x ? -1 : 1;
+    return (a->idx > b->idx) - (a->idx < b->idx);
+}
+
+/* subpixel_offset (features.hpp:103-108) */
+static double orc_subpixel_offset(float rm, float r0, float rp) {
+    const double denom = (double)rm - 2.0 * r0 + rp;
+    if (fabs(denom) < 1e-20) return 0.0;
+    const double off = 0.5 * ((double)rm - rp) / denom;
+    return off < -0.5 ? -0.5 : (off > 0.5 ? 0.5 : off);
+}
+
+/* corner_response (features.hpp:58-101) + detect_features (140-205) */
+int orc_detect_features(const float *gray, int w, int h, int max_features, double quality,
+                        int r, double *kp, float *desc) {
+    const int margin = 8 + 2; /* kPatchRadius + 2 (features.hpp:54-55) */
+    if (w < 2 * margin + 1 || h < 2 * margin + 1) return 0;
+    const size_t n = (size_t)w * (size_t)h;
+    float *ix = (float *)calloc(n, sizeof(float)), *iy = (float *)calloc(n, sizeof(float));
+    float *resp = (float *)calloc(n, sizeof(float));
+    if (!ix || !iy || !resp) {
+        free(ix), free(iy), free(resp);
+        return -1;
+    }
+#define G(x, y) gray[(size_t)(y) * w + (x)]
+    for (int y = 1; y + 1 < h; ++y)
+        for (int x = 1; x + 1 < w; ++x) {
+            ix[(size_t)y * w + x] = (G(x + 1, y - 1) - G(x - 1, y - 1)) + 2.f * (G(x + 1, y) - G(x - 1, y)) +
+                                    (G(x + 1, y + 1) - G(x - 1, y + 1));
+            iy[(size_t)y * w + x] = (G(x - 1, y + 1) - G(x - 1, y - 1)) + 2.f * (G(x, y + 1) - G(x, y - 1)) +
+                                    (G(x + 1, y + 1) - G(x + 1, y - 1));
+        }
+#undef G
+    for (int y = 3; y < h - 3; ++y)
+        for (int x = 3; x < w - 3; ++x) {
+            float sxx = 0.f, syy = 0.f, sxy = 0.f;
+            for (int dy = -2; dy <= 2; ++dy)
+                for (int dx = -2; dx <= 2; ++dx) {
+                    const float gx = ix[(size_t)(y + dy) * w + x + dx], gy = iy[(size_t)(y + dy) * w + x + dx];
+                    sxx += gx * gx;
+                    syy += gy * gy;
+                    sxy += gx * gy;
+                }
+            const float tr = 0.5f * (sxx + syy);
+            const float q = 0.25f * (sxx - syy) * (sxx - syy) + sxy * sxy;
+            const float det = sqrtf(q > 0.f ? q : 0.f);
+            resp[(size_t)y * w + x] = tr - det;
+        }
+    float max_resp = 0.f;
+    for (size_t i = 0; i < n; ++i)
+        if (resp[i] > max_resp) max_resp = resp[i];
+    const float threshold = (float)quality * max_resp;
+    int count = 0, cap = 1024;
+    orc_kp *list = (orc_kp *)malloc((size_t)cap * sizeof(orc_kp));
+    if (max_resp > 0.f && list) {
+        for (int y = margin; y < h - margin; ++y)
+            for (int x = margin; x < w - margin; ++x) {
+                const float v = resp[(size_t)y * w + x];
+                if (v <= threshold) continue;
+                int is_max = 1;
+                for (int dy = -r; dy <= r && is_max; ++dy)
+                    for (int dx = -r; dx <= r; ++dx) {
+                        if (dx == 0 && dy == 0) continue;
+                        const float nb = resp[(size_t)(y + dy) * w + x + dx];
+                        const int earlier = dy < 0 || (dy == 0 && dx < 0);
+                        if (nb > v || (nb == v && earlier)) {
+                            is_max = 0;
+                            break;
+                        }
+                    }
+                if (!is_max) continue;
+                if (count == cap) {
+                    cap *= 2;
+                    orc_kp *nl = (orc_kp *)realloc(list, (size_t)cap * sizeof(orc_kp));
+                    if (!nl) break;
+                    list = nl;
+                }
+                orc_kp *k = &list[count];
+                k->x = x + orc_subpixel_offset(resp[(size_t)y * w + x - 1], v, resp[(size_t)y * w + x + 1]);
+                k->y = y + orc_subpixel_offset(resp[(size_t)(y - 1) * w + x], v, resp[(size_t)(y + 1) * w + x]);
+                k->resp = v;
+                k->idx = count++;
+            }
+    }
+    free(ix), free(iy), free(resp);
+    if (!list) return -1;
+    qsort(list, (size_t)count, sizeof(orc_kp), orc_kp_cmp);
+    if (count > max_features) count = max_features;
+    /* fill_descriptor (features.hpp:110-134) */
+    for (int i = 0; i < count; ++i) {
+        kp[3 * i] = list[i].x;
+        kp[3 * i + 1] = list[i].y;
+        kp[3 * i + 2] = list[i].resp;
+        const int cx = (int)lround(list[i].x), cy = (int)lround(list[i].y);
+        float patch[64], mean = 0.f, norm2 = 0.f;
+        for (int by = 0; by < 8; ++by)
+            for (int bx = 0; bx < 8; ++bx) {
+                const int px = cx - 8 + 2 * bx, py = cy - 8 + 2 * by;
+                const float v = 0.25f * (gray[(size_t)py * w + px] + gray[(size_t)py * w + px + 1] +
+                                         gray[(size_t)(py + 1) * w + px] + gray[(size_t)(py + 1) * w + px + 1]);
+                patch[by * 8 + bx] = v;
+                mean += v;
+            }
+        mean /= 64;
+        for (int k = 0; k < 64; ++k) {
+            patch[k] -= mean;
+            norm2 += patch[k] * patch[k];
+        }
+        const float norm = sqrtf(norm2);
+        for (int k = 0; k < 64; ++k) desc[64 * (size_t)i + k] = norm > 1e-12f ? patch[k] / norm : 0.f;
+    }
+    free(list);
+    return count;
+}
+
+/* match_features (features.hpp:208-254) */
+int orc_match_features(const double *kp_a, const float *desc_a, int na, const double *kp_b,
+                       const float *desc_b, int nb, double ratio, double *out) {
+    if (na == 0 || nb < 2) return 0;
+    const double ratio_sq = ratio * ratio;
+    int n = 0;
+    for (int i = 0; i < na; ++i) {
+        const float *da = desc_a + 64 * (size_t)i;
+        float d1 = FLT_MAX, d2 = FLT_MAX;
+        int j1 = -1;
+        for (int j = 0; j < nb; ++j) {
+            const float *db = desc_b + 64 * (size_t)j;
+            float ssd = 0.f;
+            for (int k = 0; k < 64; k += 8) {
+                for (int u = 0; u < 8; ++u) {
+                    const float d = da[k + u] - db[k + u];
+                    ssd += d * d;
+                }
+                if (ssd > d2) break;
+            }
+            if (ssd < d1) {
+                d2 = d1;
+                d1 = ssd;
+                j1 = j;
+            } else if (ssd < d2) {
+                d2 = ssd;
+            }
+        }
+        if (j1 >= 0 && (double)d1 < ratio_sq * (double)d2) {
+            double *o = out + 5 * (size_t)n++;
+            o[0] = kp_a[3 * i];
+            o[1] = kp_a[3 * i + 1];
+            o[2] = kp_b[3 * j1];
+            o[3] = kp_b[3 * j1 + 1];
+            o[4] = 1.0 - sqrt((double)d1 / ((double)d2 > 1e-30 ? (double)d2 : 1e-30));
+        }
+    }
+    return n;
+}

@@ -96,6 +96,18 @@ int orc_emdq_field_grid(double x0, double y0, int w, int h, const double *apts,
                         int nactive, double alpha, int support, double beta, double *disp,
                         double *unc, int row_begin, int row_end);
 
+/* ---- sparse front end (features.hpp), FP32 as the
+ * reference computes it (no contraction) ---------------------------------- */
+/* to_gray (image.hpp:63-75) */
+void orc_to_gray(const uint8_t *im, int w, int h, int ch, float *out);
+/* detect_features (features.hpp:140-205): kp = double[n][3] (x, y, response),
+ * desc = float[n][64]; returns n (<= max_features). */
+int orc_detect_features(const float *gray, int w, int h, int max_features, double quality,
+                        int nms_radius, double *kp, float *desc);
+/* match_features (features.hpp:208-254): out = double[n][5]; returns n. */
+int orc_match_features(const double *kp_a, const float *desc_a, int na, const double *kp_b,
+                       const float *desc_b, int nb, double ratio, double *out);
+
 #ifdef __cplusplus
 }
 #endif

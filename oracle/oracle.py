@@ -65,6 +65,9 @@ class Oracle:
         L.orc_node_uncertainty.restype = _D
         L.orc_node_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _I, _D, _P, _P]
         L.orc_emdq_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P, _I, _I]
+        L.orc_to_gray.argtypes = [_P, _I, _I, _I, _P]
+        L.orc_detect_features.argtypes = [_P, _I, _I, _I, _D, _I, _P, _P]
+        L.orc_match_features.argtypes = [_P, _P, _I, _P, _P, _I, _D, _P]
         self.L = L
 
     # ---- canvas -------------------------------------------------------
@@ -212,6 +215,34 @@ class Oracle:
         return disp, unc
 
 
+    # ---- sparse front end (features.hpp) ----
+    def to_gray(self, image):
+        im = np.ascontiguousarray(image, np.uint8)
+        if im.ndim == 2:
+            im = im[:, :, None]
+        h, w, c = im.shape
+        out = np.zeros((h, w), np.float32)
+        self.L.orc_to_gray(_p(im), w, h, c, _p(out))
+        return out
+
+    def detect_features(self, gray, max_features=800, quality=0.005, nms_radius=4):
+        g = np.ascontiguousarray(gray, np.float32)
+        h, w = g.shape
+        kp = np.zeros((max(max_features, 1), 3))
+        desc = np.zeros((max(max_features, 1), 64), np.float32)
+        n = self.L.orc_detect_features(_p(g), w, h, int(max_features), float(quality), int(nms_radius), _p(kp),
+                                       _p(desc))
+        return kp[:n], desc[:n]
+
+    def match_features(self, kp_a, desc_a, kp_b, desc_b, ratio=0.8):
+        ka, kb = _f64(kp_a, 3), _f64(kp_b, 3)
+        da = np.ascontiguousarray(desc_a, np.float32).reshape(-1, 64)
+        db = np.ascontiguousarray(desc_b, np.float32).reshape(-1, 64)
+        out = np.zeros((max(len(ka), 1), 5))
+        n = self.L.orc_match_features(_p(ka), _p(da), len(ka), _p(kb), _p(db), len(kb), float(ratio), _p(out))
+        return out[:n]
+
+
 class Reference:
     """The real reference (headers compiled in place). Raises if not built."""
 
@@ -240,6 +271,14 @@ class Reference:
         L.ref_scene_render.argtypes = [_I, _I, _I, C.c_uint64, _I, _D, _D, _D, _I, _I, _P]
         L.ref_time_blend_frame.argtypes = [_P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _I, _P]
         L.ref_time_blend_frame.restype = _D
+        L.ref_textured_image.argtypes = [_I, _I, C.c_uint64, _P]
+        L.ref_to_gray.argtypes = [_P, _I, _I, _I, _P]
+        L.ref_detect_features.argtypes = [_P, _I, _I, _I, _D, _I, _I, _P, _P, _I]
+        L.ref_detect_features.restype = _I
+        L.ref_match_features.argtypes = [_P, _P, _I, _P, _P, _I, _D, _I, _P, _I]
+        L.ref_match_features.restype = _I
+        L.ref_time_detect_match.argtypes = [_P, _I, _I, _I, _P, _P, _I, _I, _D, _I, _D, _I, _P]
+        L.ref_time_detect_match.restype = _D
         self.L = L
 
     class Canvas:
@@ -394,6 +433,55 @@ class Reference:
         dt = self.L.ref_time_blend_frame(_p(f), w, h, c, _p(a), _p(q), len(a), float(alpha), _p(p), len(p),
                                          _p(pre), int(workers), _p(st))
         return dt, tuple(int(v) for v in st)
+
+
+    # ---- sparse front end (features.hpp) ----
+    def textured_image(self, w, h, seed):
+        out = np.zeros((h, w), np.uint8)
+        self.L.ref_textured_image(w, h, seed, _p(out))
+        return out
+
+    def to_gray(self, image):
+        im = np.ascontiguousarray(image, np.uint8)
+        if im.ndim == 2:
+            im = im[:, :, None]
+        h, w, c = im.shape
+        out = np.zeros((h, w), np.float32)
+        self.L.ref_to_gray(_p(im), w, h, c, _p(out))
+        return out
+
+    def detect_features(self, gray, max_features=800, quality=0.005, nms_radius=4, workers=1):
+        g = np.ascontiguousarray(gray, np.float32)
+        h, w = g.shape
+        cap = max(max_features, 1)
+        kp = np.zeros((cap, 3))
+        desc = np.zeros((cap, 64), np.float32)
+        n = self.L.ref_detect_features(_p(g), w, h, int(max_features), float(quality), int(nms_radius), int(workers),
+                                       _p(kp), _p(desc), cap)
+        return kp[:n], desc[:n]
+
+    def match_features(self, kp_a, desc_a, kp_b, desc_b, ratio=0.8, workers=1):
+        ka, kb = _f64(kp_a, 3), _f64(kp_b, 3)
+        da = np.ascontiguousarray(desc_a, np.float32).reshape(-1, 64)
+        db = np.ascontiguousarray(desc_b, np.float32).reshape(-1, 64)
+        cap = max(len(ka), 1)
+        out = np.zeros((cap, 5))
+        n = self.L.ref_match_features(_p(ka), _p(da), len(ka), _p(kb), _p(db), len(kb), float(ratio), int(workers),
+                                      _p(out), cap)
+        return out[:n]
+
+    def time_detect_match(self, image_b, kp_a, desc_a, max_features=800, quality=0.005, nms_radius=4, ratio=0.8,
+                          workers=1):
+        im = np.ascontiguousarray(image_b, np.uint8)
+        if im.ndim == 2:
+            im = im[:, :, None]
+        h, w, c = im.shape
+        ka = _f64(kp_a, 3)
+        da = np.ascontiguousarray(desc_a, np.float32).reshape(-1, 64)
+        counts = np.zeros(2, np.int32)
+        dt = self.L.ref_time_detect_match(_p(im), w, h, c, _p(ka), _p(da), len(ka), int(max_features), float(quality),
+                                          int(nms_radius), float(ratio), int(workers), _p(counts))
+        return dt, int(counts[0]), int(counts[1])
 
 
 def reference_available() -> bool:

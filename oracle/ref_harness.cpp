@@ -10,9 +10,11 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <random>
 #include <vector>
 
 #include "nrmosaic/config.hpp"
+#include "nrmosaic/features.hpp"
 #include "nrmosaic/fieldest.hpp"
 #include "nrmosaic/mosaic.hpp"
 #include "nrmosaic/slam.hpp"
@@ -370,6 +372,107 @@ double ref_time_blend_frame(const std::uint8_t* frame, int fw, int fh, int ch,
         stats[1] = s.blended_pixels;
         stats[2] = s.skipped_no_support;
         stats[3] = s.skipped_out_of_frame;
+    }
+    return dt;
+}
+
+// ---- sparse front end (features.hpp) ----------------
+
+// The fixture image of the reference's detector tests (test_features.cpp:14-32):
+// uniform random bytes from std::mt19937_64(seed), then two 3 x 3 box means
+// over the interior with integer division. Gray, 1 channel.
+void ref_textured_image(int w, int h, std::uint64_t seed, std::uint8_t* out) {
+    std::mt19937_64 rng(seed);
+    std::uniform_int_distribution<int> dist(0, 255);
+    std::vector<std::uint8_t> a(static_cast<std::size_t>(w) * h);
+    for (auto& p : a) p = static_cast<std::uint8_t>(dist(rng));
+    for (int pass = 0; pass < 2; ++pass) {
+        std::vector<std::uint8_t> b = a;
+        for (int y = 1; y + 1 < h; ++y)
+            for (int x = 1; x + 1 < w; ++x) {
+                int s = 0;
+                for (int v = -1; v <= 1; ++v)
+                    for (int u = -1; u <= 1; ++u) s += a[static_cast<std::size_t>(y + v) * w + (x + u)];
+                b[static_cast<std::size_t>(y) * w + x] = static_cast<std::uint8_t>(s / 9);
+            }
+        a.swap(b);
+    }
+    std::memcpy(out, a.data(), a.size());
+}
+
+// to_gray (image.hpp:63-75)
+void ref_to_gray(const std::uint8_t* im, int w, int h, int ch, float* out) {
+    const ImageF g = to_gray(to_image(im, w, h, ch));
+    if (!g.data.empty()) std::memcpy(out, g.data.data(), g.data.size() * sizeof(float));
+}
+
+static int put_features(const FrameFeatures& f, double* kp, float* desc, int cap) {
+    const int n = static_cast<int>(f.size());
+    for (int i = 0; i < n && i < cap; ++i) {
+        kp[3 * i] = f.keypoints[i].position.x;
+        kp[3 * i + 1] = f.keypoints[i].position.y;
+        kp[3 * i + 2] = f.keypoints[i].response;
+        std::memcpy(desc + 64 * static_cast<std::size_t>(i), f.descriptor(i), 64 * sizeof(float));
+    }
+    return n;
+}
+
+static FrameFeatures to_features(const double* kp, const float* desc, int n) {
+    FrameFeatures f;
+    f.keypoints.resize(n);
+    for (int i = 0; i < n; ++i) f.keypoints[i] = {{kp[3 * i], kp[3 * i + 1]}, kp[3 * i + 2]};
+    f.descriptors.assign(desc, desc + 64 * static_cast<std::size_t>(n));
+    return f;
+}
+
+// detect_features (features.hpp:140-205) on an FP32 gray image.
+int ref_detect_features(const float* gray, int w, int h, int max_features, double quality, int nms_radius,
+                        int workers, double* kp, float* desc, int cap) {
+    ImageF g = ImageF::make(w, h);
+    std::memcpy(g.data.data(), gray, g.data.size() * sizeof(float));
+    DetectorConfig cfg;
+    cfg.max_features = max_features;
+    cfg.quality_level = quality;
+    cfg.nms_radius = nms_radius;
+    cfg.workers = workers;
+    return put_features(detect_features(g, cfg), kp, desc, cap);
+}
+
+// match_features (features.hpp:208-254): rows (ax, ay, bx, by, score).
+int ref_match_features(const double* kp_a, const float* desc_a, int na, const double* kp_b, const float* desc_b,
+                       int nb, double ratio, int workers, double* out, int cap) {
+    const auto m = match_features(to_features(kp_a, desc_a, na), to_features(kp_b, desc_b, nb), ratio, workers);
+    const int n = static_cast<int>(m.size());
+    for (int i = 0; i < n && i < cap; ++i) {
+        out[5 * i] = m[i].point_a.x;
+        out[5 * i + 1] = m[i].point_a.y;
+        out[5 * i + 2] = m[i].point_b.x;
+        out[5 * i + 3] = m[i].point_b.y;
+        out[5 * i + 4] = m[i].score;
+    }
+    return n;
+}
+
+// Wall-clock of the reference's front end for one frame pair as its callers
+// run it (main.cpp:198-202): to_gray + detect_features on frame b, then
+// match_features against a's features, with `workers` threads.
+double ref_time_detect_match(const std::uint8_t* img_b, int w, int h, int ch, const double* kp_a,
+                             const float* desc_a, int na, int max_features, double quality, int nms_radius,
+                             double ratio, int workers, int* counts2) {
+    const ImageU8 im = to_image(img_b, w, h, ch);
+    const FrameFeatures fa = to_features(kp_a, desc_a, na);
+    DetectorConfig cfg;
+    cfg.max_features = max_features;
+    cfg.quality_level = quality;
+    cfg.nms_radius = nms_radius;
+    cfg.workers = workers;
+    const auto t0 = std::chrono::steady_clock::now();
+    const FrameFeatures fb = detect_features(to_gray(im), cfg);
+    const auto m = match_features(fa, fb, ratio, workers);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (counts2) {
+        counts2[0] = static_cast<int>(fb.size());
+        counts2[1] = static_cast<int>(m.size());
     }
     return dt;
 }

@@ -54,6 +54,12 @@ class Grid(C.Structure):
     _fields_ = [("x0", C.c_double), ("y0", C.c_double), ("width", C.c_int), ("height", C.c_int)]
 
 
+class DetectorConfig(C.Structure):
+    """nrm_detector_config = DetectorConfig (features.hpp:30-36)."""
+    _fields_ = [("max_features", C.c_int), ("quality_level", C.c_double), ("nms_radius", C.c_int),
+                ("ratio_test", C.c_double)]
+
+
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _F = C.POINTER(C.c_float)
@@ -107,6 +113,12 @@ SIGNATURES = [
                                   C.c_double, _P, _P, _P, _P]),
     ("nrm_emdq_points_device", C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, C.c_int, C.c_double,
                                          C.c_int, C.c_double, _P, _P, _P, _P]),
+    ("nrm_detect_features", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P, _P, _I]),
+    ("nrm_detect_features_gray", C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P, _P, _I]),
+    ("nrm_detect_features_device", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P,
+                                             _P, _P]),
+    ("nrm_match_features", C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_int, C.c_double, _P, _I]),
+    ("nrm_match_features_device", C.c_int, [_P, _P, _P, C.c_int, _P, _P, C.c_int, C.c_double, _P, _P]),
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
     ("nrm_ctx_exceptions", C.c_int, [_P, _I64, _I64]),

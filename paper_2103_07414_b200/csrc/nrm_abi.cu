@@ -564,8 +564,9 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     if (!c) return NRM_OK;
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
-    DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc, &c->misc, &c->stats,
-                      &c->pts,       &c->locals,     &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles};
+    DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc,   &c->misc,  &c->stats, &c->pts,
+                      &c->locals,    &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles, &c->feat,
+                      &c->feat_io};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();
@@ -1107,6 +1108,173 @@ int nrm_emdq_points_device(nrm_ctx* c, const double* d_q, const int32_t* d_exclu
     NRM_CUDA(cudaStreamSynchronize(c->stream));
     return points_core(c, bb, d_q, d_exclude, nq, d_apts, d_locals, d_probs, m_total, d_active, nactive, alpha,
                        support, beta, d_warps, d_pred, d_unc, d_status);
+}
+
+// ---- sparse front end (features.hpp) -------------------------------------------
+namespace {
+int detect_core(nrm_ctx* c, const uint8_t* d_image, const float* d_gray, int w, int h, int ch,
+                const nrm_detector_config* cfg, double* d_kp, float* d_desc, int* d_n) {
+    if (!cfg) return fail(NRM_EINVAL, "detect_features: null config");
+    if (w < 0 || h < 0 || (w > 0 && h > 0 && !d_image && !d_gray)) return fail(NRM_EINVAL, "detect_features: bad image");
+    if (!d_image && !d_gray) ch = 1;
+    if (d_image && ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "detect_features: channels must be 1, 3 or 4");
+    constexpr int kMargin = 10;  // kBorderMargin (features.hpp:55)
+    if (cfg->max_features < 0 || cfg->nms_radius < 0 || !std::isfinite(cfg->quality_level))
+        return fail(NRM_EINVAL, "detect_features: bad config");
+    if (cfg->nms_radius > kMargin)  // the reference would read outside the response image
+        return fail(NRM_EINVAL, "detect_features: nms_radius must be <= 10 (the border margin)");
+    if (w < 2 * kMargin + 1 || h < 2 * kMargin + 1 || cfg->max_features == 0) {  // features.hpp:144
+        NRM_CUDA(cudaMemsetAsync(d_n, 0, sizeof(int), c->stream));
+        return NRM_OK;
+    }
+    NRM_CUDA(c->feat.ensure(features_scratch_bytes(w, h, cfg->nms_radius, cfg->max_features) + 64));
+    FeatLaunch F;
+    F.image = d_image;
+    F.gray_in = d_gray;
+    F.w = w;
+    F.h = h;
+    F.ch = ch;
+    F.max_features = cfg->max_features;
+    F.nms_radius = cfg->nms_radius;
+    F.quality = static_cast<float>(cfg->quality_level);
+    F.kp = d_kp;
+    F.desc = d_desc;
+    F.status = d_n;  // status[0] = count; status[1] lives in misc
+    NRM_CUDA(c->misc.ensure(256));
+    int* st2 = reinterpret_cast<int*>(c->misc.as<char>() + 224);  // misc[224..232): keypoint count, fallback flag
+    F.status = st2;
+    F.scratch = c->feat.p;
+    NRM_CUDA(launch_detect_features(F, c->stream, &c->launches));
+    NRM_CUDA(cudaMemcpyAsync(d_n, st2, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+    return NRM_OK;
+}
+
+int match_core(nrm_ctx* c, const double* d_kpa, const float* d_da, int na, const double* d_kpb, const float* d_db,
+               int nb, double ratio, double* d_out, int* d_n) {
+    if (na < 0 || nb < 0) return fail(NRM_EINVAL, "match_features: negative size");
+    if (!std::isfinite(ratio)) return fail(NRM_EINVAL, "match_features: ratio must be finite");
+    if (na == 0 || nb < 2) {  // features.hpp:211
+        NRM_CUDA(cudaMemsetAsync(d_n, 0, sizeof(int), c->stream));
+        return NRM_OK;
+    }
+    NRM_CUDA(c->feat.ensure(match_scratch_bytes(na, nb)));
+    MatchLaunch M;
+    M.kp_a = d_kpa;
+    M.desc_a = d_da;
+    M.na = na;
+    M.kp_b = d_kpb;
+    M.desc_b = d_db;
+    M.nb = nb;
+    M.ratio = ratio;
+    M.out = d_out;
+    M.nout = d_n;
+    M.scratch = c->feat.p;
+    NRM_CUDA(launch_match_features(M, c->stream, &c->launches));
+    return NRM_OK;
+}
+}  // namespace
+
+int nrm_detect_features(nrm_ctx* c, const uint8_t* image, int w, int h, int ch, const nrm_detector_config* cfg,
+                        double* kp, float* desc, int* n) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!n || !cfg || (cfg->max_features > 0 && (!kp || !desc))) return fail(NRM_EINVAL, "detect_features: null output");
+    if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "detect_features: channels must be 1, 3 or 4");
+    if (w < 0 || h < 0 || (w > 0 && h > 0 && !image)) return fail(NRM_EINVAL, "detect_features: bad image");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    const size_t bytes = (size_t)w * h * ch;
+    NRM_CHECK(upload(c, c->frame_raw, image, bytes));
+    const int kmax = std::max(cfg->max_features, 0);
+    NRM_CUDA(c->feat_io.ensure((size_t)kmax * (3 * sizeof(double) + 64 * sizeof(float)) + 16));
+    double* d_kp = c->feat_io.as<double>();
+    float* d_desc = reinterpret_cast<float*>(d_kp + 3 * (size_t)kmax);
+    int* d_n = reinterpret_cast<int*>(d_desc + 64 * (size_t)kmax);
+    NRM_CHECK(detect_core(c, c->frame_raw.as<uint8_t>(), nullptr, w, h, ch, cfg, d_kp, d_desc, d_n));
+    NRM_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    if (*n > 0) {
+        NRM_CUDA(cudaMemcpyAsync(kp, d_kp, (size_t)*n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        NRM_CUDA(cudaMemcpyAsync(desc, d_desc, (size_t)*n * 64 * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        NRM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return NRM_OK;
+}
+
+int nrm_detect_features_gray(nrm_ctx* c, const float* gray, int w, int h, const nrm_detector_config* cfg, double* kp,
+                             float* desc, int* n) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!n || !cfg || (cfg->max_features > 0 && (!kp || !desc))) return fail(NRM_EINVAL, "detect_features: null output");
+    if (w < 0 || h < 0 || (w > 0 && h > 0 && !gray)) return fail(NRM_EINVAL, "detect_features: bad image");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    NRM_CHECK(upload(c, c->frame_raw, gray, (size_t)w * h * sizeof(float)));
+    const int kmax = std::max(cfg->max_features, 0);
+    NRM_CUDA(c->feat_io.ensure((size_t)kmax * (3 * sizeof(double) + 64 * sizeof(float)) + 16));
+    double* d_kp = c->feat_io.as<double>();
+    float* d_desc = reinterpret_cast<float*>(d_kp + 3 * (size_t)kmax);
+    int* d_n = reinterpret_cast<int*>(d_desc + 64 * (size_t)kmax);
+    NRM_CHECK(detect_core(c, nullptr, c->frame_raw.as<float>(), w, h, 1, cfg, d_kp, d_desc, d_n));
+    NRM_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    if (*n > 0) {
+        NRM_CUDA(cudaMemcpyAsync(kp, d_kp, (size_t)*n * 3 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        NRM_CUDA(cudaMemcpyAsync(desc, d_desc, (size_t)*n * 64 * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        NRM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return NRM_OK;
+}
+
+int nrm_detect_features_device(nrm_ctx* c, const uint8_t* d_image, int w, int h, int ch,
+                               const nrm_detector_config* cfg, double* d_kp, float* d_desc, int* d_n) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!d_n || !cfg || (cfg->max_features > 0 && (!d_kp || !d_desc))) return fail(NRM_EINVAL, "detect_features: null output");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    return detect_core(c, d_image, nullptr, w, h, ch, cfg, d_kp, d_desc, d_n);
+}
+
+int nrm_match_features(nrm_ctx* c, const double* kp_a, const float* desc_a, int na, const double* kp_b,
+                       const float* desc_b, int nb, double ratio, double* out, int* n) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!n || (na > 0 && (!kp_a || !desc_a || !out)) || (nb > 0 && (!kp_b || !desc_b)))
+        return fail(NRM_EINVAL, "match_features: null array");
+    if (na < 0 || nb < 0) return fail(NRM_EINVAL, "match_features: negative size");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    const size_t sa = (size_t)na, sb = (size_t)nb;
+    NRM_CUDA(c->feat_io.ensure((sa + sb) * (3 * sizeof(double) + 64 * sizeof(float)) + sa * 5 * sizeof(double) + 16));
+    double* d_kpa = c->feat_io.as<double>();
+    double* d_kpb = d_kpa + 3 * sa;
+    double* d_out = d_kpb + 3 * sb;
+    float* d_da = reinterpret_cast<float*>(d_out + 5 * sa);
+    float* d_db = d_da + 64 * sa;
+    int* d_n = reinterpret_cast<int*>(d_db + 64 * sb);
+    if (na) {
+        NRM_CUDA(cudaMemcpyAsync(d_kpa, kp_a, sa * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        NRM_CUDA(cudaMemcpyAsync(d_da, desc_a, sa * 64 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    }
+    if (nb) {
+        NRM_CUDA(cudaMemcpyAsync(d_kpb, kp_b, sb * 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        NRM_CUDA(cudaMemcpyAsync(d_db, desc_b, sb * 64 * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    }
+    NRM_CHECK(match_core(c, d_kpa, d_da, na, d_kpb, d_db, nb, ratio, d_out, d_n));
+    NRM_CUDA(cudaMemcpyAsync(n, d_n, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    if (*n > 0) {
+        NRM_CUDA(cudaMemcpyAsync(out, d_out, (size_t)*n * 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        NRM_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    return NRM_OK;
+}
+
+int nrm_match_features_device(nrm_ctx* c, const double* d_kp_a, const float* d_desc_a, int na, const double* d_kp_b,
+                              const float* d_desc_b, int nb, double ratio, double* d_out, int* d_n) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!d_n || (na > 0 && (!d_kp_a || !d_desc_a || !d_out)) || (nb > 0 && (!d_kp_b || !d_desc_b)))
+        return fail(NRM_EINVAL, "match_features: null array");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    return match_core(c, d_kp_a, d_desc_a, na, d_kp_b, d_desc_b, nb, ratio, d_out, d_n);
 }
 
 // ---- diagnostics -------------------------------------------------------------

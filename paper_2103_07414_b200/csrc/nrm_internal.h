@@ -54,7 +54,7 @@ struct nrm_ctx {
     int num_sms = 148;
     // scratch (grow-only)
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
-        active, out_a, out_b, tiles;
+        active, out_a, out_b, tiles, feat, feat_io;
     nrm::PinnedBuf staging, staging_out;
     nrm::Prof prof;
 };
@@ -212,5 +212,36 @@ cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h,
                                uint8_t* weight, cudaStream_t st, int64_t* launches);
 cudaError_t launch_canvas_write(nrm_canvas* cv, int x, int y, int w, int h, const double* rgb,
                                 const uint8_t* weight, cudaStream_t st, int64_t* launches);
+
+
+// ---- k_features.cu -------------------------------------
+struct FeatLaunch {
+    const uint8_t* image = nullptr;  // ImageU8 layout, or null when gray_in is set
+    const float* gray_in = nullptr;  // ImageF gray (detect_features' own input)
+    int w = 0, h = 0, ch = 1;
+    int max_features = 800, nms_radius = 4;
+    float quality = 0.005f;          // static_cast<float>(quality_level) (features.hpp:150)
+    double* kp = nullptr;            // [max_features][3]: x, y, response
+    float* desc = nullptr;           // [max_features][64]
+    int* status = nullptr;           // device int[2]: [0] keypoints
+    void* scratch = nullptr;         // features_scratch_bytes
+};
+size_t features_cand_cap(int w, int h, int r);
+size_t features_scratch_bytes(int w, int h, int r, int kmax);
+cudaError_t launch_detect_features(const FeatLaunch& F, cudaStream_t st, int64_t* launches);
+struct MatchLaunch {
+    const double* kp_a = nullptr;
+    const float* desc_a = nullptr;
+    int na = 0;
+    const double* kp_b = nullptr;
+    const float* desc_b = nullptr;
+    int nb = 0;
+    double ratio = 0.8;
+    double* out = nullptr;  // [na][5]: ax, ay, bx, by, score
+    int* nout = nullptr;    // device int
+    void* scratch = nullptr;
+};
+size_t match_scratch_bytes(int na, int nb);
+cudaError_t launch_match_features(const MatchLaunch& M, cudaStream_t st, int64_t* launches);
 
 }  // namespace nrm

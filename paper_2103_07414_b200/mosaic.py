@@ -453,3 +453,70 @@ def emdq_points_device(q_t, apts_t, locals_t, probs_t, active_t, alpha: float, b
                                           _tptr(locals_t), _tptr(probs_t), apts_t.shape[0], _tptr(active_t),
                                           active_t.shape[0], float(alpha), int(support), float(beta),
                                           _tptr(warps_t), _tptr(pred_t), _tptr(unc_t), _tptr(status_t)))
+
+
+# ---- sparse front end (features.hpp) ---------------------
+def _detector_config(max_features: int, quality: float, nms_radius: int, ratio: float = 0.8):
+    from ._lib import DetectorConfig
+    return DetectorConfig(int(max_features), float(quality), int(nms_radius), float(ratio))
+
+
+def detect_features(image, max_features: int = 800, quality: float = 0.005, nms_radius: int = 4,
+                    ctx: Optional[Context] = None):
+    """detect_features(to_gray(image), cfg) (features.hpp:140-205) on the GPU,
+    bit-identical to the reference. `image` is an ImageU8-layout uint8 array
+    (h, w) or (h, w, ch), or an FP32 gray image (h, w) (ImageF, the
+    reference's own detect_features input). Returns (kp (n, 3) = x, y,
+    response; desc (n, 64) float32), keypoints in the reference's order."""
+    ctx = ctx or default_context()
+    cfg = _detector_config(max_features, quality, nms_radius)
+    cap = max(int(max_features), 1)
+    kp = np.zeros((cap, 3), np.float64)
+    desc = np.zeros((cap, 64), np.float32)
+    n = C.c_int(0)
+    a = np.asarray(image)
+    if a.dtype == np.float32:
+        g = np.ascontiguousarray(a)
+        if g.ndim != 2:
+            raise ValueError("a gray image must be (h, w) float32")
+        h, w = g.shape
+        check(ctx._lib.nrm_detect_features_gray(ctx.handle, _ptr(g), w, h, C.byref(cfg), _ptr(kp), _ptr(desc),
+                                                C.byref(n)))
+    else:
+        f, w, h, ch = _frame(a)
+        check(ctx._lib.nrm_detect_features(ctx.handle, _ptr(f), w, h, ch, C.byref(cfg), _ptr(kp), _ptr(desc),
+                                           C.byref(n)))
+    return kp[:n.value], desc[:n.value]
+
+
+def detect_features_device(image_t, w: int, h: int, ch: int, kp_t, desc_t, n_t, max_features: int = 800,
+                           quality: float = 0.005, nms_radius: int = 4, ctx: Optional[Context] = None) -> None:
+    """Device-tensor variant: kp_t (max_features, 3) f64, desc_t (max_features, 64)
+    f32, n_t a device int32 scalar tensor receiving the count."""
+    ctx = ctx or default_context()
+    cfg = _detector_config(max_features, quality, nms_radius)
+    check(ctx._lib.nrm_detect_features_device(ctx.handle, _tptr(image_t), int(w), int(h), int(ch), C.byref(cfg),
+                                              _tptr(kp_t), _tptr(desc_t), _tptr(n_t)))
+
+
+def match_features(kp_a, desc_a, kp_b, desc_b, ratio: float = 0.8, ctx: Optional[Context] = None):
+    """match_features(a, b, ratio) (features.hpp:208-254) on the GPU,
+    bit-identical to the reference: rows (ax, ay, bx, by, score) in a order."""
+    ctx = ctx or default_context()
+    ka, kb = _f64(kp_a, 3, "kp_a"), _f64(kp_b, 3, "kp_b")
+    da = np.ascontiguousarray(desc_a, np.float32).reshape(-1, 64)
+    db = np.ascontiguousarray(desc_b, np.float32).reshape(-1, 64)
+    if len(da) != len(ka) or len(db) != len(kb):
+        raise ValueError("keypoint / descriptor count mismatch")
+    out = np.zeros((max(len(ka), 1), 5), np.float64)
+    n = C.c_int(0)
+    check(ctx._lib.nrm_match_features(ctx.handle, _ptr(ka), _ptr(da), len(ka), _ptr(kb), _ptr(db), len(kb),
+                                      float(ratio), _ptr(out), C.byref(n)))
+    return out[:n.value]
+
+
+def match_features_device(kp_a_t, desc_a_t, na: int, kp_b_t, desc_b_t, nb: int, ratio: float, out_t, n_t,
+                          ctx: Optional[Context] = None) -> None:
+    ctx = ctx or default_context()
+    check(ctx._lib.nrm_match_features_device(ctx.handle, _tptr(kp_a_t), _tptr(desc_a_t), int(na), _tptr(kp_b_t),
+                                             _tptr(desc_b_t), int(nb), float(ratio), _tptr(out_t), _tptr(n_t)))

@@ -173,3 +173,41 @@ def test_oracle_weighted_blend_with_unit_uncertainty_is_reference(oracle, golden
     ca, wa = a.arrays()
     cb, wb = b.arrays()
     assert np.array_equal(wa, wb) and np.array_equal(ca, cb)
+
+
+FEATURE_CASES = ["self", "translate", "noise", "tiny", "scene_rgb"]
+
+
+@pytest.mark.parametrize("case", FEATURE_CASES)
+def test_oracle_features_match_reference_bitwise(oracle, golden, case):
+    """to_gray / detect_features / match_features (features.hpp) of the C
+    restatement against the reference on its own detector-test fixtures."""
+    g = golden("features")
+    ga, gb = oracle.to_gray(g[f"{case}_a"]), oracle.to_gray(g[f"{case}_b"])
+    assert sha(ga) == str(g[f"{case}_ga_sha"]) and sha(gb) == str(g[f"{case}_gb_sha"])
+    ka, da = oracle.detect_features(ga)
+    kb, db = oracle.detect_features(gb)
+    assert np.array_equal(ka, g[f"{case}_kpa"]) and np.array_equal(kb, g[f"{case}_kpb"])
+    assert np.array_equal(da.view(np.uint32), g[f"{case}_da"].view(np.uint32))
+    assert np.array_equal(db.view(np.uint32), g[f"{case}_db"].view(np.uint32))
+    for key in g:
+        if key.startswith(f"{case}_m"):
+            ratio = int(key[len(case) + 2:]) / 100.0
+            assert np.array_equal(oracle.match_features(ka, da, kb, db, ratio), g[key]), key
+
+
+def test_features_reference_test_semantics(golden):
+    """The reference's detector tests (test_features.cpp:48-127) on the golden
+    outputs: self-matches have zero displacement, a 10-px wrap translation is
+    recovered by >= 80 % of the matches, noise gives few matches, a tiny image
+    none, and stricter ratios give fewer matches."""
+    g = golden("features")
+    m = g["self_m80"]
+    assert len(m) > 20 and np.array_equal(m[:, 0:2], m[:, 2:4])
+    assert ((m[:, 4] >= 0) & (m[:, 4] <= 1)).all()
+    t = g["translate_m80"]
+    good = ((np.abs(t[:, 2] - t[:, 0] - 10) <= 1) & (np.abs(t[:, 3] - t[:, 1]) <= 1)).sum()
+    assert len(t) > 30 and good >= 0.8 * len(t)
+    assert len(g["noise_m80"]) < min(len(g["noise_kpa"]), len(g["noise_kpb"])) // 5 + 5
+    assert len(g["tiny_kpa"]) == 0 and len(g["tiny_m80"]) == 0
+    assert len(g["translate_m60"]) <= len(g["translate_m80"]) <= len(g["translate_m95"])
