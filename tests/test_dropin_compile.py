@@ -33,3 +33,29 @@ def test_shim_compiles_against_reference_types(tmp_path):
            f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle' / 'stub'}", f"-I{REF / 'include'}", str(src)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+SRC_FEATURES = r'''
+#include "nrmosaic_b200/features.hpp"
+using namespace nrmosaic;
+// the front end as the reference CLI runs it (tools/main.cpp:169-216, 367-377)
+std::size_t run(const ImageU8& a, const ImageU8& b, const std::string& path) {
+    DetectorConfig cfg;
+    cfg.workers = 8;
+    const FrameFeatures fa = detect_features(to_gray(a), cfg);
+    const FrameFeatures fb = detect_features(b, cfg);
+    const auto m = match_features(fa, fb, cfg.ratio_test, cfg.workers);
+    save_matches(path, detect_and_match(a, b, cfg));
+    return m.size() + load_matches(path).size() + fa.descriptors.size();
+}
+'''
+
+
+@pytest.mark.skipif(not (REF / "include" / "nrmosaic" / "image.hpp").exists(), reason="reference tree absent")
+def test_features_shim_compiles_against_reference_types(tmp_path):
+    src = tmp_path / "dropin_features.cpp"
+    src.write_text(SRC_FEATURES)
+    cmd = ["g++", "-std=c++20", "-fsyntax-only", "-include", "algorithm", "-include", "memory",
+           f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle' / 'stub'}", f"-I{REF / 'include'}", str(src)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
