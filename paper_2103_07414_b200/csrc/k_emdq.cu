@@ -638,7 +638,60 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
         const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
         const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
         int nx = 0, nw = 0, nn = 0;
-        if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
+        if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED) && ne <= 32) {
+            // Lane l holds staged point l. Sorted copies of the {min, max}
+            // squared distances (a bitonic network over the lanes) turn each
+            // point's "how many others can be closer" counts into two binary
+            // searches: the same counts, hence the same classes, as the
+            // all-pairs loop below.
+            const unsigned below = (1u << lane) - 1u;
+            float dmn = INFINITY, dmx = INFINITY;
+            if (lane < ne) {
+                const float ax = w.ux[lane], ay = w.uy[lane];
+                const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
+                const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
+                dmn = fmaf(dxn, dxn, dyn * dyn);
+                dmx = fmaf(dxf, dxf, dyf * dyf);
+            }
+            float sa = dmn, sb = dmx;
+#pragma unroll
+            for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    const float pa = __shfl_xor_sync(0xffffffffu, sa, j), pb = __shfl_xor_sync(0xffffffffu, sb, j);
+                    const bool take_min = ((lane & k) == 0) == ((lane & j) == 0);
+                    sa = take_min ? fminf(sa, pa) : fmaxf(sa, pa);
+                    sb = take_min ? fminf(sb, pb) : fmaxf(sb, pb);
+                }
+            // points that can be the nearest somewhere in the sub-tile
+            const float thr = __shfl_sync(0xffffffffu, sb, 0) * (1.f + 1e-5f) + 1e-2f;
+            const unsigned mn = __ballot_sync(0xffffffffu, dmn <= thr);
+            nn = __popc(mn);
+            if (nn > NEAR_CAP)
+                nn = 255;
+            else if ((mn >> lane) & 1u)
+                nearg[st * NEAR_CAP + __popc(mn & below)] = (unsigned char)lane;
+            // cle = #{l : dmin_l <= hi_k} - 1 (k itself), clt = #{l : dmax_l < lo_k}
+            const float hi = dmx * (1.f + 1e-5f) + 1e-2f, lo = dmn * (1.f - 1e-5f) - 1e-2f;
+            int pa = 0, pb = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const float va = __shfl_sync(0xffffffffu, sa, pa + step - 1);
+                const float vb = __shfl_sync(0xffffffffu, sb, pb + step - 1);
+                if (va <= hi) pa += step;
+                if (vb < lo) pb += step;
+            }
+            const float la = __shfl_sync(0xffffffffu, sa, 31), lb = __shfl_sync(0xffffffffu, sb, 31);
+            if (pa == 31 && la <= hi) pa = 32;
+            if (pb == 31 && lb < lo) pb = 32;
+            int c = 0;
+            if (lane >= ni && lane < ne) c = pa - 1 < S ? 1 : (pb >= S ? 0 : 2);
+            const unsigned mi = __ballot_sync(0xffffffffu, c == 1), ma = __ballot_sync(0xffffffffu, c == 2);
+            nx = __popc(mi);
+            nw = __popc(ma);
+            if (c == 1) subg[st * TREC + __popc(mi & below)] = (unsigned char)lane;
+            if (c == 2) subg[st * TREC + nx + __popc(ma & below)] = (unsigned char)lane;
+        } else if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
             for (int k = lane; k < ne; k += 32) {
                 const float ax = w.ux[k], ay = w.uy[k];
                 const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
