@@ -634,122 +634,161 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     unsigned char* subg = &tp.sub[0][0];
     unsigned char* nearg = &tp.near[0][0];
     int my_nx = 0, my_na = 0, my_nn = 0;  // lane st < NW keeps sub-tile st's counts
-    for (int st = 0; st < NW; ++st) {
-        const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
-        const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
-        int nx = 0, nw = 0, nn = 0;
-        if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED) && ne <= 32) {
-            // Lane l holds staged point l. Sorted copies of the {min, max}
-            // squared distances (a bitonic network over the lanes) turn each
-            // point's "how many others can be closer" counts into two binary
-            // searches: the same counts, hence the same classes, as the
-            // all-pairs loop below.
-            const unsigned below = (1u << lane) - 1u;
-            float dmn = INFINITY, dmx = INFINITY;
-            if (lane < ne) {
-                const float ax = w.ux[lane], ay = w.uy[lane];
-                const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
-                const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
-                dmn = fmaf(dxn, dxn, dyn * dyn);
-                dmx = fmaf(dxf, dxf, dyf * dyf);
+    if (!(flags & TFLAG_EXACT_STAGED) && ne <= 32) {
+        // Lane l holds staged point l. Sorted copies of the {min, max} squared
+        // distances to the sub-tile (a bitonic network over the lanes) turn
+        // each point's "how many others can be closer" counts into two binary
+        // searches: the same counts, hence the same classes, as the all-pairs
+        // loop of the general path below. Two sub-tiles at a time for ILP.
+        constexpr int NP = 2;
+        const unsigned below = (1u << lane) - 1u;
+        const float ax = lane < ne ? w.ux[lane] : 0.f, ay = lane < ne ? w.uy[lane] : 0.f;
+        for (int st0 = 0; st0 < NW; st0 += NP) {
+            float dmn[NP], dmx[NP], sa[NP], sb[NP];
+            bool ok[NP];
+#pragma unroll
+            for (int u = 0; u < NP; ++u) {
+                const int st = st0 + u;
+                const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
+                const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
+                ok[u] = !(wx0 > wx1 || wy0 > wy1);
+                dmn[u] = dmx[u] = INFINITY;
+                if (lane < ne) {
+                    const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
+                    const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
+                    dmn[u] = fmaf(dxn, dxn, dyn * dyn);
+                    dmx[u] = fmaf(dxf, dxf, dyf * dyf);
+                }
+                sa[u] = dmn[u];
+                sb[u] = dmx[u];
             }
-            float sa = dmn, sb = dmx;
 #pragma unroll
             for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
                 for (int j = k >> 1; j > 0; j >>= 1) {
-                    const float pa = __shfl_xor_sync(0xffffffffu, sa, j), pb = __shfl_xor_sync(0xffffffffu, sb, j);
                     const bool take_min = ((lane & k) == 0) == ((lane & j) == 0);
-                    sa = take_min ? fminf(sa, pa) : fmaxf(sa, pa);
-                    sb = take_min ? fminf(sb, pb) : fmaxf(sb, pb);
-                }
-            // points that can be the nearest somewhere in the sub-tile
-            const float thr = __shfl_sync(0xffffffffu, sb, 0) * (1.f + 1e-5f) + 1e-2f;
-            const unsigned mn = __ballot_sync(0xffffffffu, dmn <= thr);
-            nn = __popc(mn);
-            if (nn > NEAR_CAP)
-                nn = 255;
-            else if ((mn >> lane) & 1u)
-                nearg[st * NEAR_CAP + __popc(mn & below)] = (unsigned char)lane;
-            // cle = #{l : dmin_l <= hi_k} - 1 (k itself), clt = #{l : dmax_l < lo_k}
-            const float hi = dmx * (1.f + 1e-5f) + 1e-2f, lo = dmn * (1.f - 1e-5f) - 1e-2f;
-            int pa = 0, pb = 0;
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const float va = __shfl_sync(0xffffffffu, sa, pa + step - 1);
-                const float vb = __shfl_sync(0xffffffffu, sb, pb + step - 1);
-                if (va <= hi) pa += step;
-                if (vb < lo) pb += step;
-            }
-            const float la = __shfl_sync(0xffffffffu, sa, 31), lb = __shfl_sync(0xffffffffu, sb, 31);
-            if (pa == 31 && la <= hi) pa = 32;
-            if (pb == 31 && lb < lo) pb = 32;
-            int c = 0;
-            if (lane >= ni && lane < ne) c = pa - 1 < S ? 1 : (pb >= S ? 0 : 2);
-            const unsigned mi = __ballot_sync(0xffffffffu, c == 1), ma = __ballot_sync(0xffffffffu, c == 2);
-            nx = __popc(mi);
-            nw = __popc(ma);
-            if (c == 1) subg[st * TREC + __popc(mi & below)] = (unsigned char)lane;
-            if (c == 2) subg[st * TREC + nx + __popc(ma & below)] = (unsigned char)lane;
-        } else if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
-            for (int k = lane; k < ne; k += 32) {
-                const float ax = w.ux[k], ay = w.uy[k];
-                const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
-                const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
-                w.wd[k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
-            }
-            __syncwarp();
-            // points that can be the nearest somewhere in the sub-tile
-            float thr = FLT_MAX;
-            for (int k = lane; k < ne; k += 32) thr = fminf(thr, w.wd[k].y);
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) thr = fminf(thr, __shfl_xor_sync(0xffffffffu, thr, d));
-            thr = thr * (1.f + 1e-5f) + 1e-2f;
-            for (int base = 0; base < ne; base += 32) {
-                const int k = base + lane;
-                const bool cand = k < ne && w.wd[k].x <= thr;
-                const unsigned mn = __ballot_sync(0xffffffffu, cand);
-                const int pos = nn + __popc(mn & ((1u << lane) - 1u));
-                if (cand && pos < NEAR_CAP) nearg[st * NEAR_CAP + pos] = (unsigned char)k;
-                nn += __popc(mn);
-            }
-            if (nn > NEAR_CAP) nn = 255;
-            for (int base = ni; base < ne; base += 32) {
-                const int k = base + lane;
-                int c = 0;
-                if (k < ne) {
-                    const float2 dk = w.wd[k];
-                    const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
-                    int cle = -1, clt = 0;  // l == k always counts in cle
-#pragma unroll 4
-                    for (int l = 0; l < ne; ++l) {
-                        const float2 dl = w.wd[l];
-                        cle += dl.x <= hi;
-                        clt += dl.y < lo;
+                    for (int u = 0; u < NP; ++u) {
+                        const float pa = __shfl_xor_sync(0xffffffffu, sa[u], j);
+                        const float pb = __shfl_xor_sync(0xffffffffu, sb[u], j);
+                        sa[u] = take_min ? fminf(sa[u], pa) : fmaxf(sa[u], pa);
+                        sb[u] = take_min ? fminf(sb[u], pb) : fmaxf(sb[u], pb);
                     }
-                    c = cle < S ? 1 : (clt >= S ? 0 : 2);
-                    w.wcls[k] = (unsigned char)c;
                 }
-                const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
-                if (c == 1) subg[st * TREC + nx + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
-                nx += __popc(mi);
+            // cle = #{l : dmin_l <= hi_k} - 1 (k itself), clt = #{l : dmax_l < lo_k}
+            float hi[NP], lo[NP];
+            int pa[NP], pb[NP];
+#pragma unroll
+            for (int u = 0; u < NP; ++u) {
+                hi[u] = dmx[u] * (1.f + 1e-5f) + 1e-2f;
+                lo[u] = dmn[u] * (1.f - 1e-5f) - 1e-2f;
+                pa[u] = pb[u] = 0;
             }
-            __syncwarp();
-            for (int base = ni; base < ne; base += 32) {
-                const int k = base + lane;
-                const int c = k < ne ? w.wcls[k] : 0;
-                const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
-                if (c == 2) subg[st * TREC + nx + nw + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
-                nw += __popc(ma);
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1)
+#pragma unroll
+                for (int u = 0; u < NP; ++u) {
+                    const float va = __shfl_sync(0xffffffffu, sa[u], pa[u] + step - 1);
+                    const float vb = __shfl_sync(0xffffffffu, sb[u], pb[u] + step - 1);
+                    if (va <= hi[u]) pa[u] += step;
+                    if (vb < lo[u]) pb[u] += step;
+                }
+#pragma unroll
+            for (int u = 0; u < NP; ++u) {
+                const int st = st0 + u;
+                const float la = __shfl_sync(0xffffffffu, sa[u], 31), lb = __shfl_sync(0xffffffffu, sb[u], 31);
+                if (pa[u] == 31 && la <= hi[u]) pa[u] = 32;
+                if (pb[u] == 31 && lb < lo[u]) pb[u] = 32;
+                // points that can be the nearest somewhere in the sub-tile
+                const float thr = __shfl_sync(0xffffffffu, sb[u], 0) * (1.f + 1e-5f) + 1e-2f;
+                const unsigned mn = __ballot_sync(0xffffffffu, dmn[u] <= thr);
+                int c = 0;
+                if (lane >= ni && lane < ne) c = pa[u] - 1 < S ? 1 : (pb[u] >= S ? 0 : 2);
+                const unsigned mi = __ballot_sync(0xffffffffu, c == 1), ma = __ballot_sync(0xffffffffu, c == 2);
+                int nx = 255, nw = 0, nn = 0;
+                if (ok[u]) {  // warp-uniform
+                    nn = __popc(mn);
+                    if (nn > NEAR_CAP)
+                        nn = 255;
+                    else if ((mn >> lane) & 1u)
+                        nearg[st * NEAR_CAP + __popc(mn & below)] = (unsigned char)lane;
+                    nx = __popc(mi);
+                    nw = __popc(ma);
+                    if (c == 1) subg[st * TREC + __popc(mi & below)] = (unsigned char)lane;
+                    if (c == 2) subg[st * TREC + nx + __popc(ma & below)] = (unsigned char)lane;
+                }
+                if (lane == st) {
+                    my_nx = nx;
+                    my_na = nw;
+                    my_nn = nn;
+                }
             }
-            __syncwarp();
-        } else {
-            nx = 255;  // sub-tile without valid pixels, or exact tile
         }
-        if (lane == st) {
-            my_nx = nx;
-            my_na = nw;
-            my_nn = nn;
+    } else {  // general path (more than 32 staged points): all pairs
+        for (int st = 0; st < NW; ++st) {
+            const float wx0 = (float)((st & 1) * 8), wy0 = (float)((st >> 1) * 4);
+            const float wx1 = fminf(wx0 + 7.f, (float)(ti1 - ti0)), wy1 = fminf(wy0 + 3.f, (float)(tj1 - tj0));
+            int nx = 0, nw = 0, nn = 0;
+            if (!(wx0 > wx1 || wy0 > wy1) && !(flags & TFLAG_EXACT_STAGED)) {
+                for (int k = lane; k < ne; k += 32) {
+                    const float ax = w.ux[k], ay = w.uy[k];
+                    const float dxn = fmaxf(fmaxf(wx0 - ax, 0.f), ax - wx1), dyn = fmaxf(fmaxf(wy0 - ay, 0.f), ay - wy1);
+                    const float dxf = fmaxf(ax - wx0, wx1 - ax), dyf = fmaxf(ay - wy0, wy1 - ay);
+                    w.wd[k] = make_float2(fmaf(dxn, dxn, dyn * dyn), fmaf(dxf, dxf, dyf * dyf));
+                }
+                __syncwarp();
+                // points that can be the nearest somewhere in the sub-tile
+                float thr = FLT_MAX;
+                for (int k = lane; k < ne; k += 32) thr = fminf(thr, w.wd[k].y);
+    #pragma unroll
+                for (int d = 16; d > 0; d >>= 1) thr = fminf(thr, __shfl_xor_sync(0xffffffffu, thr, d));
+                thr = thr * (1.f + 1e-5f) + 1e-2f;
+                for (int base = 0; base < ne; base += 32) {
+                    const int k = base + lane;
+                    const bool cand = k < ne && w.wd[k].x <= thr;
+                    const unsigned mn = __ballot_sync(0xffffffffu, cand);
+                    const int pos = nn + __popc(mn & ((1u << lane) - 1u));
+                    if (cand && pos < NEAR_CAP) nearg[st * NEAR_CAP + pos] = (unsigned char)k;
+                    nn += __popc(mn);
+                }
+                if (nn > NEAR_CAP) nn = 255;
+                for (int base = ni; base < ne; base += 32) {
+                    const int k = base + lane;
+                    int c = 0;
+                    if (k < ne) {
+                        const float2 dk = w.wd[k];
+                        const float hi = dk.y * (1.f + 1e-5f) + 1e-2f, lo = dk.x * (1.f - 1e-5f) - 1e-2f;
+                        int cle = -1, clt = 0;  // l == k always counts in cle
+    #pragma unroll 4
+                        for (int l = 0; l < ne; ++l) {
+                            const float2 dl = w.wd[l];
+                            cle += dl.x <= hi;
+                            clt += dl.y < lo;
+                        }
+                        c = cle < S ? 1 : (clt >= S ? 0 : 2);
+                        w.wcls[k] = (unsigned char)c;
+                    }
+                    const unsigned mi = __ballot_sync(0xffffffffu, c == 1);
+                    if (c == 1) subg[st * TREC + nx + __popc(mi & ((1u << lane) - 1u))] = (unsigned char)k;
+                    nx += __popc(mi);
+                }
+                __syncwarp();
+                for (int base = ni; base < ne; base += 32) {
+                    const int k = base + lane;
+                    const int c = k < ne ? w.wcls[k] : 0;
+                    const unsigned ma = __ballot_sync(0xffffffffu, c == 2);
+                    if (c == 2) subg[st * TREC + nx + nw + __popc(ma & ((1u << lane) - 1u))] = (unsigned char)k;
+                    nw += __popc(ma);
+                }
+                __syncwarp();
+            } else {
+                nx = 255;  // sub-tile without valid pixels, or exact tile
+            }
+            if (lane == st) {
+                my_nx = nx;
+                my_na = nw;
+                my_nn = nn;
+            }
         }
     }
     if (lane < NW) {
