@@ -22,9 +22,11 @@
 //                 sorts all candidates in global memory in the pathological
 //                 case of more than 2048 survivors tied at the cut
 //   k_descriptors one thread per keypoint (the reference's sequential sums)
-//   k_match       one warp per query descriptor, lanes over the candidates,
-//                 full FP32 SSD in the reference's order, (d1, j1, d2) merged
-//                 exactly as the sequential scan would; FP64 ratio test
+//   k_match       8 query descriptors x a 128-candidate chunk per CTA (staged
+//                 in shared memory), 4 candidates per lane, full FP32 SSDs in
+//                 the reference's order, (d1, j1, d2) merged exactly as the
+//                 sequential scan would; k_match_compact merges the chunks,
+//                 applies the FP64 ratio test and compacts in query order
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
@@ -135,18 +137,32 @@ __device__ __forceinline__ double subpixel_offset(float rm, float r0, float rp) 
     return fmin(fmax(off, -0.5), 0.5);
 }
 
-// Non-maximum suppression (features.hpp:153-182).
-__global__ void k_nms(const float* __restrict__ resp, int w, int h, int r, float quality,
-                      const unsigned* __restrict__ maxbits, Cand* __restrict__ out, unsigned* __restrict__ count,
-                      unsigned cap) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x + kMargin;
-    const int y = blockIdx.y + kMargin;
+// Non-maximum suppression (features.hpp:153-182) on a 32 x 8 tile of
+// responses staged in shared memory with an r-pixel halo (r <= kMargin).
+constexpr int NMS_W = 32, NMS_H = 8, NMS_HALO = kMargin;
+__global__ void __launch_bounds__(NMS_W * NMS_H) k_nms(const float* __restrict__ resp, int w, int h, int r,
+                                                       float quality, const unsigned* __restrict__ maxbits,
+                                                       Cand* __restrict__ out, unsigned* __restrict__ count,
+                                                       unsigned cap) {
+    constexpr int SW = NMS_W + 2 * NMS_HALO, SH = NMS_H + 2 * NMS_HALO;
+    __shared__ float sr[SH][SW + 1];
+    const int x0 = kMargin + blockIdx.x * NMS_W, y0 = kMargin + blockIdx.y * NMS_H;
+    const int t = threadIdx.x;
+    const int tw = NMS_W + 2 * r, th = NMS_H + 2 * r;  // staged window for this radius
+    for (int e = t; e < tw * th; e += NMS_W * NMS_H) {
+        const int sx = e % tw, sy = e / tw;
+        const int gx = x0 - r + sx, gy = y0 - r + sy;
+        sr[sy][sx] = (gx < w && gy < h) ? resp[(size_t)gy * w + gx] : 0.f;  // gx, gy >= 0 since r <= kMargin
+    }
+    __syncthreads();
+    const int lx = t % NMS_W, ly = t / NMS_W;
+    const int x = x0 + lx, y = y0 + ly;
     if (x >= w - kMargin || y >= h - kMargin) return;
     const float thr = fmul(quality, __uint_as_float(*maxbits));
-    const float v = resp[(size_t)y * w + x];
+    const float v = sr[ly + r][lx + r];
     if (!(v > thr)) return;
     for (int dy = -r; dy <= r; ++dy) {
-        const float* row = resp + (size_t)(y + dy) * w + x;
+        const float* row = &sr[ly + r + dy][lx + r];
         for (int dx = -r; dx <= r; ++dx) {
             if (dx == 0 && dy == 0) continue;
             const float n = row[dx];
@@ -341,62 +357,77 @@ __global__ void k_transpose_desc(const float* __restrict__ d, int n, float* __re
     dt[(size_t)k * n + j] = d[i];
 }
 
-// match_features (features.hpp:208-254): one warp per query descriptor a_i.
-// Each lane scans candidates j = lane, lane + 32, ... in ascending order with
-// the reference's (d1, j1, d2) update; lane summaries merge exactly (the
-// smallest index wins a tie for d1; d2 is the second smallest of the
-// multiset), which is what the sequential scan computes. The reference's
+// match_features (features.hpp:208-254). CTA = 8 query descriptors a_i (one
+// warp each) x one chunk of MCHUNK candidates staged in shared memory; each
+// lane scans 4 candidates j ascending (4 independent FP32 SSD chains in the
+// reference's order) with the reference's (d1, j1, d2) update. Summaries merge
+// exactly -- the smallest index wins a tie for d1 and d2 is the second
+// smallest of the multiset -- across lanes here and across chunks in
+// k_match_compact, which is what the sequential scan computes. The reference's
 // early exit (ssd > d2) never changes d1, j1 or d2, so full sums are used.
-__global__ void k_match(const float* __restrict__ da, int na, const float* __restrict__ dbt, int nb, double ratio_sq,
-                        int* __restrict__ best, double* __restrict__ score) {
+constexpr int MCHUNK = 128;
+struct MatchPart {
+    float d1, d2;
+    int j1, pad;
+};
+__device__ __forceinline__ void merge_part(float& d1, int& j1, float& d2, float e1, int k1, float e2) {
+    const float lo = fminf(d1, e1), hi = fmaxf(d1, e1);
+    const int jn = (d1 < e1 || (d1 == e1 && (unsigned)j1 < (unsigned)k1)) ? j1 : k1;  // j = -1 only with FLT_MAX
+    d2 = fminf(hi, fminf(d2, e2));
+    d1 = lo;
+    j1 = jn;
+}
+__global__ void __launch_bounds__(256) k_match(const float* __restrict__ da, int na, const float* __restrict__ dbt,
+                                               int nb, MatchPart* __restrict__ part) {
+    __shared__ float sb[kDim][MCHUNK];
     __shared__ float sa[8][kDim];
-    const int lane = threadIdx.x & 31, wv = threadIdx.x >> 5;
+    const int t = threadIdx.x, lane = t & 31, wv = t >> 5;
+    const int j0 = blockIdx.y * MCHUNK, nj = min(MCHUNK, nb - j0);
+    for (int e = t; e < kDim * MCHUNK; e += 256) {
+        const int k = e / MCHUNK, j = e % MCHUNK;
+        sb[k][j] = j < nj ? dbt[(size_t)k * nb + j0 + j] : 0.f;
+    }
     const int i = blockIdx.x * 8 + wv;
+    for (int k = lane; k < kDim; k += 32) sa[wv][k] = i < na ? da[(size_t)i * kDim + k] : 0.f;
+    __syncthreads();
     if (i >= na) return;
-    for (int k = lane; k < kDim; k += 32) sa[wv][k] = da[(size_t)i * kDim + k];
-    __syncwarp();
+    float ssd[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+    for (int k = 0; k < kDim; ++k) {
+        const float a = sa[wv][k];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const float d = fsub(a, sb[k][lane + 32 * u]);
+            ssd[u] = fadd(ssd[u], fmul(d, d));
+        }
+    }
     float d1 = FLT_MAX, d2 = FLT_MAX;
     int j1 = -1;
-    for (int j = lane; j < nb; j += 32) {
-        float ssd = 0.f;
-#pragma unroll 16
-        for (int k = 0; k < kDim; ++k) {
-            const float d = fsub(sa[wv][k], dbt[(size_t)k * nb + j]);
-            ssd = fadd(ssd, fmul(d, d));
-        }
-        if (ssd < d1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        if (lane + 32 * u >= nj) continue;
+        if (ssd[u] < d1) {
             d2 = d1;
-            d1 = ssd;
-            j1 = j;
-        } else if (ssd < d2) {
-            d2 = ssd;
+            d1 = ssd[u];
+            j1 = j0 + lane + 32 * u;
+        } else if (ssd[u] < d2) {
+            d2 = ssd[u];
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const float e1 = __shfl_xor_sync(0xffffffffu, d1, o), e2 = __shfl_xor_sync(0xffffffffu, d2, o);
         const int k1 = __shfl_xor_sync(0xffffffffu, j1, o);
-        const float lo = fminf(d1, e1), hi = fmaxf(d1, e1);
-        const int jn = (d1 < e1 || (d1 == e1 && (unsigned)j1 < (unsigned)k1)) ? j1 : k1;  // j = -1 only with FLT_MAX
-        d2 = fminf(hi, fminf(d2, e2));
-        d1 = lo;
-        j1 = jn;
+        merge_part(d1, j1, d2, e1, k1, e2);
     }
-    if (lane == 0) {
-        int b = -1;
-        double sc = 0.0;
-        if (j1 >= 0 && __dmul_rn(1.0, (double)d1) < __dmul_rn(ratio_sq, (double)d2)) {
-            b = j1;
-            sc = __dsub_rn(1.0, __dsqrt_rn(__ddiv_rn((double)d1, fmax((double)d2, 1e-30))));
-        }
-        best[i] = b;
-        score[i] = sc;
-    }
+    if (lane == 0) part[(size_t)i * gridDim.y + blockIdx.y] = MatchPart{d1, d2, j1, 0};
 }
 
 // Compaction of the matches in query order (one CTA, na <= 8192).
-__global__ void __launch_bounds__(1024) k_match_compact(const int* __restrict__ best, const double* __restrict__ score,
-                                                        int na, const double* __restrict__ kpa,
+// Each query's chunk summaries are merged first, then the ratio test (FP64,
+// features.hpp:241-245) decides.
+__global__ void __launch_bounds__(1024) k_match_compact(const MatchPart* __restrict__ part, int nchunks, int na,
+                                                        double ratio_sq, const double* __restrict__ kpa,
                                                         const double* __restrict__ kpb, double* __restrict__ out,
                                                         int* __restrict__ nout) {
     __shared__ int warp_tot[32];
@@ -406,7 +437,20 @@ __global__ void __launch_bounds__(1024) k_match_compact(const int* __restrict__ 
     __syncthreads();
     for (int base = 0; base < na; base += 1024) {
         const int i = base + t;
-        const bool hit = i < na && best[i] >= 0;
+        int bj = -1;
+        double sc = 0.0;
+        if (i < na) {
+            MatchPart p = part[(size_t)i * nchunks];
+            for (int c = 1; c < nchunks; ++c) {
+                const MatchPart q = part[(size_t)i * nchunks + c];
+                merge_part(p.d1, p.j1, p.d2, q.d1, q.j1, q.d2);
+            }
+            if (p.j1 >= 0 && (double)p.d1 < __dmul_rn(ratio_sq, (double)p.d2)) {
+                bj = p.j1;
+                sc = __dsub_rn(1.0, __dsqrt_rn(__ddiv_rn((double)p.d1, fmax((double)p.d2, 1e-30))));
+            }
+        }
+        const bool hit = bj >= 0;
         const unsigned m = __ballot_sync(0xffffffffu, hit);
         if (lane == 0) warp_tot[wv] = __popc(m);
         __syncthreads();
@@ -414,13 +458,12 @@ __global__ void __launch_bounds__(1024) k_match_compact(const int* __restrict__ 
         for (int w = 0; w < wv; ++w) before += warp_tot[w];
         if (hit) {
             const int o = before + __popc(m & ((1u << lane) - 1u));
-            const int j = best[i];
             double* r = out + 5 * (size_t)o;
             r[0] = kpa[3 * i];
             r[1] = kpa[3 * i + 1];
-            r[2] = kpb[3 * j];
-            r[3] = kpb[3 * j + 1];
-            r[4] = score[i];
+            r[2] = kpb[3 * bj];
+            r[3] = kpb[3 * bj + 1];
+            r[4] = sc;
         }
         __syncthreads();
         if (t == 0) {
@@ -475,8 +518,8 @@ cudaError_t launch_detect_features(const FeatLaunch& F, cudaStream_t st, int64_t
     ++*launches;
     const int iw = w - 2 * kMargin, ih = h - 2 * kMargin;
     prof_mark("k_nms", st);
-    k_nms<<<dim3((iw + 127) / 128, ih), 128, 0, st>>>(resp, w, h, F.nms_radius, F.quality, counters, cand,
-                                                      counters + 1, cap);
+    k_nms<<<dim3((iw + NMS_W - 1) / NMS_W, (ih + NMS_H - 1) / NMS_H), NMS_W * NMS_H, 0, st>>>(
+        resp, w, h, F.nms_radius, F.quality, counters, cand, counters + 1, cap);
     ++*launches;
     prof_mark("k_select", st);
     constexpr int sel_smem = SEL_CAP * (int)sizeof(Cand);
@@ -491,22 +534,23 @@ cudaError_t launch_detect_features(const FeatLaunch& F, cudaStream_t st, int64_t
 }
 
 size_t match_scratch_bytes(int na, int nb) {
-    return (size_t)nb * kDim * 4 + (size_t)na * (4 + 8) + 64;
+    const size_t nchunks = (size_t)(nb + MCHUNK - 1) / MCHUNK;
+    return (size_t)nb * kDim * 4 + 16 + (size_t)na * nchunks * sizeof(MatchPart) + 64;
 }
 
 cudaError_t launch_match_features(const MatchLaunch& M, cudaStream_t st, int64_t* launches) {
     char* base = static_cast<char*>(M.scratch);
     float* dbt = reinterpret_cast<float*>(base);
-    double* score = reinterpret_cast<double*>(base + (((size_t)M.nb * kDim * 4 + 7) & ~size_t(7)));
-    int* best = reinterpret_cast<int*>(score + M.na);
+    MatchPart* part = reinterpret_cast<MatchPart*>(base + (((size_t)M.nb * kDim * 4 + 15) & ~size_t(15)));
+    const int nchunks = (M.nb + MCHUNK - 1) / MCHUNK;
     prof_mark("k_transpose_desc", st);
     k_transpose_desc<<<(M.nb * kDim + 255) / 256, 256, 0, st>>>(M.desc_b, M.nb, dbt);
     ++*launches;
     prof_mark("k_match", st);
-    k_match<<<(M.na + 7) / 8, 256, 0, st>>>(M.desc_a, M.na, dbt, M.nb, M.ratio * M.ratio, best, score);
+    k_match<<<dim3((M.na + 7) / 8, nchunks), 256, 0, st>>>(M.desc_a, M.na, dbt, M.nb, part);
     ++*launches;
     prof_mark("k_match_compact", st);
-    k_match_compact<<<1, 1024, 0, st>>>(best, score, M.na, M.kp_a, M.kp_b, M.out, M.nout);
+    k_match_compact<<<1, 1024, 0, st>>>(part, nchunks, M.na, M.ratio * M.ratio, M.kp_a, M.kp_b, M.out, M.nout);
     ++*launches;
     return cudaGetLastError();
 }
