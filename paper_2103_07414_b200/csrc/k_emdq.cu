@@ -201,11 +201,45 @@ __device__ __forceinline__ void radius_from_hist(const int* hist, int S, int lan
 // ---------------------------------------------------------------------------
 // Supertile pass: candidate superset + rotation arc for each 64 x 64 block.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists SL, int S, float pad) {
+// Gathered candidate arrays written by k_super (the gather is fused into it).
+struct GatherOut {
+    double *x, *y, *l, *p, *phi;
+    float2* c32;
+    int* j;
+};
+
+// Also gathers the active candidates (grid-stride; k_gather's former job) for
+// the later kernels. Its own reads go through `active` directly, since other
+// CTAs are writing the gathered arrays concurrently; the values are the same.
+__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperLists SL, int S, float pad) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    {
+        const int nb = gridDim.x * gridDim.y;
+        for (int a = (blockIdx.y * gridDim.x + blockIdx.x) * ENT + t; a < L.nactive; a += nb * ENT) {
+            const int j = L.active[a];
+            const double x = L.apts[2 * j], y = L.apts[2 * j + 1];
+            G.x[a] = x;
+            G.y[a] = y;
+            G.c32[a] = make_float2((float)x, (float)y);
+#pragma unroll
+            for (int k = 0; k < 5; ++k) G.l[5 * a + k] = L.locals[5 * j + k];
+            const double p = L.probs[j];
+            G.p[a] = p < 1e-6 ? 1e-6 : p;  // std::max(probs[j], 1e-6)
+            G.phi[a] = atan2(L.locals[5 * j + 2], L.locals[5 * j + 1]);
+            G.j[a] = j;
+        }
+    }
+    auto coarse = [&](int a) {
+        const int j = L.active[a];
+        return make_float2((float)L.apts[2 * j], (float)L.apts[2 * j + 1]);
+    };
+    auto phi_of = [&](int a) {
+        const int j = L.active[a];
+        return atan2(L.locals[5 * j + 2], L.locals[5 * j + 1]);
+    };
     const int sid = blockIdx.y * SL.nsx + blockIdx.x;
     const int i0 = L.grid.i0 + blockIdx.x * ST, j0 = L.grid.j0 + blockIdx.y * ST;
     const int i1 = min(i0 + ST - 1, L.grid.i1), j1 = min(j0 + ST - 1, L.grid.j1);
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists 
     s.hist[t] = 0;
     __syncthreads();
     for (int a = t; a < N; a += ENT) {
-        const float2 c = C.c32[a];
+        const float2 c = coarse(a);
         const float dx = c.x - cx, dy = c.y - cy;
         atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
     }
@@ -235,7 +269,7 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists 
         const int a = base + lane;
         bool keep = false;
         if (a < a1) {
-            const float2 c = C.c32[a];
+            const float2 c = coarse(a);
             const float dx = c.x - cx, dy = c.y - cy;
             keep = !(fmaf(dx, dx, dy * dy) > lim2);
         }
@@ -264,10 +298,10 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, Cand C, SuperLists 
         int first = -1;
         for (int w = 0; w < NW && first < 0; ++w)
             if (s.wcnt[w] > 0) first = s.wcand[w][0];
-        phi0 = C.phi[first];
+        phi0 = phi_of(first);
         have0 = true;
         for (int k = lane; k < cnt; k += 32) {
-            double rel = C.phi[s.wcand[wid][k]] - phi0;
+            double rel = phi_of(s.wcand[wid][k]) - phi0;
             if (rel > M_PI) rel -= 2.0 * M_PI;
             if (rel < -M_PI) rel += 2.0 * M_PI;
             lo = fmin(lo, rel);
@@ -1195,19 +1229,14 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     TilePlans TP;
     TP.plan = reinterpret_cast<TilePlan*>(pbase);
 
-    prof_mark("k_gather", st);
-    k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
-                                                       c32, L.cl, L.cp, phi, cj);
-    ++*launches;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
     const int S = L.support < L.nactive ? L.support : L.nactive;
     const size_t ssm = sizeof(SSmem);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
-    e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, L, C, SL, S, 0.f);
+    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, S, 0.f);
     ++*launches;
-    e = cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int ntx = (L.grid.i1 - L.grid.i0 + ET) / ET;
     const int nty = (L.grid.j1 - L.grid.j0 + ET) / ET;
@@ -1269,21 +1298,24 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
     SL.count = SL.list + nsuper * SLIST_CAP;
     SL.flag = SL.count + nsuper;
 
-    prof_mark("k_gather", st);
-    k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
-                                                       c32, L.cl, L.cp, phi, cj);
-    ++*launches;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
     const int S = L.support < L.nactive ? L.support : L.nactive;
     // one more neighbour when a candidate may be left out; queries lie within
     // one pixel of their supertile's pixel rectangle
     const int Ssup = min(L.nactive, S + (P.excl ? 1 : 0));
-    if (!P.full_scan) {
+    if (P.full_scan) {
+        prof_mark("k_gather", st);
+        k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx,
+                                                           L.cy, c32, L.cl, L.cp, phi, cj);
+        ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    } else {
+        const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
         const size_t ssm = sizeof(SSmem);
         cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         prof_mark("k_super", st);
-        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, C, SL, Ssup, 3.f);
+        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, Ssup, 3.f);
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
