@@ -903,7 +903,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
     bool exact = false;
     const float ux = (float)col, uy = (float)row;
     const unsigned char* amb = wl + nxin;
-    if (MS > 0) {
+    if (MS > 0 && m > 0) {  // m == 0: the sure members fill S, nothing to select
         // sorted insertion of the ambiguous keys (closest-to-centre first, so
         // most later keys are rejected by one compare) into m <= MS slots
         float sd[MS > 0 ? MS : 1];
@@ -953,7 +953,7 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
                 if (q == u) k = sk[u];
             take(k);
         }
-    } else if (m > 0) {
+    } else if (MS == 0 && m > 0) {
         // many free slots (rare): repeated minimum selection; pass m + 1
         // finds the first rejected key for the near-tie test
         unsigned taken = 0u;
