@@ -2,8 +2,8 @@
 
 The oracle (the C restatement, pinned to the reference by the golden tests)
 runs the same inputs:
-  * C2 blend_frame in full: BlendStats and the weight plane must match exactly,
-    colour to 1e-3, the rendered mosaic to +-1 level;
+  * C2 and C4 blend_frame in full: BlendStats and the weight plane must match
+    exactly, colour to 1e-3, the rendered mosaic to +-1 level;
   * C2 / C4 dense EMDQ field on bands of rows spread over the frame (top,
     middle, bottom): displacement <= 1e-3 px, uncertainty <= 1e-6 relative;
   * C4 node field (K2) on windows at the frame centre and corner.
@@ -74,3 +74,24 @@ def test_c4_node_field_windows_match_oracle(nrm, ctx, oracle):
         assert np.array_equal(sup.astype(bool), osup.astype(bool))
         m = osup.astype(bool)
         assert np.abs(disp[m] - od[m]).max() <= DISP_TOL
+
+
+def test_c4_blend_frame_full_matches_oracle(nrm, ctx, oracle):
+    """configs[3] frame size: one 3840 x 2160 frame into a fresh canvas with its
+    frame lattice, in full (about 9 M footprint pixels)."""
+    wl = W.frame_workload("c4")
+    poly = nrm.invert_frame_boundary(wl.frame_w, wl.frame_h, wl.anchors, wl.warps, wl.params.alpha, ctx=ctx)
+    cv = nrm.Canvas(ctx)
+    st = nrm.blend_frame(cv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly).as_tuple()
+    ocv = oracle.canvas()
+    ost = oracle.blend_frame(ocv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly)
+    assert tuple(st) == ost, (st, ost)
+    assert ost[1] > 8_000_000
+    col, wt = cv.read()
+    ocol, owt = ocv.arrays()
+    assert np.array_equal(wt, owt)
+    assert np.abs(col.astype(np.float64) - ocol).max() <= COLOR_TOL
+    img, org = nrm.render(cv, crop=True)
+    oimg, oorg = oracle.render(ocv, crop=True)
+    assert org == oorg and img.shape == oimg.shape
+    assert np.abs(img.astype(np.int16) - oimg.astype(np.int16)).max() <= 1
