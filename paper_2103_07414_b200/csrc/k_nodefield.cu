@@ -377,21 +377,15 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     pdl_wait();
     const int half = blockIdx.x % NH;  // this CTA's column slice of the planning tile
     const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x / NH];
-    const int status = pl.h.status;
-    if (status == NF_OUTSIDE) return;
-
     const int tix = tile_i0 + blockIdx.x / NH;
     const int tjy = tile_row_of(by0 + blockIdx.y, tile_j0, s1, L.band_count);
     const int ti0 = tix * TW, tj0 = tjy * TH;  // planning tile origin
     const int hi0 = ti0 + CW * half;           // first column of this slice
-    const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + CW - 1, L.grid.i1);
-    const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
-    if (ci0 > ci1) return;  // the slice lies right of the grid
-    const int count = pl.h.count;
 
-    // ---- 0. stage the canvas half tile (the whole 64 x 32 tile lies in the
+    // ---- 0. stage the canvas slice (the whole 64 x 32 tile lies in the
     //         canvas: tiles and canvas bounds are both 32/64-aligned,
-    //         mosaic.hpp:141-151) and the first chunk of the tile's plan
+    //         mosaic.hpp:141-151) before the plan header arrives, then the
+    //         first chunk of the tile's plan
     if (MODE != 1) {
         const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (hi0 - L.phys_x0);
         {  // float planes: thread = (row r, 16-byte chunk k) for rows r and r + 16
@@ -406,6 +400,14 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
             cp_async16(&ct.w[r][16 * k], L.W + base + (long long)r * L.pitch + 16 * k);
         }
     }
+    const int status = pl.h.status;
+    const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + CW - 1, L.grid.i1);
+    const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
+    if (status == NF_OUTSIDE || ci0 > ci1) {  // outside the footprint rows / right of the grid
+        cp_async_wait_all();
+        return;
+    }
+    const int count = pl.h.count;
     if (status == NF_OK) stage_entries(s.e, pl.e, min(CHUNK, count));
     cp_async_commit();
 
