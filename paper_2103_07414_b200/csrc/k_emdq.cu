@@ -905,48 +905,46 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
     const unsigned char* amb = wl + nxin;
     if (MS > 0 && m > 0) {  // m == 0: the sure members fill S, nothing to select
         // sorted insertion of the ambiguous keys (closest-to-centre first, so
-        // most later keys are rejected by one compare) into m <= MS slots
+        // most later keys are rejected by one compare) into the m <= MS slots
+        // at the top of sd[]; the slots below hold -1 (< any d^2) and never
+        // move, so the network and the worst member (sd[MS - 1]) are static
         float sd[MS > 0 ? MS : 1];
         int sk[MS > 0 ? MS : 1];
 #pragma unroll
         for (int q = 0; q < MS; ++q) {
-            sd[q] = FLT_MAX;
+            sd[q] = q < MS - m ? -1.f : FLT_MAX;
             sk[q] = 0;
         }
-        float rej = FLT_MAX, worst = FLT_MAX;
+        float rej = FLT_MAX;
         for (int e = 0; e < namb; ++e) {
             const int k = amb[e];
             const float2 u = *reinterpret_cast<const float2*>(&p.rec0[k]);
             const float dx = u.x - ux, dy = u.y - uy;
             const float d2 = fmaf(dx, dx, dy * dy);
-            if (!(d2 < worst)) {
+            if (!(d2 < sd[MS - 1])) {
                 rej = fminf(rej, d2);
                 continue;
             }
-            rej = fminf(rej, worst);  // the current last member is evicted (or a sentinel)
+            rej = fminf(rej, sd[MS - 1]);  // the current last member is evicted (or a sentinel)
             bool lt[MS > 0 ? MS : 1];
 #pragma unroll
             for (int q = 0; q < MS; ++q) lt[q] = d2 < sd[q];
 #pragma unroll
             for (int q = MS - 1; q >= 0; --q) {
-                if (q < m) {
-                    if (q > 0 && lt[q - 1]) {
-                        sd[q] = sd[q - 1];
-                        sk[q] = sk[q - 1];
-                    } else if (lt[q]) {
-                        sd[q] = d2;
-                        sk[q] = k;
-                    }
+                if (q > 0 && lt[q - 1]) {
+                    sd[q] = sd[q - 1];
+                    sk[q] = sk[q - 1];
+                } else if (lt[q]) {
+                    sd[q] = d2;
+                    sk[q] = k;
                 }
             }
-#pragma unroll
-            for (int q = 0; q < MS; ++q)
-                if (q == m - 1) worst = sd[q];
         }
+        const float worst = sd[MS > 0 ? MS - 1 : 0];
         // near-tie between the last member and the first rejected key
         if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
         // m is warp-uniform: a real loop, not MS predicated takes
-        for (int q = 0; q < m; ++q) {
+        for (int q = MS - m; q < MS; ++q) {
             int k = sk[0];
 #pragma unroll
             for (int u = 1; u < (MS > 0 ? MS : 1); ++u)
