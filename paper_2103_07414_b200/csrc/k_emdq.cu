@@ -131,8 +131,10 @@ struct SSmem {
     int wcnt[NW];
     int wcand[NW][WCAP_S];
     double red_lo[NW], red_hi[NW];
+    double mincos;
     float R;
 };
+constexpr int SUPER_CC_CAP = 8192;  // candidates whose coarse coordinates k_super caches in shared memory
 
 __global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
                          const double* __restrict__ probs, const int32_t* __restrict__ active,
@@ -232,10 +234,18 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
             G.j[a] = j;
         }
     }
-    auto coarse = [&](int a) {
+    const int N = L.nactive;
+    // coarse coordinates of every candidate, cached in shared memory (one
+    // pass of dependent global loads instead of two)
+    float2* cc = N <= SUPER_CC_CAP ? reinterpret_cast<float2*>(smem_raw + ((sizeof(SSmem) + 15) & ~size_t(15)))
+                                   : nullptr;
+    auto coarse_g = [&](int a) {
         const int j = L.active[a];
         return make_float2((float)L.apts[2 * j], (float)L.apts[2 * j + 1]);
     };
+    if (cc)
+        for (int a = t; a < N; a += ENT) cc[a] = coarse_g(a);
+    auto coarse = [&](int a) { return cc ? cc[a] : coarse_g(a); };
     auto phi_of = [&](int a) {
         const int j = L.active[a];
         return atan2(L.locals[5 * j + 2], L.locals[5 * j + 1]);
@@ -246,7 +256,6 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     const double xlo = L.grid.gx + i0, xhi = L.grid.gx + i1, ylo = L.grid.gy + j0, yhi = L.grid.gy + j1;
     const float cx = (float)(0.5 * (xlo + xhi)), cy = (float)(0.5 * (ylo + yhi));
     const float hd = (float)(0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo)));
-    const int N = L.nactive;
 
     s.hist[t] = 0;
     __syncthreads();
@@ -263,8 +272,6 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     const int per = (N + NW - 1) / NW;
     const int a0 = wid * per, a1 = min(N, a0 + per);
     int cnt = 0;
-    double lo = 0.0, hi = 0.0, phi0 = 0.0;
-    bool have0 = false;
     for (int base = a0; base < a1; base += 32) {
         const int a = base + lane;
         bool keep = false;
@@ -293,13 +300,40 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     if (!overflow) {
         for (int k = lane; k < cnt; k += 32) SL.list[(size_t)sid * SLIST_CAP + off + k] = s.wcand[wid][k];
     }
-    // rotation arc over the list (relative to the first listed point)
+    // Rotation arc over the list, relative to the first listed point: are
+    // all phi = atan2(z, w) within less than a quarter turn? First a
+    // conservative test without atan2: every listed real part within
+    // pi/4 - 5e-7 of the first one's (cosine of the angle between the (w, z)
+    // vectors) bounds the spread below pi/2 - 1e-6. Only tiles that fail it
+    // take the exact atan2 pass (the original criterion).
+    constexpr double kCosQuarterArc = 0.7071072;  // > cos(pi/4 - 5e-7)
+    int first = -1;
+    for (int w = 0; w < NW && first < 0; ++w)
+        if (s.wcnt[w] > 0) first = s.wcand[w][0];
+    double mc = 1.0;
     if (total > 0 && !overflow) {
-        int first = -1;
-        for (int w = 0; w < NW && first < 0; ++w)
-            if (s.wcnt[w] > 0) first = s.wcand[w][0];
-        phi0 = phi_of(first);
-        have0 = true;
+        const int jf = L.active[first];
+        const double w0 = L.locals[5 * jf + 1], z0 = L.locals[5 * jf + 2];
+        const double n0 = w0 * w0 + z0 * z0;
+        for (int k = lane; k < cnt; k += 32) {
+            const int j = L.active[s.wcand[wid][k]];
+            const double w = L.locals[5 * j + 1], z = L.locals[5 * j + 2];
+            mc = fmin(mc, (w0 * w + z0 * z) / sqrt(n0 * (w * w + z * z)));
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mc = fmin(mc, __shfl_xor_sync(0xffffffffu, mc, d));
+    if (lane == 0) s.red_lo[wid] = mc;
+    __syncthreads();
+    if (t == 0) {
+        for (int w = 0; w < NW; ++w) mc = fmin(mc, s.red_lo[w]);
+        s.mincos = mc;
+    }
+    __syncthreads();
+    bool nonuniform = false;
+    if (!(s.mincos > kCosQuarterArc) && total > 0 && !overflow) {  // block-uniform
+        double lo = 0.0, hi = 0.0;
+        const double phi0 = phi_of(first);
         for (int k = lane; k < cnt; k += 32) {
             double rel = phi_of(s.wcand[wid][k]) - phi0;
             if (rel > M_PI) rel -= 2.0 * M_PI;
@@ -307,26 +341,27 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
             lo = fmin(lo, rel);
             hi = fmax(hi, rel);
         }
-    }
-    (void)have0;
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, d));
-        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, d));
-    }
-    if (lane == 0) {
-        s.red_lo[wid] = lo;
-        s.red_hi[wid] = hi;
-    }
-    __syncthreads();
-    if (t == 0) {
+        for (int d = 16; d > 0; d >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+        }
+        __syncthreads();  // red_lo reuse
+        if (lane == 0) {
+            s.red_lo[wid] = lo;
+            s.red_hi[wid] = hi;
+        }
+        __syncthreads();
         for (int w = 0; w < NW; ++w) {
             lo = fmin(lo, s.red_lo[w]);
             hi = fmax(hi, s.red_hi[w]);
         }
+        nonuniform = !((hi - lo) < (0.5 * M_PI - 1e-6));
+    }
+    if (t == 0) {
         int f = 0;
         if (overflow) f |= SFLAG_OVERFLOW;
-        if (!((hi - lo) < (0.5 * M_PI - 1e-6))) f |= SFLAG_NONUNIFORM;
+        if (nonuniform) f |= SFLAG_NONUNIFORM;
         SL.flag[sid] = f;
         SL.count[sid] = overflow ? N : total;
     }
@@ -1229,7 +1264,8 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
 
     const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
     const int S = L.support < L.nactive ? L.support : L.nactive;
-    const size_t ssm = sizeof(SSmem);
+    const size_t ssm = ((sizeof(SSmem) + 15) & ~size_t(15)) +
+                       (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
     k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, S, 0.f);
@@ -1310,7 +1346,8 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
         if (e != cudaSuccess) return e;
     } else {
         const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
-        const size_t ssm = sizeof(SSmem);
+        const size_t ssm = ((sizeof(SSmem) + 15) & ~size_t(15)) +
+                           (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
         cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         prof_mark("k_super", st);
         k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, Ssup, 3.f);
