@@ -229,6 +229,17 @@ int nrm_emdq_points_device(nrm_ctx *ctx, const double *d_q, const int32_t *d_exc
                            int support, double beta, double *d_warps, double *d_pred,
                            double *d_unc, int32_t *d_status);
 
+/* blend_frame for nf frames of one size, in order, on device pointers (the
+ * multi-GPU weak-scaling step blends several frames per rank). Frames whose
+ * footprint windows are pairwise disjoint go through one planner, one field
+ * and one exception launch for all of them (up to 16 frames); otherwise (or
+ * for node lattices of 257+ nodes) the frames are blended one by one. Results are identical to
+ * nf nrm_blend_frame_device calls. d_stats: int64[nf][4] on the device. */
+int nrm_blend_frames_device(nrm_canvas *canvas, int nf, const uint8_t *const *d_frames, int fw, int fh,
+                            int ch, const double *const *d_anchors, const double *const *d_warps,
+                            const int *n, double alpha, const double *const *polys, const int *npoly,
+                            int64_t *d_stats);
+
 /* ---- sparse front end -------------------------------
  * Corner detection and ratio-test matching before the EM, bit-identical to
  * the reference (features.hpp). */

@@ -113,6 +113,8 @@ SIGNATURES = [
                                   C.c_double, _P, _P, _P, _P]),
     ("nrm_emdq_points_device", C.c_int, [_P, _P, _P, C.c_int, _P, _P, _P, C.c_int, _P, C.c_int, C.c_double,
                                          C.c_int, C.c_double, _P, _P, _P, _P]),
+    ("nrm_blend_frames_device", C.c_int, [_P, C.c_int, _P, C.c_int, C.c_int, C.c_int, _P, _P, _P, C.c_double, _P,
+                                          _P, _P]),
     ("nrm_detect_features", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P, _P, _I]),
     ("nrm_detect_features_gray", C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P, _P, _I]),
     ("nrm_detect_features_device", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.POINTER(DetectorConfig), _P,

@@ -24,6 +24,7 @@
 //   (xpixel_warp, the reference's operation order and libm) resolves. That
 //   pass also finalises BlendStats and resets the per-context counters.
 #include <cmath>
+#include <vector>
 
 #include "nrm_common.cuh"
 #include "nrm_internal.h"
@@ -99,6 +100,13 @@ struct CanvasTile {
     uint8_t w[TH][HW];
 };
 
+
+// One frame of a batched blend (frames with pairwise disjoint footprints).
+struct NfBatchFrame {
+    NodeFieldLaunch L;  // the frame's launch, with its own queue / counters / stats
+    int ti0, tj0, tj1, s1, ntx, rows;
+    int plan_off, cta_off;  // first plan / first K1 CTA of this frame
+};
 
 __host__ __device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1, int band_count) {
     if (band_count <= 1) return tile_j0 + by;
@@ -187,7 +195,7 @@ __device__ __forceinline__ const int* chunk_nodes(const NodeFieldLaunch& L, int 
     return L.lists + (size_t)li * L.lstride;
 }
 
-__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int tile_i0,
+__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int g, int tile_i0,
                                              int tile_j0, int tile_j_last, int s1, int by0, int rows, int ntx,
                                              unsigned (*list_s)[NF_CAP]);
 
@@ -199,15 +207,30 @@ __global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
 k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
           int rows, int ntx) {
     __shared__ unsigned list_s[NF_PLAN_WARPS][NF_CAP];
-    nf_plan_tile(L, plans, tile_i0, tile_j0, tile_j_last, s1, by0, rows, ntx, list_s);
+    nf_plan_tile(L, plans, blockIdx.x * NF_PLAN_WARPS + (threadIdx.x >> 5), tile_i0, tile_j0, tile_j_last, s1, by0,
+                 rows, ntx, list_s);
     pdl_wait();
 }
 
-__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int tile_i0,
+// Planner of a batched blend: one warp per tile over all frames' tiles.
+__global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
+k_nf_plan_batch(const NfBatchFrame* __restrict__ F, int nf, NfPlan* __restrict__ plans, int total) {
+    __shared__ unsigned list_s[NF_PLAN_WARPS][NF_CAP];
+    const int gt = blockIdx.x * NF_PLAN_WARPS + (threadIdx.x >> 5);
+    if (gt < total) {
+        int f = 0;
+        while (f + 1 < nf && gt >= F[f + 1].plan_off) ++f;
+        const NfBatchFrame& fr = F[f];
+        nf_plan_tile(fr.L, plans + fr.plan_off, gt - fr.plan_off, fr.ti0, fr.tj0, fr.tj1, fr.s1, 0, fr.rows, fr.ntx,
+                     list_s);
+    }
+    pdl_wait();
+}
+
+__device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* __restrict__ plans, int g, int tile_i0,
                                              int tile_j0, int tile_j_last, int s1, int by0, int rows, int ntx,
                                              unsigned (*list_s)[NF_CAP]) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.x * NF_PLAN_WARPS + wid;
     if (g >= rows * ntx) return;
     unsigned* list = list_s[wid];
     NfPlan& pl = plans[g];
@@ -365,20 +388,20 @@ __device__ __forceinline__ void stage_entries(NfEntry* dst, const NfEntry* src, 
         cp_async16(reinterpret_cast<char*>(dst) + 16 * c, reinterpret_cast<const char*>(src) + 16 * c);
 }
 
+// One K1/K2 CTA: slice bx of launch-grid column, launch row by (see the
+// kernels below for the grid layouts).
 template <int MODE>
-__global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
-k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
-             int ntx) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+__device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfPlan* __restrict__ plans, int tile_i0,
+                                             int tile_j0, int s1, int by0, int ntx, int bx, int by,
+                                             unsigned char* smem_raw) {
     constexpr int MT = K1Shape<MODE>::MT, CW = K1Shape<MODE>::CW, NH = K1Shape<MODE>::NH;
     Smem<CW>& s = *reinterpret_cast<Smem<CW>*>(smem_raw);
     CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem<CW>) + 15) & ~size_t(15)));
     const int t = threadIdx.x;
-    pdl_wait();
-    const int half = blockIdx.x % NH;  // this CTA's column slice of the planning tile
-    const NfPlan& pl = plans[blockIdx.y * ntx + blockIdx.x / NH];
-    const int tix = tile_i0 + blockIdx.x / NH;
-    const int tjy = tile_row_of(by0 + blockIdx.y, tile_j0, s1, L.band_count);
+    const int half = bx % NH;  // this CTA's column slice of the planning tile
+    const NfPlan& pl = plans[by * ntx + bx / NH];
+    const int tix = tile_i0 + bx / NH;
+    const int tjy = tile_row_of(by0 + by, tile_j0, s1, L.band_count);
     const int ti0 = tix * TW, tj0 = tjy * TH;  // planning tile origin
     const int hi0 = ti0 + CW * half;           // first column of this slice
 
@@ -669,6 +692,31 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
     if (MODE != 1) block_add3<NT>(L.acc, nb, nns, noof);
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
+k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
+             int ntx) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    nf_field_cta<MODE>(L, plans, tile_i0, tile_j0, s1, by0, ntx, blockIdx.x, blockIdx.y, smem_raw);
+}
+
+// Batched blends of frames with pairwise disjoint footprints (the order of
+// their updates is then irrelevant): one launch over all frames' CTAs.
+template <int MODE>
+__global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
+k_node_field_batch(const NfBatchFrame* __restrict__ F, int nf, const NfPlan* __restrict__ plans) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int NH = K1Shape<MODE>::NH;
+    pdl_wait();
+    int f = 0;
+    while (f + 1 < nf && (int)blockIdx.x >= F[f + 1].cta_off) ++f;
+    const NfBatchFrame& fr = F[f];
+    const int lc = (int)blockIdx.x - fr.cta_off, per_row = fr.ntx * NH;
+    nf_field_cta<MODE>(fr.L, plans + fr.plan_off, fr.ti0, fr.tj0, fr.s1, 0, fr.ntx, lc % per_row, lc / per_row,
+                       smem_raw);
+}
+
 // Exact-tier resolution of queued pixels (mosaic.hpp:243-283 semantics), one
 // CTA. It then writes BlendStats (footprint + partial sums) and restores the
 // per-context state (acc = 0, exc_count = 0) for the next call.
@@ -775,73 +823,79 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
     return xpw_finish(s, out);
 }
 
+// Queued pixel q of launch L, resolved by one warp in the exact tier. Returns
+// (valid in lane 0) 0 blended, 1 no support, 2 out of frame, -1 (field mode).
 template <int MODE>
-__global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
-    __shared__ int red[3][EXC_THREADS / 32];
-    __shared__ bool last;
-    __shared__ double stage[EXC_THREADS / 32][32 * 6];
-    pdl_trigger();  // the next blend's planner may start (it only reads nodes)
-    pdl_wait();
-    const unsigned cnt = min(*L.exc_count, L.exc_cap);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + wid, nwarps = gridDim.x * (EXC_THREADS / 32);
-    int nb = 0, nns = 0, noof = 0;
+__device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, unsigned q, double* stage) {
+    const int lane = threadIdx.x & 31;
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
-    // one warp per queued pixel, spread over the whole GPU
-    for (unsigned q = gw; q < cnt; q += nwarps) {
-        const int2 p = L.exc[q];
-        const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
-        W5 wp;
-        // the pixel's launch chunk: tile row -> launch row (inverse of tile_row_of)
-        const int tjy = floordiv(p.y, TH);
-        const int by = L.band_count <= 1 ? tjy - L.tile_j0
-                                         : 2 * (((tjy >> 1) - L.band_s1) / L.band_count) + (tjy & 1);
-        int nsrc;
-        const int tix = floordiv(p.x, TW) - floordiv(L.grid.i0, TW);
-        const int* src = chunk_nodes(L, by / L.chunk_rows, tix / NF_GROUP_TILES, &nsrc);
-        const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp, stage[wid]);
-        if (lane != 0) continue;
-        if (MODE == 1) {
-            const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
-            if (rc == 0) {
-                double yx, yy;
-                xapply(wp, x, y, &yx, &yy);
-                if (L.disp) L.disp[o] = make_float2((float)(yx - x), (float)(yy - y));
-                if (L.support) L.support[o] = 1;
-            } else {
-                if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
-                if (L.support) L.support[o] = 0;
-            }
-            continue;
+    const int2 p = L.exc[q];
+    const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
+    W5 wp;
+    // the pixel's launch chunk: tile row -> launch row (inverse of tile_row_of)
+    const int tjy = floordiv(p.y, TH);
+    const int by = L.band_count <= 1 ? tjy - L.tile_j0
+                                     : 2 * (((tjy >> 1) - L.band_s1) / L.band_count) + (tjy & 1);
+    int nsrc;
+    const int tix = floordiv(p.x, TW) - floordiv(L.grid.i0, TW);
+    const int* src = chunk_nodes(L, by / L.chunk_rows, tix / NF_GROUP_TILES, &nsrc);
+    const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp, stage);
+    if (lane != 0) return -1;
+    if (MODE == 1) {
+        const size_t o = (size_t)(p.y - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (p.x - L.grid.i0);
+        if (rc == 0) {
+            double yx, yy;
+            xapply(wp, x, y, &yx, &yy);
+            if (L.disp) L.disp[o] = make_float2((float)(yx - x), (float)(yy - y));
+            if (L.support) L.support[o] = 1;
+        } else {
+            if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+            if (L.support) L.support[o] = 0;
         }
-        if (rc != 0) {
-            ++nns;
-            continue;
-        }
-        double yx, yy;
-        xapply(wp, x, y, &yx, &yy);
-        if (!(yx >= 0.0 && yx <= fxm && yy >= 0.0 && yy <= fym)) {
-            ++noof;
-            continue;
-        }
-        double rgb[3];
-        xsample_bilinear(L.frame, L.fw, L.fh, L.fch, yx, yy, rgb);
-        const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
-        const uint8_t wg = L.W[idx];
-        const double wd = wg;
-        // reference operation order, no contraction (mosaic.hpp:278-282); the
-        // weighted mode runs the same operations with a = w + 1 - cf, cf <= 1
-        double a = wd, cf = 1.0;
-        if (MODE == 2) {  // weighted mode (see NodeFieldLaunch::unc)
-            cf = 1.0 / fmax(xsample_bilinear_f32(L.unc, L.fw, L.fh, yx, yy), 1.0);
-            a = xsub(xadd(wd, 1.0), cf);
-        }
-        L.R[idx] = (float)(xadd(xmul(a, (double)L.R[idx]), xmul(cf, rgb[0] / 255.0)) / xadd(wd, 1.0));
-        L.G[idx] = (float)(xadd(xmul(a, (double)L.G[idx]), xmul(cf, rgb[1] / 255.0)) / xadd(wd, 1.0));
-        L.B[idx] = (float)(xadd(xmul(a, (double)L.B[idx]), xmul(cf, rgb[2] / 255.0)) / xadd(wd, 1.0));
-        L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
-        ++nb;
+        return -1;
     }
+    if (rc != 0) return 1;
+    double yx, yy;
+    xapply(wp, x, y, &yx, &yy);
+    if (!(yx >= 0.0 && yx <= fxm && yy >= 0.0 && yy <= fym)) return 2;
+    double rgb[3];
+    xsample_bilinear(L.frame, L.fw, L.fh, L.fch, yx, yy, rgb);
+    const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
+    const uint8_t wg = L.W[idx];
+    const double wd = wg;
+    // reference operation order, no contraction (mosaic.hpp:278-282); the
+    // weighted mode runs the same operations with a = w + 1 - cf, cf <= 1
+    double a = wd, cf = 1.0;
+    if (MODE == 2) {  // weighted mode (see NodeFieldLaunch::unc)
+        cf = 1.0 / fmax(xsample_bilinear_f32(L.unc, L.fw, L.fh, yx, yy), 1.0);
+        a = xsub(xadd(wd, 1.0), cf);
+    }
+    L.R[idx] = (float)(xadd(xmul(a, (double)L.R[idx]), xmul(cf, rgb[0] / 255.0)) / xadd(wd, 1.0));
+    L.G[idx] = (float)(xadd(xmul(a, (double)L.G[idx]), xmul(cf, rgb[1] / 255.0)) / xadd(wd, 1.0));
+    L.B[idx] = (float)(xadd(xmul(a, (double)L.B[idx]), xmul(cf, rgb[2] / 255.0)) / xadd(wd, 1.0));
+    L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
+    return 0;
+}
+
+// The queued pixels of one launch, one warp per pixel spread over the grid;
+// returns this thread's partial BlendStats counts (lane 0 of each warp).
+template <int MODE>
+__device__ __forceinline__ void exc_run(const NodeFieldLaunch& L, double* stage, int& nb, int& nns, int& noof) {
+    const unsigned cnt = min(*L.exc_count, L.exc_cap);
+    const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (EXC_THREADS / 32);
+    for (unsigned q = gw; q < cnt; q += nwarps) {
+        const int r = exc_pixel<MODE>(L, q, stage);
+        nb += r == 0;
+        nns += r == 1;
+        noof += r == 2;
+    }
+}
+
+// Block-sums the partial counts into L.acc (blend modes).
+template <int MODE>
+__device__ __forceinline__ void exc_accumulate(const NodeFieldLaunch& L, int nb, int nns, int noof,
+                                               int (*red)[EXC_THREADS / 32]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         nb += __shfl_xor_sync(0xffffffffu, nb, o);
@@ -854,13 +908,44 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
         red[2][wid] = noof;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && MODE != 1) {
         unsigned long long tot[3] = {0, 0, 0};
         for (int k = 0; k < 3; ++k)
             for (int w = 0; w < EXC_THREADS / 32; ++w) tot[k] += (unsigned long long)red[k][w];
-        if (MODE != 1)
-            for (int k = 0; k < 3; ++k)
-                if (tot[k]) atomicAdd(&L.acc[k], tot[k]);
+        for (int k = 0; k < 3; ++k)
+            if (tot[k]) atomicAdd(&L.acc[k], tot[k]);
+    }
+    __syncthreads();
+}
+
+// BlendStats and the per-launch state reset (one thread of the last CTA).
+template <int MODE>
+__device__ __forceinline__ void exc_finalize(const NodeFieldLaunch& L) {
+    if (MODE != 1) {
+        volatile unsigned long long* acc = L.acc;
+        if (L.stats_out) {
+            L.stats_out[0] = L.footprint;
+            L.stats_out[1] = acc[0];
+            L.stats_out[2] = acc[1];
+            L.stats_out[3] = acc[2];
+        }
+        acc[0] = acc[1] = acc[2] = 0;
+    }
+    if (L.exc_last) *L.exc_last = min(*L.exc_count, L.exc_cap);
+    *L.exc_count = 0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch L) {
+    __shared__ int red[3][EXC_THREADS / 32];
+    __shared__ bool last;
+    __shared__ double stage[EXC_THREADS / 32][32 * 6];
+    pdl_trigger();  // the next blend's planner may start (it only reads nodes)
+    pdl_wait();
+    int nb = 0, nns = 0, noof = 0;
+    exc_run<MODE>(L, stage[threadIdx.x >> 5], nb, nns, noof);
+    exc_accumulate<MODE>(L, nb, nns, noof, red);
+    if (threadIdx.x == 0) {
         __threadfence();
         last = atomicAdd(L.exc_done, 1u) == gridDim.x - 1;
     }
@@ -868,19 +953,46 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
     // the last CTA finalises BlendStats and restores the per-context state
     if (last && threadIdx.x == 0) {
         __threadfence();
-        if (MODE != 1) {
-            volatile unsigned long long* acc = L.acc;
-            if (L.stats_out) {
-                L.stats_out[0] = L.footprint;
-                L.stats_out[1] = acc[0];
-                L.stats_out[2] = acc[1];
-                L.stats_out[3] = acc[2];
-            }
-            acc[0] = acc[1] = acc[2] = 0;
-        }
-        if (L.exc_last) *L.exc_last = cnt;
-        *L.exc_count = 0;
+        exc_finalize<MODE>(L);
         *L.exc_done = 0;
+    }
+}
+
+// Exact pass of a batched blend: the queued pixels of all frames spread over
+// all warps (one warp per pixel; counts go straight to each frame's counters),
+// then the last CTA finalises every frame's BlendStats.
+template <int MODE>
+__global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions_batch(const NfBatchFrame* __restrict__ F, int nf) {
+    __shared__ unsigned pre[17];  // prefix sums of the queue lengths (nf <= 16)
+    __shared__ bool last;
+    __shared__ double stage[EXC_THREADS / 32][32 * 6];
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        pre[0] = 0u;
+        for (int f = 0; f < nf; ++f) pre[f + 1] = pre[f] + min(*F[f].L.exc_count, F[f].L.exc_cap);
+    }
+    __syncthreads();
+    const unsigned total = pre[nf];
+    const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (EXC_THREADS / 32);
+    for (unsigned i = gw; i < total; i += nwarps) {
+        int f = 0;
+        while (i >= pre[f + 1]) ++f;
+        const NodeFieldLaunch& L = F[f].L;
+        const int r = exc_pixel<MODE>(L, i - pre[f], stage[threadIdx.x >> 5]);
+        if (MODE != 1 && r >= 0) atomicAdd(&L.acc[r], 1ull);
+    }
+    __syncthreads();
+    unsigned* done = F[0].L.exc_done;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        for (int f = 0; f < nf; ++f) exc_finalize<MODE>(F[f].L);
+        *done = 0;
     }
 }
 
@@ -1044,6 +1156,61 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
     }
     prof_mark("k_node_exceptions", st);
     const cudaError_t e = launch_pdl(k_exc, dim3(EXC_BLOCKS), dim3(EXC_THREADS), 0, st, L);
+    ++*launches;
+    return e;
+}
+
+size_t node_field_batch_scratch_bytes(int nf) {
+    return (((size_t)nf * sizeof(NfBatchFrame) + 255) & ~size_t(255)) + (size_t)NF_CHUNK_TILES * sizeof(NfPlan);
+}
+
+cudaError_t launch_node_field_batch(const NodeFieldLaunch* Ls, int nf, void* scratch, cudaStream_t st,
+                                    int64_t* launches) {
+    std::vector<NfBatchFrame> F((size_t)nf);
+    int tiles = 0, ctas = 0;
+    for (int f = 0; f < nf; ++f) {
+        const NfGeom g = nf_geom(Ls[f]);
+        if (g.nchunks > 1 || Ls[f].n >= kPrefilterMinNodes) return cudaErrorNotSupported;
+        NfBatchFrame& fr = F[f];
+        fr.L = Ls[f];
+        fr.L.chunk_rows = g.chunk_rows;
+        fr.L.tile_j0 = g.tj0;
+        fr.L.band_s1 = g.s1;
+        fr.L.lists = nullptr;
+        fr.ti0 = g.ti0;
+        fr.tj0 = g.tj0;
+        fr.tj1 = g.tj1;
+        fr.s1 = g.s1;
+        fr.ntx = g.nchunks ? g.ntx : 0;
+        fr.rows = g.nchunks ? g.nty : 0;
+        fr.plan_off = tiles;
+        fr.cta_off = ctas;
+        tiles += fr.rows * fr.ntx;
+        ctas += fr.rows * fr.ntx * K1Shape<0>::NH;
+    }
+    if (tiles > NF_CHUNK_TILES) return cudaErrorNotSupported;
+    NfBatchFrame* dF = static_cast<NfBatchFrame*>(scratch);
+    NfPlan* plans = reinterpret_cast<NfPlan*>(static_cast<char*>(scratch) +
+                                              (((size_t)nf * sizeof(NfBatchFrame) + 255) & ~size_t(255)));
+    cudaError_t e = cudaMemcpyAsync(dF, F.data(), (size_t)nf * sizeof(NfBatchFrame), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return e;
+    if (tiles > 0) {
+        prof_mark("k_nf_plan", st);
+        e = launch_pdl(k_nf_plan_batch, dim3((tiles + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS), dim3(NF_PLAN_WARPS * 32),
+                       0, st, static_cast<const NfBatchFrame*>(dF), nf, plans, tiles);
+        ++*launches;
+        if (e != cudaSuccess) return e;
+        const size_t smem = ((sizeof(Smem<K1Shape<0>::CW>) + 15) & ~size_t(15)) + sizeof(CanvasTile);
+        cudaFuncSetAttribute(k_node_field_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        prof_mark("k_node_field", st);
+        e = launch_pdl(k_node_field_batch<0>, dim3(ctas), dim3(NT), smem, st, static_cast<const NfBatchFrame*>(dF),
+                       nf, static_cast<const NfPlan*>(plans));
+        ++*launches;
+        if (e != cudaSuccess) return e;
+    }
+    prof_mark("k_node_exceptions", st);
+    e = launch_pdl(k_node_exceptions_batch<0>, dim3(EXC_BLOCKS), dim3(EXC_THREADS), 0, st,
+                   static_cast<const NfBatchFrame*>(dF), nf);
     ++*launches;
     return e;
 }

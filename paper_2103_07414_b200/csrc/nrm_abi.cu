@@ -566,7 +566,7 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     cudaStreamSynchronize(c->stream);
     DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc,   &c->misc,  &c->stats, &c->pts,
                       &c->locals,    &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles, &c->feat,
-                      &c->feat_io};
+                      &c->feat_io,   &c->batch};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();
@@ -857,6 +857,131 @@ int nrm_blend_frame_weighted_device(nrm_canvas* cv, const uint8_t* d_frame, int 
                                     const double* poly, int npoly, const float* d_unc, int64_t* d_stats) {
     if (!d_unc && fw > 0 && fh > 0) return fail(NRM_EINVAL, "blend_frame_weighted: null uncertainty map");
     return blend_device(cv, d_frame, fw, fh, ch, d_anchors, d_warps, n, alpha, poly, npoly, d_unc, d_stats);
+}
+
+// ---- several frames per call ------------------------------------------------
+int nrm_blend_frames_device(nrm_canvas* cv, int nf, const uint8_t* const* d_frames, int fw, int fh, int ch,
+                            const double* const* d_anchors, const double* const* d_warps, const int* n, double alpha,
+                            const double* const* polys, const int* npoly, int64_t* d_stats) {
+    NRM_CHECK(check_canvas(cv));
+    if (nf < 0) return fail(NRM_EINVAL, "blend_frames: negative frame count");
+    if (nf == 0) return NRM_OK;
+    if (!d_frames || !d_anchors || !d_warps || !n || !polys || !npoly || !d_stats)
+        return fail(NRM_EINVAL, "blend_frames: null array");
+    if (fw < 0 || fh < 0) return fail(NRM_EINVAL, "negative frame size");
+    nrm_ctx* c = cv->ctx;
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    auto* stats = reinterpret_cast<unsigned long long*>(d_stats);
+    // the reference's per-frame checks and canvas growth, in frame order
+    struct Win {
+        bool active;
+        int i0, j0, i1, j1;
+    };
+    std::vector<Win> win((size_t)nf, Win{false, 0, 0, 0, 0});
+    for (int f = 0; f < nf; ++f) {
+        NRM_CHECK(validate_nodes(d_anchors[f], d_warps[f], n[f], alpha, false));
+        if (fw <= 0 || fh <= 0 || npoly[f] < 3) continue;
+        if (ch != 1 && ch != 3 && ch != 4) return fail(NRM_EINVAL, "frame channels must be 1, 3 or 4");
+        if (!d_frames[f] || !polys[f]) return fail(NRM_EINVAL, "null frame or polygon");
+        if (!finite_all(polys[f], (size_t)npoly[f] * 2)) return fail(NRM_EINVAL, "blend_frame: non-finite polygon");
+        const Bbox bb = footprint_bbox(polys[f], npoly[f]);
+        NRM_CHECK(ensure_contains(cv, bb.x0, bb.y0, bb.x1, bb.y1));
+        // absolute pixel window (origins are integers, so this equals
+        // blend_frame's window whatever the canvas grows to later)
+        const double orgx = (double)cv->origin_x, orgy = (double)cv->origin_y;
+        Win& w = win[f];
+        w.i0 = (int)(cv->origin_x + (int64_t)std::floor(bb.x0 - orgx));
+        w.j0 = (int)(cv->origin_y + (int64_t)std::floor(bb.y0 - orgy));
+        w.i1 = (int)(cv->origin_x + (int64_t)std::ceil(bb.x1 - orgx));
+        w.j1 = (int)(cv->origin_y + (int64_t)std::ceil(bb.y1 - orgy));
+        w.active = w.i1 >= w.i0 && w.j1 >= w.j0;
+    }
+    // pairwise disjoint footprints: the order of the updates does not matter
+    std::vector<int> act;
+    bool disjoint = true;
+    for (int f = 0; f < nf; ++f) {
+        if (!win[f].active) continue;
+        for (int e : act)
+            if (!(win[f].i1 < win[e].i0 || win[e].i1 < win[f].i0 || win[f].j1 < win[e].j0 || win[e].j1 < win[f].j0))
+                disjoint = false;
+        act.push_back(f);
+    }
+    auto sequential = [&]() -> int {
+        for (int f = 0; f < nf; ++f)
+            NRM_CHECK(blend_core(cv, d_frames[f], fw, fh, ch, d_anchors[f], d_warps[f], n[f], alpha, polys[f],
+                                 npoly[f], stats + 4 * f));
+        return NRM_OK;
+    };
+    if (!disjoint || act.size() < 2 || act.size() > 16) return sequential();
+    // per-frame counters (acc[3] u64 | exc_count u32 | pad), persistent-zero
+    const size_t nact = act.size();
+    const size_t need = nact * 32;
+    if (c->batch.cap < need) {
+        NRM_CUDA(c->batch.ensure(need));
+        NRM_CUDA(cudaMemsetAsync(c->batch.p, 0, c->batch.cap, c->stream));
+    }
+    const State st = state_of(c);
+    std::vector<size_t> cap(nact);
+    size_t qtot = 0;
+    for (size_t a = 0; a < nact; ++a) {
+        const Win& w = win[act[a]];
+        const unsigned long long fp = (unsigned long long)(w.i1 - w.i0 + 1) * (unsigned long long)(w.j1 - w.j0 + 1);
+        cap[a] = std::min<size_t>(fp, (size_t)1 << 24);
+        qtot += cap[a];
+    }
+    NRM_CUDA(c->exc.ensure(qtot * sizeof(int2) + 64));
+    std::vector<NodeFieldLaunch> Ls(nact);
+    size_t qoff = 0;
+    for (size_t a = 0; a < nact; ++a) {
+        const int f = act[a];
+        const Win& w = win[f];
+        NodeFieldLaunch& L = Ls[a];
+        L.frame = d_frames[f];
+        L.fw = fw;
+        L.fh = fh;
+        L.fch = ch;
+        L.anchors = d_anchors[f];
+        L.warps = d_warps[f];
+        L.n = n[f];
+        L.alpha = alpha;
+        L.grid.gx = 0.0;
+        L.grid.gy = 0.0;
+        L.grid.i0 = w.i0;
+        L.grid.i1 = w.i1;
+        L.grid.j0 = w.j0;
+        L.grid.j1 = w.j1;
+        L.R = cv->r;
+        L.G = cv->g;
+        L.B = cv->b;
+        L.W = cv->w;
+        L.pitch = cv->cap_w;
+        L.phys_x0 = (int)cv->phys_x0;
+        L.phys_y0 = (int)cv->phys_y0;
+        L.band_rank = cv->band_rank;
+        L.band_count = cv->band_count;
+        char* fb = c->batch.as<char>() + 32 * a;
+        L.acc = reinterpret_cast<unsigned long long*>(fb);
+        L.exc_count = reinterpret_cast<unsigned*>(fb + 24);
+        L.stats_out = stats + 4 * f;
+        L.footprint = (unsigned long long)(w.i1 - w.i0 + 1) * (unsigned long long)(w.j1 - w.j0 + 1);
+        L.exc = c->exc.as<int2>() + qoff;
+        L.exc_cap = (unsigned)cap[a];
+        L.exc_overflow = st.overflow;
+        L.exc_last = st.last_exc;
+        L.exc_done = st.exc_done;
+        qoff += cap[a];
+    }
+    NRM_CUDA(c->tiles.ensure(node_field_batch_scratch_bytes((int)nact)));
+    const cudaError_t e = launch_node_field_batch(Ls.data(), (int)nact, c->tiles.p, c->stream, &c->launches);
+    if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        return sequential();
+    }
+    NRM_CUDA(e);
+    for (int f = 0; f < nf; ++f)
+        if (!win[f].active) NRM_CUDA(cudaMemsetAsync(stats + 4 * f, 0, 4 * sizeof(unsigned long long), c->stream));
+    return NRM_OK;
 }
 
 // ---- render ----------------------------------------------------------------

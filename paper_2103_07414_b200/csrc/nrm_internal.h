@@ -54,7 +54,7 @@ struct nrm_ctx {
     int num_sms = 148;
     // scratch (grow-only)
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
-        active, out_a, out_b, tiles, feat, feat_io;
+        active, out_a, out_b, tiles, feat, feat_io, batch;
     nrm::PinnedBuf staging, staging_out;
     nrm::Prof prof;
 };
@@ -149,6 +149,14 @@ size_t node_field_scratch_bytes(const NodeFieldLaunch& L);
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches);
+// Blends of several frames whose footprints are pairwise disjoint, in one
+// planner / field / exception launch each (reference rule, frame lattices of
+// fewer than 257 nodes, all tiles in one plan chunk; otherwise
+// cudaErrorNotSupported and the caller blends frame by frame). Each Ls[f]
+// carries its own exception queue, counters and stats_out.
+size_t node_field_batch_scratch_bytes(int nf);
+cudaError_t launch_node_field_batch(const NodeFieldLaunch* Ls, int nf, void* scratch, cudaStream_t st,
+                                    int64_t* launches);
 cudaError_t launch_pixel_warp_points(const double* pts, int npts, const double* anchors,
                                      const double* warps, int n, double alpha, double* out,
                                      uint8_t* valid, cudaStream_t st, int64_t* launches);

@@ -298,6 +298,27 @@ def blend_frame_device(canvas: Canvas, frame_t, fw: int, fh: int, ch: int, ancho
                                                           _ptr(p), len(p), _tptr(unc_t), _tptr(stats_t)))
 
 
+def blend_frames_device(canvas: Canvas, frames_t, fw: int, fh: int, ch: int, anchors_t, warps_t, alpha: float,
+                        polygons, stats_t) -> None:
+    """blend_frame for several same-size frames in order (lists of device
+    tensors; stats_t int64 (nf, 4) on the device), async. Frames with
+    pairwise disjoint footprints share one planner / field / exception
+    launch; the results equal len(frames_t) blend_frame_device calls."""
+    nf = len(frames_t)
+    if not (len(anchors_t) == len(warps_t) == len(polygons) == nf):
+        raise ValueError("blend_frames: one anchors / warps / polygon per frame")
+    polys = [_f64(p, 2, "footprint_polygon") for p in polygons]
+    P = C.c_void_p
+    fr = (P * nf)(*[_tptr(t) for t in frames_t])
+    an = (P * nf)(*[_tptr(t) for t in anchors_t])
+    wa = (P * nf)(*[_tptr(t) for t in warps_t])
+    nn = (C.c_int * nf)(*[int(t.shape[0]) for t in anchors_t])
+    pp = (P * nf)(*[_ptr(p) for p in polys])
+    npo = (C.c_int * nf)(*[len(p) for p in polys])
+    check(canvas._lib.nrm_blend_frames_device(canvas.handle, nf, fr, fw, fh, ch, an, wa, nn, float(alpha), pp, npo,
+                                              _tptr(stats_t)))
+
+
 def render(canvas: Canvas, crop: bool = False):
     """render (mosaic.hpp:301-331) -> (RGBA uint8 (h, w, 4), crop origin (x, y))."""
     w, h = C.c_int(), C.c_int()

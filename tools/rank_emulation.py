@@ -1,6 +1,7 @@
 """Per-rank work of bench.py's weak-scaling step at G GPUs, on one GPU: one
-EMDQ field (K3) plus G frame blends into band 0 of G (K1), streams as in the
-bench. Estimates the per-rank step time without the collectives.
+EMDQ field (K3) plus G frame blends into band 0 of G (K1; the G frames lie in
+disjoint canvas lanes and go through one batched blend call), streams as in
+the bench. Estimates the per-rank step time without the collectives.
     python tools/rank_emulation.py [G ...]"""
 import json
 import sys
@@ -22,7 +23,9 @@ for G in Gs:
     ctx, ctx_b = M.Context(0), M.Context(0)
     ctx.set_stream(sa.cuda_stream)
     ctx_b.set_stream(sb.cuda_stream)
-    shifts = [k * fw for k in range(G)]
+    p0 = M.invert_frame_boundary(fw, fh, wl.anchors, wl.warps, alpha, ctx=ctx)
+    lane_w = float(np.ceil(p0[:, 0].max() - p0[:, 0].min()) + 64.0)  # bench.py: frames in disjoint lanes
+    shifts = [k * lane_w for k in range(G)]
     anc = [T(wl.anchors + np.array([s, 0.0])) for s in shifts]
     war = [T(W.shifted_warps(wl.warps, s, 0.0)) for s in shifts]
     polys = [M.invert_frame_boundary(fw, fh, wl.anchors + np.array([s, 0.0]), W.shifted_warps(wl.warps, s, 0.0),
@@ -43,8 +46,10 @@ for G in Gs:
         e0.record(sa)
         sb.wait_event(e0)
         M.emdq_field_device((0.0, 0.0, fw, fh), apts, loc, prob, act, alpha, beta, disp, unc, 16, ctx=ctx)
-        for k in range(G):
-            M.blend_frame_device(cv, frame_t, fw, fh, 3, anc[k], war[k], alpha, polys[k], st[k])
+        if G == 1:
+            M.blend_frame_device(cv, frame_t, fw, fh, 3, anc[0], war[0], alpha, polys[0], st[0])
+        else:
+            M.blend_frames_device(cv, [frame_t] * G, fw, fh, 3, anc, war, alpha, polys, st)
         e1 = torch.cuda.Event()
         e1.record(sb)
         sa.wait_event(e1)
