@@ -117,6 +117,15 @@ class BandedMosaic:
             reduce_stats(stats_t)
         return stats_t
 
+    def blend_frames(self, frames_t, fw, fh, ch, anchors_t, warps_t, alpha, polys, stats_t):
+        """Blends several (replicated) frames in order into this rank's stripes
+        in one batched call when their footprints are disjoint
+        (mosaic.blend_frames_device); stats_t (nf, 4) is all-reduced."""
+        self.M.blend_frames_device(self.canvas, frames_t, fw, fh, ch, anchors_t, warps_t, alpha, polys, stats_t)
+        if self.world > 1:
+            reduce_stats(stats_t)
+        return stats_t
+
     def render(self, crop: bool = False, dst: int = 0):
         """render(canvas, crop) assembled on rank `dst` -> (rgba numpy, origin)."""
         import torch
