@@ -978,14 +978,11 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         const float worst = sd[MS > 0 ? MS - 1 : 0];
         // near-tie between the last member and the first rejected key
         if (rej < FLT_MAX && !(rej - worst > d2_tol(rej))) exact = true;
-        // m is warp-uniform: a real loop, not MS predicated takes
-        for (int q = MS - m; q < MS; ++q) {
-            int k = sk[0];
+        // the members sit in the top m slots; m is warp-uniform, so these
+        // branches do not diverge and no register selection is needed
 #pragma unroll
-            for (int u = 1; u < (MS > 0 ? MS : 1); ++u)
-                if (q == u) k = sk[u];
-            take(k);
-        }
+        for (int q = 0; q < MS; ++q)
+            if (q >= MS - m) take(sk[q]);
     } else if (MS == 0 && m > 0) {
         // many free slots (rare): repeated minimum selection; pass m + 1
         // finds the first rejected key for the near-tie test
