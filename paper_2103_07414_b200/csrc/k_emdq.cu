@@ -914,6 +914,11 @@ __device__ __forceinline__ double fast_bounded_exp(double x) {
     return p * __hiloint2double((int)(n + 1023.0) << 20, 0);
 }
 
+#ifndef NRM_PIX_UNROLL
+#define NRM_PIX_UNROLL 4
+#endif
+constexpr int kPixUnroll = NRM_PIX_UNROLL;  // member-accumulation loops of k_pixels
+
 // Bound on |FP32 d^2 - exact d^2| for tile-local coordinates.
 __device__ __forceinline__ float d2_tol(float d2) { return 2e-6f * d2 + 2e-3f; }
 
@@ -932,8 +937,9 @@ __device__ __forceinline__ void fast_pixel(int col, int row, int nin, const unsi
         a4 = fmaf(w, p.rec0[k].w, a4);
         a5 += w;
     };
-#pragma unroll 4
+#pragma unroll (kPixUnroll)
     for (int k = 0; k < nin; ++k) take(k);
+#pragma unroll (kPixUnroll)
     for (int e = 0; e < nxin; ++e) take(wl[e]);
     bool exact = false;
     const float ux = (float)col, uy = (float)row;
