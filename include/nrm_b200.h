@@ -79,7 +79,8 @@ const char *nrm_last_error(void);
 /* Creates a context on CUDA device `device` with its own non-blocking stream. */
 int nrm_ctx_create(int device, nrm_ctx **out);
 int nrm_ctx_destroy(nrm_ctx *ctx);
-/* Enqueue subsequent work on an external cudaStream_t (NULL = own stream). */
+/* Enqueue subsequent work on an external cudaStream_t (NULL = own stream;
+ * the legacy default stream is cudaStreamLegacy, (void *)0x1). */
 int nrm_ctx_set_stream(nrm_ctx *ctx, void *cuda_stream);
 void *nrm_ctx_stream(nrm_ctx *ctx);
 int nrm_ctx_synchronize(nrm_ctx *ctx);
@@ -117,10 +118,22 @@ int nrm_canvas_upload(nrm_canvas *cv, int x, int y, int w, int h, const double *
  * in canvas pixels (e.g. a dense field from nrm_node_field / nrm_emdq_field).
  * Bilinear in FP64 over the occupied taps (weights renormalised), weight of
  * the nearest occupied tap; sources outside the canvas or without occupied
- * taps leave the pixel unoccupied. d == 0 is a bit-exact no-op. Single-band
- * canvases only (a banded canvas would need a halo exchange). */
+ * taps leave the pixel unoccupied. d == 0 is a bit-exact no-op.
+ * On a banded canvas (nrm_canvas_set_band) only the rows this rank owns are
+ * deformed; their sources must be current, i.e. rows within ceil(max |d_y|)+1
+ * of an owned row that other ranks own must first be brought in with
+ * nrm_canvas_pack_rows_device / nrm_canvas_unpack_rows_device (the halo
+ * exchange, paper_2103_07414_b200/dist.py). Regions of a quarter of the canvas
+ * or more run as one ping-pong pass over the canvas (a second set of planes
+ * is allocated on first use). */
 int nrm_canvas_deform(nrm_canvas *cv, int x, int y, int w, int h, const float *disp);
 int nrm_canvas_deform_device(nrm_canvas *cv, int x, int y, int w, int h, const float *d_disp);
+/* Halo rows of banded canvases: rows[nrows] (host array of
+ * logical canvas rows) across the full canvas width, packed into / unpacked
+ * from device memory d_buf as 13 * width bytes per row (R, G, B float32
+ * planes, then the uint8 weight). Asynchronous on the context stream. */
+int nrm_canvas_pack_rows_device(nrm_canvas *cv, const int *rows, int nrows, void *d_buf);
+int nrm_canvas_unpack_rows_device(nrm_canvas *cv, const int *rows, int nrows, const void *d_buf);
 /* Canvas::occupied_count (mosaic.hpp:123-127). */
 int nrm_canvas_occupied_count(nrm_canvas *cv, int64_t *out);
 
@@ -318,6 +331,14 @@ int nrm_selftest_libm(nrm_ctx *ctx, const double *x, const double *y, int n, dou
  * in the exact tier, and pixels of the last emdq_field that took the exact
  * tier. Synchronises the context stream. */
 int nrm_ctx_exceptions(nrm_ctx *ctx, int64_t *blend_exceptions, int64_t *emdq_exact);
+/* Exception-queue slots per launch (0 = default: 1/64 of the launch's
+ * pixels, at least 2^18). Deferred pixels past the capacity are never lost:
+ * they are marked in the output and resolved by a scan in the exact pass, so
+ * results do not depend on this value (tests force tiny queues with it). */
+int nrm_ctx_set_exception_capacity(nrm_ctx *ctx, int64_t slots);
+/* Number of launches on this context whose exception queue overflowed into
+ * the scan path (diagnostics; synchronises the context stream). */
+int nrm_ctx_spilled_launches(nrm_ctx *ctx, int64_t *out);
 /* Measured pipe throughput on this device, lane-operations per second:
  * which = 0: FP32 FFMA, which = 1: MUFU.EX2 (roofline denominators). */
 int nrm_selftest_peak(nrm_ctx *ctx, int which, double *ops_per_s);

@@ -207,12 +207,26 @@ static double sample_bilinear_f32(const float *m, int w, int h, double x, double
 
 static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
                             const double *anchors, const double *warps, int n, double alpha,
-                            const double *poly, int npoly, const float *unc, int64_t *stats);
+                            const double *poly, int npoly, const float *unc, int band_rank,
+                            int band_count, int64_t *stats);
 
 int orc_blend_frame(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
                     const double *anchors, const double *warps, int n, double alpha,
                     const double *poly, int npoly, int64_t *stats) {
-    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, NULL, stats);
+    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, NULL, 0, 1, stats);
+}
+
+/* Multi-GPU restatement (nrm_canvas_set_band): blend_frame
+ * restricted to the canvas rows of block-cyclic 64-row stripes
+ * floor(y / 64) mod band_count == band_rank (absolute reference rows).
+ * footprint_pixels is the whole window (the same on every rank); the other
+ * counts cover the owned rows only, so they sum to the reference's over the
+ * ranks. band_count = 1 is orc_blend_frame. */
+int orc_blend_frame_band(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                         const double *anchors, const double *warps, int n, double alpha,
+                         const double *poly, int npoly, int band_rank, int band_count, int64_t *stats) {
+    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, NULL, band_rank,
+                            band_count, stats);
 }
 
 /* Extension (not in the reference): the uncertainty-weighted update of
@@ -220,12 +234,21 @@ int orc_blend_frame(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch
 int orc_blend_frame_weighted(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
                              const double *anchors, const double *warps, int n, double alpha,
                              const double *poly, int npoly, const float *unc, int64_t *stats) {
-    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, unc, stats);
+    return blend_frame_impl(cv, frame, fw, fh, ch, anchors, warps, n, alpha, poly, npoly, unc, 0, 1, stats);
+}
+
+static int band_owns(int64_t abs_row, int band_rank, int band_count) {
+    if (band_count <= 1) return 1;
+    int64_t s = abs_row >= 0 ? abs_row / 64 : -((-abs_row + 63) / 64);
+    int64_t m = s % band_count;
+    if (m < 0) m += band_count;
+    return m == band_rank;
 }
 
 static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
                             const double *anchors, const double *warps, int n, double alpha,
-                            const double *poly, int npoly, const float *unc, int64_t *stats) {
+                            const double *poly, int npoly, const float *unc, int band_rank,
+                            int band_count, int64_t *stats) {
     stats[0] = stats[1] = stats[2] = stats[3] = 0;
     if (fw == 0 || fh == 0 || npoly < 3) return 0;
 
@@ -268,6 +291,7 @@ static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh
     for (int ry = 0; ry < bh; ++ry) {
         const int cy = py0 + ry;
         const double ref_y = orgy + cy;
+        if (!band_owns(cv->origin_y + cy, band_rank, band_count)) continue;
         for (int tx = 0; tx < ntx; ++tx) {
             const int *nodes = &tile_nodes[(size_t)tx * n];
             const int nn = tile_count[tx];

@@ -54,6 +54,10 @@ void orc_warp_apply(const double *warp5, double px, double py, double *out2);
 int orc_blend_frame(orc_canvas *c, const uint8_t *frame, int fw, int fh, int ch,
                     const double *anchors, const double *warps, int n, double alpha,
                     const double *poly, int npoly, int64_t *stats);
+/* blend_frame restricted to block-cyclic 64-row stripes (nrm_canvas_set_band). */
+int orc_blend_frame_band(orc_canvas *cv, const uint8_t *frame, int fw, int fh, int ch,
+                         const double *anchors, const double *warps, int n, double alpha,
+                         const double *poly, int npoly, int band_rank, int band_count, int64_t *stats);
 
 /* render (mosaic.hpp:301-331). Two-phase: call with out == NULL to get the size
  * (out_w, out_h; 0x0 when empty) and crop origin; then with a w*h*4 buffer. */

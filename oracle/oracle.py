@@ -57,6 +57,7 @@ class Oracle:
         L.orc_warp_apply.argtypes = [_P, _D, _D, _P]
         L.orc_blend_frame.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P]
         L.orc_blend_frame_weighted.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _P]
+        L.orc_blend_frame_band.argtypes = [_P, _P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _I, _I, _P]
         L.orc_canvas_deform.argtypes = [_P, _I, _I, _I, _I, _P]
         L.orc_render.argtypes = [_P, _I, _P, _P, _P, _P]
         L.orc_invert_frame_boundary.argtypes = [_I, _I, _P, _P, _I, _D, _D, _P, _I]
@@ -133,15 +134,20 @@ class Oracle:
         self.L.orc_warp_apply(_p(w), float(x), float(y), _p(out))
         return out
 
-    def blend_frame(self, canvas, frame, anchors, warps, alpha, poly):
+    def blend_frame(self, canvas, frame, anchors, warps, alpha, poly, band=None):
+        """band=(rank, count): the restatement of one rank of a banded canvas."""
         f = np.ascontiguousarray(frame, np.uint8)
         if f.ndim == 2:
             f = f[:, :, None]
         h, w, c = f.shape
         a, q, p = _f64(anchors, 2), _f64(warps, 5), _f64(poly, 2)
         st = np.zeros(4, np.int64)
-        rc = self.L.orc_blend_frame(canvas.h, _p(f), w, h, c, _p(a), _p(q), len(a), float(alpha), _p(p),
-                                    len(p), _p(st))
+        if band is not None:
+            rc = self.L.orc_blend_frame_band(canvas.h, _p(f), w, h, c, _p(a), _p(q), len(a), float(alpha), _p(p),
+                                             len(p), int(band[0]), int(band[1]), _p(st))
+        else:
+            rc = self.L.orc_blend_frame(canvas.h, _p(f), w, h, c, _p(a), _p(q), len(a), float(alpha), _p(p),
+                                        len(p), _p(st))
         if rc:
             raise MemoryError("oracle blend_frame")
         return tuple(int(v) for v in st)

@@ -88,6 +88,8 @@ SIGNATURES = [
     ("nrm_canvas_upload", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P, _P]),
     ("nrm_canvas_deform", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
     ("nrm_canvas_deform_device", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _P]),
+    ("nrm_canvas_pack_rows_device", C.c_int, [_P, _P, C.c_int, _P]),
+    ("nrm_canvas_unpack_rows_device", C.c_int, [_P, _P, C.c_int, _P]),
     ("nrm_canvas_occupied_count", C.c_int, [_P, _I64]),
     ("nrm_blend_frame", C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double,
                                   _P, C.c_int, C.POINTER(BlendStats)]),
@@ -124,6 +126,8 @@ SIGNATURES = [
     ("nrm_selftest_libm", C.c_int, [_P, _P, _P, C.c_int, _P, _P]),
     ("nrm_selftest_peak", C.c_int, [_P, C.c_int, _D]),
     ("nrm_ctx_exceptions", C.c_int, [_P, _I64, _I64]),
+    ("nrm_ctx_set_exception_capacity", C.c_int, [_P, C.c_int64]),
+    ("nrm_ctx_spilled_launches", C.c_int, [_P, _I64]),
     ("nrm_ctx_profile", C.c_int, [_P, C.c_int]),
     ("nrm_ctx_profile_read", C.c_int, [_P, C.c_char_p, C.c_int, _P, _P, C.c_int, _I]),
     ("nrm_plan_ensure_contains", C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,

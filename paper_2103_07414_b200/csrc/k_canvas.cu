@@ -2,6 +2,7 @@
 // host-mirror transfers behind Canvas::color()/weight() (mosaic.hpp:111-120).
 // All are HBM-bound streaming kernels: one pixel per thread, coalesced rows.
 #include <cmath>
+#include <utility>
 
 #include "nrm_common.cuh"
 #include "nrm_internal.h"
@@ -45,24 +46,30 @@ CanvasView view_of(const nrm_canvas* cv) {
     return v;
 }
 
+// Rows are walked grid-stride over gridDim.y (<= 65535), so canvases of any
+// height (up to the 2^30 rows ensure_contains allows) launch.
+constexpr int kMaxGridY = 65535;
+inline int grid_y(int h) { return h < kMaxGridY ? h : kMaxGridY; }
+
 __global__ void k_render(CanvasView v, int x0, int y0, int w, int h, uchar4* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
     if (i >= w) return;
-    const int x = x0 + i, y = y0 + j;
-    uchar4 px = make_uchar4(0, 0, 0, 0);
-    if (owns_row(v, y)) {
-        const long long idx = (v.oy + y) * v.pitch + (v.ox + x);
-        if (v.w[idx] > 0) {
-            auto q = [](float c) -> unsigned char {
-                double d = (double)c;
-                d = d < 0.0 ? 0.0 : (1.0 < d ? 1.0 : d);  // std::clamp(c, 0, 1)
-                return (unsigned char)lround(d * 255.0);
-            };
-            px = make_uchar4(q(v.r[idx]), q(v.g[idx]), q(v.b[idx]), 255);
+    for (int j = blockIdx.y; j < h; j += gridDim.y) {
+        const int x = x0 + i, y = y0 + j;
+        uchar4 px = make_uchar4(0, 0, 0, 0);
+        if (owns_row(v, y)) {
+            const long long idx = (v.oy + y) * v.pitch + (v.ox + x);
+            if (v.w[idx] > 0) {
+                auto q = [](float c) -> unsigned char {
+                    double d = (double)c;
+                    d = d < 0.0 ? 0.0 : (1.0 < d ? 1.0 : d);  // std::clamp(c, 0, 1)
+                    return (unsigned char)lround(d * 255.0);
+                };
+                px = make_uchar4(q(v.r[idx]), q(v.g[idx]), q(v.b[idx]), 255);
+            }
         }
+        out[(size_t)j * w + i] = px;
     }
-    out[(size_t)j * w + i] = px;
 }
 
 // count[0] = occupied pixels; bbox4 = {minx, miny, maxx, maxy} (atomics; init by caller).
@@ -117,32 +124,71 @@ __global__ void __launch_bounds__(256) k_occupied(CanvasView v, int w, int h, un
 __global__ void k_canvas_read(CanvasView v, int x0, int y0, int w, int h, double* __restrict__ rgb,
                               uint8_t* __restrict__ wout) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
     if (i >= w) return;
-    const long long idx = (v.oy + y0 + j) * v.pitch + (v.ox + x0 + i);
-    const size_t o = (size_t)j * w + i;
-    if (rgb) {
-        rgb[3 * o] = v.r[idx];
-        rgb[3 * o + 1] = v.g[idx];
-        rgb[3 * o + 2] = v.b[idx];
+    for (int j = blockIdx.y; j < h; j += gridDim.y) {
+        const long long idx = (v.oy + y0 + j) * v.pitch + (v.ox + x0 + i);
+        const size_t o = (size_t)j * w + i;
+        if (rgb) {
+            rgb[3 * o] = v.r[idx];
+            rgb[3 * o + 1] = v.g[idx];
+            rgb[3 * o + 2] = v.b[idx];
+        }
+        if (wout) wout[o] = v.w[idx];
     }
-    if (wout) wout[o] = v.w[idx];
 }
 
 __global__ void k_canvas_write(float* r, float* g, float* b, uint8_t* wp, long long pitch, long long ox,
                                long long oy, int x0, int y0, int w, int h,
                                const double* __restrict__ rgb, const uint8_t* __restrict__ win) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
     if (i >= w) return;
-    const long long idx = (oy + y0 + j) * pitch + (ox + x0 + i);
-    const size_t o = (size_t)j * w + i;
-    if (rgb) {
-        r[idx] = (float)rgb[3 * o];
-        g[idx] = (float)rgb[3 * o + 1];
-        b[idx] = (float)rgb[3 * o + 2];
+    for (int j = blockIdx.y; j < h; j += gridDim.y) {
+        const long long idx = (oy + y0 + j) * pitch + (ox + x0 + i);
+        const size_t o = (size_t)j * w + i;
+        if (rgb) {
+            r[idx] = (float)rgb[3 * o];
+            g[idx] = (float)rgb[3 * o + 1];
+            b[idx] = (float)rgb[3 * o + 2];
+        }
+        if (win) wp[idx] = win[o];
     }
-    if (win) wp[idx] = win[o];
+}
+
+// Halo rows for banded canvases: canvas rows rows[k] (logical
+// canvas coordinates), all logical columns, packed as per-row SoA
+// {R[w], G[w], B[w]} float32 followed by W[w] uint8 -> 13 w bytes per row.
+// Rows start on 16-byte boundaries of the physical planes (origins and the
+// pitch are multiples of 256 px), so one thread moves 4 pixels with float4 /
+// uchar4 accesses.
+__global__ void __launch_bounds__(256) k_rows_pack(CanvasView v, const int* __restrict__ rows, int nrows, int w,
+                                                   unsigned char* __restrict__ buf) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;  // quad index in the row
+    if (4 * q >= w) return;
+    const size_t row_bytes = (size_t)13 * w;
+    for (int k = blockIdx.y; k < nrows; k += gridDim.y) {
+        const long long base = (v.oy + rows[k]) * v.pitch + v.ox + 4 * q;
+        float* fr = reinterpret_cast<float*>(buf + (size_t)k * row_bytes);
+        reinterpret_cast<float4*>(fr)[q] = *reinterpret_cast<const float4*>(v.r + base);
+        reinterpret_cast<float4*>(fr + w)[q] = *reinterpret_cast<const float4*>(v.g + base);
+        reinterpret_cast<float4*>(fr + 2 * w)[q] = *reinterpret_cast<const float4*>(v.b + base);
+        reinterpret_cast<uchar4*>(fr + 3 * w)[q] = *reinterpret_cast<const uchar4*>(v.w + base);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rows_unpack(float* r, float* g, float* b, uint8_t* wp, long long pitch,
+                                                     long long ox, long long oy, const int* __restrict__ rows,
+                                                     int nrows, int w, const unsigned char* __restrict__ buf) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (4 * q >= w) return;
+    const size_t row_bytes = (size_t)13 * w;
+    for (int k = blockIdx.y; k < nrows; k += gridDim.y) {
+        const long long base = (oy + rows[k]) * pitch + ox + 4 * q;
+        const float* fr = reinterpret_cast<const float*>(buf + (size_t)k * row_bytes);
+        *reinterpret_cast<float4*>(r + base) = reinterpret_cast<const float4*>(fr)[q];
+        *reinterpret_cast<float4*>(g + base) = reinterpret_cast<const float4*>(fr + w)[q];
+        *reinterpret_cast<float4*>(b + base) = reinterpret_cast<const float4*>(fr + 2 * w)[q];
+        *reinterpret_cast<uchar4*>(wp + base) = reinterpret_cast<const uchar4*>(fr + 3 * w)[q];
+    }
 }
 
 // Canvas deformation (extension, north_star; no
@@ -150,91 +196,226 @@ __global__ void k_canvas_write(float* r, float* g, float* b, uint8_t* wp, long l
 // FP64 with the taps of sample_bilinear_rgb (image.hpp:78-92) restricted to
 // occupied pixels (weights renormalised), weight from the nearest occupied
 // tap; a source outside the canvas or with no occupied tap leaves the pixel
-// unoccupied. d == 0 reproduces the canvas bit for bit. Output goes to
-// scratch planes (sources may lie anywhere in the canvas).
-__global__ void k_canvas_deform(CanvasView v, int W, int H, int x0, int y0, int w, int h,
-                                const float2* __restrict__ disp, float* __restrict__ outr, float* __restrict__ outg,
-                                float* __restrict__ outb, uint8_t* __restrict__ outw) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    if (i >= w) return;
-    const size_t o = (size_t)j * w + i;
-    const float2 d = disp[o];
-    const double sx = xadd((double)(x0 + i), (double)d.x), sy = xadd((double)(y0 + j), (double)d.y);
-    float cr = 0.f, cg = 0.f, cb = 0.f;
+// unoccupied. d == 0 reproduces the canvas bit for bit.
+struct Px {
+    float r, g, b;
+    uint8_t w;
+};
+__device__ __forceinline__ Px deform_sample(const CanvasView& v, int W, int H, int x, int y, float2 d) {
+    const double sx = xadd((double)x, (double)d.x), sy = xadd((double)y, (double)d.y);
+    Px o{0.f, 0.f, 0.f, 0};
+    if (!(sx >= 0.0 && sx <= W - 1.0 && sy >= 0.0 && sy <= H - 1.0)) return o;
+    int tx0 = (int)sx, ty0 = (int)sy;
+    if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
+    if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
+    const double fx = xsub(sx, (double)tx0), fy = xsub(sy, (double)ty0);
+    const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
+    const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
+    const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
+    const double bw[4] = {xmul(gx, gy), xmul(fx, gy), xmul(gx, fy), xmul(fx, fy)};
+    double nr = 0.0, ng = 0.0, nb = 0.0, den = 0.0, best = -1.0;
     uint8_t cw = 0;
-    if (sx >= 0.0 && sx <= W - 1.0 && sy >= 0.0 && sy <= H - 1.0) {
-        int tx0 = (int)sx, ty0 = (int)sy;
-        if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
-        if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
-        const double fx = xsub(sx, (double)tx0), fy = xsub(sy, (double)ty0);
-        const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
-        const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
-        const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
-        const double bw[4] = {xmul(gx, gy), xmul(fx, gy), xmul(gx, fy), xmul(fx, fy)};
-        double nr = 0.0, ng = 0.0, nb = 0.0, den = 0.0, best = -1.0;
-        for (int t = 0; t < 4; ++t) {
-            const long long idx = (v.oy + tys[t]) * v.pitch + (v.ox + txs[t]);
-            const uint8_t wt = v.w[idx];
-            if (wt == 0) continue;
-            nr = xadd(nr, xmul(bw[t], (double)v.r[idx]));
-            ng = xadd(ng, xmul(bw[t], (double)v.g[idx]));
-            nb = xadd(nb, xmul(bw[t], (double)v.b[idx]));
-            den = xadd(den, bw[t]);
-            if (bw[t] > best) {
-                best = bw[t];
-                cw = wt;
-            }
-        }
-        if (den > 0.0) {
-            cr = (float)(nr / den);
-            cg = (float)(ng / den);
-            cb = (float)(nb / den);
-        } else {
-            cw = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const long long idx = (v.oy + tys[t]) * v.pitch + (v.ox + txs[t]);
+        const uint8_t wt = __ldg(v.w + idx);
+        if (wt == 0) continue;
+        nr = xadd(nr, xmul(bw[t], (double)__ldg(v.r + idx)));
+        ng = xadd(ng, xmul(bw[t], (double)__ldg(v.g + idx)));
+        nb = xadd(nb, xmul(bw[t], (double)__ldg(v.b + idx)));
+        den = xadd(den, bw[t]);
+        if (bw[t] > best) {
+            best = bw[t];
+            cw = wt;
         }
     }
-    outr[o] = cr;
-    outg[o] = cg;
-    outb[o] = cb;
-    outw[o] = cw;
+    if (den > 0.0) {
+        o.r = (float)(nr / den);
+        o.g = (float)(ng / den);
+        o.b = (float)(nb / den);
+        o.w = cw;
+    }
+    return o;
+}
+
+// Ping-pong pass over the whole logical canvas: 4 pixels per thread (the
+// logical origin and the pitch are multiples of 256 px, so every quad is a
+// 16-byte aligned float4 / uchar4 of each plane). Pixels of the region are
+// resampled, the others copied, into the alternate planes (whose role is
+// swapped with the canvas planes afterwards). Rows this rank does not own
+// are skipped.
+__global__ void __launch_bounds__(256) k_canvas_deform_pp(CanvasView v, int W, int H, int rx0, int ry0, int rw,
+                                                          int rh, const float2* __restrict__ disp,
+                                                          float* __restrict__ outr, float* __restrict__ outg,
+                                                          float* __restrict__ outb, uint8_t* __restrict__ outw) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = 4 * q;
+    if (x >= W) return;
+    for (int y = blockIdx.y; y < H; y += gridDim.y) {
+        if (!owns_row(v, y)) continue;
+        const long long base = (v.oy + y) * v.pitch + v.ox + x;
+        float4 cr = *reinterpret_cast<const float4*>(v.r + base);
+        float4 cg = *reinterpret_cast<const float4*>(v.g + base);
+        float4 cb = *reinterpret_cast<const float4*>(v.b + base);
+        uchar4 cw = *reinterpret_cast<const uchar4*>(v.w + base);
+        const bool row_in = y >= ry0 && y < ry0 + rh;
+        if (row_in && x + 3 >= rx0 && x < rx0 + rw) {
+            float* pr = &cr.x;
+            float* pg = &cg.x;
+            float* pb = &cb.x;
+            unsigned char* pw = &cw.x;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int xi = x + k;
+                if (xi < rx0 || xi >= rx0 + rw) continue;
+                const Px o = deform_sample(v, W, H, xi, y, disp[(size_t)(y - ry0) * rw + (xi - rx0)]);
+                pr[k] = o.r;
+                pg[k] = o.g;
+                pb[k] = o.b;
+                pw[k] = o.w;
+            }
+        }
+        *reinterpret_cast<float4*>(outr + base) = cr;
+        *reinterpret_cast<float4*>(outg + base) = cg;
+        *reinterpret_cast<float4*>(outb + base) = cb;
+        *reinterpret_cast<uchar4*>(outw + base) = cw;
+    }
+}
+
+// Small regions: resample into region-sized scratch planes, then copy the
+// owned rows back (k_deform_commit) -- no pass over the rest of the canvas.
+__global__ void k_canvas_deform_region(CanvasView v, int W, int H, int x0, int y0, int w, int h,
+                                       const float2* __restrict__ disp, float* __restrict__ outr,
+                                       float* __restrict__ outg, float* __restrict__ outb,
+                                       uint8_t* __restrict__ outw) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= w) return;
+    for (int j = blockIdx.y; j < h; j += gridDim.y) {
+        if (!owns_row(v, y0 + j)) continue;
+        const size_t o = (size_t)j * w + i;
+        const Px p = deform_sample(v, W, H, x0 + i, y0 + j, disp[o]);
+        outr[o] = p.r;
+        outg[o] = p.g;
+        outb[o] = p.b;
+        outw[o] = p.w;
+    }
+}
+
+__global__ void k_deform_commit(CanvasView v, float* r, float* g, float* b, uint8_t* wp, int x0, int y0, int w,
+                                int h, const float* __restrict__ sr, const float* __restrict__ sg,
+                                const float* __restrict__ sb, const uint8_t* __restrict__ sw) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= w) return;
+    for (int j = blockIdx.y; j < h; j += gridDim.y) {
+        if (!owns_row(v, y0 + j)) continue;
+        const long long idx = (v.oy + y0 + j) * v.pitch + (v.ox + x0 + i);
+        const size_t o = (size_t)j * w + i;
+        r[idx] = sr[o];
+        g[idx] = sg[o];
+        b[idx] = sb[o];
+        wp[idx] = sw[o];
+    }
 }
 
 }  // namespace
 
-cudaError_t launch_canvas_deform(const nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
+cudaError_t canvas_alt_planes(nrm_canvas* cv, cudaStream_t st) {
+    if (cv->ar) return cudaSuccess;
+    const size_t npx = (size_t)cv->cap_w * (size_t)cv->cap_h;
+    cudaError_t e = cudaMalloc(&cv->ar, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&cv->ag, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&cv->ab, npx * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&cv->aw, npx);
+    // pixels outside the logical window must read as empty after a swap
+    // (ensure_contains inside the reservation relies on it)
+    if (e == cudaSuccess) e = cudaMemsetAsync(cv->ar, 0, npx * sizeof(float), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cv->ag, 0, npx * sizeof(float), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cv->ab, 0, npx * sizeof(float), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cv->aw, 0, npx, st);
+    if (e != cudaSuccess) {
+        cudaFree(cv->ar);
+        cudaFree(cv->ag);
+        cudaFree(cv->ab);
+        cudaFree(cv->aw);
+        cv->ar = cv->ag = cv->ab = nullptr;
+        cv->aw = nullptr;
+    }
+    return e;
+}
+
+bool deform_uses_ping_pong(const nrm_canvas* cv, int w, int h) {
+    // a region of a quarter of the canvas or more: one pass over the canvas
+    // (13 B read + 13 B written per pixel) beats scratch + copy-back (which
+    // moves the region twice)
+    return 4 * (double)w * (double)h >= (double)cv->width * (double)cv->height;
+}
+
+cudaError_t launch_canvas_deform(nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
                                  cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
+    const CanvasView v = view_of(cv);
+    if (deform_uses_ping_pong(cv, w, h)) {
+        cudaError_t e = canvas_alt_planes(cv, st);
+        if (e != cudaSuccess) return e;
+        const int quads = cv->width / 4;
+        prof_mark("k_canvas_deform", st);
+        k_canvas_deform_pp<<<dim3((quads + 255) / 256, grid_y(cv->height)), 256, 0, st>>>(
+            v, cv->width, cv->height, x, y, w, h, disp, cv->ar, cv->ag, cv->ab, cv->aw);
+        ++*launches;
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        std::swap(cv->r, cv->ar);
+        std::swap(cv->g, cv->ag);
+        std::swap(cv->b, cv->ab);
+        std::swap(cv->w, cv->aw);
+        return cudaSuccess;
+    }
     const size_t npx = (size_t)w * h;
     float* r = scratch;
     float* g = r + npx;
     float* b = g + npx;
     uint8_t* wt = reinterpret_cast<uint8_t*>(b + npx);
     prof_mark("k_canvas_deform", st);
-    k_canvas_deform<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), cv->width, cv->height, x, y, w, h, disp,
-                                                              r, g, b, wt);
+    k_canvas_deform_region<<<dim3((w + 255) / 256, grid_y(h)), 256, 0, st>>>(v, cv->width, cv->height, x, y, w, h,
+                                                                           disp, r, g, b, wt);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // scratch -> canvas planes
-    const long long ox = cv->origin_x - cv->phys_x0, oy = cv->origin_y - cv->phys_y0;
-    const size_t off = (size_t)(oy + y) * cv->cap_w + (size_t)(ox + x);
-    float* planes[3] = {cv->r, cv->g, cv->b};
-    const float* src[3] = {r, g, b};
-    for (int k = 0; k < 3; ++k) {
-        e = cudaMemcpy2DAsync(planes[k] + off, (size_t)cv->cap_w * sizeof(float), src[k], (size_t)w * sizeof(float),
-                              (size_t)w * sizeof(float), (size_t)h, cudaMemcpyDeviceToDevice, st);
-        if (e != cudaSuccess) return e;
-    }
-    return cudaMemcpy2DAsync(cv->w + off, (size_t)cv->cap_w, wt, (size_t)w, (size_t)w, (size_t)h,
-                             cudaMemcpyDeviceToDevice, st);
+    prof_mark("k_deform_commit", st);
+    k_deform_commit<<<dim3((w + 255) / 256, grid_y(h)), 256, 0, st>>>(v, cv->r, cv->g, cv->b, cv->w, x, y, w, h, r, g,
+                                                                    b, wt);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_pack(const nrm_canvas* cv, const int* d_rows, int nrows, void* d_buf, cudaStream_t st,
+                             int64_t* launches) {
+    if (nrows <= 0 || cv->width <= 0) return cudaSuccess;
+    const int quads = cv->width / 4;
+    prof_mark("k_rows_pack", st);
+    k_rows_pack<<<dim3((quads + 255) / 256, grid_y(nrows)), 256, 0, st>>>(view_of(cv), d_rows, nrows, cv->width,
+                                                                          static_cast<unsigned char*>(d_buf));
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rows_unpack(nrm_canvas* cv, const int* d_rows, int nrows, const void* d_buf, cudaStream_t st,
+                               int64_t* launches) {
+    if (nrows <= 0 || cv->width <= 0) return cudaSuccess;
+    const int quads = cv->width / 4;
+    prof_mark("k_rows_unpack", st);
+    k_rows_unpack<<<dim3((quads + 255) / 256, grid_y(nrows)), 256, 0, st>>>(
+        cv->r, cv->g, cv->b, cv->w, cv->cap_w, cv->origin_x - cv->phys_x0, cv->origin_y - cv->phys_y0, d_rows, nrows,
+        cv->width, static_cast<const unsigned char*>(d_buf));
+    ++*launches;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
     prof_mark("k_render", st);
-    k_render<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), x, y, w, h, reinterpret_cast<uchar4*>(out));
+    k_render<<<dim3((w + 255) / 256, grid_y(h)), 256, 0, st>>>(view_of(cv), x, y, w, h, reinterpret_cast<uchar4*>(out));
     ++*launches;
     return cudaGetLastError();
 }
@@ -253,7 +434,7 @@ cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h,
                                uint8_t* weight, cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
     prof_mark("k_canvas_read", st);
-    k_canvas_read<<<dim3((w + 255) / 256, h), 256, 0, st>>>(view_of(cv), x, y, w, h, rgb, weight);
+    k_canvas_read<<<dim3((w + 255) / 256, grid_y(h)), 256, 0, st>>>(view_of(cv), x, y, w, h, rgb, weight);
     ++*launches;
     return cudaGetLastError();
 }
@@ -262,10 +443,10 @@ cudaError_t launch_canvas_write(nrm_canvas* cv, int x, int y, int w, int h, cons
                                 const uint8_t* weight, cudaStream_t st, int64_t* launches) {
     if (w <= 0 || h <= 0) return cudaSuccess;
     prof_mark("k_canvas_write", st);
-    k_canvas_write<<<dim3((w + 255) / 256, h), 256, 0, st>>>(cv->r, cv->g, cv->b, cv->w, cv->cap_w,
-                                                            cv->origin_x - cv->phys_x0,
-                                                            cv->origin_y - cv->phys_y0, x, y, w, h, rgb,
-                                                            weight);
+    k_canvas_write<<<dim3((w + 255) / 256, grid_y(h)), 256, 0, st>>>(cv->r, cv->g, cv->b, cv->w, cv->cap_w,
+                                                                    cv->origin_x - cv->phys_x0,
+                                                                    cv->origin_y - cv->phys_y0, x, y, w, h, rgb,
+                                                                    weight);
     ++*launches;
     return cudaGetLastError();
 }

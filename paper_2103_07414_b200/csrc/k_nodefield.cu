@@ -114,15 +114,40 @@ __host__ __device__ __forceinline__ int tile_row_of(int by, int tile_j0, int s1,
     return 2 * s + (by & 1);
 }
 
+// Marks a deferred pixel whose queue slot overflowed: the blend's weight
+// byte gets bit 7 (weights never exceed kWeightCap = 30), the node field's
+// displacement becomes NaN (or its support byte 0xFF without a displacement
+// output). K1 has not written the pixel; the exact pass finds the marks by a
+// scan of the launch window and resolves them like queued pixels.
+constexpr uint8_t kSpillBit = 0x80;
+template <int MODE>
+__device__ __forceinline__ void spill_mark(const NodeFieldLaunch& L, int i, int j) {
+    if (MODE == 1) {
+        const size_t o = (size_t)(j - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+        if (L.disp)
+            L.disp[o] = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+        else if (L.support)
+            L.support[o] = 0xFF;
+    } else {
+        const long long idx = (long long)(j - L.phys_y0) * L.pitch + (i - L.phys_x0);
+        L.W[idx] = (uint8_t)(L.W[idx] | kSpillBit);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ void defer_pixel(const NodeFieldLaunch& L, bool pred, int i, int j) {
+    if (queue_push(pred, i, j, L.exc, L.exc_count, L.exc_cap)) spill_mark<MODE>(L, i, j);
+}
+
 // Pushes every valid pixel of the tile to the exception queue.
+template <int MODE>
 __device__ void tile_to_exceptions(const NodeFieldLaunch& L, int ci0, int ci1, int cj0, int cj1) {
     const int w = ci1 - ci0 + 1, h = cj1 - cj0 + 1;
     const int total = w * h;
     for (int base = 0; base < total; base += NT) {
         const int e = base + threadIdx.x;
         const bool v = e < total;
-        queue_push(v, ci0 + (v ? e % w : 0), cj0 + (v ? e / w : 0), L.exc, L.exc_count, L.exc_cap,
-                   L.exc_overflow);
+        defer_pixel<MODE>(L, v, ci0 + (v ? e % w : 0), cj0 + (v ? e / w : 0));
     }
 }
 
@@ -435,7 +460,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
     cp_async_commit();
 
     if (status == NF_EXACT) {
-        tile_to_exceptions(L, ci0, ci1, cj0, cj1);
+        tile_to_exceptions<MODE>(L, ci0, ci1, cj0, cj1);
         cp_async_wait_all();
         return;
     }
@@ -687,7 +712,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
                 }
             }
         }
-        queue_push(exc, i, jj, L.exc, L.exc_count, L.exc_cap, L.exc_overflow);
+        defer_pixel<MODE>(L, exc, i, jj);
     }
     if (MODE != 1) block_add3<NT>(L.acc, nb, nns, noof);
 }
@@ -826,10 +851,9 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
 // Queued pixel q of launch L, resolved by one warp in the exact tier. Returns
 // (valid in lane 0) 0 blended, 1 no support, 2 out of frame, -1 (field mode).
 template <int MODE>
-__device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, unsigned q, double* stage) {
+__device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, int2 p, double* stage) {
     const int lane = threadIdx.x & 31;
     const double fxm = L.fw - 1.0, fym = L.fh - 1.0;
-    const int2 p = L.exc[q];
     const double x = L.grid.gx + p.x, y = L.grid.gy + p.y;
     W5 wp;
     // the pixel's launch chunk: tile row -> launch row (inverse of tile_row_of)
@@ -877,18 +901,71 @@ __device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, unsigned q, d
     return 0;
 }
 
-// The queued pixels of one launch, one warp per pixel spread over the grid;
+__device__ __forceinline__ bool band_owns_abs_row(const NodeFieldLaunch& L, int j) {
+    return L.band_count <= 1 || posmod(floordiv(j, kStripeRows), L.band_count) == L.band_rank;
+}
+
+// Spilled pixels of a launch (queue overflow, see spill_mark): a scan of the
+// launch window, one warp per 32 consecutive pixels; each marked pixel is
+// unmarked and resolved by the whole warp. `fn(p, r)` receives each result.
+template <int MODE, class Fn>
+__device__ __forceinline__ void exc_scan(const NodeFieldLaunch& L, double* stage, unsigned gw, unsigned nwarps,
+                                         Fn fn) {
+    const int lane = threadIdx.x & 31;
+    const long long wdt = L.grid.i1 - L.grid.i0 + 1, hgt = L.grid.j1 - L.grid.j0 + 1;
+    const long long total = wdt * hgt;
+    for (long long base = (long long)gw * 32; base < total; base += (long long)nwarps * 32) {
+        const long long e = base + lane;
+        int i = 0, j = 0;
+        bool mk = false;
+        if (e < total) {
+            j = L.grid.j0 + (int)(e / wdt);
+            i = L.grid.i0 + (int)(e % wdt);
+            if (band_owns_abs_row(L, j)) {
+                if (MODE == 1) {
+                    const size_t o = (size_t)e;
+                    if (L.disp) {
+                        mk = isnan(L.disp[o].x);
+                    } else if (L.support && L.support[o] == 0xFF) {
+                        mk = true;
+                        L.support[o] = 0;
+                    }
+                } else {
+                    const long long idx = (long long)(j - L.phys_y0) * L.pitch + (i - L.phys_x0);
+                    const uint8_t wv = L.W[idx];
+                    if (wv & kSpillBit) {
+                        mk = true;
+                        L.W[idx] = (uint8_t)(wv & (uint8_t)~kSpillBit);
+                    }
+                }
+            }
+        }
+        unsigned m = __ballot_sync(0xffffffffu, mk);
+        __syncwarp();
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const int2 p = make_int2(__shfl_sync(0xffffffffu, i, l), __shfl_sync(0xffffffffu, j, l));
+            fn(exc_pixel<MODE>(L, p, stage));
+        }
+    }
+}
+
+// The deferred pixels of one launch -- the queued ones, then (after a queue
+// overflow) the spilled ones -- one warp per pixel spread over the grid;
 // returns this thread's partial BlendStats counts (lane 0 of each warp).
 template <int MODE>
 __device__ __forceinline__ void exc_run(const NodeFieldLaunch& L, double* stage, int& nb, int& nns, int& noof) {
-    const unsigned cnt = min(*L.exc_count, L.exc_cap);
+    const unsigned total = *L.exc_count;
+    const unsigned cnt = min(total, L.exc_cap);
     const unsigned gw = blockIdx.x * (EXC_THREADS / 32) + (threadIdx.x >> 5), nwarps = gridDim.x * (EXC_THREADS / 32);
-    for (unsigned q = gw; q < cnt; q += nwarps) {
-        const int r = exc_pixel<MODE>(L, q, stage);
+    auto tally = [&](int r) {
         nb += r == 0;
         nns += r == 1;
         noof += r == 2;
-    }
+    };
+    for (unsigned q = gw; q < cnt; q += nwarps) tally(exc_pixel<MODE>(L, L.exc[q], stage));
+    if (total > L.exc_cap) exc_scan<MODE>(L, stage, gw, nwarps, tally);
 }
 
 // Block-sums the partial counts into L.acc (blend modes).
@@ -931,7 +1008,8 @@ __device__ __forceinline__ void exc_finalize(const NodeFieldLaunch& L) {
         }
         acc[0] = acc[1] = acc[2] = 0;
     }
-    if (L.exc_last) *L.exc_last = min(*L.exc_count, L.exc_cap);
+    if (L.exc_last) *L.exc_last = *L.exc_count;  // queued + spilled
+    if (L.exc_overflow && *L.exc_count > L.exc_cap) atomicAdd(L.exc_overflow, 1u);  // diagnostics: spilled launches
     *L.exc_count = 0;
 }
 
@@ -979,8 +1057,15 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions_batch(const NfB
         int f = 0;
         while (i >= pre[f + 1]) ++f;
         const NodeFieldLaunch& L = F[f].L;
-        const int r = exc_pixel<MODE>(L, i - pre[f], stage[threadIdx.x >> 5]);
+        const int r = exc_pixel<MODE>(L, L.exc[i - pre[f]], stage[threadIdx.x >> 5]);
         if (MODE != 1 && r >= 0) atomicAdd(&L.acc[r], 1ull);
+    }
+    for (int f = 0; f < nf; ++f) {  // spilled pixels of frames whose queue overflowed
+        const NodeFieldLaunch& L = F[f].L;
+        if (*L.exc_count <= L.exc_cap) continue;
+        exc_scan<MODE>(L, stage[threadIdx.x >> 5], gw, nwarps, [&](int r) {
+            if (MODE != 1 && r >= 0) atomicAdd(&L.acc[r], 1ull);
+        });
     }
     __syncthreads();
     unsigned* done = F[0].L.exc_done;

@@ -135,12 +135,12 @@ bool finite_all(const double* p, size_t n) {
 
 // ---- canvas storage ------------------------------------------------------
 void free_planes(nrm_canvas* cv) {
-    cudaFree(cv->r);
-    cudaFree(cv->g);
-    cudaFree(cv->b);
+    float* f[6] = {cv->r, cv->g, cv->b, cv->ar, cv->ag, cv->ab};
+    for (float* p : f) cudaFree(p);
     cudaFree(cv->w);
-    cv->r = cv->g = cv->b = nullptr;
-    cv->w = nullptr;
+    cudaFree(cv->aw);
+    cv->r = cv->g = cv->b = cv->ar = cv->ag = cv->ab = nullptr;
+    cv->w = cv->aw = nullptr;
 }
 
 // Reallocates physical storage to cover absolute [x0,x1) x [y0,y1) and
@@ -164,10 +164,24 @@ int grow_physical(nrm_canvas* cv, int64_t x0, int64_t y0, int64_t x1, int64_t y1
         cudaFree(w);
         return cuda_fail(e, "canvas allocation");
     }
-    NRM_CUDA(cudaMemsetAsync(r, 0, npx * sizeof(float), c->stream));
-    NRM_CUDA(cudaMemsetAsync(g, 0, npx * sizeof(float), c->stream));
-    NRM_CUDA(cudaMemsetAsync(b, 0, npx * sizeof(float), c->stream));
-    NRM_CUDA(cudaMemsetAsync(w, 0, npx, c->stream));
+    // on any failure below the new planes are released (the canvas keeps its old storage)
+    auto release_new = [&](cudaError_t err, const char* what) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(r);
+        cudaFree(g);
+        cudaFree(b);
+        cudaFree(w);
+        return cuda_fail(err, what);
+    };
+#define NRM_GROW(call)                                        \
+    do {                                                      \
+        const cudaError_t e__ = (call);                       \
+        if (e__ != cudaSuccess) return release_new(e__, #call); \
+    } while (0)
+    NRM_GROW(cudaMemsetAsync(r, 0, npx * sizeof(float), c->stream));
+    NRM_GROW(cudaMemsetAsync(g, 0, npx * sizeof(float), c->stream));
+    NRM_GROW(cudaMemsetAsync(b, 0, npx * sizeof(float), c->stream));
+    NRM_GROW(cudaMemsetAsync(w, 0, npx, c->stream));
     if (cv->width > 0 && cv->r) {
         const size_t spitch = (size_t)cv->cap_w, dpitch = (size_t)w64;
         const size_t soff = (size_t)(cv->origin_y - cv->phys_y0) * spitch + (size_t)(cv->origin_x - cv->phys_x0);
@@ -175,13 +189,14 @@ int grow_physical(nrm_canvas* cv, int64_t x0, int64_t y0, int64_t x1, int64_t y1
         float* planes_old[3] = {cv->r, cv->g, cv->b};
         float* planes_new[3] = {r, g, b};
         for (int k = 0; k < 3; ++k)
-            NRM_CUDA(cudaMemcpy2DAsync(planes_new[k] + doff, dpitch * sizeof(float), planes_old[k] + soff,
+            NRM_GROW(cudaMemcpy2DAsync(planes_new[k] + doff, dpitch * sizeof(float), planes_old[k] + soff,
                                        spitch * sizeof(float), (size_t)cv->width * sizeof(float),
                                        (size_t)cv->height, cudaMemcpyDeviceToDevice, c->stream));
-        NRM_CUDA(cudaMemcpy2DAsync(w + doff, dpitch, cv->w + soff, spitch, (size_t)cv->width,
+        NRM_GROW(cudaMemcpy2DAsync(w + doff, dpitch, cv->w + soff, spitch, (size_t)cv->width,
                                    (size_t)cv->height, cudaMemcpyDeviceToDevice, c->stream));
-        NRM_CUDA(cudaStreamSynchronize(c->stream));
+        NRM_GROW(cudaStreamSynchronize(c->stream));
     }
+#undef NRM_GROW
     free_planes(cv);
     cv->r = r;
     cv->g = g;
@@ -293,6 +308,18 @@ State state_of(nrm_ctx* c) {
             reinterpret_cast<unsigned*>(b + 36), reinterpret_cast<unsigned*>(b + 40)};
 }
 
+// Exception-queue slots for a launch over `pixels` grid pixels. The fast
+// tiers defer ~1e-5 of the pixels (34 of 2.6 M on C2), or whole tiles whose
+// warps span more than a quarter turn; a deferral past the capacity is not
+// lost but marked in the output and found by the exact pass's scan
+// (k_nodefield.cu spill_mark), so the queue is sized for the common case:
+// 1/64 of the pixels, at least 2^18 slots (8 B each).
+size_t exception_capacity(const nrm_ctx* c, size_t pixels) {
+    size_t cap = std::max<size_t>((size_t)1 << 18, pixels / 64);
+    if (c->exc_cap_override > 0) cap = (size_t)c->exc_cap_override;
+    return std::max<size_t>(1, std::min<size_t>({cap, pixels, (size_t)0x7fffffff}));
+}
+
 // Shared core of blend_frame: everything after the inputs are in HBM.
 // d_stats: int64[4] on the device, written by the exception pass.
 int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
@@ -315,7 +342,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
         return NRM_OK;
     }
     const unsigned long long footprint = (unsigned long long)bw * (unsigned long long)bh;
-    const size_t exc_cap = std::min<size_t>(footprint, (size_t)1 << 26);
+    const size_t exc_cap = exception_capacity(c, footprint);
     NRM_CUDA(c->exc.ensure(exc_cap * sizeof(int2) + 64));
     const State st = state_of(c);
 
@@ -360,16 +387,6 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     return NRM_OK;
 }
 
-int check_overflow(nrm_ctx* c) {
-    unsigned flag = 0;
-    NRM_CUDA(cudaMemcpy(&flag, state_of(c).overflow, sizeof(flag), cudaMemcpyDeviceToHost));
-    if (flag) {
-        cudaMemset(state_of(c).overflow, 0, sizeof(unsigned));
-        return fail(NRM_ECUDA, "exception queue overflow");
-    }
-    return NRM_OK;
-}
-
 int check_canvas(const nrm_canvas* cv) {
     if (!cv || !cv->ctx) return fail(NRM_ESTATE, "null canvas");
     return NRM_OK;
@@ -408,7 +425,8 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     NRM_CHECK(grid_indices(grid, &fg));
     const size_t npx = (size_t)grid->width * (size_t)grid->height;
     if (npx == 0) return NRM_OK;
-    NRM_CUDA(c->exc.ensure(npx * sizeof(int2) + 64));
+    const size_t exc_cap = exception_capacity(c, npx);
+    NRM_CUDA(c->exc.ensure(exc_cap * sizeof(int2) + 64));
     const State st = state_of(c);
     NodeFieldLaunch L;
     L.anchors = d_anchors;
@@ -420,7 +438,7 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.support = d_support;
     L.exc = c->exc.as<int2>();
     L.exc_count = st.exc_count;
-    L.exc_cap = (unsigned)std::min<size_t>(npx, 0xffffffffu);
+    L.exc_cap = (unsigned)exc_cap;
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
     L.exc_done = st.exc_done;
@@ -566,7 +584,7 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     cudaStreamSynchronize(c->stream);
     DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc,   &c->misc,  &c->stats, &c->pts,
                       &c->locals,    &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles, &c->feat,
-                      &c->feat_io,   &c->batch};
+                      &c->feat_io,   &c->batch,  &c->halo};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();
@@ -697,10 +715,8 @@ int nrm_canvas_upload(nrm_canvas* cv, int x, int y, int w, int h, const double* 
 // ---- extension: canvas deformation (north_star) ------------
 static int deform_core(nrm_canvas* cv, int x, int y, int w, int h, const float* d_disp) {
     nrm_ctx* c = cv->ctx;
-    if (cv->band_count > 1)
-        return fail(NRM_EINVAL, "canvas_deform: banded canvases need a halo exchange (not supported)");
     const size_t npx = (size_t)w * h;
-    NRM_CUDA(c->out_b.ensure(npx * 13 + 64));
+    if (!deform_uses_ping_pong(cv, w, h)) NRM_CUDA(c->out_b.ensure(npx * 13 + 64));
     NRM_CUDA(launch_canvas_deform(cv, x, y, w, h, reinterpret_cast<const float2*>(d_disp), c->out_b.as<float>(),
                                   c->stream, &c->launches));
     return NRM_OK;
@@ -728,6 +744,43 @@ int nrm_canvas_deform_device(nrm_canvas* cv, int x, int y, int w, int h, const f
     DeviceGuard g(cv->ctx->device);
     ProfScope prof_scope(cv->ctx);
     return deform_core(cv, x, y, w, h, d_disp);
+}
+
+// ---- halo rows of banded canvases -----------------------------
+static int rows_common(nrm_canvas* cv, const int* rows, int nrows, const void* d_buf) {
+    NRM_CHECK(check_canvas(cv));
+    if (nrows < 0) return fail(NRM_EINVAL, "rows: negative count");
+    if (nrows > 0 && (!rows || !d_buf)) return fail(NRM_EINVAL, "rows: null argument");
+    for (int k = 0; k < nrows; ++k)
+        if (rows[k] < 0 || rows[k] >= cv->height) return fail(NRM_EINVAL, "rows: row outside the canvas");
+    if (nrows == 0) return NRM_OK;
+    nrm_ctx* c = cv->ctx;
+    NRM_CUDA(c->halo.ensure((size_t)nrows * sizeof(int)));
+    NRM_CUDA(cudaMemcpyAsync(c->halo.p, rows, (size_t)nrows * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    return NRM_OK;
+}
+
+int nrm_canvas_pack_rows_device(nrm_canvas* cv, const int* rows, int nrows, void* d_buf) {
+    if (cv && cv->ctx) {
+        DeviceGuard g(cv->ctx->device);
+        ProfScope prof_scope(cv->ctx);
+        NRM_CHECK(rows_common(cv, rows, nrows, d_buf));
+        NRM_CUDA(launch_rows_pack(cv, cv->ctx->halo.as<int>(), nrows, d_buf, cv->ctx->stream, &cv->ctx->launches));
+        return NRM_OK;
+    }
+    return check_canvas(cv);
+}
+
+int nrm_canvas_unpack_rows_device(nrm_canvas* cv, const int* rows, int nrows, const void* d_buf) {
+    if (cv && cv->ctx) {
+        DeviceGuard g(cv->ctx->device);
+        ProfScope prof_scope(cv->ctx);
+        NRM_CHECK(rows_common(cv, rows, nrows, d_buf));
+        NRM_CUDA(launch_rows_unpack(cv, cv->ctx->halo.as<int>(), nrows, d_buf, cv->ctx->stream,
+                                    &cv->ctx->launches));
+        return NRM_OK;
+    }
+    return check_canvas(cv);
 }
 
 static int occupied_scan(nrm_canvas* cv, unsigned long long* count, int bbox[4]) {
@@ -809,7 +862,6 @@ int blend_host(nrm_canvas* cv, const uint8_t* frame, int fw, int fh, int ch, con
     NRM_CUDA(c->staging_out.ensure(64));
     NRM_CUDA(cudaMemcpyAsync(c->staging_out.p, c->stats.p, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
     NRM_CUDA(cudaStreamSynchronize(c->stream));
-    NRM_CHECK(check_overflow(c));
     std::memcpy(out, c->staging_out.p, sizeof(nrm_blend_stats));
     return NRM_OK;
 }
@@ -927,7 +979,7 @@ int nrm_blend_frames_device(nrm_canvas* cv, int nf, const uint8_t* const* d_fram
     for (size_t a = 0; a < nact; ++a) {
         const Win& w = win[act[a]];
         const unsigned long long fp = (unsigned long long)(w.i1 - w.i0 + 1) * (unsigned long long)(w.j1 - w.j0 + 1);
-        cap[a] = std::min<size_t>(fp, (size_t)1 << 24);
+        cap[a] = exception_capacity(c, fp);
         qtot += cap[a];
     }
     NRM_CUDA(c->exc.ensure(qtot * sizeof(int2) + 64));
@@ -1077,7 +1129,6 @@ int nrm_node_field(nrm_ctx* c, const nrm_grid* grid, const double* anchors, cons
     if (disp) NRM_CUDA(cudaMemcpyAsync(disp, c->out_a.p, npx * sizeof(float2), cudaMemcpyDeviceToHost, c->stream));
     if (support) NRM_CUDA(cudaMemcpyAsync(support, c->out_b.p, npx, cudaMemcpyDeviceToHost, c->stream));
     NRM_CUDA(cudaStreamSynchronize(c->stream));
-    NRM_CHECK(check_overflow(c));
     return NRM_OK;
 }
 
@@ -1533,6 +1584,23 @@ int nrm_ctx_exceptions(nrm_ctx* c, int64_t* blend_exceptions, int64_t* emdq_exac
     NRM_CUDA(cudaMemcpy(v, state_of(c).last_exc, sizeof(v), cudaMemcpyDeviceToHost));
     if (blend_exceptions) *blend_exceptions = v[0];
     if (emdq_exact) *emdq_exact = v[1];
+    return NRM_OK;
+}
+
+int nrm_ctx_set_exception_capacity(nrm_ctx* c, int64_t slots) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (slots < 0) return fail(NRM_EINVAL, "exception capacity must be >= 0");
+    c->exc_cap_override = slots;
+    return NRM_OK;
+}
+
+int nrm_ctx_spilled_launches(nrm_ctx* c, int64_t* out) {
+    if (!c || !out) return fail(NRM_EINVAL, "null argument");
+    DeviceGuard g(c->device);
+    unsigned v = 0;
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    NRM_CUDA(cudaMemcpy(&v, state_of(c).overflow, sizeof(v), cudaMemcpyDeviceToHost));
+    *out = v;
     return NRM_OK;
 }
 

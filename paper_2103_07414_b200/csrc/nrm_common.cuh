@@ -259,22 +259,25 @@ __host__ __device__ __forceinline__ int posmod(int a, int b) {
 }
 
 // Warp-aggregated append to a global queue of (i, j) pixel indices.
-__device__ __forceinline__ void queue_push(bool pred, int i, int j, int2* q, unsigned* count,
-                                           unsigned cap, unsigned* overflow) {
+// Warp-aggregated push of (i, j) for the lanes with pred. `count` counts
+// every push; a push past `cap` is not stored and returns true for that lane
+// (the caller then marks the pixel in its output so the exact pass finds it
+// by a scan: nothing is dropped).
+__device__ __forceinline__ bool queue_push(bool pred, int i, int j, int2* q, unsigned* count, unsigned cap) {
     const unsigned mask = __ballot_sync(0xffffffffu, pred);
-    if (!mask) return;
+    if (!mask) return false;
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(mask) - 1;
     unsigned base = 0;
     if (lane == leader) base = atomicAdd(count, (unsigned)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (pred) {
-        const unsigned slot = base + __popc(mask & ((1u << lane) - 1u));
-        if (slot < cap)
-            q[slot] = make_int2(i, j);
-        else
-            atomicExch(overflow, 1u);
+    if (!pred) return false;
+    const unsigned slot = base + __popc(mask & ((1u << lane) - 1u));
+    if (slot < cap) {
+        q[slot] = make_int2(i, j);
+        return false;
     }
+    return true;
 }
 
 // Block-wide sum of up to three counters, added atomically to dst[0..2].

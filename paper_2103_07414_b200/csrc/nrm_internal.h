@@ -52,9 +52,10 @@ struct nrm_ctx {
     cudaStream_t stream = nullptr;
     int64_t launches = 0;
     int num_sms = 148;
+    int64_t exc_cap_override = 0;  // nrm_ctx_set_exception_capacity (tests); 0 = default sizing
     // scratch (grow-only)
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
-        active, out_a, out_b, tiles, feat, feat_io, batch;
+        active, out_a, out_b, tiles, feat, feat_io, batch, halo;
     nrm::PinnedBuf staging, staging_out;
     nrm::Prof prof;
 };
@@ -72,6 +73,12 @@ struct nrm_canvas {
     float* g = nullptr;
     float* b = nullptr;
     uint8_t* w = nullptr;
+    // alternate planes of the same physical extent for the ping-pong canvas
+    // deformation (allocated on first use, dropped when the canvas grows)
+    float* ar = nullptr;
+    float* ag = nullptr;
+    float* ab = nullptr;
+    uint8_t* aw = nullptr;
     // reservation (absolute, tile-aligned), 0-size when none
     int64_t res_x0 = 0, res_y0 = 0, res_x1 = 0, res_y1 = 0;
     int band_rank = 0, band_count = 1;
@@ -132,7 +139,7 @@ struct NodeFieldLaunch {
     int2* exc = nullptr;
     unsigned* exc_count = nullptr;
     unsigned exc_cap = 0;
-    unsigned* exc_overflow = nullptr;  // sticky; the host checks and clears it
+    unsigned* exc_overflow = nullptr;  // launches whose queue overflowed (diagnostics, accumulated)
     unsigned* exc_last = nullptr;      // pixels the last exception pass resolved (diagnostics)
     unsigned* exc_done = nullptr;      // finished exception CTAs (persistent-zero)
     void* plans = nullptr;             // tile-plan scratch (node_field_plan_bytes(n))
@@ -211,9 +218,18 @@ cudaError_t launch_points_bbox(const double* q, int nq, double* out4, cudaStream
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches);
 // Extension: canvas deformation new(p) = old(p + d(p)) over a logical
-// region; scratch holds 13 B per region pixel.
-cudaError_t launch_canvas_deform(const nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
+// region. Regions of a quarter of the canvas or more run one ping-pong pass
+// over the canvas into the alternate planes (swapped in afterwards); smaller
+// ones use `scratch` (13 B per region pixel) and a copy-back.
+bool deform_uses_ping_pong(const nrm_canvas* cv, int w, int h);
+cudaError_t launch_canvas_deform(nrm_canvas* cv, int x, int y, int w, int h, const float2* disp, float* scratch,
                                  cudaStream_t st, int64_t* launches);
+// Halo rows of banded canvases: rows (logical canvas rows, device int array)
+// packed as {R, G, B float32, W uint8} x canvas width per row (13 w bytes).
+cudaError_t launch_rows_pack(const nrm_canvas* cv, const int* d_rows, int nrows, void* d_buf, cudaStream_t st,
+                             int64_t* launches);
+cudaError_t launch_rows_unpack(nrm_canvas* cv, const int* d_rows, int nrows, const void* d_buf, cudaStream_t st,
+                               int64_t* launches);
 cudaError_t launch_occupied(const nrm_canvas* cv, unsigned long long* count, int* bbox4,
                             cudaStream_t st, int64_t* launches);
 cudaError_t launch_canvas_read(const nrm_canvas* cv, int x, int y, int w, int h, double* rgb,

@@ -15,6 +15,10 @@ Collectives (torch.distributed; NCCL over NVLink on GPUs, gloo in tests):
   assemble_bbox     -- crop box for render(crop=True): min/max over ranks
   assemble_render   -- rendered RGBA bands: each rank sends only its owned
                        rows (one gather of equal-size padded stripe packs)
+  exchange_halo     -- canvas deformation (north_star extension): before a
+                       rank resamples its stripes, the rows within the halo
+                       H = ceil(max |d_y|) + 1 of them that other ranks own
+                       are sent point to point by their owners (halo_plan)
 No collective touches the per-pixel data path of blend_frame itself.
 """
 from __future__ import annotations
@@ -33,6 +37,32 @@ def owned_rows_mask(origin_y: int, height: int, rank: int, world: int) -> np.nda
         return np.ones(height, bool)
     rows = np.arange(height, dtype=np.int64) + int(origin_y)
     return np.mod(np.floor_divide(rows, STRIPE_ROWS), world) == rank
+
+
+def halo_plan(origin_y: int, height: int, world: int, halo: int, y0: int = 0, h: Optional[int] = None):
+    """Rows each rank must receive before deforming the canvas rows [y0, y0+h)
+    with |d_y| <= halo - 1: plan[q][r] = sorted canvas rows owned by rank r
+    that rank q reads (within `halo` rows of a row q owns in the region).
+    Every rank computes the same plan, so rank r sends plan[q][r] to each q
+    and receives plan[r][q] from each q."""
+    if h is None:
+        h = height - y0
+    plan = [[np.zeros(0, np.int32) for _ in range(world)] for _ in range(world)]
+    if world <= 1 or h <= 0 or halo <= 0:
+        return plan
+    owner = np.mod(np.floor_divide(np.arange(height, dtype=np.int64) + int(origin_y), STRIPE_ROWS), world)
+    for q in range(world):
+        mine = np.zeros(height, bool)
+        mine[y0:y0 + h] = owner[y0:y0 + h] == q
+        # dilate by `halo` rows (cumulative-sum window)
+        c = np.concatenate([[0], np.cumsum(mine)])
+        lo = np.clip(np.arange(height) - halo, 0, height)
+        hi = np.clip(np.arange(height) + halo + 1, 0, height)
+        near = (c[hi] - c[lo]) > 0
+        for r in range(world):
+            if r != q:
+                plan[q][r] = np.nonzero(near & (owner == r))[0].astype(np.int32)
+    return plan
 
 
 def broadcast_inputs(tensors: Sequence, src: int = 0, group=None) -> None:
@@ -95,6 +125,39 @@ def assemble_render(local_rgba, origin_y: int, rank: int, world: int, dst: int =
     return local_rgba
 
 
+def exchange_halo(plan, rank: int, world: int, row_bytes: int, pack, unpack, device=None, group=None) -> int:
+    """Point-to-point halo exchange of a banded canvas: this rank sends the
+    rows other ranks read (plan[q][rank]) and receives the rows it reads
+    (plan[rank][q]). pack(rows, buf) / unpack(rows, buf) move rows between
+    the canvas and flat uint8 buffers of row_bytes per row (on the GPU path,
+    Canvas.pack_rows / unpack_rows on torch's current stream; the transfers
+    are NCCL send/recv over NVLink). Returns the bytes received."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return 0
+    ops, recvs = [], []
+    for q in range(world):
+        if q == rank:
+            continue
+        out_rows = plan[q][rank]
+        if len(out_rows):
+            buf = torch.empty(len(out_rows) * row_bytes, dtype=torch.uint8, device=device)
+            pack(out_rows, buf)
+            ops.append(dist.P2POp(dist.isend, buf, q, group=group))
+        in_rows = plan[rank][q]
+        if len(in_rows):
+            buf = torch.empty(len(in_rows) * row_bytes, dtype=torch.uint8, device=device)
+            recvs.append((in_rows, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, q, group=group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for rows, buf in recvs:
+        unpack(rows, buf)
+    return sum(int(b.numel()) for _, b in recvs)
+
+
 class BandedMosaic:
     """A canvas banded across the ranks of the default process group
     (GPU product path: libnrm_b200 on this rank's device)."""
@@ -104,6 +167,13 @@ class BandedMosaic:
         self.M = M
         self.rank, self.world = rank, world
         self.ctx = M.Context(device)
+        # Every kernel of this rank runs on torch's current stream of the
+        # device, so the collectives below (issued by torch on the same
+        # stream, or ordered after it by NCCL) see the kernels' results and
+        # the kernels see inputs torch produced (broadcast frames, zeroed
+        # render buffers) without extra events.
+        import torch
+        self.ctx.set_stream(torch.cuda.current_stream(device).cuda_stream)
         self.canvas = M.Canvas(self.ctx)
         if reserve is not None:
             self.canvas.reserve(reserve)
@@ -126,6 +196,28 @@ class BandedMosaic:
             reduce_stats(stats_t)
         return stats_t
 
+    def deform(self, disp_t, x: int = 0, y: int = 0, group=None):
+        """Canvas deformation (north_star extension) of the rectangle at
+        (x, y) with disp_t's (h, w) shape (CUDA float32 tensor, canvas px).
+        Each rank resamples only its stripes: the halo H = ceil(max |d_y|) + 1
+        is agreed by a max all-reduce, the rows within H of its stripes come
+        from their owners (exchange_halo), then the kernel runs locally."""
+        import torch
+        import torch.distributed as dist
+        h = int(disp_t.shape[0])
+        halo = 0
+        if self.world > 1:
+            dmax = disp_t[..., 1].abs().max() if disp_t.numel() else torch.zeros((), device=disp_t.device)
+            hv = (torch.ceil(dmax) + 1).to(torch.int64).reshape(1)
+            dist.all_reduce(hv, op=dist.ReduceOp.MAX, group=group)
+            halo = int(hv.item())
+            _, oy = self.canvas.origin_offset()
+            plan = halo_plan(int(oy), self.canvas.height(), self.world, halo, y, h)
+            exchange_halo(plan, self.rank, self.world, 13 * self.canvas.width(), self.canvas.pack_rows,
+                          self.canvas.unpack_rows, device=torch.device("cuda", self.ctx.device), group=group)
+        self.canvas.deform(disp_t, x, y)
+        return halo
+
     def render(self, crop: bool = False, dst: int = 0):
         """render(canvas, crop) assembled on rank `dst` -> (rgba numpy, origin)."""
         import torch
@@ -136,7 +228,8 @@ class BandedMosaic:
         x0, y0, x1, y1 = 0, 0, w - 1, h - 1
         dev = torch.device("cuda", self.ctx.device)
         if crop:
-            x0, y0, x1, y1 = assemble_bbox(self.canvas.occupied_bbox(), device=dev)
+            bb = self.canvas.occupied_bbox()
+            x0, y0, x1, y1 = assemble_bbox(bb, device=dev) if self.world > 1 else bb
             if x1 < x0:
                 return np.zeros((0, 0, 4), np.uint8), (ox, oy)
         out = torch.zeros((y1 - y0 + 1, x1 - x0 + 1, 4), dtype=torch.uint8, device=dev)

@@ -74,7 +74,11 @@ class Context:
 
     def set_stream(self, stream_handle: Optional[int]) -> None:
         """Run subsequent work on an external cudaStream_t (e.g.
-        torch.cuda.current_stream().cuda_stream); None = own stream."""
+        torch.cuda.current_stream().cuda_stream); None = own stream. Handle 0
+        (torch's default stream) is passed as cudaStreamLegacy (0x1), since a
+        NULL stream means "own stream" at the C ABI."""
+        if stream_handle is not None and int(stream_handle) == 0:
+            stream_handle = 1  # cudaStreamLegacy
         check(self._lib.nrm_ctx_set_stream(self._h, stream_handle))
 
     def stream(self) -> int:
@@ -86,6 +90,16 @@ class Context:
     def launch_count(self) -> int:
         v = C.c_int64()
         check(self._lib.nrm_ctx_launch_count(self._h, C.byref(v)))
+        return v.value
+
+    def set_exception_capacity(self, slots: int) -> None:
+        """Exception-queue slots per launch (0 = default); results never
+        depend on it (overflowing deferrals are resolved by a scan)."""
+        check(self._lib.nrm_ctx_set_exception_capacity(self._h, int(slots)))
+
+    def spilled_launches(self) -> int:
+        v = C.c_int64()
+        check(self._lib.nrm_ctx_spilled_launches(self._h, C.byref(v)))
         return v.value
 
     def exceptions(self):
@@ -215,6 +229,20 @@ class Canvas:
             if d.ndim != 3 or d.shape[2] != 2:
                 raise ValueError("disp must be (h, w, 2)")
             check(self._lib.nrm_canvas_deform(self._h, int(x), int(y), d.shape[1], d.shape[0], _ptr(d)))
+
+    def pack_rows(self, rows, buf_t) -> None:
+        """Halo rows (banded canvases): canvas rows `rows` across the full
+        width into the CUDA uint8 tensor buf_t (13 * width bytes per row)."""
+        r = np.ascontiguousarray(rows, np.int32)
+        if buf_t.numel() < len(r) * 13 * self.width():
+            raise ValueError("pack_rows: buffer too small")
+        check(self._lib.nrm_canvas_pack_rows_device(self._h, _ptr(r), len(r), _tptr(buf_t)))
+
+    def unpack_rows(self, rows, buf_t) -> None:
+        r = np.ascontiguousarray(rows, np.int32)
+        if buf_t.numel() < len(r) * 13 * self.width():
+            raise ValueError("unpack_rows: buffer too small")
+        check(self._lib.nrm_canvas_unpack_rows_device(self._h, _ptr(r), len(r), _tptr(buf_t)))
 
     def color(self, x: int, y: int) -> np.ndarray:
         return self.read(x, y, 1, 1)[0][0, 0]

@@ -93,8 +93,8 @@ def test_weighted_blend_rejects_shape_and_null(nrm, ctx, golden):
 
 
 def test_deform_edges(nrm, ctx, golden):
-    """Sources beyond the canvas leave pixels unoccupied; banded canvases are
-    refused (no halo exchange); bad regions are rejected."""
+    """Sources beyond the canvas leave pixels unoccupied; bad regions are
+    rejected (also on banded canvases)."""
     g = golden("blend_c1")
     poly = g["polys"][: g["npoly"][0]]
     cv = nrm.Canvas(ctx)
@@ -108,11 +108,13 @@ def test_deform_edges(nrm, ctx, golden):
     assert (wt1 == 0).all()
     with pytest.raises(ValueError):
         cv.deform(np.zeros((10, 10, 2), np.float32), x=w - 5, y=0)  # region outside the canvas
+    # banded canvases deform their own stripes (halo rows: dist.exchange_halo)
     banded = nrm.Canvas(ctx)
     banded.ensure_contains((0.0, 0.0, 300.0, 300.0))
     banded.set_band(0, 2)
+    banded.deform(np.zeros((8, 8, 2), np.float32))
     with pytest.raises(ValueError):
-        banded.deform(np.zeros((8, 8, 2), np.float32))
+        banded.deform(np.zeros((8, 8, 2), np.float32), x=-1)
 
 
 def test_rgba_frame_ignores_alpha(nrm, ctx, oracle, golden):
