@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <sstream>
 #include <stdexcept>
@@ -145,36 +146,57 @@ inline std::vector<MatchPair> detect_and_match(const ImageU8& image_a, const Ima
     return match_features(fa, fb, cfg.ratio_test, cfg.workers);
 }
 
-/// Match files (features.hpp:272-305): one match per line "ax ay bx by score",
-/// '#' comments, coordinates at full double precision.
+/// Match files: the reference's text format (features.hpp:272-305) -- one
+/// match per line "ax ay bx by score" at 17 significant digits (so doubles
+/// round-trip), '#' comment lines, the same error text for malformed lines --
+/// so files written by either implementation load in the other.
 inline void save_matches(const std::string& path, const std::vector<MatchPair>& matches) {
     std::ofstream out(path);
     if (!out) throw std::runtime_error("cannot write " + path);
-    out << "# ax ay bx by score\n";
-    char line[192];
-    for (const MatchPair& m : matches) {
-        std::snprintf(line, sizeof line, "%.17g %.17g %.17g %.17g %.17g\n", m.point_a.x, m.point_a.y, m.point_b.x,
-                      m.point_b.y, m.score);
-        out << line;
-    }
+    std::ostringstream text;
+    text.precision(17);  // default float field at precision 17 == printf %.17g
+    text << "# ax ay bx by score\n";
+    for (const MatchPair& m : matches)
+        text << m.point_a.x << ' ' << m.point_a.y << ' ' << m.point_b.x << ' ' << m.point_b.y << ' ' << m.score
+             << '\n';
+    out << text.str();
 }
 
 inline std::vector<MatchPair> load_matches(const std::string& path) {
     std::ifstream in(path);
     if (!in) throw std::runtime_error("cannot open " + path);
-    std::vector<MatchPair> out;
-    std::string text;
-    for (int lineno = 1; std::getline(in, text); ++lineno) {
-        const auto first = text.find_first_not_of(" \t\r");
-        if (first == std::string::npos || text[first] == '#') continue;
-        std::istringstream fields(text);
+    std::vector<MatchPair> result;
+    std::string row;
+    int number = 0;
+    while (std::getline(in, row)) {
+        ++number;
+        // tokens separated by blanks; a row of blanks or starting with '#' is skipped
+        std::vector<double> vals;
+        const char* c = row.c_str();
+        bool bad = false;
+        while (true) {
+            while (*c == ' ' || *c == '\t' || *c == '\r') ++c;
+            if (!*c) break;
+            if (vals.empty() && *c == '#') break;
+            char* end = nullptr;
+            const double v = std::strtod(c, &end);
+            if (end == c || (*end && *end != ' ' && *end != '\t' && *end != '\r')) {
+                bad = true;
+                break;
+            }
+            vals.push_back(v);
+            c = end;
+        }
+        if (vals.empty() && !bad) continue;
+        if (bad || vals.size() != 5)
+            throw std::runtime_error(path + ":" + std::to_string(number) + ": expected 5 fields 'ax ay bx by score'");
         MatchPair m;
-        double extra = 0.0;
-        if (!(fields >> m.point_a.x >> m.point_a.y >> m.point_b.x >> m.point_b.y >> m.score) || (fields >> extra))
-            throw std::runtime_error(path + ":" + std::to_string(lineno) + ": expected 5 fields 'ax ay bx by score'");
-        out.push_back(m);
+        m.point_a = Vec2{vals[0], vals[1]};
+        m.point_b = Vec2{vals[2], vals[3]};
+        m.score = vals[4];
+        result.push_back(m);
     }
-    return out;
+    return result;
 }
 
 }  // namespace nrmosaic

@@ -24,9 +24,16 @@
 // fieldest.hpp:263-270) as blend_local_points().
 //
 // Canvas pixels live in HBM. Canvas::color()/weight() read through a host
-// mirror that is downloaded lazily after GPU updates; writes through
-// color()/weight_ref() mark the mirror dirty and are uploaded before the next
-// GPU operation on that canvas (the explicit sync SURVEY §7 calls for).
+// mirror kept per 256 x 256 tile and downloaded lazily after GPU updates;
+// writes through color()/weight_ref() mark their tile dirty and are uploaded
+// before the next GPU operation on that canvas (the explicit sync SURVEY §7
+// calls for).
+//
+// Production callers that include both nrmosaic/mosaic.hpp and
+// nrmosaic/slam.hpp (which includes nrmosaic/mosaic.hpp itself, slam.hpp:16)
+// switch with an include path instead of an edit: -Iinclude/override ahead
+// of the reference's include directory makes every "nrmosaic/mosaic.hpp"
+// resolve to include/override/nrmosaic/mosaic.hpp, which forwards here.
 //
 // Types: by default Vec2, Rect, DualQuat2, WarpFunction and ImageU8 come
 // from the reference headers (nrmosaic/geometry.hpp, dualquat.hpp,
@@ -43,7 +50,10 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
+#include <utility>
 #include <vector>
+#include <algorithm>
 
 #include "nrm_b200.h"
 
@@ -203,6 +213,13 @@ inline std::vector<Vec2> invert_frame_boundary(int frame_w, int frame_h, std::sp
 }
 
 /// Canvas (mosaic.hpp:100-182), HBM-resident.
+///
+/// color()/weight()/weight_ref() go through a host mirror kept per 256 x 256
+/// canvas tile (Canvas::kTile): the first access to a tile after a GPU update
+/// downloads that tile only (1.6 MB), writes mark it dirty, and dirty tiles
+/// are uploaded before the next GPU operation on the canvas. Returned
+/// pointers stay valid until the next GPU operation or ensure_contains, like
+/// the reference's until its next reallocation.
 class Canvas {
 public:
     static constexpr int kWeightCap = 30;
@@ -217,9 +234,7 @@ public:
     Canvas(Canvas&& o) noexcept { *this = std::move(o); }
     Canvas& operator=(Canvas&& o) noexcept {
         std::swap(h_, o.h_);
-        std::swap(color_, o.color_);
-        std::swap(weight_, o.weight_);
-        std::swap(mirror_, o.mirror_);
+        std::swap(tiles_, o.tiles_);
         return *this;
     }
 
@@ -233,22 +248,22 @@ public:
     }
 
     double* color(int x, int y) {
-        pull();
-        mirror_ = Mirror::Dirty;
-        return &color_[(static_cast<std::size_t>(y) * width() + x) * 3];
+        Tile& t = tile(x, y);
+        t.dirty = true;
+        return &t.color[t.offset(x, y) * 3];
     }
     const double* color(int x, int y) const {
-        pull();
-        return &color_[(static_cast<std::size_t>(y) * width() + x) * 3];
+        const Tile& t = tile(x, y);
+        return &t.color[t.offset(x, y) * 3];
     }
     std::uint8_t weight(int x, int y) const {
-        pull();
-        return weight_[static_cast<std::size_t>(y) * width() + x];
+        const Tile& t = tile(x, y);
+        return t.weight[t.offset(x, y)];
     }
     std::uint8_t& weight_ref(int x, int y) {
-        pull();
-        mirror_ = Mirror::Dirty;
-        return weight_[static_cast<std::size_t>(y) * width() + x];
+        Tile& t = tile(x, y);
+        t.dirty = true;
+        return t.weight[t.offset(x, y)];
     }
     bool occupied(int x, int y) const { return weight(x, y) > 0; }
     std::int64_t occupied_count() const {
@@ -261,48 +276,67 @@ public:
     void ensure_contains(const Rect& r) {
         push();
         b200::check(nrm_canvas_ensure_contains(h_, r.x0, r.y0, r.x1, r.y1));
-        mirror_ = Mirror::Stale;
+        tiles_.clear();  // canvas coordinates may have shifted
     }
 
     /// B200 extensions: pre-allocate HBM for a region; band for multi-GPU.
     void reserve(const Rect& r) { b200::check(nrm_canvas_reserve(h_, r.x0, r.y0, r.x1, r.y1)); }
     void set_band(int rank, int count) { b200::check(nrm_canvas_set_band(h_, rank, count)); }
+    /// The C handle, after uploading host edits (call before any GPU operation).
     nrm_canvas* handle() const {
         push();
         return h_;
     }
-    void invalidate_mirror() { mirror_ = Mirror::Stale; }
+    /// Drops the host mirror (after a GPU update of the canvas).
+    void invalidate_mirror() { tiles_.clear(); }
 
 private:
-    enum class Mirror { Stale, Clean, Dirty };
     struct Info {
         std::int64_t ox, oy;
         int w, h;
+    };
+    struct Tile {
+        int x0 = 0, y0 = 0, w = 0, h = 0;
+        bool dirty = false;
+        std::vector<double> color;
+        std::vector<std::uint8_t> weight;
+        std::size_t offset(int x, int y) const {
+            return static_cast<std::size_t>(y - y0) * static_cast<std::size_t>(w) + static_cast<std::size_t>(x - x0);
+        }
     };
     Info info() const {
         Info i{};
         b200::check(nrm_canvas_info(h_, &i.ox, &i.oy, &i.w, &i.h));
         return i;
     }
-    void pull() const {
-        if (mirror_ != Mirror::Stale) return;
+    Tile& tile(int x, int y) const {
         const Info i = info();
-        color_.assign(static_cast<std::size_t>(i.w) * i.h * 3, 0.0);
-        weight_.assign(static_cast<std::size_t>(i.w) * i.h, 0);
-        if (i.w && i.h) b200::check(nrm_canvas_download(h_, 0, 0, i.w, i.h, color_.data(), weight_.data()));
-        mirror_ = Mirror::Clean;
+        if (x < 0 || y < 0 || x >= i.w || y >= i.h) throw std::out_of_range("Canvas: pixel outside the canvas");
+        const std::int64_t tx = x / kTile, ty = y / kTile;
+        const std::int64_t key = ty * ((i.w + kTile - 1) / kTile) + tx;
+        auto it = tiles_.find(key);
+        if (it != tiles_.end()) return it->second;
+        Tile t;
+        t.x0 = static_cast<int>(tx * kTile);
+        t.y0 = static_cast<int>(ty * kTile);
+        t.w = std::min(kTile, i.w - t.x0);
+        t.h = std::min(kTile, i.h - t.y0);
+        t.color.assign(static_cast<std::size_t>(t.w) * t.h * 3, 0.0);
+        t.weight.assign(static_cast<std::size_t>(t.w) * t.h, 0);
+        b200::check(nrm_canvas_download(h_, t.x0, t.y0, t.w, t.h, t.color.data(), t.weight.data()));
+        return tiles_.emplace(key, std::move(t)).first->second;
     }
     void push() const {
-        if (mirror_ != Mirror::Dirty) return;
-        const Info i = info();
-        b200::check(nrm_canvas_upload(h_, 0, 0, i.w, i.h, color_.data(), weight_.data()));
-        mirror_ = Mirror::Clean;
+        for (auto& [key, t] : tiles_) {
+            (void)key;
+            if (!t.dirty) continue;
+            b200::check(nrm_canvas_upload(h_, t.x0, t.y0, t.w, t.h, t.color.data(), t.weight.data()));
+            t.dirty = false;
+        }
     }
 
     nrm_canvas* h_ = nullptr;
-    mutable std::vector<double> color_;
-    mutable std::vector<std::uint8_t> weight_;
-    mutable Mirror mirror_ = Mirror::Stale;
+    mutable std::unordered_map<std::int64_t, Tile> tiles_;
 };
 
 struct BlendStats {

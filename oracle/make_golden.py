@@ -238,8 +238,32 @@ def features_cases():
     np.savez_compressed(OUT / "features.npz", **out)
 
 
+def pipeline_cases():
+    """The reference's production call sequence (tests/cpp/pipeline_dump.cpp:
+    detect -> match -> Engine::process_frame -> blend_frame -> render, as
+    tools/main.cpp run_mosaic) on its own 200-frame synthetic scenes, run by
+    oracle/_ref/pipeline_ref (unmodified reference headers); plus the
+    reference's own acceptance main (oracle/_ref/acceptance_ref) output."""
+    import subprocess
+    import tempfile
+    from oracle.pipeline_io import read_dump
+    exe = ROOT / "oracle" / "_ref" / "pipeline_ref"
+    for path in ("scan", "outback"):
+        with tempfile.TemporaryDirectory() as td:
+            out = Path(td) / "p.bin"
+            subprocess.run([str(exe), str(out), path, "200", "8"], check=True, capture_output=True)
+            d = read_dump(out)
+        np.savez_compressed(OUT / f"pipeline_{path}.npz", **d)
+        print(path, d["mosaic"].shape, int(d["blended"].sum()), "blends")
+    acc = subprocess.run([str(ROOT / "oracle" / "_ref" / "acceptance_ref")], capture_output=True, text=True)
+    (OUT / "acceptance_ref.txt").write_text(acc.stdout)
+    print(acc.stdout.splitlines()[-1])
+
+
 if __name__ == "__main__":
-    if sys.argv[1:] == ["estep"]:
+    if sys.argv[1:] == ["pipeline"]:
+        pipeline_cases()
+    elif sys.argv[1:] == ["estep"]:
         estep_cases()
     elif sys.argv[1:] == ["features"]:
         features_cases()
@@ -247,3 +271,4 @@ if __name__ == "__main__":
         main()
         estep_cases()
         features_cases()
+        pipeline_cases()

@@ -83,15 +83,50 @@ def build_oracle() -> None:
         _run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"])
 
 
+REF_INCLUDE = Path("/root/reference/proj/include")
+REF_TESTS = Path("/root/reference/proj/tests")
+
+
 def build_cpp_tests() -> None:
-    """C++ drop-in test (tests/cpp/test_shim.cpp) against the shim header."""
-    src = ROOT / "tests" / "cpp" / "test_shim.cpp"
-    if not src.exists():
+    """C++ drop-in tests, linked against libnrm_b200.so (rpath $ORIGIN):
+      tests/cpp/test_shim       -- the reference's test_mosaic.cpp suite on the
+                                   shim header, with the reference's own types
+                                   where the reference tree exists;
+      tests/cpp/pipeline_b200   -- tests/cpp/pipeline_dump.cpp (the reference's
+                                   production call sequence) compiled with
+                                   -Iinclude/override, i.e. unchanged sources
+                                   whose "nrmosaic/mosaic.hpp" is the B200 one;
+      tests/cpp/acceptance_b200 -- the reference's own tests/acceptance.cpp,
+                                   compiled the same way (reference tree only).
+    The binaries travel to the GPU box with the snapshot."""
+    cpp = ROOT / "tests" / "cpp"
+    rpath = "-Wl,-rpath,$ORIGIN/../../paper_2103_07414_b200"
+    link = [f"-L{PKG}", "-lnrm_b200", rpath, "-lpthread"]
+    have_ref = (REF_INCLUDE / "nrmosaic" / "mosaic.hpp").exists()
+    shim = ROOT / "include" / "nrmosaic_b200" / "mosaic.hpp"
+    override = ROOT / "include" / "override" / "nrmosaic" / "mosaic.hpp"
+    src = cpp / "test_shim.cpp"
+    out = cpp / "test_shim"
+    if src.exists() and _stale(out, [src, LIB, shim]):
+        types = ["-include", "algorithm", "-include", "memory", f"-I{ROOT / 'oracle' / 'stub'}",
+                 f"-I{REF_INCLUDE}"] if have_ref else ["-DNRM_B200_STANDALONE_TYPES"]
+        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", *types, str(src), "-o", str(out), *link])
+    if not have_ref:
         return
-    out = ROOT / "tests" / "cpp" / "test_shim"
-    if _stale(out, [src, LIB, ROOT / "include" / "nrmosaic_b200" / "mosaic.hpp"]):
-        _run(["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", "-DNRM_B200_STANDALONE_TYPES",
-              str(src), "-o", str(out), f"-L{PKG}", "-lnrm_b200", f"-Wl,-rpath,{PKG}"])
+    common = ["g++", "-std=c++20", "-O2", "-DNDEBUG", "-include", "algorithm", "-include", "memory",
+              f"-I{ROOT / 'include' / 'override'}", f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle' / 'stub'}",
+              f"-I{REF_INCLUDE}", f"-I{REF_TESTS}"]
+    jobs = []
+    for name, source in (("pipeline_b200", cpp / "pipeline_dump.cpp"),
+                         ("acceptance_b200", REF_TESTS / "acceptance.cpp")):
+        out = cpp / name
+        deps = [source, LIB, shim, override, ROOT / "include" / "nrmosaic_b200" / "features.hpp",
+                ROOT / "include" / "override" / "nrmosaic" / "features.hpp"]
+        if _stale(out, deps):
+            jobs.append([*common, str(source), "-o", str(out), *link])
+    if jobs:
+        with ThreadPoolExecutor(max_workers=2) as ex:
+            list(ex.map(_run, jobs))
 
 
 def main() -> None:
