@@ -260,9 +260,47 @@ def pipeline_cases():
     print(acc.stdout.splitlines()[-1])
 
 
+def c3_sequence_case(nframes=200):
+    """BASELINE configs[2] (C3) at full size through the REFERENCE: 200 1080p
+    frames along a serpentine scan into the 8192^2 canvas (the sequence of
+    tests/test_gpu_sequence.py: the C2 frame and its flip alternating, the
+    C2 frame lattice moved with each frame), blended by the reference's
+    blend_frame with its own invert_frame_boundary footprints. Stored: the
+    lattice inputs (so the GPU test does not depend on host linear algebra),
+    the frame's SHA, per-frame BlendStats, the final canvas geometry, the
+    SHA of the weight plane, and colour / render values at 200k seeded
+    occupied pixels."""
+    R = Reference()
+    wl = W.frame_workload("c2")
+    offs = W.scan_offsets(nframes, wl.frame_w, wl.frame_h, wl.canvas)
+    frames = [wl.frame, np.ascontiguousarray(wl.frame[::-1])]
+    cv = R.canvas()
+    stats = []
+    for k, (tx, ty) in enumerate(offs):
+        anchors = wl.anchors + np.array([tx, ty])
+        warps = W.shifted_warps(wl.warps, tx, ty)
+        poly = R.invert_frame_boundary(wl.frame_w, wl.frame_h, anchors, warps, wl.params.alpha)
+        stats.append(R.blend_frame(cv, frames[k % 2], anchors, warps, wl.params.alpha, poly, workers=8))
+    ox, oy, w, h = cv.info()
+    col, wt = cv.arrays()
+    full, _ = R.render(cv, crop=False)
+    rng = np.random.default_rng(3)
+    occ = np.flatnonzero(wt.reshape(-1) > 0)
+    pick = np.sort(rng.choice(occ, min(200_000, len(occ)), replace=False))
+    ys, xs = np.divmod(pick, w)
+    np.savez_compressed(
+        OUT / "c3_sequence.npz", anchors=wl.anchors, warps=wl.warps, alpha=wl.params.alpha, offsets=offs,
+        frame_sha=sha(wl.frame), stats=np.array(stats, np.int64), info=np.array([ox, oy, w, h], np.int64),
+        weight_sha=sha(wt), occupied=np.int64(len(occ)), sample_xy=np.stack([xs, ys], 1).astype(np.int32),
+        sample_color=col.reshape(-1, 3)[pick], sample_render=full.reshape(-1, 4)[pick])
+    print("c3", (ox, oy, w, h), "occupied", len(occ), "blended", int(np.array(stats)[:, 1].sum()))
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["pipeline"]:
         pipeline_cases()
+    elif sys.argv[1:] == ["c3"]:
+        c3_sequence_case()
     elif sys.argv[1:] == ["estep"]:
         estep_cases()
     elif sys.argv[1:] == ["features"]:
@@ -272,3 +310,4 @@ if __name__ == "__main__":
         estep_cases()
         features_cases()
         pipeline_cases()
+        c3_sequence_case()

@@ -288,6 +288,9 @@ static int blend_frame_impl(orc_canvas *cv, const uint8_t *frame, int fw, int fh
 
     const double fx_max = fw - 1.0, fy_max = fh - 1.0;
     int64_t blended = 0, no_support = 0, out_of_frame = 0;
+    /* rows are independent (each pixel is written once; the counts are
+     * order-free integer sums), so OpenMP rows give the serial result */
+#pragma omp parallel for schedule(dynamic, 4) reduction(+ : blended, no_support, out_of_frame)
     for (int ry = 0; ry < bh; ++ry) {
         const int cy = py0 + ry;
         const double ref_y = orgy + cy;
@@ -512,31 +515,24 @@ static int key_less(double da, int ja, double db, int jb) {
     return da < db || (!(db < da) && ja < jb);
 }
 
-int orc_blend_local(const double *locals, const double *apts, const double *probs,
-                    const int32_t *active, int nactive, double qx, double qy, double alpha,
-                    int support, double *out5) {
-    if (nactive <= 0 || support <= 0) return -1;
-    if (support > ORC_MAX_SUPPORT) support = ORC_MAX_SUPPORT;
-    const int kk = support < nactive ? support : nactive;
-    /* partial_sort of the first kk (d2, j) keys: bounded insertion gives the
-     * same (unique) prefix since keys are distinct in j. */
-    double kd[ORC_MAX_SUPPORT];
-    int kj[ORC_MAX_SUPPORT];
-    int cnt = 0;
-    for (int a = 0; a < nactive; ++a) {
-        const int j = active[a];
-        const double ex = qx - apts[2 * j], ey = qy - apts[2 * j + 1];
-        const double d2 = ex * ex + ey * ey;
-        if (cnt == kk && !key_less(d2, j, kd[kk - 1], kj[kk - 1])) continue;
-        int pos = cnt < kk ? cnt++ : kk - 1;
-        while (pos > 0 && key_less(d2, j, kd[pos - 1], kj[pos - 1])) {
-            kd[pos] = kd[pos - 1];
-            kj[pos] = kj[pos - 1];
-            --pos;
-        }
-        kd[pos] = d2;
-        kj[pos] = j;
+/* Inserts key (d2, j) into the sorted kk-prefix kd/kj holding cnt keys:
+ * partial_sort of the first kk (d2, j) keys, as a bounded insertion (keys
+ * are distinct in j, so the prefix is unique). */
+static void knn_insert(double d2, int j, double *kd, int *kj, int *cnt, int kk) {
+    if (*cnt == kk && !key_less(d2, j, kd[kk - 1], kj[kk - 1])) return;
+    int pos = *cnt < kk ? (*cnt)++ : kk - 1;
+    while (pos > 0 && key_less(d2, j, kd[pos - 1], kj[pos - 1])) {
+        kd[pos] = kd[pos - 1];
+        kj[pos] = kj[pos - 1];
+        --pos;
     }
+    kd[pos] = d2;
+    kj[pos] = j;
+}
+
+/* The blend of fieldest.hpp:86-96 over the kk selected keys (ascending). */
+static int blend_keys(const double *locals, const double *probs, const double *kd, const int *kj, int kk,
+                      double alpha, double *out5) {
     const double d2min = kd[0];
     double w[ORC_MAX_SUPPORT];
     for (int i = 0; i < kk; ++i) {
@@ -572,6 +568,23 @@ int orc_blend_local(const double *locals, const double *apts, const double *prob
     return 0;
 }
 
+int orc_blend_local(const double *locals, const double *apts, const double *probs,
+                    const int32_t *active, int nactive, double qx, double qy, double alpha,
+                    int support, double *out5) {
+    if (nactive <= 0 || support <= 0) return -1;
+    if (support > ORC_MAX_SUPPORT) support = ORC_MAX_SUPPORT;
+    const int kk = support < nactive ? support : nactive;
+    double kd[ORC_MAX_SUPPORT];
+    int kj[ORC_MAX_SUPPORT];
+    int cnt = 0;
+    for (int a = 0; a < nactive; ++a) {
+        const int j = active[a];
+        const double ex = qx - apts[2 * j], ey = qy - apts[2 * j + 1];
+        knn_insert(ex * ex + ey * ey, j, kd, kj, &cnt, kk);
+    }
+    return blend_keys(locals, probs, kd, kj, kk, alpha, out5);
+}
+
 /* node_uncertainty (fieldest.hpp:44-52) with bounded_exp (geometry.hpp:85-88). */
 double orc_node_uncertainty(double qx, double qy, const double *pts, int m, double beta) {
     if (!(beta > 0.0) || m <= 0) return NAN;
@@ -592,6 +605,7 @@ double orc_node_uncertainty(double qx, double qy, const double *pts, int m, doub
 void orc_node_field_grid(double x0, double y0, int w, int h, const double *anchors,
                          const double *warps, int n, double alpha, double *disp,
                          uint8_t *support) {
+#pragma omp parallel for schedule(dynamic, 1)
     for (int j = 0; j < h; ++j)
         for (int i = 0; i < w; ++i) {
             const double px = x0 + i, py = y0 + j;
@@ -640,6 +654,120 @@ int orc_emdq_field_grid(double x0, double y0, int w, int h, const double *apts,
         }
     free(pts);
     return rc;
+}
+
+/* The same dense EMDQ field with a uniform-grid kNN search (cells of about
+ * four candidates, rings searched outward until the next ring cannot hold a
+ * key below the current k-th) and OpenMP over rows. The kk selected keys,
+ * their order and all arithmetic are those of orc_blend_local /
+ * orc_node_uncertainty, so every output is bit-identical to the full scan
+ * (tests/test_oracle_golden.py checks it); it only makes the canvas-scale
+ * configurations (C2 / C4 / C5 full frames) checkable in seconds. The
+ * uncertainty is bounded_exp(beta * d2) of the nearest key: the minimum over
+ * all candidates of the same d2 expression node_uncertainty evaluates. */
+int orc_emdq_field_grid_fast(double x0, double y0, int w, int h, const double *apts,
+                             const double *locals, const double *probs, const int32_t *active,
+                             int nactive, double alpha, int support, double beta, double *disp,
+                             double *unc, int row_begin, int row_end) {
+    if (nactive <= 0 || support <= 0) return -1;
+    if (support > ORC_MAX_SUPPORT) support = ORC_MAX_SUPPORT;
+    const int kk = support < nactive ? support : nactive;
+    double bx0 = DBL_MAX, by0 = DBL_MAX, bx1 = -DBL_MAX, by1 = -DBL_MAX;
+    for (int a = 0; a < nactive; ++a) {
+        const double px = apts[2 * active[a]], py = apts[2 * active[a] + 1];
+        bx0 = px < bx0 ? px : bx0;
+        by0 = py < by0 ? py : by0;
+        bx1 = px > bx1 ? px : bx1;
+        by1 = py > by1 ? py : by1;
+    }
+    const double area = (bx1 - bx0 + 1.0) * (by1 - by0 + 1.0);
+    double cs = sqrt(4.0 * area / nactive);
+    if (!(cs >= 1.0)) cs = 1.0;
+    int gw = (int)((bx1 - bx0) / cs) + 1, gh = (int)((by1 - by0) / cs) + 1;
+    if (gw > 4096) gw = 4096;
+    if (gh > 4096) gh = 4096;
+    const double csx = (bx1 - bx0) / gw + 1e-9, csy = (by1 - by0) / gh + 1e-9;
+    int *start = (int *)calloc((size_t)gw * gh + 1, sizeof(int));
+    int *items = (int *)malloc(sizeof(int) * (size_t)nactive);
+    int *fill = (int *)calloc((size_t)gw * gh, sizeof(int));
+    if (!start || !items || !fill) { free(start); free(items); free(fill); return -1; }
+#define ORC_CELL(px, py, cx, cy)                                        \
+    do {                                                                \
+        cx = (int)(((px) - bx0) / csx); cy = (int)(((py) - by0) / csy); \
+        cx = cx < 0 ? 0 : (cx >= gw ? gw - 1 : cx);                     \
+        cy = cy < 0 ? 0 : (cy >= gh ? gh - 1 : cy);                     \
+    } while (0)
+    for (int a = 0; a < nactive; ++a) {
+        int cx, cy;
+        ORC_CELL(apts[2 * active[a]], apts[2 * active[a] + 1], cx, cy);
+        ++start[(size_t)cy * gw + cx + 1];
+    }
+    for (size_t c = 0; c < (size_t)gw * gh; ++c) start[c + 1] += start[c];
+    for (int a = 0; a < nactive; ++a) {
+        int cx, cy;
+        ORC_CELL(apts[2 * active[a]], apts[2 * active[a] + 1], cx, cy);
+        const size_t c = (size_t)cy * gw + cx;
+        items[start[c] + fill[c]++] = active[a];
+    }
+    free(fill);
+    if (row_begin < 0) row_begin = 0;
+    if (row_end > h || row_end < 0) row_end = h;
+    const double cmin = csx < csy ? csx : csy;
+    int rc = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : rc)
+    for (int j = row_begin; j < row_end; ++j) {
+        for (int i = 0; i < w; ++i) {
+            const double qx = x0 + i, qy = y0 + j;
+            const size_t o = (size_t)j * w + i;
+            double kd[ORC_MAX_SUPPORT];
+            int kj[ORC_MAX_SUPPORT];
+            int cnt = 0, cx, cy;
+            ORC_CELL(qx, qy, cx, cy);
+            /* distance from q to the boundary of its (clamped) cell block */
+            const double ox = qx < bx0 ? bx0 - qx : (qx > bx1 ? qx - bx1 : 0.0);
+            const double oy = qy < by0 ? by0 - qy : (qy > by1 ? qy - by1 : 0.0);
+            const double outside2 = ox * ox + oy * oy; /* every candidate is at least this far (squared) */
+            for (int r = 0;; ++r) {
+                const int xa = cx - r, xb = cx + r, ya = cy - r, yb = cy + r;
+                for (int yy = ya; yy <= yb; ++yy) {
+                    if (yy < 0 || yy >= gh) continue;
+                    const int step = (yy == ya || yy == yb) ? 1 : (xb - xa > 0 ? xb - xa : 1);
+                    for (int xx = xa; xx <= xb; xx += step) {
+                        if (xx < 0 || xx >= gw) continue;
+                        const size_t c = (size_t)yy * gw + xx;
+                        for (int t = start[c]; t < start[c + 1]; ++t) {
+                            const int jj = items[t];
+                            const double ex = qx - apts[2 * jj], ey = qy - apts[2 * jj + 1];
+                            knn_insert(ex * ex + ey * ey, jj, kd, kj, &cnt, kk);
+                        }
+                    }
+                }
+                if (xa <= 0 && ya <= 0 && xb >= gw - 1 && yb >= gh - 1) break; /* every cell seen */
+                if (cnt == kk) {
+                    /* a candidate outside rings 0..r lies r full cells away
+                     * along one axis, and never closer than the bbox on either:
+                     * d2 >= ox^2 + oy^2 + (r cmin)^2 */
+                    const double lim2 = outside2 + (r * cmin) * (r * cmin);
+                    if (lim2 * (1.0 - 1e-9) > kd[kk - 1]) break;
+                }
+            }
+            double wp[5], yv[2];
+            if (blend_keys(locals, probs, kd, kj, kk, alpha, wp)) {
+                rc = 1;
+                continue;
+            }
+            orc_warp_apply(wp, qx, qy, yv);
+            disp[2 * o] = yv[0] - qx;
+            disp[2 * o + 1] = yv[1] - qy;
+            double arg = beta * kd[0];
+            if (55.0 < arg) arg = 55.0;
+            unc[o] = exp(arg);
+        }
+    }
+#undef ORC_CELL
+    free(start);
+    free(items);
+    return rc ? -1 : 0;
 }
 
 /* ==========================================================================

@@ -99,6 +99,11 @@ int orc_emdq_field_grid(double x0, double y0, int w, int h, const double *apts,
                         const double *locals, const double *probs, const int32_t *active,
                         int nactive, double alpha, int support, double beta, double *disp,
                         double *unc, int row_begin, int row_end);
+/* orc_emdq_field_grid with a grid kNN search and OpenMP rows: bit-identical. */
+int orc_emdq_field_grid_fast(double x0, double y0, int w, int h, const double *apts,
+                             const double *locals, const double *probs, const int32_t *active,
+                             int nactive, double alpha, int support, double beta, double *disp,
+                             double *unc, int row_begin, int row_end);
 
 /* ---- sparse front end (features.hpp), FP32 as the
  * reference computes it (no contraction) ---------------------------------- */

@@ -66,6 +66,7 @@ class Oracle:
         L.orc_node_uncertainty.restype = _D
         L.orc_node_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _I, _D, _P, _P]
         L.orc_emdq_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P, _I, _I]
+        L.orc_emdq_field_grid_fast.argtypes = [_D, _D, _I, _I, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P, _I, _I]
         L.orc_to_gray.argtypes = [_P, _I, _I, _I, _P]
         L.orc_detect_features.argtypes = [_P, _I, _I, _I, _D, _I, _P, _P]
         L.orc_match_features.argtypes = [_P, _P, _I, _P, _P, _I, _D, _P]
@@ -208,7 +209,8 @@ class Oracle:
         return disp, sup
 
     def emdq_field_grid(self, grid, apts, locals_, probs, active, alpha, beta, support=16,
-                        rows: Optional[tuple] = None):
+                        rows: Optional[tuple] = None, fast: bool = False):
+        """fast=True: the grid-kNN / OpenMP variant (bit-identical outputs)."""
         x0, y0, w, h = grid
         ap, lo = _f64(apts, 2), _f64(locals_, 5)
         pr = np.ascontiguousarray(probs, np.float64)
@@ -216,7 +218,8 @@ class Oracle:
         disp = np.zeros((h, w, 2))
         unc = np.zeros((h, w))
         r0, r1 = rows if rows else (0, h)
-        self.L.orc_emdq_field_grid(float(x0), float(y0), w, h, _p(ap), _p(lo), _p(pr), _p(ac), len(ac),
+        fn = self.L.orc_emdq_field_grid_fast if fast else self.L.orc_emdq_field_grid
+        fn(float(x0), float(y0), w, h, _p(ap), _p(lo), _p(pr), _p(ac), len(ac),
                                    float(alpha), int(support), float(beta), _p(disp), _p(unc), r0, r1)
         return disp, unc
 

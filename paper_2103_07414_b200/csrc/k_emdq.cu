@@ -80,6 +80,8 @@ constexpr int TREC = 64;          // staged records per tile (in + ambiguous)
 constexpr int TCAND = 128;        // tile candidates before classification
 constexpr int PLAN_WARPS = 8;     // planning warps (tiles) per CTA
 constexpr int TFLAG_EXACT_SUPER = 1, TFLAG_EXACT_STAGED = 2;
+constexpr double kLocalMax = 256.0;    // px: staged tile-local coordinates (|u| < 2^8, ulp 2^-15)
+constexpr double kScaleLever = 640.0;  // px: max S |P| for the fast tier (k_nodefield.cu)
 constexpr int NEAR_CAP = 8;       // per sub-tile: candidates that can be the nearest
 
 // Per-tile plan written by k_plan, read by k_pixels (one 16 x 16 tile).
@@ -671,9 +673,11 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     float4* r1g = tp.rec1;
     int* sg = tp.sidx;
     float d2lo = FLT_MAX, d2hi = 0.f;
+    double sdev = 0.0, umax = 0.0;
     for (int k = lane; k < ne; k += 32) {
         const int a = w.sidx[k];
         const W5 q = load_w5(&C.l[5 * a]);
+        sdev = fmax(sdev, fabs(q.s - s0));
         const double hx = 0.5 * ox, hy = 0.5 * oy;
         const double qa_dx = (q.w * hx - q.z * hy) + q.dx;  // q * T(o)
         const double qa_dy = (q.w * hy + q.z * hx) + q.dy;
@@ -681,6 +685,7 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
         r1g[k] = make_float4((float)q.w, (float)q.z, (float)(qa_dx + (-px * q.w - py * q.z)),
                              (float)(qa_dy + (px * q.z - py * q.w)));
         const double ux = C.x[a] - ox, uy = C.y[a] - oy;
+        umax = fmax(umax, fmax(fabs(ux), fabs(uy)));
         r0g[k] = make_float4((float)ux, (float)uy, (float)C.p[a], (float)(q.s - s0));
         sg[k] = a;
         tp.axy[k] = make_double2(C.x[a], C.y[a]);
@@ -695,8 +700,16 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     for (int d = 16; d > 0; d >>= 1) {
         d2lo = fminf(d2lo, __shfl_xor_sync(0xffffffffu, d2lo, d));
         d2hi = fmaxf(d2hi, __shfl_xor_sync(0xffffffffu, d2hi, d));
+        sdev = fmax(sdev, __shfl_xor_sync(0xffffffffu, sdev, d));
+        umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, d));
     }
     if ((float)L.alpha * (d2hi - d2lo) >= 60.f) flags |= TFLAG_EXACT_STAGED;
+    // Margins of the FP32 tier: tile-local coordinates below
+    // kLocalMax px carry <= 2^-9 ulp ~ 1.5e-5 px of rounding, which the d^2
+    // tolerance d2_tol covers; and the field error model of the node field
+    // (k_nodefield.cu kScaleLever) bounds the scale lever S |P|.
+    if (umax >= kLocalMax || sdev * (fmax(fabs(P0), fabs(P1)) + 2.0 * ET) > kScaleLever)
+        flags |= TFLAG_EXACT_STAGED;
     __syncwarp();
 
     // 6. per sub-tile refinement of the tile-ambiguous (FP32, conservative margins)

@@ -5,10 +5,14 @@
   uncertainty-weighted rule (the EMDQ field's per-pixel uncertainty of the
   frame) and compared with the C restatement: per-frame BlendStats and the
   weight plane exact, colour within 1e-3.
-* C3 at full size (200 1080p frames into an 8192^2 canvas), GPU only, via
-  size-independent properties: the weighted rule with u == 1 equals the
-  reference rule bit for bit over the whole sequence, and 4 block-cyclic
-  bands assemble to the single canvas bit for bit."""
+* C3 at full size (200 1080p frames into an 8192^2 canvas) against the
+  REFERENCE (golden c3_sequence.npz from oracle/_ref, oracle/make_golden.py):
+  every frame's BlendStats and the final weight plane exact, colour within
+  1e-3 and the rendered mosaic within +-1 level at 200k sampled pixels --
+  through blend_frame and through the weighted extension with u == 1;
+* the same sequence via size-independent properties: the weighted rule with
+  u == 1 equals the reference rule bit for bit over the whole sequence, and 4
+  block-cyclic bands assemble to the single canvas bit for bit."""
 import numpy as np
 import pytest
 
@@ -47,6 +51,44 @@ def test_c3_small_sequence_weighted_matches_oracle(nrm, ctx, oracle):
     assert np.array_equal(wt, owt)
     assert np.abs(col.astype(np.float64) - ocol).max() <= COLOR_TOL
     assert (wt > 1).sum() > 0.3 * (wt > 0).sum()  # the footprints overlap
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_c3_full_sequence_matches_reference(nrm, ctx, golden, weighted):
+    import hashlib
+    import torch
+    g = golden("c3_sequence")
+    wl = W.frame_workload("c2")
+    assert hashlib.sha256(np.ascontiguousarray(wl.frame).tobytes()).hexdigest() == str(g["frame_sha"]), \
+        "the synthetic C2 frame differs from the one the golden was made with"
+    fw, fh, alpha = wl.frame_w, wl.frame_h, float(g["alpha"])
+    assert np.array_equal(W.scan_offsets(len(g["offsets"]), fw, fh, wl.canvas), g["offsets"])
+    dev = torch.device("cuda", 0)
+    frames_t = [torch.from_numpy(np.ascontiguousarray(f)).to(dev) for f in (wl.frame, wl.frame[::-1])]
+    ones_t = torch.ones((fh, fw), dtype=torch.float32, device=dev) if weighted else None
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    cv = nrm.Canvas(ctx)
+    st = torch.zeros((len(g["offsets"]), 4), dtype=torch.int64, device=dev)
+    torch.cuda.synchronize()
+    for k, (tx, ty) in enumerate(g["offsets"]):
+        anchors = g["anchors"] + np.array([tx, ty])
+        warps = W.shifted_warps(g["warps"], tx, ty)
+        poly = nrm.invert_frame_boundary(fw, fh, anchors, warps, alpha, ctx=ctx)
+        a_t, q_t = T(anchors), T(warps)
+        torch.cuda.synchronize()
+        nrm.blend_frame_device(cv, frames_t[k % 2], fw, fh, 3, a_t, q_t, alpha, poly, st[k], unc_t=ones_t)
+    ctx.synchronize()
+    assert np.array_equal(st.cpu().numpy(), g["stats"]), "per-frame BlendStats differ from the reference"
+    ox, oy = cv.origin_offset()
+    assert (int(ox), int(oy), cv.width(), cv.height()) == tuple(int(v) for v in g["info"])
+    col, wt = cv.read()
+    assert hashlib.sha256(wt.tobytes()).hexdigest() == str(g["weight_sha"]), "weight plane differs"
+    xs, ys = g["sample_xy"][:, 0], g["sample_xy"][:, 1]
+    assert np.abs(col[ys, xs].astype(np.float64) - g["sample_color"]).max() <= COLOR_TOL
+    del col
+    img, _ = nrm.render(cv, crop=False)
+    assert np.abs(img[ys, xs].astype(np.int16) - g["sample_render"].astype(np.int16)).max() <= 1
+    assert int((img[..., 3] > 0).sum()) == int(g["occupied"])
 
 
 def _planes_equal(a, b, rows=512):

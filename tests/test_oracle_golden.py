@@ -211,3 +211,42 @@ def test_features_reference_test_semantics(golden):
     assert len(g["noise_m80"]) < min(len(g["noise_kpa"]), len(g["noise_kpb"])) // 5 + 5
     assert len(g["tiny_kpa"]) == 0 and len(g["tiny_m80"]) == 0
     assert len(g["translate_m60"]) <= len(g["translate_m80"]) <= len(g["translate_m95"])
+
+
+def test_fast_emdq_grid_reproduces_the_reference_golden(oracle, golden):
+    """orc_emdq_field_grid_fast (grid kNN + OpenMP rows), the checker the
+    full-frame C2/C4/C5 GPU tests use, reproduces the reference's dense C1
+    field bit for bit (golden SHA from oracle/_ref)."""
+    g = golden("emdq_c1")
+    x0, y0, w, h = g["grid"]
+    disp, unc = oracle.emdq_field_grid((x0, y0, int(w), int(h)), g["apts"], g["locals"], g["probs"], g["active"],
+                                       float(g["alpha"]), float(g["beta"]), 16, fast=True)
+    assert sha(disp) == str(g["disp_sha"])
+    assert sha(unc) == str(g["unc_sha"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fast_emdq_grid_equals_full_scan(oracle, seed):
+    """Clustered / duplicated candidates (index tie-breaks), queries far outside
+    the candidates' box, support 1..32, canvas-scale coordinates: the grid
+    search selects the same keys in the same order as the full scan."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    m = n + 5
+    off = np.array([0.0, 0.0]) if seed % 3 == 0 else rng.uniform(8000, 32000, 2) * rng.choice([-1, 1], 2)
+    apts = np.round(rng.normal(0, 60, (m, 2)) * 4) / 4 + off
+    if seed % 2:
+        apts[: n // 2] = apts[n // 2: 2 * (n // 2)]  # exact duplicates: (d2, j) ties
+    loc = np.zeros((m, 5))
+    ang = rng.uniform(-3, 3, m)
+    loc[:, 0] = rng.uniform(0.5, 2, m)
+    loc[:, 1], loc[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    loc[:, 3:] = rng.normal(0, 5, (m, 2))
+    pr = rng.uniform(0, 1, m)
+    pr[::7] = 0.0
+    act = np.sort(rng.choice(m, n, replace=False)).astype(np.int32)
+    grid = (off[0] - 300.5, off[1] - 200.25, 257, 181)
+    for sup in (1, 7, 16, 32):
+        a = oracle.emdq_field_grid(grid, apts, loc, pr, act, 1e-3, 2e-3, sup)
+        b = oracle.emdq_field_grid(grid, apts, loc, pr, act, 1e-3, 2e-3, sup, fast=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), sup
