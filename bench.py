@@ -14,8 +14,13 @@ the launching stream, L2 flushed between steps with a 256 MiB write).
 e2e:   the same step through the host-pointer C ABI (pinned host buffers): frame,
        control points and matches H2D, the field + uncertainty and BlendStats D2H.
 N > 1: one process per GPU (torchrun); each step is a batch of N frames; rank r
-computes the EMDQ field of frame r and blends all N frames into the block-cyclic
+computes the EMDQ field of frame r, the N frames' control points are
+all-gathered (NCCL), and every rank blends all N frames into the block-cyclic
 64-row canvas stripes it owns (weak scaling); BlendStats are all-reduced (NCCL).
+--mode canvas: the configs[3]/[4] canvas-wide pass instead -- per step the node
+lattice is broadcast, each rank computes the node field on its stripes of the
+canvas, exchanges halo rows with its neighbours (NCCL send/recv) and deforms its
+stripes (run_canvas_mode).
 """
 from __future__ import annotations
 
@@ -254,11 +259,19 @@ def main():
     ap.add_argument("--no-features", action="store_true", help="skip the feature detection / matching side measurement")
     ap.add_argument("--e2e-inflight", type=int, default=2,
                     help="EMDQ field calls in flight in the e2e loop (own context + pinned outputs each)")
+    ap.add_argument("--mode", default="frame", choices=["frame", "canvas"],
+                    help="frame: the headline per-frame step; canvas: canvas-wide node field + canvas "
+                         "deformation over row bands (configs[3]/[4] canvas, --canvas px)")
+    ap.add_argument("--canvas", type=int, default=0, help="canvas mode: canvas size (default 16384 c4, 32768 c5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference_arm(args, args.config)
+    if env_int("WORLD_SIZE", 1) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator ranks visible in the log
+    if args.mode == "canvas":
+        return run_canvas_mode(args)
 
     import torch
     import torch.distributed as dist
@@ -325,8 +338,17 @@ def main():
         cv.set_band(rank, world)
 
     frame_t = torch.from_numpy(np.ascontiguousarray(wl.frame)).to(dev)
-    anc_t = [torch.from_numpy(a).to(dev) for a in anchors_k]
-    war_t = [torch.from_numpy(q).to(dev) for q in warps_k]
+    # control points: rank r holds frame r's node graph (its host SLAM / EM
+    # produced it); every step all-gathers them (NCCL over NVLink), since each
+    # rank blends every frame into its stripes. The per-frame
+    # anchors / warps tensors are views into the gathered buffer.
+    nn_ = len(wl.anchors)
+    nodes_mine = torch.from_numpy(np.concatenate([anchors_k[rank].ravel(), warps_k[rank].ravel()])).to(dev)
+    nodes_all = torch.zeros((nfr, 7 * nn_), dtype=torch.float64, device=dev)
+    for k in range(nfr):  # untimed initial fill (the timed step refreshes it)
+        nodes_all[k] = torch.from_numpy(np.concatenate([anchors_k[k].ravel(), warps_k[k].ravel()]))
+    anc_t = [nodes_all[k, :2 * nn_].view(nn_, 2) for k in range(nfr)]
+    war_t = [nodes_all[k, 2 * nn_:].view(nn_, 5) for k in range(nfr)]
     apts_t = torch.from_numpy(e.apts).to(dev)
     loc_t = torch.from_numpy(e.locals_).to(dev)
     prob_t = torch.from_numpy(e.probs).to(dev)
@@ -347,15 +369,35 @@ def main():
         else:
             M.blend_frames_device(cv, [frame_t] * nfr, fw, fh, 3, anc_t, war_t, alpha, polys, stats_t)
 
+    def gather_nodes():
+        """All-gather of the step's control points; returns a handle whose
+        wait() orders the caller's current stream after it."""
+        if world == 1:
+            return None
+        if functional:  # gloo: host staging
+            stream.synchronize()
+            parts = [torch.empty(7 * nn_, dtype=torch.float64) for _ in range(world)]
+            dist.all_gather(parts, nodes_mine.cpu())
+            nodes_all.copy_(torch.stack(parts).to(dev))
+            return None
+        return dist.all_gather_into_tensor(nodes_all, nodes_mine, async_op=True)
+
     def step(timed: bool, overlap: bool = True):
         if timed:
             flush.fill_(1)  # L2 flush (untimed): 256 MiB > 126 MB L2
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
+        work = gather_nodes()  # overlaps K3 (which needs only this rank's own matches)
         if overlap:
             stream_b.wait_event(e0)  # K1 on stream B starts with K3 on stream A
         M.emdq_field_device(grid, apts_t, loc_t, prob_t, act_t, alpha, beta, disp_t, unc_t, 16, ctx=ctx)
         e1.record(stream)
+        if work is not None:
+            if overlap:
+                with torch.cuda.stream(stream_b):
+                    work.wait()
+            else:
+                work.wait()
         blend_all()
         if overlap:
             eb = torch.cuda.Event()
@@ -621,6 +663,231 @@ def main():
     return 0
 
 
+def canvas_lattice(n: int, seed: int = 5):
+    """Canvas-covering node lattice at the 4K frame scale (hex 480 px, alpha
+    3.125e-6) over an n x n canvas, with a smooth synthetic deformation: node
+    scales 1 +- 0.01 and rotations +- 0.01 rad varying over ~10k px, a few px
+    of translation. Smooth like a SLAM node graph (neighbouring nodes carry
+    similar warps)."""
+    from paper_2103_07414_b200 import workload as W
+    sp = W.scaled_params(3840, 2160)
+    anchors = W.hex_lattice((0.0, 0.0, float(n), float(n)), sp.hex_spacing)
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(0, 2 * np.pi, 6)
+    x, y = anchors[:, 0] / 10000.0, anchors[:, 1] / 10000.0
+    sc = 1.0 + 0.01 * np.sin(x + ph[0]) * np.cos(y + ph[1])
+    ang = 0.01 * np.sin(0.7 * x + ph[2] + 1.3 * y)
+    warps = np.zeros((len(anchors), 5))
+    warps[:, 0] = sc
+    warps[:, 1], warps[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    # translations chosen so the field x -> s R x + t displaces by a few px
+    disp = np.stack([3.0 * np.sin(2 * x + ph[4]), 3.0 * np.cos(2 * y + ph[5])], 1)
+    c, s_ = np.cos(ang), np.sin(ang)
+    tx = (anchors[:, 0] + disp[:, 0]) / sc - (c * anchors[:, 0] - s_ * anchors[:, 1])
+    ty = (anchors[:, 1] + disp[:, 1]) / sc - (s_ * anchors[:, 0] + c * anchors[:, 1])
+    w_, z_ = warps[:, 1], warps[:, 2]
+    # translation t = 2 M d, M = [[w, -z], [z, w]]  ->  d = M^T t / 2
+    warps[:, 3] = 0.5 * (w_ * tx + z_ * ty)
+    warps[:, 4] = 0.5 * (-z_ * tx + w_ * ty)
+    return anchors, warps, sp.alpha
+
+
+def fill_canvas(cv, seed: int = 1, chunk: int = 256):
+    """Deterministic occupied content over the whole logical canvas (upload in
+    row chunks), so a deformation pass moves real data."""
+    w, h = cv.width(), cv.height()
+    rng = np.random.default_rng(seed)
+    col = rng.random((chunk, w, 3))
+    wt = rng.integers(1, 31, (chunk, w)).astype(np.uint8)
+    for y in range(0, h, chunk):
+        rows = min(chunk, h - y)
+        cv.write(0, y, col[:rows], wt[:rows])
+
+
+def deform_numbers(ctx, stream, n: int, disp, hbm_peak):
+    """Canvas deformation side measurement (north_star extension): one
+    ping-pong pass over an n x n canvas through the canvas-wide field `disp`
+    (device, n x n x 2). HBM-bound gather: algorithmic bytes per pixel =
+    13 read (R, G, B float32 + W u8 at the source; the 4 bilinear taps of
+    neighbouring pixels share cache lines) + 13 written + 8 displacement."""
+    import torch
+    from paper_2103_07414_b200 import mosaic as M
+    cv = M.Canvas(ctx)
+    cv.reserve((0.0, 0.0, n - 1.0, n - 1.0))
+    cv.ensure_contains((0.0, 0.0, n - 1.0, n - 1.0))
+    fill_canvas(cv)
+    cv.deform(disp)  # allocates the alternate planes
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        cv.deform(disp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = min(ts)
+    gbs = 34.0 * n * n / (ms * 1e-3) / 1e9
+    cv.close()
+    torch.cuda.empty_cache()
+    return {"workload": f"canvas deformation new(p) = old(p + d(p)) over a {n}x{n} canvas (ping-pong pass)",
+            "ms": ms, "gpx_per_s": n * n / (ms * 1e-3) / 1e9,
+            "roofline_k_canvas_deform": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                                         "frac": gbs / hbm_peak if hbm_peak else None,
+                                         "algorithmic": "34 B/px: 13 read + 13 written + 8 displacement"}}
+
+
+def run_canvas_mode(args):
+    """configs[3]/[4] canvas-wide pass over row bands. Per step:
+    the node lattice is broadcast from rank 0 (NCCL); every rank computes the
+    node field on its block-cyclic stripes of the canvas (K2,
+    nrm_node_field_band_device), agrees on the halo H = ceil(max |d_y|) + 1
+    (max all-reduce), receives the rows within H of its stripes from their
+    owners (dist.exchange_halo, NCCL send/recv) and deforms its stripes
+    (k_canvas_deform). value = canvas Mpix/s over the whole job."""
+    import torch
+    import torch.distributed as dist
+    from paper_2103_07414_b200 import dist as D
+    from paper_2103_07414_b200 import mosaic as M
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    functional = world > 1 and env_int("NRM_BENCH_FUNCTIONAL_GLOO", 0) == 1
+    if functional:
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world > 1:
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    ctx = M.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    n = args.canvas or (32768 if args.config == "c5" else 16384)
+    anchors, warps, alpha = canvas_lattice(n)
+    nodes_src = torch.from_numpy(np.concatenate([anchors.ravel(), warps.ravel()])).to(dev)
+    nodes = torch.zeros_like(nodes_src)
+    na = len(anchors)
+    a_t, q_t = nodes[:2 * na].view(na, 2), nodes[2 * na:].view(na, 5)
+    cv = M.Canvas(ctx)
+    cv.reserve((0.0, 0.0, n - 1.0, n - 1.0))
+    cv.ensure_contains((0.0, 0.0, n - 1.0, n - 1.0))
+    fill_canvas(cv)
+    cv.set_band(rank, world)
+    disp = torch.zeros((n, n, 2), dtype=torch.float32, device=dev)
+    grid = (0.0, 0.0, n, n)
+    row_bytes = 13 * n
+    halo_bytes = [0]
+
+    def bcast():
+        if world == 1:
+            nodes.copy_(nodes_src)
+        elif functional:
+            stream.synchronize()
+            t = nodes_src.cpu()
+            dist.broadcast(t, src=0)
+            nodes.copy_(t.to(dev))
+        else:
+            if rank == 0:
+                nodes.copy_(nodes_src)
+            dist.broadcast(nodes, src=0)
+
+    def step():
+        bcast()
+        M.node_field_band_device(grid, a_t, q_t, alpha, disp, None, rank, world, ctx=ctx)
+        if world > 1:
+            hv = (torch.ceil(disp[..., 1].abs().max()) + 1).to(torch.int64).reshape(1)
+            if functional:
+                stream.synchronize()
+                hc = hv.cpu()
+                dist.all_reduce(hc, op=dist.ReduceOp.MAX)
+                halo = int(hc.item())
+            else:
+                dist.all_reduce(hv, op=dist.ReduceOp.MAX)
+                halo = int(hv.item())  # host read (D2H) of the agreed halo
+            plan = D.halo_plan(0, n, world, halo)
+            if functional:
+                stream.synchronize()
+
+                def pack(rows, buf):
+                    t = torch.empty_like(buf, device=dev)
+                    cv.pack_rows(rows, t)
+                    stream.synchronize()
+                    buf.copy_(t.cpu())
+
+                def unpack(rows, buf):
+                    t = buf.to(dev)
+                    torch.cuda.synchronize()
+                    cv.unpack_rows(rows, t)
+                halo_bytes[0] = D.exchange_halo(plan, rank, world, row_bytes, pack, unpack, device="cpu")
+            else:
+                halo_bytes[0] = D.exchange_halo(plan, rank, world, row_bytes, cv.pack_rows, cv.unpack_rows,
+                                                device=dev)
+        cv.deform(disp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.05)
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clk.mark("start")
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark("end")
+    launches = ctx.launch_count() - l0
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if functional:
+            t = t.cpu()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ctx.profile(True)
+    step()
+    torch.cuda.synchronize()
+    kt = {k: v[0] for k, v in ctx.kernel_times().items()}
+    ctx.profile(False)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    if rank == 0:
+        value = n * n / 1e6 * args.steps / (ms * 1e-3)
+        dk = kt.get("k_canvas_deform")
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": f"{'configs[4]' if args.config == 'c5' else 'configs[3]'} canvas-wide pass: "
+                                   f"node field + canvas deformation over a {n}x{n} canvas, {na}-node lattice",
+                       "parallelism": f"band{world}" if world > 1 else "single",
+                       "l2": f"inputs ({n}x{n} canvas, {13 * n * n / 1e9:.1f} GB) larger than L2"},
+            "e2e": {"value": value, "unit": "Mpix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8 if world > 1 else 0,
+                    "note": "canvas-resident pass: the only host traffic per step is the agreed halo (8 B)"},
+            "gpu_launches": int(launches), "clocks": clocks,
+            "halo_bytes_received_per_step": halo_bytes[0],
+            "kernels_ms": kt,
+            "roofline": {"kernel": "k_canvas_deform", "bound": "hbm",
+                         "achieved": 34.0 * n * n / world / (dk * 1e-3) / 1e9 if dk else None,
+                         "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "traffic": None},
+        }
+        if dk and peaks.get("hbm_gbs"):
+            line["roofline"]["frac"] = line["roofline"]["achieved"] / peaks["hbm_gbs"]
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
     """Side measurement (BASELINE configs[3]: the canvas-wide field of a
     16384^2 canvas with its canvas-covering 1,497-node lattice, K2 =
@@ -634,13 +901,8 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
     from paper_2103_07414_b200 import workload as W
     dev = torch.device("cuda", torch.cuda.current_device())
     sp = W.scaled_params(3840, 2160)
-    anchors = W.hex_lattice((0.0, 0.0, float(n), float(n)), sp.hex_spacing)
+    anchors, warps, _ = canvas_lattice(n)
     rng = np.random.default_rng(5)
-    warps = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(anchors), 1))
-    ang = rng.uniform(-0.02, 0.02, len(anchors))
-    warps[:, 0] = rng.uniform(0.99, 1.01, len(anchors))
-    warps[:, 1], warps[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
-    warps[:, 3:5] = rng.normal(0, 4.0, (len(anchors), 2))
     a_t, q_t = torch.from_numpy(anchors).to(dev), torch.from_numpy(warps).to(dev)
     disp = torch.empty((n, n, 2), dtype=torch.float32, device=dev)
     sup = torch.empty((n, n), dtype=torch.uint8, device=dev)
@@ -665,7 +927,10 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
     ctx.profile(False)
     k_ms = kt.get("k_node_field", (ms, 1))[0]
     ach = n * n * per_px * 18.0 / (k_ms * 1e-3) / 1e12
-    del disp, sup
+    del sup
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    deform = deform_numbers(ctx, stream, n, disp, peaks.get("hbm_gbs"))
+    del disp
     torch.cuda.empty_cache()
     return {"workload": f"configs[3] canvas-wide node field: {n}x{n} grid, {len(anchors)}-node canvas lattice",
             "ms": ms, "gpx_per_s": n * n / (ms * 1e-3) / 1e9,
@@ -674,7 +939,8 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
                                       "frac": ach / fp32_peak,
                                       "algorithmic": f"{n * n} px x {per_px:.1f} contributing nodes x 18 flops",
                                       "note": "the inner-node sums run on the tensor cores (3xTF32 mma.sync); "
-                                              "this is the reference loop's FP32 work against the FP32 peak"}}
+                                              "this is the reference loop's FP32 work against the FP32 peak"},
+            "canvas_deform": deform}
 
 
 def em_estep_numbers(ctx, with_cpu: bool):

@@ -196,6 +196,18 @@ int nrm_node_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_an
                           const double *d_warps, int n, double alpha, float *d_disp,
                           uint8_t *d_support);
 
+/* The dense node field restricted to the block-cyclic 64-row stripes of
+ * rank band_rank of band_count (nrm_canvas_set_band's rule on absolute rows):
+ * only those rows of d_disp / d_support are written. The grid origin must be
+ * integral; its planning tiles are anchored to absolute reference pixels like
+ * the canvas's, so the ranks' rows together are bit-identical to the
+ * band_count = 1 call for any band count (the canvas-wide field of a
+ * multi-GPU canvas deformation). Values agree with
+ * nrm_node_field_device to the field tolerance. */
+int nrm_node_field_band_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_anchors,
+                               const double *d_warps, int n, double alpha, float *d_disp,
+                               uint8_t *d_support, int band_rank, int band_count);
+
 /* ---- footprint: invert_frame_boundary (mosaic.hpp:58-96) -------------- */
 /* Writes up to cap points to poly[cap][2]; *npoly = the full polygon size. */
 int nrm_invert_frame_boundary(nrm_ctx *ctx, int fw, int fh, const double *anchors,

@@ -375,25 +375,29 @@ int orc_canvas_deform(orc_canvas *cv, int x0, int y0, int w, int h, const float 
             double c3[3] = {0.0, 0.0, 0.0};
             uint8_t cw = 0;
             if (sx >= 0.0 && sx <= W - 1.0 && sy >= 0.0 && sy <= H - 1.0) {
+                /* FP64 source position, FP32 weights and blend (nrm_canvas_deform):
+                 * this file is built with -ffp-contract=off, like the kernel's
+                 * explicit round-to-nearest float operations */
                 int tx0 = (int)sx, ty0 = (int)sy;
                 if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
                 if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
-                const double fx = sx - tx0, fy = sy - ty0;
+                const float fx = (float)(sx - tx0), fy = (float)(sy - ty0);
                 const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
-                const double gx = 1.0 - fx, gy = 1.0 - fy;
+                const float gx = 1.0f - fx, gy = 1.0f - fy;
                 const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
-                const double bw[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
-                double n3[3] = {0.0, 0.0, 0.0}, den = 0.0, best = -1.0;
+                const float bw[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
+                float n3[3] = {0.0f, 0.0f, 0.0f}, den = 0.0f, best = -1.0f;
                 for (int t = 0; t < 4; ++t) {
                     const size_t idx = (size_t)tys[t] * W + txs[t];
                     const uint8_t wt = cv->weight[idx];
                     if (wt == 0) continue;
-                    for (int k = 0; k < 3; ++k) n3[k] = n3[k] + bw[t] * (double)(float)cv->color[3 * idx + k];
+                    for (int k = 0; k < 3; ++k) n3[k] = n3[k] + bw[t] * (float)cv->color[3 * idx + k];
                     den = den + bw[t];
                     if (bw[t] > best) { best = bw[t]; cw = wt; }
                 }
-                if (den > 0.0) {
-                    for (int k = 0; k < 3; ++k) c3[k] = (double)(float)(n3[k] / den);
+                if (den > 0.0f) {
+                    const float inv = 1.0f / den; /* correctly rounded, then three products */
+                    for (int k = 0; k < 3; ++k) c3[k] = (double)(n3[k] * inv);
                 } else {
                     cw = 0;
                 }

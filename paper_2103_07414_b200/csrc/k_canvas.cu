@@ -201,6 +201,9 @@ struct Px {
     float r, g, b;
     uint8_t w;
 };
+// FP64 source position (the displacement is added exactly at any canvas
+// coordinate), FP32 bilinear weights and blend with explicit round-to-nearest
+// operations (no contraction), restated bit for bit by orc_canvas_deform.
 __device__ __forceinline__ Px deform_sample(const CanvasView& v, int W, int H, int x, int y, float2 d) {
     const double sx = xadd((double)x, (double)d.x), sy = xadd((double)y, (double)d.y);
     Px o{0.f, 0.f, 0.f, 0};
@@ -208,31 +211,41 @@ __device__ __forceinline__ Px deform_sample(const CanvasView& v, int W, int H, i
     int tx0 = (int)sx, ty0 = (int)sy;
     if (tx0 > W - 2) tx0 = W - 2 >= 0 ? W - 2 : 0;
     if (ty0 > H - 2) ty0 = H - 2 >= 0 ? H - 2 : 0;
-    const double fx = xsub(sx, (double)tx0), fy = xsub(sy, (double)ty0);
-    const int tx1 = tx0 + 1 < W - 1 ? tx0 + 1 : W - 1, ty1 = ty0 + 1 < H - 1 ? ty0 + 1 : H - 1;
-    const double gx = xsub(1.0, fx), gy = xsub(1.0, fy);
-    const int txs[4] = {tx0, tx1, tx0, tx1}, tys[4] = {ty0, ty0, ty1, ty1};
-    const double bw[4] = {xmul(gx, gy), xmul(fx, gy), xmul(gx, fy), xmul(fx, fy)};
-    double nr = 0.0, ng = 0.0, nb = 0.0, den = 0.0, best = -1.0;
+    const float fx = (float)xsub(sx, (double)tx0), fy = (float)xsub(sy, (double)ty0);
+    const int dx1 = tx0 + 1 < W - 1 ? 1 : W - 1 - tx0;  // tx1 - tx0 (0 on a one-pixel-wide canvas)
+    const int dy1 = ty0 + 1 < H - 1 ? 1 : H - 1 - ty0;
+    const float gx = __fsub_rn(1.f, fx), gy = __fsub_rn(1.f, fy);
+    const float bw[4] = {__fmul_rn(gx, gy), __fmul_rn(fx, gy), __fmul_rn(gx, fy), __fmul_rn(fx, fy)};
+    const int txs[4] = {tx0, tx0 + dx1, tx0, tx0 + dx1}, tys[4] = {ty0, ty0, ty0 + dy1, ty0 + dy1};
+    uint8_t wt[4];
+    float tr[4], tg[4], tb[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {  // all 16 tap loads at once (one latency round)
+        const long long idx = (v.oy + tys[t]) * v.pitch + (v.ox + txs[t]);
+        wt[t] = __ldg(v.w + idx);
+        tr[t] = __ldg(v.r + idx);
+        tg[t] = __ldg(v.g + idx);
+        tb[t] = __ldg(v.b + idx);
+    }
+    float nr = 0.f, ng = 0.f, nb = 0.f, den = 0.f, best = -1.f;
     uint8_t cw = 0;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-        const long long idx = (v.oy + tys[t]) * v.pitch + (v.ox + txs[t]);
-        const uint8_t wt = __ldg(v.w + idx);
-        if (wt == 0) continue;
-        nr = xadd(nr, xmul(bw[t], (double)__ldg(v.r + idx)));
-        ng = xadd(ng, xmul(bw[t], (double)__ldg(v.g + idx)));
-        nb = xadd(nb, xmul(bw[t], (double)__ldg(v.b + idx)));
-        den = xadd(den, bw[t]);
+        if (wt[t] == 0) continue;
+        nr = __fadd_rn(nr, __fmul_rn(bw[t], tr[t]));
+        ng = __fadd_rn(ng, __fmul_rn(bw[t], tg[t]));
+        nb = __fadd_rn(nb, __fmul_rn(bw[t], tb[t]));
+        den = __fadd_rn(den, bw[t]);
         if (bw[t] > best) {
             best = bw[t];
-            cw = wt;
+            cw = wt[t];
         }
     }
-    if (den > 0.0) {
-        o.r = (float)(nr / den);
-        o.g = (float)(ng / den);
-        o.b = (float)(nb / den);
+    if (den > 0.f) {
+        const float inv = __frcp_rn(den);  // correctly rounded 1 / den, then three products
+        o.r = __fmul_rn(nr, inv);
+        o.g = __fmul_rn(ng, inv);
+        o.b = __fmul_rn(nb, inv);
         o.w = cw;
     }
     return o;
@@ -243,23 +256,49 @@ __device__ __forceinline__ Px deform_sample(const CanvasView& v, int W, int H, i
 // 16-byte aligned float4 / uchar4 of each plane). Pixels of the region are
 // resampled, the others copied, into the alternate planes (whose role is
 // swapped with the canvas planes afterwards). Rows this rank does not own
-// are skipped.
-__global__ void __launch_bounds__(256) k_canvas_deform_pp(CanvasView v, int W, int H, int rx0, int ry0, int rw,
-                                                          int rh, const float2* __restrict__ disp,
-                                                          float* __restrict__ outr, float* __restrict__ outg,
-                                                          float* __restrict__ outb, uint8_t* __restrict__ outw) {
+// are skipped. Quads entirely inside the region never read their own pixels:
+// per pixel the pass moves the algorithmic 13 B read (taps, shared between
+// neighbours through L1/L2) + 8 B displacement + 13 B written (ncu:
+// dram__bytes = 34.0 B/px, profiles/r02_deform_ncu.txt).
+#ifndef NRM_DEF_MINB
+#define NRM_DEF_MINB 4  // 64 registers, 4 CTAs per SM: 2.26 ms vs 3.30 ms unconstrained (16384^2, tools/deform_probe.py)
+#endif
+__global__ void __launch_bounds__(256, NRM_DEF_MINB) k_canvas_deform_pp(
+    CanvasView v, int W, int H, int rx0, int ry0, int rw, int rh, const float2* __restrict__ disp,
+    float* __restrict__ outr, float* __restrict__ outg, float* __restrict__ outb, uint8_t* __restrict__ outw) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int x = 4 * q;
     if (x >= W) return;
+    const bool cols_all = x >= rx0 && x + 3 < rx0 + rw, cols_any = x + 3 >= rx0 && x < rx0 + rw;
     for (int y = blockIdx.y; y < H; y += gridDim.y) {
         if (!owns_row(v, y)) continue;
         const long long base = (v.oy + y) * v.pitch + v.ox + x;
-        float4 cr = *reinterpret_cast<const float4*>(v.r + base);
-        float4 cg = *reinterpret_cast<const float4*>(v.g + base);
-        float4 cb = *reinterpret_cast<const float4*>(v.b + base);
-        uchar4 cw = *reinterpret_cast<const uchar4*>(v.w + base);
         const bool row_in = y >= ry0 && y < ry0 + rh;
-        if (row_in && x + 3 >= rx0 && x < rx0 + rw) {
+        float4 cr, cg, cb;
+        uchar4 cw;
+        if (!(row_in && cols_all)) {  // some pixels of the quad are copied through
+            cr = *reinterpret_cast<const float4*>(v.r + base);
+            cg = *reinterpret_cast<const float4*>(v.g + base);
+            cb = *reinterpret_cast<const float4*>(v.b + base);
+            cw = *reinterpret_cast<const uchar4*>(v.w + base);
+        }
+        if (row_in && cols_any) {
+            const size_t o = (size_t)(y - ry0) * rw + (x - rx0);
+            float2 dq[4];
+            if (cols_all && (o & 1) == 0) {  // two 16-byte loads for the quad's displacements
+                const float4 a = __ldg(reinterpret_cast<const float4*>(disp + o));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(disp + o) + 1);
+                dq[0] = make_float2(a.x, a.y);
+                dq[1] = make_float2(a.z, a.w);
+                dq[2] = make_float2(b.x, b.y);
+                dq[3] = make_float2(b.z, b.w);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int xi = x + k;
+                    dq[k] = (xi >= rx0 && xi < rx0 + rw) ? __ldg(disp + o + k) : make_float2(0.f, 0.f);
+                }
+            }
             float* pr = &cr.x;
             float* pg = &cg.x;
             float* pb = &cb.x;
@@ -268,11 +307,11 @@ __global__ void __launch_bounds__(256) k_canvas_deform_pp(CanvasView v, int W, i
             for (int k = 0; k < 4; ++k) {
                 const int xi = x + k;
                 if (xi < rx0 || xi >= rx0 + rw) continue;
-                const Px o = deform_sample(v, W, H, xi, y, disp[(size_t)(y - ry0) * rw + (xi - rx0)]);
-                pr[k] = o.r;
-                pg[k] = o.g;
-                pb[k] = o.b;
-                pw[k] = o.w;
+                const Px px = deform_sample(v, W, H, xi, y, dq[k]);
+                pr[k] = px.r;
+                pg[k] = px.g;
+                pb[k] = px.b;
+                pw[k] = px.w;
             }
         }
         *reinterpret_cast<float4*>(outr + base) = cr;

@@ -420,9 +420,22 @@ int grid_indices(const nrm_grid* g, FieldGrid* out) {
 }
 
 int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, const double* d_warps,
-                    int n, double alpha, float* d_disp, uint8_t* d_support) {
+                    int n, double alpha, float* d_disp, uint8_t* d_support, int band_rank = 0, int band_count = 1,
+                    bool absolute = false) {
     FieldGrid fg;
     NRM_CHECK(grid_indices(grid, &fg));
+    if (absolute) {
+        // stripes are anchored to absolute rows: index space = absolute pixels
+        if (grid->x0 != std::floor(grid->x0) || grid->y0 != std::floor(grid->y0) || std::fabs(grid->x0) > 1e9 ||
+            std::fabs(grid->y0) > 1e9)
+            return fail(NRM_EINVAL, "node_field: a banded grid needs an integral origin");
+        fg.gx = 0.0;
+        fg.gy = 0.0;
+        fg.i0 = (int)grid->x0;
+        fg.j0 = (int)grid->y0;
+        fg.i1 = fg.i0 + grid->width - 1;
+        fg.j1 = fg.j0 + grid->height - 1;
+    }
     const size_t npx = (size_t)grid->width * (size_t)grid->height;
     if (npx == 0) return NRM_OK;
     const size_t exc_cap = exception_capacity(c, npx);
@@ -434,6 +447,8 @@ int node_field_core(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, c
     L.n = n;
     L.alpha = alpha;
     L.grid = fg;
+    L.band_rank = band_rank;
+    L.band_count = band_count;
     L.disp = reinterpret_cast<float2*>(d_disp);
     L.support = d_support;
     L.exc = c->exc.as<int2>();
@@ -1139,6 +1154,18 @@ int nrm_node_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anch
     DeviceGuard g(c->device);
     ProfScope prof_scope(c);
     return node_field_core(c, grid, d_anchors, d_warps, n, alpha, d_disp, d_support);
+}
+
+int nrm_node_field_band_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, const double* d_warps,
+                               int n, double alpha, float* d_disp, uint8_t* d_support, int band_rank,
+                               int band_count) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (band_count < 1 || band_rank < 0 || band_rank >= band_count)
+        return fail(NRM_EINVAL, "node_field: need 0 <= band_rank < band_count");
+    NRM_CHECK(validate_nodes(d_anchors, d_warps, n, alpha, false));
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    return node_field_core(c, grid, d_anchors, d_warps, n, alpha, d_disp, d_support, band_rank, band_count, true);
 }
 
 // ---- footprint -------------------------------------------------------------

@@ -405,6 +405,17 @@ def node_field_device(grid, anchors_t, warps_t, alpha: float, disp_t, support_t=
                                          _tptr(support_t)))
 
 
+def node_field_band_device(grid, anchors_t, warps_t, alpha: float, disp_t, support_t, band_rank: int,
+                           band_count: int, ctx: Optional[Context] = None) -> None:
+    """node_field_device restricted to the rows of block-cyclic 64-row stripe
+    band `band_rank` of `band_count` (integral grid origin)."""
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    check(ctx._lib.nrm_node_field_band_device(ctx.handle, C.byref(g), _tptr(anchors_t), _tptr(warps_t),
+                                              anchors_t.shape[0], float(alpha), _tptr(disp_t), _tptr(support_t),
+                                              int(band_rank), int(band_count)))
+
+
 def invert_frame_boundary(frame_w: int, frame_h: int, anchors, warps, alpha: float,
                           step: float = 8.0, ctx: Optional[Context] = None) -> np.ndarray:
     """invert_frame_boundary (mosaic.hpp:58-96) -> polygon (k, 2)."""

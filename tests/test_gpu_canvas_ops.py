@@ -233,3 +233,46 @@ def test_banded_mosaic_runs_on_torchs_stream(nrm, golden):
     img, org = bm.render(crop=True)
     rimg, rorg = nrm.render(ref, crop=True)
     assert np.array_equal(img, rimg) and tuple(org) == tuple(rorg)
+
+
+def test_banded_node_field_is_bitwise_identical(nrm, ctx):
+    """The canvas-wide field split into block-cyclic stripes (one call per
+    rank): the ranks' rows together are the single field bit for bit."""
+    import torch
+    from paper_2103_07414_b200 import workload as W
+    from paper_2103_07414_b200 import dist as D
+    sp = W.scaled_params(1920, 1080)
+    x0, y0, w, h = -512, -333, 2304, 1500
+    anchors = W.hex_lattice((x0, y0, x0 + w, y0 + h), sp.hex_spacing)
+    rng = np.random.default_rng(9)
+    warps = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(anchors), 1))
+    ang = rng.uniform(-0.05, 0.05, len(anchors))
+    warps[:, 0] = rng.uniform(0.995, 1.005, len(anchors))
+    warps[:, 1], warps[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    warps[:, 3:5] = rng.normal(0, 3.0, (len(anchors), 2))
+    dev = torch.device("cuda", 0)
+    a_t, q_t = torch.from_numpy(anchors).to(dev), torch.from_numpy(warps).to(dev)
+    grid = (float(x0), float(y0), w, h)
+    d_full = torch.zeros((h, w, 2), dtype=torch.float32, device=dev)
+    s_full = torch.zeros((h, w), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    nrm.node_field_band_device(grid, a_t, q_t, sp.alpha, d_full, s_full, 0, 1, ctx=ctx)
+    d_rel = torch.zeros_like(d_full)
+    nrm.node_field_device(grid, a_t, q_t, sp.alpha, d_rel, None, ctx=ctx)
+    ctx.synchronize()
+    assert (d_rel - d_full).abs().max().item() <= 1e-3  # other tiling, same field
+    for world in (2, 3):
+        d_b = torch.full((h, w, 2), float("nan"), dtype=torch.float32, device=dev)
+        s_b = torch.full((h, w), 7, dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize()
+        for r in range(world):
+            nrm.node_field_band_device(grid, a_t, q_t, sp.alpha, d_b, s_b, r, world, ctx=ctx)
+        ctx.synchronize()
+        assert torch.equal(d_b, d_full) and torch.equal(s_b, s_full)
+        # a single rank writes only its own rows
+        d_1 = torch.full((h, w, 2), float("nan"), dtype=torch.float32, device=dev)
+        torch.cuda.synchronize()
+        nrm.node_field_band_device(grid, a_t, q_t, sp.alpha, d_1, s_b, 1, world, ctx=ctx)
+        ctx.synchronize()
+        mask = torch.from_numpy(D.owned_rows_mask(y0, h, 1, world)).to(dev)
+        assert torch.equal(d_1[mask], d_full[mask]) and torch.isnan(d_1[~mask]).all()
