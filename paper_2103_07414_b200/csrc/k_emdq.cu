@@ -907,26 +907,6 @@ struct FastOut {
     bool exact;                    // boundary near-tie: rerun in the exact tier
 };
 
-// exp(min(x, 55)) for x >= 0 to ~1e-9 relative (fast tier of bounded_exp,
-// geometry.hpp:85-88): 2^n exp(r), n = rint(x / ln2), |r| <= ln2 / 2.
-__device__ __forceinline__ double fast_bounded_exp(double x) {
-    x = fmin(x, 55.0);
-    const double n = rint(x * 1.4426950408889634);
-    double r = fma(-n, 6.93147180369123816490e-01, x);
-    r = fma(-n, 1.90821492927058770002e-10, r);
-    double p = 1.0 / 362880.0;
-    p = fma(p, r, 1.0 / 40320.0);
-    p = fma(p, r, 1.0 / 5040.0);
-    p = fma(p, r, 1.0 / 720.0);
-    p = fma(p, r, 1.0 / 120.0);
-    p = fma(p, r, 1.0 / 24.0);
-    p = fma(p, r, 1.0 / 6.0);
-    p = fma(p, r, 0.5);
-    p = fma(p, r, 1.0);
-    p = fma(p, r, 1.0);
-    return p * __hiloint2double((int)(n + 1023.0) << 20, 0);
-}
-
 #ifndef NRM_PIX_UNROLL
 #define NRM_PIX_UNROLL 4
 #endif
@@ -1076,17 +1056,26 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     }
     const int ne = h.ne, nin = h.nin;
     const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
-    // separable weight tables (prob and the tile-wide d^2 floor folded into ey)
+    // separable weight tables (prob and the tile-wide d^2 floor folded into
+    // ey): thread = (record k, 4 columns / rows); the per-record terms once,
+    // float4 stores (ex[k][4q .. 4q+3], ey[k][4q .. 4q+3])
     if (!(flags & TFLAG_EXACT_STAGED)) {
-        const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
-        for (int e = t; e < ne * ET; e += ENT) {  // one column and one row entry per iteration
-            const int k = e / ET, c = e % ET;
+        const int k = t >> 2, c0 = 4 * (t & 3);
+        if (k < ne) {
+            const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
             const float4 r0 = sp.rec0[k];
             const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
             const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
-            const float dx = r0.x - (float)c, dy = r0.y - (float)c;
-            ex[k][c] = ex2_approx(nal * (dx * dx - dxr));
-            ey[k][c] = ex2_approx(fmaf(nal, dy * dy - dyr, nal * (dxr + dyr - d2ref))) * r0.z;
+            const float base = nal * (dxr + dyr - d2ref);
+            float vx[4], vy[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float dx = r0.x - (float)(c0 + i), dy = r0.y - (float)(c0 + i);
+                vx[i] = ex2_approx(nal * (dx * dx - dxr));
+                vy[i] = ex2_approx(fmaf(nal, dy * dy - dyr, base)) * r0.z;
+            }
+            *reinterpret_cast<float4*>(&ex[k][c0]) = make_float4(vx[0], vx[1], vx[2], vx[3]);
+            *reinterpret_cast<float4*>(&ey[k][c0]) = make_float4(vy[0], vy[1], vy[2], vy[3]);
         }
     }
     __syncthreads();
@@ -1115,15 +1104,22 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
     const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
     const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
-    const double sb = h.s0 + (double)dlb;
-    const double yx = h.Y0[0] + (h.e0[0] + (double)dlb * h.P[0] + sb * (double)Qx);
-    const double yy = h.Y0[1] + (h.e0[1] + (double)dlb * h.P[1] + sb * (double)Qy);
-    if (od) *od = make_float2((float)(yx - qx), (float)(yy - qy));
+    // displacement y - q = (Y0 - tile origin - u) + (e0 + dl P + (s0 + dl) Q(u)):
+    // the first part is a small per-tile constant (bd, FP64 -> FP32), the
+    // second stays ~1e2 px, so FP32 keeps it to ~1e-5 px at any coordinate
+    // (the K1/K2 epilogue; error model: k_nodefield.cu kScaleLever)
+    if (od) {
+        const float sbf = (float)h.s0 + dlb;
+        const float rx = fmaf(sbf, Qx, fmaf(dlb, (float)h.P[0], (float)h.e0[0]));
+        const float ry = fmaf(sbf, Qy, fmaf(dlb, (float)h.P[1], (float)h.e0[1]));
+        const float bdx = (float)(h.Y0[0] - (L.grid.gx + ti0)), bdy = (float)(h.Y0[1] - (L.grid.gy + tj0));
+        *od = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
+    }
     if (ou) {
         // bounded_exp(beta d2min) (fieldest.hpp:44-52) to FP32 output
         // precision: d2min in FP64 over the points that can be the nearest in
-        // this sub-tile, exp by 2^n exp(r) with |r| <= ln2/2 and a degree-9
-        // polynomial (relative error < 1e-9, far inside the 1e-6 bar)
+        // this sub-tile; exp(x) = 2^n 2^f, n = rint(x log2 e), |f| <= 1/2 in
+        // FP64, 2^f on MUFU.EX2 (relative error < 3e-7, inside the 1e-6 bar)
         double d2m = DBL_MAX;
         const int nl = nnear == 255 ? ne : nnear;
         for (int e = 0; e < nl; ++e) {
@@ -1132,7 +1128,9 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
             const double dx = qx - a.x, dy = qy - a.y;
             d2m = fmin(d2m, fma(dx, dx, dy * dy));
         }
-        *ou = (float)fast_bounded_exp(L.beta * d2m);
+        const double tx = fmin(L.beta * d2m, 55.0) * 1.4426950408889634;
+        const double n = rint(tx);
+        *ou = ex2_approx((float)(tx - n)) * __int_as_float(((int)n + 127) << 23);
     }
 }
 
