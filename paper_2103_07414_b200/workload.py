@@ -236,31 +236,149 @@ def _knn(pts: np.ndarray, k: int, chunk: int = 2048) -> np.ndarray:
     return out
 
 
+def _fit_locals(apts, bpts, pool, knn: int):
+    """M-step of estimate_field (fieldest.hpp:177-192, refit 239-255): for
+    each j in pool, a similarity over j and its knn nearest pool members
+    (excluding j); scale gated to (0.05, 20), else the translation bpts[j] -
+    apts[j] (WarpFunction{1, from_translation})."""
+    from scipy.spatial import cKDTree
+    pool = np.asarray(pool)
+    pa, pb = apts[pool], bpts[pool]
+    kk = min(knn, len(pool) - 1)
+    out = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(pool), 1))
+    if kk >= 1:
+        _, nb = cKDTree(pa).query(pa, k=kk + 1)
+        nb = nb[:, 1:]  # drop self (distance 0; duplicates keep one of them)
+        src = np.concatenate([pa[:, None, :], pa[nb]], axis=1)
+        dst = np.concatenate([pb[:, None, :], pb[nb]], axis=1)
+        sc, ang, t = fit_similarity_batch(src, dst)
+        ok = np.isfinite(sc) & (sc > 0.05) & (sc < 20.0)
+        w, z = np.cos(0.5 * ang), np.sin(0.5 * ang)
+        tx, ty = t[:, 0] / np.where(ok, sc, 1.0), t[:, 1] / np.where(ok, sc, 1.0)
+        out[ok] = np.stack([sc, w, z, 0.5 * (tx * w + ty * z), 0.5 * (-tx * z + ty * w)], 1)[ok]
+    tr = ~(np.arange(len(pool)) < 0)
+    if kk >= 1:
+        tr = ~ok
+    d = pb - pa
+    out[tr] = np.stack([np.ones(tr.sum()), np.ones(tr.sum()), np.zeros(tr.sum()), 0.5 * d[tr, 0], 0.5 * d[tr, 1]], 1)
+    locals_ = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(apts), 1))
+    locals_[pool] = out
+    return locals_
+
+
+def _blend_local_batch(locals_, apts, probs, active, queries, exclude, alpha: float, support: int = 16):
+    """detail::blend_local (fieldest.hpp:75-97) at many queries (vectorized):
+    the `support` nearest active candidates (leaving out exclude[q], -1 for
+    none), w = exp(-alpha (d2 - d2min)) max(p, 1e-6), dq_blend with the
+    nearest as hemisphere reference; returns the blended warps (nq, 5)."""
+    from scipy.spatial import cKDTree
+    act = np.asarray(active)
+    k = min(support + 1, len(act))
+    d, ii = cKDTree(apts[act]).query(queries, k=k)
+    if k == 1:
+        d, ii = d[:, None], ii[:, None]
+    cand = act[ii]
+    keep = cand != np.asarray(exclude)[:, None]
+    # the first `support` kept candidates per query
+    order = np.argsort(~keep, axis=1, kind="stable")[:, :min(support, k)]
+    cand = np.take_along_axis(cand, order, 1)
+    d2 = np.take_along_axis(d, order, 1) ** 2
+    kept = np.take_along_axis(keep, order, 1)
+    w = np.exp(-alpha * (d2 - d2[:, :1])) * np.maximum(probs[cand], 1e-6) * kept
+    q = locals_[cand]  # (nq, S, 5)
+    ref = q[:, :1, 1:3]
+    flip = (q[..., 1:3] * ref).sum(-1) < 0
+    dq = np.where(flip[..., None], -q[..., 1:], q[..., 1:])
+    ws = w.sum(1)
+    mean = (w[..., None] * dq).sum(1) / ws[:, None]
+    nrm = np.hypot(mean[:, 0], mean[:, 1])
+    out = np.empty((len(queries), 5))
+    out[:, 0] = (w * q[..., 0]).sum(1) / ws
+    out[:, 1:] = mean / nrm[:, None]
+    return out
+
+
+def _apply_warps(w5, p):
+    wq, zq, dx, dy, s_ = w5[:, 1], w5[:, 2], w5[:, 3], w5[:, 4], w5[:, 0]
+    c, sn = wq * wq - zq * zq, 2 * wq * zq
+    x = c * p[:, 0] - sn * p[:, 1] + 2 * (dx * wq - dy * zq)
+    y = sn * p[:, 0] + c * p[:, 1] + 2 * (dx * zq + dy * wq)
+    return np.stack([x * s_, y * s_], 1)
+
+
+def estimate_field_host(apts, bpts, sp, seed: int = 1234, max_iters: int = 10, knn: int = 8, support: int = 16,
+                        rel_tol: float = 1e-4, seed_trials: int = 64):
+    """The EM control loop of estimate_field (fieldest.hpp:112-272), which
+    north_star keeps on the host, restated in numpy for workload generation:
+    consensus seeding over random triples (scale gate 0.2-5, Gaussian
+    consensus score), slack gates 9x / 25x tau^2, then EM iterations of
+    probs = exp(-r^2 / (2 (tau/2)^2)), the kNN-8 local-similarity M-step
+    with the (0.05, 20) scale gate, the leave-one-out blend_local E-step and
+    the tau^2 gate, until the predictions move less than rel_tol of the field
+    span; finally inliers = r^2 < tau^2, their probabilities and the refit of
+    their locals over the inlier set (fieldest.hpp:227-255). Differences from
+    the reference: numpy's RNG for the seed triples, kNN ties in tree order;
+    tests/test_host.py measures the agreement with the reference's own
+    estimate_field (oracle/_ref). Returns (locals, probs, inliers, resid2)."""
+    n = len(apts)
+    tau2 = sp.inlier_threshold ** 2
+    sig2 = 0.25 * tau2
+    rng = np.random.default_rng(seed)
+    best, seed_sim = -1.0, None
+    for _ in range(seed_trials):
+        i, j, k = rng.integers(0, n, 3)
+        if i == j or j == k or i == k:
+            continue
+        tri_a, tri_b = apts[[i, j, k]][None], bpts[[i, j, k]][None]
+        sc, ang, t = fit_similarity_batch(tri_a, tri_b)
+        if not (0.2 <= sc[0] <= 5.0):
+            continue
+        w = similarity_warp(sc[0], ang[0], t[0])[None]
+        pred = _apply_warps(np.repeat(w, n, 0), apts)
+        score = np.exp(-((pred - bpts) ** 2).sum(1) / (2 * sig2)).sum()
+        if score > best:
+            best, seed_sim = score, w
+    if seed_sim is None:
+        raise ValueError("estimate_field_host: every seed triple degenerate")
+    resid2 = ((_apply_warps(np.repeat(seed_sim, n, 0), apts) - bpts) ** 2).sum(1)
+    gated = lambda slack: np.nonzero(resid2 < tau2 * slack)[0]  # noqa: E731
+    active = gated(9.0)
+    if len(active) < 4:
+        active = gated(25.0)
+    prev = None
+    for _ in range(max_iters):
+        probs = np.exp(-resid2 / (2 * sig2))
+        locals_ = _fit_locals(apts, bpts, active, knn)
+        f = _blend_local_batch(locals_, apts, probs, active, apts, np.arange(n), sp.alpha, support)
+        pred = _apply_warps(f, apts)
+        resid2 = ((pred - bpts) ** 2).sum(1)
+        nxt = gated(1.0)
+        if len(nxt) >= 4:
+            active = nxt
+        if prev is not None:
+            delta = np.hypot(*(pred - prev).T).max()
+            span = max(1.0, np.hypot(*(pred - apts).T).max())
+            if delta < rel_tol * span:
+                break
+        prev = pred
+    inliers = np.nonzero(resid2 < tau2)[0]
+    probs = np.exp(-resid2 / (2 * sig2))
+    locals_ = _fit_locals(apts, bpts, inliers, knn)
+    return locals_, probs, inliers.astype(np.int32), resid2
+
+
 def emdq_inputs(frame_w: int, frame_h: int, n_match: int, outlier_frac: float, seed: int,
                 knn: int = 8, noise: float = 0.25) -> EmdqInputs:
-    """Matches with known smooth deformation; locals = similarity fitted over
-    each inlier and its knn nearest inliers (fieldest.hpp:240-255); probs from
-    the fit residual, exp(-r^2 / (2 (tau/2)^2)) (fieldest.hpp:239)."""
+    """Matches with a known smooth deformation (plus noise on the inliers and
+    uniform outliers), run through the host EM of estimate_field
+    (estimate_field_host): locals, probabilities and the active set are the
+    EM's final refit over its own inliers (fieldest.hpp:227-255)."""
     sp = scaled_params(frame_w, frame_h)
     a, b, inlier, deform = synth_matches(frame_w, frame_h, sp.s, n_match, outlier_frac, seed)
     rng = np.random.default_rng(seed + 1)
     b = b + rng.normal(0, noise * sp.s, b.shape) * inlier[:, None]
-    act = np.nonzero(inlier)[0]
-    pa, pb = a[act], b[act]
-    nb = _knn(pa, knn)
-    src = np.concatenate([pa[:, None, :], pa[nb]], axis=1)
-    dst = np.concatenate([pb[:, None, :], pb[nb]], axis=1)
-    sc, ang, t = fit_similarity_batch(src, dst)
-    locals_ = np.tile(np.array([1.0, 1.0, 0.0, 0.0, 0.0]), (len(a), 1))
-    for r, j in enumerate(act):
-        locals_[j] = similarity_warp(sc[r], ang[r], t[r])
-    c, s_ = np.cos(ang), np.sin(ang)
-    pred = np.stack([sc * (c * pa[:, 0] - s_ * pa[:, 1]) + t[:, 0], sc * (s_ * pa[:, 0] + c * pa[:, 1]) + t[:, 1]], 1)
-    r2 = ((pred - pb) ** 2).sum(1)
-    sigma2 = 0.25 * sp.inlier_threshold ** 2
-    probs = np.zeros(len(a))
-    probs[act] = np.exp(-r2 / (2 * sigma2))
-    return EmdqInputs(a, b, locals_, probs, act.astype(np.int32), deform)
+    locals_, probs, act, _ = estimate_field_host(a, b, sp, seed=seed + 2, knn=knn)
+    return EmdqInputs(a, b, locals_, probs, act, deform)
 
 
 # ---------------------------------------------------------------------------

@@ -99,3 +99,21 @@ def test_scaled_params_match_config():
     assert p.s == 4.0 and abs(p.alpha - 1.25e-5) < 1e-18 and p.hex_spacing == 240.0
     p = W.scaled_params(640, 480)
     assert abs(p.s - 1.5555555555555556) < 1e-15
+
+
+def test_host_em_matches_the_reference_estimate_field(golden):
+    """workload.estimate_field_host (the EM control loop of estimate_field,
+    fieldest.hpp:112-272, restated in numpy for the bench and test inputs)
+    against the reference's own estimate_field on the C1 golden matches
+    (oracle/_ref via make_golden.py): the same inlier set, the refit locals
+    (fieldest.hpp:239-255, kNN-8 similarity with the scale gate) to 1e-9 and
+    the EM-residual probabilities to 1e-5 relative."""
+    from paper_2103_07414_b200 import workload as W
+    g = golden("emdq_c1")
+    sp = W.scaled_params(640, 480)
+    assert sp.alpha == float(g["alpha"])
+    loc, pr, act, _ = W.estimate_field_host(g["apts"], g["bpts"], sp)
+    assert np.array_equal(np.sort(act), np.sort(g["active"]))
+    a = g["active"]
+    assert np.abs(loc[a] - g["locals"][a]).max() <= 1e-9
+    assert np.abs(pr[a] / g["probs"][a] - 1).max() <= 1e-5
