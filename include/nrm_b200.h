@@ -208,6 +208,18 @@ int nrm_node_field_band_device(nrm_ctx *ctx, const nrm_grid *grid, const double 
                                const double *d_warps, int n, double alpha, float *d_disp,
                                uint8_t *d_support, int band_rank, int band_count);
 
+/* ---- node variance field: Engine::blended_variance_at (slam.hpp:703-714) --
+ * at every grid pixel: out[j][i] = sum_k w_k var_k / sum_k w_k with
+ * w_k = exp(-alpha (|pos_k - p|^2 - d2min(p))) over all n nodes (their
+ * current positions pos[n][2], variances var[n]); 0 without nodes. A per-pixel
+ * uncertainty source for nrm_blend_frame_weighted. Values
+ * agree with the reference's FP64 formula to 1e-6 of max |var|. O(n) per
+ * pixel (no cutoff, like the reference): frame lattices. */
+int nrm_variance_field(nrm_ctx *ctx, const nrm_grid *grid, const double *positions,
+                       const double *variances, int n, double alpha, float *out);
+int nrm_variance_field_device(nrm_ctx *ctx, const nrm_grid *grid, const double *d_positions,
+                              const double *d_variances, int n, double alpha, float *d_out);
+
 /* ---- footprint: invert_frame_boundary (mosaic.hpp:58-96) -------------- */
 /* Writes up to cap points to poly[cap][2]; *npoly = the full polygon size. */
 int nrm_invert_frame_boundary(nrm_ctx *ctx, int fw, int fh, const double *anchors,

@@ -398,6 +398,19 @@ inline void deform_canvas(Canvas& canvas, int x, int y, int w, int h, std::span<
     canvas.invalidate_mirror();
 }
 
+/// Engine::blended_variance_at (slam.hpp:703-714) at every pixel (x0 + i, y0 + j)
+/// of a w x h grid: the node-variance map (node current positions and
+/// variances), a per-pixel uncertainty source for blend_frame_weighted
+/// (e.g. unc = 1 + v / v0). out receives w * h floats.
+inline void blended_variance_field(double x0, double y0, int w, int h, std::span<const Vec2> positions,
+                                   std::span<const double> variances, double alpha, float* out) {
+    if (positions.size() != variances.size()) throw std::invalid_argument("blended_variance_field: size mismatch");
+    const auto p = b200::pack_points(positions);
+    const nrm_grid g{x0, y0, w, h};
+    b200::check(nrm_variance_field(b200::context(), &g, p.data(), variances.data(),
+                                   static_cast<int>(positions.size()), alpha, out));
+}
+
 /// render (mosaic.hpp:301-331).
 inline ImageU8 render(const Canvas& canvas, bool crop = false, Vec2* crop_origin = nullptr) {
     int w = 0, h = 0;

@@ -774,6 +774,33 @@ int orc_emdq_field_grid_fast(double x0, double y0, int w, int h, const double *a
     return rc ? -1 : 0;
 }
 
+/* Engine::blended_variance_at (slam.hpp:703-714) at every pixel (x0 + i,
+ * y0 + j) of a grid: d2min over the node positions, then the
+ * exp(-alpha (d2 - d2min))-weighted mean of the node variances (0 without
+ * nodes). The reference's operation order. */
+void orc_variance_field(double x0, double y0, int w, int h, const double *pos, const double *var, int n,
+                        double alpha, double *out) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int j = 0; j < h; ++j)
+        for (int i = 0; i < w; ++i) {
+            const double px = x0 + i, py = y0 + j;
+            double d2min = DBL_MAX;
+            for (int k = 0; k < n; ++k) {
+                const double dx = pos[2 * k] - px, dy = pos[2 * k + 1] - py;
+                const double d2 = dx * dx + dy * dy;
+                d2min = d2 < d2min ? d2 : d2min; /* std::min(d2min, d2) */
+            }
+            double wsum = 0.0, acc = 0.0;
+            for (int k = 0; k < n; ++k) {
+                const double dx = pos[2 * k] - px, dy = pos[2 * k + 1] - py;
+                const double wk = exp(-alpha * ((dx * dx + dy * dy) - d2min));
+                wsum += wk;
+                acc += wk * var[k];
+            }
+            out[(size_t)j * w + i] = wsum > 0.0 ? acc / wsum : 0.0;
+        }
+}
+
 /* ==========================================================================
  * Sparse front end (features.hpp). FP32 arithmetic in the
  * reference's order; this file is built with -ffp-contract=off, so every

@@ -86,6 +86,9 @@ int orc_blend_local(const double *locals, const double *apts, const double *prob
 
 /* node_uncertainty (fieldest.hpp:44-52) over pts[m]. Returns NaN on bad input. */
 double orc_node_uncertainty(double qx, double qy, const double *pts, int m, double beta);
+/* Engine::blended_variance_at (slam.hpp:703-714) at every grid pixel. */
+void orc_variance_field(double x0, double y0, int w, int h, const double *pos, const double *var, int n,
+                        double alpha, double *out);
 
 /* Dense grids (the north_star's per-pixel evaluation; SURVEY §8c route).
  * Query pixel (i, j) is the reference coordinate (x0 + i, y0 + j).

@@ -64,6 +64,7 @@ class Oracle:
         L.orc_blend_local.argtypes = [_P, _P, _P, _P, _I, _D, _D, _D, _I, _P]
         L.orc_node_uncertainty.argtypes = [_D, _D, _P, _I, _D]
         L.orc_node_uncertainty.restype = _D
+        L.orc_variance_field.argtypes = [_D, _D, _I, _I, _P, _P, _I, _D, _P]
         L.orc_node_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _I, _D, _P, _P]
         L.orc_emdq_field_grid.argtypes = [_D, _D, _I, _I, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P, _I, _I]
         L.orc_emdq_field_grid_fast.argtypes = [_D, _D, _I, _I, _P, _P, _P, _P, _I, _D, _I, _D, _P, _P, _I, _I]
@@ -208,6 +209,16 @@ class Oracle:
                                    _p(sup))
         return disp, sup
 
+    def variance_field(self, grid, positions, variances, alpha):
+        """Engine::blended_variance_at (slam.hpp:703-714) at every grid pixel."""
+        x0, y0, w, h = grid
+        ps = _f64(positions, 2)
+        vs = np.ascontiguousarray(variances, np.float64)
+        out = np.zeros((h, w))
+        self.L.orc_variance_field(float(x0), float(y0), int(w), int(h), _p(ps), _p(vs), len(ps), float(alpha),
+                                  _p(out))
+        return out
+
     def emdq_field_grid(self, grid, apts, locals_, probs, active, alpha, beta, support=16,
                         rows: Optional[tuple] = None, fast: bool = False):
         """fast=True: the grid-kNN / OpenMP variant (bit-identical outputs)."""
@@ -276,6 +287,7 @@ class Reference:
         L.ref_synth_matches.argtypes = [_I, _I, _D, _I, _I, C.c_uint64, _P, _P]
         L.ref_estimate_locals.argtypes = [_P, _P, _I, _P, _I, _D, _D, _D, _I, _I, C.c_uint64, _I, _P, _P, _P, _P, _P]
         L.ref_warp_update.argtypes = [_P, _P, _P]
+        L.ref_blended_variance_at.argtypes = [_P, _I, _P, _P, _I, _D, _P]
         L.ref_estep_loo.argtypes = [_P, _P, _P, _P, _I, _P, _I, _D, _I, _I, _I, _I, _P, _P, _P]
         L.ref_scene_render.argtypes = [_I, _I, _I, C.c_uint64, _I, _D, _D, _D, _I, _I, _P]
         L.ref_time_blend_frame.argtypes = [_P, _I, _I, _I, _P, _P, _I, _D, _P, _I, _P, _I, _P]
@@ -360,6 +372,13 @@ class Reference:
         out = np.zeros(5)
         self.L.ref_blend_local(_p(lo), _p(ap), _p(pr), _p(ac), len(ac), float(qx), float(qy), float(alpha),
                                int(support), len(ap), _p(out))
+        return out
+
+    def blended_variance_at(self, pts, positions, variances, alpha):
+        q, ps = _f64(pts, 2), _f64(positions, 2)
+        vs = np.ascontiguousarray(variances, np.float64)
+        out = np.zeros(len(q))
+        self.L.ref_blended_variance_at(_p(q), len(q), _p(ps), _p(vs), len(ps), float(alpha), _p(out))
         return out
 
     def node_uncertainty(self, qx, qy, pts, beta):

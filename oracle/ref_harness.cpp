@@ -13,12 +13,35 @@
 #include <random>
 #include <vector>
 
+// Engine::blended_variance_at (slam.hpp:703-714) is private; the checker
+// ref_blended_variance_at calls it on a default Engine (test infrastructure
+// only). The standard headers the reference uses come first, unaffected.
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <filesystem>
+#include <fstream>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <optional>
+#include <span>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <utility>
+#define private public
 #include "nrmosaic/config.hpp"
 #include "nrmosaic/features.hpp"
 #include "nrmosaic/fieldest.hpp"
 #include "nrmosaic/mosaic.hpp"
 #include "nrmosaic/slam.hpp"
 #include "nrmosaic/synth.hpp"
+#undef private
 #include "oracles.hpp"
 
 using namespace nrmosaic;
@@ -475,6 +498,19 @@ double ref_time_detect_match(const std::uint8_t* img_b, int w, int h, int ch, co
         counts2[1] = static_cast<int>(m.size());
     }
     return dt;
+}
+
+/* Engine::blended_variance_at (slam.hpp:703-714) at npts points. */
+void ref_blended_variance_at(const double* pts, int npts, const double* pos, const double* var, int n, double alpha,
+                             double* out) {
+    Engine::Params prm;
+    prm.alpha = alpha;
+    Engine eng(prm);
+    std::vector<Vec2> p(n);
+    for (int i = 0; i < n; ++i) p[i] = Vec2{pos[2 * i], pos[2 * i + 1]};
+    const std::span<const Vec2> ps(p);
+    const std::span<const double> vs(var, (size_t)n);
+    for (int k = 0; k < npts; ++k) out[k] = eng.blended_variance_at(Vec2{pts[2 * k], pts[2 * k + 1]}, ps, vs);
 }
 
 }  // extern "C"

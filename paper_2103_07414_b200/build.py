@@ -27,7 +27,8 @@ NVCC_FLAGS = [
     "-Xptxas", "-v",
     f"-I{ROOT / 'include'}",
 ]
-SOURCES = ["nrm_abi.cu", "k_nodefield.cu", "k_emdq.cu", "k_canvas.cu", "k_features.cu", "k_selftest.cu"]
+SOURCES = ["nrm_abi.cu", "k_nodefield.cu", "k_emdq.cu", "k_canvas.cu", "k_features.cu", "k_selftest.cu",
+           "k_variance.cu"]
 
 
 def _nvcc() -> str:

@@ -1156,6 +1156,44 @@ int nrm_node_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anch
     return node_field_core(c, grid, d_anchors, d_warps, n, alpha, d_disp, d_support);
 }
 
+// ---- node variance field (Engine::blended_variance_at, slam.hpp:703-714) ----
+int nrm_variance_field_device(nrm_ctx* c, const nrm_grid* grid, const double* d_pos, const double* d_var, int n,
+                              double alpha, float* d_out) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!grid || grid->width < 0 || grid->height < 0) return fail(NRM_EINVAL, "bad grid");
+    if (!std::isfinite(grid->x0) || !std::isfinite(grid->y0)) return fail(NRM_EINVAL, "non-finite grid origin");
+    if (n < 0 || (n > 0 && (!d_pos || !d_var))) return fail(NRM_EINVAL, "variance_field: bad node arrays");
+    if (!std::isfinite(alpha) || alpha < 0.0) return fail(NRM_EINVAL, "alpha must be finite and >= 0");
+    if ((size_t)grid->width * grid->height == 0) return NRM_OK;
+    if (!d_out) return fail(NRM_EINVAL, "variance_field: null output");
+    DeviceGuard g(c->device);
+    ProfScope prof_scope(c);
+    NRM_CUDA(launch_variance_field(grid->x0, grid->y0, grid->width, grid->height, d_pos, d_var, n, alpha, d_out,
+                                   c->stream, &c->launches));
+    return NRM_OK;
+}
+
+int nrm_variance_field(nrm_ctx* c, const nrm_grid* grid, const double* pos, const double* var, int n, double alpha,
+                       float* out) {
+    if (!c) return fail(NRM_ESTATE, "null context");
+    if (!grid || grid->width < 0 || grid->height < 0) return fail(NRM_EINVAL, "bad grid");
+    if (n < 0 || (n > 0 && (!pos || !var))) return fail(NRM_EINVAL, "variance_field: bad node arrays");
+    if (n > 0 && (!finite_all(pos, (size_t)n * 2) || !finite_all(var, (size_t)n)))
+        return fail(NRM_EINVAL, "variance_field: non-finite node arrays");
+    const size_t npx = (size_t)grid->width * grid->height;
+    if (npx == 0) return NRM_OK;
+    if (!out) return fail(NRM_EINVAL, "variance_field: null output");
+    DeviceGuard g(c->device);
+    NRM_CHECK(upload(c, c->anchors, pos, (size_t)n * 2 * sizeof(double)));
+    NRM_CHECK(upload(c, c->warps, var, (size_t)n * sizeof(double)));
+    NRM_CUDA(c->out_a.ensure(npx * sizeof(float)));
+    NRM_CHECK(nrm_variance_field_device(c, grid, c->anchors.as<double>(), c->warps.as<double>(), n, alpha,
+                                        c->out_a.as<float>()));
+    NRM_CUDA(cudaMemcpyAsync(out, c->out_a.p, npx * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    NRM_CUDA(cudaStreamSynchronize(c->stream));
+    return NRM_OK;
+}
+
 int nrm_node_field_band_device(nrm_ctx* c, const nrm_grid* grid, const double* d_anchors, const double* d_warps,
                                int n, double alpha, float* d_disp, uint8_t* d_support, int band_rank,
                                int band_count) {

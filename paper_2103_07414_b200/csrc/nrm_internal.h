@@ -214,6 +214,10 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
 // Device-side bounding box of nq points -> out4 = {minx, miny, maxx, maxy}.
 cudaError_t launch_points_bbox(const double* q, int nq, double* out4, cudaStream_t st, int64_t* launches);
 
+// ---- k_variance.cu (Engine::blended_variance_at, slam.hpp:703-714, per pixel) ----
+cudaError_t launch_variance_field(double x0, double y0, int w, int h, const double* pos, const double* var, int n,
+                                  double alpha, float* out, cudaStream_t st, int64_t* launches);
+
 // ---- k_canvas.cu ----------------------------------------------------------
 cudaError_t launch_render(const nrm_canvas* cv, int x, int y, int w, int h, uint8_t* out,
                           cudaStream_t st, int64_t* launches);

@@ -416,6 +416,22 @@ def node_field_band_device(grid, anchors_t, warps_t, alpha: float, disp_t, suppo
                                               int(band_rank), int(band_count)))
 
 
+def variance_field(grid, positions, variances, alpha: float, ctx: Optional[Context] = None) -> np.ndarray:
+    """Engine::blended_variance_at (slam.hpp:703-714) at every pixel of grid =
+    (x0, y0, width, height) -> (h, w) float32: the exp(-alpha (d2 -
+    d2min))-weighted mean of the node variances at their current positions.
+    A per-pixel uncertainty source for blend_frame(..., unc=...)."""
+    ctx = ctx or default_context()
+    g = Grid(float(grid[0]), float(grid[1]), int(grid[2]), int(grid[3]))
+    p = _f64(positions, 2, "positions")
+    v = np.ascontiguousarray(variances, np.float64)
+    if len(v) != len(p):
+        raise ValueError("positions / variances size mismatch")
+    out = np.zeros((g.height, g.width), np.float32)
+    check(ctx._lib.nrm_variance_field(ctx.handle, C.byref(g), _ptr(p), _ptr(v), len(p), float(alpha), _ptr(out)))
+    return out
+
+
 def invert_frame_boundary(frame_w: int, frame_h: int, anchors, warps, alpha: float,
                           step: float = 8.0, ctx: Optional[Context] = None) -> np.ndarray:
     """invert_frame_boundary (mosaic.hpp:58-96) -> polygon (k, 2)."""

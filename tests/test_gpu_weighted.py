@@ -89,3 +89,42 @@ def test_weighted_device_variant(nrm, ctx, golden):
     ca, wa = a.read()
     cb, wb = b.read()
     assert np.array_equal(wa, wb) and np.array_equal(ca, cb)
+
+
+@pytest.mark.parametrize("off", [0.0, 21000.0])
+def test_node_variance_field_matches_oracle(nrm, ctx, oracle, off):
+    """Dense Engine::blended_variance_at (slam.hpp:703-714, SURVEY §8a a19):
+    within 1e-6 of max |var| of the reference formula (oracle, pinned to the
+    reference by test_variance_field_restates_the_reference)."""
+    rng = np.random.default_rng(12)
+    n = 73
+    pos = rng.uniform(-50, 700, (n, 2)) + off
+    var = rng.uniform(0.0, 40.0, n)
+    grid = (off - 3.5, off + 2.0, 640, 480)
+    v = nrm.variance_field(grid, pos, var, 8.265e-5, ctx=ctx)
+    ov = oracle.variance_field(grid, pos, var, 8.265e-5)
+    assert np.abs(v - ov).max() <= 1e-6 * var.max()
+
+
+def test_blend_weighted_by_node_variance(nrm, ctx, oracle):
+    """The node-variance map as the uncertainty of the weighted blend:
+    u = 1 + v / 4 at the frame's own node positions (the SLAM engine's
+    current positions), against the oracle's weighted blend with the same map."""
+    from paper_2103_07414_b200 import workload as W
+    wl = W.frame_workload("c1")
+    rng = np.random.default_rng(3)
+    var = rng.uniform(0.0, 20.0, len(wl.anchors))
+    pos = np.stack([W._apply_warps(wl.warps[i:i + 1], wl.anchors[i:i + 1])[0] for i in range(len(wl.anchors))])
+    v = nrm.variance_field((0.0, 0.0, wl.frame_w, wl.frame_h), pos, var, wl.params.alpha, ctx=ctx)
+    unc = (1.0 + v / 4.0).astype(np.float32)
+    assert unc.max() > 2.0
+    poly = nrm.invert_frame_boundary(wl.frame_w, wl.frame_h, wl.anchors, wl.warps, wl.params.alpha, ctx=ctx)
+    cv, ocv = nrm.Canvas(ctx), oracle.canvas()
+    for k in range(2):
+        st = nrm.blend_frame(cv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly, unc=unc).as_tuple()
+        ost = oracle.blend_frame_weighted(ocv, wl.frame, wl.anchors, wl.warps, wl.params.alpha, poly, unc)
+        assert st == ost
+    col, wt = cv.read()
+    ocol, owt = ocv.arrays()
+    assert np.array_equal(wt, owt)
+    assert np.abs(col.astype(np.float64) - ocol).max() <= 1e-3

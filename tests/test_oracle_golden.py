@@ -250,3 +250,21 @@ def test_fast_emdq_grid_equals_full_scan(oracle, seed):
         a = oracle.emdq_field_grid(grid, apts, loc, pr, act, 1e-3, 2e-3, sup)
         b = oracle.emdq_field_grid(grid, apts, loc, pr, act, 1e-3, 2e-3, sup, fast=True)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), sup
+
+
+def test_variance_field_restates_the_reference():
+    """orc_variance_field = Engine::blended_variance_at (slam.hpp:703-714),
+    called on the reference itself (oracle/_ref), bit for bit."""
+    from oracle import oracle as orc
+    if not orc.reference_available():
+        pytest.skip("oracle/_ref not built (reference tree absent)")
+    O, R = orc.Oracle(), orc.Reference()
+    rng = np.random.default_rng(4)
+    for off, n in ((0.0, 70), (23000.0, 5), (-9000.5, 160)):
+        pos = rng.uniform(-100, 700, (n, 2)) + off
+        var = rng.uniform(0, 50, n)
+        grid = (off - 20.5, off + 10.25, 37, 23)
+        a = O.variance_field(grid, pos, var, 2e-4)
+        gx, gy = np.meshgrid(grid[0] + np.arange(grid[2]), grid[1] + np.arange(grid[3]))
+        b = R.blended_variance_at(np.stack([gx.ravel(), gy.ravel()], 1), pos, var, 2e-4).reshape(a.shape)
+        assert np.array_equal(a, b)
