@@ -183,6 +183,14 @@ int nrm_render_device(nrm_canvas *cv, int x, int y, int w, int h, uint8_t *d_out
  * returns x1 < x0 when nothing is occupied. */
 int nrm_canvas_occupied_bbox(nrm_canvas *cv, int *x0, int *y0, int *x1, int *y1);
 
+/* ---- PNG output (image.hpp:160-192 save_png) --------
+ * Writes image[h][w][channels] (1: gray, 3: RGB, 4: RGBA, as save_png) as an
+ * 8-bit non-interlaced PNG, deflating bands of scanlines on `threads` host
+ * threads (<= 0: all cores) at zlib `level` (-1 default, 0..9). Host only,
+ * needs no device. E.g. the RGBA of nrm_render. */
+int nrm_save_png(const char *path, const uint8_t *image, int w, int h, int channels, int level,
+                 int threads);
+
 /* ---- node field: pixel_warp (mosaic.hpp:22-51) ------------------------ */
 /* pixel_warp at npts arbitrary points (exact FP64 path). out_warps[npts][5];
  * valid[i] = 0 where the reference returns nullopt. */

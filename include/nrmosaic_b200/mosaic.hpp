@@ -398,6 +398,17 @@ inline void deform_canvas(Canvas& canvas, int x, int y, int w, int h, std::span<
     canvas.invalidate_mirror();
 }
 
+/// save_png (image.hpp:160-192) with the parallel band encoder of
+/// nrm_save_png: ImageU8 with 1 / 3 / 4 channels -> 8-bit PNG. For the
+/// render() of a canvas-wide mosaic (up to 4 GiB of RGBA) the bands are
+/// deflated on all host cores. Throws std::runtime_error on I/O failure.
+inline void save_png_parallel(const std::string& path, const ImageU8& im, int threads = 0, int level = 6) {
+    const int rc = nrm_save_png(path.c_str(), im.data.data(), im.width, im.height, im.channels, level, threads);
+    if (rc == NRM_EINVAL && im.channels != 1 && im.channels != 3 && im.channels != 4)
+        throw std::runtime_error("unsupported channel count");
+    if (rc != NRM_OK) throw std::runtime_error(std::string("nrm_b200: ") + nrm_last_error());
+}
+
 /// Engine::blended_variance_at (slam.hpp:703-714) at every pixel (x0 + i, y0 + j)
 /// of a w x h grid: the node-variance map (node current positions and
 /// variances), a per-pixel uncertainty source for blend_frame_weighted

@@ -106,6 +106,7 @@ SIGNATURES = [
     ("nrm_node_field", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int, C.c_double, _P, _P]),
     ("nrm_node_field_device", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int, C.c_double, _P, _P]),
     ("nrm_node_field_band_device", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int, C.c_double, _P, _P, C.c_int, C.c_int]),
+    ("nrm_save_png", C.c_int, [C.c_char_p, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     ("nrm_variance_field", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int, C.c_double, _P]),
     ("nrm_variance_field_device", C.c_int, [_P, C.POINTER(Grid), _P, _P, C.c_int, C.c_double, _P]),
     ("nrm_invert_frame_boundary", C.c_int, [_P, C.c_int, C.c_int, _P, _P, C.c_int, C.c_double,

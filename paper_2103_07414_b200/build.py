@@ -28,7 +28,7 @@ NVCC_FLAGS = [
     f"-I{ROOT / 'include'}",
 ]
 SOURCES = ["nrm_abi.cu", "k_nodefield.cu", "k_emdq.cu", "k_canvas.cu", "k_features.cu", "k_selftest.cu",
-           "k_variance.cu"]
+           "k_variance.cu", "png_io.cu"]
 
 
 def _nvcc() -> str:
@@ -72,7 +72,7 @@ def build_lib(force: bool = False, extra_flags: tuple = (), lib: Path = LIB, obj
             list(ex.map(lambda c: _run(c, objdir / (Path(c[-1]).stem + ".ptxas.log")), jobs))
     if force or jobs or _stale(lib, objs):
         _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib),
-              *map(str, objs), "-cudart", "static", "-Xcompiler", "-fPIC"])
+              *map(str, objs), "-cudart", "static", "-Xcompiler", "-fPIC", "-lz"])
     return lib
 
 

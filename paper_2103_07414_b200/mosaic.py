@@ -416,6 +416,17 @@ def node_field_band_device(grid, anchors_t, warps_t, alpha: float, disp_t, suppo
                                               int(band_rank), int(band_count)))
 
 
+def save_png(path, image: np.ndarray, level: int = 6, threads: int = 0) -> None:
+    """save_png (image.hpp:160-192): image (h, w) or (h, w, c), c in {1, 3, 4},
+    uint8 -> an 8-bit PNG (bands deflated in parallel on the host)."""
+    im = np.ascontiguousarray(image, np.uint8)
+    if im.ndim == 2:
+        im = im[:, :, None]
+    h, w, c = im.shape
+    lib = _lib.load()
+    check(lib.nrm_save_png(str(path).encode(), _ptr(im), w, h, c, int(level), int(threads)))
+
+
 def variance_field(grid, positions, variances, alpha: float, ctx: Optional[Context] = None) -> np.ndarray:
     """Engine::blended_variance_at (slam.hpp:703-714) at every pixel of grid =
     (x0, y0, width, height) -> (h, w) float32: the exp(-alpha (d2 -
