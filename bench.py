@@ -257,6 +257,7 @@ def main():
     ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
     ap.add_argument("--no-canvas-field", action="store_true", help="skip the canvas-wide field side measurement")
     ap.add_argument("--no-features", action="store_true", help="skip the feature detection / matching side measurement")
+    ap.add_argument("--no-replay", action="store_true", help="skip the recorded-node-state replay side measurement")
     ap.add_argument("--e2e-inflight", type=int, default=2,
                     help="EMDQ field calls in flight in the e2e loop (own context + pinned outputs each)")
     ap.add_argument("--mode", default="frame", choices=["frame", "canvas"],
@@ -637,6 +638,9 @@ def main():
     feats = None
     if rank == 0 and not args.no_features:
         feats = features_numbers(ctx, stream, with_cpu=world == 1 and not args.no_cpu_baseline)
+    replay = None
+    if rank == 0 and not args.no_replay:
+        replay = replay_numbers(ctx, stream)
 
     if rank == 0:
         line = {
@@ -655,6 +659,7 @@ def main():
             "em_estep": estep,
             "canvas_field": canvas_field,
             "features": feats,
+            "replay": replay,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -1062,6 +1067,63 @@ def features_numbers(ctx, stream, with_cpu: bool):
         except Exception as ex:  # noqa: BLE001  (reported, never required)
             r["cpu_reference"] = {"unavailable": repr(ex)}
     return r
+
+
+def replay_numbers(ctx, stream, reps: int = 20):
+    """blend_frame driven by node states a SLAM run
+    recorded with the reference's own snapshot writer (snapshot.hpp:17-44;
+    tests/golden/replay_scan.npz, read by paper_2103_07414_b200/replay.py):
+    the recorded 480x270 frames with their node graphs and footprints into a
+    fresh canvas per pass, device-resident. Valid when every replayed
+    BlendStats equals the reference pipeline's own (pipeline_scan.npz)."""
+    import torch
+    from paper_2103_07414_b200 import mosaic as M
+    from paper_2103_07414_b200 import replay as RP
+    from paper_2103_07414_b200 import workload as W
+    gp, pp = ROOT / "tests" / "golden" / "replay_scan.npz", ROOT / "tests" / "golden" / "pipeline_scan.npz"
+    if not gp.exists():
+        return {"unavailable": "tests/golden/replay_scan.npz missing"}
+    g, ref = dict(np.load(gp)), dict(np.load(pp))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ts = [int(t) for t in g["frames_t"]]
+    w, h = (int(v) for v in g["size"])
+    alpha = W.scaled_params(w, h).alpha
+    items = []
+    for t in ts:
+        s = RP.read_snapshot(bytes(g[f"snapshot_{t}"]))
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        items.append((T(g[f"frame_{t}"]), T(s.anchors), T(s.warps), g[f"footprint_{t}"]))
+    st = torch.zeros((len(ts), 4), dtype=torch.int64, device=dev)
+
+    def one_pass():
+        cv = M.Canvas(ctx)
+        cv.reserve((-600.0, -300.0, 1100.0, 600.0))
+        for k, (f, a, q, poly) in enumerate(items):
+            M.blend_frame_device(cv, f, w, h, 3, a, q, alpha, poly, st[k])
+        return cv
+
+    cv = one_pass()
+    torch.cuda.synchronize()
+    ok = bool(np.array_equal(st.cpu().numpy(), ref["stats"][ts]))
+    del cv
+    best = None
+    for _ in range(reps):
+        cv = M.Canvas(ctx)
+        cv.reserve((-600.0, -300.0, 1100.0, 600.0))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k, (f, a, q, poly) in enumerate(items):
+            M.blend_frame_device(cv, f, w, h, 3, a, q, alpha, poly, st[k])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+        del cv
+    return {"workload": f"{len(ts)} recorded {w}x{h} frames with their recorded node graphs (reference "
+                        f"write_snapshot, scan scene) into a fresh canvas",
+            "ms_per_frame": best / len(ts), "frames_per_s": 1e3 * len(ts) / best,
+            "stats_equal_reference_pipeline": ok}
 
 
 def wl_contributors(wl, poly, sample: int = 20000):

@@ -296,9 +296,35 @@ def c3_sequence_case(nframes=200):
     print("c3", (ox, oy, w, h), "occupied", len(occ), "blended", int(np.array(stats)[:, 1].sum()))
 
 
+def replay_case(frames=12):
+    """Recorded node states for replay: the reference
+    pipeline's own write_snapshot / TrajectoryWriter output (snapshot.hpp)
+    for the first frames of the `scan` scene (oracle/_ref/snapshot_dump), with
+    the blended frames and their footprints. The same run as
+    pipeline_scan.npz's first frames, so replayed blends must reproduce its
+    BlendStats."""
+    import subprocess
+    import tempfile
+    exe = ROOT / "oracle" / "_ref" / "snapshot_dump"
+    with tempfile.TemporaryDirectory() as td:
+        out = subprocess.run([str(exe), td, str(frames), "scan"], check=True, capture_output=True, text=True)
+        w, h = map(int, out.stdout.split())
+        ts = sorted(int(p.stem.split("_")[1]) for p in Path(td).glob("snapshot_*.json"))
+        data = {"frames_t": np.array(ts, np.int32), "size": np.array([w, h], np.int32),
+                "trajectory": np.frombuffer(Path(td, "trajectory.jsonl").read_bytes(), np.uint8)}
+        for t in ts:
+            data[f"snapshot_{t}"] = np.frombuffer(Path(td, f"snapshot_{t}.json").read_bytes(), np.uint8)
+            data[f"frame_{t}"] = np.frombuffer(Path(td, f"frame_{t}.rgb").read_bytes(), np.uint8).reshape(h, w, 3)
+            data[f"footprint_{t}"] = np.loadtxt(Path(td, f"footprint_{t}.txt")).reshape(-1, 2)
+    np.savez_compressed(OUT / "replay_scan.npz", **data)
+    print("replay", ts)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["pipeline"]:
         pipeline_cases()
+    elif sys.argv[1:] == ["replay"]:
+        replay_case()
     elif sys.argv[1:] == ["c3"]:
         c3_sequence_case()
     elif sys.argv[1:] == ["estep"]:
@@ -311,3 +337,4 @@ if __name__ == "__main__":
         features_cases()
         pipeline_cases()
         c3_sequence_case()
+        replay_case()
