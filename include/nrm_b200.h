@@ -12,9 +12,10 @@
  * Conventions
  *   - Every function returns NRM_OK (0) or an NRM_E* code; never throws.
  *     nrm_last_error() gives a thread-local message for the last failure.
- *   - Host-pointer entry points copy inputs in (pinned host memory is copied
- *     directly, pageable memory through the context's pinned staging) and
- *     block until results are on the host.
+ *   - Host-pointer entry points copy inputs to the device with
+ *     cudaMemcpyAsync on the context stream (fast from pinned host memory;
+ *     pageable memory goes through the driver's own staging) and block until
+ *     results are on the host.
  *   - *_device entry points take device pointers, enqueue on the context's
  *     stream and return without synchronising.
  *   - Array layouts:
