@@ -6,7 +6,9 @@
 // (oracle/make_golden.py replay_case; paper_2103_07414_b200/replay.py reads
 // them). Built against the unmodified reference headers (oracle/Makefile).
 //
-// usage: snapshot_dump <outdir> <frames> [scan|outback]
+// usage: snapshot_dump <outdir> <frames> [scan|outback] [scene_frames]
+//   the scene is built for scene_frames (default 200, the camera path spans
+//   the scene's frames) and the first <frames> of it are run
 //   <outdir>/snapshot_<t>.json   write_snapshot after frame t (blended frames)
 //   <outdir>/frame_<t>.rgb       the frame (w*h*3 bytes), footprint_<t>.txt
 //   <outdir>/trajectory.jsonl    TrajectoryWriter lines, every frame
@@ -26,7 +28,8 @@ int main(int argc, char** argv) {
     if (argc < 3) return 2;
     const std::string dir = argv[1];
     SceneSpec spec;
-    spec.frames = std::atoi(argv[2]);
+    const int run_frames = std::atoi(argv[2]);
+    spec.frames = argc > 4 ? std::atoi(argv[4]) : 200;
     spec.path = argc > 3 ? argv[3] : "scan";
     spec.path_extent = 240.0;
     const SyntheticScene scene = SyntheticScene::build(spec);
@@ -46,7 +49,7 @@ int main(int argc, char** argv) {
         for (const Vec2& p : engine.last_footprint()) std::fprintf(f, "%.17g %.17g\n", p.x, p.y);
         std::fclose(f);
     };
-    for (int t = 0; t < spec.frames; ++t) {
+    for (int t = 0; t < run_frames; ++t) {
         const ImageU8 frame = scene.render_frame(t, 8);
         const FrameFeatures cur = detect_features(to_gray(frame), det);
         if (t == 0) {
