@@ -125,9 +125,11 @@ struct PlanWarp {
 
 // Pixel-kernel shared memory (one tile).
 struct PixSmem {
-    TilePlan p;
+    TilePlan p;                        // staged by one TMA bulk copy
     float ex[TREC][ET], ey[TREC][ET];  // separable weights: w = ex[k][col] * ey[k][row]
+    unsigned long long bar;            // TMA completion
 };
+static_assert(sizeof(TilePlan) % 16 == 0, "TMA bulk copies move 16-byte multiples");
 struct SSmem {
     int hist[256];
     int wcnt[NW];
@@ -1138,15 +1140,18 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
 template <int MAXS>
 __global__ void __launch_bounds__(ENT, NRM_PIX_MINB)
 k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
-    __shared__ __align__(16) PixSmem s;
-    pdl_wait();
+    __shared__ __align__(128) PixSmem s;
     const int g = blockIdx.y * TP.ntx + blockIdx.x;
-    {
-        const uint4* src = reinterpret_cast<const uint4*>(&TP.plan[g]);
-        uint4* dst = reinterpret_cast<uint4*>(&s.p);
-        for (int k = threadIdx.x; k < (int)(sizeof(TilePlan) / 16); k += ENT) dst[k] = src[k];
-    }
+    // the tile plan (4 KB) arrives by one TMA bulk copy (cp.async.bulk): one
+    // thread arms the barrier and issues it, no register round trip
+    if (threadIdx.x == 0) mbar_init(&s.bar, 1);
     __syncthreads();
+    pdl_wait();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&s.bar, (unsigned)sizeof(TilePlan));
+        bulk_g2s(&s.p, &TP.plan[g], (unsigned)sizeof(TilePlan), &s.bar);
+    }
+    mbar_wait(&s.bar, 0);
     pixels_tile<MAXS>(L, C, SL, s.p, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
 }
 
