@@ -738,12 +738,294 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
     if (MODE != 1) block_add3<NT>(L.acc, nb, nns, noof);
 }
 
+#ifndef NRM_K2_MMASYNC
+// ---------------------------------------------------------------------------
+// K2 on the 5th-generation tensor cores (tcgen05). CTA = one 64 x 32 planning
+// tile, 256 threads. The inner-node sums are one product per chunk of 32
+// listed nodes, D[col][n] += A[col][k] B[n][k] with
+//   A = ex (M = 64 tile columns), B[32 j + row][k] = ey[k][row] q_k[j]
+//   (N = 6 components x 32 rows = 192),
+// 3xTF32 split products (Al Bh + Ah Bl + Ah Bh) accumulated in FP32 in tensor
+// memory (64 lanes x 192 columns); one thread issues the MMAs and commits
+// them to an mbarrier. Ring nodes (the 1e-6 cutoff crosses the tile) stay on
+// the CUDA cores in registers; the epilogue adds the accumulator read back
+// from tensor memory with tcgen05.ld (16x256b: the mma.sync fragment layout,
+// so each thread owns 8 pixels as before). Operand layout and descriptors:
+// nrm_common.cuh, validated by tools/probes/tcgen05_probe.cu.
+// ---------------------------------------------------------------------------
+constexpr int TC_K = 32;                                       // listed nodes per chunk (4 MMA k-steps)
+constexpr int TC_M = TW, TC_N = 6 * TH;                        // 64 x 192
+constexpr unsigned TC_IDESC = umma_idesc_tf32(TC_M, TC_N);
+constexpr int TC_TMEM_COLS = 256;                              // >= TC_N, power of two
+struct __align__(128) SmemTC {
+    float ah[TC_K * TC_M], al[TC_K * TC_M];  // A = ex, K-major canonical (umma_kmajor_off), TF32 hi / lo
+    float bh[TC_K * TC_N], bl[TC_K * TC_N];  // B = ey * q_j
+    float ey[TC_K][EYP];                     // row factor [node][row] (ring nodes)
+    float eyt[TH][TC_K + 4];                 // row factor [row][node] (B build: 16-byte reads)
+    float qt[8][TC_K];                       // [component][node]: qw, qz, qdx, qdy, ds, 1 (zero for ring nodes)
+    NfEntry e[TC_K];
+    unsigned long long bar;                  // MMA completion
+    unsigned tmem;                           // tensor-memory base address
+};
+
+__device__ __forceinline__ void nf_field_tc(const NodeFieldLaunch& L, const NfPlan* __restrict__ plans, int tile_i0,
+                                            int tile_j0, int s1, int by0, int ntx, int bx, int by,
+                                            unsigned char* smem_raw) {
+    SmemTC& s = *reinterpret_cast<SmemTC*>(smem_raw);
+    const int t = threadIdx.x;
+    const NfPlan& pl = plans[by * ntx + bx];
+    const int tix = tile_i0 + bx;
+    const int tjy = tile_row_of(by0 + by, tile_j0, s1, L.band_count);
+    const int ti0 = tix * TW, tj0 = tjy * TH;
+    const int status = pl.h.status;
+    const int ci0 = max(ti0, L.grid.i0), ci1 = min(ti0 + TW - 1, L.grid.i1);
+    const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
+    if (status == NF_OUTSIDE || ci0 > ci1) return;
+    if (status == NF_EXACT) {
+        tile_to_exceptions<1>(L, ci0, ci1, cj0, cj1);
+        return;
+    }
+    if (status == NF_EMPTY) {  // no node reaches the tile: no support anywhere
+        const int w = ci1 - ci0 + 1;
+        for (int e = t; e < w * (cj1 - cj0 + 1); e += NT) {
+            const int i = ci0 + e % w, j = cj0 + e / w;
+            const size_t o = (size_t)(j - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+            if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+            if (L.support) L.support[o] = 0;
+        }
+        return;
+    }
+    const int count = pl.h.count, ninner = pl.h.ninner;
+    stage_entries(s.e, pl.e, min(TC_K, count));
+    cp_async_commit();
+    if (t < 32) tmem_alloc<TC_TMEM_COLS>(&s.tmem);
+    if (t == 0) mbar_init(&s.bar, 1);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const unsigned tmem = s.tmem;
+
+    const double ox = L.grid.gx + ti0, oy = L.grid.gy + tj0;  // unclipped tile origin
+    const double nal = -L.alpha * kLog2e;
+    const int lane = t & 31, wid = t >> 5, g = lane >> 2, tig = lane & 3;
+    // warp w reads tensor-memory lanes 32 (w % 4) .. + 15 = tile columns
+    // cb = 16 (w % 4) .., and rows rb = 16 (w / 4) ..; thread pixels:
+    // (cb + 8 (f >> 1) + g, rb + 8 mt + 2 tig + (f & 1))
+    const int cb = 16 * (wid & 3), rb = 16 * (wid >> 2);
+    float acc[2][6][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+#pragma unroll
+            for (int f = 0; f < 4; ++f) acc[mt][j][f] = 0.f;
+    unsigned amb = 0, phase = 0;
+    bool pending = false, any_mma = false;  // block-uniform
+    for (int c0 = 0; c0 < count; c0 += TC_K) {
+        const int cn = min(TC_K, count - c0);
+        const int kin = min(max(ninner - c0, 0), cn);  // inner nodes of this chunk come first
+        const int cn8 = (cn + 7) & ~7;
+        if (c0 > 0) {
+            if (pending) {  // the previous chunk's MMAs have read A and B
+                mbar_wait(&s.bar, phase);
+                phase ^= 1u;
+                pending = false;
+            }
+            __syncthreads();  // and every thread is done with its ring nodes
+            stage_entries(s.e, pl.e + c0, cn);
+            cp_async_commit();
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // A (column factor, hi / lo): thread = (column, 4 consecutive nodes),
+        // one 16-byte store of each half per group; (c, 4 kq) sits at byte
+        // umma_kmajor_off = 16 TC_M kq + 128 (c / 8) + 16 (c % 8)
+        for (int u = t; u < TC_M * (cn8 / 4); u += NT) {
+            const int c = u & (TC_M - 1), kq = u / TC_M, k0 = 4 * kq;
+            float h4[4], l4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int k = k0 + i;
+                float v = 0.f;
+                if (k < cn) {
+                    const double d = s.e[k].a.x - (ox + c);
+                    v = ex2_approx((float)(nal * d * d));
+                }
+                h4[i] = tf32_hi(v);
+                l4[i] = v - h4[i];
+            }
+            const int o = 4 * TC_M * kq + 32 * (c >> 3) + 4 * (c & 7);
+            *reinterpret_cast<float4*>(&s.ah[o]) = make_float4(h4[0], h4[1], h4[2], h4[3]);
+            *reinterpret_cast<float4*>(&s.al[o]) = make_float4(l4[0], l4[1], l4[2], l4[3]);
+        }
+        {  // row factor: thread = (row, every 8th node)
+            const int r = t & 31;
+            const double y = oy + r;
+            for (int k = t >> 5; k < cn8; k += 8) {
+                float v = 0.f;
+                if (k < cn) {
+                    const double dy = s.e[k].a.y - y;
+                    v = ex2_approx((float)(nal * dy * dy));
+                }
+                s.ey[k][r] = v;
+                s.eyt[r][k] = v;
+            }
+        }
+        for (int k = t; k < cn8; k += NT) {
+            const bool in = k < kin;  // ring nodes and padding: zero B rows
+            const float4 q = s.e[k].q;
+            s.qt[0][k] = in ? q.x : 0.f;
+            s.qt[1][k] = in ? q.y : 0.f;
+            s.qt[2][k] = in ? q.z : 0.f;
+            s.qt[3][k] = in ? q.w : 0.f;
+            s.qt[4][k] = in ? s.e[k].d : 0.f;
+            s.qt[5][k] = in ? 1.f : 0.f;
+        }
+        __syncthreads();
+        if (kin > 0) {
+            // B (hi / lo): thread = (n = 32 j + row, 4 consecutive nodes); items
+            // u = t + 256 i walk n by 64 (mod 192) and kq by 1 (+1 on wrap)
+            const int kin8 = (kin + 7) & ~7, nq = kin8 / 4;
+            int n = t < TC_N ? t : t - TC_N, kq = t < TC_N ? 0 : 1;
+            while (kq < nq) {
+                const int j = n >> 5, r = n & 31;
+                const float4 e4 = *reinterpret_cast<const float4*>(&s.eyt[r][4 * kq]);
+                const float4 q4 = *reinterpret_cast<const float4*>(&s.qt[j][4 * kq]);
+                const float v0 = e4.x * q4.x, v1 = e4.y * q4.y, v2 = e4.z * q4.z, v3 = e4.w * q4.w;
+                const float h0 = tf32_hi(v0), h1 = tf32_hi(v1), h2 = tf32_hi(v2), h3 = tf32_hi(v3);
+                const int o = 4 * TC_N * kq + 32 * (n >> 3) + 4 * (n & 7);
+                *reinterpret_cast<float4*>(&s.bh[o]) = make_float4(h0, h1, h2, h3);
+                *reinterpret_cast<float4*>(&s.bl[o]) = make_float4(v0 - h0, v1 - h1, v2 - h2, v3 - h3);
+                n += NT - TC_N;
+                ++kq;
+                if (n >= TC_N) {
+                    n -= TC_N;
+                    ++kq;
+                }
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+            if (t == 0) {
+                const unsigned a_h = smem_addr(s.ah), a_l = smem_addr(s.al), b_h = smem_addr(s.bh),
+                               b_l = smem_addr(s.bl);
+                for (int ks = 0; ks < nq / 2; ++ks) {
+                    const unsigned oa = ks * 32 * TC_M, ob = ks * 32 * TC_N;
+                    const unsigned long long dah = umma_desc(a_h + oa, 16 * TC_M, 128),
+                                             dal = umma_desc(a_l + oa, 16 * TC_M, 128),
+                                             dbh = umma_desc(b_h + ob, 16 * TC_N, 128),
+                                             dbl = umma_desc(b_l + ob, 16 * TC_N, 128);
+                    umma_tf32(tmem, dal, dbh, TC_IDESC, (any_mma || ks > 0) ? 1u : 0u);
+                    umma_tf32(tmem, dah, dbl, TC_IDESC, 1u);
+                    umma_tf32(tmem, dah, dbh, TC_IDESC, 1u);
+                }
+                umma_commit(&s.bar);
+            }
+            pending = true;
+            any_mma = true;
+        }
+        // ring nodes on the CUDA cores, per-pixel 1e-6 cutoff (overlaps the MMAs)
+        for (int k = kin; k < cn; ++k) {
+            const float4 q = s.e[k].q;
+            const float dd = s.e[k].d;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const float2 eyv = *reinterpret_cast<const float2*>(&s.ey[k][rb + 8 * mt + 2 * tig]);
+#pragma unroll
+                for (int hc = 0; hc < 2; ++hc) {
+                    const int c = cb + 8 * hc + g, o = umma_kmajor_off(c, k, TC_M) >> 2;
+                    const float exv = s.ah[o] + s.al[o];
+#pragma unroll
+                    for (int hr = 0; hr < 2; ++hr) {
+                        const int f = 2 * hc + hr;
+                        float w = exv * (hr ? eyv.y : eyv.x);
+                        const bool in = w > kCutHi;
+                        amb |= (unsigned)((w >= kCutLo) && !in) << (4 * mt + f);
+                        w = in ? w : 0.f;
+                        acc[mt][0][f] = fmaf(w, q.x, acc[mt][0][f]);
+                        acc[mt][1][f] = fmaf(w, q.y, acc[mt][1][f]);
+                        acc[mt][2][f] = fmaf(w, q.z, acc[mt][2][f]);
+                        acc[mt][3][f] = fmaf(w, q.w, acc[mt][3][f]);
+                        acc[mt][4][f] = fmaf(w, dd, acc[mt][4][f]);
+                        acc[mt][5][f] += w;
+                    }
+                }
+            }
+        }
+    }
+    if (pending) mbar_wait(&s.bar, phase);
+    tc_fence_after();
+    if (any_mma) {
+        const unsigned tl = tmem + ((unsigned)(32 * (wid & 3)) << 16);
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            float v[8];
+            tmem_ld_16x256b_x2(tl + (unsigned)(32 * j + rb), v);
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+                acc[0][j][f] += v[f];
+                acc[1][j][f] += v[4 + f];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (wid == 0) tmem_dealloc<TC_TMEM_COLS>(tmem);
+
+    // epilogue (K2 of nf_field_cta with this thread's pixel map)
+    const double Y00 = pl.h.Y0[0], Y01 = pl.h.Y0[1];
+    const float P0f = (float)pl.h.P[0], P1f = (float)pl.h.P[1], s0f = (float)pl.h.s0;
+    const float e00f = (float)pl.h.e0[0], e01f = (float)pl.h.e0[1];
+    const float bdx = (float)(Y00 - ox), bdy = (float)(Y01 - oy);
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const int mt = p >> 2, f = p & 3;
+        const int col = cb + 8 * (f >> 1) + g, r = rb + 8 * mt + 2 * tig + (f & 1);
+        const int i = ti0 + col, jj = tj0 + r;
+        const float s0v = acc[mt][0][f], s1v = acc[mt][1][f], s2v = acc[mt][2][f];
+        const float s3v = acc[mt][3][f], s4v = acc[mt][4][f], s5v = acc[mt][5][f];
+        const bool valid = i >= ci0 && i <= ci1 && jj >= cj0 && jj <= cj1;
+        bool exc = false;
+        if (valid) {
+            const size_t o = (size_t)(jj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (i - L.grid.i0);
+            if ((amb >> p) & 1u) {
+                exc = true;
+            } else if (s5v == 0.f) {
+                if (L.disp) L.disp[o] = make_float2(0.f, 0.f);
+                if (L.support) L.support[o] = 0;
+            } else {
+                const float rn = rsqrtf(fmaf(s0v, s0v, s1v * s1v));
+                const float qw = s0v * rn, qz = s1v * rn, qdx = s2v * rn, qdy = s3v * rn;
+                const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
+                const float ux = (float)col, uy = (float)r;
+                const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
+                const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
+                const float dl = __fdividef(s4v, s5v);  // s5 > 0, far from 2^126
+                const float sbf = s0f + dl;
+                const float rx = fmaf(sbf, Qx, fmaf(dl, P0f, e00f));
+                const float ry = fmaf(sbf, Qy, fmaf(dl, P1f, e01f));
+                if (L.disp) L.disp[o] = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
+                if (L.support) L.support[o] = 1;
+            }
+        }
+        defer_pixel<1>(L, exc, i, jj);
+    }
+}
+#endif
+
 template <int MODE>
 __global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
 k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
              int ntx) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     pdl_wait();
+#ifndef NRM_K2_MMASYNC
+    if constexpr (MODE == 1) {
+        nf_field_tc(L, plans, tile_i0, tile_j0, s1, by0, ntx, blockIdx.x, blockIdx.y, smem_raw);
+        return;
+    }
+#endif
     nf_field_cta<MODE>(L, plans, tile_i0, tile_j0, s1, by0, ntx, blockIdx.x, blockIdx.y, smem_raw);
 }
 
@@ -1233,7 +1515,12 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         L.lcounts = L.lists + (size_t)g.nchunks * L.col_groups * L.lstride;
     }
     const size_t base = (sizeof(Smem<K1Shape<0>::CW>) + 15) & ~size_t(15);
-    const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : sizeof(Smem<K1Shape<1>::CW>);
+#ifndef NRM_K2_MMASYNC
+    const size_t smem_k2 = sizeof(SmemTC);
+#else
+    const size_t smem_k2 = sizeof(Smem<K1Shape<1>::CW>);
+#endif
+    const size_t smem = mode != 1 ? base + sizeof(CanvasTile) : smem_k2;
     const int nh = mode == 1 ? K1Shape<1>::NH : K1Shape<0>::NH;
     const int kmode = mode == 1 ? 1 : (L.unc ? 2 : 0);  // 2: uncertainty-weighted blend
     auto k_field = kmode == 0 ? k_node_field<0> : (kmode == 1 ? k_node_field<1> : k_node_field<2>);
