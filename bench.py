@@ -253,7 +253,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false",
                     help="run K1 after K3 on one stream (default: K1 || K3 on two streams)")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: min(--steps, 300))")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="e2e steps (default: --steps clamped to [200, 300])")
     ap.add_argument("--no-estep", action="store_true", help="skip the EM E-step side measurement")
     ap.add_argument("--no-canvas-field", action="store_true", help="skip the canvas-wide field side measurement")
     ap.add_argument("--no-features", action="store_true", help="skip the feature detection / matching side measurement")
@@ -537,8 +537,11 @@ def main():
         while pending:
             pending.popleft().result()
 
-    e2e_steps = args.e2e_steps or min(args.steps, 300)
-    for _ in range(2 * inflight):
+    # the e2e loop is its own timed region (host threads, PCIe in both
+    # directions): at least 200 frames so short --steps runs still measure the
+    # steady state, not the pipeline's ramp
+    e2e_steps = args.e2e_steps or max(200, min(args.steps, 300))
+    for _ in range(max(10, 2 * inflight)):
         e2e_step()
     e2e_drain()
     torch.cuda.synchronize()
@@ -900,9 +903,8 @@ def run_canvas_mode(args):
 def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
     """Side measurement (BASELINE configs[3]: the canvas-wide field of a
     16384^2 canvas with its canvas-covering 1,497-node lattice, K2 =
-    k_node_field<1>): one pass, device-timed, with the roofline of the same
-    accumulation the blend uses (tensor cores), here without the canvas
-    epilogue.
+    k_node_field<1>, its inner-node sums on tcgen05): one pass, device-timed,
+    with the FP32 roofline of the reference's loop and the tensor-core view.
     Algorithmic work: contributing (pixel, node) pairs x 18 flops, counted
     with the reference's cutoff on a seeded pixel sample."""
     import torch
@@ -947,8 +949,18 @@ def canvas_field_numbers(ctx, stream, fp32_peak: float, n: int = 16384):
             "roofline_k_node_field": {"bound": "fp32", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
                                       "frac": ach / fp32_peak,
                                       "algorithmic": f"{n * n} px x {per_px:.1f} contributing nodes x 18 flops",
-                                      "note": "the inner-node sums run on the tensor cores (3xTF32 mma.sync); "
-                                              "this is the reference loop's FP32 work against the FP32 peak"},
+                                      "note": "the inner-node sums run on the 5th-generation tensor cores "
+                                              "(tcgen05.mma kind::tf32, 3xTF32 split products, FP32 accumulators "
+                                              "in tensor memory); this is the reference loop's FP32 work against "
+                                              "the FP32 peak",
+                                      "tensor_view": {
+                                          "achieved_tflops": n * n * per_px * 36.0 / (k_ms * 1e-3) / 1e12,
+                                          "definition": "3 TF32 products x 6 sums x 2 flops per contributing "
+                                                        "(pixel, node) pair (a lower bound: inner nodes are "
+                                                        "listed per 64 x 32 tile) over the k_node_field time",
+                                          "peak_tflops": peaks.get("bf16_tflops", 0.0) / 2.0 or None,
+                                          "peak_source": "dense TF32 = half the measured dense bf16 "
+                                                         "(MEASURED_PEAKS.json)"}},
             "canvas_deform": deform}
 
 

@@ -60,7 +60,13 @@ constexpr int NF_CHUNK_TILES = 2048;  // tile plans resident per launch chunk
 constexpr int NF_PLAN_WARPS = 8;      // planning warps (tiles) per CTA
 constexpr int NF_GROUP_TILES = 64;    // prefilter node lists per 64 tile columns (4096 px)
 constexpr int EXC_THREADS = 128;
-constexpr int EXC_BLOCKS = 148;
+#ifndef NRM_EXC_BLOCKS
+#define NRM_EXC_BLOCKS 148
+#endif
+#ifndef NRM_EXC_KC
+#define NRM_EXC_KC 4
+#endif
+constexpr int EXC_BLOCKS = NRM_EXC_BLOCKS;  // exception-pass CTAs (one warp per queued pixel, grid-stride)
 constexpr float kCutHi = (float)(1e-6 * (1.0 + 4e-6));
 constexpr float kCutLo = (float)(1e-6 * (1.0 - 4e-6));
 // Fast-tier accuracy. Its position error follows
@@ -1056,7 +1062,7 @@ k_node_field_batch(const NfBatchFrame* __restrict__ F, int nf, const NfPlan* __r
 __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ anchors,
                                 const double* __restrict__ warps, const int* __restrict__ src, int n, double alpha,
                                 W5* out, double* stage = nullptr) {
-    constexpr int KC = 4;  // node chunks whose weights are evaluated together (latency, not throughput)
+    constexpr int KC = NRM_EXC_KC;  // node chunks whose weights are evaluated together
     const int lane = threadIdx.x & 31;
     const double na = -alpha;
     double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
