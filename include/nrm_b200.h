@@ -365,9 +365,11 @@ int nrm_selftest_libm(nrm_ctx *ctx, const double *x, const double *y, int n, dou
  * tier. Synchronises the context stream. */
 int nrm_ctx_exceptions(nrm_ctx *ctx, int64_t *blend_exceptions, int64_t *emdq_exact);
 /* Exception-queue slots per launch (0 = default: 1/64 of the launch's
- * pixels, at least 2^18). Deferred pixels past the capacity are never lost:
- * they are marked in the output and resolved by a scan in the exact pass, so
- * results do not depend on this value (tests force tiny queues with it). */
+ * pixels, at least 2^18, for the node field and the blend; 1/32, at least
+ * 2^16, for the EMDQ field). Deferred pixels past the capacity are never
+ * lost: the node field and the blend mark them in the output and resolve
+ * them by a scan in the exact pass, the EMDQ field resolves them in place,
+ * so results do not depend on this value (tests force tiny queues with it). */
 int nrm_ctx_set_exception_capacity(nrm_ctx *ctx, int64_t slots);
 /* Number of launches on this context whose exception queue overflowed into
  * the scan path (diagnostics; synchronises the context stream). */

@@ -33,6 +33,7 @@
 //     are bit-identical to the reference's).
 //   Tiles whose candidates span more than a quarter turn of rotation
 //   (hemisphere flips possible) or overflow a capacity run in the exact tier.
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+
     {
         const int nb = gridDim.x * gridDim.y;
         for (int a = (blockIdx.y * gridDim.x + blockIdx.x) * ENT + t; a < L.nactive; a += nb * ENT) {
@@ -491,6 +493,11 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
 template <int MAXS>
 __device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx, int n, int S, const Cand C,
                                             double alpha, double beta, float2* od, float* ou) {
+#ifdef NRM_DEV_SKIP_EXACT  // development timing only: wrong results for exact-tier pixels
+    if (od) *od = make_float2(0.f, 0.f);
+    if (ou) *ou = 1.f;
+    return;
+#endif
     if (S <= 16 || MAXS <= 16)
         emdq_exact<16>(qx, qy, idx, n, S, C, alpha, beta, od, ou);
     else
@@ -508,6 +515,9 @@ __global__ void __launch_bounds__(PLAN_WARPS * 32)
 k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
+    // this chunk's exact-tier queue starts empty (the previous chunk's
+    // exception pass, or the previous call's, precedes this grid)
+    if (L.exq_count && threadIdx.x == 0 && blockIdx.x == 0) *L.exq_count = 0u;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     PlanWarp& w = reinterpret_cast<PlanWarp*>(smem_raw)[wid];
     const int g = blockIdx.x * PLAN_WARPS + wid;  // tile index within the chunk
@@ -1043,96 +1053,107 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
     const int pi = ti0 + lx, pj = tj0 + ly;
     const bool valid = pi <= ti1 && pj <= tj1;
     const size_t o = (size_t)(pj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (pi - L.grid.i0);
-    const double qx = L.grid.gx + pi, qy = L.grid.gy + pj;
     float2* od = (valid && L.disp) ? &L.disp[o] : nullptr;
     float* ou = (valid && L.unc) ? &L.unc[o] : nullptr;
 
-    if (flags & TFLAG_EXACT_SUPER) {  // exact brute force over the supertile list
-        const int sid = (ty / (ST / ET)) * SL.nsx + tx / (ST / ET);
-        const int* src = (SL.flag[sid] & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
-        if (valid) {
-            if (L.exact_count) atomicAdd(L.exact_count, 1u);
-            exact_dispatch<MAXS>(qx, qy, src, SL.count[sid], S, C, L.alpha, L.beta, od, ou);
-        }
-        return;
-    }
-    const int ne = h.ne, nin = h.nin;
-    const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
-    // separable weight tables (prob and the tile-wide d^2 floor folded into
-    // ey): thread = (record k, 4 columns / rows); the per-record terms once,
-    // float4 stores (ex[k][4q .. 4q+3], ey[k][4q .. 4q+3])
-    if (!(flags & TFLAG_EXACT_STAGED)) {
-        const int k = t >> 2, c0 = 4 * (t & 3);
-        if (k < ne) {
-            const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
-            const float4 r0 = sp.rec0[k];
-            const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
-            const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
-            const float base = nal * (dxr + dyr - d2ref);
-            float vx[4], vy[4];
+    // Exact-tier pixels. Whole tiles or sub-tiles flagged for the exact tier
+    // run it here, a thread per pixel (all lanes busy). Single pixels on a
+    // near-tie (~4e-5 of them on C2) are queued for k_emdq_exceptions (a warp
+    // per pixel) instead: resolved here, each cost its thread ~10 us of
+    // serial FP64 work and cold instruction fetches, which held the whole
+    // CTA and, at 86 pixels, a third of this kernel's time. Every lane
+    // reaches the push below (no early returns).
+    bool inline_exact = true;  // tile / sub-tile flagged for the exact tier
+    bool queue_exact = false;  // a single pixel on a near-tie
+    const int* xsrc = nullptr;  // inline exact: candidate list (staged list or supertile list)
+    int xn = 0;
+    if (!(flags & TFLAG_EXACT_SUPER)) {  // tile-uniform
+        const int ne = h.ne, nin = h.nin;
+        const int nxin = h.nx[wid], namb = h.na[wid], nnear = h.nn[wid];
+        // separable weight tables (prob and the tile-wide d^2 floor folded into
+        // ey): thread = (record k, 4 columns / rows); the per-record terms once,
+        // float4 stores (ex[k][4q .. 4q+3], ey[k][4q .. 4q+3])
+        if (!(flags & TFLAG_EXACT_STAGED)) {
+            const int k = t >> 2, c0 = 4 * (t & 3);
+            if (k < ne) {
+                const float nal = (float)(-L.alpha * kLog2e), d2ref = h.d2ref;
+                const float4 r0 = sp.rec0[k];
+                const float cx = fminf(fmaxf(r0.x, 0.f), (float)(ET - 1)), cy = fminf(fmaxf(r0.y, 0.f), (float)(ET - 1));
+                const float dxr = (r0.x - cx) * (r0.x - cx), dyr = (r0.y - cy) * (r0.y - cy);
+                const float base = nal * (dxr + dyr - d2ref);
+                float vx[4], vy[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float dx = r0.x - (float)(c0 + i), dy = r0.y - (float)(c0 + i);
-                vx[i] = ex2_approx(nal * (dx * dx - dxr));
-                vy[i] = ex2_approx(fmaf(nal, dy * dy - dyr, base)) * r0.z;
+                for (int i = 0; i < 4; ++i) {
+                    const float dx = r0.x - (float)(c0 + i), dy = r0.y - (float)(c0 + i);
+                    vx[i] = ex2_approx(nal * (dx * dx - dxr));
+                    vy[i] = ex2_approx(fmaf(nal, dy * dy - dyr, base)) * r0.z;
+                }
+                *reinterpret_cast<float4*>(&ex[k][c0]) = make_float4(vx[0], vx[1], vx[2], vx[3]);
+                *reinterpret_cast<float4*>(&ey[k][c0]) = make_float4(vy[0], vy[1], vy[2], vy[3]);
             }
-            *reinterpret_cast<float4*>(&ex[k][c0]) = make_float4(vx[0], vx[1], vx[2], vx[3]);
-            *reinterpret_cast<float4*>(&ey[k][c0]) = make_float4(vy[0], vy[1], vy[2], vy[3]);
+        }
+        __syncthreads();
+        xsrc = sp.sidx;
+        xn = ne;
+        const int wi = nin + nxin, m = S - wi;
+        if (!(flags & TFLAG_EXACT_STAGED) && !(nxin == 255 || m < 0 || wi + namb < S || namb > 32)) {
+            inline_exact = false;
+            FastOut fo;
+            if (valid) {
+                fast_dispatch(lx, ly, nin, sp.sub[wid], nxin, namb, m, sp, ex, ey, fo);
+                queue_exact = fo.exact || !(fo.s5 > 0.f);
+            }
+            if (valid && !queue_exact) {
+                const double qx = L.grid.gx + pi, qy = L.grid.gy + pj;
+            const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
+            const float qw = fo.s0 * rn, qz = fo.s1 * rn, qdx = fo.s2 * rn, qdy = fo.s3 * rn;
+            const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
+            const float ux = (float)lx, uy = (float)ly;
+            const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
+            const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
+            const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
+            // displacement y - q = (Y0 - tile origin - u) + (e0 + dl P + (s0 + dl) Q(u)):
+            // the first part is a small per-tile constant (bd, FP64 -> FP32), the
+            // second stays ~1e2 px, so FP32 keeps it to ~1e-5 px at any coordinate
+            // (the K1/K2 epilogue; error model: k_nodefield.cu kScaleLever)
+            if (od) {
+                const float sbf = (float)h.s0 + dlb;
+                const float rx = fmaf(sbf, Qx, fmaf(dlb, (float)h.P[0], (float)h.e0[0]));
+                const float ry = fmaf(sbf, Qy, fmaf(dlb, (float)h.P[1], (float)h.e0[1]));
+                const float bdx = (float)(h.Y0[0] - (L.grid.gx + ti0)), bdy = (float)(h.Y0[1] - (L.grid.gy + tj0));
+                *od = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
+            }
+            if (ou) {
+                // bounded_exp(beta d2min) (fieldest.hpp:44-52) to FP32 output
+                // precision: d2min in FP64 over the points that can be the nearest in
+                // this sub-tile; exp(x) = 2^n 2^f, n = rint(x log2 e), |f| <= 1/2 in
+                // FP64, 2^f on MUFU.EX2 (relative error < 3e-7, inside the 1e-6 bar)
+                double d2m = DBL_MAX;
+                const int nl = nnear == 255 ? ne : nnear;
+                for (int e = 0; e < nl; ++e) {
+                    const int k = nnear == 255 ? e : sp.near[wid][e];
+                    const double2 a = sp.axy[k];
+                    const double dx = qx - a.x, dy = qy - a.y;
+                    d2m = fmin(d2m, fma(dx, dx, dy * dy));
+                }
+                const double tx = fmin(L.beta * d2m, 55.0) * 1.4426950408889634;
+                const double n = rint(tx);
+                *ou = ex2_approx((float)(tx - n)) * __int_as_float(((int)n + 127) << 23);
+            }
+            }
         }
     }
-    __syncthreads();
-    if (!valid) return;
-    if (flags & TFLAG_EXACT_STAGED) {
-        if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, sp.sidx, ne, S, C, L.alpha, L.beta, od, ou);
-        return;
+    if (flags & TFLAG_EXACT_SUPER) {
+        const int sid = (ty / (ST / ET)) * SL.nsx + tx / (ST / ET);
+        xsrc = (SL.flag[sid] & SFLAG_OVERFLOW) ? nullptr : SL.list + (size_t)sid * SLIST_CAP;
+        xn = xsrc ? SL.count[sid] : L.nactive;
     }
-    const int wi = nin + nxin, m = S - wi;
-    FastOut fo;
-    bool exr = nxin == 255 || m < 0 || wi + namb < S || namb > 32;
-    if (!exr) {
-        fast_dispatch(lx, ly, nin, sp.sub[wid], nxin, namb, m, sp, ex, ey, fo);
-        exr = fo.exact || !(fo.s5 > 0.f);
-    }
-    if (exr) {
-        if (L.exact_count) atomicAdd(L.exact_count, 1u);
-        exact_dispatch<MAXS>(qx, qy, sp.sidx, ne, S, C, L.alpha, L.beta, od, ou);
-        return;
-    }
-    const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
-    const float qw = fo.s0 * rn, qz = fo.s1 * rn, qdx = fo.s2 * rn, qdy = fo.s3 * rn;
-    const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
-    const float ux = (float)lx, uy = (float)ly;
-    const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
-    const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
-    const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
-    // displacement y - q = (Y0 - tile origin - u) + (e0 + dl P + (s0 + dl) Q(u)):
-    // the first part is a small per-tile constant (bd, FP64 -> FP32), the
-    // second stays ~1e2 px, so FP32 keeps it to ~1e-5 px at any coordinate
-    // (the K1/K2 epilogue; error model: k_nodefield.cu kScaleLever)
-    if (od) {
-        const float sbf = (float)h.s0 + dlb;
-        const float rx = fmaf(sbf, Qx, fmaf(dlb, (float)h.P[0], (float)h.e0[0]));
-        const float ry = fmaf(sbf, Qy, fmaf(dlb, (float)h.P[1], (float)h.e0[1]));
-        const float bdx = (float)(h.Y0[0] - (L.grid.gx + ti0)), bdy = (float)(h.Y0[1] - (L.grid.gy + tj0));
-        *od = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
-    }
-    if (ou) {
-        // bounded_exp(beta d2min) (fieldest.hpp:44-52) to FP32 output
-        // precision: d2min in FP64 over the points that can be the nearest in
-        // this sub-tile; exp(x) = 2^n 2^f, n = rint(x log2 e), |f| <= 1/2 in
-        // FP64, 2^f on MUFU.EX2 (relative error < 3e-7, inside the 1e-6 bar)
-        double d2m = DBL_MAX;
-        const int nl = nnear == 255 ? ne : nnear;
-        for (int e = 0; e < nl; ++e) {
-            const int k = nnear == 255 ? e : sp.near[wid][e];
-            const double2 a = sp.axy[k];
-            const double dx = qx - a.x, dy = qy - a.y;
-            d2m = fmin(d2m, fma(dx, dx, dy * dy));
-        }
-        const double tx = fmin(L.beta * d2m, 55.0) * 1.4426950408889634;
-        const double n = rint(tx);
-        *ou = ex2_approx((float)(tx - n)) * __int_as_float(((int)n + 127) << 23);
+    if ((inline_exact || queue_exact) && valid && L.exact_count) atomicAdd(L.exact_count, 1u);
+    // queued unless there is no queue or the slot was past its capacity
+    if (inline_exact) {
+        if (valid) exact_dispatch<MAXS>(L.grid.gx + pi, L.grid.gy + pj, xsrc, xn, S, C, L.alpha, L.beta, od, ou);
+    } else if (L.exq ? queue_push(queue_exact, pi, pj, L.exq, L.exq_count, L.exq_cap) : queue_exact) {
+        exact_dispatch<MAXS>(L.grid.gx + pi, L.grid.gy + pj, xsrc, xn, S, C, L.alpha, L.beta, od, ou);
     }
 }
 
@@ -1153,6 +1174,184 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
     }
     mbar_wait(&s.bar, 0);
     pixels_tile<MAXS>(L, C, SL, s.p, s.ex, s.ey, TP.tx0 + blockIdx.x, TP.ty0 + blockIdx.y, S);
+}
+
+// ---------------------------------------------------------------------------
+// k_emdq_exceptions: the dense field's exact-tier pixels (queued by
+// k_pixels), one warp per pixel, bit-identical to emdq_exact / the
+// reference's blend_local + node_uncertainty (fieldest.hpp:44-52, 75-97):
+//   * the S nearest by (d^2, j) over the pixel's supertile list: S rounds of
+//     a warp-wide minimum over the keys above the previous round's (lanes
+//     scan strided candidates, FP64 d^2 as xdist2);
+//   * lane s holds member s: its weight exp(-alpha (d^2 - d2min)) prob in
+//     parallel (glibc-exact exp), then the reference's ordered sums (wsum,
+//     then the hemisphere-aligned weighted warps) as a shuffle chain;
+//   * lane 0 normalises, applies and writes the displacement and the
+//     uncertainty bounded_exp(beta d2min).
+// ---------------------------------------------------------------------------
+constexpr int EXQ_THREADS = 128, EXQ_BLOCKS = 148 * 8;  // 4736 warps resident at most; idle ones exit
+__device__ __forceinline__ void warp_min_key(double& d, int& j, int& a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, d, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, j, o), oa = __shfl_xor_sync(0xffffffffu, a, o);
+        if (key_less(od, oj, d, j)) {
+            d = od;
+            j = oj;
+            a = oa;
+        }
+    }
+}
+
+__device__ void exact_pixel_warp(const EmdqLaunch& L, const Cand& C, const TilePlans& TP, int S, int pi, int pj) {
+    const int lane = threadIdx.x & 31;
+    const double qx = L.grid.gx + pi, qy = L.grid.gy + pj;
+    // the pixel's tile plan (this launch chunk): its staged list (in +
+    // ambiguous, at most TREC) holds every candidate of the pixel's S nearest
+    const int g = ((pj - L.grid.j0) / ET - TP.ty0) * TP.ntx + (pi - L.grid.i0) / ET - TP.tx0;
+    const int* src = TP.plan[g].sidx;
+    const int n = TP.plan[g].hdr.ne;
+    // 1. the kk = min(S, n) nearest, in (d^2, j) order. Up to 4 candidates
+    //    per lane (lists of at most 128) stay in registers across the rounds;
+    //    longer lists are rescanned every round.
+    constexpr int RC = 4;
+    double my_d2 = DBL_MAX, last_d = -1.0;
+    int my_a = -1, last_j = -1, kk = 0;
+    if (n <= 32 * RC) {
+        double cd[RC];
+        int cj[RC], ca[RC];
+#pragma unroll
+        for (int r = 0; r < RC; ++r) {
+            const int e = lane + 32 * r;
+            cd[r] = DBL_MAX;
+            cj[r] = INT_MAX;
+            ca[r] = -1;
+            if (e < n) {
+                const int a = src ? src[e] : e;
+                ca[r] = a;
+                cj[r] = C.j[a];
+                cd[r] = xdist2(qx, qy, C.x[a], C.y[a]);
+            }
+        }
+        for (int s = 0; s < S; ++s) {
+            double bd = DBL_MAX;
+            int bj = INT_MAX, ba = -1;
+#pragma unroll
+            for (int r = 0; r < RC; ++r)
+                if (ca[r] >= 0 && key_less(last_d, last_j, cd[r], cj[r]) && key_less(cd[r], cj[r], bd, bj)) {
+                    bd = cd[r];
+                    bj = cj[r];
+                    ba = ca[r];
+                }
+            warp_min_key(bd, bj, ba);
+            if (ba < 0) break;  // warp-uniform: no candidate left
+            if (lane == s) {
+                my_d2 = bd;
+                my_a = ba;
+            }
+            last_d = bd;
+            last_j = bj;
+            ++kk;
+        }
+    } else {
+        for (int s = 0; s < S; ++s) {
+            double bd = DBL_MAX;
+            int bj = INT_MAX, ba = -1;
+            for (int e = lane; e < n; e += 32) {
+                const int a = src ? src[e] : e;
+                const int j = C.j[a];
+                const double d2 = xdist2(qx, qy, C.x[a], C.y[a]);
+                if (key_less(last_d, last_j, d2, j) && key_less(d2, j, bd, bj)) {
+                    bd = d2;
+                    bj = j;
+                    ba = a;
+                }
+            }
+            warp_min_key(bd, bj, ba);
+            if (ba < 0) break;  // warp-uniform: no candidate left
+            if (lane == s) {
+                my_d2 = bd;
+                my_a = ba;
+            }
+            last_d = bd;
+            last_j = bj;
+            ++kk;
+        }
+    }
+    const double d2min = __shfl_sync(0xffffffffu, my_d2, 0);  // DBL_MAX when kk == 0
+    // 2. weights, in parallel (emdq_blend_exact's expressions)
+    const bool mem = lane < kk;
+    double w = 0.0;
+    if (mem) w = xmul(xexp(xmul(-L.alpha, xsub(my_d2, d2min))), C.p[my_a]);
+    const unsigned pos = __ballot_sync(0xffffffffu, mem && w > 0.0);
+    int rc = kk == 0 ? 1 : (pos ? 0 : 2);
+    double wsum = 0.0;
+    for (int s = 0; s < kk; ++s) wsum = xadd(wsum, __shfl_sync(0xffffffffu, w, s));
+    // 3. hemisphere-aligned weighted warps, summed in member order
+    const int ref = pos ? __ffs(pos) - 1 : 0;
+    double q0 = 0.0, qw = 0.0, qz = 0.0, qdx = 0.0, qdy = 0.0;
+    if (mem) {
+        const double* q = &C.l[5 * my_a];
+        q0 = q[0];
+        qw = q[1];
+        qz = q[2];
+        qdx = q[3];
+        qdy = q[4];
+    }
+    const double rw = __shfl_sync(0xffffffffu, qw, ref), rz = __shfl_sync(0xffffffffu, qz, ref);
+    if (xadd(xmul(qw, rw), xmul(qz, rz)) < 0.0) {
+        qw = -qw;
+        qz = -qz;
+        qdx = -qdx;
+        qdy = -qdy;
+    }
+    const double p0 = xmul(w, qw), p1 = xmul(w, qz), p2 = xmul(w, qdx), p3 = xmul(w, qdy), p4 = xmul(w, q0);
+    double sw = 0.0, sz = 0.0, sdx = 0.0, sdy = 0.0, ss = 0.0;
+    for (unsigned m = pos; m; m &= m - 1u) {  // contributing members (w > 0) in order
+        const int s = __ffs(m) - 1;
+        sw = xadd(sw, __shfl_sync(0xffffffffu, p0, s));
+        sz = xadd(sz, __shfl_sync(0xffffffffu, p1, s));
+        sdx = xadd(sdx, __shfl_sync(0xffffffffu, p2, s));
+        sdy = xadd(sdy, __shfl_sync(0xffffffffu, p3, s));
+        ss = xadd(ss, __shfl_sync(0xffffffffu, p4, s));
+    }
+    if (lane != 0) return;
+    W5 f;
+    if (rc == 0) {
+        const double mw = sw / wsum, mz = sz / wsum, mdx = sdx / wsum, mdy = sdy / wsum;
+        const double nr = xhypot(mw, mz);
+        if (!(nr >= 1e-300))
+            rc = 2;
+        else
+            f = W5{ss / wsum, mw / nr, mz / nr, mdx / nr, mdy / nr};
+    }
+    const size_t o = (size_t)(pj - L.grid.j0) * (L.grid.i1 - L.grid.i0 + 1) + (pi - L.grid.i0);
+    if (L.disp) {
+        float2 dout = make_float2(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+        if (rc == 0) {
+            double yx, yy;
+            xapply(f, qx, qy, &yx, &yy);
+            dout = make_float2((float)(yx - qx), (float)(yy - qy));
+        }
+        L.disp[o] = dout;
+    }
+    if (L.unc) {
+        double arg = xmul(L.beta, d2min);
+        if (55.0 < arg) arg = 55.0;
+        L.unc[o] = (float)xexp(arg);
+    }
+}
+
+// One launch per chunk of tiles, after that chunk's k_pixels (the next
+// chunk's k_plan empties the queue and rewrites the plans).
+__global__ void __launch_bounds__(EXQ_THREADS) k_emdq_exceptions(EmdqLaunch L, Cand C, TilePlans TP, int S) {
+    pdl_wait();
+    const unsigned cnt = min(*L.exq_count, L.exq_cap);
+    const unsigned gw = blockIdx.x * (EXQ_THREADS / 32) + (threadIdx.x >> 5), nw = gridDim.x * (EXQ_THREADS / 32);
+    for (unsigned i = gw; i < cnt; i += nw) {
+        const int2 p = L.exq[i];
+        exact_pixel_warp(L, C, TP, S, p.x, p.y);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1244,11 +1443,21 @@ __global__ void k_points_bbox(const double* __restrict__ q, int nq, double* out4
 
 }  // namespace
 
+// Exact-tier queue of a dense field: the fast tier defers ~4e-5 of the pixels
+// on C2 (86 of 2.07 M), plus whole tiles flagged for the exact tier; 1/32 of
+// the grid, at least 2^16 slots of 8 B. A push past the capacity resolves its
+// pixel in place (k_pixels), so nothing depends on the size.
+static unsigned emdq_queue_cap(const FieldGrid& g) {
+    const size_t px = (size_t)(g.i1 - g.i0 + 1) * (size_t)(g.j1 - g.j0 + 1);
+    return (unsigned)std::min<size_t>(std::max<size_t>((size_t)1 << 16, px / 32), (size_t)1 << 30);
+}
+static size_t emdq_queue_bytes(const FieldGrid& g) { return (size_t)emdq_queue_cap(g) * sizeof(int2) + 16; }
+
 size_t emdq_scratch_bytes(int nactive, const FieldGrid& g, bool tile_plans) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nsuper = (size_t)nsx * nsy;
-    const size_t plans = tile_plans ? (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan) : 0;
+    const size_t plans = tile_plans ? (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan) + 256 + emdq_queue_bytes(g) : 0;
     return na * 9 * sizeof(double) + na * sizeof(float2) + na * sizeof(int) + nsuper * (SLIST_CAP + 2) * sizeof(int) +
            plans + 1024;
 }
@@ -1280,6 +1489,15 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     pbase = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(pbase) + 255) & ~uintptr_t(255));
     TilePlans TP;
     TP.plan = reinterpret_cast<TilePlan*>(pbase);
+    EmdqLaunch LQ = L;  // with the exact-tier queue behind the tile plans
+    {
+        char* qb = pbase + (size_t)EMDQ_CHUNK_TILES * sizeof(TilePlan);
+        qb = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(qb) + 255) & ~uintptr_t(255));
+        LQ.exq_count = reinterpret_cast<unsigned*>(qb);
+        LQ.exq = reinterpret_cast<int2*>(qb + 16);
+        LQ.exq_cap = emdq_queue_cap(L.grid);
+        if (L.exq_cap_override > 0 && (uint64_t)L.exq_cap_override < LQ.exq_cap) LQ.exq_cap = (unsigned)L.exq_cap_override;
+    }
 
     const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
     const int S = L.support < L.nactive ? L.support : L.nactive;
@@ -1287,7 +1505,7 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
                        (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
-    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, S, 0.f);
+    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(LQ, G, SL, S, 0.f);
     ++*launches;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1304,15 +1522,19 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
         TP.ntx = ntx;
         const int ntiles = rows * ntx;
         prof_mark("k_plan", st);
-        e = launch_pdl(k_plan, dim3((ntiles + PLAN_WARPS - 1) / PLAN_WARPS), dim3(PLAN_WARPS * 32), psm, st, L, C, SL,
+        e = launch_pdl(k_plan, dim3((ntiles + PLAN_WARPS - 1) / PLAN_WARPS), dim3(PLAN_WARPS * 32), psm, st, LQ, C, SL,
                        TP, ntiles, S);
         if (e != cudaSuccess) return e;
         ++*launches;
         prof_mark("k_pixels", st);
-        e = launch_pdl(S <= 16 ? k_pixels<16> : k_pixels<MAX_SUPPORT>, dim3(ntx, rows), dim3(ENT), 0, st, L, C, SL,
+        e = launch_pdl(S <= 16 ? k_pixels<16> : k_pixels<MAX_SUPPORT>, dim3(ntx, rows), dim3(ENT), 0, st, LQ, C, SL,
                        TP, S);
         ++*launches;
         e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        prof_mark("k_emdq_exceptions", st);
+        e = launch_pdl(k_emdq_exceptions, dim3(EXQ_BLOCKS), dim3(EXQ_THREADS), 0, st, LQ, C, TP, S);
+        ++*launches;
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

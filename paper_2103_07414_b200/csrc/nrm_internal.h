@@ -190,6 +190,12 @@ struct EmdqLaunch {
     float2* disp = nullptr;
     float* unc = nullptr;
     unsigned* exact_count = nullptr;  // pixels that took the exact tier (diagnostics, accumulated)
+    // exact-tier queue of the dense field (k_pixels -> k_emdq_exceptions),
+    // carved from the scratch by launch_emdq_field
+    int2* exq = nullptr;
+    unsigned* exq_count = nullptr;
+    unsigned exq_cap = 0;
+    int64_t exq_cap_override = 0;  // nrm_ctx_set_exception_capacity (tests); 0 = default sizing
     // scratch: gathered candidates (SoA, nactive each)
     double* cx = nullptr;
     double* cy = nullptr;

@@ -276,3 +276,27 @@ def test_banded_node_field_is_bitwise_identical(nrm, ctx):
         ctx.synchronize()
         mask = torch.from_numpy(D.owned_rows_mask(y0, h, 1, world)).to(dev)
         assert torch.equal(d_1[mask], d_full[mask]) and torch.isnan(d_1[~mask]).all()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_emdq_exact_queue_matches_inline_exact_bitwise(nrm, ctx, name):
+    """The dense EMDQ field queues single near-tie pixels for the warp-parallel
+    exact pass (k_emdq_exceptions). With a one-slot queue every pixel but one
+    runs the thread-per-pixel exact tier inside k_pixels instead; both must
+    give the same bits (the inline tier is the one pinned to the reference)."""
+    from paper_2103_07414_b200 import workload as W
+    wl = W.frame_workload(name)
+    e = wl.emdq
+    grid = (0.0, 0.0, wl.frame_w, wl.frame_h)
+    args = (grid, e.apts, e.locals_, e.probs, e.active, wl.params.alpha, wl.params.beta, 16)
+    d0, u0 = nrm.emdq_field(*args, ctx=ctx)
+    n_exact = ctx.exceptions()[1]
+    assert n_exact > 1, "no exact-tier pixels: the test does not reach the queue"
+    ctx.set_exception_capacity(1)
+    try:
+        d1, u1 = nrm.emdq_field(*args, ctx=ctx)
+    finally:
+        ctx.set_exception_capacity(0)
+    assert ctx.exceptions()[1] == n_exact
+    assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
+    assert np.array_equal(u0.view(np.uint32), u1.view(np.uint32))
