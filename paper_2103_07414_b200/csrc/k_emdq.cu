@@ -1212,45 +1212,78 @@ __device__ void exact_pixel_warp(const EmdqLaunch& L, const Cand& C, const TileP
     const int* src = TP.plan[g].sidx;
     const int n = TP.plan[g].hdr.ne;
     // 1. the kk = min(S, n) nearest, in (d^2, j) order. Up to 4 candidates
-    //    per lane (lists of at most 128) stay in registers across the rounds;
-    //    longer lists are rescanned every round.
+    //    per lane (lists of at most 128) stay in registers, sorted per lane;
+    //    each round takes the warp minimum of the lanes' heads (keys compared
+    //    as integers: d^2 >= 0, so its bits order like the values) and the
+    //    winner shifts its list. Longer lists are rescanned every round.
     constexpr int RC = 4;
     double my_d2 = DBL_MAX, last_d = -1.0;
     int my_a = -1, last_j = -1, kk = 0;
     if (n <= 32 * RC) {
-        double cd[RC];
+        unsigned long long cu[RC];
         int cj[RC], ca[RC];
 #pragma unroll
         for (int r = 0; r < RC; ++r) {
             const int e = lane + 32 * r;
-            cd[r] = DBL_MAX;
+            cu[r] = ~0ull;
             cj[r] = INT_MAX;
             ca[r] = -1;
             if (e < n) {
                 const int a = src ? src[e] : e;
                 ca[r] = a;
                 cj[r] = C.j[a];
-                cd[r] = xdist2(qx, qy, C.x[a], C.y[a]);
+                cu[r] = (unsigned long long)__double_as_longlong(xdist2(qx, qy, C.x[a], C.y[a]));
             }
         }
+        auto lt = [](unsigned long long ua, int ja, unsigned long long ub, int jb) {
+            return ua < ub || (ua == ub && ja < jb);
+        };
+        auto cx = [&](int p, int q) {  // compare-exchange: slot p gets the smaller key
+            if (lt(cu[q], cj[q], cu[p], cj[p])) {
+                const unsigned long long tu = cu[p];
+                const int tj = cj[p], ta = ca[p];
+                cu[p] = cu[q];
+                cj[p] = cj[q];
+                ca[p] = ca[q];
+                cu[q] = tu;
+                cj[q] = tj;
+                ca[q] = ta;
+            }
+        };
+        cx(0, 1);  // 4-element sorting network
+        cx(2, 3);
+        cx(0, 2);
+        cx(1, 3);
+        cx(1, 2);
         for (int s = 0; s < S; ++s) {
-            double bd = DBL_MAX;
-            int bj = INT_MAX, ba = -1;
+            unsigned long long bu = cu[0];
+            int bj = cj[0], ba = ca[0];
 #pragma unroll
-            for (int r = 0; r < RC; ++r)
-                if (ca[r] >= 0 && key_less(last_d, last_j, cd[r], cj[r]) && key_less(cd[r], cj[r], bd, bj)) {
-                    bd = cd[r];
-                    bj = cj[r];
-                    ba = ca[r];
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long ou = __shfl_xor_sync(0xffffffffu, bu, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, bj, o), oa = __shfl_xor_sync(0xffffffffu, ba, o);
+                if (lt(ou, oj, bu, bj)) {
+                    bu = ou;
+                    bj = oj;
+                    ba = oa;
                 }
-            warp_min_key(bd, bj, ba);
+            }
             if (ba < 0) break;  // warp-uniform: no candidate left
+            if (ca[0] == ba) {  // the winner's next candidate becomes its head
+#pragma unroll
+                for (int r = 0; r + 1 < RC; ++r) {
+                    cu[r] = cu[r + 1];
+                    cj[r] = cj[r + 1];
+                    ca[r] = ca[r + 1];
+                }
+                cu[RC - 1] = ~0ull;
+                cj[RC - 1] = INT_MAX;
+                ca[RC - 1] = -1;
+            }
             if (lane == s) {
-                my_d2 = bd;
+                my_d2 = __longlong_as_double((long long)bu);
                 my_a = ba;
             }
-            last_d = bd;
-            last_j = bj;
             ++kk;
         }
     } else {
