@@ -79,7 +79,10 @@ struct SuperLists {
 
 constexpr int TREC = 64;          // staged records per tile (in + ambiguous)
 constexpr int TCAND = 128;        // tile candidates before classification
-constexpr int PLAN_WARPS = 8;     // planning warps (tiles) per CTA
+#ifndef NRM_PLAN_WARPS
+#define NRM_PLAN_WARPS 4  // 4-tile CTAs: finer than 8 for the last of ~2.3 waves (51.2 -> 48.9 us on C2)
+#endif
+constexpr int PLAN_WARPS = NRM_PLAN_WARPS;  // planning warps (tiles) per CTA
 constexpr int TFLAG_EXACT_SUPER = 1, TFLAG_EXACT_STAGED = 2;
 constexpr double kLocalMax = 256.0;    // px: staged tile-local coordinates (|u| < 2^8, ulp 2^-15)
 constexpr double kScaleLever = 640.0;  // px: max S |P| for the fast tier (k_nodefield.cu)
