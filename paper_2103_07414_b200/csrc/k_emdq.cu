@@ -1193,6 +1193,11 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
 //     uncertainty bounded_exp(beta d2min).
 // ---------------------------------------------------------------------------
 constexpr int EXQ_THREADS = 128, EXQ_BLOCKS = 148 * 8;  // 4736 warps resident at most; idle ones exit
+struct ExqWarp {
+    uint4 key[TREC];      // d^2 bits (lo, hi), j
+    int4 mem[MAX_SUPPORT];  // members in order: candidate, -, d^2 bits (lo, hi)
+};
+__shared__ ExqWarp exq_smem[EXQ_THREADS / 32];
 __device__ __forceinline__ void warp_min_key(double& d, int& j, int& a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1213,106 +1218,51 @@ __device__ void exact_pixel_warp(const EmdqLaunch& L, const Cand& C, const TileP
     // ambiguous, at most TREC) holds every candidate of the pixel's S nearest
     const int g = ((pj - L.grid.j0) / ET - TP.ty0) * TP.ntx + (pi - L.grid.i0) / ET - TP.tx0;
     const int* src = TP.plan[g].sidx;
-    const int n = TP.plan[g].hdr.ne;
-    // 1. the kk = min(S, n) nearest, in (d^2, j) order. Up to 4 candidates
-    //    per lane (lists of at most 128) stay in registers, sorted per lane;
-    //    each round takes the warp minimum of the lanes' heads (keys compared
-    //    as integers: d^2 >= 0, so its bits order like the values) and the
-    //    winner shifts its list. Longer lists are rescanned every round.
-    constexpr int RC = 4;
-    double my_d2 = DBL_MAX, last_d = -1.0;
-    int my_a = -1, last_j = -1, kk = 0;
-    if (n <= 32 * RC) {
-        unsigned long long cu[RC];
-        int cj[RC], ca[RC];
+    const int n = min(TP.plan[g].hdr.ne, TREC);  // queued pixels come from planned (non-exact) tiles: ne <= TREC
+    // 1. the kk = min(S, n) nearest, in (d^2, j) order: every staged
+    //    candidate (n <= TREC = 64, two per lane) gets its rank among all n by
+    //    one pass over the warp's keys in shared memory (d^2 >= 0, so its bits
+    //    compare as integers; ties by j); the one of rank s goes to lane s.
+    ExqWarp& xw = exq_smem[threadIdx.x >> 5];
+    double my_d2 = DBL_MAX;
+    int my_a = -1;
+    const int kk = min(S, n);
+    {
+        unsigned long long ku[2];
+        int kj[2], ka[2];
 #pragma unroll
-        for (int r = 0; r < RC; ++r) {
+        for (int r = 0; r < 2; ++r) {
             const int e = lane + 32 * r;
-            cu[r] = ~0ull;
-            cj[r] = INT_MAX;
-            ca[r] = -1;
+            ku[r] = ~0ull;
+            kj[r] = INT_MAX;
+            ka[r] = -1;
             if (e < n) {
-                const int a = src ? src[e] : e;
-                ca[r] = a;
-                cj[r] = C.j[a];
-                cu[r] = (unsigned long long)__double_as_longlong(xdist2(qx, qy, C.x[a], C.y[a]));
+                const int a = src[e];
+                ka[r] = a;
+                kj[r] = C.j[a];
+                ku[r] = (unsigned long long)__double_as_longlong(xdist2(qx, qy, C.x[a], C.y[a]));
+                xw.key[e] = make_uint4((unsigned)ku[r], (unsigned)(ku[r] >> 32), (unsigned)kj[r], 0u);
             }
         }
-        auto lt = [](unsigned long long ua, int ja, unsigned long long ub, int jb) {
-            return ua < ub || (ua == ub && ja < jb);
-        };
-        auto cx = [&](int p, int q) {  // compare-exchange: slot p gets the smaller key
-            if (lt(cu[q], cj[q], cu[p], cj[p])) {
-                const unsigned long long tu = cu[p];
-                const int tj = cj[p], ta = ca[p];
-                cu[p] = cu[q];
-                cj[p] = cj[q];
-                ca[p] = ca[q];
-                cu[q] = tu;
-                cj[q] = tj;
-                ca[q] = ta;
-            }
-        };
-        cx(0, 1);  // 4-element sorting network
-        cx(2, 3);
-        cx(0, 2);
-        cx(1, 3);
-        cx(1, 2);
-        for (int s = 0; s < S; ++s) {
-            unsigned long long bu = cu[0];
-            int bj = cj[0], ba = ca[0];
+        __syncwarp();
+        int rank[2] = {0, 0};
+        for (int e = 0; e < n; ++e) {
+            const uint4 o = xw.key[e];  // broadcast
+            const unsigned long long ou = ((unsigned long long)o.y << 32) | o.x;
+            const int oj = (int)o.z;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long ou = __shfl_xor_sync(0xffffffffu, bu, o);
-                const int oj = __shfl_xor_sync(0xffffffffu, bj, o), oa = __shfl_xor_sync(0xffffffffu, ba, o);
-                if (lt(ou, oj, bu, bj)) {
-                    bu = ou;
-                    bj = oj;
-                    ba = oa;
-                }
-            }
-            if (ba < 0) break;  // warp-uniform: no candidate left
-            if (ca[0] == ba) {  // the winner's next candidate becomes its head
+            for (int r = 0; r < 2; ++r) rank[r] += (ou < ku[r] || (ou == ku[r] && oj < kj[r])) ? 1 : 0;
+        }
 #pragma unroll
-                for (int r = 0; r + 1 < RC; ++r) {
-                    cu[r] = cu[r + 1];
-                    cj[r] = cj[r + 1];
-                    ca[r] = ca[r + 1];
-                }
-                cu[RC - 1] = ~0ull;
-                cj[RC - 1] = INT_MAX;
-                ca[RC - 1] = -1;
-            }
-            if (lane == s) {
-                my_d2 = __longlong_as_double((long long)bu);
-                my_a = ba;
-            }
-            ++kk;
+        for (int r = 0; r < 2; ++r)
+            if (ka[r] >= 0 && rank[r] < kk) xw.mem[rank[r]] = make_int4(ka[r], 0, (int)(unsigned)ku[r], (int)(ku[r] >> 32));
+        __syncwarp();
+        if (lane < kk) {
+            const int4 m = xw.mem[lane];
+            my_a = m.x;
+            my_d2 = __longlong_as_double((long long)(((unsigned long long)(unsigned)m.w << 32) | (unsigned)m.z));
         }
-    } else {
-        for (int s = 0; s < S; ++s) {
-            double bd = DBL_MAX;
-            int bj = INT_MAX, ba = -1;
-            for (int e = lane; e < n; e += 32) {
-                const int a = src ? src[e] : e;
-                const int j = C.j[a];
-                const double d2 = xdist2(qx, qy, C.x[a], C.y[a]);
-                if (key_less(last_d, last_j, d2, j) && key_less(d2, j, bd, bj)) {
-                    bd = d2;
-                    bj = j;
-                    ba = a;
-                }
-            }
-            warp_min_key(bd, bj, ba);
-            if (ba < 0) break;  // warp-uniform: no candidate left
-            if (lane == s) {
-                my_d2 = bd;
-                my_a = ba;
-            }
-            last_d = bd;
-            last_j = bj;
-            ++kk;
-        }
+        __syncwarp();  // the warp's next pixel rewrites the keys
     }
     const double d2min = __shfl_sync(0xffffffffu, my_d2, 0);  // DBL_MAX when kk == 0
     // 2. weights, in parallel (emdq_blend_exact's expressions)
