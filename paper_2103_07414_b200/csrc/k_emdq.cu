@@ -1192,7 +1192,10 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
 //   * lane 0 normalises, applies and writes the displacement and the
 //     uncertainty bounded_exp(beta d2min).
 // ---------------------------------------------------------------------------
-constexpr int EXQ_THREADS = 128, EXQ_BLOCKS = 148 * 8;  // 4736 warps resident at most; idle ones exit
+#ifndef NRM_EXQ_BLOCKS
+#define NRM_EXQ_BLOCKS 148
+#endif
+constexpr int EXQ_THREADS = 128, EXQ_BLOCKS = NRM_EXQ_BLOCKS;  // grid-stride; warps without a pixel exit
 struct ExqWarp {
     uint4 key[TREC];      // d^2 bits (lo, hi), j
     int4 mem[MAX_SUPPORT];  // members in order: candidate, -, d^2 bits (lo, hi)
