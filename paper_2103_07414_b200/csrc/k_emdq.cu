@@ -226,7 +226,8 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-
+    // this call's count of exact-tier pixels (k_pixels adds to it)
+    if (L.exact_count && t == 0 && blockIdx.x == 0 && blockIdx.y == 0) *L.exact_count = 0u;
     {
         const int nb = gridDim.x * gridDim.y;
         for (int a = (blockIdx.y * gridDim.x + blockIdx.x) * ENT + t; a < L.nactive; a += nb * ENT) {
@@ -1494,9 +1495,10 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
                        (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     prof_mark("k_super", st);
-    k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(LQ, G, SL, S, 0.f);
+    // programmatic launch: its CTAs become resident while the stream's previous
+    // kernel drains and wait in pdl_wait() before touching any scratch
+    cudaError_t e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, LQ, G, SL, S, 0.f);
     ++*launches;
-    cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int ntx = (L.grid.i1 - L.grid.i0 + ET) / ET;
     const int nty = (L.grid.j1 - L.grid.j0 + ET) / ET;

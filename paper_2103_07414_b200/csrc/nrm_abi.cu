@@ -493,9 +493,8 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     L.cy = base + na;
     L.cl = base + 2 * na;
     L.cp = base + 7 * na;  // phi, c32, j, supertile lists and plans follow: see launch_emdq_field
-    L.exact_count = state_of(c).emdq_exact;
+    L.exact_count = state_of(c).emdq_exact;  // zeroed by k_super (no memset node in the PDL chain)
     L.exq_cap_override = c->exc_cap_override;
-    NRM_CUDA(cudaMemsetAsync(L.exact_count, 0, sizeof(unsigned), c->stream));
     NRM_CUDA(launch_emdq_field(L, c->stream, &c->launches));
     return NRM_OK;
 }
