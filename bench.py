@@ -590,6 +590,10 @@ def main():
                    "share_of_step": tot_ms / max(sum(v[0] for v in kt.values()), 1e-9)}
             if name in insts and per > 0:
                 ent["issue_frac"] = insts[name] / (per * 1e-3 * nsm * 4 * clk_hz)
+            if name in traffic and per > 0 and peaks.get("hbm_gbs"):
+                # every kernel's HBM view: ncu DRAM bytes per launch over its live launch time
+                gbs = traffic[name] / (per * 1e-3) / 1e9
+                ent.update({"hbm_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"]})
             if name in algo:
                 # total algorithmic flops over total kernel time (= per launch when a
                 # step's work is split into equal launch chunks)
