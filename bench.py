@@ -571,12 +571,22 @@ def main():
         peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
         fp32_peak = 2.0 * ctx.peak("fp32") / 1e12   # measured FFMA lane-ops/s -> TFLOP/s (FMA = 2 flops)
         contrib = wl_contributors(wl, polys[0])
-        # algorithmic FP32 flops per unit:
+        # algorithmic FP64-reference flops per unit (DESIGN.md §7 "Algorithmic work"),
+        # counted on the reference's code, not the kernels':
         #   K1 per contributing (pixel, node) pair (w > 1e-6, mosaic.hpp:249-262):
         #      d2 5 + exponent 1 + exp 1 + 5 weighted sums x 2 + wsum 1 = 18
-        #   K3 per pixel: 16 blend members x (distance 5 + exp 1 + prob 1 + 5 sums x 2 + wsum 1) = 288
-        # per profiled step: K1 blends nfr frames, K3 computes one field
-        algo = {"k_node_field": contrib["pairs"] * 18.0 * nfr, "k_pixels": fw * fh * 16 * 18.0}
+        #   K1 per blended pixel (mosaic.hpp:267-282): mean 5 div + normalize 8
+        #      (hypot 4, 4 div; dualquat.hpp:45-51) + apply 23 (dualquat.hpp:75-80,
+        #      x scale) + bilinear 38 (image.hpp:81-90) + running average 15 = 89
+        #   K3 per pixel: 16 blend members x (distance 5 + exp 1 + prob 1 + 5 sums
+        #      x 2 + wsum 1) = 288, plus dq_blend's normalise 13 + apply 23 +
+        #      displacement 2 + bounded_exp(beta d2min) 2 = 40 (fieldest.hpp:75-97,
+        #      dualquat.hpp:133-162)
+        # per profiled step and rank: K1 blends this rank's bands (1/world of the
+        # rows) of nfr = world frames, K3 computes one field
+        blended = float(sum(int(st[k][1]) for k in range(len(st))))
+        algo = {"k_node_field": (contrib["pairs"] * 18.0 * nfr + blended * 89.0) / world,
+                "k_pixels": fw * fh * (16 * 18.0 + 40.0)}
         traffic = load_traffic()
         # issue-rate view: ncu warp instructions per launch over the live launch
         # time against the scheduler peak (SMs x 4 issue slots x SM clock)
@@ -610,8 +620,11 @@ def main():
             roof = {"kernel": name, "bound": "fp32", "achieved": None, "peak": fp32_peak, "unit": "TFLOP/s",
                     "frac": None, "traffic": traffic.get(name)}
         roof["algorithmic"] = {"k_node_field": f"{contrib['pairs']:.4g} contributing pixel-node pairs "
-                                               f"({contrib['per_px']:.1f}/px) x 18 flops",
-                               "k_pixels": f"{fw * fh} px x 16 members x 18 flops"}
+                                               f"({contrib['per_px']:.1f}/px) x 18 flops + {blended:.4g} blended "
+                                               f"px x 89 flops (the reference's per-pixel epilogue)",
+                               "k_pixels": f"{fw * fh} px x (16 members x 18 + 40 epilogue) flops",
+                               "definition": "flops of the reference's FP64 code per unit (DESIGN.md §7), "
+                                             "against the FP32 peak"}
         # HBM view of the fused update: 29 B per footprint pixel (canvas r+w 26 B + frame 3 B)
         kb = kt.get("k_node_field", (0.0, 1))
         fp_px = int(st[0][0])
