@@ -22,17 +22,20 @@
 //     their warps conjugated to the tile origin (T(-P) q T(o)); the ambiguous
 //     are then re-classified per 8 x 4 sub-tile (FP32, conservative margins),
 //     leaving ~2 free slots per pixel. Plans go to HBM (L2-resident).
-//   k_pixels (one CTA per tile, warp = sub-tile, one pixel per thread): one
-//     pass over the sure members accumulating weighted warps (weights on
-//     MUFU.EX2 relative to a tile-wide d^2 floor: the common factor cancels in
-//     dq_blend's normalisation), an early-reject sorted insertion of the
-//     ambiguous (closest first) into the m = S - |in| free slots, their
-//     accumulation and the epilogue. When the selected and rejected boundary
-//     keys are within the FP32 error bound, the pixel re-runs in the exact
-//     tier (FP64, reference operation order and libm: the kNN set and blend
-//     are bit-identical to the reference's).
+//   k_pixels (one CTA per tile, plan staged by one TMA bulk copy, warp =
+//     sub-tile, one pixel per thread): one pass over the sure members
+//     accumulating weighted warps (weights on MUFU.EX2 relative to a
+//     tile-wide d^2 floor: the common factor cancels in dq_blend's
+//     normalisation), an early-reject sorted insertion of the ambiguous
+//     (closest first) into the m = S - |in| free slots, their accumulation and
+//     the epilogue. When the selected and rejected boundary keys are within
+//     the FP32 error bound, the pixel is queued for the exact tier.
+//   k_emdq_exceptions (after each chunk's k_pixels): the queued pixels, a
+//     warp per pixel, in the exact tier (FP64, reference operation order and
+//     libm: the kNN set and blend are bit-identical to the reference's).
 //   Tiles whose candidates span more than a quarter turn of rotation
-//   (hemisphere flips possible) or overflow a capacity run in the exact tier.
+//   (hemisphere flips possible) or overflow a capacity run the exact tier in
+//   k_pixels, a thread per pixel.
 #include <algorithm>
 #include <cfloat>
 #include <climits>
@@ -497,11 +500,6 @@ __device__ void emdq_exact(double qx, double qy, const int* __restrict__ idx, in
 template <int MAXS>
 __device__ __noinline__ void exact_dispatch(double qx, double qy, const int* idx, int n, int S, const Cand C,
                                             double alpha, double beta, float2* od, float* ou) {
-#ifdef NRM_DEV_SKIP_EXACT  // development timing only: wrong results for exact-tier pixels
-    if (od) *od = make_float2(0.f, 0.f);
-    if (ou) *ou = 1.f;
-    return;
-#endif
     if (S <= 16 || MAXS <= 16)
         emdq_exact<16>(qx, qy, idx, n, S, C, alpha, beta, od, ou);
     else
@@ -1109,41 +1107,41 @@ __device__ __forceinline__ void pixels_tile(const EmdqLaunch& L, const Cand& C, 
             }
             if (valid && !queue_exact) {
                 const double qx = L.grid.gx + pi, qy = L.grid.gy + pj;
-            const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
-            const float qw = fo.s0 * rn, qz = fo.s1 * rn, qdx = fo.s2 * rn, qdy = fo.s3 * rn;
-            const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
-            const float ux = (float)lx, uy = (float)ly;
-            const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
-            const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
-            const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
-            // displacement y - q = (Y0 - tile origin - u) + (e0 + dl P + (s0 + dl) Q(u)):
-            // the first part is a small per-tile constant (bd, FP64 -> FP32), the
-            // second stays ~1e2 px, so FP32 keeps it to ~1e-5 px at any coordinate
-            // (the K1/K2 epilogue; error model: k_nodefield.cu kScaleLever)
-            if (od) {
-                const float sbf = (float)h.s0 + dlb;
-                const float rx = fmaf(sbf, Qx, fmaf(dlb, (float)h.P[0], (float)h.e0[0]));
-                const float ry = fmaf(sbf, Qy, fmaf(dlb, (float)h.P[1], (float)h.e0[1]));
-                const float bdx = (float)(h.Y0[0] - (L.grid.gx + ti0)), bdy = (float)(h.Y0[1] - (L.grid.gy + tj0));
-                *od = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
-            }
-            if (ou) {
-                // bounded_exp(beta d2min) (fieldest.hpp:44-52) to FP32 output
-                // precision: d2min in FP64 over the points that can be the nearest in
-                // this sub-tile; exp(x) = 2^n 2^f, n = rint(x log2 e), |f| <= 1/2 in
-                // FP64, 2^f on MUFU.EX2 (relative error < 3e-7, inside the 1e-6 bar)
-                double d2m = DBL_MAX;
-                const int nl = nnear == 255 ? ne : nnear;
-                for (int e = 0; e < nl; ++e) {
-                    const int k = nnear == 255 ? e : sp.near[wid][e];
-                    const double2 a = sp.axy[k];
-                    const double dx = qx - a.x, dy = qy - a.y;
-                    d2m = fmin(d2m, fma(dx, dx, dy * dy));
+                const float rn = rsqrtf(fmaf(fo.s0, fo.s0, fo.s1 * fo.s1));
+                const float qw = fo.s0 * rn, qz = fo.s1 * rn, qdx = fo.s2 * rn, qdy = fo.s3 * rn;
+                const float cc = qw * qw - qz * qz, ss = 2.f * qw * qz;
+                const float ux = (float)lx, uy = (float)ly;
+                const float Qx = cc * ux - ss * uy + 2.f * (qdx * qw - qdy * qz);
+                const float Qy = ss * ux + cc * uy + 2.f * (qdx * qz + qdy * qw);
+                const float dlb = __fdividef(fo.s4, fo.s5);  // s5 > 0 (checked above)
+                // displacement y - q = (Y0 - tile origin - u) + (e0 + dl P + (s0 + dl) Q(u)):
+                // the first part is a small per-tile constant (bd, FP64 -> FP32), the
+                // second stays ~1e2 px, so FP32 keeps it to ~1e-5 px at any coordinate
+                // (the K1/K2 epilogue; error model: k_nodefield.cu kScaleLever)
+                if (od) {
+                    const float sbf = (float)h.s0 + dlb;
+                    const float rx = fmaf(sbf, Qx, fmaf(dlb, (float)h.P[0], (float)h.e0[0]));
+                    const float ry = fmaf(sbf, Qy, fmaf(dlb, (float)h.P[1], (float)h.e0[1]));
+                    const float bdx = (float)(h.Y0[0] - (L.grid.gx + ti0)), bdy = (float)(h.Y0[1] - (L.grid.gy + tj0));
+                    *od = make_float2((bdx - ux) + rx, (bdy - uy) + ry);
                 }
-                const double tx = fmin(L.beta * d2m, 55.0) * 1.4426950408889634;
-                const double n = rint(tx);
-                *ou = ex2_approx((float)(tx - n)) * __int_as_float(((int)n + 127) << 23);
-            }
+                if (ou) {
+                    // bounded_exp(beta d2min) (fieldest.hpp:44-52) to FP32 output
+                    // precision: d2min in FP64 over the points that can be the nearest in
+                    // this sub-tile; exp(x) = 2^n 2^f, n = rint(x log2 e), |f| <= 1/2 in
+                    // FP64, 2^f on MUFU.EX2 (relative error < 3e-7, inside the 1e-6 bar)
+                    double d2m = DBL_MAX;
+                    const int nl = nnear == 255 ? ne : nnear;
+                    for (int e = 0; e < nl; ++e) {
+                        const int k = nnear == 255 ? e : sp.near[wid][e];
+                        const double2 a = sp.axy[k];
+                        const double dx = qx - a.x, dy = qy - a.y;
+                        d2m = fmin(d2m, fma(dx, dx, dy * dy));
+                    }
+                    const double tx = fmin(L.beta * d2m, 55.0) * 1.4426950408889634;
+                    const double n = rint(tx);
+                    *ou = ex2_approx((float)(tx - n)) * __int_as_float(((int)n + 127) << 23);
+                }
             }
         }
     }
@@ -1184,9 +1182,10 @@ k_pixels(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int S) {
 // k_emdq_exceptions: the dense field's exact-tier pixels (queued by
 // k_pixels), one warp per pixel, bit-identical to emdq_exact / the
 // reference's blend_local + node_uncertainty (fieldest.hpp:44-52, 75-97):
-//   * the S nearest by (d^2, j) over the pixel's supertile list: S rounds of
-//     a warp-wide minimum over the keys above the previous round's (lanes
-//     scan strided candidates, FP64 d^2 as xdist2);
+//   * the S nearest by (d^2, j) over the tile's staged list (the tile plan
+//     of this launch chunk, at most 64 candidates): each candidate's rank
+//     among all of them in one pass over the warp's keys in shared memory
+//     (FP64 d^2 as xdist2);
 //   * lane s holds member s: its weight exp(-alpha (d^2 - d2min)) prob in
 //     parallel (glibc-exact exp), then the reference's ordered sums (wsum,
 //     then the hemisphere-aligned weighted warps) as a shuffle chain;
