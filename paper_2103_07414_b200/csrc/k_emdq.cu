@@ -146,6 +146,10 @@ struct SSmem {
     float R;
 };
 constexpr int SUPER_CC_CAP = 8192;  // candidates whose coarse coordinates k_super caches in shared memory
+#ifndef NRM_SUPER_FUSED_GATHER_MAX
+#define NRM_SUPER_FUSED_GATHER_MAX 2048
+#endif
+constexpr int SUPER_FUSED_GATHER_MAX = NRM_SUPER_FUSED_GATHER_MAX;  // above: a separate k_gather first
 
 __global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
                          const double* __restrict__ probs, const int32_t* __restrict__ active,
@@ -224,14 +228,18 @@ struct GatherOut {
 // Also gathers the active candidates (grid-stride; k_gather's former job) for
 // the later kernels. Its own reads go through `active` directly, since other
 // CTAs are writing the gathered arrays concurrently; the values are the same.
-__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperLists SL, int S, float pad) {
+// gathered: the candidates were gathered by k_gather before this grid (large
+// candidate sets): every CTA then reads the contiguous coarse coordinates
+// G.c32 instead of the active -> apts chain of dependent loads.
+__global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperLists SL, int S, float pad,
+                                              int gathered) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     // this call's count of exact-tier pixels (k_pixels adds to it)
     if (L.exact_count && t == 0 && blockIdx.x == 0 && blockIdx.y == 0) *L.exact_count = 0u;
-    {
+    if (!gathered) {
         const int nb = gridDim.x * gridDim.y;
         for (int a = (blockIdx.y * gridDim.x + blockIdx.x) * ENT + t; a < L.nactive; a += nb * ENT) {
             const int j = L.active[a];
@@ -253,6 +261,7 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     float2* cc = N <= SUPER_CC_CAP ? reinterpret_cast<float2*>(smem_raw + ((sizeof(SSmem) + 15) & ~size_t(15)))
                                    : nullptr;
     auto coarse_g = [&](int a) {
+        if (gathered) return G.c32[a];
         const int j = L.active[a];
         return make_float2((float)L.apts[2 * j], (float)L.apts[2 * j + 1]);
     };
@@ -1496,7 +1505,19 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     prof_mark("k_super", st);
     // programmatic launch: its CTAs become resident while the stream's previous
     // kernel drains and wait in pdl_wait() before touching any scratch
-    cudaError_t e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, LQ, G, SL, S, 0.f);
+    // small candidate sets: the gather is fused into k_super (one launch less
+    // on the critical chain); large ones: k_gather first, so that every
+    // supertile CTA reads the contiguous coarse coordinates
+    const int gathered = L.nactive > SUPER_FUSED_GATHER_MAX ? 1 : 0;
+    if (gathered) {
+        prof_mark("k_gather", st);
+        k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
+                                                           c32, L.cl, L.cp, phi, cj);
+        ++*launches;
+        cudaError_t eg = cudaGetLastError();
+        if (eg != cudaSuccess) return eg;
+    }
+    cudaError_t e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, LQ, G, SL, S, 0.f, gathered);
     ++*launches;
     if (e != cudaSuccess) return e;
     const int ntx = (L.grid.i1 - L.grid.i0 + ET) / ET;
@@ -1581,7 +1602,7 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
                            (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
         cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         prof_mark("k_super", st);
-        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, Ssup, 3.f);
+        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, Ssup, 3.f, 0);
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
