@@ -6,6 +6,7 @@
 
 #include "nrm_common.cuh"
 #include "nrm_internal.h"
+#include "frame_rgba.cuh"
 
 namespace nrm {
 namespace {
@@ -357,6 +358,29 @@ __global__ void k_deform_commit(CanvasView v, float* r, float* g, float* b, uint
 }
 
 }  // namespace
+
+__global__ void __launch_bounds__(RGBA_THREADS) k_frame_rgba(FrameSet fs, int fw, int fh, int fch,
+                                                             uint8_t* __restrict__ out, size_t pitch,
+                                                             size_t slot_bytes) {
+    const int fr = blockIdx.y;
+    const uint8_t* base = fs.f[0];  // a select, not a dynamic index (that would copy the parameters to local memory)
+#pragma unroll
+    for (int k = 1; k < kFrameSlots; ++k)
+        if (fr == k) base = fs.f[k];
+    rgba_convert(base, out + slot_bytes * fr, fw, fh, fch, pitch, blockIdx.x, gridDim.x);
+}
+
+cudaError_t launch_frame_rgba(const FrameSet& fs, int nf, int fw, int fh, int fch, uint8_t* out, size_t pitch,
+                              size_t slot_bytes, cudaStream_t st, int64_t* launches) {
+    if (nf <= 0 || nf > kFrameSlots) return cudaErrorInvalidValue;
+    prof_mark("k_frame_rgba", st);
+    const long long total = (long long)((fw + 3) / 4) * fh;
+    const int blocks = (int)std::max(1LL, std::min((total + RGBA_THREADS * RGBA_GROUPS - 1) / (RGBA_THREADS * RGBA_GROUPS),
+                                                   (long long)148 * 8));
+    k_frame_rgba<<<dim3(blocks, nf), RGBA_THREADS, 0, st>>>(fs, fw, fh, fch, out, pitch, slot_bytes);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t canvas_alt_planes(nrm_canvas* cv, cudaStream_t st) {
     if (cv->ar) return cudaSuccess;

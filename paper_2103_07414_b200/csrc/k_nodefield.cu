@@ -28,6 +28,7 @@
 
 #include "nrm_common.cuh"
 #include "nrm_internal.h"
+#include "frame_rgba.cuh"
 
 namespace nrm {
 namespace {
@@ -244,11 +245,22 @@ __device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* _
 // The planner reads only the nodes, so it may run while the previous blend's
 // exact pass finishes (programmatic dependent launch); it waits for that
 // predecessor before exiting, which keeps the canvas order for the next
-// kernel (k_node_field waits for the planner).
+// kernel (k_node_field waits for the planner). The last `conv` CTAs convert
+// the frame for the texture: the previous blend's k_node_field, the only
+// reader of those rows, has exited before this launch can start (its exact
+// pass, the PDL primary here, starts only after all its CTAs exit).
+constexpr int NF_CONV_BLOCKS = 2 * 148;
 __global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
 k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
-          int rows, int ntx) {
+          int rows, int ntx, int conv) {
+    static_assert(NF_PLAN_WARPS * 32 == RGBA_THREADS, "conversion CTA shape");
     __shared__ unsigned list_s[NF_PLAN_WARPS][NF_CAP];
+    const int nplan = gridDim.x - conv;
+    if ((int)blockIdx.x >= nplan) {
+        rgba_convert(L.frame, L.frgba, L.fw, L.fh, L.fch, L.frgba_pitch, blockIdx.x - nplan, conv);
+        pdl_wait();
+        return;
+    }
     nf_plan_tile(L, plans, blockIdx.x * NF_PLAN_WARPS + (threadIdx.x >> 5), tile_i0, tile_j0, tile_j_last, s1, by0,
                  rows, ntx, list_s);
     pdl_wait();
@@ -705,18 +717,32 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
                         const float fx = rx - (float)(x0 - Y0x), fy = ry - (float)(y0 - Y0y);
                         const int x1 = min(x0 + 1, L.fw - 1), y1 = min(y0 + 1, L.fh - 1);
                         const unsigned row0 = (unsigned)y0 * (unsigned)L.fw, row1 = (unsigned)y1 * (unsigned)L.fw;
-                        float va[3], vb[3], vc[3], vd[3];
-                        texel_u32(L.frame, row0 + x0, L.fch, va);
-                        texel_u32(L.frame, row0 + x1, L.fch, vb);
-                        texel_u32(L.frame, row1 + x0, L.fch, vc);
-                        texel_u32(L.frame, row1 + x1, L.fch, vd);
                         const float gx = 1.f - fx, gy = 1.f - fy;
-                        const float vr = (gx * va[0] + fx * vb[0]) * gy + (gx * vc[0] + fx * vd[0]) * fy;
-                        const float vg = (gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy;
-                        const float vbl = (gx * va[2] + fx * vb[2]) * gy + (gx * vc[2] + fx * vd[2]) * fy;
+                        float vr, vg, vbl;  // bilinear sample / 255
+                        if (L.ftex) {
+                            // three 2 x 2 gathers of the RGBA8 texture, already / 255:
+                            // .w (x0, y0), .z (x1, y0), .x (x0, y1), .y (x1, y1); the
+                            // clamped address mode gives x1 = min(x0 + 1, fw - 1) likewise
+                            const float tx = (float)x0 + 1.f, ty = (float)y0 + 1.f;
+                            const float4 cr = tex2Dgather<float4>((cudaTextureObject_t)L.ftex, tx, ty, 0);
+                            const float4 cg = tex2Dgather<float4>((cudaTextureObject_t)L.ftex, tx, ty, 1);
+                            const float4 cb = tex2Dgather<float4>((cudaTextureObject_t)L.ftex, tx, ty, 2);
+                            vr = (gx * cr.w + fx * cr.z) * gy + (gx * cr.x + fx * cr.y) * fy;
+                            vg = (gx * cg.w + fx * cg.z) * gy + (gx * cg.x + fx * cg.y) * fy;
+                            vbl = (gx * cb.w + fx * cb.z) * gy + (gx * cb.x + fx * cb.y) * fy;
+                        } else {
+                            float va[3], vb[3], vc[3], vd[3];
+                            texel_u32(L.frame, row0 + x0, L.fch, va);
+                            texel_u32(L.frame, row0 + x1, L.fch, vb);
+                            texel_u32(L.frame, row1 + x0, L.fch, vc);
+                            texel_u32(L.frame, row1 + x1, L.fch, vd);
+                            constexpr float k255 = 1.f / 255.f;
+                            vr = ((gx * va[0] + fx * vb[0]) * gy + (gx * vc[0] + fx * vd[0]) * fy) * k255;
+                            vg = ((gx * va[1] + fx * vb[1]) * gy + (gx * vc[1] + fx * vd[1]) * fy) * k255;
+                            vbl = ((gx * va[2] + fx * vb[2]) * gy + (gx * vc[2] + fx * vd[2]) * fy) * k255;
+                        }
                         const uint8_t wg = ct.w[r][hcol];
                         const float wd = (float)wg, inv = __fdividef(1.f, wd + 1.f);
-                        constexpr float k255 = 1.f / 255.f;
                         const long long idx = (long long)(jj - L.phys_y0) * L.pitch + (i - L.phys_x0);
                         // reference rule: (w c + v) / (w + 1); weighted mode:
                         // ((w + 1 - cf) c + cf v) / (w + 1), identical for cf == 1
@@ -730,9 +756,9 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
                         }
                         // explicit FMAs: the same instructions in both modes, so
                         // cf == 1 reproduces the reference rule bit for bit
-                        L.R[idx] = fmaf(a, ct.r[r][hcol], cf * (vr * k255)) * inv;
-                        L.G[idx] = fmaf(a, ct.g[r][hcol], cf * (vg * k255)) * inv;
-                        L.B[idx] = fmaf(a, ct.b[r][hcol], cf * (vbl * k255)) * inv;
+                        L.R[idx] = fmaf(a, ct.r[r][hcol], cf * vr) * inv;
+                        L.G[idx] = fmaf(a, ct.g[r][hcol], cf * vg) * inv;
+                        L.B[idx] = fmaf(a, ct.b[r][hcol], cf * vbl) * inv;
                         L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
                         ++nb;
                     }
@@ -1542,9 +1568,10 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         const int rows = min(g.chunk_rows, g.nty - by0);
         if ((size_t)rows * g.ntx > (size_t)NF_CHUNK_TILES) return cudaErrorInvalidValue;  // ntx > chunk
         prof_mark("k_nf_plan", st);
-        cudaError_t e = launch_pdl(k_nf_plan, dim3((rows * g.ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS),
+        const int conv = (ci == 0 && L.frgba) ? NF_CONV_BLOCKS : 0;
+        cudaError_t e = launch_pdl(k_nf_plan, dim3((rows * g.ntx + NF_PLAN_WARPS - 1) / NF_PLAN_WARPS + conv),
                                    dim3(NF_PLAN_WARPS * 32), 0, st, L, plans, g.ti0, g.tj0, g.tj1, g.s1, by0, rows,
-                                   g.ntx);
+                                   g.ntx, conv);
         ++*launches;
         if (e != cudaSuccess) return e;
         prof_mark("k_node_field", st);

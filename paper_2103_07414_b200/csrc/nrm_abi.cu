@@ -320,6 +320,64 @@ size_t exception_capacity(const nrm_ctx* c, size_t pixels) {
     return std::max<size_t>(1, std::min<size_t>({cap, pixels, (size_t)0x7fffffff}));
 }
 
+// K1's frame textures: frames converted to RGBA8 rows (pitch a multiple of
+// 128 B), frame k into slot k of the context's frame_rgba buffer, and a
+// texture object per slot (point sampling, clamped addresses, normalised
+// reads), rebuilt only when a slot's storage or the frame shape changes. A
+// batch converts in one k_frame_rgba launch; a single frame (`fused`) hands
+// the conversion to its planner launch (NodeFieldLaunch::frgba).
+int frame_textures(nrm_ctx* c, int nf, const uint8_t* const* d_frames, int fw, int fh, int ch,
+                   NodeFieldLaunch* const* Ls, bool fused) {
+    if (nf <= 0 || nf > kFrameSlots) return fail(NRM_EINVAL, "frame texture count out of range");
+    const size_t pitch = ((size_t)fw * 4 + 127) & ~size_t(127), bytes = pitch * (size_t)fh;
+    if (c->frame_rgba.cap < bytes * (size_t)nf) {
+        NRM_CUDA(cudaStreamSynchronize(c->stream));  // the old storage may still be sampled
+        NRM_CUDA(c->frame_rgba.ensure(bytes * (size_t)nf));
+    }
+    if (fused) {
+        if (nf != 1) return fail(NRM_EINVAL, "fused frame conversion takes one frame");
+        Ls[0]->frgba = c->frame_rgba.as<uint8_t>();
+        Ls[0]->frgba_pitch = pitch;
+    } else {
+        FrameSet fs = {};
+        for (int k = 0; k < nf; ++k) fs.f[k] = d_frames[k];
+        NRM_CUDA(launch_frame_rgba(fs, nf, fw, fh, ch, c->frame_rgba.as<uint8_t>(), pitch, bytes, c->stream,
+                                   &c->launches));
+    }
+    for (int k = 0; k < nf; ++k) {
+        uint8_t* dst = c->frame_rgba.as<uint8_t>() + bytes * (size_t)k;
+        if (!c->ftex[k] || c->ftex_ptr[k] != dst || c->ftex_w[k] != fw || c->ftex_h[k] != fh ||
+            c->ftex_pitch[k] != pitch) {
+            if (c->ftex[k]) {
+                NRM_CUDA(cudaStreamSynchronize(c->stream));  // no launch may still use the old object
+                cudaDestroyTextureObject((cudaTextureObject_t)c->ftex[k]);
+                c->ftex[k] = 0;
+            }
+            cudaResourceDesc rd = {};
+            rd.resType = cudaResourceTypePitch2D;
+            rd.res.pitch2D.devPtr = dst;
+            rd.res.pitch2D.desc = cudaCreateChannelDesc<uchar4>();
+            rd.res.pitch2D.width = (size_t)fw;
+            rd.res.pitch2D.height = (size_t)fh;
+            rd.res.pitch2D.pitchInBytes = pitch;
+            cudaTextureDesc td = {};
+            td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+            td.filterMode = cudaFilterModePoint;
+            td.readMode = cudaReadModeNormalizedFloat;
+            td.normalizedCoords = 0;
+            cudaTextureObject_t t = 0;
+            NRM_CUDA(cudaCreateTextureObject(&t, &rd, &td, nullptr));
+            c->ftex[k] = (unsigned long long)t;
+            c->ftex_ptr[k] = dst;
+            c->ftex_w[k] = fw;
+            c->ftex_h[k] = fh;
+            c->ftex_pitch[k] = pitch;
+        }
+        Ls[k]->ftex = c->ftex[k];
+    }
+    return NRM_OK;
+}
+
 // Shared core of blend_frame: everything after the inputs are in HBM.
 // d_stats: int64[4] on the device, written by the exception pass.
 int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, const double* d_anchors,
@@ -383,6 +441,10 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.exc_done = st.exc_done;
     NRM_CUDA(c->tiles.ensure(node_field_scratch_bytes(L)));
     L.plans = c->tiles.p;
+    if (ch == 3 || ch == 4) {
+        NodeFieldLaunch* lp = &L;
+        NRM_CHECK(frame_textures(c, 1, &d_frame, fw, fh, ch, &lp, true));
+    }
     NRM_CUDA(launch_node_field(L, 0, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -597,9 +659,11 @@ int nrm_ctx_destroy(nrm_ctx* c) {
     if (!c) return NRM_OK;
     DeviceGuard g(c->device);
     cudaStreamSynchronize(c->stream);
+    for (unsigned long long t : c->ftex)
+        if (t) cudaDestroyTextureObject((cudaTextureObject_t)t);
     DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc,   &c->misc,  &c->stats, &c->pts,
                       &c->locals,    &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles, &c->feat,
-                      &c->feat_io,   &c->batch,  &c->halo};
+                      &c->feat_io,   &c->batch,  &c->halo,   &c->frame_rgba};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();
@@ -1038,6 +1102,15 @@ int nrm_blend_frames_device(nrm_canvas* cv, int nf, const uint8_t* const* d_fram
         L.exc_last = st.last_exc;
         L.exc_done = st.exc_done;
         qoff += cap[a];
+    }
+    if (ch == 3 || ch == 4) {  // one conversion launch for every active frame
+        std::vector<const uint8_t*> fr(nact);
+        std::vector<NodeFieldLaunch*> lp(nact);
+        for (size_t a = 0; a < nact; ++a) {
+            fr[a] = d_frames[act[a]];
+            lp[a] = &Ls[a];
+        }
+        NRM_CHECK(frame_textures(c, (int)nact, fr.data(), fw, fh, ch, lp.data(), false));
     }
     NRM_CUDA(c->tiles.ensure(node_field_batch_scratch_bytes((int)nact)));
     const cudaError_t e = launch_node_field_batch(Ls.data(), (int)nact, c->tiles.p, c->stream, &c->launches);

@@ -40,6 +40,8 @@ struct Prof {
     size_t used = 0;
 };
 
+constexpr int kFrameSlots = 16;  // frames of a batched blend (nrm_blend_frames_device)
+
 // Records a timing mark for the context of the current API call (no-op
 // unless that context has profiling enabled).
 void prof_mark(const char* name, cudaStream_t st);
@@ -55,7 +57,14 @@ struct nrm_ctx {
     int64_t exc_cap_override = 0;  // nrm_ctx_set_exception_capacity (tests); 0 = default sizing
     // scratch (grow-only)
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
-        active, out_a, out_b, tiles, feat, feat_io, batch, halo;
+        active, out_a, out_b, tiles, feat, feat_io, batch, halo,
+        frame_rgba;  // K1: RGBA8 copies of the blended frames (texture storage, one slot per frame)
+    // texture objects over the frame_rgba slots, rebuilt when a slot's storage
+    // or the frame shape changes
+    unsigned long long ftex[nrm::kFrameSlots] = {};
+    const void* ftex_ptr[nrm::kFrameSlots] = {};
+    int ftex_w[nrm::kFrameSlots] = {}, ftex_h[nrm::kFrameSlots] = {};
+    size_t ftex_pitch[nrm::kFrameSlots] = {};
     nrm::PinnedBuf staging, staging_out;
     nrm::Prof prof;
 };
@@ -108,6 +117,14 @@ struct NodeFieldLaunch {
     // inputs
     const uint8_t* frame = nullptr;  // ImageU8 layout: h x w x fch, fch in {1, 3, 4}
     int fw = 0, fh = 0, fch = 3;
+    // the same frame as an RGBA8 texture (normalised reads; 0: none): the fast
+    // tier's bilinear sample is three 2 x 2 gathers (tex2Dgather) instead of
+    // twelve byte loads and conversions
+    unsigned long long ftex = 0;
+    // when set, the first k_nf_plan launch appends conversion CTAs that write
+    // the frame's RGBA8 rows (pitch frgba_pitch) the texture reads
+    uint8_t* frgba = nullptr;
+    size_t frgba_pitch = 0;
     // optional (extension): frame-aligned per-pixel
     // uncertainty (fw x fh, node_uncertainty >= 1); the blend's update step is
     // scaled by the confidence 1 / max(u, 1) sampled bilinearly at the frame
@@ -156,6 +173,13 @@ size_t node_field_scratch_bytes(const NodeFieldLaunch& L);
 
 // mode 0 = blend into canvas, 1 = node field (disp/support)
 cudaError_t launch_node_field(const NodeFieldLaunch& L, int mode, cudaStream_t st, int64_t* launches);
+// ImageU8 frames (fch 3 or 4) -> RGBA8 rows of `pitch` bytes, frame k into
+// out + k * slot_bytes (K1's frame textures); one launch for all frames.
+struct FrameSet {
+    const uint8_t* f[kFrameSlots];
+};
+cudaError_t launch_frame_rgba(const FrameSet& fs, int nf, int fw, int fh, int fch, uint8_t* out, size_t pitch,
+                              size_t slot_bytes, cudaStream_t st, int64_t* launches);
 // Blends of several frames whose footprints are pairwise disjoint, in one
 // planner / field / exception launch each (reference rule, frame lattices of
 // fewer than 257 nodes, all tiles in one plan chunk; otherwise

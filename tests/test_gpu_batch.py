@@ -65,7 +65,7 @@ def test_batch_takes_one_launch_per_stage(nrm, ctx):
     n0 = ctx.launch_count()
     nrm.blend_frames_device(cv, [fr] * 8, wl.frame_w, wl.frame_h, 3, anc, war, wl.params.alpha, polys, st)
     ctx.synchronize()
-    assert ctx.launch_count() - n0 == 3  # planner, field, exception pass for all 8 frames
+    assert ctx.launch_count() - n0 == 4  # frame textures, planner, field, exception pass for all 8 frames
     assert (st[:, 1] > 0).all()
 
 
