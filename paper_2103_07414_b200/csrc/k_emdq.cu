@@ -780,35 +780,22 @@ k_plan(EmdqLaunch L, Cand C, SuperLists SL, TilePlans TP, int ntiles, int S) {
                         sb[u] = take_min ? fminf(sb[u], pb) : fmaxf(sb[u], pb);
                     }
                 }
-            // cle = #{l : dmin_l <= hi_k} - 1 (k itself), clt = #{l : dmax_l < lo_k}
-            float hi[NP], lo[NP];
-            int pa[NP], pb[NP];
-#pragma unroll
-            for (int u = 0; u < NP; ++u) {
-                hi[u] = dmx[u] * (1.f + 1e-5f) + 1e-2f;
-                lo[u] = dmn[u] * (1.f - 1e-5f) - 1e-2f;
-                pa[u] = pb[u] = 0;
-            }
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1)
-#pragma unroll
-                for (int u = 0; u < NP; ++u) {
-                    const float va = __shfl_sync(0xffffffffu, sa[u], pa[u] + step - 1);
-                    const float vb = __shfl_sync(0xffffffffu, sb[u], pb[u] + step - 1);
-                    if (va <= hi[u]) pa[u] += step;
-                    if (vb < lo[u]) pb[u] += step;
-                }
+            // The classes only compare the counts with S: cle = #{l : dmin_l <= hi_k} - 1 < S
+            // <=> hi_k < the (S+1)-th smallest dmin (lane S of the sorted copy; none when
+            // S >= 32), and clt = #{l : dmax_l < lo_k} >= S <=> the S-th smallest dmax
+            // (lane S - 1) < lo_k: the same classes as counting, from two broadcasts.
 #pragma unroll
             for (int u = 0; u < NP; ++u) {
                 const int st = st0 + u;
-                const float la = __shfl_sync(0xffffffffu, sa[u], 31), lb = __shfl_sync(0xffffffffu, sb[u], 31);
-                if (pa[u] == 31 && la <= hi[u]) pa[u] = 32;
-                if (pb[u] == 31 && lb < lo[u]) pb[u] = 32;
+                const float hi = dmx[u] * (1.f + 1e-5f) + 1e-2f, lo = dmn[u] * (1.f - 1e-5f) - 1e-2f;
+                const float tin = __shfl_sync(0xffffffffu, sa[u], S < 32 ? S : 31);
+                const float tout = __shfl_sync(0xffffffffu, sb[u], S - 1);
+                const bool in = S >= 32 || hi < tin;
                 // points that can be the nearest somewhere in the sub-tile
                 const float thr = __shfl_sync(0xffffffffu, sb[u], 0) * (1.f + 1e-5f) + 1e-2f;
                 const unsigned mn = __ballot_sync(0xffffffffu, dmn[u] <= thr);
                 int c = 0;
-                if (lane >= ni && lane < ne) c = pa[u] - 1 < S ? 1 : (pb[u] >= S ? 0 : 2);
+                if (lane >= ni && lane < ne) c = in ? 1 : (tout >= lo ? 2 : 0);
                 const unsigned mi = __ballot_sync(0xffffffffu, c == 1), ma = __ballot_sync(0xffffffffu, c == 2);
                 int nx = 255, nw = 0, nn = 0;
                 if (ok[u]) {  // warp-uniform
