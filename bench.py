@@ -299,7 +299,8 @@ def main():
     ctx = M.Context(local)
     # explicit stream: kernels and events share it. K3 (the longer dependency
     # chain) gets the higher priority so K1 fills the SMs it leaves idle.
-    stream = torch.cuda.Stream(dev, priority=-1 if env_int("NRM_BENCH_PRIO", 1) else 0)
+    prio = env_int("NRM_BENCH_PRIO", 1)  # 1: K3 stream high, 2: K1 stream high, 0: equal
+    stream = torch.cuda.Stream(dev, priority=-1 if prio == 1 else 0)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
 
@@ -329,7 +330,7 @@ def main():
     rect = (x_lo, wl.canvas_rect[1], wl.canvas_rect[2] + shift[-1], wl.canvas_rect[3])
 
     # K1 (canvas) runs on its own context/stream so it overlaps K3 (independent work)
-    stream_b = torch.cuda.Stream(dev)
+    stream_b = torch.cuda.Stream(dev, priority=-1 if prio == 2 else 0)
     ctx_b = M.Context(local)
     ctx_b.set_stream(stream_b.cuda_stream)
     cv = M.Canvas(ctx_b if args.overlap else ctx)
