@@ -1198,6 +1198,18 @@ __device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, int2 p, doubl
     int nsrc;
     const int tix = floordiv(p.x, TW) - floordiv(L.grid.i0, TW);
     const int* src = chunk_nodes(L, by / L.chunk_rows, tix / NF_GROUP_TILES, &nsrc);
+    // blend modes: the pixel's canvas values do not depend on the exact
+    // evaluation, so lane 0 issues their loads first and their latency hides
+    // behind it (the pass is a latency chain at the end of the K1 stream)
+    const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
+    uint8_t wg = 0;
+    float cr = 0.f, cg = 0.f, cb = 0.f;
+    if (MODE != 1 && lane == 0) {
+        wg = L.W[idx];
+        cr = L.R[idx];
+        cg = L.G[idx];
+        cb = L.B[idx];
+    }
     const int rc = xpixel_warp_warp(x, y, L.anchors, L.warps, src, nsrc, L.alpha, &wp, stage);
     if (lane != 0) return -1;
     if (MODE == 1) {
@@ -1219,8 +1231,6 @@ __device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, int2 p, doubl
     if (!(yx >= 0.0 && yx <= fxm && yy >= 0.0 && yy <= fym)) return 2;
     double rgb[3];
     xsample_bilinear(L.frame, L.fw, L.fh, L.fch, yx, yy, rgb);
-    const long long idx = (long long)(p.y - L.phys_y0) * L.pitch + (p.x - L.phys_x0);
-    const uint8_t wg = L.W[idx];
     const double wd = wg;
     // reference operation order, no contraction (mosaic.hpp:278-282); the
     // weighted mode runs the same operations with a = w + 1 - cf, cf <= 1
@@ -1229,9 +1239,9 @@ __device__ __forceinline__ int exc_pixel(const NodeFieldLaunch& L, int2 p, doubl
         cf = 1.0 / fmax(xsample_bilinear_f32(L.unc, L.fw, L.fh, yx, yy), 1.0);
         a = xsub(xadd(wd, 1.0), cf);
     }
-    L.R[idx] = (float)(xadd(xmul(a, (double)L.R[idx]), xmul(cf, rgb[0] / 255.0)) / xadd(wd, 1.0));
-    L.G[idx] = (float)(xadd(xmul(a, (double)L.G[idx]), xmul(cf, rgb[1] / 255.0)) / xadd(wd, 1.0));
-    L.B[idx] = (float)(xadd(xmul(a, (double)L.B[idx]), xmul(cf, rgb[2] / 255.0)) / xadd(wd, 1.0));
+    L.R[idx] = (float)(xadd(xmul(a, (double)cr), xmul(cf, rgb[0] / 255.0)) / xadd(wd, 1.0));
+    L.G[idx] = (float)(xadd(xmul(a, (double)cg), xmul(cf, rgb[1] / 255.0)) / xadd(wd, 1.0));
+    L.B[idx] = (float)(xadd(xmul(a, (double)cb), xmul(cf, rgb[2] / 255.0)) / xadd(wd, 1.0));
     L.W[idx] = wg < kWeightCap ? (uint8_t)(wg + 1) : wg;
     return 0;
 }
