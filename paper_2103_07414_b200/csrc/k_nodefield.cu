@@ -1364,6 +1364,16 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
     __shared__ bool last;
     __shared__ double stage[EXC_THREADS / 32][32 * 6];
     pdl_trigger();  // the next blend's planner may start (it only reads nodes)
+    // the exact evaluation's dependent reads of inputs no kernel writes (the
+    // exp table, small node arrays) start before the wait for the field grid,
+    // so a queued pixel finds them in this SM's L1
+    prefetch_l1(reinterpret_cast<const char*>(kExpTab) + 128 * (threadIdx.x & 15));
+    if (L.n <= 256) {
+        for (int o = 128 * threadIdx.x; o < 16 * L.n; o += 128 * EXC_THREADS)
+            prefetch_l1(reinterpret_cast<const char*>(L.anchors) + o);
+        for (int o = 128 * threadIdx.x; o < 40 * L.n; o += 128 * EXC_THREADS)
+            prefetch_l1(reinterpret_cast<const char*>(L.warps) + o);
+    }
     pdl_wait();
     int nb = 0, nns = 0, noof = 0;
     exc_run<MODE>(L, stage[threadIdx.x >> 5], nb, nns, noof);

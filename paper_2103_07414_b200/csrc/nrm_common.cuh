@@ -204,6 +204,10 @@ __device__ __forceinline__ double xsample_bilinear_f32(const float* __restrict__
 #ifndef NRM_NO_PDL
 #define NRM_PDL 1
 #endif
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ void pdl_wait() {
 #ifdef NRM_PDL
     asm volatile("griddepcontrol.wait;" ::: "memory");
