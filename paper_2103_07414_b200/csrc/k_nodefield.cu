@@ -1092,6 +1092,7 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
     const int lane = threadIdx.x & 31;
     const double na = -alpha;
     double wsum = 0.0, aw = 0.0, az = 0.0, adx = 0.0, ady = 0.0, as = 0.0;
+    double accj = 0.0;  // staged path: lane j < 6 keeps sum j (aw, az, adx, ady, as, wsum)
     double ref_w = 0.0, ref_z = 0.0;
     bool have_ref = false;
     for (int g0 = 0; g0 < n; g0 += 32 * KC) {
@@ -1130,8 +1131,9 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
                 qc[1] = -qc[1]; qc[2] = -qc[2]; qc[3] = -qc[3]; qc[4] = -qc[4];
             }
             if (stage) {
-                // contributors' terms in index order through shared memory; lane 0
-                // adds them with pipelined loads (same sequence of rounded adds)
+                // contributors' terms in index order through shared memory; lane j
+                // < 6 adds term j of each in turn (the same sequence of rounded
+                // adds per sum, the six sums' latency chains side by side)
                 if (contrib[c]) {
                     double* d = stage + 6 * __popc(m & ((1u << lane) - 1u));
                     d[0] = xmul(w[c], qc[1]);
@@ -1142,18 +1144,10 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
                     d[5] = w[c];
                 }
                 __syncwarp();
-                if (lane == 0) {
+                if (lane < 6) {
                     const int cnt = __popc(m);
-#pragma unroll 4
-                    for (int e = 0; e < cnt; ++e) {
-                        const double* d = stage + 6 * e;
-                        aw = xadd(aw, d[0]);
-                        az = xadd(az, d[1]);
-                        adx = xadd(adx, d[2]);
-                        ady = xadd(ady, d[3]);
-                        as = xadd(as, d[4]);
-                        wsum = xadd(wsum, d[5]);
-                    }
+#pragma unroll 8
+                    for (int e = 0; e < cnt; ++e) accj = xadd(accj, stage[6 * e + lane]);
                 }
                 __syncwarp();
                 continue;
@@ -1171,13 +1165,13 @@ __device__ int xpixel_warp_warp(double x, double y, const double* __restrict__ a
             }
         }
     }
-    if (stage) {  // lane 0 holds the sums
-        aw = __shfl_sync(0xffffffffu, aw, 0);
-        az = __shfl_sync(0xffffffffu, az, 0);
-        adx = __shfl_sync(0xffffffffu, adx, 0);
-        ady = __shfl_sync(0xffffffffu, ady, 0);
-        as = __shfl_sync(0xffffffffu, as, 0);
-        wsum = __shfl_sync(0xffffffffu, wsum, 0);
+    if (stage) {  // lanes 0..5 hold the sums
+        aw = __shfl_sync(0xffffffffu, accj, 0);
+        az = __shfl_sync(0xffffffffu, accj, 1);
+        adx = __shfl_sync(0xffffffffu, accj, 2);
+        ady = __shfl_sync(0xffffffffu, accj, 3);
+        as = __shfl_sync(0xffffffffu, accj, 4);
+        wsum = __shfl_sync(0xffffffffu, accj, 5);
     }
     XPW s{wsum, aw, az, adx, ady, as, ref_w, ref_z, have_ref};
     return xpw_finish(s, out);
