@@ -114,9 +114,15 @@ struct Smem {
 
 // K1 only: the tile's canvas values, staged with cp.async at kernel entry.
 struct CanvasTile {
-    float r[TH][HW], g[TH][HW], b[TH][HW];
+    float r[TH][HW], g[TH][HW], b[TH][HW];  // one 32 x 32 TMA box each (128-byte aligned)
     uint8_t w[TH][HW];
+    unsigned long long bar;  // TMA completion
 };
+// CanvasTile's offset in the dynamic shared memory (TMA destinations: 128 B)
+template <int CW>
+__host__ __device__ constexpr size_t canvas_tile_offset() {
+    return (sizeof(Smem<CW>) + 127) & ~size_t(127);
+}
 
 
 // One frame of a batched blend (frames with pairwise disjoint footprints).
@@ -460,7 +466,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
                                              unsigned char* smem_raw) {
     constexpr int MT = K1Shape<MODE>::MT, CW = K1Shape<MODE>::CW, NH = K1Shape<MODE>::NH;
     Smem<CW>& s = *reinterpret_cast<Smem<CW>*>(smem_raw);
-    CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + ((sizeof(Smem<CW>) + 15) & ~size_t(15)));
+    CanvasTile& ct = *reinterpret_cast<CanvasTile*>(smem_raw + canvas_tile_offset<CW>());
     const int t = threadIdx.x;
     const int half = bx % NH;  // this CTA's column slice of the planning tile
     const NfPlan& pl = plans[by * ntx + bx / NH];
@@ -473,7 +479,18 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
     //         canvas: tiles and canvas bounds are both 32/64-aligned,
     //         mosaic.hpp:141-151) before the plan header arrives, then the
     //         first chunk of the tile's plan
-    if (MODE != 1) {
+    const bool tma = MODE != 1 && L.ctm_ok;  // launch-uniform
+    if (tma) {  // four 32 x 32 boxes by TMA, one thread; everyone waits before the epilogue
+        if (t == 0) {
+            mbar_init(&ct.bar, 1);
+            mbar_expect_tx(&ct.bar, (unsigned)(3 * sizeof(ct.r) + sizeof(ct.w)));
+            const int x = hi0 - (int)L.phys_x0, y = tj0 - (int)L.phys_y0;
+            tma_load_2d(ct.r, &L.ctm[0], x, y, &ct.bar);
+            tma_load_2d(ct.g, &L.ctm[1], x, y, &ct.bar);
+            tma_load_2d(ct.b, &L.ctm[2], x, y, &ct.bar);
+            tma_load_2d(ct.w, &L.ctm[3], x, y, &ct.bar);
+        }
+    } else if (MODE != 1) {
         const long long base = (long long)(tj0 - L.phys_y0) * L.pitch + (hi0 - L.phys_x0);
         {  // float planes: thread = (row r, 16-byte chunk k) for rows r and r + 16
             const int k = t & 7, r = t >> 3;  // r < 32
@@ -490,8 +507,13 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
     const int status = pl.h.status;
     const int ci0 = max(hi0, L.grid.i0), ci1 = min(hi0 + CW - 1, L.grid.i1);
     const int cj0 = max(tj0, L.grid.j0), cj1 = min(tj0 + TH - 1, L.grid.j1);
-    if (status == NF_OUTSIDE || ci0 > ci1) {  // outside the footprint rows / right of the grid
+    // an early exit must not leave a copy into this CTA's shared memory in flight
+    auto drain = [&]() {
         cp_async_wait_all();
+        if (tma && t == 0) mbar_wait(&ct.bar, 0);
+    };
+    if (status == NF_OUTSIDE || ci0 > ci1) {  // outside the footprint rows / right of the grid
+        drain();
         return;
     }
     const int count = pl.h.count;
@@ -500,7 +522,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
 
     if (status == NF_EXACT) {
         tile_to_exceptions<MODE>(L, ci0, ci1, cj0, cj1);
-        cp_async_wait_all();
+        drain();
         return;
     }
 
@@ -517,7 +539,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
             }
             ++ns;
         }
-        cp_async_wait_all();
+        drain();
         if (MODE != 1) block_add3<NT>(L.acc, 0, ns, 0);
         return;
     }
@@ -657,6 +679,7 @@ __device__ __forceinline__ void nf_field_cta(const NodeFieldLaunch& L, const NfP
         }
     }
 
+    if (tma) mbar_wait(&ct.bar, 0);  // the canvas tile has landed
     // ---- E. epilogue --------------------------------------------------------
     // Output position y = Y0 + r with the integer tile image origin Y0 and a
     // tile-relative remainder r = e0 + dl P + (s0 + dl) Q(u) that stays small
@@ -1048,8 +1071,8 @@ __device__ __forceinline__ void nf_field_tc(const NodeFieldLaunch& L, const NfPl
 
 template <int MODE>
 __global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
-k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int s1, int by0,
-             int ntx) {
+k_node_field(const __grid_constant__ NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0,
+             int s1, int by0, int ntx) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     pdl_wait();
 #ifndef NRM_K2_MMASYNC
@@ -1066,7 +1089,7 @@ k_node_field(NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, i
 template <int MODE>
 __global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
 k_node_field_batch(const NfBatchFrame* __restrict__ F, int nf, const NfPlan* __restrict__ plans) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr int NH = K1Shape<MODE>::NH;
     pdl_wait();
     int f = 0;
@@ -1560,7 +1583,7 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         L.lists = reinterpret_cast<int*>(reinterpret_cast<char*>(L.plans) + (size_t)NF_CHUNK_TILES * sizeof(NfPlan));
         L.lcounts = L.lists + (size_t)g.nchunks * L.col_groups * L.lstride;
     }
-    const size_t base = (sizeof(Smem<K1Shape<0>::CW>) + 15) & ~size_t(15);
+    const size_t base = canvas_tile_offset<K1Shape<0>::CW>();
 #ifndef NRM_K2_MMASYNC
     const size_t smem_k2 = sizeof(SmemTC);
 #else
@@ -1640,7 +1663,7 @@ cudaError_t launch_node_field_batch(const NodeFieldLaunch* Ls, int nf, void* scr
                        0, st, static_cast<const NfBatchFrame*>(dF), nf, plans, tiles);
         ++*launches;
         if (e != cudaSuccess) return e;
-        const size_t smem = ((sizeof(Smem<K1Shape<0>::CW>) + 15) & ~size_t(15)) + sizeof(CanvasTile);
+        const size_t smem = canvas_tile_offset<K1Shape<0>::CW>() + sizeof(CanvasTile);
         cudaFuncSetAttribute(k_node_field_batch<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         prof_mark("k_node_field", st);
         e = launch_pdl(k_node_field_batch<0>, dim3(ctas), dim3(NT), smem, st, static_cast<const NfBatchFrame*>(dF),

@@ -2,6 +2,7 @@
 // HBM-resident canvases with the reference's growth bookkeeping, transfers
 // and kernel orchestration. No compute happens on the host: every per-pixel
 // result comes from the kernels in k_*.cu.
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -320,6 +321,37 @@ size_t exception_capacity(const nrm_ctx* c, size_t pixels) {
     return std::max<size_t>(1, std::min<size_t>({cap, pixels, (size_t)0x7fffffff}));
 }
 
+// K1's canvas tensor maps (TMA): the four planes as 2D tensors of cap_w x
+// cap_h elements, box 32 x 32 (one K1 CTA's canvas tile). The encoder comes
+// from the driver through the runtime (no libcuda link). Returns false (and
+// K1 stages the tile with cp.async) when a plane does not meet TMA's
+// alignment rules or the encoder is unavailable.
+bool canvas_tensor_maps(const nrm_canvas* cv, NodeFieldLaunch& L) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || cv->cap_w % 16 != 0) return false;
+    const void* planes[4] = {cv->r, cv->g, cv->b, cv->w};
+    for (int k = 0; k < 4; ++k) {
+        if (reinterpret_cast<uintptr_t>(planes[k]) % 16 != 0) return false;
+        const bool f32 = k < 3;
+        const cuuint64_t dims[2] = {(cuuint64_t)cv->cap_w, (cuuint64_t)cv->cap_h};
+        const cuuint64_t stride[1] = {(cuuint64_t)cv->cap_w * (f32 ? 4u : 1u)};
+        const cuuint32_t box[2] = {32, 32}, estride[2] = {1, 1};
+        if (encode(&L.ctm[k], f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                   const_cast<void*>(planes[k]), dims, stride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
+}
+
 // K1's frame textures: frames converted to RGBA8 rows (pitch a multiple of
 // 128 B), frame k into slot k of the context's frame_rgba buffer, and a
 // texture object per slot (point sampling, clamped addresses, normalised
@@ -439,6 +471,7 @@ int blend_core(nrm_canvas* cv, const uint8_t* d_frame, int fw, int fh, int ch, c
     L.exc_overflow = st.overflow;
     L.exc_last = st.last_exc;
     L.exc_done = st.exc_done;
+    L.ctm_ok = canvas_tensor_maps(cv, L) ? 1 : 0;
     NRM_CUDA(c->tiles.ensure(node_field_scratch_bytes(L)));
     L.plans = c->tiles.p;
     if (ch == 3 || ch == 4) {

@@ -2,6 +2,7 @@
 // launch interfaces shared between translation units.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -114,6 +115,10 @@ struct FieldGrid {
 };
 
 struct NodeFieldLaunch {
+    // K1: TMA tensor maps of the canvas planes R, G, B (FP32) and W (u8), box
+    // 32 x 32 (one K1 CTA's canvas tile); `ctm_ok` 0: cp.async staging instead
+    alignas(64) CUtensorMap ctm[4];
+    int ctm_ok = 0;
     // inputs
     const uint8_t* frame = nullptr;  // ImageU8 layout: h x w x fch, fch in {1, 3, 4}
     int fw = 0, fh = 0, fch = 3;
