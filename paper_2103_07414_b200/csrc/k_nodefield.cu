@@ -1095,6 +1095,14 @@ k_node_field_batch(const NfBatchFrame* __restrict__ F, int nf, const NfPlan* __r
     int f = 0;
     while (f + 1 < nf && (int)blockIdx.x >= F[f + 1].cta_off) ++f;
     const NfBatchFrame& fr = F[f];
+    if (fr.L.ctm_ok && threadIdx.x == 0) {
+        // the frame table's tensor maps were copied in by the host: acquire
+        // them for the TMA unit (its descriptor cache may hold this address's
+        // maps from an earlier call)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(&fr.L.ctm[k]) : "memory");
+    }
     const int lc = (int)blockIdx.x - fr.cta_off, per_row = fr.ntx * NH;
     nf_field_cta<MODE>(fr.L, plans + fr.plan_off, fr.ti0, fr.tj0, fr.s1, 0, fr.ntx, lc % per_row, lc / per_row,
                        smem_raw);

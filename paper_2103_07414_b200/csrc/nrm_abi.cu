@@ -1136,6 +1136,15 @@ int nrm_blend_frames_device(nrm_canvas* cv, int nf, const uint8_t* const* d_fram
         L.exc_done = st.exc_done;
         qoff += cap[a];
     }
+    // one canvas, so one set of tensor maps, copied into every frame's launch
+    // (the batch kernel reads them from its frame table in global memory)
+    if (nact > 0 && canvas_tensor_maps(cv, Ls[0])) {
+        Ls[0].ctm_ok = 1;
+        for (size_t a = 1; a < nact; ++a) {
+            for (int k = 0; k < 4; ++k) Ls[a].ctm[k] = Ls[0].ctm[k];
+            Ls[a].ctm_ok = 1;
+        }
+    }
     if (ch == 3 || ch == 4) {  // one conversion launch for every active frame
         std::vector<const uint8_t*> fr(nact);
         std::vector<NodeFieldLaunch*> lp(nact);
