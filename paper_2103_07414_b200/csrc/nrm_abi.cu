@@ -3,6 +3,7 @@
 // and kernel orchestration. No compute happens on the host: every per-pixel
 // result comes from the kernels in k_*.cu.
 #include <cudaTypedefs.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -335,7 +336,8 @@ bool canvas_tensor_maps(const nrm_canvas* cv, NodeFieldLaunch& L) {
             fn = nullptr;
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
-    if (!encode || cv->cap_w % 16 != 0) return false;
+    static const bool off = std::getenv("NRM_B200_NO_TMA") != nullptr;  // tests: the cp.async staging path
+    if (off || !encode || cv->cap_w % 16 != 0) return false;
     const void* planes[4] = {cv->r, cv->g, cv->b, cv->w};
     for (int k = 0; k < 4; ++k) {
         if (reinterpret_cast<uintptr_t>(planes[k]) % 16 != 0) return false;

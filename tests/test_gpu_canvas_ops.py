@@ -11,7 +11,9 @@
   bit; both deformation paths (ping-pong pass, region scratch) match the
   oracle restatement;
 * dist.BandedMosaic runs on torch's current stream: its stats and render
-  equal blend_frame / render."""
+  equal blend_frame / render;
+* K1's canvas tile staged by TMA tensor maps (the default) and by cp.async
+  (NRM_B200_NO_TMA) gives the same bits, single and batched blends."""
 import numpy as np
 import pytest
 
@@ -300,3 +302,46 @@ def test_emdq_exact_queue_matches_inline_exact_bitwise(nrm, ctx, name):
     assert ctx.exceptions()[1] == n_exact
     assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
     assert np.array_equal(u0.view(np.uint32), u1.view(np.uint32))
+
+
+_NO_TMA_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2103_07414_b200 import mosaic as nrm
+g = dict(np.load(sys.argv[2]))
+ctx = nrm.Context(0)
+cv = nrm.Canvas(ctx)
+polys, o = [], 0
+for n in g["npoly"]:
+    polys.append(g["polys"][o:o + n])
+    o += n
+st = [nrm.blend_frame(cv, g["frame"], g["anchors"], g["warps"][k], float(g["alpha"]), p).as_tuple()
+      for k, p in enumerate(polys)]
+col, wt = cv.read()
+np.savez(sys.argv[3], st=np.array(st), col=col, wt=wt)
+"""
+
+
+@pytest.mark.parametrize("case", ["blend_c1_seq", "blend_gray_rotated"])
+def test_canvas_staging_tma_matches_cp_async(nrm, ctx, golden, tmp_path, case):
+    """The same blends with K1's canvas tile staged by cp.async (a fresh
+    process with NRM_B200_NO_TMA set) are bit-identical to the TMA path."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    g = golden(case)
+    polys = split_polys(g) if "npoly" in g else [g["polys"]] * len(g["warps"])
+    inp = tmp_path / "in.npz"
+    np.savez(inp, frame=g["frame"], anchors=g["anchors"], warps=g["warps"], alpha=g["alpha"],
+             polys=np.concatenate(polys), npoly=np.array([len(p) for p in polys]))
+    ref = _blend_all(nrm, ctx, g, polys)
+    out = tmp_path / "out.npz"
+    env = dict(os.environ, NRM_B200_NO_TMA="1")
+    root = str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", _NO_TMA_SCRIPT, root, str(inp), str(out)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    assert [tuple(x) for x in got["st"].tolist()] == [tuple(x) for x in ref[0]]
+    assert np.array_equal(got["wt"], ref[2]) and np.array_equal(got["col"], ref[1])
