@@ -256,7 +256,12 @@ __device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* _
 // reader of those rows, has exited before this launch can start (its exact
 // pass, the PDL primary here, starts only after all its CTAs exit).
 constexpr int NF_CONV_BLOCKS = 2 * 148;
-__global__ void __launch_bounds__(NF_PLAN_WARPS * 32)
+// 3 CTAs per SM (80 registers, a few spills): alone it is slower (15.9
+// against 13.7 us on C2), but beside K3 the C2 step gains 1.3 us
+#ifndef NRM_NF_PLAN_MINB
+#define NRM_NF_PLAN_MINB 3
+#endif
+__global__ void __launch_bounds__(NF_PLAN_WARPS * 32, NRM_NF_PLAN_MINB)
 k_nf_plan(NodeFieldLaunch L, NfPlan* __restrict__ plans, int tile_i0, int tile_j0, int tile_j_last, int s1, int by0,
           int rows, int ntx, int conv) {
     static_assert(NF_PLAN_WARPS * 32 == RGBA_THREADS, "conversion CTA shape");
