@@ -73,6 +73,8 @@ void prof_mark(const char* name, cudaStream_t st) {
     ++p.used;
 }
 
+bool prof_serialized() { return g_prof_ctx && g_prof_ctx->prof.on; }
+
 ProfScope::ProfScope(nrm_ctx* c) : prev(g_prof_ctx) { g_prof_ctx = c; }
 ProfScope::~ProfScope() {
     if (g_prof_ctx) prof_mark(nullptr, g_prof_ctx->stream);  // end of the call
