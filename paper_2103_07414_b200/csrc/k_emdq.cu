@@ -151,10 +151,81 @@ constexpr int SUPER_CC_CAP = 8192;  // candidates whose coarse coordinates k_sup
 #endif
 constexpr int SUPER_FUSED_GATHER_MAX = NRM_SUPER_FUSED_GATHER_MAX;  // above: a separate k_gather first
 
+// Candidate bins for large candidate sets: 64 px cells on the supertile grid
+// plus a margin ring that takes every candidate outside it. EmdqLaunch::
+// cell_cnt holds count[nc] (persistent-zero), EmdqLaunch::cells start[nc + 1]
+// | cursor[nc] | candidate index[N], nc = (nsx + 2) (nsy + 2).
+constexpr int BIN_MAX_N = 1 << 17;  // k_super keeps an N-bit membership bitmap in shared memory
+struct CellGrid {
+    float x0, y0;  // absolute coordinates of supertile (0, 0)'s first pixel
+    int nsx, nsy;
+};
+__host__ __device__ __forceinline__ int cell_count_of(const CellGrid& cg) { return (cg.nsx + 2) * (cg.nsy + 2); }
+__device__ __forceinline__ int cell_of(const CellGrid& cg, float2 c) {
+    int cx = (int)floorf((c.x - cg.x0) * (1.f / ST)), cy = (int)floorf((c.y - cg.y0) * (1.f / ST));
+    cx = min(max(cx, -1), cg.nsx);
+    cy = min(max(cy, -1), cg.nsy);
+    return (cy + 1) * (cg.nsx + 2) + (cx + 1);
+}
+
+// One CTA: exclusive scan of the cell counts into start / cursor; the counts
+// are zeroed for the next call.
+__global__ void __launch_bounds__(1024) k_bin_scan(int* __restrict__ cnt, int* __restrict__ cells, int nc, int n) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    int* start = cells;
+    int* cur = cells + nc + 1;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < nc; base += 1024) {
+        const int c = base + t;
+        const int v = c < nc ? cnt[c] : 0;
+        int x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int w = wsum[lane];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= d) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const int excl = carry + (wid > 0 ? wsum[wid - 1] : 0) + x - v;
+        if (c < nc) {
+            start[c] = excl;
+            cur[c] = excl;
+            cnt[c] = 0;
+        }
+        __syncthreads();
+        if (t == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (t == 0) start[nc] = n;
+}
+
+// Candidate indices grouped by cell (the order inside a cell is arbitrary:
+// k_super's lists come out in index order through its bitmap).
+__global__ void k_bin_scatter(const float2* __restrict__ c32, int n, CellGrid cg, int* __restrict__ cells) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= n) return;
+    const int nc = cell_count_of(cg);
+    const int pos = atomicAdd(&cells[nc + 1 + cell_of(cg, c32[a])], 1);
+    cells[2 * nc + 1 + pos] = a;
+}
+
 __global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
                          const double* __restrict__ probs, const int32_t* __restrict__ active,
                          int nactive, double* cx, double* cy, float2* c32, double* cl, double* cp,
-                         double* cphi, int* cj) {
+                         double* cphi, int* cj, int* cells, CellGrid cg) {
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= nactive) return;
     const int j = active[a];
@@ -162,6 +233,7 @@ __global__ void k_gather(const double* __restrict__ apts, const double* __restri
     cx[a] = x;
     cy[a] = y;
     c32[a] = make_float2((float)x, (float)y);
+    if (cells) atomicAdd(&cells[cell_of(cg, c32[a])], 1);  // bin counts (zero on entry)
 #pragma unroll
     for (int k = 0; k < 5; ++k) cl[5 * a + k] = locals[5 * j + k];
     const double p = probs[j];
@@ -232,7 +304,7 @@ struct GatherOut {
 // candidate sets): every CTA then reads the contiguous coarse coordinates
 // G.c32 instead of the active -> apts chain of dependent loads.
 __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperLists SL, int S, float pad,
-                                              int gathered) {
+                                              int gathered, CellGrid cg) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     SSmem& s = *reinterpret_cast<SSmem*>(smem_raw);
@@ -258,8 +330,9 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     const int N = L.nactive;
     // coarse coordinates of every candidate, cached in shared memory (one
     // pass of dependent global loads instead of two)
-    float2* cc = N <= SUPER_CC_CAP ? reinterpret_cast<float2*>(smem_raw + ((sizeof(SSmem) + 15) & ~size_t(15)))
-                                   : nullptr;
+    float2* cc = !L.cells && N <= SUPER_CC_CAP
+                     ? reinterpret_cast<float2*>(smem_raw + ((sizeof(SSmem) + 15) & ~size_t(15)))
+                     : nullptr;
     auto coarse_g = [&](int a) {
         if (gathered) return G.c32[a];
         const int j = L.active[a];
@@ -280,34 +353,163 @@ __global__ void __launch_bounds__(ENT) k_super(EmdqLaunch L, GatherOut G, SuperL
     const float hd = (float)(0.5 * sqrt((xhi - xlo) * (xhi - xlo) + (yhi - ylo) * (yhi - ylo)));
 
     s.hist[t] = 0;
-    __syncthreads();
-    for (int a = t; a < N; a += ENT) {
-        const float2 c = coarse(a);
-        const float dx = c.x - cx, dy = c.y - cy;
-        atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
-    }
-    __syncthreads();
-    if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
-    __syncthreads();
-    const float lim = s.R + 2.f * hd + 1.f + pad, lim2 = lim * lim;
     // per-warp contiguous chunks keep the list order deterministic
     const int per = (N + NW - 1) / NW;
     const int a0 = wid * per, a1 = min(N, a0 + per);
     int cnt = 0;
-    for (int base = a0; base < a1; base += 32) {
-        const int a = base + lane;
-        bool keep = false;
-        if (a < a1) {
+    if (L.cells) {
+        // Binned: the same histogram bin of the S-th nearest and the same list
+        // as the full scans below, from the cells near the supertile only.
+        const int ncx = cg.nsx + 2, ncy = cg.nsy + 2, nc = ncx * ncy;
+        const int* cstart = L.cells;
+        const int* cidx = L.cells + 2 * nc + 1;
+        unsigned* bits = reinterpret_cast<unsigned*>(smem_raw + ((sizeof(SSmem) + 15) & ~size_t(15)));
+        for (int w = t; w < (N + 31) / 32; w += ENT) bits[w] = 0u;
+        const int scx = blockIdx.x + 1, scy = blockIdx.y + 1;
+        // (a) ring search: the smallest square of (2r + 1)^2 cells around the
+        //     supertile holding >= S candidates bounds the S-th nearest by the
+        //     square's far corner (rho); a non-empty margin cell in the square
+        //     (candidates outside the grid, unbounded) or too few: rho = inf
+        if (wid == 0) {
+            int cum = 0, r = 0;
+            bool unbounded = false;
+            for (;; ++r) {
+                int c = 0;
+                for (int dy = -r + lane; dy <= r; dy += 32) {
+                    const int y = scy + dy;
+                    if (y < 0 || y >= ncy) continue;
+                    const int xl = max(scx - r, 0), xh = min(scx + r, ncx - 1);
+                    auto cell_n = [&](int x) { return cstart[y * ncx + x + 1] - cstart[y * ncx + x]; };
+                    auto margin = [&](int x) { return x == 0 || x == ncx - 1 || y == 0 || y == ncy - 1; };
+                    if (dy == -r || dy == r) {
+                        const int n = cstart[y * ncx + xh + 1] - cstart[y * ncx + xl];
+                        c += n;
+                        if (n > 0)
+                            for (int x = xl; x <= xh; ++x) unbounded |= margin(x) && cell_n(x) > 0;
+                    } else {
+                        if (scx - r >= 0) {
+                            c += cell_n(scx - r);
+                            unbounded |= margin(scx - r) && cell_n(scx - r) > 0;
+                        }
+                        if (scx + r < ncx) {
+                            c += cell_n(scx + r);
+                            unbounded |= margin(scx + r) && cell_n(scx + r) > 0;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+                cum += c;
+                if (cum >= S || (scx - r <= 0 && scy - r <= 0 && scx + r >= ncx - 1 && scy + r >= ncy - 1)) break;
+            }
+            unbounded = __any_sync(0xffffffffu, unbounded) || cum < S;
+            if (lane == 0) {
+                float rho = INFINITY;
+                if (!unbounded) {
+                    const float sx0 = cg.x0 + ST * (float)(blockIdx.x - r), sx1 = cg.x0 + ST * (float)(blockIdx.x + r + 1);
+                    const float sy0 = cg.y0 + ST * (float)(blockIdx.y - r), sy1 = cg.y0 + ST * (float)(blockIdx.y + r + 1);
+                    const float dxm = fmaxf(cx - sx0, sx1 - cx), dym = fmaxf(cy - sy0, sy1 - cy);
+                    rho = sqrtf(dxm * dxm + dym * dym) + 2.f;
+                }
+                s.R = rho;  // (reused: the scan radius, then the list radius)
+            }
+        }
+        __syncthreads();
+        // the cell rows and columns a disc of radius rad around the centre touches
+        auto window = [&](float rad, int& x_lo, int& x_hi, int& y_lo, int& y_hi) {
+            if (!(rad < 1e30f)) {
+                x_lo = 0, x_hi = ncx - 1, y_lo = 0, y_hi = ncy - 1;
+                return;
+            }
+            x_lo = max(0, (int)floorf((cx - rad - cg.x0) * (1.f / ST)) + 1 - 1);
+            x_hi = min(ncx - 1, (int)floorf((cx + rad - cg.x0) * (1.f / ST)) + 1 + 1);
+            y_lo = max(0, (int)floorf((cy - rad - cg.y0) * (1.f / ST)) + 1 - 1);
+            y_hi = min(ncy - 1, (int)floorf((cy + rad - cg.y0) * (1.f / ST)) + 1 + 1);
+        };
+        int x_lo, x_hi, y_lo, y_hi;
+        window(s.R, x_lo, x_hi, y_lo, y_hi);
+        // (b) histogram over the window: every candidate within rho is in it
+        //     and at least S are, so the first bin whose cumulative count
+        //     reaches S is the full histogram's
+        for (int y = y_lo + wid; y <= y_hi; y += NW) {  // a warp per cell row: the rows' load chains overlap
+            const int e0 = cstart[y * ncx + x_lo], e1 = cstart[y * ncx + x_hi + 1];
+            for (int e = e0 + lane; e < e1; e += 32) {
+                const float2 c = G.c32[cidx[e]];
+                const float dx = c.x - cx, dy = c.y - cy;
+                atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
+            }
+        }
+        __syncthreads();
+        if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
+        __syncthreads();
+        const float lim = s.R + 2.f * hd + 1.f + pad, lim2 = lim * lim;
+        // (c) membership over the list window (the full scan's test), as bits
+        window(lim, x_lo, x_hi, y_lo, y_hi);
+        for (int y = y_lo + wid; y <= y_hi; y += NW) {
+            const int e0 = cstart[y * ncx + x_lo], e1 = cstart[y * ncx + x_hi + 1];
+            for (int e = e0 + lane; e < e1; e += 32) {
+                const int a = cidx[e];
+                const float2 c = G.c32[a];
+                const float dx = c.x - cx, dy = c.y - cy;
+                if (!(fmaf(dx, dx, dy * dy) > lim2)) atomicOr(&bits[a >> 5], 1u << (a & 31));
+            }
+        }
+        __syncthreads();
+        // (d) each warp's index range, in index order (the full scan's chunks)
+        if (a0 < a1) {
+            const int wlast = (a1 - 1) >> 5;
+            for (int wb = a0 >> 5; wb <= wlast; wb += 32) {
+                const int word = wb + lane;
+                unsigned b = 0u;
+                if (word <= wlast) {
+                    b = bits[word];
+                    const int lo = word * 32;
+                    if (lo < a0) b &= ~0u << (a0 - lo);
+                    if (a1 - lo < 32) b &= (1u << (a1 - lo)) - 1u;
+                }
+                const int nb = __popc(b);
+                int incl = nb;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                int pos = cnt + incl - nb;
+                while (b) {
+                    const int k = __ffs(b) - 1;
+                    b &= b - 1u;
+                    if (pos < WCAP_S) s.wcand[wid][pos] = word * 32 + k;
+                    ++pos;
+                }
+                cnt += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+    } else {
+        __syncthreads();
+        for (int a = t; a < N; a += ENT) {
             const float2 c = coarse(a);
             const float dx = c.x - cx, dy = c.y - cy;
-            keep = !(fmaf(dx, dx, dy * dy) > lim2);
+            atomicAdd(&s.hist[hist_bin(fmaf(dx, dx, dy * dy))], 1);
         }
-        const unsigned msk = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-            const int pos = cnt + __popc(msk & ((1u << lane) - 1u));
-            if (pos < WCAP_S) s.wcand[wid][pos] = a;
+        __syncthreads();
+        if (wid == 0) radius_from_hist(s.hist, S, lane, &s.R);
+        __syncthreads();
+        const float lim = s.R + 2.f * hd + 1.f + pad, lim2 = lim * lim;
+        for (int base = a0; base < a1; base += 32) {
+            const int a = base + lane;
+            bool keep = false;
+            if (a < a1) {
+                const float2 c = coarse(a);
+                const float dx = c.x - cx, dy = c.y - cy;
+                keep = !(fmaf(dx, dx, dy * dy) > lim2);
+            }
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = cnt + __popc(msk & ((1u << lane) - 1u));
+                if (pos < WCAP_S) s.wcand[wid][pos] = a;
+            }
+            cnt += __popc(msk);
         }
-        cnt += __popc(msk);
     }
     if (lane == 0) s.wcnt[wid] = cnt;
     __syncthreads();
@@ -1438,6 +1640,15 @@ static unsigned emdq_queue_cap(const FieldGrid& g) {
 }
 static size_t emdq_queue_bytes(const FieldGrid& g) { return (size_t)emdq_queue_cap(g) * sizeof(int2) + 16; }
 
+void emdq_cell_bytes(int nactive, const FieldGrid& g, size_t* count_bytes, size_t* bin_bytes) {
+    *count_bytes = *bin_bytes = 0;
+    if (nactive <= SUPER_FUSED_GATHER_MAX || nactive > BIN_MAX_N) return;
+    const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
+    const size_t nc = (size_t)(nsx + 2) * (nsy + 2);
+    *count_bytes = nc * sizeof(int);
+    *bin_bytes = (2 * nc + 1 + (size_t)nactive) * sizeof(int);
+}
+
 size_t emdq_scratch_bytes(int nactive, const FieldGrid& g, bool tile_plans) {
     const size_t na = (size_t)nactive;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
@@ -1486,8 +1697,12 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
 
     const GatherOut G{L.cx, L.cy, L.cl, L.cp, phi, c32, cj};
     const int S = L.support < L.nactive ? L.support : L.nactive;
+    const CellGrid cg{(float)(L.grid.gx + L.grid.i0), (float)(L.grid.gy + L.grid.j0), SL.nsx, nsy};
+    if (L.nactive <= SUPER_FUSED_GATHER_MAX || L.nactive > BIN_MAX_N || !LQ.cell_cnt) LQ.cells = LQ.cell_cnt = nullptr;
+    const bool binned = LQ.cells != nullptr;  // set by the caller when emdq_cell_bytes() > 0
     const size_t ssm = ((sizeof(SSmem) + 15) & ~size_t(15)) +
-                       (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
+                       (binned ? (size_t)((L.nactive + 31) / 32) * sizeof(unsigned)
+                               : (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0));
     cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     // programmatic launch: its CTAs become resident while the stream's previous
     // kernel drains and wait in pdl_wait() before touching any scratch
@@ -1498,13 +1713,21 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     if (gathered) {
         prof_mark("k_gather", st);
         k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
-                                                           c32, L.cl, L.cp, phi, cj);
+                                                           c32, L.cl, L.cp, phi, cj, LQ.cell_cnt, cg);
         ++*launches;
         cudaError_t eg = cudaGetLastError();
         if (eg != cudaSuccess) return eg;
+        if (binned) {
+            prof_mark("k_bin", st);
+            k_bin_scan<<<1, 1024, 0, st>>>(LQ.cell_cnt, LQ.cells, cell_count_of(cg), L.nactive);
+            k_bin_scatter<<<(L.nactive + 255) / 256, 256, 0, st>>>(c32, L.nactive, cg, LQ.cells);
+            *launches += 2;
+            eg = cudaGetLastError();
+            if (eg != cudaSuccess) return eg;
+        }
     }
     prof_mark("k_super", st);
-    cudaError_t e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, LQ, G, SL, S, 0.f, gathered);
+    cudaError_t e = launch_pdl(k_super, dim3(SL.nsx, nsy), dim3(ENT), ssm, st, LQ, G, SL, S, 0.f, gathered, cg);
     ++*launches;
     if (e != cudaSuccess) return e;
     const int ntx = (L.grid.i1 - L.grid.i0 + ET) / ET;
@@ -1579,7 +1802,7 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
     if (P.full_scan) {
         prof_mark("k_gather", st);
         k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx,
-                                                           L.cy, c32, L.cl, L.cp, phi, cj);
+                                                           L.cy, c32, L.cl, L.cp, phi, cj, nullptr, CellGrid{});
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
@@ -1589,7 +1812,9 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
                            (L.nactive <= SUPER_CC_CAP ? (size_t)L.nactive * sizeof(float2) : 0);
         cudaFuncSetAttribute(k_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         prof_mark("k_super", st);
-        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(L, G, SL, Ssup, 3.f, 0);
+        EmdqLaunch Lp = L;
+        Lp.cells = Lp.cell_cnt = nullptr;  // the point queries' supertiles scan every candidate
+        k_super<<<dim3(SL.nsx, nsy), ENT, ssm, st>>>(Lp, G, SL, Ssup, 3.f, 0, CellGrid{});
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

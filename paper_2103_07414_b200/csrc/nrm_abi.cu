@@ -594,6 +594,17 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     L.cp = base + 7 * na;  // phi, c32, j, supertile lists and plans follow: see launch_emdq_field
     L.exact_count = state_of(c).emdq_exact;  // zeroed by k_super (no memset node in the PDL chain)
     L.exq_cap_override = c->exc_cap_override;
+    size_t cnt_bytes = 0, bin_bytes = 0;
+    emdq_cell_bytes(nactive, fg, &cnt_bytes, &bin_bytes);
+    if (cnt_bytes) {  // large candidate sets: binned supertile scans
+        const bool grow = c->emdq_cell_cnt.cap < cnt_bytes;
+        NRM_CUDA(c->emdq_cell_cnt.ensure(cnt_bytes));
+        // the bin counts start at zero; k_bin_scan re-zeroes every count it used
+        if (grow) NRM_CUDA(cudaMemsetAsync(c->emdq_cell_cnt.p, 0, c->emdq_cell_cnt.cap, c->stream));
+        NRM_CUDA(c->emdq_cells.ensure(bin_bytes));
+        L.cell_cnt = c->emdq_cell_cnt.as<int>();
+        L.cells = c->emdq_cells.as<int>();
+    }
     NRM_CUDA(launch_emdq_field(L, c->stream, &c->launches));
     return NRM_OK;
 }
@@ -700,7 +711,7 @@ int nrm_ctx_destroy(nrm_ctx* c) {
         if (t) cudaDestroyTextureObject((cudaTextureObject_t)t);
     DevBuf* bufs[] = {&c->frame_raw, &c->anchors, &c->warps, &c->exc,   &c->misc,  &c->stats, &c->pts,
                       &c->locals,    &c->probs,   &c->active, &c->out_a, &c->out_b, &c->tiles, &c->feat,
-                      &c->feat_io,   &c->batch,  &c->halo,   &c->frame_rgba};
+                      &c->feat_io,   &c->batch,  &c->halo,   &c->frame_rgba, &c->emdq_cells, &c->emdq_cell_cnt};
     for (DevBuf* b : bufs) b->release();
     c->staging.release();
     c->staging_out.release();

@@ -57,6 +57,8 @@ struct nrm_ctx {
     int num_sms = 148;
     int64_t exc_cap_override = 0;  // nrm_ctx_set_exception_capacity (tests); 0 = default sizing
     // scratch (grow-only)
+    nrm::DevBuf emdq_cell_cnt;  // K3 candidate bin counts (zeroed on allocation, kept zero by k_bin_scan)
+    nrm::DevBuf emdq_cells;     // K3 candidate bins: starts, cursors, indices
     nrm::DevBuf frame_raw, anchors, warps, exc, misc, stats, pts, locals, probs,
         active, out_a, out_b, tiles, feat, feat_io, batch, halo,
         frame_rgba;  // K1: RGBA8 copies of the blended frames (texture storage, one slot per frame)
@@ -225,6 +227,13 @@ struct EmdqLaunch {
     unsigned* exq_count = nullptr;
     unsigned exq_cap = 0;
     int64_t exq_cap_override = 0;  // nrm_ctx_set_exception_capacity (tests); 0 = default sizing
+    // large candidate sets: the candidates binned into 64 px cells (the
+    // supertile grid plus a margin ring), so k_super scans only the cells
+    // near each supertile. cell_cnt: per-cell counts, persistent-zero (its
+    // own buffer: a call with fewer cells must not leave data where a later
+    // call with more cells counts); cells: start[nc + 1] | cursor[nc] | index[N]
+    int* cell_cnt = nullptr;
+    int* cells = nullptr;
     // scratch: gathered candidates (SoA, nactive each)
     double* cx = nullptr;
     double* cy = nullptr;
@@ -232,6 +241,8 @@ struct EmdqLaunch {
     double* cp = nullptr;   // max(prob, 1e-6)
 };
 cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* launches);
+// binning buffers for a call (0, 0: no binning at this size)
+void emdq_cell_bytes(int nactive, const FieldGrid& g, size_t* count_bytes, size_t* bin_bytes);
 size_t emdq_scratch_bytes(int nactive, const FieldGrid& g, bool tile_plans = true);
 // Scattered queries (EM E-step / final field): L.grid is a grid covering the
 // queries (only its supertile geometry is used); exact tier throughout.

@@ -51,5 +51,29 @@ for seed in range(40):
     d, u = nrm.emdq_field((x0, y0, w, h), apts, loc, probs, active, float(rng.uniform(1e-4, 5e-3)),
                           float(rng.uniform(1e-4, 5e-3)), S, ctx=ctx)
     out[f"r{seed}_d"], out[f"r{seed}_u"] = d, u
+for seed in range(16):  # large candidate sets (binned supertile scans), some far outside the grid
+    rng = np.random.default_rng(1900 + seed)
+    m = int(rng.integers(3000, 30000))
+    w, h = int(rng.integers(300, 2000)), int(rng.integers(200, 1200))
+    x0, y0 = float(rng.uniform(-3e4, 3e4)), float(rng.uniform(-3e4, 3e4))
+    apts = np.stack([rng.uniform(x0 - 80, x0 + w + 80, m), rng.uniform(y0 - 80, y0 + h + 80, m)], 1)
+    if seed % 3 == 0:  # clusters
+        c = np.stack([rng.uniform(x0, x0 + w, 9), rng.uniform(y0, y0 + h, 9)], 1)
+        apts[: m // 2] = c[rng.integers(0, 9, m // 2)] + rng.normal(0, 6.0, (m // 2, 2))
+    if seed % 4 == 1:  # a sprinkling far outside the grid (margin cells)
+        k = m // 50
+        apts[:k] += rng.choice([-1.0, 1.0], (k, 2)) * rng.uniform(500, 5000, (k, 2))
+    ang = rng.uniform(-0.02, 0.02, m)
+    loc = np.zeros((m, 5))
+    loc[:, 0] = rng.uniform(0.9, 1.1, m)
+    loc[:, 1], loc[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    loc[:, 3:5] = rng.normal(0, 8.0, (m, 2))
+    probs = rng.uniform(0, 1, m)
+    active = np.sort(rng.choice(m, int(rng.integers(2100, m + 1)), replace=False)).astype(np.int32)
+    S = int((16, 8, 32, 4)[seed % 4])
+    print("large case", seed, m, w, h, len(active), S, flush=True)
+    d, u = nrm.emdq_field((x0, y0, w, h), apts, loc, probs, active, float(rng.uniform(1e-4, 2e-3)),
+                          float(rng.uniform(1e-4, 2e-3)), S, ctx=ctx)
+    out[f"L{seed}_d"], out[f"L{seed}_u"] = d, u
 np.savez(sys.argv[1], **out)
 print("saved", len(out), "arrays")
