@@ -13,7 +13,9 @@
 * dist.BandedMosaic runs on torch's current stream: its stats and render
   equal blend_frame / render;
 * K1's canvas tile staged by TMA tensor maps (the default) and by cp.async
-  (NRM_B200_NO_TMA) gives the same bits, single and batched blends."""
+  (NRM_B200_NO_TMA) gives the same bits, single and batched blends;
+* the binned supertile scan of large candidate sets keeps its bin counts
+  clean across calls with different grid sizes."""
 import numpy as np
 import pytest
 
@@ -302,6 +304,42 @@ def test_emdq_exact_queue_matches_inline_exact_bitwise(nrm, ctx, name):
     assert ctx.exceptions()[1] == n_exact
     assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
     assert np.array_equal(u0.view(np.uint32), u1.view(np.uint32))
+
+
+def _large_emdq_case(seed, w, h):
+    rng = np.random.default_rng(seed)
+    m = 6000
+    apts = np.stack([rng.uniform(-80, w + 80, m), rng.uniform(-80, h + 80, m)], 1)
+    apts[:60] += rng.choice([-1.0, 1.0], (60, 2)) * rng.uniform(500, 3000, (60, 2))  # margin cells
+    ang = rng.uniform(-0.05, 0.05, m)
+    loc = np.zeros((m, 5))
+    loc[:, 0] = rng.uniform(0.9, 1.1, m)
+    loc[:, 1], loc[:, 2] = np.cos(ang / 2), np.sin(ang / 2)
+    loc[:, 3:5] = rng.normal(0, 6.0, (m, 2))
+    probs = rng.uniform(0, 1, m)
+    active = np.sort(rng.choice(m, 5000, replace=False)).astype(np.int32)
+    return (0.0, 0.0, w, h), apts, loc, probs, active, 5e-4, 5e-4, 16
+
+
+def test_binned_supertile_scan_mixed_grid_sizes(nrm, ctx, oracle):
+    """Large candidate sets take the binned supertile scan (persistent-zero
+    bin counts). A large grid, then a small one, then the large one again
+    must give the same bits for the large grid, and rows of both match the
+    oracle."""
+    big = _large_emdq_case(11, 1400, 900)
+    small = _large_emdq_case(12, 300, 200)
+    d0, u0 = nrm.emdq_field(*big, ctx=ctx)
+    ds, us = nrm.emdq_field(*small, ctx=ctx)
+    d1, u1 = nrm.emdq_field(*big, ctx=ctx)
+    assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
+    assert np.array_equal(u0.view(np.uint32), u1.view(np.uint32))
+    for args, d, u in ((big, d0, u0), (small, ds, us)):
+        grid, apts, loc, probs, active, alpha, beta, S = args
+        h = int(grid[3])
+        for j in (0, h // 2, h - 1):
+            od, ou = oracle.emdq_field_grid(grid, apts, loc, probs, active, alpha, beta, S, rows=(j, j + 1), fast=True)
+            assert np.abs(d[j] - od[j]).max() <= 1e-3
+            assert np.abs(u[j] / ou[j] - 1).max() <= 1e-6
 
 
 _NO_TMA_SCRIPT = r"""
