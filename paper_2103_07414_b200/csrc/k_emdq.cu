@@ -159,7 +159,7 @@ constexpr int SUPER_FUSED_GATHER_MAX = NRM_SUPER_FUSED_GATHER_MAX;  // above: a 
 
 // Candidate bins for large candidate sets: 64 px cells on the supertile grid
 // plus a margin ring that takes every candidate outside it. EmdqLaunch::
-// cell_cnt holds count[nc] (persistent-zero), EmdqLaunch::cells start[nc + 1]
+// cell_cnt holds a CTA ticket and count[nc] (persistent-zero), EmdqLaunch::cells start[nc + 1]
 // | cursor[nc] | candidate index[N], nc = (nsx + 2) (nsy + 2).
 constexpr int BIN_MAX_N = 1 << 17;  // k_super keeps an N-bit membership bitmap in shared memory
 struct CellGrid {
@@ -174,19 +174,19 @@ __device__ __forceinline__ int cell_of(const CellGrid& cg, float2 c) {
     return (cy + 1) * (cg.nsx + 2) + (cx + 1);
 }
 
-// One CTA: exclusive scan of the cell counts into start / cursor; the counts
-// are zeroed for the next call.
-__global__ void __launch_bounds__(1024) k_bin_scan(int* __restrict__ cnt, int* __restrict__ cells, int nc, int n) {
+// One CTA (the last k_gather CTA to finish): exclusive scan of the cell
+// counts into start / cursor; the counts are zeroed for the next call.
+__device__ void bin_scan_block(int* __restrict__ cnt, int* __restrict__ cells, int nc, int n) {
     __shared__ int wsum[32];
     __shared__ int carry;
     int* start = cells;
     int* cur = cells + nc + 1;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = blockDim.x >> 5;
     if (t == 0) carry = 0;
     __syncthreads();
-    for (int base = 0; base < nc; base += 1024) {
+    for (int base = 0; base < nc; base += blockDim.x) {
         const int c = base + t;
-        const int v = c < nc ? cnt[c] : 0;
+        const int v = c < nc ? __ldcg(&cnt[c]) : 0;  // other CTAs' atomics: read at L2
         int x = v;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(1024) k_bin_scan(int* __restrict__ cnt, int* _
         if (lane == 31) wsum[wid] = x;
         __syncthreads();
         if (wid == 0) {
-            int w = wsum[lane];
+            int w = lane < nw ? wsum[lane] : 0;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, w, d);
                 if (lane >= d) w += y;
             }
-            wsum[lane] = w;
+            if (lane < nw) wsum[lane] = w;
         }
         __syncthreads();
         const int excl = carry + (wid > 0 ? wsum[wid - 1] : 0) + x - v;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(1024) k_bin_scan(int* __restrict__ cnt, int* _
             cnt[c] = 0;
         }
         __syncthreads();
-        if (t == 1023) carry = excl + v;
+        if (t == blockDim.x - 1) carry = excl + v;
         __syncthreads();
     }
     if (t == 0) start[nc] = n;
@@ -228,24 +228,46 @@ __global__ void k_bin_scatter(const float2* __restrict__ c32, int n, CellGrid cg
     cells[2 * nc + 1 + pos] = a;
 }
 
-__global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
-                         const double* __restrict__ probs, const int32_t* __restrict__ active,
-                         int nactive, double* cx, double* cy, float2* c32, double* cl, double* cp,
-                         double* cphi, int* cj, int* cells, CellGrid cg) {
-    const int a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= nactive) return;
+__device__ __forceinline__ void gather_one(const double* __restrict__ apts, const double* __restrict__ locals,
+                                           const double* __restrict__ probs, const int32_t* __restrict__ active,
+                                           int a, double* cx, double* cy, float2* c32, double* cl, double* cp,
+                                           double* cphi, int* cj, int* cnt, const CellGrid& cg) {
     const int j = active[a];
     const double x = apts[2 * j], y = apts[2 * j + 1];
     cx[a] = x;
     cy[a] = y;
     c32[a] = make_float2((float)x, (float)y);
-    if (cells) atomicAdd(&cells[cell_of(cg, c32[a])], 1);  // bin counts (zero on entry)
+    if (cnt) atomicAdd(&cnt[1 + cell_of(cg, c32[a])], 1);  // bin counts (zero on entry)
 #pragma unroll
     for (int k = 0; k < 5; ++k) cl[5 * a + k] = locals[5 * j + k];
     const double p = probs[j];
     cp[a] = p < 1e-6 ? 1e-6 : p;  // std::max(probs[j], 1e-6)
     cphi[a] = atan2(locals[5 * j + 2], locals[5 * j + 1]);
     cj[a] = j;
+}
+
+// cnt (binned calls): [0] a CTA ticket, [1 + cell] the bin counts, both
+// persistent-zero; the last CTA scans the counts into `bins`.
+__global__ void k_gather(const double* __restrict__ apts, const double* __restrict__ locals,
+                         const double* __restrict__ probs, const int32_t* __restrict__ active,
+                         int nactive, double* cx, double* cy, float2* c32, double* cl, double* cp,
+                         double* cphi, int* cj, int* cnt, int* bins, CellGrid cg) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < nactive) gather_one(apts, locals, probs, active, a, cx, cy, c32, cl, cp, cphi, cj, cnt, cg);
+    if (cnt) {
+        __shared__ bool last;
+        __syncthreads();  // this CTA's counts are issued
+        if (threadIdx.x == 0) {
+            __threadfence();
+            last = atomicAdd(&cnt[0], 1) == (int)gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last) {
+            __threadfence();
+            bin_scan_block(cnt + 1, bins, cell_count_of(cg), nactive);
+            if (threadIdx.x == 0) cnt[0] = 0;
+        }
+    }
 }
 
 __device__ __forceinline__ bool key_less(double da, int ja, double db, int jb) {
@@ -1651,7 +1673,7 @@ void emdq_cell_bytes(int nactive, const FieldGrid& g, size_t* count_bytes, size_
     if (nactive <= SUPER_FUSED_GATHER_MAX || nactive > BIN_MAX_N) return;
     const int nsx = (g.i1 - g.i0 + ST) / ST, nsy = (g.j1 - g.j0 + ST) / ST;
     const size_t nc = (size_t)(nsx + 2) * (nsy + 2);
-    *count_bytes = nc * sizeof(int);
+    *count_bytes = (nc + 1) * sizeof(int);  // a CTA ticket, then the counts
     *bin_bytes = (2 * nc + 1 + (size_t)nactive) * sizeof(int);
 }
 
@@ -1719,15 +1741,14 @@ cudaError_t launch_emdq_field(const EmdqLaunch& L, cudaStream_t st, int64_t* lau
     if (gathered) {
         prof_mark("k_gather", st);
         k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx, L.cy,
-                                                           c32, L.cl, L.cp, phi, cj, LQ.cell_cnt, cg);
+                                                           c32, L.cl, L.cp, phi, cj, LQ.cell_cnt, LQ.cells, cg);
         ++*launches;
         cudaError_t eg = cudaGetLastError();
         if (eg != cudaSuccess) return eg;
-        if (binned) {
-            prof_mark("k_bin", st);
-            k_bin_scan<<<1, 1024, 0, st>>>(LQ.cell_cnt, LQ.cells, cell_count_of(cg), L.nactive);
+        if (binned) {  // (k_gather's last CTA scanned the counts)
+            prof_mark("k_bin_scatter", st);
             k_bin_scatter<<<(L.nactive + 255) / 256, 256, 0, st>>>(c32, L.nactive, cg, LQ.cells);
-            *launches += 2;
+            *launches += 1;
             eg = cudaGetLastError();
             if (eg != cudaSuccess) return eg;
         }
@@ -1808,7 +1829,7 @@ cudaError_t launch_emdq_points(const EmdqLaunch& L, const PointsLaunch& P, cudaS
     if (P.full_scan) {
         prof_mark("k_gather", st);
         k_gather<<<(L.nactive + 255) / 256, 256, 0, st>>>(L.apts, L.locals, L.probs, L.active, L.nactive, L.cx,
-                                                           L.cy, c32, L.cl, L.cp, phi, cj, nullptr, CellGrid{});
+                                                           L.cy, c32, L.cl, L.cp, phi, cj, nullptr, nullptr, CellGrid{});
         ++*launches;
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

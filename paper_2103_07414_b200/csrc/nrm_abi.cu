@@ -599,7 +599,7 @@ int emdq_core(nrm_ctx* c, const nrm_grid* grid, const double* d_apts, const doub
     if (cnt_bytes) {  // large candidate sets: binned supertile scans
         const bool grow = c->emdq_cell_cnt.cap < cnt_bytes;
         NRM_CUDA(c->emdq_cell_cnt.ensure(cnt_bytes));
-        // the bin counts start at zero; k_bin_scan re-zeroes every count it used
+        // the bin counts start at zero; the last k_gather CTA re-zeroes every count it used
         if (grow) NRM_CUDA(cudaMemsetAsync(c->emdq_cell_cnt.p, 0, c->emdq_cell_cnt.cap, c->stream));
         NRM_CUDA(c->emdq_cells.ensure(bin_bytes));
         L.cell_cnt = c->emdq_cell_cnt.as<int>();
