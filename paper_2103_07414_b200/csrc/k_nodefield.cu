@@ -253,8 +253,8 @@ __device__ __forceinline__ void nf_plan_tile(const NodeFieldLaunch& L, NfPlan* _
 // predecessor before exiting, which keeps the canvas order for the next
 // kernel (k_node_field waits for the planner). The last `conv` CTAs convert
 // the frame for the texture: the previous blend's k_node_field, the only
-// reader of those rows, has exited before this launch can start (its exact
-// pass, the PDL primary here, starts only after all its CTAs exit).
+// reader of those rows, has finished before this launch can start (its exact
+// pass, the PDL primary here, triggers only after waiting for that grid).
 constexpr int NF_CONV_BLOCKS = 2 * 148;
 // 3 CTAs per SM (80 registers, a few spills): alone it is slower (15.9
 // against 13.7 us on C2), but beside K3 the C2 step gains 1.3 us
@@ -1077,8 +1077,12 @@ __device__ __forceinline__ void nf_field_tc(const NodeFieldLaunch& L, const NfPl
 template <int MODE>
 __global__ void __launch_bounds__(NT, K1Shape<MODE>::MINB)
 k_node_field(const __grid_constant__ NodeFieldLaunch L, const NfPlan* __restrict__ plans, int tile_i0, int tile_j0,
-             int s1, int by0, int ntx) {
+             int s1, int by0, int ntx, int trig) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    // last launch chunk: the exception pass may become resident during the
+    // last wave (it waits for this grid before reading the queue); earlier
+    // chunks are followed by the next chunk's planner, which rewrites the plans
+    if (trig) pdl_trigger();
     pdl_wait();
 #ifndef NRM_K2_MMASYNC
     if constexpr (MODE == 1) {
@@ -1393,7 +1397,6 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
     __shared__ int red[3][EXC_THREADS / 32];
     __shared__ bool last;
     __shared__ double stage[EXC_THREADS / 32][32 * 6];
-    pdl_trigger();  // the next blend's planner may start (it only reads nodes)
     // the exact evaluation's dependent reads of inputs no kernel writes (the
     // exp table, small node arrays) start before the wait for the field grid,
     // so a queued pixel finds them in this SM's L1
@@ -1405,6 +1408,10 @@ __global__ void __launch_bounds__(EXC_THREADS) k_node_exceptions(NodeFieldLaunch
             prefetch_l1(reinterpret_cast<const char*>(L.warps) + o);
     }
     pdl_wait();
+    // the field grid triggered this pass early: the next blend's planner
+    // (which rewrites the frame texture) may start only once it has finished;
+    // it may still overlap this pass (it only reads nodes)
+    pdl_trigger();
     int nb = 0, nns = 0, noof = 0;
     exc_run<MODE>(L, stage[threadIdx.x >> 5], nb, nns, noof);
     exc_accumulate<MODE>(L, nb, nns, noof, red);
@@ -1626,7 +1633,8 @@ cudaError_t launch_node_field(const NodeFieldLaunch& L0, int mode, cudaStream_t 
         if (e != cudaSuccess) return e;
         prof_mark("k_node_field", st);
         e = launch_pdl(k_field, dim3(nh * g.ntx, rows), dim3(NT), smem, st, L,
-                                         static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx);
+                                         static_cast<const NfPlan*>(plans), g.ti0, g.tj0, g.s1, by0, g.ntx,
+                                         ci == g.nchunks - 1 ? 1 : 0);
         ++*launches;
         if (e != cudaSuccess) return e;
     }
