@@ -1,4 +1,4 @@
-// K1's frame textures: ImageU8 frames (1, 3 or 4 channels) converted to RGBA8
+// K1's frame textures: ImageU8 frames with 3 or 4 channels converted to RGBA8
 // rows so the fast tier's bilinear sample is three tex2Dgather calls. Used by
 // k_frame_rgba (batched blends) and by the conversion CTAs of k_nf_plan.
 #pragma once
