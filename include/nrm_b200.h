@@ -77,7 +77,11 @@ typedef struct nrm_grid {
 int nrm_abi_version(void);
 const char *nrm_last_error(void);
 
-/* Creates a context on CUDA device `device` with its own non-blocking stream. */
+/* Creates a context on CUDA device `device` with its own non-blocking stream.
+ * Device scratch grows on first use and is kept until nrm_ctx_destroy.
+ * Blends and node fields plan in chunks of 8,192 tiles, about 200 MB. Dense
+ * EMDQ fields plan in chunks of 32,768 tiles, 128 MB plus the candidate
+ * arrays. Both sizes fit a 4K frame into one launch chunk. */
 int nrm_ctx_create(int device, nrm_ctx **out);
 int nrm_ctx_destroy(nrm_ctx *ctx);
 /* Enqueue subsequent work on an external cudaStream_t (NULL = own stream;
